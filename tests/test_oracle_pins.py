@@ -1,0 +1,297 @@
+"""Pins of the CPU oracle against what the paper and the mathematics fix.
+
+Every test here is independent of the oracle's own quadrature: closed forms,
+mpmath brute force (oracle/brute.py), exact identities of the boundary
+integral equations, Laplace steady limits, direct solves.
+A plausible mistake in the oracle (a dropped term, a wrong sign, a wrong power
+of alpha, a transposed operand, a wrong dual-hat value) fails at least one.
+"""
+import math
+
+import mpmath as mp
+import numpy as np
+import pytest
+
+import workloads as W
+from oracle import brute as B
+from oracle import oracle as O
+from workloads.configs import Workload
+
+
+@pytest.fixture(scope="module")
+def c1():
+    w = W.get("C1")
+    return w, O.OracleMesh(w)
+
+
+_DENSE = {}
+
+
+def dense_c1(m, kind):
+    """C1 matrices are computed once per session"""
+    if kind not in _DENSE:
+        _DENSE[kind] = m.dense(kind)
+    return _DENSE[kind]
+
+
+# ----------------------------------------------------------------- P1: U*
+def test_ustar_closed_form():
+    L = O.lib()
+    # SPEC S:136-138 (closed-form instances of P:48-54)
+    assert L.ora_ustar(10.0, 0.0, 1.0) == pytest.approx(10 / (4 * math.pi), rel=1e-15)
+    assert L.ora_ustar(10.0, 1.0, 0.0) == 0.0
+    assert L.ora_ustar(1.0, 4.0, 1.0) == pytest.approx(math.exp(-1) / (4 * math.pi), rel=1e-15)
+    assert L.ora_ustar(1.0, 4.0, -1.0) == 0.0
+    # d_{n_y} U* at alpha=1, x-y=(1,0), n_y=(1,0), s=1: e^{-1/4}/(8 pi) = 0.0309874986 (SPEC S:147 erratum)
+    assert L.ora_ustar_dny(1.0, 1.0, 1.0, 1.0) == pytest.approx(0.0309874986, rel=1e-9)
+    assert L.ora_ustar_dny(1.0, 1.0, 1.0, 1.0) == pytest.approx(math.exp(-0.25) / (8 * math.pi), rel=1e-15)
+    # finite-difference consistency of d/dn_y: U*(x - (y + eps n)) derivative in eps
+    alpha, x, y, n, s = 0.7, np.array([0.3, -0.2]), np.array([0.1, 0.25]), np.array([0.6, 0.8]), 0.37
+    f = lambda e: L.ora_ustar(alpha, float(np.sum((x - y - e * n) ** 2)), s)
+    fd = (f(1e-5) - f(-1e-5)) / 2e-5
+    an = L.ora_ustar_dny(alpha, float(np.dot(x - y, n)), float(np.sum((x - y) ** 2)), s)
+    assert fd == pytest.approx(an, rel=1e-8)
+
+
+def test_ustar_normalisation():
+    # int_{R^2} U*(z, t) dz = 1 (SPEC S:181 erratum), polar quadrature
+    L = O.lib()
+    for alpha, t in [(0.7, 0.3), (10.0, 2.0)]:
+        v = mp.quad(lambda r: 2 * mp.pi * r * L.ora_ustar(alpha, float(r * r), t), [0, 1, 10, mp.inf])
+        assert float(v) == pytest.approx(1.0, abs=1e-12)
+
+
+# ----------------------------------------------------------------- P3: E1
+def test_e1_against_mpmath():
+    xs = np.concatenate([np.logspace(-14, 0, 60), np.linspace(1.0, 60.0, 120), [100.0, 300.0, 700.0]])
+    for x in xs:
+        ref = mp.e1(mp.mpf(x))
+        assert abs(O.e1(x) - ref) <= 3e-15 * ref, x
+    assert O.e1(1.0) == pytest.approx(0.21938393439552027, rel=1e-15)
+    x = 1e-12
+    assert abs(O.e1(x) + math.log(x) + 0.5772156649015329) < 1e-11
+
+
+# ---------------------------------------------------- P2: time antiderivatives
+@pytest.mark.parametrize("alpha,r2", [(0.7, 0.09), (1.0, 1e-4), (10.0, 0.5)])
+def test_time_antiderivatives(alpha, r2):
+    """H'' = (1/alpha) U*, F' = U*, Q'' = (1/alpha) d_ny U* / dot, with H, F, Q -> 0 at s -> 0"""
+    L = O.lib()
+    us = lambda s: mp.mpf(alpha) / (4 * mp.pi * s) * mp.exp(-mp.mpf(alpha) * r2 / (4 * s))
+    for s in (0.05, 0.37, 2.0):
+        Fs = mp.quad(us, [0, s])
+        assert L.ora_F(alpha, r2, s) == pytest.approx(float(Fs), rel=1e-13)
+        Hs = mp.quad(lambda v: (s - v) * us(v) / alpha, [0, s])         # double antiderivative
+        assert L.ora_H(alpha, r2, s) == pytest.approx(float(Hs), rel=1e-13)
+        dn = lambda v: mp.mpf(alpha) ** 2 / (8 * mp.pi * v * v) * mp.exp(-mp.mpf(alpha) * r2 / (4 * v))
+        Qs = mp.quad(lambda v: (s - v) * dn(v) / alpha, [0, s])
+        assert L.ora_Q(alpha, r2, s) == pytest.approx(float(Qs), rel=1e-13)
+
+
+# ------------------------------------------- P4: entries vs mpmath brute force
+BF_CASES = [
+    # ker, a, b, p, q, rel, sx, sy      (C1 geometry: 4 segments per side, h = 1/4, h_t = 1/16)
+    (0, 0, 0, 1, 1, 1, (1, 1), (1, 1)),      # V identical, d = 0 (log r)
+    (0, 1, 0, 1, 1, 1, (1, 1), (1, 1)),      # V identical, d = 1 (r^2 log r)
+    (0, 4, 1, 1, 1, 1, (1, 1), (1, 1)),      # V identical, d = 3
+    (0, 0, 0, 3, 4, 2, (1, 1), (1, 1)),      # V corner (1,0), d = 0
+    (0, 1, 0, 3, 4, 2, (1, 1), (1, 1)),      # V corner, d = 1
+    (0, 0, 0, 1, 2, 2, (1, 1), (1, 1)),      # V collinear neighbours
+    (0, 0, 0, 1, 3, 0, (1, 1), (1, 1)),      # V gap 1, d = 0
+    (2, 0, 0, 3, 4, 2, (1, 1), (1, 0)),      # K corner, falling hat, d = 0 (dot/r^2)
+    (2, 1, 0, 3, 4, 2, (1, 1), (0, 1)),      # K corner, rising hat, d = 1
+    (2, 0, 0, 4, 3, 3, (1, 1), (1, 0)),      # K corner, other orientation
+    (2, 0, 0, 2, 5, 0, (1, 1), (1, 0)),      # K near, d = 0
+    (1, 0, 0, 2, 2, 1, (0.5, 1), (1, 0.5)),  # F identical, linear shapes
+    (1, 1, 0, 3, 4, 2, (1, 0.5), (0.5, 0)),  # F corner, d = 1
+]
+
+
+@pytest.mark.parametrize("case", BF_CASES)
+def test_pair_integrals_brute_force(c1, case):
+    w, m = c1
+    ker, a, b, p, q, rel, sx, sy = case
+    X = (tuple(m.seg_a[p]), tuple(m.seg_b[p]))
+    Y = (tuple(m.seg_a[q]), tuple(m.seg_b[q]))
+    ref = float(B.pair(ker, w.alpha, w.t_breaks, a, b, X, Y, m.seg_n[q], sx, sy, rel))
+    got = m.pair(ker, 0, a, b, p, q, sx, sy)
+    assert got == pytest.approx(ref, rel=1e-12, abs=1e-18)
+
+
+def test_half_segment_pairs_brute_force():
+    """half segments on the L-shape (re-entrant corner, graded steps, alpha = 1/2)"""
+    w = W.get("LT")
+    m = O.OracleMesh(w)
+    half = []
+    for i in range(m.ng):
+        a, b = m.seg_a[i], m.seg_b[i]
+        mid = 0.5 * (a + b)
+        half += [(tuple(a), tuple(mid)), (tuple(mid), tuple(b))]
+    nrm = np.repeat(m.seg_n, 2, axis=0)
+    # re-entrant corner (0.5,0.5) is node 8 (4+2+2): half 15 ends there, half 16 starts there
+    cases = [(0, 0, 0, 15, 16, 2, (1, 1), (1, 1)), (1, 0, 0, 20, 20, 1, (0.5, 1), (1, 0.5)),
+             (1, 1, 0, 15, 16, 2, (0, 1), (1, 0)), (0, 2, 1, 20, 21, 2, (1, 1), (1, 1)),
+             (1, 3, 3, 5, 8, 0, (1, 0), (0, 1))]
+    for ker, a, b, p, q, rel, sx, sy in cases:
+        ref = float(B.pair(ker, w.alpha, w.t_breaks, a, b, half[p], half[q], nrm[q], sx, sy, rel))
+        got = m.pair(ker, 1, a, b, p, q, sx, sy)
+        assert got == pytest.approx(ref, rel=1e-12, abs=1e-18), (ker, a, b, p, q)
+
+
+# --------------------------------------------------------- P5: V_h structure
+def test_V_structure(c1):
+    w, m = c1
+    V = dense_c1(m, "V")
+    ng, nt = m.ng, m.nt
+    for a in range(nt):
+        for b in range(nt):
+            blk = V[a * ng:(a + 1) * ng, b * ng:(b + 1) * ng]
+            if b > a:
+                assert np.all(blk == 0.0)                          # causality, bitwise
+            else:
+                assert np.all(blk > 0.0)                           # U* > 0
+                assert np.abs(blk - blk.T).max() <= 1e-15 * np.abs(blk).max()
+                ref = V[(a - b) * ng:(a - b + 1) * ng, :ng]          # Toeplitz in the lag
+                assert np.abs(blk - ref).max() <= 1e-13 * np.abs(ref).max()
+    ev = np.linalg.eigvalsh(0.5 * (V + V.T))
+    assert ev[0] > 0.0                                              # P:92-93 positive definite
+    assert np.abs(V - V.T).max() > 1e-6                             # but not symmetric
+
+
+def _circle(nseg, alpha):
+    th = 2 * np.pi * np.arange(nseg) / nseg
+    return Workload(name="circle", vertices=list(zip(np.cos(th), np.sin(th))),
+                    segments_per_side=[1] * nseg, t_breaks=np.array([0.0, 1e6]), alpha=alpha,
+                    x_star=(2.0, 2.0), tol=1e-10)
+
+
+@pytest.mark.parametrize("alpha", [1.0, 10.0])
+def test_steady_limits_laplace(alpha):
+    """one time step T -> infinity on the unit circle: V/T -> Laplace single layer (eigenvalues
+    1/(2n)), K 1/T -> -1/2 (interior double layer), D_curl/T -> Laplace hypersingular (n/2).
+    Independent of alpha: pins every 1/alpha prefactor."""
+    nseg, T = 128, 1e6
+    w = _circle(nseg, alpha)
+    m = O.OracleMesh(w)
+    V = m.dense("V") / T
+    h = m.seg_h[0]
+    th = 2 * np.pi * (np.arange(nseg) + 0.5) / nseg
+    for n, ref in [(1, 0.5), (2, 0.25), (3, 1 / 6), (4, 0.125)]:
+        v = np.cos(n * th)
+        assert (v @ V @ v) / (h * v @ v) == pytest.approx(ref, rel=5e-3)
+    K = m.dense("K") / T
+    assert np.allclose(K.sum(axis=1) / (h * 1.0), -0.5, atol=2e-3)
+    D = m.dense("D") / T
+    thd = 2 * np.pi * np.arange(nseg) / nseg + np.pi / nseg        # dual nodes = midpoints
+    Lt = m.seg_h[0]
+    Myy = np.zeros((nseg, nseg))
+    for l in range(nseg):
+        Myy[l, l] = 4 * Lt / 6
+        Myy[l, (l + 1) % nseg] = Myy[l, (l - 1) % nseg] = Lt / 6
+    for n in (1, 2, 3, 4):
+        v = np.cos(n * thd)
+        assert (v @ D @ v) / (v @ Myy @ v) == pytest.approx(n / 2, rel=2e-3)
+
+
+# ---------------------------------------------- P6: K row sums (1/2 I jump)
+@pytest.mark.parametrize("a,i", [(0, 1), (3, 1), (0, 0), (5, 2), (15, 3)])
+def test_K_rowsum_jump_relation(c1, a, i):
+    """sum_{b<=a, n} K[(a,i),(b,n)] = int_{tau_a} int_{gamma_i} (M_0 1 - 1/2): K 1 = M_0 1 - 1/2
+    from eq. (3) with u = 1; exact at the discrete level (trial hats sum to one)."""
+    w, m = c1
+    t = w.t_breaks
+    s = sum(m.entry("K", a, i, b, n) for b in range(a + 1) for n in range(m.ng))
+    ref = float(B.K_rowsum_unit_square(w.alpha, t[a], t[a + 1], m.seg_a[i][0], m.seg_b[i][0]))
+    assert abs(s - ref) <= 1e-13 * 0.5 * m.seg_h[i] * (t[a + 1] - t[a])
+
+
+def test_K_collinear_zero(c1):
+    w, m = c1
+    assert m.pair(2, 0, 0, 0, 1, 1) == 0.0          # identical
+    assert m.pair(2, 0, 2, 0, 1, 2) == 0.0          # collinear neighbours
+    assert m.pair(2, 0, 2, 0, 1, 3, (1, 1), (1, 0)) == 0.0   # collinear, disjoint
+
+
+# ---------------------------------------------- P7: D normal-term row sums
+@pytest.mark.parametrize("a,l", [(2, 1), (4, 0), (9, 1)])
+def test_D_rowsum_identity(c1, a, l):
+    """sum_{b<=a, k} D[(a,l),(b,k)] = int_{tau_a} int psi_l(x) int_Gamma (n_x.n_y) U*(x-y,t)
+    (D = -d_n W, applied to u = 1; the curl term vanishes since sum_k psi_k' = 0)."""
+    w, m = c1
+    t = w.t_breaks
+    pieces = {1: [(0.125, 0.25, 0, 0.5), (0.25, 0.375, 0.5, 1), (0.375, 0.5, 1, 0.5), (0.5, 0.625, 0.5, 0)],
+              0: [("L", 0.125, 0.0, 0, 0.5), (0.0, 0.125, 0.5, 1), (0.125, 0.25, 1, 0.5),
+                  (0.25, 0.375, 0.5, 0)]}[l]
+    s = sum(m.entry("D", a, l, b, k) for b in range(a + 1) for k in range(m.ng))
+    ref = float(B.D_rowsum_unit_square(w.alpha, t[a], t[a + 1], pieces))
+    assert s == pytest.approx(ref, rel=1e-12)
+
+
+def test_D_structure(c1):
+    w, m = c1
+    D = dense_c1(m, "D")
+    ng = m.ng
+    for a in range(m.nt):
+        for b in range(a + 1):
+            blk = D[a * ng:(a + 1) * ng, b * ng:(b + 1) * ng]
+            assert np.abs(blk - blk.T).max() <= 1e-14 * np.abs(D).max()   # symmetric blocks
+    assert np.linalg.eigvalsh(0.5 * (D + D.T))[0] > 0.0
+    K = dense_c1(m, "K")
+    assert np.abs(K[:ng, :ng] - K[:ng, :ng].T).max() > 1e-6          # K is not
+
+
+# ------------------------------------------------------- P9: mass matrices
+def test_mass_matrices(c1):
+    w, m = c1
+    h, ht = 0.25, 1.0 / 16
+    Mp = m.mass_primal()
+    assert Mp[0, 0] == pytest.approx(h * ht / 2, rel=1e-15) and Mp[0, 1] == pytest.approx(h * ht / 2)
+    Md = m.mass_dual()
+    assert Md[5, 5] == pytest.approx(0.75 * h * ht, rel=1e-15)
+    assert Md[5, 4] == pytest.approx(h * ht / 8) and Md[5, 6] == pytest.approx(h * ht / 8)
+    np.testing.assert_allclose(Md.sum(axis=1), h * ht, rtol=1e-14)      # row sums |sigma|
+    np.testing.assert_allclose(Md.sum(axis=0), h * ht, rtol=1e-14)
+    # non-uniform lengths: row sum = h_t (h_{l-1} + 2 h_l + h_{l+1}) / 4 (SURVEY a6 check h=(1,2,3))
+    hm, h0, hp = 1.0, 2.0, 3.0
+    vm, vp = hm / (hm + h0), hp / (h0 + hp)
+    assert hm * vm / 4 + h0 * (2 + vm + vp) / 4 + hp * vp / 4 == pytest.approx(2.0, rel=1e-15)
+
+
+# --------------------------------------------------------------- P10: GMRES
+def test_gmres_identity_one_iteration():
+    b = np.random.default_rng(0).normal(size=50)
+    x, it, hist = O.gmres(lambda v: v, lambda r: r, b, 1e-10)
+    assert it == 1 and np.allclose(x, b, rtol=1e-14)
+
+
+def test_gmres_matches_direct_solve(c1):
+    w, m = c1
+    V, K = dense_c1(m, "V"), dense_c1(m, "K")
+    b = m.rhs(K, W.dirichlet_data(w))
+    wd = O.block_forward_solve(V, b, m.ng)
+    assert np.abs(V @ wd - b).max() <= 1e-13 * np.abs(b).max()
+    x, it, hist = O.gmres(lambda v: V @ v, lambda r: r, b, 1e-10)
+    assert np.all(np.diff(hist) <= 1e-15)                          # monotone (full GMRES)
+    assert np.abs(x - wd).max() <= 1e-8 * np.abs(wd).max()
+    assert 20 <= it <= 35                                           # SURVEY 8(c) band: ~27
+    D = dense_c1(m, "D")
+    for mode, band in ((1, (14, 26)), (2, (10, 22))):
+        C = O.make_preconditioner(mode, D, m.mass_dual(), m.lumped_dual())
+        x, itp, hist = O.gmres(lambda v: V @ v, C, b, 1e-10)
+        assert band[0] <= itp <= band[1]
+        assert np.abs(x - wd).max() <= 1e-8 * np.abs(wd).max()
+
+
+# ------------------------------------------- P11: convergence of w_h (end to end)
+@pytest.mark.slow
+def test_w_converges_under_refinement():
+    errs = []
+    for name in ("C1", "S32"):
+        w = W.get(name)
+        m = O.OracleMesh(w)
+        V, K = m.dense("V"), m.dense("K")
+        wd = O.block_forward_solve(V, m.rhs(K, W.dirichlet_data(w)), m.ng)
+        e, r = m.l2_error(wd)
+        errs.append(e / r)
+    assert errs[0] == pytest.approx(0.330, abs=0.01)                # prototype: 0.330 -> 0.154
+    assert errs[1] < errs[0] / 1.8
