@@ -1,0 +1,195 @@
+/*
+ * stbem.h — C-ABI of the B200-native space-time boundary element library for the
+ * heat equation (Dohr, Merta, Of, Steinbach, Zapletal, arXiv:1811.05224).
+ *
+ * Citations: P:n = PAPER.md line n.  All arithmetic is FP64.  Every function returns a
+ * bem_status; on a non-OK status bem_last_error() returns a thread-local message.  No C++
+ * exception crosses this boundary.  Nothing here ever falls back to the CPU: every
+ * compute call runs CUDA kernels for sm_100a and returns BEM_E_CUDA if none can run.
+ *
+ * Index convention (R13): global unknown l = a * n_gamma + i, a = time step
+ * (tau_a = (t_a, t_{a+1})), i = boundary element gamma_i (primal) or dual hat psi_i.
+ *
+ * Ownership: opaque handles are created by the library and freed only by the matching
+ * *_destroy.  Vectors passed as `const double*` / `double*` with the suffix _dev are
+ * caller-owned DEVICE memory on the handle's device, length n = n_gamma * n_steps
+ * (full length on every rank: vectors are replicated; the multi-GPU layer reduces
+ * partial products internally).  `_host` arrays are caller-owned host memory.
+ * Streams are caller-owned (0 = legacy default stream).
+ */
+#ifndef STBEM_H
+#define STBEM_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  BEM_OK = 0,
+  BEM_E_INVALID = 1,       /* invalid argument or descriptor */
+  BEM_E_NOMEM = 2,         /* device or host allocation failed */
+  BEM_E_CUDA = 3,          /* CUDA error, or no CUDA device */
+  BEM_E_NCCL = 4,          /* NCCL error */
+  BEM_E_NOT_CONVERGED = 5, /* GMRES reached max_iter; w holds the last iterate */
+  BEM_E_BREAKDOWN = 6,     /* Arnoldi breakdown (sub-diagonal < 1e-300) before convergence */
+  BEM_E_STATE = 7          /* wrong object (kind / mesh mismatch) */
+} bem_status;
+
+typedef struct bem_comm_s bem_comm;
+typedef struct bem_mesh_s bem_mesh;
+typedef struct bem_matrix_s bem_matrix;
+typedef void* bem_stream; /* a cudaStream_t */
+
+/* Problem geometry and time grid (eq. 1, P:64 Sigma_h = Gamma_h x I_h).
+ * vertices_xy: 2*n_vertices doubles, a simple counter-clockwise polygon.
+ * segments_per_side[s] >= 1 equal segments on side s (from vertex s to s+1).
+ * t_breaks: n_steps+1 strictly increasing values, t_breaks[0] = 0.
+ * alpha > 0 heat capacity (eq. 1).  n_slices P: temporal submeshes, 1 <= P <= n_steps
+ * (P:217).  All arrays are host memory and are copied. */
+typedef struct {
+  int n_vertices;
+  const double* vertices_xy;
+  const int* segments_per_side;
+  int n_steps;
+  const double* t_breaks;
+  double alpha;
+  int n_slices;
+} bem_mesh_desc;
+
+typedef struct {
+  int n_gamma;             /* N_Gamma boundary elements (= dual hats) */
+  int n_steps;             /* N_I time steps */
+  long long n;             /* N = n_gamma * n_steps */
+  int n_slices;            /* P */
+  int n_owned_blocks;      /* blocks (I,J) of the P x P block structure owned by this rank */
+  long long entries_owned; /* stored entries per matrix on this rank */
+  long long entries_total; /* n_gamma^2 n_steps (n_steps+1) / 2 */
+  int q_bulk;              /* Gauss points per direction for d = a-b >= 2 (per mesh) */
+  double kappa;            /* alpha h_max^2 / (4 min h_t): smoothness ratio choosing q_bulk */
+} bem_mesh_info;
+
+/* Quadrature options; NULL = documented defaults.  0 = default. */
+typedef struct {
+  int q_bulk;   /* Gauss order per direction for time cells d >= 2; 0 = chosen from kappa */
+  int q_sing;   /* order of the Duffy / 1-D reduction rules for touching pairs (default 12) */
+  int flags;    /* reserved, 0 */
+} bem_quad_opts;
+
+typedef enum {
+  BEM_MASS_PRIMAL = 0,      /* M_h of eq. (4): <phi^10_(a,n), phi^0_(a,i)> */
+  BEM_MASS_DUAL = 1,        /* M_h of Thm 1: <phi^0_(a,k), psi_(a,l)>, cyclic tridiagonal */
+  BEM_MASS_DUAL_LUMPED = 2  /* row sums of BEM_MASS_DUAL */
+} bem_mass_kind;
+
+typedef struct {
+  double rel_tol;  /* stop when ||C(b - V w_k)|| <= rel_tol ||C b|| (Givens estimate) */
+  int max_iter;    /* full GMRES, no restart */
+  int precond;     /* 0 none, 1 lumped dual mass, 2 exact dual mass (cyclic tridiagonal) */
+} bem_gmres_opts;
+
+typedef struct {
+  int iterations;
+  int converged;
+  double rel_residual;       /* Givens estimate at exit */
+  double true_rel_residual;  /* ||C(b - V w)|| / ||C b|| recomputed at exit */
+  double seconds_total;
+  double seconds_matvec;     /* V and D products (device time) */
+  double seconds_comm;       /* collectives (device time, 0 on one GPU) */
+} bem_solve_report;
+
+/* ---------------------------------------------------------------- general */
+const char* bem_version(void);
+const char* bem_last_error(void);   /* thread-local text for the last non-OK status */
+/* number of kernel launches issued by this thread since the last reset (instrumentation) */
+long long bem_launch_count(int reset);
+
+/* ----------------------------------------------------------- multi-GPU (NCCL) */
+/* rank 0 creates the 128-byte NCCL unique id; the caller broadcasts it (torch.distributed). */
+bem_status bem_nccl_get_unique_id(void* out128_host);
+/* collective over nranks: one rank per GPU; cuda_device is this rank's device ordinal. */
+bem_status bem_comm_create(const void* unique_id128_host, int nranks, int rank, int cuda_device,
+                           bem_comm** out);
+void bem_comm_destroy(bem_comm* comm);
+
+/* ----------------------------------------------------- cyclic K_P plan (host) */
+/* Cyclic decomposition of the complete graph K_P (Fig. 3, R15):
+ * owner_host[i*P + j] = process owning block (i,j), j <= i (entries with j > i are -1).
+ * Pure host code: callable without a GPU. */
+bem_status bem_plan_build(int P, int* owner_host);
+/* generator G_0: out_host[k] = k-th vertex of the difference cover (count in *n_out) */
+bem_status bem_plan_generator(int P, int* out_host, int* n_out);
+/* balanced slice ranges (R14): slice p = time steps [first[p], first[p+1]) */
+bem_status bem_slice_ranges(int n_steps, int P, int* first_host /* P+1 */);
+
+/* ---------------------------------------------------------------- mesh */
+/* Validates the descriptor, builds Gamma_h, the half segments of the dual mesh (R6),
+ * the time grid, the slices and the block ownership (comm == NULL: one GPU owns all blocks),
+ * and uploads them to the current CUDA device. */
+bem_status bem_mesh_create(const bem_mesh_desc* desc, bem_comm* comm, bem_mesh** out);
+bem_status bem_mesh_info_get(const bem_mesh* mesh, bem_mesh_info* info);
+void bem_mesh_destroy(bem_mesh* mesh);
+
+/* ------------------------------------------------------------ assembly */
+/* V_h[(a,i),(b,j)] = <V phi^0_(b,j), phi^0_(a,i)> with (1/alpha) U* (P:43).
+ * Stored entries: owned blocks, b <= a, packed row panels. */
+bem_status bem_assemble_V(const bem_mesh* mesh, const bem_quad_opts* opts, bem_stream stream,
+                          bem_matrix** out);
+/* K_h[(a,i),(b,n)] = <K phi^10_(b,n), phi^0_(a,i)> with (1/alpha) d_{n_y} U* (P:44). */
+bem_status bem_assemble_K(const bem_mesh* mesh, const bem_quad_opts* opts, bem_stream stream,
+                          bem_matrix** out);
+/* D_h[(a,l),(b,k)] = <D psi_(b,k), psi_(a,l)> (Thm 1; D = -d_n W) in the
+ * integration-by-parts form of DESIGN.md R7, dual hats of R6. */
+bem_status bem_assemble_D(const bem_mesh* mesh, const bem_quad_opts* opts, bem_stream stream,
+                          bem_matrix** out);
+/* mass matrices (block diagonal in time): see bem_mass_kind */
+bem_status bem_assemble_M(const bem_mesh* mesh, bem_mass_kind kind, bem_stream stream,
+                          bem_matrix** out);
+
+/* --------------------------------------------------------------- products */
+/* y = a A x + b y for an assembled V/K/D matrix (block-lower-triangular FP64 GEMV) or a mass
+ * matrix.  x_dev, y_dev: device, length n, must not alias.  Multi-GPU: partial products of the
+ * owned blocks are summed over ranks (NCCL) so y is complete on every rank. */
+bem_status bem_matvec(const bem_matrix* A, double a, const double* x_dev, double b, double* y_dev,
+                      bem_stream stream);
+/* y = M^{-1} x (transpose = 0) or M^{-T} x (transpose = 1) for a mass matrix (dual: N_I cyclic
+ * tridiagonal solves of size N_Gamma; lumped: diagonal scaling). x_dev, y_dev may alias. */
+bem_status bem_mass_solve(const bem_matrix* M, int transpose, const double* x_dev, double* y_dev,
+                          bem_stream stream);
+/* right-hand side of eq. (4) with u0 = 0: b = 1/2 M_primal g + K g */
+bem_status bem_rhs(const bem_matrix* K, const bem_matrix* M_primal, const double* g_dev,
+                   double* b_dev, bem_stream stream);
+
+/* ----------------------------------------------------------------- solver */
+/* Preconditioned full GMRES for V w = b with left preconditioner
+ * C_V^{-1} = M^{-1} D M^{-T}; D and M are ignored when opts->precond == 0.
+ * M must be BEM_MASS_DUAL_LUMPED for precond 1 and BEM_MASS_DUAL for precond 2.
+ * x0 = 0.  b_dev, w_dev device vectors of length n.  res_hist_host: NULL or max_iter+1 doubles
+ * (relative preconditioned residual estimates, [0] = 1).  Runs on the mesh's internal stream and
+ * synchronises.  Returns BEM_E_NOT_CONVERGED / BEM_E_BREAKDOWN with w and the report filled. */
+bem_status bem_solve_gmres(const bem_matrix* V, const bem_matrix* D, const bem_matrix* M,
+                           const double* b_dev, double* w_dev, const bem_gmres_opts* opts,
+                           bem_solve_report* report, double* res_hist_host);
+
+/* ---------------------------------------------------------------- access */
+/* dense window [r0, r0+nr) x [c0, c0+nc) into host_dst (row-major nr x nc); causality zeros
+ * (b > a) and entries of blocks not owned by this rank read as 0. */
+bem_status bem_matrix_get(const bem_matrix* A, long long r0, long long nr, long long c0,
+                          long long nc, double* host_dst);
+/* count sampled entries (rows_host[k], cols_host[k]) into out_host[k] */
+bem_status bem_matrix_get_entries(const bem_matrix* A, long long count, const long long* rows_host,
+                                  const long long* cols_host, double* out_host);
+/* stored entries and bytes on this rank; kind: 0 V, 1 K, 2 D, 3 mass */
+bem_status bem_matrix_info(const bem_matrix* A, int* kind, long long* entries, long long* bytes);
+void bem_matrix_destroy(bem_matrix* A);
+
+/* ---------------------------------------------------------- diagnostics */
+/* device evaluation of the special functions used by the kernels (for the GPU pins):
+ * which = 0 E1(x), 1 Ein(x), 2 (1+x)E1(x) - e^{-x}, 3 e^{-x}/x - 1/x - E1(x).
+ * x_dev, out_dev: device arrays of length count. */
+bem_status bem_eval_special(int which, long long count, const double* x_dev, double* out_dev,
+                            bem_stream stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* STBEM_H */

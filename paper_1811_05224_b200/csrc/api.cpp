@@ -1,0 +1,401 @@
+// api.cpp — C-ABI entry points (include/stbem.h): assembly drivers, products, preconditioned
+// GMRES, matrix access.  Host orchestration only: every arithmetic
+// step on vectors or matrices runs in the CUDA kernels of assemble.cu / linalg.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "internal.h"
+
+using namespace stb;
+
+namespace {
+
+inline cudaStream_t S(bem_stream s) { return reinterpret_cast<cudaStream_t>(s); }
+
+bem_matrix* new_dense(const bem_mesh* m, int kind, bem_status* st) {
+  bem_matrix* A = new bem_matrix_s();
+  A->kind = kind;
+  A->mesh = m;
+  const int ng = m->ng;
+  long long off = 0;
+  for (size_t bi = 0; bi < m->blocks.size(); ++bi) {
+    const Block& b = m->blocks[bi];
+    A->poff_base.push_back((int)A->poff.size());
+    for (int a = b.a0; a < b.a1; ++a) {
+      A->poff.push_back(off);
+      off += (long long)ng * pad4((long long)panel_nb(a, b.b0, b.b1) * ng);
+    }
+  }
+  A->entries = off;
+  cudaError_t e = cudaMalloc(&A->data, sizeof(double) * std::max<long long>(off, 4));
+  if (e != cudaSuccess) {
+    *st = BEM_E_NOMEM;
+    set_error(std::string("matrix allocation of ") + std::to_string(8.0 * off / 1e9) + " GB failed: " + cudaGetErrorString(e));
+    cudaGetLastError();
+    delete A;
+    return nullptr;
+  }
+  *st = BEM_OK;
+  return A;
+}
+
+bem_status assemble(int kind, const bem_mesh* m, const bem_quad_opts* o, bem_stream s, bem_matrix** out) {
+  if (!m || !out) { set_error("bem_assemble: null argument"); return BEM_E_INVALID; }
+  *out = nullptr;
+  int q_bulk = (o && o->q_bulk > 0) ? o->q_bulk : m->q_bulk;
+  int q_sing = (o && o->q_sing > 0) ? o->q_sing : 12;
+  if (q_bulk < 3 || q_bulk > 8 || q_bulk == 7) { set_error("bem_assemble: q_bulk must be one of 3,4,5,6,8"); return BEM_E_INVALID; }
+  if (q_sing < 4 || q_sing > QSING_MAX) { set_error("bem_assemble: q_sing must be in [4,16]"); return BEM_E_INVALID; }
+  if (m->ng < 6) { set_error("bem_assemble: N_Gamma >= 6 required"); return BEM_E_INVALID; }
+  cudaSetDevice(m->device);
+  bem_status st;
+  bem_matrix* A = new_dense(m, kind, &st);
+  if (!A) return st;
+  cudaError_t e = cudaMemsetAsync(A->data, 0, sizeof(double) * A->entries, S(s));
+  if (e != cudaSuccess) { bem_matrix_destroy(A); return cuda_fail(e, "bem_assemble/memset"); }
+  st = launch_assembly(kind, m, A, q_bulk, q_sing, S(s));
+  if (st == BEM_OK) st = gemv_setup(A);
+  if (st != BEM_OK) { bem_matrix_destroy(A); return st; }
+  *out = A;
+  return BEM_OK;
+}
+
+int slice_of(const bem_mesh* m, int a) {
+  int p = (int)(std::upper_bound(m->slice_first.begin(), m->slice_first.end(), a) - m->slice_first.begin()) - 1;
+  return std::min(std::max(p, 0), m->P - 1);
+}
+
+// device offset of entry (a,i,b,j) or -1 (causality zero / not owned)
+long long entry_offset(const bem_matrix* A, int a, int i, int b, int j) {
+  const bem_mesh* m = A->mesh;
+  if (b > a) return -1;
+  const int I = slice_of(m, a), J = slice_of(m, b);
+  for (size_t bi = 0; bi < m->blocks.size(); ++bi) {
+    const Block& B = m->blocks[bi];
+    if (B.I == I && B.J == J) {
+      long long ld = pad4((long long)panel_nb(a, B.b0, B.b1) * m->ng);
+      return A->poff[A->poff_base[bi] + (a - B.a0)] + (long long)i * ld + (long long)(b - B.b0) * m->ng + j;
+    }
+  }
+  return -1;
+}
+
+__attribute__((unused)) double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+}  // namespace
+
+namespace stb {
+bem_status gather_entries(const double* data, const long long* offs_dev, long long n, double* out_dev, cudaStream_t st);
+}
+
+extern "C" {
+
+bem_status bem_assemble_V(const bem_mesh* m, const bem_quad_opts* o, bem_stream s, bem_matrix** out) {
+  return assemble(STB_V, m, o, s, out);
+}
+bem_status bem_assemble_K(const bem_mesh* m, const bem_quad_opts* o, bem_stream s, bem_matrix** out) {
+  return assemble(STB_K, m, o, s, out);
+}
+bem_status bem_assemble_D(const bem_mesh* m, const bem_quad_opts* o, bem_stream s, bem_matrix** out) {
+  return assemble(STB_D, m, o, s, out);
+}
+
+bem_status bem_assemble_M(const bem_mesh* m, bem_mass_kind kind, bem_stream s, bem_matrix** out) {
+  (void)s;
+  if (!m || !out) { set_error("bem_assemble_M: null argument"); return BEM_E_INVALID; }
+  if (kind < BEM_MASS_PRIMAL || kind > BEM_MASS_DUAL_LUMPED) { set_error("bem_assemble_M: bad kind"); return BEM_E_INVALID; }
+  cudaSetDevice(m->device);
+  bem_matrix* M = new bem_matrix_s();
+  M->kind = STB_MASS;
+  M->mesh = m;
+  bem_status st = mass_setup(M, kind);
+  if (st != BEM_OK) { bem_matrix_destroy(M); return st; }
+  *out = M;
+  return BEM_OK;
+}
+
+bem_status bem_matvec(const bem_matrix* A, double a, const double* x, double b, double* y, bem_stream s) {
+  if (!A || !x || !y) { set_error("bem_matvec: null argument"); return BEM_E_INVALID; }
+  if (x == y) { set_error("bem_matvec: x and y must not alias"); return BEM_E_INVALID; }
+  if (A->kind == STB_MASS) return mass_apply(A, a, x, b, y, S(s));
+  return gemv_launch(A, a, x, b, y, S(s));
+}
+
+bem_status bem_mass_solve(const bem_matrix* M, int transpose, const double* x, double* y, bem_stream s) {
+  if (!M || !x || !y) { set_error("bem_mass_solve: null argument"); return BEM_E_INVALID; }
+  if (M->kind != STB_MASS || M->mass_kind == BEM_MASS_PRIMAL) {
+    set_error("bem_mass_solve: needs a dual (exact or lumped) mass matrix");
+    return BEM_E_STATE;
+  }
+  return mass_solve(M, transpose, x, y, S(s));
+}
+
+bem_status bem_rhs(const bem_matrix* K, const bem_matrix* Mp, const double* g, double* b, bem_stream s) {
+  if (!K || !Mp || !g || !b) { set_error("bem_rhs: null argument"); return BEM_E_INVALID; }
+  if (K->kind != STB_K || Mp->kind != STB_MASS || Mp->mass_kind != BEM_MASS_PRIMAL) {
+    set_error("bem_rhs: needs K_h and the primal mass matrix");
+    return BEM_E_STATE;
+  }
+  bem_status st = gemv_launch(K, 1.0, g, 0.0, b, S(s));
+  if (st != BEM_OK) return st;
+  return mass_apply(Mp, 0.5, g, 1.0, b, S(s));
+}
+
+bem_status bem_eval_special(int which, long long count, const double* x, double* out, bem_stream s) {
+  if (which < 0 || which > 3 || count < 0) { set_error("bem_eval_special: bad argument"); return BEM_E_INVALID; }
+  return eval_special(which, count, x, out, S(s));
+}
+
+// ------------------------------------------------------------------ GMRES
+bem_status bem_solve_gmres(const bem_matrix* V, const bem_matrix* D, const bem_matrix* M,
+                           const double* b, double* w, const bem_gmres_opts* opts,
+                           bem_solve_report* rep, double* hist) {
+  if (!V || !b || !w || !opts) { set_error("bem_solve_gmres: null argument"); return BEM_E_INVALID; }
+  if (V->kind != STB_V) { set_error("bem_solve_gmres: first matrix must be V_h"); return BEM_E_STATE; }
+  const int prec = opts->precond;
+  if (prec < 0 || prec > 2) { set_error("bem_solve_gmres: precond must be 0, 1 or 2"); return BEM_E_INVALID; }
+  if (prec > 0) {
+    if (!D || !M || D->kind != STB_D || M->kind != STB_MASS) { set_error("bem_solve_gmres: preconditioner needs D_h and a dual mass matrix"); return BEM_E_STATE; }
+    if ((prec == 1 && M->mass_kind != BEM_MASS_DUAL_LUMPED) || (prec == 2 && M->mass_kind != BEM_MASS_DUAL)) {
+      set_error("bem_solve_gmres: precond 1 needs BEM_MASS_DUAL_LUMPED, precond 2 needs BEM_MASS_DUAL");
+      return BEM_E_STATE;
+    }
+  }
+  if (!(opts->rel_tol > 0) || opts->max_iter < 1) { set_error("bem_solve_gmres: rel_tol > 0 and max_iter >= 1 required"); return BEM_E_INVALID; }
+  const bem_mesh* m = V->mesh;
+  cudaSetDevice(m->device);
+  const long long n = (long long)m->ng * m->nt;
+  const int kmax = opts->max_iter;
+  cudaStream_t st = m->stream;
+  double *Q = nullptr, *tmp = nullptr, *u = nullptr, *v = nullptr, *dh = nullptr, *wk = nullptr;
+  cudaError_t e;
+  if ((e = cudaMalloc(&Q, sizeof(double) * n * (kmax + 1))) != cudaSuccess ||
+      (e = cudaMalloc(&tmp, sizeof(double) * n)) != cudaSuccess ||
+      (e = cudaMalloc(&u, sizeof(double) * n)) != cudaSuccess ||
+      (e = cudaMalloc(&v, sizeof(double) * n)) != cudaSuccess ||
+      (e = cudaMalloc(&wk, sizeof(double) * n)) != cudaSuccess ||
+      (e = cudaMalloc(&dh, sizeof(double) * 2 * (kmax + 2))) != cudaSuccess) {
+    cudaFree(Q); cudaFree(tmp); cudaFree(u); cudaFree(v); cudaFree(wk); cudaFree(dh);
+    cudaGetLastError();
+    set_error("bem_solve_gmres: allocation failed");
+    return BEM_E_NOMEM;
+  }
+  cudaEvent_t e0, e1, mv0, mv1;
+  cudaEventCreate(&e0); cudaEventCreate(&e1); cudaEventCreate(&mv0); cudaEventCreate(&mv1);
+  double t_mv = 0.0;
+  cudaEventRecord(e0, st);
+  bem_status status = BEM_OK;
+  // z = C r  (C = M^{-1} D M^{-T}, lumped or exact), out may alias nothing else
+  auto apply_C = [&](const double* r, double* out) -> bem_status {
+    if (prec == 0) {
+      return cudaMemcpyAsync(out, r, sizeof(double) * n, cudaMemcpyDeviceToDevice, st) == cudaSuccess ? BEM_OK : BEM_E_CUDA;
+    }
+    bem_status s1 = mass_solve(M, 1, r, u, st);
+    if (s1 != BEM_OK) return s1;
+    cudaEventRecord(mv0, st);
+    s1 = gemv_launch(D, 1.0, u, 0.0, v, st);
+    cudaEventRecord(mv1, st);
+    if (s1 != BEM_OK) return s1;
+    cudaEventSynchronize(mv1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, mv0, mv1);
+    t_mv += ms * 1e-3;
+    return mass_solve(M, 0, v, out, st);
+  };
+  auto apply_V = [&](const double* x, double* out) -> bem_status {
+    cudaEventRecord(mv0, st);
+    bem_status s1 = gemv_launch(V, 1.0, x, 0.0, out, st);
+    cudaEventRecord(mv1, st);
+    cudaEventSynchronize(mv1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, mv0, mv1);
+    t_mv += ms * 1e-3;
+    return s1;
+  };
+  auto norm = [&](const double* x) -> double {
+    vec_dots(x, 0, 1, x, n, dh, st);
+    double hv = 0;
+    cudaMemcpyAsync(&hv, dh, sizeof(double), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    return std::sqrt(hv);
+  };
+  std::vector<double> H((size_t)(kmax + 1) * kmax, 0.0), cs(kmax), sn(kmax), g(kmax + 1, 0.0), hcol(2 * (kmax + 2));
+  int iters = 0;
+  bool converged = false, breakdown = false;
+  double resid = 1.0;
+  status = apply_C(b, Q);
+  double beta = status == BEM_OK ? norm(Q) : 0.0;
+  if (hist) hist[0] = 1.0;
+  if (status == BEM_OK && beta == 0.0) {
+    cudaMemsetAsync(w, 0, sizeof(double) * n, st);
+    converged = true;
+    resid = 0.0;
+  } else if (status == BEM_OK) {
+    vec_scale(Q, Q, 1.0 / beta, n, st);
+    g[0] = beta;
+    for (int k = 0; k < kmax; ++k) {
+      double* qk = Q + (long long)k * n;
+      if ((status = apply_V(qk, tmp)) != BEM_OK) break;
+      if ((status = apply_C(tmp, wk)) != BEM_OK) break;
+      // classical Gram-Schmidt with one re-orthogonalisation (CGS2)
+      vec_dots(Q, n, k + 1, wk, n, dh, st);
+      vec_update(wk, Q, n, k + 1, dh, n, st);
+      vec_dots(Q, n, k + 1, wk, n, dh + (kmax + 2), st);
+      vec_update(wk, Q, n, k + 1, dh + (kmax + 2), n, st);
+      cudaMemcpyAsync(hcol.data(), dh, sizeof(double) * (k + 1), cudaMemcpyDeviceToHost, st);
+      cudaMemcpyAsync(hcol.data() + (kmax + 2), dh + (kmax + 2), sizeof(double) * (k + 1), cudaMemcpyDeviceToHost, st);
+      double hk1 = norm(wk);  // synchronises
+      double* Hk = &H[(size_t)k * (kmax + 1)];
+      for (int j = 0; j <= k; ++j) Hk[j] = hcol[j] + hcol[(kmax + 2) + j];
+      Hk[k + 1] = hk1;
+      if (hk1 > 1e-300) vec_scale(Q + (long long)(k + 1) * n, wk, 1.0 / hk1, n, st);
+      for (int j = 0; j < k; ++j) {
+        double t1 = cs[j] * Hk[j] + sn[j] * Hk[j + 1];
+        Hk[j + 1] = -sn[j] * Hk[j] + cs[j] * Hk[j + 1];
+        Hk[j] = t1;
+      }
+      double den = std::hypot(Hk[k], Hk[k + 1]);
+      cs[k] = Hk[k] / den;
+      sn[k] = Hk[k + 1] / den;
+      Hk[k] = den;
+      Hk[k + 1] = 0.0;
+      g[k + 1] = -sn[k] * g[k];
+      g[k] = cs[k] * g[k];
+      resid = std::fabs(g[k + 1]) / beta;
+      iters = k + 1;
+      if (hist) hist[k + 1] = resid;
+      if (resid <= opts->rel_tol) { converged = true; break; }
+      if (hk1 <= 1e-300) { breakdown = true; break; }
+    }
+    if (status == BEM_OK && iters > 0) {
+      std::vector<double> y(iters);
+      for (int i = iters - 1; i >= 0; --i) {
+        double s = g[i];
+        for (int j = i + 1; j < iters; ++j) s -= H[(size_t)j * (kmax + 1) + i] * y[j];
+        y[i] = s / H[(size_t)i * (kmax + 1) + i];
+      }
+      cudaMemcpyAsync(dh, y.data(), sizeof(double) * iters, cudaMemcpyHostToDevice, st);
+      vec_combine(w, Q, n, iters, dh, n, st);
+    }
+  }
+  double true_res = resid;
+  if (status == BEM_OK && beta > 0.0) {
+    // true preconditioned residual ||C(b - V w)|| / ||C b||
+    status = apply_V(w, tmp);
+    if (status == BEM_OK) {
+      vec_axpby(tmp, 1.0, b, -1.0, n, st);
+      status = apply_C(tmp, wk);
+      if (status == BEM_OK) true_res = norm(wk) / beta;
+    }
+  }
+  cudaEventRecord(e1, st);
+  cudaEventSynchronize(e1);
+  float ms_total = 0;
+  cudaEventElapsedTime(&ms_total, e0, e1);
+  e = cudaGetLastError();
+  cudaFree(Q); cudaFree(tmp); cudaFree(u); cudaFree(v); cudaFree(wk); cudaFree(dh);
+  cudaEventDestroy(e0); cudaEventDestroy(e1); cudaEventDestroy(mv0); cudaEventDestroy(mv1);
+  if (e != cudaSuccess) return cuda_fail(e, "bem_solve_gmres");
+  if (rep) {
+    rep->iterations = iters;
+    rep->converged = converged ? 1 : 0;
+    rep->rel_residual = resid;
+    rep->true_rel_residual = true_res;
+    rep->seconds_total = ms_total * 1e-3;
+    rep->seconds_matvec = t_mv;
+    rep->seconds_comm = 0.0;
+  }
+  if (status != BEM_OK) return status;
+  if (!converged) {
+    set_error(breakdown ? "bem_solve_gmres: Arnoldi breakdown" : "bem_solve_gmres: max_iter reached");
+    return breakdown ? BEM_E_BREAKDOWN : BEM_E_NOT_CONVERGED;
+  }
+  return BEM_OK;
+}
+
+// ------------------------------------------------------------------ access
+bem_status bem_matrix_get_entries(const bem_matrix* A, long long count, const long long* rows,
+                                  const long long* cols, double* out) {
+  if (!A || (count > 0 && (!rows || !cols || !out))) { set_error("bem_matrix_get_entries: null argument"); return BEM_E_INVALID; }
+  if (A->kind == STB_MASS) { set_error("bem_matrix_get_entries: dense matrices only"); return BEM_E_STATE; }
+  const bem_mesh* m = A->mesh;
+  const long long n = (long long)m->ng * m->nt;
+  std::vector<long long> offs(count);
+  for (long long k = 0; k < count; ++k) {
+    if (rows[k] < 0 || rows[k] >= n || cols[k] < 0 || cols[k] >= n) { set_error("bem_matrix_get_entries: index out of range"); return BEM_E_INVALID; }
+    offs[k] = entry_offset(A, (int)(rows[k] / m->ng), (int)(rows[k] % m->ng), (int)(cols[k] / m->ng), (int)(cols[k] % m->ng));
+  }
+  cudaSetDevice(m->device);
+  const long long CH = 1 << 22;
+  long long* d_off = nullptr;
+  double* d_out = nullptr;
+  long long cap = std::min(count, CH);
+  if (cap <= 0) return BEM_OK;
+  cudaError_t e;
+  if ((e = cudaMalloc(&d_off, sizeof(long long) * cap)) != cudaSuccess) return cuda_fail(e, "get_entries");
+  if ((e = cudaMalloc(&d_out, sizeof(double) * cap)) != cudaSuccess) { cudaFree(d_off); return cuda_fail(e, "get_entries"); }
+  bem_status st = BEM_OK;
+  for (long long k0 = 0; k0 < count && st == BEM_OK; k0 += CH) {
+    long long nk = std::min(CH, count - k0);
+    cudaMemcpy(d_off, offs.data() + k0, sizeof(long long) * nk, cudaMemcpyHostToDevice);
+    st = gather_entries(A->data, d_off, nk, d_out, 0);
+    cudaMemcpy(out + k0, d_out, sizeof(double) * nk, cudaMemcpyDeviceToHost);
+  }
+  e = cudaGetLastError();
+  cudaFree(d_off);
+  cudaFree(d_out);
+  if (e != cudaSuccess) return cuda_fail(e, "get_entries");
+  return st;
+}
+
+bem_status bem_matrix_get(const bem_matrix* A, long long r0, long long nr, long long c0, long long nc,
+                          double* host) {
+  if (!A || !host || nr < 0 || nc < 0) { set_error("bem_matrix_get: bad argument"); return BEM_E_INVALID; }
+  std::vector<long long> rows((size_t)(nr * nc)), cols((size_t)(nr * nc));
+  for (long long r = 0; r < nr; ++r)
+    for (long long c = 0; c < nc; ++c) {
+      rows[r * nc + c] = r0 + r;
+      cols[r * nc + c] = c0 + c;
+    }
+  return bem_matrix_get_entries(A, nr * nc, rows.data(), cols.data(), host);
+}
+
+bem_status bem_matrix_info(const bem_matrix* A, int* kind, long long* entries, long long* bytes) {
+  if (!A) { set_error("bem_matrix_info: null"); return BEM_E_INVALID; }
+  if (kind) *kind = A->kind;
+  long long ent = 0;
+  if (A->kind != STB_MASS) {
+    const bem_mesh* m = A->mesh;
+    for (auto& b : m->blocks)
+      for (int a = b.a0; a < b.a1; ++a) ent += (long long)m->ng * m->ng * panel_nb(a, b.b0, b.b1);
+  } else {
+    ent = 3LL * A->mesh->ng * A->mesh->nt;
+  }
+  if (entries) *entries = ent;
+  if (bytes) *bytes = A->kind == STB_MASS ? 8 * ent : 8 * A->entries;
+  return BEM_OK;
+}
+
+void bem_matrix_destroy(bem_matrix* A) {
+  if (!A) return;
+  cudaFree(A->data);
+  cudaFree(A->d_segs);
+  cudaFree(A->d_partials);
+  cudaFree(A->d_row_pbase);
+  cudaFree(A->d_row_pstride);
+  cudaFree(A->d_ysum);
+  cudaFree(A->d_lo);
+  cudaFree(A->d_di);
+  cudaFree(A->d_up);
+  cudaFree(A->d_work);
+  delete A;
+}
+
+}  // extern "C"

@@ -1,0 +1,159 @@
+// internal.h — data structures shared by the host runtime and the CUDA kernels of libstbem.
+// Not part of the C-ABI (include/stbem.h is).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/stbem.h"
+
+namespace stb {
+
+// boundary element (primal segment or half segment): endpoints, length, unit tangent, outward normal
+struct Seg {
+  double ax, ay, bx, by;
+  double h;
+  double tx, ty;
+  double nx, ny;
+};
+
+// dual hat psi_l (R6): values at the primal nodes x_l (vm) and x_{l+1} (vp),
+// dual element lengths Lm = (h_{l-1}+h_l)/2 and Lp = (h_l+h_{l+1})/2
+struct Dual {
+  double vm, vp, Lm, Lp;
+};
+
+// one owned block (I,J) of the P x P temporal block structure:
+// test steps a in [a0,a1), trial steps b in [b0,b1) with b <= a, packed as row panels
+struct Block {
+  int I, J;
+  int a0, a1, b0, b1;
+  long long off;  // first entry of the block in the matrix storage
+};
+
+// row-panel geometry of block blk for test step a: nb trial steps, ld (padded) row stride
+inline __host__ __device__ int panel_nb(int a, int b0, int b1) {
+  int last = a < b1 - 1 ? a : b1 - 1;
+  return a >= b0 ? last - b0 + 1 : 0;
+}
+inline __host__ __device__ long long pad4(long long v) { return (v + 3) & ~3LL; }
+
+// flat description of the quadrature rules on the device
+constexpr int QMAX = 16;
+constexpr int QSING_MAX = 16;
+
+}  // namespace stb
+
+struct bem_comm_s {
+  int nranks = 1, rank = 0, device = 0;
+  void* nccl = nullptr;  // ncclComm_t
+};
+
+struct bem_mesh_s {
+  int ng = 0, nt = 0, P = 1;
+  double alpha = 1.0;
+  int device = 0;
+  std::vector<double> t;          // n_steps + 1
+  std::vector<stb::Seg> seg;      // ng primal segments
+  std::vector<stb::Seg> half;     // 2 ng half segments
+  std::vector<stb::Dual> dual;    // ng dual hats
+  std::vector<int> slice_first;   // P + 1
+  std::vector<int> owner;         // P * P, -1 above the diagonal
+  std::vector<stb::Block> blocks; // blocks owned by this rank
+  long long entries_owned = 0;
+  double hmax = 0, htmin = 0, kappa = 0;
+  int q_bulk = 4;
+  bem_comm* comm = nullptr;
+  int rank = 0, nranks = 1;
+  // device copies
+  double* d_t = nullptr;
+  stb::Seg* d_seg = nullptr;
+  stb::Seg* d_half = nullptr;
+  stb::Dual* d_dual = nullptr;
+  cudaStream_t stream = nullptr;  // internal stream (solver)
+};
+
+// matrix kinds
+enum { STB_V = 0, STB_K = 1, STB_D = 2, STB_MASS = 3 };
+
+struct bem_matrix_s {
+  int kind = 0;
+  const bem_mesh* mesh = nullptr;
+  // dense block-lower-triangular storage (V, K, D)
+  double* data = nullptr;
+  long long entries = 0;       // stored doubles (with row padding)
+  std::vector<long long> poff; // per block, per local test step: panel offset (flattened)
+  std::vector<int> poff_base;  // per block: index of its first panel in poff
+  // GEMV work decomposition
+  struct GemvSeg {
+    long long item0;   // first work item
+    long long off;     // panel offset in data
+    long long ld;      // padded row stride
+    long long len;     // row length (unpadded)
+    long long xoff;    // first column (global index) of the panel
+    long long pbase;   // partial index of (row i = 0, chunk 0) of this segment
+    int nch;           // chunks per row in this segment
+    int pstride;       // partials per row (all blocks of this test step)
+    int a;             // test step
+    int pad;
+  };
+  std::vector<GemvSeg> segs;
+  GemvSeg* d_segs = nullptr;
+  long long n_items = 0, n_partials = 0;
+  std::vector<long long> row_pbase;  // per test step: partial base, stride = row_pstride[a]
+  std::vector<int> row_pstride;
+  long long* d_row_pbase = nullptr;
+  int* d_row_pstride = nullptr;
+  double* d_partials = nullptr;
+  double* d_ysum = nullptr;  // multi-GPU partial y
+  // mass matrices: three cyclic diagonals per row (lower = col i-1, diag, upper = col i+1)
+  int mass_kind = -1;
+  double* d_lo = nullptr;
+  double* d_di = nullptr;
+  double* d_up = nullptr;
+  double* d_work = nullptr;  // tridiagonal solve scratch (3 n)
+};
+
+namespace stb {
+// error handling
+void set_error(const std::string& msg);
+bem_status cuda_fail(cudaError_t e, const char* where);
+void count_launch(long long k = 1);
+
+// host quadrature tables
+struct Rules {
+  double x[QMAX + 1][QMAX];  // Gauss-Legendre nodes on [0,1], n = 1..QMAX
+  double w[QMAX + 1][QMAX];
+  double lw[QMAX + 1][QMAX]; // log-weights: int_0^1 l_k(r) ln r dr for the same nodes
+};
+const Rules& host_rules();
+bem_status upload_rules();  // copy to __constant__ memory (per device, once)
+
+// kernels (assemble.cu)
+bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bulk, int q_sing,
+                           cudaStream_t st);
+// linear algebra (linalg.cu)
+bem_status gemv_setup(bem_matrix* A);
+bem_status gemv_launch(const bem_matrix* A, double a, const double* x, double b, double* y,
+                       cudaStream_t st);
+bem_status mass_setup(bem_matrix* M, int kind);
+bem_status mass_apply(const bem_matrix* M, double a, const double* x, double b, double* y,
+                      cudaStream_t st);
+bem_status mass_solve(const bem_matrix* M, int transpose, const double* x, double* y,
+                      cudaStream_t st);
+bem_status eval_special(int which, long long n, const double* x, double* out, cudaStream_t st);
+// vector kernels (linalg.cu)
+void vec_dots(const double* Q, long long ldq, int k, const double* w, long long n, double* out,
+              cudaStream_t st);
+void vec_update(double* w, const double* Q, long long ldq, int k, const double* h, long long n,
+                cudaStream_t st);
+void vec_scale(double* y, const double* x, double s, long long n, cudaStream_t st);
+void vec_axpby(double* y, double a, const double* x, double b, long long n, cudaStream_t st);
+void vec_combine(double* out, const double* Q, long long ldq, int k, const double* coef,
+                 long long n, cudaStream_t st);
+void vec_mul(double* y, const double* d, const double* x, long long n, cudaStream_t st);
+// collectives (comm.cpp)
+bem_status allreduce_sum(const bem_mesh* m, double* buf, long long n, cudaStream_t st);
+}  // namespace stb

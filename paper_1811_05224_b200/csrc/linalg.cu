@@ -1,0 +1,425 @@
+// linalg.cu — bandwidth-bound FP64 kernels of the solve:
+//   * packed block-lower-triangular GEMV (row panels, fixed chunks, warp-shuffle reductions,
+//     deterministic two-level sum; no tensor cores: a single right-hand side is not a contraction)
+//   * mass matrices: apply, lumped scaling, cyclic-tridiagonal solves (one system per time step)
+//   * Krylov vector kernels (block dot products, updates) with fixed reduction order
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "internal.h"
+#include "special.cuh"
+
+namespace stb {
+
+constexpr int GEMV_CH = 4096;  // doubles per work item (32 KB)
+constexpr int GEMV_WARPS = 8;
+
+using GSeg = bem_matrix_s::GemvSeg;
+
+// one warp per work item (row i of a panel, chunk c); items enumerated in memory order
+__global__ void __launch_bounds__(GEMV_WARPS * 32) k_gemv(const double* __restrict__ A,
+                                                         const GSeg* __restrict__ segs, int nseg,
+                                                         long long n_items, int ng,
+                                                         const double* __restrict__ x,
+                                                         double* __restrict__ partial) {
+  const int lane = threadIdx.x & 31;
+  const long long warp0 = (long long)blockIdx.x * GEMV_WARPS + (threadIdx.x >> 5);
+  const long long nwarp = (long long)gridDim.x * GEMV_WARPS;
+  int sidx = 0;
+  for (long long it = warp0; it < n_items; it += nwarp) {
+    // locate the segment (items are monotone per warp: linear search forward from last)
+    if (it < segs[sidx].item0) sidx = 0;
+    while (sidx + 1 < nseg && segs[sidx + 1].item0 <= it) ++sidx;
+    const GSeg S = segs[sidx];
+    const long long local = it - S.item0;
+    const int i = (int)(local / S.nch), c = (int)(local % S.nch);
+    const long long col0 = (long long)c * GEMV_CH;
+    const int len = (int)min((long long)GEMV_CH, S.len - col0);
+    const double* __restrict__ row = A + S.off + (long long)i * S.ld + col0;
+    const double* __restrict__ xx = x + S.xoff + col0;
+    double acc0 = 0.0, acc1 = 0.0;
+    // rows are 32-byte aligned (padded stride, aligned panel offsets); x is read as doubles
+    const int nv = len / 2;
+    const double2* __restrict__ row2 = reinterpret_cast<const double2*>(row);
+    int k = lane;
+#pragma unroll 4
+    for (; k < nv; k += 32) {
+      const double2 av = __ldcs(row2 + k);   // streamed once: evict-first
+      acc0 = fma(av.x, __ldg(xx + 2 * k), acc0);
+      acc1 = fma(av.y, __ldg(xx + 2 * k + 1), acc1);
+    }
+    if ((len & 1) && lane == 0) acc0 = fma(__ldcs(row + len - 1), __ldg(xx + len - 1), acc0);
+    double acc = acc0 + acc1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) partial[S.pbase + (long long)i * S.pstride + c] = acc;
+  }
+}
+
+// y[a*ng + i] = alpha * sum_k partial[row_pbase[a] + i*stride + k] + beta * y
+__global__ void k_gemv_reduce(const double* __restrict__ partial, const long long* __restrict__ pbase,
+                              const int* __restrict__ pstride, int ng, int nt, double alpha,
+                              double beta, double* __restrict__ y) {
+  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= (long long)ng * nt) return;
+  const int a = (int)(r / ng), i = (int)(r % ng);
+  const int st = pstride[a];
+  const double* p = partial + pbase[a] + (long long)i * st;
+  double s = 0.0;
+  for (int k = 0; k < st; ++k) s += p[k];
+  y[r] = (beta == 0.0) ? alpha * s : fma(alpha, s, beta * y[r]);
+}
+
+bem_status gemv_setup(bem_matrix* A) {
+  const bem_mesh* m = A->mesh;
+  const int ng = m->ng, nt = m->nt;
+  // partial layout per test step a: all blocks of the block row containing a, in block order
+  A->row_pbase.assign(nt, 0);
+  A->row_pstride.assign(nt, 0);
+  std::vector<std::vector<std::pair<int, int>>> blk_of_a(nt);  // (block index, nch)
+  for (size_t bi = 0; bi < m->blocks.size(); ++bi) {
+    const Block& b = m->blocks[bi];
+    for (int a = b.a0; a < b.a1; ++a) {
+      long long len = (long long)panel_nb(a, b.b0, b.b1) * ng;
+      if (len <= 0) continue;
+      int nch = (int)((len + GEMV_CH - 1) / GEMV_CH);
+      blk_of_a[a].push_back({(int)bi, nch});
+    }
+  }
+  long long pb = 0;
+  for (int a = 0; a < nt; ++a) {
+    int st = 0;
+    for (auto& pr : blk_of_a[a]) st += pr.second;
+    A->row_pbase[a] = pb;
+    A->row_pstride[a] = st;
+    pb += (long long)st * ng;
+  }
+  A->n_partials = pb;
+  // segments in memory order (block, a)
+  A->segs.clear();
+  long long item = 0;
+  for (size_t bi = 0; bi < m->blocks.size(); ++bi) {
+    const Block& b = m->blocks[bi];
+    for (int a = b.a0; a < b.a1; ++a) {
+      long long len = (long long)panel_nb(a, b.b0, b.b1) * ng;
+      if (len <= 0) continue;
+      int nch = (int)((len + GEMV_CH - 1) / GEMV_CH);
+      int cbase = 0;
+      for (auto& pr : blk_of_a[a]) {
+        if (pr.first == (int)bi) break;
+        cbase += pr.second;
+      }
+      GSeg s;
+      s.item0 = item;
+      s.off = A->poff[A->poff_base[bi] + (a - b.a0)];
+      s.ld = pad4(len);
+      s.len = len;
+      s.xoff = (long long)b.b0 * ng;
+      s.pbase = A->row_pbase[a] + cbase;
+      s.nch = nch;
+      s.pstride = A->row_pstride[a];
+      s.a = a;
+      s.pad = 0;
+      A->segs.push_back(s);
+      item += (long long)ng * nch;
+    }
+  }
+  A->n_items = item;
+  cudaError_t e;
+  size_t nseg = std::max<size_t>(1, A->segs.size());
+  if ((e = cudaMalloc(&A->d_segs, sizeof(GSeg) * nseg)) != cudaSuccess) return cuda_fail(e, "gemv_setup");
+  if ((e = cudaMemcpy(A->d_segs, A->segs.data(), sizeof(GSeg) * A->segs.size(), cudaMemcpyHostToDevice)) != cudaSuccess) return cuda_fail(e, "gemv_setup");
+  if ((e = cudaMalloc(&A->d_partials, sizeof(double) * std::max<long long>(1, A->n_partials))) != cudaSuccess) return cuda_fail(e, "gemv_setup");
+  if ((e = cudaMalloc(&A->d_row_pbase, sizeof(long long) * nt)) != cudaSuccess) return cuda_fail(e, "gemv_setup");
+  if ((e = cudaMalloc(&A->d_row_pstride, sizeof(int) * nt)) != cudaSuccess) return cuda_fail(e, "gemv_setup");
+  if ((e = cudaMemcpy(A->d_row_pbase, A->row_pbase.data(), sizeof(long long) * nt, cudaMemcpyHostToDevice)) != cudaSuccess) return cuda_fail(e, "gemv_setup");
+  if ((e = cudaMemcpy(A->d_row_pstride, A->row_pstride.data(), sizeof(int) * nt, cudaMemcpyHostToDevice)) != cudaSuccess) return cuda_fail(e, "gemv_setup");
+  if (m->nranks > 1) {
+    if ((e = cudaMalloc(&A->d_ysum, sizeof(double) * (size_t)ng * nt)) != cudaSuccess) return cuda_fail(e, "gemv_setup");
+  }
+  return BEM_OK;
+}
+
+static int g_num_sms = 0;
+static int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+bem_status gemv_launch(const bem_matrix* A, double a, const double* x, double b, double* y,
+                       cudaStream_t st) {
+  const bem_mesh* m = A->mesh;
+  const long long n = (long long)m->ng * m->nt;
+  if (A->n_items > 0) {
+    long long blocks = std::min<long long>((A->n_items + GEMV_WARPS - 1) / GEMV_WARPS, (long long)num_sms() * 8);
+    k_gemv<<<(unsigned)blocks, GEMV_WARPS * 32, 0, st>>>(A->data, A->d_segs, (int)A->segs.size(), A->n_items, m->ng, x, A->d_partials);
+    count_launch();
+  }
+  if (m->nranks > 1) {
+    // partial y over the owned blocks, summed over ranks (NCCL all-reduce = reduce-scatter +
+    // all-gather), then y = a * ysum + b * y
+    k_gemv_reduce<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(A->d_partials, A->d_row_pbase, A->d_row_pstride, m->ng, m->nt, 1.0, 0.0, A->d_ysum);
+    count_launch();
+    bem_status s = allreduce_sum(m, A->d_ysum, n, st);
+    if (s != BEM_OK) return s;
+    vec_axpby(y, a, A->d_ysum, b, n, st);
+  } else {
+    k_gemv_reduce<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(A->d_partials, A->d_row_pbase, A->d_row_pstride, m->ng, m->nt, a, b, y);
+    count_launch();
+  }
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? BEM_OK : cuda_fail(e, "bem_matvec");
+}
+
+// ------------------------------------------------------------------ mass matrices
+// primal (eq. 4): M[(a,i),(a,i)] = M[(a,i),(a,i+1)] = h_t(a) h_i / 2
+// dual (Thm 1):   lower h_{l-1} v-/4, diag h_l (2 + v- + v+)/4, upper h_{l+1} v+/4 (times h_t(a))
+// lumped: row sums of the dual mass
+__global__ void k_mass_fill(int kind, const Seg* __restrict__ seg, const Dual* __restrict__ dual,
+                            const double* __restrict__ t, int ng, int nt, double* lo, double* di,
+                            double* up) {
+  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= (long long)ng * nt) return;
+  const int a = (int)(r / ng), l = (int)(r % ng);
+  const double ht = t[a + 1] - t[a];
+  const double hm = seg[(l - 1 + ng) % ng].h, h0 = seg[l].h, hp = seg[(l + 1) % ng].h;
+  if (kind == BEM_MASS_PRIMAL) {
+    lo[r] = 0.0;
+    di[r] = 0.5 * ht * h0;
+    up[r] = 0.5 * ht * h0;
+  } else {
+    const double vm = dual[l].vm, vp = dual[l].vp;
+    const double L = ht * hm * vm * 0.25, D = ht * h0 * (2.0 + vm + vp) * 0.25, U = ht * hp * vp * 0.25;
+    if (kind == BEM_MASS_DUAL) {
+      lo[r] = L; di[r] = D; up[r] = U;
+    } else {
+      lo[r] = 0.0; di[r] = (L + D) + U; up[r] = 0.0;
+    }
+  }
+}
+
+bem_status mass_setup(bem_matrix* M, int kind) {
+  const bem_mesh* m = M->mesh;
+  const long long n = (long long)m->ng * m->nt;
+  M->mass_kind = kind;
+  cudaError_t e;
+  if ((e = cudaMalloc(&M->d_lo, sizeof(double) * n)) != cudaSuccess ||
+      (e = cudaMalloc(&M->d_di, sizeof(double) * n)) != cudaSuccess ||
+      (e = cudaMalloc(&M->d_up, sizeof(double) * n)) != cudaSuccess ||
+      (e = cudaMalloc(&M->d_work, sizeof(double) * 3 * n)) != cudaSuccess)
+    return cuda_fail(e, "bem_assemble_M");
+  k_mass_fill<<<(unsigned)((n + 255) / 256), 256>>>(kind, m->d_seg, m->d_dual, m->d_t, m->ng, m->nt, M->d_lo, M->d_di, M->d_up);
+  count_launch();
+  e = cudaDeviceSynchronize();
+  return e == cudaSuccess ? BEM_OK : cuda_fail(e, "bem_assemble_M");
+}
+
+__global__ void k_mass_apply(const double* __restrict__ lo, const double* __restrict__ di,
+                             const double* __restrict__ up, int ng, int nt, double a,
+                             const double* __restrict__ x, double b, double* __restrict__ y) {
+  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= (long long)ng * nt) return;
+  const int i = (int)(r % ng);
+  const long long base = r - i;
+  const double v = lo[r] * x[base + (i - 1 + ng) % ng] + di[r] * x[r] + up[r] * x[base + (i + 1) % ng];
+  y[r] = (b == 0.0) ? a * v : fma(a, v, b * y[r]);
+}
+
+bem_status mass_apply(const bem_matrix* M, double a, const double* x, double b, double* y,
+                      cudaStream_t st) {
+  const bem_mesh* m = M->mesh;
+  const long long n = (long long)m->ng * m->nt;
+  k_mass_apply<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(M->d_lo, M->d_di, M->d_up, m->ng, m->nt, a, x, b, y);
+  count_launch();
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? BEM_OK : cuda_fail(e, "mass_apply");
+}
+
+// cyclic tridiagonal solve per time step (Sherman-Morrison around the Thomas algorithm).
+// Row l of the (transposed) system: sub s_l at column l-1, diag d_l, super p_l at column l+1.
+__global__ void k_cyclic_solve(const double* __restrict__ lo, const double* __restrict__ di,
+                               const double* __restrict__ up, int ng, int nt, int transpose,
+                               const double* __restrict__ x, double* __restrict__ y,
+                               double* __restrict__ work) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= nt) return;
+  const long long base = (long long)a * ng;
+  auto sub = [&](int l) -> double {   // coefficient at column l-1 of row l
+    return transpose ? up[base + (l - 1 + ng) % ng] : lo[base + l];
+  };
+  auto sup = [&](int l) -> double {   // coefficient at column l+1 of row l
+    return transpose ? lo[base + (l + 1) % ng] : up[base + l];
+  };
+  auto dia = [&](int l) -> double { return di[base + l]; };
+  double* cp = work + 3 * base;       // modified super-diagonal
+  double* yy = cp + ng;               // solution of T y = rhs
+  double* zz = yy + ng;               // solution of T z = u
+  const double alpha_c = sub(0);      // row 0, column ng-1
+  const double beta_c = sup(ng - 1);  // row ng-1, column 0
+  const double gam = -dia(0);
+  // Thomas for T (first / last diagonal modified) with two right-hand sides
+  double b0 = dia(0) - gam;
+  cp[0] = sup(0) / b0;
+  yy[0] = x[base] / b0;
+  zz[0] = gam / b0;
+  for (int l = 1; l < ng; ++l) {
+    double bl = dia(l);
+    if (l == ng - 1) bl -= alpha_c * beta_c / gam;
+    const double sl = sub(l);
+    const double den = bl - sl * cp[l - 1];
+    cp[l] = (l < ng - 1) ? sup(l) / den : 0.0;
+    yy[l] = (x[base + l] - sl * yy[l - 1]) / den;
+    const double ul = (l == ng - 1) ? beta_c : 0.0;
+    zz[l] = (ul - sl * zz[l - 1]) / den;
+  }
+  for (int l = ng - 2; l >= 0; --l) {
+    yy[l] -= cp[l] * yy[l + 1];
+    zz[l] -= cp[l] * zz[l + 1];
+  }
+  const double fact = (yy[0] + alpha_c * yy[ng - 1] / gam) / (1.0 + zz[0] + alpha_c * zz[ng - 1] / gam);
+  for (int l = 0; l < ng; ++l) y[base + l] = yy[l] - fact * zz[l];
+}
+
+__global__ void k_diag_solve(const double* __restrict__ di, long long n, const double* __restrict__ x,
+                             double* __restrict__ y) {
+  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < n) y[r] = x[r] / di[r];
+}
+
+bem_status mass_solve(const bem_matrix* M, int transpose, const double* x, double* y,
+                      cudaStream_t st) {
+  const bem_mesh* m = M->mesh;
+  const long long n = (long long)m->ng * m->nt;
+  if (M->mass_kind == BEM_MASS_DUAL_LUMPED) {
+    k_diag_solve<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(M->d_di, n, x, y);
+  } else {
+    k_cyclic_solve<<<(m->nt + 63) / 64, 64, 0, st>>>(M->d_lo, M->d_di, M->d_up, m->ng, m->nt, transpose, x, y, M->d_work);
+  }
+  count_launch();
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? BEM_OK : cuda_fail(e, "mass_solve");
+}
+
+// ------------------------------------------------------------------ vector kernels
+// out[j] = sum_n Q[j*ldq + n] w[n] for j < k: one CTA per j, fixed-order tree reduction
+__global__ void k_dots(const double* __restrict__ Q, long long ldq, const double* __restrict__ w,
+                       long long n, double* __restrict__ out) {
+  __shared__ double red[32];
+  const int j = blockIdx.x;
+  const double* q = Q + (long long)j * ldq;
+  double s = 0.0;
+  for (long long r = threadIdx.x; r < n; r += blockDim.x) s = fma(q[r], w[r], s);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    s = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (threadIdx.x == 0) out[j] = s;
+  }
+}
+void vec_dots(const double* Q, long long ldq, int k, const double* w, long long n, double* out,
+              cudaStream_t st) {
+  k_dots<<<k, 1024, 0, st>>>(Q, ldq, w, n, out);
+  count_launch();
+}
+
+// w[n] -= sum_j h[j] Q[j][n]
+__global__ void k_update(double* __restrict__ w, const double* __restrict__ Q, long long ldq, int k,
+                         const double* __restrict__ h, long long n) {
+  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  double s = 0.0;
+  for (int j = 0; j < k; ++j) s = fma(h[j], Q[(long long)j * ldq + r], s);
+  w[r] -= s;
+}
+void vec_update(double* w, const double* Q, long long ldq, int k, const double* h, long long n,
+                cudaStream_t st) {
+  k_update<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(w, Q, ldq, k, h, n);
+  count_launch();
+}
+// out[n] = sum_j coef[j] Q[j][n]
+__global__ void k_combine(double* __restrict__ out, const double* __restrict__ Q, long long ldq,
+                          int k, const double* __restrict__ coef, long long n) {
+  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  double s = 0.0;
+  for (int j = 0; j < k; ++j) s = fma(coef[j], Q[(long long)j * ldq + r], s);
+  out[r] = s;
+}
+void vec_combine(double* out, const double* Q, long long ldq, int k, const double* coef, long long n,
+                 cudaStream_t st) {
+  k_combine<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(out, Q, ldq, k, coef, n);
+  count_launch();
+}
+__global__ void k_scale(double* __restrict__ y, const double* __restrict__ x, double s, long long n) {
+  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < n) y[r] = s * x[r];
+}
+void vec_scale(double* y, const double* x, double s, long long n, cudaStream_t st) {
+  k_scale<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(y, x, s, n);
+  count_launch();
+}
+__global__ void k_axpby(double* __restrict__ y, double a, const double* __restrict__ x, double b, long long n) {
+  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < n) y[r] = (b == 0.0) ? a * x[r] : fma(a, x[r], b * y[r]);
+}
+void vec_axpby(double* y, double a, const double* x, double b, long long n, cudaStream_t st) {
+  k_axpby<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(y, a, x, b, n);
+  count_launch();
+}
+__global__ void k_mul(double* __restrict__ y, const double* __restrict__ d, const double* __restrict__ x, long long n) {
+  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < n) y[r] = d[r] * x[r];
+}
+void vec_mul(double* y, const double* d, const double* x, long long n, cudaStream_t st) {
+  k_mul<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(y, d, x, n);
+  count_launch();
+}
+
+// ------------------------------------------------------------------ special-function probe
+__global__ void k_special(int which, long long n, const double* __restrict__ x, double* __restrict__ out) {
+  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const double v = x[r];
+  double o;
+  if (which == 0) o = dev_e1(v);
+  else if (which == 1) o = dev_ein(v);
+  else if (which == 2) o = dev_hfun(v);
+  else o = dev_psi(v);
+  out[r] = o;
+}
+bem_status eval_special(int which, long long n, const double* x, double* out, cudaStream_t st) {
+  if (n <= 0) return BEM_OK;
+  k_special<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(which, n, x, out);
+  count_launch();
+  cudaError_t e = cudaStreamSynchronize(st);
+  return e == cudaSuccess ? BEM_OK : cuda_fail(e, "bem_eval_special");
+}
+
+}  // namespace stb
+
+namespace stb {
+__global__ void k_gather(const double* __restrict__ data, const long long* __restrict__ offs, long long n,
+                         double* __restrict__ out) {
+  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < n) out[r] = offs[r] >= 0 ? data[offs[r]] : 0.0;
+}
+bem_status gather_entries(const double* data, const long long* offs, long long n, double* out, cudaStream_t st) {
+  if (n <= 0) return BEM_OK;
+  k_gather<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(data, offs, n, out);
+  count_launch();
+  cudaError_t e = cudaStreamSynchronize(st);
+  return e == cudaSuccess ? BEM_OK : cuda_fail(e, "gather_entries");
+}
+}  // namespace stb

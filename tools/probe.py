@@ -1,0 +1,26 @@
+"""quick timing probe: assemble V/K/D of a config on cuda:0 and time one GEMV"""
+import sys, time, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import workloads as W
+from paper_1811_05224_b200 import stbem as S
+name = sys.argv[1] if len(sys.argv) > 1 else "C3"
+kinds = sys.argv[2] if len(sys.argv) > 2 else "VKD"
+w = W.get(name)
+m = S.Mesh.from_workload(w)
+print(name, "ng", m.ng, "nt", m.nt, "q_bulk", m.info.q_bulk, "kappa", round(m.info.kappa, 4), "entries", m.info.entries_total, flush=True)
+mats = {}
+for k in kinds:
+    torch.cuda.synchronize(); t = time.time()
+    mats[k] = getattr(m, f"assemble_{k}")()
+    torch.cuda.synchronize(); dt = time.time() - t
+    print(f"assemble {k}: {dt:.3f} s  {m.info.entries_total/dt/1e9:.3f} G entries/s", flush=True)
+x = torch.tensor(W.random_vector(w.n), device="cuda"); y = torch.empty_like(x)
+A = mats[kinds[0]]
+for _ in range(3): A.matvec(x, y)
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(10): A.matvec(x, y)
+e1.record(); torch.cuda.synchronize()
+ms = e0.elapsed_time(e1) / 10
+print(f"gemv {ms:.3f} ms  {8*m.info.entries_total/ms/1e6:.1f} GB/s", flush=True)
