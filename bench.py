@@ -1,0 +1,322 @@
+#!/usr/bin/env python
+"""bench.py — one step = the whole hot path of arXiv:1811.05224 on one workload (BJ configs[2],
+C3: unit square, 256 segments x 256 uniform steps, N = 65536, alpha = 1):
+  mesh (a1) -> assemble V_h, K_h, D_h (a2-a5) -> mass matrices (a6) -> b = 1/2 M g + K g (a7)
+  -> preconditioned GMRES to 1e-10 (a8-a10, lumped dual mass).
+
+python bench.py [--gpus N] [--steps K] [--warmup W] [--impl native|reference] [--config C3]
+Under torchrun (N > 1) one rank per GPU; P = 2N temporal slices owned by the cyclic K_P plan.
+Prints ONE JSON line on rank 0 (contract in the task statement / DESIGN.md section 7).
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "element-pair integrals/s (assembly), matvec HBM GB/s, GMRES solve s at 1/2/4/8 GPU"
+UNIT = "element-pair integrals/s"
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+# FP64 DFMA peak: 148 SMs x 64 FP64 FMA/clk x 2 flop x 1.965 GHz (B200_PROFILING.md unit counts,
+# MEASURED_PEAKS sm_max_mhz); tools/fp64_peak.cu measured 34.1 TFLOP/s on this pool (profiles/).
+FP64_PEAK_DERIVED = 148 * 64 * 2 * 1.965e9 / 1e12
+# static FP64 flops of one bulk D_h kernel evaluation (h and E1 at one point pair and one time
+# node, small-x branch: two degree-20/21 Horner chains + combination), DESIGN.md section 6
+FLOPS_PER_EVAL = {"V": 52, "K": 50, "D": 98}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--precond", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region"""
+
+    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown," \
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
+             "clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = [r for r in self.rows if len(r) >= 7]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[3 + k].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------- oracle baseline
+def cpu_baseline(w, seconds, steps=1):
+    """the oracle as it stands (oracle/stbem_oracle.c, OpenMP, all host cores) on a bounded sample
+    of the same workload: V, K, D entries of a band of test rows around a = N_I/2 (all trial steps
+    b <= a), sized to ~`seconds` of CPU work; value = entries computed per second."""
+    from oracle import oracle as O
+    m = O.OracleMesh(w)
+    ng, nt = w.n_gamma, w.n_steps
+    a = nt // 2
+    rng = np.random.default_rng(1811)
+    # calibrate on a small sample, then size the timed sample
+    def run(kind, cnt):
+        rows = a * ng + rng.integers(0, ng, cnt)
+        cols = rng.integers(0, (a + 1) * ng, cnt)
+        t0 = time.perf_counter()
+        m.entries(kind, rows, cols)
+        return time.perf_counter() - t0
+    per = {k: max(run(k, 2000), 1e-6) / 2000 for k in "VKD"}
+    cost = sum(per.values())                      # seconds for one (V, K, D) entry triple
+    triples = max(1000, int(seconds / cost / 3))
+    t0 = time.perf_counter()
+    for k in "VKD":
+        run(k, triples)
+    dt = time.perf_counter() - t0
+    return {"value": 3 * triples / dt, "unit": UNIT, "cores": O.lib().ora_num_threads(), "kind": "oracle",
+            "sample": f"{triples} random entries each of V_h, K_h, D_h in test row a={a} of {w.name} "
+                      f"(all b <= a), {dt:.1f} s", "seconds": dt}
+
+
+# ---------------------------------------------------------------------- native step
+def native(args):
+    import torch
+    import torch.distributed as dist
+
+    import workloads as W
+    from paper_1811_05224_b200 import stbem as S
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    comm = S.Comm(rank, world, local) if world > 1 else None
+    w = W.get(args.config)
+    P = 1 if world == 1 else 2 * world
+    dev = torch.device("cuda", local)
+    g_host = torch.tensor(W.dirichlet_data(w), dtype=torch.float64).pin_memory()
+    w_host = torch.empty(w.n, dtype=torch.float64).pin_memory()
+    g = g_host.to(dev)
+    b = torch.empty_like(g)
+    wv = torch.empty_like(g)
+    tol = w.tol
+    Mkind = S.MASS_DUAL_LUMPED if args.precond == 1 else S.MASS_DUAL
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize()
+
+    def step(e2e):
+        """one pass of the hot path; e2e: the host copies of the public API are inside"""
+        ph = {}
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+        ev[0].record()
+        mesh = S.Mesh.from_workload(w, n_slices=P, comm=comm)
+        gg = g
+        if e2e:
+            gg = torch.empty_like(g)
+            gg.copy_(g_host, non_blocking=True)
+        V = mesh.assemble_V()
+        ev[1].record()
+        K = mesh.assemble_K()
+        ev[2].record()
+        D = mesh.assemble_D()
+        ev[3].record()
+        Mp = mesh.assemble_M(S.MASS_PRIMAL)
+        Mc = mesh.assemble_M(Mkind) if args.precond else None
+        S.rhs(K, Mp, gg, b)
+        ev[4].record()
+        rep = S.solve_gmres(V, b, wv, D=D if args.precond else None, M=Mc, rel_tol=tol, max_iter=200,
+                            precond=args.precond, history=False)
+        if e2e:
+            w_host.copy_(wv, non_blocking=True)
+        ev[5].record()
+        ev[5].synchronize()
+        ph["assemble_V"] = ev[0].elapsed_time(ev[1]) / 1e3
+        ph["assemble_K"] = ev[1].elapsed_time(ev[2]) / 1e3
+        ph["assemble_D"] = ev[2].elapsed_time(ev[3]) / 1e3
+        ph["rhs"] = ev[3].elapsed_time(ev[4]) / 1e3
+        ph["solve"] = ev[4].elapsed_time(ev[5]) / 1e3
+        ph["total"] = ev[0].elapsed_time(ev[5]) / 1e3
+        stats = {k: A.stats() for k, A in zip("VKD", (V, K, D))}
+        info = {f: getattr(mesh.info, f) for f, _ in mesh.info._fields_}
+        for A in (V, K, D, Mp) + ((Mc,) if Mc else ()):
+            A.close()
+        mesh.close()
+        return ph, rep, stats, info
+
+    for _ in range(args.warmup):
+        step(False)
+    barrier()
+    clocks = ClockSampler(local)
+    if rank == 0:
+        clocks.start()
+    S.launch_count(reset=True)
+    barrier()
+    t_wall = time.perf_counter()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    phases, reps, stats = [], [], None
+    for _ in range(args.steps):
+        ph, rep, stats, info = step(False)
+        phases.append(ph)
+        reps.append(rep)
+    e1.record()
+    barrier()
+    t_dev = e0.elapsed_time(e1) / 1e3
+    launches = S.launch_count()
+    wall = time.perf_counter() - t_wall
+    # e2e: same step through the public API with host buffers (H2D of g, D2H of w inside)
+    barrier()
+    e2 = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    e2[0].record()
+    for _ in range(args.steps):
+        step(True)
+    e2[1].record()
+    barrier()
+    t_e2e = e2[0].elapsed_time(e2[1]) / 1e3
+    ck = clocks.stop() if rank == 0 else None
+    if world > 1:
+        tt = torch.tensor([t_dev, t_e2e], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_dev, t_e2e = tt.tolist()
+    entries_total = info["entries_total"]
+    units_per_step = 3 * entries_total                     # V, K, D entries (element-pair integrals)
+    ms = 1e3 * t_dev / args.steps
+    value = units_per_step * args.steps / t_dev
+    e2e = units_per_step * args.steps / t_e2e
+    ph = {k: float(np.median([p[k] for p in phases])) for k in phases[0]}
+    rep = reps[-1]
+    # GEMV bandwidth: algorithmic bytes per product = 8 * stored entries (owned) + 16 N
+    n = w.n
+    bytes_per_gemv = 8 * info["entries_owned"] + 16 * n
+    n_mv = rep["n_matvec_V"] + rep["n_matvec_D"]
+    gemv_s = rep["seconds_matvec"] / max(1, n_mv)
+    peaks = json.load(open(PEAKS_PATH)) if os.path.exists(PEAKS_PATH) else {}
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    gemv_gbs = bytes_per_gemv / gemv_s / 1e9 if gemv_s > 0 else None
+    # dominant kernel: the longest assembly kernel family of the step
+    fam = []
+    for k in "VKD":
+        st = stats[k]
+        fam.append((st["ms_bulk"], k, "bulk", st))
+    ms_dom, kdom, _, st = max(fam)
+    flops = st["evals_bulk"] * FLOPS_PER_EVAL[kdom]
+    achieved = flops / (ms_dom * 1e-3) / 1e12
+    asm_s = ph["assemble_V"] + ph["assemble_K"] + ph["assemble_D"]
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"BJ configs[2] ({w.name}): {w.note}", "n_gamma": w.n_gamma, "n_steps": w.n_steps,
+                   "N": n, "alpha": w.alpha, "slices_P": P, "gmres_tol": tol, "precond": ["none", "lumped", "exact"][args.precond],
+                   "parallelism": f"cyclic K_P blocks over {world} GPU" + ("s" if world > 1 else ""),
+                   "l2": "inputs larger than L2 (each matrix 17 GB >> 126 MB)"},
+        "components": {
+            "assembly_pairs_per_s": units_per_step / asm_s,
+            "assembly_s": {"V": ph["assemble_V"], "K": ph["assemble_K"], "D": ph["assemble_D"]},
+            "matvec_gbs": gemv_gbs, "matvec_frac_of_hbm": (gemv_gbs / hbm_peak) if gemv_gbs else None,
+            "gmres_solve_s": ph["solve"], "gmres_iterations": rep["iterations"],
+            "gmres_true_rel_residual": rep["true_rel_residual"], "time_to_solution_s": ph["total"],
+            "kernel_ms": {k: {"bulk": stats[k]["ms_bulk"], "near": stats[k]["ms_near"], "sing": stats[k]["ms_sing"]} for k in "VKD"},
+        },
+        "roofline": {"bound": "alu", "kernel": f"k_bulk_{kdom}", "achieved": achieved, "peak": FP64_PEAK_DERIVED,
+                     "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_DERIVED, "traffic": None,
+                     "peak_note": "FP64 DFMA: 148 SM x 64 FMA/clk x 2 x 1.965 GHz (derived); measured 34.1 TFLOP/s",
+                     "flops_per_launch": flops, "evals_per_launch": st["evals_bulk"], "flops_per_eval": FLOPS_PER_EVAL[kdom]},
+        "roofline_gemv": {"bound": "hbm", "achieved": gemv_gbs, "peak": hbm_peak, "unit": "GB/s",
+                          "frac": (gemv_gbs / hbm_peak) if gemv_gbs else None, "bytes_per_launch": bytes_per_gemv},
+        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n},
+        "gpu_launches": int(launches),
+        "clocks": ck,
+        "wall_s": wall,
+    }
+    if rank == 0:
+        if world == 1 and not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline(w, args.cpu_seconds)
+        print(json.dumps(out), flush=True)
+    if comm:
+        comm.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------- reference arm
+def reference(args):
+    """the oracle (this tier's reference arm) on the host cores, same config/metric/unit; each step
+    is a bounded sample of the workload (rank 0 only; other ranks exit 0)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import workloads as W
+    w = W.get(args.config)
+    per_step = max(3.0, 60.0 / max(1, args.steps + args.warmup))
+    for _ in range(args.warmup):
+        cpu_baseline(w, per_step / 3)
+    vals, secs = [], []
+    for _ in range(args.steps):
+        r = cpu_baseline(w, per_step)
+        vals.append(r["value"])
+        secs.append(r["seconds"])
+    v = float(np.median(vals))
+    out = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.median(secs)),
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "impl": "reference",
+           "config": {"workload": f"BJ configs[2] ({w.name}): {w.note}", "n_gamma": w.n_gamma, "n_steps": w.n_steps, "N": w.n},
+           "cpu_baseline": {"value": v, "unit": UNIT, "cores": r["cores"], "kind": "oracle", "sample": r["sample"]},
+           "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        reference(a)
+    else:
+        native(a)

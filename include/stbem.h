@@ -95,7 +95,21 @@ typedef struct {
   double seconds_total;
   double seconds_matvec;     /* V and D products (device time) */
   double seconds_comm;       /* collectives (device time, 0 on one GPU) */
+  int n_matvec_V;            /* V_h products performed (incl. the true-residual check) */
+  int n_matvec_D;            /* D_h products performed */
 } bem_solve_report;
+
+/* Per-matrix assembly statistics: device time of the three assembly kernel families, measured
+ * with CUDA events on the stream passed to bem_assemble_*, and the exact number of kernel
+ * evaluations (point pair x time node for the bulk, point pair x lag for the near cells) that
+ * the shipped quadrature performs (DESIGN.md section 6 turns them into FP64 FLOPs). */
+typedef struct {
+  double ms_bulk, ms_near, ms_sing;
+  long long evals_bulk, evals_near;
+  int q_bulk, q_sing;
+  int launches;
+  long long entries;         /* stored (unpadded) entries */
+} bem_assembly_stats;
 
 /* ---------------------------------------------------------------- general */
 const char* bem_version(void);
@@ -164,11 +178,13 @@ bem_status bem_rhs(const bem_matrix* K, const bem_matrix* M_primal, const double
  * C_V^{-1} = M^{-1} D M^{-T}; D and M are ignored when opts->precond == 0.
  * M must be BEM_MASS_DUAL_LUMPED for precond 1 and BEM_MASS_DUAL for precond 2.
  * x0 = 0.  b_dev, w_dev device vectors of length n.  res_hist_host: NULL or max_iter+1 doubles
- * (relative preconditioned residual estimates, [0] = 1).  Runs on the mesh's internal stream and
- * synchronises.  Returns BEM_E_NOT_CONVERGED / BEM_E_BREAKDOWN with w and the report filled. */
+ * (relative preconditioned residual estimates, [0] = 1).  Runs on `stream` (ordered after the work
+ * already queued there, e.g. the right-hand side) and synchronises it once per iteration (the
+ * Hessenberg column goes to the host for the Givens rotation).  Returns BEM_E_NOT_CONVERGED /
+ * BEM_E_BREAKDOWN with w and the report filled. */
 bem_status bem_solve_gmres(const bem_matrix* V, const bem_matrix* D, const bem_matrix* M,
                            const double* b_dev, double* w_dev, const bem_gmres_opts* opts,
-                           bem_solve_report* report, double* res_hist_host);
+                           bem_solve_report* report, double* res_hist_host, bem_stream stream);
 
 /* ---------------------------------------------------------------- access */
 /* dense window [r0, r0+nr) x [c0, c0+nc) into host_dst (row-major nr x nc); causality zeros
@@ -180,6 +196,7 @@ bem_status bem_matrix_get_entries(const bem_matrix* A, long long count, const lo
                                   const long long* cols_host, double* out_host);
 /* stored entries and bytes on this rank; kind: 0 V, 1 K, 2 D, 3 mass */
 bem_status bem_matrix_info(const bem_matrix* A, int* kind, long long* entries, long long* bytes);
+bem_status bem_matrix_stats(const bem_matrix* A, bem_assembly_stats* out);
 void bem_matrix_destroy(bem_matrix* A);
 
 /* ---------------------------------------------------------- diagnostics */

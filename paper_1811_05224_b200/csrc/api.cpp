@@ -47,7 +47,7 @@ bem_matrix* new_dense(const bem_mesh* m, int kind, bem_status* st) {
 bem_status assemble(int kind, const bem_mesh* m, const bem_quad_opts* o, bem_stream s, bem_matrix** out) {
   if (!m || !out) { set_error("bem_assemble: null argument"); return BEM_E_INVALID; }
   *out = nullptr;
-  int q_bulk = (o && o->q_bulk > 0) ? o->q_bulk : m->q_bulk;
+  int q_bulk = (o && o->q_bulk > 0) ? o->q_bulk : (kind == STB_D ? m->q_bulk_d : m->q_bulk);
   int q_sing = (o && o->q_sing > 0) ? o->q_sing : 12;
   if (q_bulk < 3 || q_bulk > 8 || q_bulk == 7) { set_error("bem_assemble: q_bulk must be one of 3,4,5,6,8"); return BEM_E_INVALID; }
   if (q_sing < 4 || q_sing > QSING_MAX) { set_error("bem_assemble: q_sing must be in [4,16]"); return BEM_E_INVALID; }
@@ -156,7 +156,7 @@ bem_status bem_eval_special(int which, long long count, const double* x, double*
 // ------------------------------------------------------------------ GMRES
 bem_status bem_solve_gmres(const bem_matrix* V, const bem_matrix* D, const bem_matrix* M,
                            const double* b, double* w, const bem_gmres_opts* opts,
-                           bem_solve_report* rep, double* hist) {
+                           bem_solve_report* rep, double* hist, bem_stream stream) {
   if (!V || !b || !w || !opts) { set_error("bem_solve_gmres: null argument"); return BEM_E_INVALID; }
   if (V->kind != STB_V) { set_error("bem_solve_gmres: first matrix must be V_h"); return BEM_E_STATE; }
   const int prec = opts->precond;
@@ -173,16 +173,20 @@ bem_status bem_solve_gmres(const bem_matrix* V, const bem_matrix* D, const bem_m
   cudaSetDevice(m->device);
   const long long n = (long long)m->ng * m->nt;
   const int kmax = opts->max_iter;
-  cudaStream_t st = m->stream;
+  cudaStream_t st = S(stream);
   double *Q = nullptr, *tmp = nullptr, *u = nullptr, *v = nullptr, *dh = nullptr, *wk = nullptr;
+  double* hpin = nullptr;  // pinned host copy of the Hessenberg column
   cudaError_t e;
-  if ((e = cudaMalloc(&Q, sizeof(double) * n * (kmax + 1))) != cudaSuccess ||
-      (e = cudaMalloc(&tmp, sizeof(double) * n)) != cudaSuccess ||
-      (e = cudaMalloc(&u, sizeof(double) * n)) != cudaSuccess ||
-      (e = cudaMalloc(&v, sizeof(double) * n)) != cudaSuccess ||
-      (e = cudaMalloc(&wk, sizeof(double) * n)) != cudaSuccess ||
-      (e = cudaMalloc(&dh, sizeof(double) * 2 * (kmax + 2))) != cudaSuccess) {
-    cudaFree(Q); cudaFree(tmp); cudaFree(u); cudaFree(v); cudaFree(wk); cudaFree(dh);
+  // stream-ordered allocations: no device-wide synchronisation
+  if ((e = cudaMallocAsync(&Q, sizeof(double) * n * (kmax + 1), st)) != cudaSuccess ||
+      (e = cudaMallocAsync(&tmp, sizeof(double) * n, st)) != cudaSuccess ||
+      (e = cudaMallocAsync(&u, sizeof(double) * n, st)) != cudaSuccess ||
+      (e = cudaMallocAsync(&v, sizeof(double) * n, st)) != cudaSuccess ||
+      (e = cudaMallocAsync(&wk, sizeof(double) * n, st)) != cudaSuccess ||
+      (e = cudaMallocAsync(&dh, sizeof(double) * 2 * (kmax + 2), st)) != cudaSuccess ||
+      (e = cudaMallocHost(&hpin, sizeof(double) * 2 * (kmax + 2))) != cudaSuccess) {
+    cudaFreeAsync(Q, st); cudaFreeAsync(tmp, st); cudaFreeAsync(u, st); cudaFreeAsync(v, st);
+    cudaFreeAsync(wk, st); cudaFreeAsync(dh, st); cudaFreeHost(hpin);
     cudaGetLastError();
     set_error("bem_solve_gmres: allocation failed");
     return BEM_E_NOMEM;
@@ -190,6 +194,7 @@ bem_status bem_solve_gmres(const bem_matrix* V, const bem_matrix* D, const bem_m
   cudaEvent_t e0, e1, mv0, mv1;
   cudaEventCreate(&e0); cudaEventCreate(&e1); cudaEventCreate(&mv0); cudaEventCreate(&mv1);
   double t_mv = 0.0;
+  int nmv_V = 0, nmv_D = 0;
   cudaEventRecord(e0, st);
   bem_status status = BEM_OK;
   // z = C r  (C = M^{-1} D M^{-T}, lumped or exact), out may alias nothing else
@@ -201,6 +206,7 @@ bem_status bem_solve_gmres(const bem_matrix* V, const bem_matrix* D, const bem_m
     if (s1 != BEM_OK) return s1;
     cudaEventRecord(mv0, st);
     s1 = gemv_launch(D, 1.0, u, 0.0, v, st);
+    ++nmv_D;
     cudaEventRecord(mv1, st);
     if (s1 != BEM_OK) return s1;
     cudaEventSynchronize(mv1);
@@ -212,6 +218,7 @@ bem_status bem_solve_gmres(const bem_matrix* V, const bem_matrix* D, const bem_m
   auto apply_V = [&](const double* x, double* out) -> bem_status {
     cudaEventRecord(mv0, st);
     bem_status s1 = gemv_launch(V, 1.0, x, 0.0, out, st);
+    ++nmv_V;
     cudaEventRecord(mv1, st);
     cudaEventSynchronize(mv1);
     float ms = 0;
@@ -221,12 +228,12 @@ bem_status bem_solve_gmres(const bem_matrix* V, const bem_matrix* D, const bem_m
   };
   auto norm = [&](const double* x) -> double {
     vec_dots(x, 0, 1, x, n, dh, st);
-    double hv = 0;
-    cudaMemcpyAsync(&hv, dh, sizeof(double), cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(hpin + 2 * (kmax + 2) - 1, dh, sizeof(double), cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
-    return std::sqrt(hv);
+    return std::sqrt(hpin[2 * (kmax + 2) - 1]);
   };
-  std::vector<double> H((size_t)(kmax + 1) * kmax, 0.0), cs(kmax), sn(kmax), g(kmax + 1, 0.0), hcol(2 * (kmax + 2));
+  std::vector<double> H((size_t)(kmax + 1) * kmax, 0.0), cs(kmax), sn(kmax), g(kmax + 1, 0.0);
+  double* hcol = hpin;
   int iters = 0;
   bool converged = false, breakdown = false;
   double resid = 1.0;
@@ -249,8 +256,8 @@ bem_status bem_solve_gmres(const bem_matrix* V, const bem_matrix* D, const bem_m
       vec_update(wk, Q, n, k + 1, dh, n, st);
       vec_dots(Q, n, k + 1, wk, n, dh + (kmax + 2), st);
       vec_update(wk, Q, n, k + 1, dh + (kmax + 2), n, st);
-      cudaMemcpyAsync(hcol.data(), dh, sizeof(double) * (k + 1), cudaMemcpyDeviceToHost, st);
-      cudaMemcpyAsync(hcol.data() + (kmax + 2), dh + (kmax + 2), sizeof(double) * (k + 1), cudaMemcpyDeviceToHost, st);
+      cudaMemcpyAsync(hcol, dh, sizeof(double) * (k + 1), cudaMemcpyDeviceToHost, st);
+      cudaMemcpyAsync(hcol + (kmax + 2), dh + (kmax + 2), sizeof(double) * (k + 1), cudaMemcpyDeviceToHost, st);
       double hk1 = norm(wk);  // synchronises
       double* Hk = &H[(size_t)k * (kmax + 1)];
       for (int j = 0; j <= k; ++j) Hk[j] = hcol[j] + hcol[(kmax + 2) + j];
@@ -281,7 +288,8 @@ bem_status bem_solve_gmres(const bem_matrix* V, const bem_matrix* D, const bem_m
         for (int j = i + 1; j < iters; ++j) s -= H[(size_t)j * (kmax + 1) + i] * y[j];
         y[i] = s / H[(size_t)i * (kmax + 1) + i];
       }
-      cudaMemcpyAsync(dh, y.data(), sizeof(double) * iters, cudaMemcpyHostToDevice, st);
+      for (int i = 0; i < iters; ++i) hpin[i] = y[i];
+      cudaMemcpyAsync(dh, hpin, sizeof(double) * iters, cudaMemcpyHostToDevice, st);
       vec_combine(w, Q, n, iters, dh, n, st);
     }
   }
@@ -300,7 +308,10 @@ bem_status bem_solve_gmres(const bem_matrix* V, const bem_matrix* D, const bem_m
   float ms_total = 0;
   cudaEventElapsedTime(&ms_total, e0, e1);
   e = cudaGetLastError();
-  cudaFree(Q); cudaFree(tmp); cudaFree(u); cudaFree(v); cudaFree(wk); cudaFree(dh);
+  cudaFreeAsync(Q, st); cudaFreeAsync(tmp, st); cudaFreeAsync(u, st); cudaFreeAsync(v, st);
+  cudaFreeAsync(wk, st); cudaFreeAsync(dh, st);
+  cudaStreamSynchronize(st);
+  cudaFreeHost(hpin);
   cudaEventDestroy(e0); cudaEventDestroy(e1); cudaEventDestroy(mv0); cudaEventDestroy(mv1);
   if (e != cudaSuccess) return cuda_fail(e, "bem_solve_gmres");
   if (rep) {
@@ -311,6 +322,8 @@ bem_status bem_solve_gmres(const bem_matrix* V, const bem_matrix* D, const bem_m
     rep->seconds_total = ms_total * 1e-3;
     rep->seconds_matvec = t_mv;
     rep->seconds_comm = 0.0;
+    rep->n_matvec_V = nmv_V;
+    rep->n_matvec_D = nmv_D;
   }
   if (status != BEM_OK) return status;
   if (!converged) {
@@ -365,6 +378,23 @@ bem_status bem_matrix_get(const bem_matrix* A, long long r0, long long nr, long 
       cols[r * nc + c] = c0 + c;
     }
   return bem_matrix_get_entries(A, nr * nc, rows.data(), cols.data(), host);
+}
+
+bem_status bem_matrix_stats(const bem_matrix* A, bem_assembly_stats* o) {
+  if (!A || !o) { set_error("bem_matrix_stats: null"); return BEM_E_INVALID; }
+  o->ms_bulk = A->ms_bulk;
+  o->ms_near = A->ms_near;
+  o->ms_sing = A->ms_sing;
+  o->evals_bulk = A->ev_bulk;
+  o->evals_near = A->ev_near;
+  o->q_bulk = A->q_bulk;
+  o->q_sing = A->q_sing;
+  o->launches = A->launches;
+  long long ent = 0;
+  int kind = 0;
+  bem_matrix_info(A, &kind, &ent, nullptr);
+  o->entries = ent;
+  return BEM_OK;
 }
 
 bem_status bem_matrix_info(const bem_matrix* A, int* kind, long long* entries, long long* bytes) {

@@ -82,7 +82,7 @@ __device__ __forceinline__ Lags make_lags(const double* __restrict__ t, int a, i
   return L;
 }
 
-__device__ __forceinline__ double seg_dist(const Seg& X, const Seg& Y) {
+__host__ __device__ inline double seg_dist(const Seg& X, const Seg& Y) {
   auto pd = [](double px, double py, const Seg& S) {
     double dx = px - S.ax, dy = py - S.ay;
     double f = dx * S.tx + dy * S.ty;
@@ -93,19 +93,19 @@ __device__ __forceinline__ double seg_dist(const Seg& X, const Seg& Y) {
   return fmin(fmin(pd(X.ax, X.ay, Y), pd(X.bx, X.by, Y)), fmin(pd(Y.ax, Y.ay, X), pd(Y.bx, Y.by, X)));
 }
 // Gauss order for non-touching pairs in cells d <= 1 (measured table)
-__device__ __forceinline__ int near_order(const Seg& X, const Seg& Y) {
+__host__ __device__ inline int near_order(const Seg& X, const Seg& Y) {
   double rho = seg_dist(X, Y) / fmax(X.h, Y.h);
   return rho < 2.5 ? 10 : (rho < 5.0 ? 8 : 6);
 }
 // relation of elements p, q of a closed chain of n: 0 disjoint, 1 identical,
 // 2 X.end == Y.start, 3 X.start == Y.end
-__device__ __forceinline__ int chain_rel(int p, int q, int n) {
+__host__ __device__ inline int chain_rel(int p, int q, int n) {
   if (p == q) return 1;
   if ((p + 1) % n == q) return 2;
   if ((q + 1) % n == p) return 3;
   return 0;
 }
-__device__ __forceinline__ bool collinear(const Seg& X, const Seg& Y) {
+__host__ __device__ inline bool collinear(const Seg& X, const Seg& Y) {
   double d0 = (X.ax - Y.ax) * Y.nx + (X.ay - Y.ay) * Y.ny;
   double d1 = (X.bx - Y.ax) * Y.nx + (X.by - Y.ay) * Y.ny;
   double tol = 1e-13 * fmax(X.h, Y.h);
@@ -113,11 +113,15 @@ __device__ __forceinline__ bool collinear(const Seg& X, const Seg& Y) {
 }
 
 // ================================================================= bulk V
-// thread = segment pair (i, j): warp = row i, lane = column j; band of R test steps
+// thread = segment pair (i, j): warp = row i, lane = column j; band of R test steps.
+// Every point pair is first evaluated with the small-x form (branch-free, unrolled: the Q*Q
+// Horner chains interleave); the rare points with x >= 4 are then overwritten by the large-x
+// form (exp + polynomial in 1/x).
 template <int Q, int R>
 __global__ void __launch_bounds__(128) k_bulk_V(BlockArgs B, const Seg* __restrict__ seg,
                                                 const double* __restrict__ t, double alpha,
                                                 int nband) {
+  constexpr int QQ = Q * Q;
   const int ng = B.ng;
   const int j = blockIdx.x * 32 + (threadIdx.x & 31);
   const int i = blockIdx.y * 4 + (threadIdx.x >> 5);
@@ -130,7 +134,7 @@ __global__ void __launch_bounds__(128) k_bulk_V(BlockArgs B, const Seg* __restri
   if (bmax < B.b0) return;
   const Seg X = seg[i], Y = seg[j];
   const bool reg = (i == j);
-  double c[Q * Q], L[Q * Q], ic[Q * Q];
+  double c[QQ], L[QQ];
 #pragma unroll
   for (int u = 0; u < Q; ++u) {
     double px = fma(c_gx[Q][u], X.bx - X.ax, X.ax), py = fma(c_gx[Q][u], X.by - X.ay, X.ay);
@@ -141,7 +145,6 @@ __global__ void __launch_bounds__(128) k_bulk_V(BlockArgs B, const Seg* __restri
       double cc = 0.25 * alpha * (dx * dx + dy * dy);
       c[u * Q + v] = cc;
       L[u * Q + v] = cc > 0.0 ? log(cc) : 0.0;
-      ic[u * Q + v] = cc > 0.0 ? 1.0 / cc : 0.0;
     }
   }
   const double scale = X.h * Y.h / (4.0 * STB_PI);
@@ -158,17 +161,31 @@ __global__ void __launch_bounds__(128) k_bulk_V(BlockArgs B, const Seg* __restri
       if (x <= r_hi && x > y) {
         const double s = t[x] - ty;
         const double lns = log(s), is = 1.0 / s;
+        const double g0 = STB_GAMMA - lns;
+        double hv[QQ];
+        bool large = false;
+#pragma unroll
+        for (int p = 0; p < QQ; ++p) {
+          const double xx = c[p] * is;
+          hv[p] = fma(-(1.0 + xx), reg ? g0 : g0 + L[p], gh_poly(xx));
+          large |= xx >= STB_XSPLIT;
+        }
+        if (large) {
+#pragma unroll
+          for (int p = 0; p < QQ; ++p) {
+            const double xx = c[p] * is;
+            if (xx >= STB_XSPLIT) {
+              const double tt = 1.0 / xx, e = exp(-xx);
+              hv[p] = fma(1.0 + xx, e1_large(tt, e) + (reg ? L[p] : 0.0), -e);
+            }
+          }
+        }
         double acc = 0.0;
 #pragma unroll
         for (int u = 0; u < Q; ++u) {
           double part = 0.0;
 #pragma unroll
-          for (int v = 0; v < Q; ++v) {
-            const int p = u * Q + v;
-            const double xx = c[p] * is;
-            const double gl = STB_GAMMA + (reg ? 0.0 : L[p]) - lns;
-            part = fma(c_gw[Q][v], bulk_h(xx, gl, s * ic[p], reg ? L[p] : 0.0), part);
-          }
+          for (int v = 0; v < Q; ++v) part = fma(c_gw[Q][v], hv[u * Q + v], part);
           acc = fma(c_gw[Q][u], part, acc);
         }
         Phi[r] = s * acc;
@@ -198,6 +215,7 @@ template <int Q, int R>
 __global__ void __launch_bounds__(128) k_bulk_K(BlockArgs B, const Seg* __restrict__ seg,
                                                 const double* __restrict__ t, double alpha,
                                                 int nband) {
+  constexpr int QQ = Q * Q;
   const int ng = B.ng;
   const int lane = threadIdx.x & 31;
   const int n = blockIdx.x * 31 + lane - 1;       // output column (valid for lane >= 1)
@@ -213,7 +231,7 @@ __global__ void __launch_bounds__(128) k_bulk_K(BlockArgs B, const Seg* __restri
   if (bmax < B.b0) return;
   const Seg X = seg[i], Y = seg[j];
   const bool zero = collinear(X, Y) || (n >= ng && lane >= 1);
-  double c[Q * Q], L[Q * Q], ic[Q * Q], dw[Q * Q];
+  double c[QQ], L[QQ], dw[QQ];
 #pragma unroll
   for (int u = 0; u < Q; ++u) {
     double px = fma(c_gx[Q][u], X.bx - X.ax, X.ax), py = fma(c_gx[Q][u], X.by - X.ay, X.ay);
@@ -225,7 +243,6 @@ __global__ void __launch_bounds__(128) k_bulk_K(BlockArgs B, const Seg* __restri
       cc = zero ? 1.0 : cc;
       c[u * Q + v] = cc;
       L[u * Q + v] = log(cc);
-      ic[u * Q + v] = 1.0 / cc;
       dw[u * Q + v] = zero ? 0.0 : c_gw[Q][u] * c_gw[Q][v] * (dx * Y.nx + dy * Y.ny);
     }
   }
@@ -243,14 +260,31 @@ __global__ void __launch_bounds__(128) k_bulk_K(BlockArgs B, const Seg* __restri
       if (x <= r_hi && x > y && !zero) {
         const double s = t[x] - ty;
         const double lns = log(s), is = 1.0 / s;
+        const double g0 = STB_GAMMA - lns;
+        double ps[QQ];
+        bool large = false;
+#pragma unroll
+        for (int p = 0; p < QQ; ++p) {
+          const double xx = c[p] * is;
+          ps[p] = psi_poly(xx) + (g0 + L[p]);
+          large |= xx >= STB_XSPLIT;
+        }
+        if (large) {
+#pragma unroll
+          for (int p = 0; p < QQ; ++p) {
+            const double xx = c[p] * is;
+            if (xx >= STB_XSPLIT) {
+              const double tt = 1.0 / xx, e = exp(-xx);
+              ps[p] = e * tt - tt - e1_large(tt, e);
+            }
+          }
+        }
         double a0 = 0.0, a1 = 0.0;
 #pragma unroll
-        for (int p = 0; p < Q * Q; ++p) {
-          const double xx = c[p] * is;
-          const double ps = dw[p] * bulk_psi(xx, STB_GAMMA + L[p] - lns, s * ic[p]);
-          const double f = c_gx[Q][p % Q];
-          a1 = fma(f, ps, a1);
-          a0 += ps;
+        for (int p = 0; p < QQ; ++p) {
+          const double v = dw[p] * ps[p];
+          a1 = fma(c_gx[Q][p % Q], v, a1);
+          a0 += v;
         }
         P0[r] = a0 - a1;   // lambda_0 = 1 - f
         P1[r] = a1;
@@ -283,57 +317,81 @@ __global__ void __launch_bounds__(128) k_bulk_K(BlockArgs B, const Seg* __restri
 // ================================================================= D tiles
 // CTA: warp w <-> half row p = 2 L0 - 1 + w (w < 2 TL + 2), lane <-> half column
 // q = 2 K0 - 1 + lane; entries (l, k), l in [L0, L0+TL), k in [K0, K0+15).
-constexpr int DTL = 3;
+// Combine (deterministic, no atomics): stage 1 contracts the 4 half columns of each dual hat k
+// inside the warp with three shuffles per quantity; stage 2 contracts the 4 half rows of each
+// dual hat l through shared memory.
 constexpr int DTK = 15;
-constexpr int DWARPS = 2 * DTL + 2;  // 8
+constexpr int DTL_BULK = 3;   // dual rows per CTA (8 warps)
+constexpr int DTL_NEAR = 3;
 
 struct DMom {
   double v, f00, f01, f10, f11;
 };
 
-// combine the 5 half-pair moments of the CTA into D entries and store them
-__device__ __forceinline__ void d_combine_store(const BlockArgs& B, const Dual* __restrict__ dual,
-                                                const Seg* __restrict__ half, double (*sm)[32][5],
-                                                int L0, int K0, int a, int b, bool add) {
-  const int ng = B.ng, nh = 2 * ng;
-  for (int e = threadIdx.x; e < DTL * DTK; e += blockDim.x) {
-    const int l = L0 + e / DTK, k = K0 + e % DTK;
-    if (l >= ng || k >= ng) continue;
-    const Dual dl = dual[l], dk = dual[k];
-    const double dvl[4] = {1.0 / dl.Lm, 1.0 / dl.Lm, -1.0 / dl.Lp, -1.0 / dl.Lp};
-    const double dvk[4] = {1.0 / dk.Lm, 1.0 / dk.Lm, -1.0 / dk.Lp, -1.0 / dk.Lp};
-    const double vl[4][2] = {{0.0, dl.vm}, {dl.vm, 1.0}, {1.0, dl.vp}, {dl.vp, 0.0}};
-    const double vk[4][2] = {{0.0, dk.vm}, {dk.vm, 1.0}, {1.0, dk.vp}, {dk.vp, 0.0}};
-    double acc = 0.0;
+struct DLane {
+  double cv[2], c0[2], c1[2];  // role lo (n = lane&1) and hi (n + 2) coefficients of dual k
+  double nn;                   // n_p . n_q
+  __device__ void init(const Dual* __restrict__ dual, const Seg& X, const Seg& Y, int K0, int ng, int lane) {
+    nn = X.nx * Y.nx + X.ny * Y.ny;
 #pragma unroll
-    for (int m = 0; m < 4; ++m) {
-      const int pl = 2 * (l - L0) + m;
-      const Seg& Hp = half[((2 * l - 1 + m) % nh + nh) % nh];
-#pragma unroll
-      for (int nn_ = 0; nn_ < 4; ++nn_) {
-        const int ql = 2 * (k - K0) + nn_;
-        const Seg& Hq = half[((2 * k - 1 + nn_) % nh + nh) % nh];
-        const double nn = Hp.nx * Hq.nx + Hp.ny * Hq.ny;
-        const double* M = sm[pl][ql];
-        double fn = vl[m][0] * (vk[nn_][0] * M[1] + vk[nn_][1] * M[2]) +
-                    vl[m][1] * (vk[nn_][0] * M[3] + vk[nn_][1] * M[4]);
-        acc += dvl[m] * dvk[nn_] * M[0] + nn * fn;
+    for (int role = 0; role < 2; ++role) {
+      const int n = (lane & 1) + 2 * role;
+      const int jj = (lane - n) >> 1;
+      const int k = K0 + jj;
+      cv[role] = c0[role] = c1[role] = 0.0;
+      if (lane - n >= 0 && jj < DTK && k < ng) {
+        const Dual d = dual[k];
+        cv[role] = n < 2 ? 1.0 / d.Lm : -1.0 / d.Lp;
+        const double v0[4] = {0.0, d.vm, 1.0, d.vp}, v1[4] = {d.vm, 1.0, d.vp, 0.0};
+        c0[role] = nn * v0[n];
+        c1[role] = nn * v1[n];
       }
     }
-    double* p = entry_ptr(B, a, l, b, k);
-    if (add) *p += acc; else *p = acc;
   }
+  // stage 1: T at even lanes 2j = sum over the 4 half columns of dual K0 + j; stored to smem
+  __device__ void stage1(const DMom& M, double* __restrict__ T, int lane) const {
+    double A[3], Bq[3];
+#pragma unroll
+    for (int role = 0; role < 2; ++role) {
+      double* o = role ? Bq : A;
+      o[0] = cv[role] * M.v;
+      o[1] = c0[role] * M.f00 + c1[role] * M.f01;
+      o[2] = c0[role] * M.f10 + c1[role] * M.f11;
+    }
+#pragma unroll
+    for (int qn = 0; qn < 3; ++qn) {
+      const double s = A[qn] + __shfl_down_sync(0xffffffffu, A[qn], 1) +
+                       __shfl_down_sync(0xffffffffu, Bq[qn], 2) + __shfl_down_sync(0xffffffffu, Bq[qn], 3);
+      if (!(lane & 1) && (lane >> 1) < DTK) T[(lane >> 1) * 3 + qn] = s;
+    }
+  }
+};
+
+// stage 2: entry (l, k) = sum_m [dv_l[m] T_v + v_l[m][0] T_f0 + v_l[m][1] T_f1](half row of m)
+template <int TL>
+__device__ __forceinline__ double d_stage2(const Dual& dl, const double* __restrict__ T, int lr, int kc) {
+  const double dv[4] = {1.0 / dl.Lm, 1.0 / dl.Lm, -1.0 / dl.Lp, -1.0 / dl.Lp};
+  const double v0[4] = {0.0, dl.vm, 1.0, dl.vp}, v1[4] = {dl.vm, 1.0, dl.vp, 0.0};
+  double acc = 0.0;
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    const double* Tm = T + ((2 * lr + m) * DTK + kc) * 3;
+    acc += dv[m] * Tm[0] + v0[m] * Tm[1] + v1[m] * Tm[2];
+  }
+  return acc;
 }
 
-template <int Q, int R>
-__global__ void __launch_bounds__(256) k_bulk_D(BlockArgs B, const Seg* __restrict__ half,
-                                                const Dual* __restrict__ dual,
-                                                const double* __restrict__ t, double alpha,
-                                                int nband) {
-  __shared__ double sm[R][DWARPS][32][5];
+template <int Q, int R, int TL>
+__global__ void __launch_bounds__(32 * (2 * TL + 2)) k_bulk_D(BlockArgs B, const Seg* __restrict__ half,
+                                                            const Dual* __restrict__ dual,
+                                                            const double* __restrict__ t, double alpha,
+                                                            int nband) {
+  constexpr int QQ = Q * Q;
+  constexpr int NW = 2 * TL + 2;
+  __shared__ double sT[R][NW * DTK * 3];
   const int ng = B.ng, nh = 2 * ng;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int K0 = blockIdx.x * DTK, L0 = blockIdx.y * DTL;
+  const int K0 = blockIdx.x * DTK, L0 = blockIdx.y * TL;
   const int p = ((2 * L0 - 1 + w) % nh + nh) % nh;
   const int q = ((2 * K0 - 1 + lane) % nh + nh) % nh;
   const int band = blockIdx.z;
@@ -344,8 +402,10 @@ __global__ void __launch_bounds__(256) k_bulk_D(BlockArgs B, const Seg* __restri
   if (bmax < B.b0) return;
   const Seg X = half[p], Y = half[q];
   const bool reg = (p == q);
-  const bool do_f = (X.nx * Y.nx + X.ny * Y.ny) != 0.0;
-  double c[Q * Q], L[Q * Q], ic[Q * Q];
+  DLane DL;
+  DL.init(dual, X, Y, K0, ng, lane);
+  const bool do_f = DL.nn != 0.0;
+  double c[QQ], L[QQ];
 #pragma unroll
   for (int u = 0; u < Q; ++u) {
     double px = fma(c_gx[Q][u], X.bx - X.ax, X.ax), py = fma(c_gx[Q][u], X.by - X.ay, X.ay);
@@ -356,7 +416,6 @@ __global__ void __launch_bounds__(256) k_bulk_D(BlockArgs B, const Seg* __restri
       double cc = 0.25 * alpha * (dx * dx + dy * dy);
       c[u * Q + v] = cc;
       L[u * Q + v] = cc > 0.0 ? log(cc) : 0.0;
-      ic[u * Q + v] = cc > 0.0 ? 1.0 / cc : 0.0;
     }
   }
   const double sv = X.h * Y.h / (4.0 * STB_PI), sf = alpha * X.h * Y.h / (4.0 * STB_PI);
@@ -373,20 +432,37 @@ __global__ void __launch_bounds__(256) k_bulk_D(BlockArgs B, const Seg* __restri
       if (x <= r_hi && x > y) {
         const double s = t[x] - ty;
         const double lns = log(s), is = 1.0 / s;
+        const double g0 = STB_GAMMA - lns;
+        double hv[QQ], ev[QQ];
+        bool large = false;
+#pragma unroll
+        for (int pp = 0; pp < QQ; ++pp) {
+          const double xx = c[pp] * is;
+          const double gl = reg ? g0 : g0 + L[pp];
+          ev[pp] = ein_poly(xx) - gl;
+          hv[pp] = fma(-(1.0 + xx), gl, gh_poly(xx));
+          large |= xx >= STB_XSPLIT;
+        }
+        if (large) {
+#pragma unroll
+          for (int pp = 0; pp < QQ; ++pp) {
+            const double xx = c[pp] * is;
+            if (xx >= STB_XSPLIT) {
+              const double tt = 1.0 / xx, e = exp(-xx);
+              ev[pp] = e1_large(tt, e) + (reg ? L[pp] : 0.0);
+              hv[pp] = fma(1.0 + xx, ev[pp], -e);
+            }
+          }
+        }
         double av = 0.0, a00 = 0.0, a01 = 0.0, a10 = 0.0, a11 = 0.0;
 #pragma unroll
         for (int u = 0; u < Q; ++u) {
           double tv = 0.0, tf0 = 0.0, tf1 = 0.0;
 #pragma unroll
           for (int v = 0; v < Q; ++v) {
-            const int pp = u * Q + v;
-            const double xx = c[pp] * is;
-            const double gl = STB_GAMMA + (reg ? 0.0 : L[pp]) - lns;
-            double hv, ev;
-            bulk_h_e1(xx, gl, s * ic[pp], reg ? L[pp] : 0.0, hv, ev);
             const double wv = c_gw[Q][v], fv = c_gx[Q][v];
-            tv = fma(wv, hv, tv);
-            const double we = wv * ev;
+            tv = fma(wv, hv[u * Q + v], tv);
+            const double we = wv * ev[u * Q + v];
             tf1 = fma(fv, we, tf1);
             tf0 += we;
           }
@@ -414,19 +490,16 @@ __global__ void __launch_bounds__(256) k_bulk_D(BlockArgs B, const Seg* __restri
       for (int r = 0; r < R; ++r) {
         DMom G{Phi[r + 1].v - Phi[r].v, Phi[r + 1].f00 - Phi[r].f00, Phi[r + 1].f01 - Phi[r].f01,
                Phi[r + 1].f10 - Phi[r].f10, Phi[r + 1].f11 - Phi[r].f11};
-        double* M = sm[r][w][lane];
-        M[0] = Gp[r].v - G.v;
-        M[1] = Gp[r].f00 - G.f00;
-        M[2] = Gp[r].f01 - G.f01;
-        M[3] = Gp[r].f10 - G.f10;
-        M[4] = Gp[r].f11 - G.f11;
+        DMom M{Gp[r].v - G.v, Gp[r].f00 - G.f00, Gp[r].f01 - G.f01, Gp[r].f10 - G.f10, Gp[r].f11 - G.f11};
+        DL.stage1(M, sT[r] + w * DTK * 3, lane);
         Gp[r] = G;
       }
       __syncthreads();
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const int a = r_lo + r;
-        if (a < r_hi && a - b >= 2) d_combine_store(B, dual, half, sm[r], L0, K0, a, b, false);
+      for (int e = threadIdx.x; e < R * TL * DTK; e += blockDim.x) {
+        const int r = e / (TL * DTK), lr = (e / DTK) % TL, kc = e % DTK;
+        const int a = r_lo + r, l = L0 + lr, k = K0 + kc;
+        if (a < r_hi && a - b >= 2 && l < ng && k < ng)
+          *entry_ptr(B, a, l, b, k) = d_stage2<TL>(dual[l], sT[r], lr, kc);
       }
       __syncthreads();
     } else {
@@ -498,14 +571,68 @@ __global__ void __launch_bounds__(128) k_near_VK(BlockArgs B, const Seg* __restr
   *entry_ptr(B, a, i, b, j) = val;
 }
 
-// D near cells: half-pair threads in the D tile, 5 moments each, smem combine
-__global__ void __launch_bounds__(256) k_near_D(BlockArgs B, const Seg* __restrict__ half,
-                                                const Dual* __restrict__ dual,
-                                                const double* __restrict__ t, double alpha) {
-  __shared__ double sm[DWARPS][32][5];
+// D near cells: half-pair threads in the D tile, the 5 moments in one pass over the points
+__device__ __forceinline__ void dev_h_e1(double x, double& h, double& e1) {
+  if (x < STB_XSPLIT) {
+    const double gl = STB_GAMMA + log(x);
+    e1 = ein_poly(x) - gl;
+    h = fma(-(1.0 + x), gl, gh_poly(x));
+  } else if (x > STB_XUNDER) {
+    e1 = 0.0;
+    h = 0.0;
+  } else {
+    const double tt = 1.0 / x, e = exp(-x);
+    e1 = e1_large(tt, e);
+    h = fma(1.0 + x, e1, -e);
+  }
+}
+
+__device__ DMom near_moments(const Seg& X, const Seg& Y, const Lags& Lg, double alpha, int q, bool do_f) {
+  double mv = 0.0, m00 = 0.0, m01 = 0.0, m10 = 0.0, m11 = 0.0;
+  for (int u = 0; u < q; ++u) {
+    const double fu = c_gx[q][u];
+    const double px = fma(fu, X.bx - X.ax, X.ax), py = fma(fu, X.by - X.ay, X.ay);
+    double tv = 0.0, tf0 = 0.0, tf1 = 0.0;
+    for (int v = 0; v < q; ++v) {
+      const double fv = c_gx[q][v];
+      const double qx = fma(fv, Y.bx - Y.ax, Y.ax), qy = fma(fv, Y.by - Y.ay, Y.ay);
+      const double dx = px - qx, dy = py - qy;
+      const double c = 0.25 * alpha * (dx * dx + dy * dy);
+      double kv = 0.0, kf = 0.0;
+      for (int m = 0; m < Lg.n; ++m) {
+        double h, e1;
+        dev_h_e1(c / Lg.s[m], h, e1);
+        kv = fma(Lg.e[m] * Lg.s[m], h, kv);
+        kf = fma(Lg.e[m], e1, kf);
+      }
+      const double wv = c_gw[q][v];
+      tv = fma(wv, kv, tv);
+      const double we = wv * kf;
+      tf1 = fma(fv, we, tf1);
+      tf0 += we;
+    }
+    tf0 -= tf1;
+    const double wu = c_gw[q][u];
+    mv = fma(wu, tv, mv);
+    const double w1 = wu * fu, w0 = wu - w1;
+    m00 = fma(w0, tf0, m00);
+    m01 = fma(w0, tf1, m01);
+    m10 = fma(w1, tf0, m10);
+    m11 = fma(w1, tf1, m11);
+  }
+  const double sv = X.h * Y.h / (4.0 * STB_PI), sf = do_f ? alpha * X.h * Y.h / (4.0 * STB_PI) : 0.0;
+  return DMom{sv * mv, sf * m00, sf * m01, sf * m10, sf * m11};
+}
+
+template <int TL>
+__global__ void __launch_bounds__(32 * (2 * TL + 2)) k_near_D(BlockArgs B, const Seg* __restrict__ half,
+                                                            const Dual* __restrict__ dual,
+                                                            const double* __restrict__ t, double alpha) {
+  constexpr int NW = 2 * TL + 2;
+  __shared__ double sT[NW * DTK * 3];
   const int ng = B.ng, nh = 2 * ng;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int K0 = blockIdx.x * DTK, L0 = blockIdx.y * DTL;
+  const int K0 = blockIdx.x * DTK, L0 = blockIdx.y * TL;
   const int cell = blockIdx.z;
   const int a = B.a0 + cell / 2, b = a - (cell % 2);
   if (a >= B.a1 || b < B.b0 || b >= B.b1) return;
@@ -513,20 +640,16 @@ __global__ void __launch_bounds__(256) k_near_D(BlockArgs B, const Seg* __restri
   const int q = ((2 * K0 - 1 + lane) % nh + nh) % nh;
   const Seg X = half[p], Y = half[q];
   const Lags Lg = make_lags(t, a, b);
-  double* M = sm[w][lane];
-  M[0] = M[1] = M[2] = M[3] = M[4] = 0.0;
-  if (chain_rel(p, q, nh) == 0) {
-    const int qo = near_order(X, Y);
-    M[0] = pair_regular<0>(X, Y, Lg, alpha, qo, 1, 1, 1, 1);
-    if ((X.nx * Y.nx + X.ny * Y.ny) != 0.0) {
-      M[1] = pair_regular<1>(X, Y, Lg, alpha, qo, 1, 0, 1, 0);
-      M[2] = pair_regular<1>(X, Y, Lg, alpha, qo, 1, 0, 0, 1);
-      M[3] = pair_regular<1>(X, Y, Lg, alpha, qo, 0, 1, 1, 0);
-      M[4] = pair_regular<1>(X, Y, Lg, alpha, qo, 0, 1, 0, 1);
-    }
-  }
+  DLane DL;
+  DL.init(dual, X, Y, K0, ng, lane);
+  DMom M{0, 0, 0, 0, 0};
+  if (chain_rel(p, q, nh) == 0) M = near_moments(X, Y, Lg, alpha, near_order(X, Y), DL.nn != 0.0);
+  DL.stage1(M, sT + w * DTK * 3, lane);
   __syncthreads();
-  d_combine_store(B, dual, half, sm, L0, K0, a, b, false);
+  for (int e = threadIdx.x; e < TL * DTK; e += blockDim.x) {
+    const int lr = e / DTK, kc = e % DTK, l = L0 + lr, k = K0 + kc;
+    if (l < ng && k < ng) *entry_ptr(B, a, l, b, k) = d_stage2<TL>(dual[l], sT, lr, kc);
+  }
 }
 
 // ================================================================= singular (touching) pairs
@@ -683,10 +806,51 @@ static void launch_bulk_q(int kind, const BlockArgs& BA, const bem_mesh* m, cuda
     dim3 grid((ng + 30) / 31, (ng + 3) / 4, nband);
     k_bulk_K<Q, R><<<grid, 128, 0, st>>>(BA, m->d_seg, m->d_t, m->alpha, nband);
   } else {
-    dim3 grid((ng + DTK - 1) / DTK, (ng + DTL - 1) / DTL, nband);
-    k_bulk_D<Q, 2><<<grid, 32 * DWARPS, 0, st>>>(BA, m->d_half, m->d_dual, m->d_t, m->alpha, nband);
+    constexpr int TL = DTL_BULK;
+    dim3 grid((ng + DTK - 1) / DTK, (ng + TL - 1) / TL, nband);
+    k_bulk_D<Q, 2, TL><<<grid, 32 * (2 * TL + 2), 0, st>>>(BA, m->d_half, m->d_dual, m->d_t, m->alpha, nband);
   }
   count_launch();
+}
+
+// exact evaluation counts of the shipped quadrature (host side, same rules as the kernels)
+static long long bulk_nodes(const Block& b, int R) {
+  long long nodes = 0;
+  const int nband = (b.a1 - b.a0 + R - 1) / R;
+  for (int band = 0; band < nband; ++band) {
+    const int r_hi = b.a1 - R * band, r_lo = std::max(b.a0, r_hi - R);
+    const int bmax = std::min(b.b1 - 1, r_hi - 1 - 2);
+    if (bmax < b.b0) continue;
+    for (int y = b.b0; y <= bmax + 1; ++y)
+      for (int x = r_lo; x <= r_hi; ++x)
+        if (x > y) ++nodes;
+  }
+  return nodes;
+}
+static long long near_point_pairs(int kind, const bem_mesh* m) {
+  // sum over (half-)segment pairs of q^2 x (kernel passes), touching pairs excluded
+  long long acc = 0;
+  const int ng = m->ng;
+  if (kind == STB_D) {
+    const int nh = 2 * ng;
+    for (int p = 0; p < nh; ++p)
+      for (int q = 0; q < nh; ++q) {
+        if (chain_rel(p, q, nh)) continue;
+        const Seg &X = m->half[p], &Y = m->half[q];
+        const int qo = near_order(X, Y);
+        const bool nn = (X.nx * Y.nx + X.ny * Y.ny) != 0.0;
+        acc += (long long)qo * qo * (nn ? 5 : 1);
+      }
+  } else {
+    for (int i = 0; i < ng; ++i)
+      for (int j = 0; j < ng; ++j) {
+        if (chain_rel(i, j, ng)) continue;
+        if (kind == STB_K && collinear(m->seg[i], m->seg[j])) continue;
+        const int qo = near_order(m->seg[i], m->seg[j]);
+        acc += (long long)qo * qo;
+      }
+  }
+  return acc;
 }
 
 bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bulk, int q_sing,
@@ -697,6 +861,22 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bul
   if (e != cudaSuccess) return cuda_fail(e, "assemble/poff");
   e = cudaMemcpyAsync(d_poff, A->poff.data(), sizeof(long long) * A->poff.size(), cudaMemcpyHostToDevice, st);
   if (e != cudaSuccess) { cudaFree(d_poff); return cuda_fail(e, "assemble/poff copy"); }
+  // CUDA events on the launching stream around each kernel family, per block
+  std::vector<cudaEvent_t> ev;
+  auto mark = [&]() {
+    cudaEvent_t x;
+    cudaEventCreate(&x);
+    cudaEventRecord(x, st);
+    ev.push_back(x);
+  };
+  std::vector<int> fam;  // family of the interval ending at ev[k+1]: 0 bulk, 1 near, 2 sing
+  A->q_bulk = q_bulk;
+  A->q_sing = q_sing;
+  A->ev_bulk = A->ev_near = 0;
+  A->launches = 0;
+  const long long near_pp = near_point_pairs(kind, m);
+  const long long spatial = (kind == STB_D) ? 4LL * ng * ng : (long long)ng * ng;
+  mark();
   for (size_t bi = 0; bi < m->blocks.size(); ++bi) {
     const Block& blk = m->blocks[bi];
     BlockArgs BA;
@@ -704,7 +884,6 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bul
     BA.poff = d_poff + A->poff_base[bi];
     BA.a0 = blk.a0; BA.a1 = blk.a1; BA.b0 = blk.b0; BA.b1 = blk.b1;
     BA.ng = ng;
-    // bulk: cells d >= 2 exist if a1 - 1 - (b0) >= 2
     const int R = (kind == STB_D) ? 2 : 4;
     const int nband = (blk.a1 - blk.a0 + R - 1) / R;
     if (blk.a1 - 1 - blk.b0 >= 2) {
@@ -715,20 +894,31 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bul
         case 6: launch_bulk_q<6>(kind, BA, m, st, nband); break;
         default: launch_bulk_q<8>(kind, BA, m, st, nband); break;
       }
+      mark();
+      fam.push_back(0);
+      A->launches++;
+      A->ev_bulk += bulk_nodes(blk, R) * spatial * q_bulk * q_bulk;
     }
-    // near cells (d <= 1) and touching pairs, only where such cells exist in this block
     const bool has_near = blk.b1 - 1 >= blk.a0 - 1 && blk.b0 <= blk.a1 - 1;
     if (has_near) {
       const int ncell = 2 * (blk.a1 - blk.a0);
+      long long lags = 0;
+      for (int a = blk.a0; a < blk.a1; ++a) {
+        if (a >= blk.b0 && a < blk.b1) lags += 1;                // d = 0: one lag
+        if (a - 1 >= blk.b0 && a - 1 < blk.b1) lags += 3;        // d = 1: three lags
+      }
+      A->ev_near += lags * near_pp;
       if (kind == STB_D) {
-        dim3 grid((ng + DTK - 1) / DTK, (ng + DTL - 1) / DTL, ncell);
-        k_near_D<<<grid, 32 * DWARPS, 0, st>>>(BA, m->d_half, m->d_dual, m->d_t, m->alpha);
+        dim3 grid((ng + DTK - 1) / DTK, (ng + DTL_NEAR - 1) / DTL_NEAR, ncell);
+        k_near_D<DTL_NEAR><<<grid, 32 * (2 * DTL_NEAR + 2), 0, st>>>(BA, m->d_half, m->d_dual, m->d_t, m->alpha);
       } else {
         dim3 grid((ng + 31) / 32, (ng + 3) / 4, ncell);
         if (kind == STB_V) k_near_VK<STB_V><<<grid, 128, 0, st>>>(BA, m->d_seg, m->d_t, m->alpha);
         else k_near_VK<STB_K><<<grid, 128, 0, st>>>(BA, m->d_seg, m->d_t, m->alpha);
       }
       count_launch();
+      mark();
+      fam.push_back(1);
       const int per_row = kind == STB_V ? 3 : (kind == STB_K ? 4 : 5);
       const long long nwarps = (long long)ncell * ng * per_row;
       const unsigned nblk = (unsigned)((nwarps + 3) / 4);
@@ -736,10 +926,20 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bul
       else if (kind == STB_K) k_sing<STB_K><<<nblk, 128, 0, st>>>(BA, m->d_seg, m->d_half, m->d_dual, m->d_t, m->alpha, q_sing, nwarps);
       else k_sing<STB_D><<<nblk, 128, 0, st>>>(BA, m->d_seg, m->d_half, m->d_dual, m->d_t, m->alpha, q_sing, nwarps);
       count_launch();
+      mark();
+      fam.push_back(2);
+      A->launches += 2;
     }
   }
   e = cudaGetLastError();
   cudaStreamSynchronize(st);
+  A->ms_bulk = A->ms_near = A->ms_sing = 0.0;
+  for (size_t k = 0; k + 1 < ev.size(); ++k) {
+    float ms = 0.0f;
+    cudaEventElapsedTime(&ms, ev[k], ev[k + 1]);
+    (fam[k] == 0 ? A->ms_bulk : fam[k] == 1 ? A->ms_near : A->ms_sing) += ms;
+  }
+  for (auto x : ev) cudaEventDestroy(x);
   cudaFree(d_poff);
   if (e != cudaSuccess) return cuda_fail(e, "assemble/launch");
   e = cudaGetLastError();

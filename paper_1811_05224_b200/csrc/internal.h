@@ -64,7 +64,8 @@ struct bem_mesh_s {
   std::vector<stb::Block> blocks; // blocks owned by this rank
   long long entries_owned = 0;
   double hmax = 0, htmin = 0, kappa = 0;
-  int q_bulk = 4;
+  int q_bulk = 4;     // V_h, K_h (primal segments)
+  int q_bulk_d = 4;   // D_h (half segments)
   bem_comm* comm = nullptr;
   int rank = 0, nranks = 1;
   // device copies
@@ -114,6 +115,10 @@ struct bem_matrix_s {
   double* d_di = nullptr;
   double* d_up = nullptr;
   double* d_work = nullptr;  // tridiagonal solve scratch (3 n)
+  // assembly statistics
+  double ms_bulk = 0, ms_near = 0, ms_sing = 0;
+  long long ev_bulk = 0, ev_near = 0;
+  int q_bulk = 0, q_sing = 0, launches = 0;
 };
 
 namespace stb {

@@ -310,6 +310,10 @@ bem_status bem_mesh_create(const bem_mesh_desc* d, bem_comm* comm, bem_mesh** ou
   m->kappa = m->alpha * m->hmax * m->hmax / (4.0 * m->htmin);
   // Gauss order for the bulk (d >= 2) from the measured error table
   m->q_bulk = m->kappa <= 0.065 ? 4 : (m->kappa <= 0.3 ? 5 : (m->kappa <= 1.0 ? 6 : 8));
+  {  // half segments: kappa / 4
+    const double kh = 0.25 * m->kappa;
+    m->q_bulk_d = kh <= 0.005 ? 3 : (kh <= 0.07 ? 4 : (kh <= 0.3 ? 5 : (kh <= 1.0 ? 6 : 8)));
+  }
 
   // slices and plan
   m->slice_first.resize(P + 1);

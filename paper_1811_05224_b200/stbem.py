@@ -50,7 +50,18 @@ class SolveReport(ctypes.Structure):
     _fields_ = [("iterations", ctypes.c_int), ("converged", ctypes.c_int),
                 ("rel_residual", ctypes.c_double), ("true_rel_residual", ctypes.c_double),
                 ("seconds_total", ctypes.c_double), ("seconds_matvec", ctypes.c_double),
-                ("seconds_comm", ctypes.c_double)]
+                ("seconds_comm", ctypes.c_double), ("n_matvec_V", ctypes.c_int),
+                ("n_matvec_D", ctypes.c_int)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class AssemblyStats(ctypes.Structure):
+    _fields_ = [("ms_bulk", ctypes.c_double), ("ms_near", ctypes.c_double), ("ms_sing", ctypes.c_double),
+                ("evals_bulk", ctypes.c_longlong), ("evals_near", ctypes.c_longlong),
+                ("q_bulk", ctypes.c_int), ("q_sing", ctypes.c_int), ("launches", ctypes.c_int),
+                ("entries", ctypes.c_longlong)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -83,10 +94,11 @@ _SIGS = {
     "bem_matvec": (I, [P, D, P, D, P, P]),
     "bem_mass_solve": (I, [P, I, P, P, P]),
     "bem_rhs": (I, [P, P, P, P, P]),
-    "bem_solve_gmres": (I, [P, P, P, P, P, ctypes.POINTER(GmresOpts), ctypes.POINTER(SolveReport), P]),
+    "bem_solve_gmres": (I, [P, P, P, P, P, ctypes.POINTER(GmresOpts), ctypes.POINTER(SolveReport), P, P]),
     "bem_matrix_get": (I, [P, LL, LL, LL, LL, P]),
     "bem_matrix_get_entries": (I, [P, LL, P, P, P]),
     "bem_matrix_info": (I, [P, P, P, P]),
+    "bem_matrix_stats": (I, [P, ctypes.POINTER(AssemblyStats)]),
     "bem_matrix_destroy": (None, [P]),
     "bem_eval_special": (I, [I, LL, P, P, P]),
 }
@@ -256,6 +268,11 @@ class Matrix:
         check(lib().bem_matrix_info(self.h, ctypes.byref(k), ctypes.byref(e), ctypes.byref(b)))
         return {"kind": k.value, "entries": e.value, "bytes": b.value}
 
+    def stats(self):
+        st = AssemblyStats()
+        check(lib().bem_matrix_stats(self.h, ctypes.byref(st)))
+        return st.as_dict()
+
     def matvec(self, x, y, a=1.0, b=0.0, stream=None):
         check(lib().bem_matvec(self.h, float(a), _ptr(x), float(b), _ptr(y), _stream(stream)))
         return y
@@ -286,13 +303,13 @@ def rhs(K, Mp, g, b, stream=None):
     return b
 
 
-def solve_gmres(V, b, w, D=None, M=None, rel_tol=1e-10, max_iter=500, precond=0, history=True):
+def solve_gmres(V, b, w, D=None, M=None, rel_tol=1e-10, max_iter=500, precond=0, history=True, stream=None):
     o = GmresOpts(float(rel_tol), int(max_iter), int(precond))
     rep = SolveReport()
     hist = np.zeros(max_iter + 1) if history else None
     st = lib().bem_solve_gmres(V.h, D.h if D else None, M.h if M else None, _ptr(b), _ptr(w),
                                ctypes.byref(o), ctypes.byref(rep),
-                               hist.ctypes.data if history else None)
+                               hist.ctypes.data if history else None, _stream(stream))
     if st not in (BEM_OK, BEM_E_NOT_CONVERGED, BEM_E_BREAKDOWN):
         check(st)
     r = rep.as_dict()
