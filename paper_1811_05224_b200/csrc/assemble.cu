@@ -112,6 +112,22 @@ __host__ __device__ inline bool collinear(const Seg& X, const Seg& Y) {
   return fabs(d0) < tol && fabs(d1) < tol;
 }
 
+// large-x forms, out of line: rare, and keeping them out of the unrolled point loops keeps the
+// kernels inside the instruction cache
+__device__ __noinline__ double large_h(double x, double lreg) {
+  const double tt = 1.0 / x, e = exp(-x);
+  return fma(1.0 + x, e1_large(tt, e) + lreg, -e);
+}
+__device__ __noinline__ double large_psi(double x) {
+  const double tt = 1.0 / x, e = exp(-x);
+  return e * tt - tt - e1_large(tt, e);
+}
+__device__ __noinline__ double2 large_h_e1(double x, double lreg) {
+  const double tt = 1.0 / x, e = exp(-x);
+  const double e1 = e1_large(tt, e) + lreg;
+  return make_double2(fma(1.0 + x, e1, -e), e1);
+}
+
 // ================================================================= bulk V
 // thread = segment pair (i, j): warp = row i, lane = column j; band of R test steps.
 // Every point pair is first evaluated with the small-x form (branch-free, unrolled: the Q*Q
@@ -148,16 +164,16 @@ __global__ void __launch_bounds__(128) k_bulk_V(BlockArgs B, const Seg* __restri
     }
   }
   const double scale = X.h * Y.h / (4.0 * STB_PI);
-  double Gp[R];
+  double Gp[R];  // G_a(y-1) = Phi(a+1, y-1) - Phi(a, y-1) for the band rows
 #pragma unroll
   for (int r = 0; r < R; ++r) Gp[r] = 0.0;
   for (int y = B.b0; y <= bmax + 1; ++y) {
     const double ty = t[y];
-    double Phi[R + 1];
-#pragma unroll
+    double phi_prev = 0.0;
+#pragma unroll 1
     for (int r = 0; r <= R; ++r) {
       const int x = r_lo + r;
-      Phi[r] = 0.0;
+      double phi = 0.0;
       if (x <= r_hi && x > y) {
         const double s = t[x] - ty;
         const double lns = log(s), is = 1.0 / s;
@@ -174,10 +190,7 @@ __global__ void __launch_bounds__(128) k_bulk_V(BlockArgs B, const Seg* __restri
 #pragma unroll
           for (int p = 0; p < QQ; ++p) {
             const double xx = c[p] * is;
-            if (xx >= STB_XSPLIT) {
-              const double tt = 1.0 / xx, e = exp(-xx);
-              hv[p] = fma(1.0 + xx, e1_large(tt, e) + (reg ? L[p] : 0.0), -e);
-            }
+            if (xx >= STB_XSPLIT) hv[p] = large_h(xx, reg ? L[p] : 0.0);
           }
         }
         double acc = 0.0;
@@ -188,21 +201,15 @@ __global__ void __launch_bounds__(128) k_bulk_V(BlockArgs B, const Seg* __restri
           for (int v = 0; v < Q; ++v) part = fma(c_gw[Q][v], hv[u * Q + v], part);
           acc = fma(c_gw[Q][u], part, acc);
         }
-        Phi[r] = s * acc;
+        phi = s * acc;
       }
-    }
-    if (y > B.b0) {
-      const int b = y - 1;
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const int a = r_lo + r;
-        const double G = Phi[r + 1] - Phi[r];
-        if (a < r_hi && a - b >= 2) *entry_ptr(B, a, i, b, j) = scale * (Gp[r] - G);
-        Gp[r] = G;
+      if (r > 0) {
+        const int a = x - 1, b = y - 1;
+        const double G = phi - phi_prev;
+        if (y > B.b0 && a < r_hi && a - b >= 2) *entry_ptr(B, a, i, b, j) = scale * (Gp[r - 1] - G);
+        Gp[r - 1] = G;
       }
-    } else {
-#pragma unroll
-      for (int r = 0; r < R; ++r) Gp[r] = Phi[r + 1] - Phi[r];
+      phi_prev = phi;
     }
   }
 }
@@ -252,11 +259,11 @@ __global__ void __launch_bounds__(128) k_bulk_K(BlockArgs B, const Seg* __restri
   for (int r = 0; r < R; ++r) Gp0[r] = Gp1[r] = 0.0;
   for (int y = B.b0; y <= bmax + 1; ++y) {
     const double ty = t[y];
-    double P0[R + 1], P1[R + 1];
-#pragma unroll
+    double p0_prev = 0.0, p1_prev = 0.0;
+#pragma unroll 1
     for (int r = 0; r <= R; ++r) {
       const int x = r_lo + r;
-      P0[r] = P1[r] = 0.0;
+      double P0 = 0.0, P1 = 0.0;
       if (x <= r_hi && x > y && !zero) {
         const double s = t[x] - ty;
         const double lns = log(s), is = 1.0 / s;
@@ -273,10 +280,7 @@ __global__ void __launch_bounds__(128) k_bulk_K(BlockArgs B, const Seg* __restri
 #pragma unroll
           for (int p = 0; p < QQ; ++p) {
             const double xx = c[p] * is;
-            if (xx >= STB_XSPLIT) {
-              const double tt = 1.0 / xx, e = exp(-xx);
-              ps[p] = e * tt - tt - e1_large(tt, e);
-            }
+            if (xx >= STB_XSPLIT) ps[p] = large_psi(xx);
           }
         }
         double a0 = 0.0, a1 = 0.0;
@@ -286,30 +290,22 @@ __global__ void __launch_bounds__(128) k_bulk_K(BlockArgs B, const Seg* __restri
           a1 = fma(c_gx[Q][p % Q], v, a1);
           a0 += v;
         }
-        P0[r] = a0 - a1;   // lambda_0 = 1 - f
-        P1[r] = a1;
+        P0 = a0 - a1;   // lambda_0 = 1 - f
+        P1 = a1;
       }
-    }
-    if (y > B.b0) {
-      const int b = y - 1;
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const int a = r_lo + r;
-        const double G0 = P0[r + 1] - P0[r], G1 = P1[r + 1] - P1[r];
-        if (a < r_hi && a - b >= 2) {
-          const double m0 = Gp0[r] - G0, m1 = Gp1[r] - G1;
+      if (r > 0) {
+        const int a = x - 1, b = y - 1;
+        const double G0 = P0 - p0_prev, G1 = P1 - p1_prev;
+        if (y > B.b0 && a < r_hi && a - b >= 2) {
+          const double m0 = Gp0[r - 1] - G0, m1 = Gp1[r - 1] - G1;
           const double left = __shfl_up_sync(0xffffffffu, m1, 1);
           if (out_ok) *entry_ptr(B, a, i, b, n) = scale * (left + m0);
         }
-        Gp0[r] = G0;
-        Gp1[r] = G1;
+        Gp0[r - 1] = G0;
+        Gp1[r - 1] = G1;
       }
-    } else {
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        Gp0[r] = P0[r + 1] - P0[r];
-        Gp1[r] = P1[r + 1] - P1[r];
-      }
+      p0_prev = P0;
+      p1_prev = P1;
     }
   }
 }
@@ -382,7 +378,7 @@ __device__ __forceinline__ double d_stage2(const Dual& dl, const double* __restr
 }
 
 template <int Q, int R, int TL>
-__global__ void __launch_bounds__(32 * (2 * TL + 2)) k_bulk_D(BlockArgs B, const Seg* __restrict__ half,
+__global__ void __launch_bounds__(32 * (2 * TL + 2), (Q <= 3 ? 2 : 1)) k_bulk_D(BlockArgs B, const Seg* __restrict__ half,
                                                             const Dual* __restrict__ dual,
                                                             const double* __restrict__ t, double alpha,
                                                             int nband) {
@@ -405,6 +401,7 @@ __global__ void __launch_bounds__(32 * (2 * TL + 2)) k_bulk_D(BlockArgs B, const
   DLane DL;
   DL.init(dual, X, Y, K0, ng, lane);
   const bool do_f = DL.nn != 0.0;
+  const bool any_f = __any_sync(0xffffffffu, do_f);
   double c[QQ], L[QQ];
 #pragma unroll
   for (int u = 0; u < Q; ++u) {
@@ -424,33 +421,43 @@ __global__ void __launch_bounds__(32 * (2 * TL + 2)) k_bulk_D(BlockArgs B, const
   for (int r = 0; r < R; ++r) Gp[r] = DMom{0, 0, 0, 0, 0};
   for (int y = B.b0; y <= bmax + 1; ++y) {
     const double ty = t[y];
-    DMom Phi[R + 1];
-#pragma unroll
+    DMom prev{0, 0, 0, 0, 0};
+#pragma unroll 1
     for (int r = 0; r <= R; ++r) {
       const int x = r_lo + r;
-      Phi[r] = DMom{0, 0, 0, 0, 0};
+      DMom phi{0, 0, 0, 0, 0};
       if (x <= r_hi && x > y) {
         const double s = t[x] - ty;
         const double lns = log(s), is = 1.0 / s;
         const double g0 = STB_GAMMA - lns;
         double hv[QQ], ev[QQ];
         bool large = false;
+        if (any_f) {  // warp-uniform: some lane of the warp needs the normal term (n_p . n_q != 0)
 #pragma unroll
-        for (int pp = 0; pp < QQ; ++pp) {
-          const double xx = c[pp] * is;
-          const double gl = reg ? g0 : g0 + L[pp];
-          ev[pp] = ein_poly(xx) - gl;
-          hv[pp] = fma(-(1.0 + xx), gl, gh_poly(xx));
-          large |= xx >= STB_XSPLIT;
+          for (int pp = 0; pp < QQ; ++pp) {
+            const double xx = c[pp] * is;
+            const double gl = reg ? g0 : g0 + L[pp];
+            ev[pp] = ein_poly(xx) - gl;
+            hv[pp] = fma(-(1.0 + xx), gl, gh_poly(xx));
+            large |= xx >= STB_XSPLIT;
+          }
+        } else {      // perpendicular half segments: only the curl kernel
+#pragma unroll
+          for (int pp = 0; pp < QQ; ++pp) {
+            const double xx = c[pp] * is;
+            ev[pp] = 0.0;
+            hv[pp] = fma(-(1.0 + xx), reg ? g0 : g0 + L[pp], gh_poly(xx));
+            large |= xx >= STB_XSPLIT;
+          }
         }
         if (large) {
 #pragma unroll
           for (int pp = 0; pp < QQ; ++pp) {
             const double xx = c[pp] * is;
             if (xx >= STB_XSPLIT) {
-              const double tt = 1.0 / xx, e = exp(-xx);
-              ev[pp] = e1_large(tt, e) + (reg ? L[pp] : 0.0);
-              hv[pp] = fma(1.0 + xx, ev[pp], -e);
+              const double2 he = large_h_e1(xx, reg ? L[pp] : 0.0);
+              hv[pp] = he.x;
+              ev[pp] = he.y;
             }
           }
         }
@@ -475,25 +482,25 @@ __global__ void __launch_bounds__(32 * (2 * TL + 2)) k_bulk_D(BlockArgs B, const
           a10 = fma(w1, tf0, a10);
           a11 = fma(w1, tf1, a11);
         }
-        Phi[r].v = sv * s * av;
+        phi.v = sv * s * av;
         if (do_f) {
-          Phi[r].f00 = sf * a00;
-          Phi[r].f01 = sf * a01;
-          Phi[r].f10 = sf * a10;
-          Phi[r].f11 = sf * a11;
+          phi.f00 = sf * a00;
+          phi.f01 = sf * a01;
+          phi.f10 = sf * a10;
+          phi.f11 = sf * a11;
         }
       }
+      if (r > 0) {
+        const DMom G{phi.v - prev.v, phi.f00 - prev.f00, phi.f01 - prev.f01, phi.f10 - prev.f10, phi.f11 - prev.f11};
+        const DMom& g = Gp[r - 1];
+        const DMom M{g.v - G.v, g.f00 - G.f00, g.f01 - G.f01, g.f10 - G.f10, g.f11 - G.f11};
+        if (y > B.b0) DL.stage1(M, sT[r - 1] + w * DTK * 3, lane);
+        Gp[r - 1] = G;
+      }
+      prev = phi;
     }
     if (y > B.b0) {
       const int b = y - 1;
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        DMom G{Phi[r + 1].v - Phi[r].v, Phi[r + 1].f00 - Phi[r].f00, Phi[r + 1].f01 - Phi[r].f01,
-               Phi[r + 1].f10 - Phi[r].f10, Phi[r + 1].f11 - Phi[r].f11};
-        DMom M{Gp[r].v - G.v, Gp[r].f00 - G.f00, Gp[r].f01 - G.f01, Gp[r].f10 - G.f10, Gp[r].f11 - G.f11};
-        DL.stage1(M, sT[r] + w * DTK * 3, lane);
-        Gp[r] = G;
-      }
       __syncthreads();
       for (int e = threadIdx.x; e < R * TL * DTK; e += blockDim.x) {
         const int r = e / (TL * DTK), lr = (e / DTK) % TL, kc = e % DTK;
@@ -502,11 +509,6 @@ __global__ void __launch_bounds__(32 * (2 * TL + 2)) k_bulk_D(BlockArgs B, const
           *entry_ptr(B, a, l, b, k) = d_stage2<TL>(dual[l], sT[r], lr, kc);
       }
       __syncthreads();
-    } else {
-#pragma unroll
-      for (int r = 0; r < R; ++r)
-        Gp[r] = DMom{Phi[r + 1].v - Phi[r].v, Phi[r + 1].f00 - Phi[r].f00, Phi[r + 1].f01 - Phi[r].f01,
-                     Phi[r + 1].f10 - Phi[r].f10, Phi[r + 1].f11 - Phi[r].f11};
     }
   }
 }
@@ -798,7 +800,7 @@ template <int Q>
 static void launch_bulk_q(int kind, const BlockArgs& BA, const bem_mesh* m, cudaStream_t st,
                           int nband) {
   const int ng = m->ng;
-  constexpr int R = 4;
+  constexpr int R = 8;
   if (kind == STB_V) {
     dim3 grid((ng + 31) / 32, (ng + 3) / 4, nband);
     k_bulk_V<Q, R><<<grid, 128, 0, st>>>(BA, m->d_seg, m->d_t, m->alpha, nband);
@@ -808,7 +810,7 @@ static void launch_bulk_q(int kind, const BlockArgs& BA, const bem_mesh* m, cuda
   } else {
     constexpr int TL = DTL_BULK;
     dim3 grid((ng + DTK - 1) / DTK, (ng + TL - 1) / TL, nband);
-    k_bulk_D<Q, 2, TL><<<grid, 32 * (2 * TL + 2), 0, st>>>(BA, m->d_half, m->d_dual, m->d_t, m->alpha, nband);
+    k_bulk_D<Q, 4, TL><<<grid, 32 * (2 * TL + 2), 0, st>>>(BA, m->d_half, m->d_dual, m->d_t, m->alpha, nband);
   }
   count_launch();
 }
@@ -884,7 +886,7 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bul
     BA.poff = d_poff + A->poff_base[bi];
     BA.a0 = blk.a0; BA.a1 = blk.a1; BA.b0 = blk.b0; BA.b1 = blk.b1;
     BA.ng = ng;
-    const int R = (kind == STB_D) ? 2 : 4;
+    const int R = (kind == STB_D) ? 4 : 8;
     const int nband = (blk.a1 - blk.a0 + R - 1) / R;
     if (blk.a1 - 1 - blk.b0 >= 2) {
       switch (q_bulk) {
