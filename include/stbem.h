@@ -132,6 +132,10 @@ void bem_comm_destroy(bem_comm* comm);
 bem_status bem_plan_build(int P, int* owner_host);
 /* generator G_0: out_host[k] = k-th vertex of the difference cover (count in *n_out) */
 bem_status bem_plan_generator(int P, int* out_host, int* n_out);
+/* blocks (I,J) owned by `rank` of `nranks` GPUs when the P processes of the plan are mapped
+ * round-robin to GPUs (process p -> GPU p mod nranks, R15): writes 2*count ints
+ * (I, J pairs, row-major block order) to out_host (capacity P*(P+1) ints) and the count. */
+bem_status bem_plan_owned_blocks(int P, int nranks, int rank, int* out_host, int* count);
 /* balanced slice ranges (R14): slice p = time steps [first[p], first[p+1]) */
 bem_status bem_slice_ranges(int n_steps, int P, int* first_host /* P+1 */);
 

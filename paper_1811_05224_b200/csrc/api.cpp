@@ -32,7 +32,19 @@ bem_matrix* new_dense(const bem_mesh* m, int kind, bem_status* st) {
     }
   }
   A->entries = off;
-  cudaError_t e = cudaMalloc(&A->data, sizeof(double) * std::max<long long>(off, 4));
+  // stream-ordered allocation from the device pool, which keeps freed matrix storage for the
+  // next assembly (repeated solves do not pay cudaMalloc / cudaFree of tens of GB)
+  static bool pool_ready = false;
+  if (!pool_ready) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, m->device) == cudaSuccess) {
+      unsigned long long thr = ~0ULL;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    pool_ready = true;
+  }
+  cudaError_t e = cudaMallocAsync(&A->data, sizeof(double) * std::max<long long>(off, 4), (cudaStream_t)0);
+  if (e == cudaSuccess) e = cudaStreamSynchronize((cudaStream_t)0);
   if (e != cudaSuccess) {
     *st = BEM_E_NOMEM;
     set_error(std::string("matrix allocation of ") + std::to_string(8.0 * off / 1e9) + " GB failed: " + cudaGetErrorString(e));
@@ -415,7 +427,10 @@ bem_status bem_matrix_info(const bem_matrix* A, int* kind, long long* entries, l
 
 void bem_matrix_destroy(bem_matrix* A) {
   if (!A) return;
-  cudaFree(A->data);
+  if (A->data) {
+    cudaFreeAsync(A->data, (cudaStream_t)0);
+    cudaStreamSynchronize((cudaStream_t)0);
+  }
   cudaFree(A->d_segs);
   cudaFree(A->d_partials);
   cudaFree(A->d_row_pbase);

@@ -378,7 +378,7 @@ __device__ __forceinline__ double d_stage2(const Dual& dl, const double* __restr
 }
 
 template <int Q, int R, int TL>
-__global__ void __launch_bounds__(32 * (2 * TL + 2), (Q <= 3 ? 2 : 1)) k_bulk_D(BlockArgs B, const Seg* __restrict__ half,
+__global__ void __launch_bounds__(32 * (2 * TL + 2), (TL <= 3 && Q <= 3 ? 2 : 1)) k_bulk_D(BlockArgs B, const Seg* __restrict__ half,
                                                             const Dual* __restrict__ dual,
                                                             const double* __restrict__ t, double alpha,
                                                             int nband) {
@@ -808,9 +808,9 @@ static void launch_bulk_q(int kind, const BlockArgs& BA, const bem_mesh* m, cuda
     dim3 grid((ng + 30) / 31, (ng + 3) / 4, nband);
     k_bulk_K<Q, R><<<grid, 128, 0, st>>>(BA, m->d_seg, m->d_t, m->alpha, nband);
   } else {
-    constexpr int TL = DTL_BULK;
+    constexpr int TL = (Q <= 3) ? 7 : DTL_BULK;   // 16 warps at <= 128 registers for Q = 3
     dim3 grid((ng + DTK - 1) / DTK, (ng + TL - 1) / TL, nband);
-    k_bulk_D<Q, 4, TL><<<grid, 32 * (2 * TL + 2), 0, st>>>(BA, m->d_half, m->d_dual, m->d_t, m->alpha, nband);
+    k_bulk_D<Q, 8, TL><<<grid, 32 * (2 * TL + 2), 0, st>>>(BA, m->d_half, m->d_dual, m->d_t, m->alpha, nband);
   }
   count_launch();
 }
@@ -886,7 +886,7 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bul
     BA.poff = d_poff + A->poff_base[bi];
     BA.a0 = blk.a0; BA.a1 = blk.a1; BA.b0 = blk.b0; BA.b1 = blk.b1;
     BA.ng = ng;
-    const int R = (kind == STB_D) ? 4 : 8;
+    const int R = 8;
     const int nband = (blk.a1 - blk.a0 + R - 1) / R;
     if (blk.a1 - 1 - blk.b0 >= 2) {
       switch (q_bulk) {

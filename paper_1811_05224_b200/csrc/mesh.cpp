@@ -193,6 +193,24 @@ bem_status bem_plan_generator(int P, int* out_host, int* n_out) {
   return BEM_OK;
 }
 
+bem_status bem_plan_owned_blocks(int P, int nranks, int rank, int* out, int* count) {
+  if (P < 1 || nranks < 1 || rank < 0 || rank >= nranks || !out || !count) {
+    set_error("bem_plan_owned_blocks: invalid argument");
+    return BEM_E_INVALID;
+  }
+  auto o = cyclic_plan(P, nullptr);
+  int c = 0;
+  for (int I = 0; I < P; ++I)
+    for (int J = 0; J <= I; ++J)
+      if (o[I * P + J] % nranks == rank) {
+        out[2 * c] = I;
+        out[2 * c + 1] = J;
+        ++c;
+      }
+  *count = c;
+  return BEM_OK;
+}
+
 bem_status bem_slice_ranges(int n_steps, int P, int* first) {
   if (P < 1 || n_steps < 1 || !first) { set_error("bem_slice_ranges: invalid argument"); return BEM_E_INVALID; }
   if (P > n_steps) {

@@ -83,6 +83,7 @@ _SIGS = {
     "bem_comm_destroy": (None, [P]),
     "bem_plan_build": (I, [I, P]),
     "bem_plan_generator": (I, [I, P, P]),
+    "bem_plan_owned_blocks": (I, [I, I, I, P, P]),
     "bem_slice_ranges": (I, [I, I, P]),
     "bem_mesh_create": (I, [ctypes.POINTER(MeshDesc), P, PP]),
     "bem_mesh_info_get": (I, [P, ctypes.POINTER(MeshInfo)]),
@@ -155,6 +156,13 @@ def plan_generator(P):
     n = ctypes.c_int(0)
     check(lib().bem_plan_generator(P, out.ctypes.data, ctypes.addressof(n)))
     return out[: n.value].tolist()
+
+
+def plan_owned_blocks(P, nranks, rank):
+    out = np.zeros(P * (P + 1), dtype=np.int32)
+    n = ctypes.c_int(0)
+    check(lib().bem_plan_owned_blocks(P, nranks, rank, out.ctypes.data, ctypes.addressof(n)))
+    return [tuple(x) for x in out[: 2 * n.value].reshape(-1, 2).tolist()]
 
 
 def slice_ranges(n_steps, P):
