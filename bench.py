@@ -27,9 +27,6 @@ PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 # FP64 DFMA peak: 148 SMs x 64 FP64 FMA/clk x 2 flop x 1.965 GHz (B200_PROFILING.md unit counts,
 # MEASURED_PEAKS sm_max_mhz); tools/fp64_peak.cu measured 34.1 TFLOP/s on this pool (profiles/).
 FP64_PEAK_DERIVED = 148 * 64 * 2 * 1.965e9 / 1e12
-# static FP64 flops of one bulk D_h kernel evaluation (h and E1 at one point pair and one time
-# node, small-x branch: two degree-20/21 Horner chains + combination), DESIGN.md section 6
-FLOPS_PER_EVAL = {"V": 52, "K": 50, "D": 98}
 
 
 def parse():
@@ -246,7 +243,13 @@ def native(args):
         st = stats[k]
         fam.append((st["ms_bulk"], k, "bulk", st))
     ms_dom, kdom, _, st = max(fam)
-    flops = st["evals_bulk"] * FLOPS_PER_EVAL[kdom]
+    flops = st["flops_bulk"]
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "r01_traffic.json")
+    if os.path.exists(tpath):
+        tj = json.load(open(tpath)).get(f"k_bulk_{kdom}")
+        if tj and tj.get("config") == args.config:
+            traffic = tj["traffic_bytes_per_launch"]
     achieved = flops / (ms_dom * 1e-3) / 1e12
     asm_s = ph["assemble_V"] + ph["assemble_K"] + ph["assemble_D"]
     out = {
@@ -266,9 +269,11 @@ def native(args):
             "kernel_ms": {k: {"bulk": stats[k]["ms_bulk"], "near": stats[k]["ms_near"], "sing": stats[k]["ms_sing"]} for k in "VKD"},
         },
         "roofline": {"bound": "alu", "kernel": f"k_bulk_{kdom}", "achieved": achieved, "peak": FP64_PEAK_DERIVED,
-                     "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_DERIVED, "traffic": None,
+                     "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_DERIVED, "traffic": traffic,
+                     "traffic_note": "dram read+write bytes per launch from ncu --set full (profiles/r01_ncu_bulkD_C3.txt); the kernel is FP64-bound, traffic = the matrix stores",
                      "peak_note": "FP64 DFMA: 148 SM x 64 FMA/clk x 2 x 1.965 GHz (derived); measured 34.1 TFLOP/s",
-                     "flops_per_launch": flops, "evals_per_launch": st["evals_bulk"], "flops_per_eval": FLOPS_PER_EVAL[kdom]},
+                     "flops_per_launch": flops, "evals_per_launch": st["evals_bulk"],
+                     "flops_note": "algorithmic: evaluations x static FP64 flops of the small-x path (DFMA=2), DESIGN.md section 6"},
         "roofline_gemv": {"bound": "hbm", "achieved": gemv_gbs, "peak": hbm_peak, "unit": "GB/s",
                           "frac": (gemv_gbs / hbm_peak) if gemv_gbs else None, "bytes_per_launch": bytes_per_gemv},
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n},

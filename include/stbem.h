@@ -109,6 +109,7 @@ typedef struct {
   int q_bulk, q_sing;
   int launches;
   long long entries;         /* stored (unpadded) entries */
+  double flops_bulk;         /* algorithmic FP64 flops of the bulk kernels */
 } bem_assembly_stats;
 
 /* ---------------------------------------------------------------- general */

@@ -406,6 +406,7 @@ bem_status bem_matrix_stats(const bem_matrix* A, bem_assembly_stats* o) {
   int kind = 0;
   bem_matrix_info(A, &kind, &ent, nullptr);
   o->entries = ent;
+  o->flops_bulk = A->flops_bulk;
   return BEM_OK;
 }
 

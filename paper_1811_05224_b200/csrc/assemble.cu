@@ -53,6 +53,9 @@ struct BlockArgs {
   const long long* poff;  // panel offsets for this block (index a - a0)
   int a0, a1, b0, b1;
   int ng;                 // entries per panel row block (N_Gamma)
+  const double4* lag;     // (s, ln s, 1/s) per time-node pair
+  int ldlag;              // n_steps + 1
+  int qfar;               // near-cell Gauss order for well-separated pairs
 };
 
 __device__ __forceinline__ double* entry_ptr(const BlockArgs& B, int a, int i, int b, int j) {
@@ -93,9 +96,10 @@ __host__ __device__ inline double seg_dist(const Seg& X, const Seg& Y) {
   return fmin(fmin(pd(X.ax, X.ay, Y), pd(X.bx, X.by, Y)), fmin(pd(Y.ax, Y.ay, X), pd(Y.bx, Y.by, X)));
 }
 // Gauss order for non-touching pairs in cells d <= 1 (measured table)
-__host__ __device__ inline int near_order(const Seg& X, const Seg& Y) {
+// qfar: order for well-separated pairs (rho >= 9), min(6, q_bulk + 1) from the mesh's kappa
+__host__ __device__ inline int near_order(const Seg& X, const Seg& Y, int qfar) {
   double rho = seg_dist(X, Y) / fmax(X.h, Y.h);
-  return rho < 2.5 ? 10 : (rho < 5.0 ? 8 : 6);
+  return rho < 2.5 ? 10 : (rho < 5.0 ? 8 : (rho < 9.0 ? 6 : qfar));
 }
 // relation of elements p, q of a closed chain of n: 0 disjoint, 1 identical,
 // 2 X.end == Y.start, 3 X.start == Y.end
@@ -168,15 +172,14 @@ __global__ void __launch_bounds__(128) k_bulk_V(BlockArgs B, const Seg* __restri
 #pragma unroll
   for (int r = 0; r < R; ++r) Gp[r] = 0.0;
   for (int y = B.b0; y <= bmax + 1; ++y) {
-    const double ty = t[y];
     double phi_prev = 0.0;
 #pragma unroll 1
     for (int r = 0; r <= R; ++r) {
       const int x = r_lo + r;
       double phi = 0.0;
       if (x <= r_hi && x > y) {
-        const double s = t[x] - ty;
-        const double lns = log(s), is = 1.0 / s;
+        const double4 nd = B.lag[x * B.ldlag + y];
+        const double s = nd.x, lns = nd.y, is = nd.z;
         const double g0 = STB_GAMMA - lns;
         double hv[QQ];
         bool large = false;
@@ -258,15 +261,14 @@ __global__ void __launch_bounds__(128) k_bulk_K(BlockArgs B, const Seg* __restri
 #pragma unroll
   for (int r = 0; r < R; ++r) Gp0[r] = Gp1[r] = 0.0;
   for (int y = B.b0; y <= bmax + 1; ++y) {
-    const double ty = t[y];
     double p0_prev = 0.0, p1_prev = 0.0;
 #pragma unroll 1
     for (int r = 0; r <= R; ++r) {
       const int x = r_lo + r;
       double P0 = 0.0, P1 = 0.0;
       if (x <= r_hi && x > y && !zero) {
-        const double s = t[x] - ty;
-        const double lns = log(s), is = 1.0 / s;
+        const double4 nd = B.lag[x * B.ldlag + y];
+        const double s = nd.x, lns = nd.y, is = nd.z;
         const double g0 = STB_GAMMA - lns;
         double ps[QQ];
         bool large = false;
@@ -420,15 +422,14 @@ __global__ void __launch_bounds__(32 * (2 * TL + 2), (TL <= 3 && Q <= 3 ? 2 : 1)
 #pragma unroll
   for (int r = 0; r < R; ++r) Gp[r] = DMom{0, 0, 0, 0, 0};
   for (int y = B.b0; y <= bmax + 1; ++y) {
-    const double ty = t[y];
     DMom prev{0, 0, 0, 0, 0};
 #pragma unroll 1
     for (int r = 0; r <= R; ++r) {
       const int x = r_lo + r;
       DMom phi{0, 0, 0, 0, 0};
       if (x <= r_hi && x > y) {
-        const double s = t[x] - ty;
-        const double lns = log(s), is = 1.0 / s;
+        const double4 nd = B.lag[x * B.ldlag + y];
+        const double s = nd.x, lns = nd.y, is = nd.z;
         const double g0 = STB_GAMMA - lns;
         double hv[QQ], ev[QQ];
         bool large = false;
@@ -561,14 +562,14 @@ __global__ void __launch_bounds__(128) k_near_VK(BlockArgs B, const Seg* __restr
   double val = 0.0;
   if (KIND == STB_V) {
     const Seg Y = seg[j];
-    if (chain_rel(i, j, ng) == 0) val = pair_regular<0>(X, Y, Lg, alpha, near_order(X, Y), 1, 1, 1, 1);
+    if (chain_rel(i, j, ng) == 0) val = pair_regular<0>(X, Y, Lg, alpha, near_order(X, Y, B.qfar), 1, 1, 1, 1);
   } else {
     const int jl = (j - 1 + ng) % ng;
     const Seg Yl = seg[jl], Yr = seg[j];
     if (chain_rel(i, jl, ng) == 0 && !collinear(X, Yl))
-      val += pair_regular<2>(X, Yl, Lg, alpha, near_order(X, Yl), 1, 1, 0, 1);
+      val += pair_regular<2>(X, Yl, Lg, alpha, near_order(X, Yl, B.qfar), 1, 1, 0, 1);
     if (chain_rel(i, j, ng) == 0 && !collinear(X, Yr))
-      val += pair_regular<2>(X, Yr, Lg, alpha, near_order(X, Yr), 1, 1, 1, 0);
+      val += pair_regular<2>(X, Yr, Lg, alpha, near_order(X, Yr, B.qfar), 1, 1, 1, 0);
   }
   *entry_ptr(B, a, i, b, j) = val;
 }
@@ -645,7 +646,7 @@ __global__ void __launch_bounds__(32 * (2 * TL + 2)) k_near_D(BlockArgs B, const
   DLane DL;
   DL.init(dual, X, Y, K0, ng, lane);
   DMom M{0, 0, 0, 0, 0};
-  if (chain_rel(p, q, nh) == 0) M = near_moments(X, Y, Lg, alpha, near_order(X, Y), DL.nn != 0.0);
+  if (chain_rel(p, q, nh) == 0) M = near_moments(X, Y, Lg, alpha, near_order(X, Y, B.qfar), DL.nn != 0.0);
   DL.stage1(M, sT + w * DTK * 3, lane);
   __syncthreads();
   for (int e = threadIdx.x; e < TL * DTK; e += blockDim.x) {
@@ -829,7 +830,7 @@ static long long bulk_nodes(const Block& b, int R) {
   }
   return nodes;
 }
-static long long near_point_pairs(int kind, const bem_mesh* m) {
+static long long near_point_pairs(int kind, const bem_mesh* m, int qfar) {
   // sum over (half-)segment pairs of q^2 x (kernel passes), touching pairs excluded
   long long acc = 0;
   const int ng = m->ng;
@@ -839,16 +840,15 @@ static long long near_point_pairs(int kind, const bem_mesh* m) {
       for (int q = 0; q < nh; ++q) {
         if (chain_rel(p, q, nh)) continue;
         const Seg &X = m->half[p], &Y = m->half[q];
-        const int qo = near_order(X, Y);
-        const bool nn = (X.nx * Y.nx + X.ny * Y.ny) != 0.0;
-        acc += (long long)qo * qo * (nn ? 5 : 1);
+        const int qo = near_order(X, Y, qfar);
+        acc += (long long)qo * qo;
       }
   } else {
     for (int i = 0; i < ng; ++i)
       for (int j = 0; j < ng; ++j) {
         if (chain_rel(i, j, ng)) continue;
         if (kind == STB_K && collinear(m->seg[i], m->seg[j])) continue;
-        const int qo = near_order(m->seg[i], m->seg[j]);
+        const int qo = near_order(m->seg[i], m->seg[j], qfar);
         acc += (long long)qo * qo;
       }
   }
@@ -876,8 +876,27 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bul
   A->q_sing = q_sing;
   A->ev_bulk = A->ev_near = 0;
   A->launches = 0;
-  const long long near_pp = near_point_pairs(kind, m);
+  const int qfar = std::min(6, q_bulk + 1);
+  const long long near_pp = near_point_pairs(kind, m, qfar);
   const long long spatial = (kind == STB_D) ? 4LL * ng * ng : (long long)ng * ng;
+  // algorithmic FP64 flops per bulk kernel evaluation (static count of the small-x path,
+  // DFMA = 2): V 41, K 39 (collinear pairs skipped: K = 0 there),
+  // D 80 (curl + normal term) or 41 (perpendicular half segments: curl only)
+  double flops_per_node = 0.0;  // sum over spatial pairs of flops per point pair
+  if (kind == STB_V) {
+    flops_per_node = 41.0 * ng * ng;
+  } else if (kind == STB_K) {
+    for (int i = 0; i < ng; ++i)
+      for (int j = 0; j < ng; ++j)
+        if (!collinear(m->seg[i], m->seg[j])) flops_per_node += 39.0;
+  } else {
+    for (int p = 0; p < 2 * ng; ++p)
+      for (int q = 0; q < 2 * ng; ++q) {
+        const Seg &X = m->half[p], &Y = m->half[q];
+        flops_per_node += (X.nx * Y.nx + X.ny * Y.ny) != 0.0 ? 80.0 : 41.0;
+      }
+  }
+  A->flops_bulk = 0.0;
   mark();
   for (size_t bi = 0; bi < m->blocks.size(); ++bi) {
     const Block& blk = m->blocks[bi];
@@ -886,6 +905,9 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bul
     BA.poff = d_poff + A->poff_base[bi];
     BA.a0 = blk.a0; BA.a1 = blk.a1; BA.b0 = blk.b0; BA.b1 = blk.b1;
     BA.ng = ng;
+    BA.lag = m->d_lag;
+    BA.ldlag = m->nt + 1;
+    BA.qfar = qfar;
     const int R = 8;
     const int nband = (blk.a1 - blk.a0 + R - 1) / R;
     if (blk.a1 - 1 - blk.b0 >= 2) {
@@ -899,7 +921,9 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bul
       mark();
       fam.push_back(0);
       A->launches++;
-      A->ev_bulk += bulk_nodes(blk, R) * spatial * q_bulk * q_bulk;
+      const long long nodes = bulk_nodes(blk, R);
+      A->ev_bulk += nodes * spatial * q_bulk * q_bulk;
+      A->flops_bulk += (double)nodes * q_bulk * q_bulk * flops_per_node;
     }
     const bool has_near = blk.b1 - 1 >= blk.a0 - 1 && blk.b0 <= blk.a1 - 1;
     if (has_near) {

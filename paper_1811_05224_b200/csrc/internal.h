@@ -73,6 +73,7 @@ struct bem_mesh_s {
   stb::Seg* d_seg = nullptr;
   stb::Seg* d_half = nullptr;
   stb::Dual* d_dual = nullptr;
+  double4* d_lag = nullptr;       // (s, ln s, 1/s, 0) for time nodes x > y: index x*(nt+1)+y
   cudaStream_t stream = nullptr;  // internal stream (solver)
 };
 
@@ -118,6 +119,7 @@ struct bem_matrix_s {
   // assembly statistics
   double ms_bulk = 0, ms_near = 0, ms_sing = 0;
   long long ev_bulk = 0, ev_near = 0;
+  double flops_bulk = 0;
   int q_bulk = 0, q_sing = 0, launches = 0;
 };
 

@@ -363,6 +363,14 @@ bem_status bem_mesh_create(const bem_mesh_desc* d, bem_comm* comm, bem_mesh** ou
     if (e != cudaSuccess) { delete m; return cuda_fail(e, "bem_mesh_create/cudaSetDevice"); }
     m->device = comm->device;
   }
+  // time-node lag table: s = t_x - t_y, ln s, 1/s for every node pair x > y (shared by all
+  // spatial pairs; removes one log and one division per node and thread from the bulk kernels)
+  std::vector<double4> lagtab((size_t)(m->nt + 1) * (m->nt + 1));
+  for (int x = 0; x <= m->nt; ++x)
+    for (int y = 0; y <= m->nt; ++y) {
+      double sv = m->t[x] - m->t[y];
+      lagtab[(size_t)x * (m->nt + 1) + y] = x > y ? make_double4(sv, std::log(sv), 1.0 / sv, 0.0) : make_double4(0.0, 0.0, 0.0, 0.0);
+    }
   bem_status st = upload_rules();
   if (st != BEM_OK) { delete m; return st; }
   auto up = [&](void** dst, const void* src, size_t bytes) -> cudaError_t {
@@ -374,6 +382,7 @@ bem_status bem_mesh_create(const bem_mesh_desc* d, bem_comm* comm, bem_mesh** ou
       (e = up((void**)&m->d_seg, m->seg.data(), sizeof(Seg) * ng)) != cudaSuccess ||
       (e = up((void**)&m->d_half, m->half.data(), sizeof(Seg) * 2 * ng)) != cudaSuccess ||
       (e = up((void**)&m->d_dual, m->dual.data(), sizeof(Dual) * ng)) != cudaSuccess ||
+      (e = up((void**)&m->d_lag, lagtab.data(), sizeof(double4) * lagtab.size())) != cudaSuccess ||
       (e = cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking)) != cudaSuccess) {
     bem_mesh_destroy(m);
     return cuda_fail(e, "bem_mesh_create/upload");
@@ -405,6 +414,7 @@ void bem_mesh_destroy(bem_mesh* m) {
   cudaFree(m->d_seg);
   cudaFree(m->d_half);
   cudaFree(m->d_dual);
+  cudaFree(m->d_lag);
   if (m->stream) cudaStreamDestroy(m->stream);
   delete m;
 }

@@ -61,7 +61,7 @@ class AssemblyStats(ctypes.Structure):
     _fields_ = [("ms_bulk", ctypes.c_double), ("ms_near", ctypes.c_double), ("ms_sing", ctypes.c_double),
                 ("evals_bulk", ctypes.c_longlong), ("evals_near", ctypes.c_longlong),
                 ("q_bulk", ctypes.c_int), ("q_sing", ctypes.c_int), ("launches", ctypes.c_int),
-                ("entries", ctypes.c_longlong)]
+                ("entries", ctypes.c_longlong), ("flops_bulk", ctypes.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
