@@ -99,17 +99,21 @@ typedef struct {
   int n_matvec_D;            /* D_h products performed */
 } bem_solve_report;
 
-/* Per-matrix assembly statistics: device time of the three assembly kernel families, measured
- * with CUDA events on the stream passed to bem_assemble_*, and the exact number of kernel
- * evaluations (point pair x time node for the bulk, point pair x lag for the near cells) that
- * the shipped quadrature performs (DESIGN.md section 6 turns them into FP64 FLOPs). */
+/* Per-matrix assembly statistics: device time of the assembly kernel families, measured with
+ * CUDA events on the stream passed to bem_assemble_*, and the number of time-node evaluations
+ * (entry-level spatial pair x time node) of the bulk (d >= 2) and near (d <= 1) kernels, split by
+ * evaluation regime: [0] A moment polynomial, [1] B Taylor about the
+ * cluster centre, [2] Z exponentially small, [3] C point by point. */
 typedef struct {
   double ms_bulk, ms_near, ms_sing;
-  long long evals_bulk, evals_near;
+  long long evals_bulk, evals_near;   /* node evaluations (sum over regimes) */
   int q_bulk, q_sing;
   int launches;
   long long entries;         /* stored (unpadded) entries */
   double flops_bulk;         /* algorithmic FP64 flops of the bulk kernels */
+  double ms_records;         /* pair-record (moment) kernels */
+  long long nodes_bulk[4];   /* bulk node evaluations per regime A, B, Z, C */
+  long long nodes_near[4];   /* near-cell node evaluations per regime */
 } bem_assembly_stats;
 
 /* ---------------------------------------------------------------- general */

@@ -407,6 +407,11 @@ bem_status bem_matrix_stats(const bem_matrix* A, bem_assembly_stats* o) {
   bem_matrix_info(A, &kind, &ent, nullptr);
   o->entries = ent;
   o->flops_bulk = A->flops_bulk;
+  o->ms_records = A->ms_records;
+  for (int k = 0; k < 4; ++k) {
+    o->nodes_bulk[k] = A->nodes_bulk[k];
+    o->nodes_near[k] = A->nodes_near[k];
+  }
   return BEM_OK;
 }
 

@@ -117,8 +117,9 @@ struct bem_matrix_s {
   double* d_up = nullptr;
   double* d_work = nullptr;  // tridiagonal solve scratch (3 n)
   // assembly statistics
-  double ms_bulk = 0, ms_near = 0, ms_sing = 0;
-  long long ev_bulk = 0, ev_near = 0;
+  double ms_bulk = 0, ms_near = 0, ms_sing = 0, ms_records = 0;
+  long long ev_bulk = 0, ev_near = 0, nodes_expected = 0;
+  long long nodes_bulk[4] = {0, 0, 0, 0}, nodes_near[4] = {0, 0, 0, 0};  // regimes A, B, Z, C
   double flops_bulk = 0;
   int q_bulk = 0, q_sing = 0, launches = 0;
 };

@@ -1,0 +1,634 @@
+// moments.cuh — separable (moment) evaluation of the regular-pair space-time integrals,
+// included by assemble.cu (one translation unit: the Gauss tables live in __constant__ there).
+//
+// An entry of time cell (a,b) is the four-lag second difference of node values
+//   Phi(x, y) = sum_p W_p G(t_x - t_y; c_p),   c_p = alpha r_p^2 / 4
+// over the quadrature points p of the (half-)segment pairs that make up one matrix entry, with
+// G the double (V, D curl: H) or single (D normal: F; K: Q) time antiderivative.  G depends on
+// the point only through c and on the node only through s = t_x - t_y.  Terms of G that are
+// affine in s with point-only coefficients cancel in every second difference whose four lags are
+// positive (sum eps_m s_m = 0, sum eps_m = 0), so the bulk evaluates the regularised
+//   H~ = s h(x) + (s+c)(gamma + ln c)      = s GH(x) + (s+c) ln s          (x = c/s)
+//   F~ = E1(x) + gamma + ln c              = Ein(x) + ln s
+//   Q~ = e^{-x}/x - E1(x) - s/c - gamma - ln c = PSI(x) - ln s
+// (GH, Ein, PSI entire).  Three regimes per (entry, node), chosen per lane:
+//   A  x_max = c_max/s < 4: the polynomials of moment_coeffs.h in x, so the sum over points is
+//      sum_k f_k s^{-k} M_k with time-independent moments M_k = sum_p W_p c_p^k: one Horner
+//      chain in u = 1/s per kernel family, independent of the number of quadrature points.
+//   B  the points are clustered, rho = (c_max - c0)/c0 <= 0.3: Taylor expansion in c around c0
+//      with shifted moments m_k = sum_p W_p (c_p - c0)^k; the node-dependent Taylor
+//      coefficients of E1 / (1+x)E1 - e^{-x} / e^{-x}/x - E1 come from the recurrence for
+//      e^{-x}/x (x f = e^{-x}).  The remainder is bounded by rho^K (the pole of E1' at c = 0)
+//      and e^{-x0} (rho x0)^K / K! <= rho^K / sqrt(2 pi K) (the exponential), so the order per
+//      pair is K = min(32, ceil(ln 1e-17 / ln rho)) (relative error below 1e-17 sum |W|).
+//   Z  x_min >= 50: the E1 / exp parts are below 1e-23; only the affine constants remain.
+//   C  otherwise: the point-by-point sum (same quadrature), dealt over the 32 lanes of the warp.
+// The records (moments and constants) depend on the spatial pair only: built once per
+// assembly by k_records, reused by every block, band and time node.
+#pragma once
+
+#include "moment_coeffs.h"
+
+namespace stb {
+
+constexpr int MKA = 17;          // regime-A polynomial degree (MGH, MEIN; MPSI padded)
+constexpr int MKB = 32;          // regime-B maximum Taylor order
+constexpr double MRHO = 0.3;     // regime-B cluster bound (c_max - c0 <= MRHO c0)
+constexpr double MXZ = 50.0;     // regime Z threshold on x_min
+// record layout (field-major, stride npairs): common fields, then one block per family
+enum { RF_CMAX = 0, RF_CMIN = 1, RF_C0 = 2, RF_KB = 3, RF_COMMON = 4 };
+enum { FA = 0, FM0 = MKA + 1, FM1 = MKA + 2, FB = MKA + 3, FC0 = MKA + MKB + 4, FC1 = MKA + MKB + 5,
+       FAMSZ = MKA + MKB + 6 };
+enum { FAM_H = 0, FAM_F = 1, FAM_Q = 2 };
+
+template <int KIND> struct Fams;
+template <> struct Fams<STB_V> { static constexpr int n = 1, f0 = FAM_H, f1 = -1; };
+template <> struct Fams<STB_K> { static constexpr int n = 1, f0 = FAM_Q, f1 = -1; };
+template <> struct Fams<STB_D> { static constexpr int n = 2, f0 = FAM_H, f1 = FAM_F; };
+template <int KIND> constexpr int rec_fields() { return RF_COMMON + Fams<KIND>::n * FAMSZ; }
+
+static __device__ __constant__ const double STB_INV[MKB + 2] = {
+    0.0,      1.0,      1.0 / 2,  1.0 / 3,  1.0 / 4,  1.0 / 5,  1.0 / 6,  1.0 / 7,  1.0 / 8,
+    1.0 / 9,  1.0 / 10, 1.0 / 11, 1.0 / 12, 1.0 / 13, 1.0 / 14, 1.0 / 15, 1.0 / 16, 1.0 / 17,
+    1.0 / 18, 1.0 / 19, 1.0 / 20, 1.0 / 21, 1.0 / 22, 1.0 / 23, 1.0 / 24, 1.0 / 25, 1.0 / 26,
+    1.0 / 27, 1.0 / 28, 1.0 / 29, 1.0 / 30, 1.0 / 31, 1.0 / 32, 1.0 / 33};
+
+__device__ __forceinline__ double mpoly(int fam, int k) {
+  if (fam == FAM_H) return STB_MGH[k];
+  if (fam == FAM_F) return STB_MEIN[k];
+  return k <= STB_MPSI_DEG ? STB_MPSI[k] : 0.0;
+}
+
+struct MomArgs {
+  double* rec;            // record storage (rec_fields x npairs)
+  long long npairs;       // ng * ng
+  const Seg* seg;
+  const Seg* half;
+  const Dual* dual;
+  double alpha;
+  int ng;
+  int q;                  // bulk Gauss order (bulk records)
+  int qfar;               // near-cell order of well-separated pairs (near records)
+  unsigned long long* counters;  // node evaluations per regime: A, B, Z, C
+};
+
+// ------------------------------------------------------------- point enumeration
+// Visits every quadrature point of the (half-)segment pairs that make up entry (I, J) with its
+// weights for the kernel families of KIND: vis(c, w_first_family, w_second_family).
+//   V: (seg I, seg J), H weight h_X h_Y w_u w_v / 4pi
+//   K: entry (i, n) of the primal hat phi_n: (seg i, seg n-1) rising, (seg i, seg n) falling;
+//      Q weight alpha h_X h_Y w_u w_v ((x - y).n_y) phi_n(y) / 8pi; collinear pairs are 0
+//   D: dual hats psi_l, psi_k on their 4 half segments each (R6, R7): curl weight
+//      h_X h_Y w_u w_v psi_l' psi_k' / 4pi (H), normal weight alpha h_X h_Y w_u w_v
+//      (n_x.n_y) psi_l psi_k / 4pi (F)
+// NEAR: touching sub-pairs are skipped (k_sing adds them) and the order follows the distance.
+struct SubPair {
+  Seg X, Y;
+  int q;
+  int side;                 // K: 0 = gamma_{n-1} (hat rising), 1 = gamma_n (falling)
+  double sa, sb;            // weight scales of the two families
+  double l0, l1, k0, k1;    // D: psi_l on X and psi_k on Y, linear from (l0 / k0) to (l1 / k1)
+};
+
+template <int KIND, bool NEAR, class Fn>
+__device__ __forceinline__ void for_subpairs(const MomArgs& M, int I, int J, Fn&& fn) {
+  const int ng = M.ng;
+  SubPair sp;
+  if (KIND == STB_V) {
+    if (NEAR && chain_rel(I, J, ng)) return;
+    sp.X = M.seg[I];
+    sp.Y = M.seg[J];
+    sp.q = NEAR ? near_order(sp.X, sp.Y, M.qfar) : M.q;
+    sp.sa = sp.X.h * sp.Y.h / (4.0 * STB_PI);
+    sp.sb = 0.0;
+    fn(sp);
+  } else if (KIND == STB_K) {
+    sp.X = M.seg[I];
+#pragma unroll 1
+    for (int side = 0; side < 2; ++side) {
+      const int j = side == 0 ? (J - 1 + ng) % ng : J;
+      sp.Y = M.seg[j];
+      if (collinear(sp.X, sp.Y)) continue;
+      if (NEAR && chain_rel(I, j, ng)) continue;
+      sp.q = NEAR ? near_order(sp.X, sp.Y, M.qfar) : M.q;
+      sp.side = side;
+      sp.sa = M.alpha / (8.0 * STB_PI) * sp.X.h * sp.Y.h;
+      sp.sb = 0.0;
+      fn(sp);
+    }
+  } else {
+    const int nh = 2 * ng;
+    const Dual dl = M.dual[I], dk = M.dual[J];
+#pragma unroll 1
+    for (int m = 0; m < 4; ++m) {
+      const int p = (2 * I - 1 + m + nh) % nh;
+      sp.X = M.half[p];
+      const double dvl = m < 2 ? 1.0 / dl.Lm : -1.0 / dl.Lp;
+      sp.l0 = m == 0 ? 0.0 : (m == 1 ? dl.vm : (m == 2 ? 1.0 : dl.vp));
+      sp.l1 = m == 0 ? dl.vm : (m == 1 ? 1.0 : (m == 2 ? dl.vp : 0.0));
+#pragma unroll 1
+      for (int n = 0; n < 4; ++n) {
+        const int qh = (2 * J - 1 + n + nh) % nh;
+        if (NEAR && chain_rel(p, qh, nh)) continue;
+        sp.Y = M.half[qh];
+        sp.q = NEAR ? near_order(sp.X, sp.Y, M.qfar) : M.q;
+        const double dvk = n < 2 ? 1.0 / dk.Lm : -1.0 / dk.Lp;
+        sp.k0 = n == 0 ? 0.0 : (n == 1 ? dk.vm : (n == 2 ? 1.0 : dk.vp));
+        sp.k1 = n == 0 ? dk.vm : (n == 1 ? 1.0 : (n == 2 ? dk.vp : 0.0));
+        const double hh = sp.X.h * sp.Y.h / (4.0 * STB_PI);
+        sp.sa = hh * dvl * dvk;
+        sp.sb = M.alpha * hh * (sp.X.nx * sp.Y.nx + sp.X.ny * sp.Y.ny);
+        fn(sp);
+      }
+    }
+  }
+}
+
+// quadrature point (u, v) of a sub-pair: c = alpha r^2 / 4 and the two family weights
+template <int KIND>
+__device__ __forceinline__ void sub_point(const SubPair& sp, double alpha, int u, int v, double& c,
+                                          double& wa, double& wb) {
+  const int q = sp.q;
+  const double fu = c_gx[q][u], fv = c_gx[q][v];
+  const double px = fma(fu, sp.X.bx - sp.X.ax, sp.X.ax), py = fma(fu, sp.X.by - sp.X.ay, sp.X.ay);
+  const double qx = fma(fv, sp.Y.bx - sp.Y.ax, sp.Y.ax), qy = fma(fv, sp.Y.by - sp.Y.ay, sp.Y.ay);
+  const double dx = px - qx, dy = py - qy;
+  c = 0.25 * alpha * (dx * dx + dy * dy);
+  const double w = c_gw[q][u] * c_gw[q][v];
+  if (KIND == STB_V) {
+    wa = sp.sa * w;
+    wb = 0.0;
+  } else if (KIND == STB_K) {
+    wa = sp.sa * w * (dx * sp.Y.nx + dy * sp.Y.ny) * (sp.side == 0 ? fv : 1.0 - fv);
+    wb = 0.0;
+  } else {
+    wa = sp.sa * w;
+    wb = sp.sb * w * fma(sp.l1 - sp.l0, fu, sp.l0) * fma(sp.k1 - sp.k0, fv, sp.k0);
+  }
+}
+
+template <int KIND, bool NEAR, class Vis>
+__device__ __forceinline__ void for_points(const MomArgs& M, int I, int J, Vis&& vis) {
+  for_subpairs<KIND, NEAR>(M, I, J, [&](const SubPair& sp) {
+    for (int u = 0; u < sp.q; ++u)
+      for (int v = 0; v < sp.q; ++v) {
+        double c, wa, wb;
+        sub_point<KIND>(sp, M.alpha, u, v, c, wa, wb);
+        vis(c, wa, wb);
+      }
+  });
+}
+
+// the points of entry (I, J) dealt round-robin to the 32 lanes of a warp (lane's share only)
+template <int KIND, bool NEAR, class Vis>
+__device__ __forceinline__ void for_points_lane(const MomArgs& M, int I, int J, int lane, Vis&& vis) {
+  int base = 0;
+  for_subpairs<KIND, NEAR>(M, I, J, [&](const SubPair& sp) {
+    const int n = sp.q * sp.q;
+    for (int idx = (lane - base) & 31; idx < n; idx += 32) {
+      double c, wa, wb;
+      sub_point<KIND>(sp, M.alpha, idx / sp.q, idx % sp.q, c, wa, wb);
+      vis(c, wa, wb);
+    }
+    base = (base + n) & 31;
+  });
+}
+
+// ------------------------------------------------------------- records
+// One thread per entry-level spatial pair (I, J): c range, regime-A moments premultiplied by the
+// polynomial coefficients, regime-B shifted moments, and the affine constants
+//   C0 = sum W (gamma + ln c), C1 = sum W c (gamma + ln c)  (H);  C0 (F, Q);  C1 = sum W / c (Q)
+template <int KIND, bool NEAR>
+__global__ void __launch_bounds__(128) k_records(MomArgs M) {
+  const long long pair = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (pair >= M.npairs) return;
+  const int I = (int)(pair / M.ng), J = (int)(pair % M.ng);
+  double* rec = M.rec + pair;
+  const long long S = M.npairs;
+  double cmin = 1e300, cmax = 0.0;
+  int npts = 0;
+  for_points<KIND, NEAR>(M, I, J, [&](double c, double, double) {
+    cmin = fmin(cmin, c);
+    cmax = fmax(cmax, c);
+    ++npts;
+  });
+  if (npts == 0) cmin = 0.0;
+  const double c0m = 0.5 * (cmin + cmax);
+  const bool okB = cmin > 0.0 && (cmax - c0m) <= MRHO * c0m;
+  const double c0 = okB ? c0m : 0.0;
+  const double rho = okB ? (cmax - c0m) / c0m : 1.0;
+  const int kb = rho <= 1e-6 ? 3 : min(MKB, max(3, (int)ceil(log(1e-17) / log(rho))));
+  rec[RF_CMAX * S] = cmax;
+  rec[RF_CMIN * S] = cmin;
+  rec[RF_C0 * S] = c0;
+  rec[RF_KB * S] = (double)kb;
+#pragma unroll 1
+  for (int slot = 0; slot < Fams<KIND>::n; ++slot) {
+    const int fam = slot == 0 ? Fams<KIND>::f0 : Fams<KIND>::f1;
+    double* R = rec + (RF_COMMON + slot * FAMSZ) * S;
+    // regime A: M_k = sum W c^k
+    double mk[MKA + 1];
+#pragma unroll
+    for (int k = 0; k <= MKA; ++k) mk[k] = 0.0;
+    for_points<KIND, NEAR>(M, I, J, [&](double c, double wa, double wb) {
+      const double w = slot == 0 ? wa : wb;
+      double pw = w;
+#pragma unroll
+      for (int k = 0; k <= MKA; ++k) {
+        mk[k] += pw;
+        pw *= c;
+      }
+    });
+#pragma unroll
+    for (int k = 0; k <= MKA; ++k) R[(FA + k) * S] = mpoly(fam, k) * mk[k];
+    R[FM0 * S] = mk[0];
+    R[FM1 * S] = mk[1];
+    // regime B: m_k = sum W (c - c0)^k
+    double mb[MKB + 1];
+#pragma unroll
+    for (int k = 0; k <= MKB; ++k) mb[k] = 0.0;
+    if (okB) {
+      for_points<KIND, NEAR>(M, I, J, [&](double c, double wa, double wb) {
+        const double w = slot == 0 ? wa : wb;
+        const double d = c - c0;
+        double pw = w;
+#pragma unroll
+        for (int k = 0; k <= MKB; ++k) {
+          mb[k] += pw;
+          pw *= d;
+        }
+      });
+    }
+#pragma unroll
+    for (int k = 0; k <= MKB; ++k) R[(FB + k) * S] = mb[k];
+    // affine constants (all points at c > 0)
+    double C0 = 0.0, C1 = 0.0;
+    if (cmin > 0.0) {
+      for_points<KIND, NEAR>(M, I, J, [&](double c, double wa, double wb) {
+        const double w = slot == 0 ? wa : wb;
+        const double g = STB_GAMMA + log(c);
+        C0 = fma(w, g, C0);
+        C1 += fam == FAM_Q ? w / c : w * c * g;
+      });
+    }
+    R[FC0 * S] = C0;
+    R[FC1 * S] = C1;
+  }
+}
+
+// ------------------------------------------------------------- node evaluation
+// regime A from registers
+template <int KIND>
+struct RegA {
+  double P[Fams<KIND>::n][MKA + 1];
+  double M0[Fams<KIND>::n], M1[Fams<KIND>::n];
+  double cmax;
+  __device__ __forceinline__ void load(const double* __restrict__ rec, long long S) {
+    cmax = rec[RF_CMAX * S];
+#pragma unroll
+    for (int f = 0; f < Fams<KIND>::n; ++f) {
+      const double* R = rec + (RF_COMMON + f * FAMSZ) * S;
+#pragma unroll
+      for (int k = 0; k <= MKA; ++k) P[f][k] = R[(FA + k) * S];
+      M0[f] = R[FM0 * S];
+      M1[f] = R[FM1 * S];
+    }
+  }
+  // Phi~ at the node (s, ln s, u = 1/s)
+  __device__ __forceinline__ double eval(double s, double lns, double u) const {
+    double out = 0.0;
+#pragma unroll
+    for (int f = 0; f < Fams<KIND>::n; ++f) {
+      const int fam = f == 0 ? Fams<KIND>::f0 : Fams<KIND>::f1;
+      double acc = P[f][MKA];
+#pragma unroll
+      for (int k = MKA - 1; k >= 0; --k) acc = fma(acc, u, P[f][k]);
+      if (fam == FAM_H) out += fma(s, fma(lns, M0[f], acc), lns * M1[f]);
+      else if (fam == FAM_F) out += fma(lns, M0[f], acc);
+      else out += fma(-lns, M0[f], acc);
+    }
+    return out;
+  }
+};
+
+// point-by-point regularised contributions (regime C), same function as regimes A / B / Z
+__device__ __forceinline__ double pt_h(double c, double s, double lns, double u) {
+  const double x = c * u;
+  if (x < STB_XSPLIT) return fma(s, gh_poly(x), (s + c) * lns);
+  const double e = x > STB_XUNDER ? 0.0 : exp(-x);
+  const double hf = x > STB_XUNDER ? 0.0 : fma(1.0 + x, e1_large(1.0 / x, e), -e);
+  return fma(s, hf, (s + c) * (STB_GAMMA + log(c)));
+}
+__device__ __forceinline__ double pt_f(double c, double lns, double u) {
+  const double x = c * u;
+  if (x < STB_XSPLIT) return ein_poly(x) + lns;
+  const double e1 = x > STB_XUNDER ? 0.0 : e1_large(1.0 / x, exp(-x));
+  return e1 + STB_GAMMA + log(c);
+}
+__device__ __forceinline__ double pt_q(double c, double s, double lns, double u) {
+  const double x = c * u;
+  if (x < STB_XSPLIT) return psi_poly(x) - lns;
+  const double t = 1.0 / x;
+  const double e = x > STB_XUNDER ? 0.0 : exp(-x);
+  const double k = x > STB_XUNDER ? 0.0 : e * t - e1_large(t, e);
+  return k - s / c - (STB_GAMMA + log(c));
+}
+
+// regimes B and Z (out of line: rare); *regime = 1 (B), 2 (Z) or 3 (C: not evaluated here)
+template <int KIND>
+__device__ __noinline__ double phi_bz(const MomArgs M, long long pair, double s, double u, int* regime) {
+  const long long S = M.npairs;
+  const double* rec = M.rec + pair;
+  const double cmin = rec[RF_CMIN * S], c0 = rec[RF_C0 * S];
+  const bool zz = cmin > 0.0 && cmin * u >= MXZ;
+  if (!zz && !(c0 > 0.0)) {
+    *regime = 3;
+    return 0.0;
+  }
+  double T[2] = {0.0, 0.0};
+  if (!zz) {
+    // Taylor coefficients at x0 of e^{-x}/x: a_j = (e_j - a_{j-1}) / x0, e_j = e^{-x0}(-1)^j/j!
+    const int kb = (int)rec[RF_KB * S];
+    const double x0 = c0 * u, ix0 = 1.0 / x0, ex = exp(-x0);
+    const double E1 = x0 < STB_XSPLIT ? ein_poly(x0) - (STB_GAMMA + log(x0)) : e1_large(ix0, ex);
+    double ej = ex, am2 = 0.0, am1 = ex * ix0;  // a_{k-2}, a_{k-1} at k = 1
+    double upk = 1.0;
+    double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll 1
+    for (int k = 0; k <= kb; ++k) {
+      double c_0 = 0.0, c_1 = 0.0;   // coefficient of u^k m_k for the two families
+      double ak = 0.0;               // a_k (k >= 1)
+      if (k >= 1) {
+        ej = -ej * STB_INV[k];
+        ak = (ej - am1) * ix0;
+      }
+#pragma unroll
+      for (int f = 0; f < Fams<KIND>::n; ++f) {
+        const int fam = f == 0 ? Fams<KIND>::f0 : Fams<KIND>::f1;
+        double cf;
+        if (fam == FAM_H) {
+          // h(x0+d) = h(x0) + h'(x0) d + sum_{j>=0} b_j d^{j+2} / ((j+1)(j+2)), b_j = -(j+1)a_{j+1} - a_j
+          if (k == 0) cf = fma(1.0 + x0, E1, -ex);
+          else if (k == 1) cf = E1 - am1;
+          else cf = (-(k - 1) * am1 - am2) * (STB_INV[k - 1] * STB_INV[k]);
+        } else if (fam == FAM_F) {
+          cf = k == 0 ? E1 : -am1 * STB_INV[k];               // E1' = -e^{-x}/x
+        } else {
+          // (e^{-x}/x - E1)' = -e^{-x}/x^2: coefficient -b_{k-1}/k
+          cf = k == 0 ? am1 - E1 : fma(k, ak, am1) * STB_INV[k];
+        }
+        if (f == 0) c_0 = cf; else c_1 = cf;
+      }
+      const double* R0 = rec + (RF_COMMON + FB + k) * S;
+      acc0 = fma(c_0 * upk, R0[0], acc0);
+      if (Fams<KIND>::n == 2) acc1 = fma(c_1 * upk, R0[FAMSZ * S], acc1);
+      upk *= u;
+      if (k >= 1) {
+        am2 = am1;
+        am1 = ak;
+      }
+    }
+    T[0] = acc0;
+    T[1] = acc1;
+  }
+  *regime = zz ? 2 : 1;
+  double out = 0.0;
+#pragma unroll
+  for (int f = 0; f < Fams<KIND>::n; ++f) {
+    const int fam = f == 0 ? Fams<KIND>::f0 : Fams<KIND>::f1;
+    const double* R = rec + (RF_COMMON + f * FAMSZ) * S;
+    const double C0 = R[FC0 * S], C1 = R[FC1 * S];
+    if (fam == FAM_H) out += fma(s, T[f] + C0, C1);
+    else if (fam == FAM_F) out += T[f] + C0;
+    else out += T[f] - fma(s, C1, C0);
+  }
+  return out;
+}
+
+// regime C, warp-cooperative: every lane evaluates its round-robin share of the points of
+// entry (I, J) at node (s, u) (all lanes pass the same arguments); returns the warp sum
+template <int KIND, bool NEAR>
+__device__ __noinline__ double phi_c_warp(const MomArgs M, int I, int J, double s, double lns, double u) {
+  const int lane = threadIdx.x & 31;
+  double out = 0.0;
+  for_points_lane<KIND, NEAR>(M, I, J, lane, [&](double c, double wa, double wb) {
+    if (KIND == STB_V) out = fma(wa, pt_h(c, s, lns, u), out);
+    else if (KIND == STB_K) out = fma(wa, pt_q(c, s, lns, u), out);
+    else {
+      out = fma(wa, pt_h(c, s, lns, u), out);
+      if (wb != 0.0) out = fma(wb, pt_f(c, lns, u), out);
+    }
+  });
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) out += __shfl_xor_sync(0xffffffffu, out, o);
+  return out;
+}
+
+// true node value for the near cells: Phi = Phi~ - affine part
+template <int KIND>
+__device__ __forceinline__ double affine_part(const double* __restrict__ rec, long long S, double s) {
+  double out = 0.0;
+#pragma unroll
+  for (int f = 0; f < Fams<KIND>::n; ++f) {
+    const int fam = f == 0 ? Fams<KIND>::f0 : Fams<KIND>::f1;
+    const double* R = rec + (RF_COMMON + f * FAMSZ) * S;
+    const double C0 = R[FC0 * S], C1 = R[FC1 * S];
+    if (fam == FAM_H) out += fma(s, C0, C1);
+    else if (fam == FAM_F) out += C0;
+    else out -= fma(s, C1, C0);
+  }
+  return out;
+}
+
+// warp-aggregated regime counters
+__device__ __forceinline__ void count_regimes(unsigned long long* ctr, unsigned long long nA,
+                                              unsigned long long nB, unsigned long long nZ,
+                                              unsigned long long nC) {
+  if (!ctr) return;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    nA += __shfl_xor_sync(0xffffffffu, nA, o);
+    nB += __shfl_xor_sync(0xffffffffu, nB, o);
+    nZ += __shfl_xor_sync(0xffffffffu, nZ, o);
+    nC += __shfl_xor_sync(0xffffffffu, nC, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(ctr + 0, nA);
+    if (nB) atomicAdd(ctr + 1, nB);
+    if (nZ) atomicAdd(ctr + 2, nZ);
+    if (nC) atomicAdd(ctr + 3, nC);
+  }
+}
+
+// ------------------------------------------------------------- bulk cells (d >= 2)
+// thread = entry-level pair (I, J): warp = row I, lane = column J (coalesced stores); band of R
+// test steps; the thread sweeps the trial nodes y and evaluates the R+1 nodes (x, y) of the band
+// once each (1.125 node evaluations per entry at R = 8).  Column fast path: when the node with
+// the smallest lag is in regime A for every lane, all R+1 nodes are (s grows with x), and the
+// R+1 Horner chains run unrolled and interleaved.
+template <int KIND, int R>
+__global__ void __launch_bounds__(128) k_bulk_m(BlockArgs B, MomArgs M) {
+  const int ng = B.ng;
+  const int lane = threadIdx.x & 31;
+  const int J0 = blockIdx.x * 32 + lane;
+  const int I0 = blockIdx.y * 4 + (threadIdx.x >> 5);
+  const bool valid = I0 < ng && J0 < ng;
+  const int I = min(I0, ng - 1), J = min(J0, ng - 1);
+  const int band = blockIdx.z;
+  const int r_hi = B.a1 - R * band;
+  const int r_lo = max(B.a0, r_hi - R);
+  if (r_hi <= r_lo) return;                       // CTA-uniform
+  const int bmax = min(B.b1 - 1, r_hi - 1 - 2);
+  if (bmax < B.b0) return;                        // CTA-uniform
+  const long long pair = (long long)I * ng + J;
+  const long long S = M.npairs;
+  RegA<KIND> A;
+  A.load(M.rec + pair, S);
+  unsigned long long nA = 0, nB = 0, nZ = 0, nC = 0;
+  double Gp[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) Gp[r] = 0.0;
+  for (int y = B.b0; y <= bmax + 1; ++y) {
+    double phi[R + 1];
+    const int xf = max(r_lo, y + 1);
+    const double umax = B.lag[xf * B.ldlag + y].z;
+    if (__all_sync(0xffffffffu, A.cmax * umax < STB_MXA)) {
+#pragma unroll
+      for (int r = 0; r <= R; ++r) {
+        const int x = r_lo + r;
+        phi[r] = 0.0;
+        if (x <= r_hi && x > y) {
+          const double4 nd = B.lag[x * B.ldlag + y];
+          phi[r] = A.eval(nd.x, nd.y, nd.z);
+          ++nA;
+        }
+      }
+    } else {
+      unsigned cmask = 0;   // nodes r of this lane left to regime C
+#pragma unroll
+      for (int r = 0; r <= R; ++r) {
+        const int x = r_lo + r;
+        double v = 0.0;
+        if (x <= r_hi && x > y) {
+          const double4 nd = B.lag[x * B.ldlag + y];
+          if (A.cmax * nd.z < STB_MXA) {
+            v = A.eval(nd.x, nd.y, nd.z);
+            ++nA;
+          } else {
+            int reg = 0;
+            v = phi_bz<KIND>(M, pair, nd.x, nd.z, &reg);
+            nB += reg == 1;
+            nZ += reg == 2;
+            if (reg == 3) {
+              cmask |= 1u << r;
+              ++nC;
+            }
+          }
+        }
+        phi[r] = v;
+      }
+      unsigned lanes = __ballot_sync(0xffffffffu, cmask != 0);
+      while (lanes) {                                   // warp-uniform
+        const int src = __ffs(lanes) - 1;
+        lanes &= lanes - 1;
+        unsigned cm = __shfl_sync(0xffffffffu, cmask, src);
+        const int Is = __shfl_sync(0xffffffffu, I, src), Js = __shfl_sync(0xffffffffu, J, src);
+        while (cm) {
+          const int r = __ffs(cm) - 1;
+          cm &= cm - 1;
+          const double4 nd = B.lag[(r_lo + r) * B.ldlag + y];
+          const double v = phi_c_warp<KIND, false>(M, Is, Js, nd.x, nd.y, nd.z);
+          if (lane == src) {
+#pragma unroll
+            for (int rr = 0; rr <= R; ++rr)
+              if (rr == r) phi[rr] = v;
+          }
+        }
+      }
+    }
+    if (y > B.b0) {
+      const int b = y - 1;
+#pragma unroll
+      for (int r = 1; r <= R; ++r) {
+        const int a = r_lo + r - 1;
+        const double G = phi[r] - phi[r - 1];
+        if (valid && a < r_hi && a - b >= 2) *entry_ptr(B, a, I, b, J) = Gp[r - 1] - G;
+        Gp[r - 1] = G;
+      }
+    } else {
+#pragma unroll
+      for (int r = 1; r <= R; ++r) Gp[r - 1] = phi[r] - phi[r - 1];
+    }
+  }
+  if (!valid) nA = nB = nZ = nC = 0;
+  count_regimes(M.counters, nA, nB, nZ, nC);
+}
+
+// ------------------------------------------------------------- near cells (d <= 1)
+// thread = entry-level pair; it walks the test steps a of its chunk: entry (a, a) = Phi(a+1, a),
+// entry (a, a-1) = Phi(a+1, a-1) - Phi(a, a-1) - Phi(a+1, a) (Phi(a, a) = 0: G vanishes at s = 0),
+// with the true node values Phi = Phi~ - affine part (the affine terms do not cancel here).
+// Touching sub-pairs are excluded from the near records; k_sing adds them afterwards.
+template <int KIND>
+__global__ void __launch_bounds__(128) k_near_m(BlockArgs B, MomArgs M, int chunk) {
+  const int ng = B.ng;
+  const int lane = threadIdx.x & 31;
+  const int J0 = blockIdx.x * 32 + lane;
+  const int I0 = blockIdx.y * 4 + (threadIdx.x >> 5);
+  const bool valid = I0 < ng && J0 < ng;
+  const int I = min(I0, ng - 1), J = min(J0, ng - 1);
+  const int a_beg = B.a0 + blockIdx.z * chunk;
+  const int a_end = min(B.a1, a_beg + chunk);
+  const long long pair = (long long)I * ng + J;
+  const long long S = M.npairs;
+  const double* rec = M.rec + pair;
+  RegA<KIND> A;
+  A.load(rec, S);
+  unsigned long long nA = 0, nB = 0, nZ = 0, nC = 0;
+  // node value for every lane (warp-uniform call: regime C is computed cooperatively)
+  auto node = [&](int x, int y) -> double {
+    const double4 nd = B.lag[x * B.ldlag + y];
+    double v = 0.0;
+    bool needC = false;
+    if (A.cmax * nd.z < STB_MXA) {
+      v = A.eval(nd.x, nd.y, nd.z);
+      ++nA;
+    } else {
+      int reg = 0;
+      v = phi_bz<KIND>(M, pair, nd.x, nd.z, &reg);
+      nB += reg == 1;
+      nZ += reg == 2;
+      if (reg == 3) {
+        needC = true;
+        ++nC;
+      }
+    }
+    unsigned lanes = __ballot_sync(0xffffffffu, needC);
+    while (lanes) {
+      const int src = __ffs(lanes) - 1;
+      lanes &= lanes - 1;
+      const int Is = __shfl_sync(0xffffffffu, I, src), Js = __shfl_sync(0xffffffffu, J, src);
+      const double c = phi_c_warp<KIND, true>(M, Is, Js, nd.x, nd.y, nd.z);
+      if (lane == src) v = c;
+    }
+    return v - affine_part<KIND>(rec, S, nd.x);
+  };
+  double prev = 0.0;  // Phi(a, a-1)
+  if (a_beg < a_end && a_beg >= 1 && a_beg - 1 >= B.b0 && a_beg - 1 < B.b1) prev = node(a_beg, a_beg - 1);
+#pragma unroll 1
+  for (int a = a_beg; a < a_end; ++a) {
+    const bool d0 = a >= B.b0 && a < B.b1, d1 = a - 1 >= B.b0 && a - 1 < B.b1;
+    double p10 = 0.0;
+    if (d0 || d1) p10 = node(a + 1, a);
+    if (d0 && valid) *entry_ptr(B, a, I, a, J) = p10;
+    if (d1) {
+      const double p20 = node(a + 1, a - 1);
+      if (valid) *entry_ptr(B, a, I, a - 1, J) = p20 - prev - p10;
+    }
+    prev = p10;
+  }
+  if (!valid) nA = nB = nZ = nC = 0;
+  count_regimes(M.counters, nA, nB, nZ, nC);
+}
+
+}  // namespace stb

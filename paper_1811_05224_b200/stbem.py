@@ -61,10 +61,16 @@ class AssemblyStats(ctypes.Structure):
     _fields_ = [("ms_bulk", ctypes.c_double), ("ms_near", ctypes.c_double), ("ms_sing", ctypes.c_double),
                 ("evals_bulk", ctypes.c_longlong), ("evals_near", ctypes.c_longlong),
                 ("q_bulk", ctypes.c_int), ("q_sing", ctypes.c_int), ("launches", ctypes.c_int),
-                ("entries", ctypes.c_longlong), ("flops_bulk", ctypes.c_double)]
+                ("entries", ctypes.c_longlong), ("flops_bulk", ctypes.c_double),
+                ("ms_records", ctypes.c_double), ("nodes_bulk", ctypes.c_longlong * 4),
+                ("nodes_near", ctypes.c_longlong * 4)]
 
     def as_dict(self):
-        return {k: getattr(self, k) for k, _ in self._fields_}
+        out = {}
+        for k, _ in self._fields_:
+            v = getattr(self, k)
+            out[k] = list(v) if k.startswith("nodes_") else v
+        return out
 
 
 _lib = None

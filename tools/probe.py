@@ -1,4 +1,4 @@
-"""quick timing probe: assemble V/K/D of a config on cuda:0 and time one GEMV"""
+"""quick timing probe: assemble V/K/D of a config on cuda:0 (twice; stats of the second), one GEMV"""
 import sys, time, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
@@ -11,10 +11,18 @@ m = S.Mesh.from_workload(w)
 print(name, "ng", m.ng, "nt", m.nt, "q_bulk", m.info.q_bulk, "kappa", round(m.info.kappa, 4), "entries", m.info.entries_total, flush=True)
 mats = {}
 for k in kinds:
-    torch.cuda.synchronize(); t = time.time()
-    mats[k] = getattr(m, f"assemble_{k}")()
-    torch.cuda.synchronize(); dt = time.time() - t
-    print(f"assemble {k}: {dt:.3f} s  {m.info.entries_total/dt/1e9:.3f} G entries/s", flush=True)
+    for rep in range(2):
+        mats[k] = None
+        torch.cuda.synchronize(); t = time.time()
+        mats[k] = getattr(m, f"assemble_{k}")()
+        torch.cuda.synchronize(); dt = time.time() - t
+    st = mats[k].stats()
+    nb, nn = st["nodes_bulk"], st["nodes_near"]
+    fb = [v / max(1, sum(nb)) for v in nb]
+    fn = [v / max(1, sum(nn)) for v in nn]
+    print(f"assemble {k}: {dt:.3f} s  {m.info.entries_total/dt/1e9:.3f} G entries/s | ms rec {st['ms_records']:.2f} "
+          f"bulk {st['ms_bulk']:.2f} near {st['ms_near']:.2f} sing {st['ms_sing']:.2f} | bulk regimes A/B/Z/C "
+          f"{fb[0]:.4f}/{fb[1]:.4f}/{fb[2]:.4f}/{fb[3]:.5f} near {fn[0]:.3f}/{fn[1]:.3f}/{fn[2]:.3f}/{fn[3]:.4f}", flush=True)
 x = torch.tensor(W.random_vector(w.n), device="cuda"); y = torch.empty_like(x)
 A = mats[kinds[0]]
 for _ in range(3): A.matvec(x, y)
