@@ -72,8 +72,10 @@ typedef struct {
 typedef struct {
   int q_bulk;   /* Gauss order per direction for time cells d >= 2; 0 = chosen from kappa */
   int q_sing;   /* order of the Duffy / 1-D reduction rules for touching pairs (default 12) */
-  int flags;    /* reserved, 0 */
+  int flags;    /* BEM_QUAD_LEGACY_SING: touching pairs by per-lag singular rules (k_sing) instead
+                   of moment records; 0 = records whenever alpha (h_X+h_Y)^2 / (4 min h_t) < 4 */
 } bem_quad_opts;
+#define BEM_QUAD_LEGACY_SING 1
 
 typedef enum {
   BEM_MASS_PRIMAL = 0,      /* M_h of eq. (4): <phi^10_(a,n), phi^0_(a,i)> */
@@ -114,6 +116,7 @@ typedef struct {
   double ms_records;         /* pair-record (moment) kernels */
   long long nodes_bulk[4];   /* bulk node evaluations per regime A, B, Z, C */
   long long nodes_near[4];   /* near-cell node evaluations per regime */
+  int fused_sing;            /* 1: touching pairs through moment records, 0: per-lag k_sing */
 } bem_assembly_stats;
 
 /* ---------------------------------------------------------------- general */

@@ -70,7 +70,7 @@ bem_status assemble(int kind, const bem_mesh* m, const bem_quad_opts* o, bem_str
   if (!A) return st;
   cudaError_t e = cudaMemsetAsync(A->data, 0, sizeof(double) * A->entries, S(s));
   if (e != cudaSuccess) { bem_matrix_destroy(A); return cuda_fail(e, "bem_assemble/memset"); }
-  st = launch_assembly(kind, m, A, q_bulk, q_sing, S(s));
+  st = launch_assembly(kind, m, A, q_bulk, q_sing, o ? o->flags : 0, S(s));
   if (st == BEM_OK) st = gemv_setup(A);
   if (st != BEM_OK) { bem_matrix_destroy(A); return st; }
   *out = A;
@@ -408,6 +408,7 @@ bem_status bem_matrix_stats(const bem_matrix* A, bem_assembly_stats* o) {
   o->entries = ent;
   o->flops_bulk = A->flops_bulk;
   o->ms_records = A->ms_records;
+  o->fused_sing = A->fused_sing;
   for (int k = 0; k < 4; ++k) {
     o->nodes_bulk[k] = A->nodes_bulk[k];
     o->nodes_near[k] = A->nodes_near[k];

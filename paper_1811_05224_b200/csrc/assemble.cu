@@ -273,11 +273,23 @@ static void launch_kind(int which, const BlockArgs& BA, const MomArgs& M, int ng
   count_launch();
 }
 template <int KIND>
-static void launch_records(const MomArgs& MB, const MomArgs& MN, cudaStream_t st) {
+static void launch_records(const MomArgs& MB, const MomArgs& MN, const MomArgs* MS, int q_sing,
+                           cudaStream_t st) {
   const unsigned nblk = (unsigned)((MB.npairs + 127) / 128);
   k_records<KIND, false><<<nblk, 128, 0, st>>>(MB);
   k_records<KIND, true><<<nblk, 128, 0, st>>>(MN);
   count_launch(2);
+  if (MS) {
+    k_sing_records<KIND><<<(unsigned)((MS->npairs + 127) / 128), 128, 0, st>>>(*MS, q_sing);
+    count_launch();
+  }
+}
+template <int KIND>
+static void launch_sing_m(const BlockArgs& BA, const MomArgs& MS, int nsteps, cudaStream_t st) {
+  const int chunk = 16;
+  dim3 grid((unsigned)((MS.npairs + 127) / 128), (nsteps + chunk - 1) / chunk);
+  k_sing_m<KIND><<<grid, 128, 0, st>>>(BA, MS, chunk);
+  count_launch();
 }
 
 // time nodes evaluated per entry-level pair by the bulk kernel of one block (host count,
@@ -297,7 +309,7 @@ static long long bulk_nodes(const Block& b, int R) {
 }
 
 bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bulk, int q_sing,
-                           cudaStream_t st) {
+                           int flags, cudaStream_t st) {
   const int ng = m->ng;
   long long* d_poff = nullptr;
   cudaError_t e = cudaMalloc(&d_poff, sizeof(long long) * std::max<size_t>(1, A->poff.size()));
@@ -306,12 +318,19 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bul
   if (e != cudaSuccess) { cudaFree(d_poff); return cuda_fail(e, "assemble/poff copy"); }
   // pair records (bulk order and near orders) and regime counters, stream-ordered
   const long long npairs = (long long)ng * ng;
+  const long long nsrec = 5LL * ng;
   const int nf = kind == STB_D ? rec_fields<STB_D>() : rec_fields<STB_V>();
+  // touching pairs through moment records (regime A) when every touching sub-pair satisfies
+  // c_max / min h_t < 4 with c_max <= alpha (h_X + h_Y)^2 / 4; otherwise the per-lag k_sing
+  const double hpair = (kind == STB_D ? 1.0 : 2.0) * m->hmax;
+  const bool fused_sing = !(flags & BEM_QUAD_LEGACY_SING) &&
+                          0.25 * m->alpha * hpair * hpair / m->htmin < 0.99 * 4.0;
+  A->fused_sing = fused_sing ? 1 : 0;
   double* d_rec = nullptr;
   unsigned long long* d_ctr = nullptr;
-  if ((e = cudaMallocAsync((void**)&d_rec, sizeof(double) * 2 * nf * npairs, st)) != cudaSuccess ||
-      (e = cudaMallocAsync((void**)&d_ctr, sizeof(unsigned long long) * 8, st)) != cudaSuccess ||
-      (e = cudaMemsetAsync(d_ctr, 0, sizeof(unsigned long long) * 8, st)) != cudaSuccess) {
+  if ((e = cudaMallocAsync((void**)&d_rec, sizeof(double) * nf * (2 * npairs + nsrec), st)) != cudaSuccess ||
+      (e = cudaMallocAsync((void**)&d_ctr, sizeof(unsigned long long) * 12, st)) != cudaSuccess ||
+      (e = cudaMemsetAsync(d_ctr, 0, sizeof(unsigned long long) * 12, st)) != cudaSuccess) {
     cudaFree(d_poff);
     return cuda_fail(e, "assemble/records");
   }
@@ -332,10 +351,14 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bul
   MomArgs MN = MB;
   MN.rec = d_rec + (long long)nf * npairs;
   MN.counters = d_ctr + 4;
+  MomArgs MS = MB;
+  MS.rec = d_rec + 2LL * nf * npairs;
+  MS.npairs = nsrec;
+  MS.counters = d_ctr + 8;
   mark();
-  if (kind == STB_V) launch_records<STB_V>(MB, MN, st);
-  else if (kind == STB_K) launch_records<STB_K>(MB, MN, st);
-  else launch_records<STB_D>(MB, MN, st);
+  if (kind == STB_V) launch_records<STB_V>(MB, MN, fused_sing ? &MS : nullptr, q_sing, st);
+  else if (kind == STB_K) launch_records<STB_K>(MB, MN, fused_sing ? &MS : nullptr, q_sing, st);
+  else launch_records<STB_D>(MB, MN, fused_sing ? &MS : nullptr, q_sing, st);
   mark();
   fam.push_back(3);
   A->launches += 2;
@@ -370,21 +393,27 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bul
       else launch_kind<STB_D>(1, BA, MN, ng, chunk, nz, st);
       mark();
       fam.push_back(1);
-      const int ncell = 2 * (blk.a1 - blk.a0);
-      const int per_row = kind == STB_V ? 3 : (kind == STB_K ? 4 : 5);
-      const long long nwarps = (long long)ncell * ng * per_row;
-      const unsigned nblk = (unsigned)((nwarps + 3) / 4);
-      if (kind == STB_V) k_sing<STB_V><<<nblk, 128, 0, st>>>(BA, m->d_seg, m->d_half, m->d_dual, m->d_t, m->alpha, q_sing, nwarps);
-      else if (kind == STB_K) k_sing<STB_K><<<nblk, 128, 0, st>>>(BA, m->d_seg, m->d_half, m->d_dual, m->d_t, m->alpha, q_sing, nwarps);
-      else k_sing<STB_D><<<nblk, 128, 0, st>>>(BA, m->d_seg, m->d_half, m->d_dual, m->d_t, m->alpha, q_sing, nwarps);
-      count_launch();
+      if (fused_sing) {
+        if (kind == STB_V) launch_sing_m<STB_V>(BA, MS, blk.a1 - blk.a0, st);
+        else if (kind == STB_K) launch_sing_m<STB_K>(BA, MS, blk.a1 - blk.a0, st);
+        else launch_sing_m<STB_D>(BA, MS, blk.a1 - blk.a0, st);
+      } else {
+        const int ncell = 2 * (blk.a1 - blk.a0);
+        const int per_row = kind == STB_V ? 3 : (kind == STB_K ? 4 : 5);
+        const long long nwarps = (long long)ncell * ng * per_row;
+        const unsigned nblk = (unsigned)((nwarps + 3) / 4);
+        if (kind == STB_V) k_sing<STB_V><<<nblk, 128, 0, st>>>(BA, m->d_seg, m->d_half, m->d_dual, m->d_t, m->alpha, q_sing, nwarps);
+        else if (kind == STB_K) k_sing<STB_K><<<nblk, 128, 0, st>>>(BA, m->d_seg, m->d_half, m->d_dual, m->d_t, m->alpha, q_sing, nwarps);
+        else k_sing<STB_D><<<nblk, 128, 0, st>>>(BA, m->d_seg, m->d_half, m->d_dual, m->d_t, m->alpha, q_sing, nwarps);
+        count_launch();
+      }
       mark();
       fam.push_back(2);
       A->launches += 2;
     }
   }
   e = cudaGetLastError();
-  unsigned long long ctr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long ctr[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   cudaError_t e2 = cudaMemcpyAsync(ctr, d_ctr, sizeof(ctr), cudaMemcpyDeviceToHost, st);
   cudaFreeAsync(d_rec, st);
   cudaFreeAsync(d_ctr, st);
@@ -414,6 +443,10 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bul
   if (e != cudaSuccess) return cuda_fail(e, "assemble/kernels");
   if (A->ev_bulk != A->nodes_expected) {
     set_error("assemble: bulk node count mismatch");
+    return BEM_E_CUDA;
+  }
+  if (ctr[11] != 0) {
+    set_error("assemble: touching-pair moment record outside regime A (use BEM_QUAD_LEGACY_SING)");
     return BEM_E_CUDA;
   }
   return BEM_OK;

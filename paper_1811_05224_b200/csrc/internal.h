@@ -121,7 +121,7 @@ struct bem_matrix_s {
   long long ev_bulk = 0, ev_near = 0, nodes_expected = 0;
   long long nodes_bulk[4] = {0, 0, 0, 0}, nodes_near[4] = {0, 0, 0, 0};  // regimes A, B, Z, C
   double flops_bulk = 0;
-  int q_bulk = 0, q_sing = 0, launches = 0;
+  int q_bulk = 0, q_sing = 0, launches = 0, fused_sing = 0;
 };
 
 namespace stb {
@@ -141,7 +141,7 @@ bem_status upload_rules();  // copy to __constant__ memory (per device, once)
 
 // kernels (assemble.cu)
 bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bulk, int q_sing,
-                           cudaStream_t st);
+                           int flags, cudaStream_t st);
 // linear algebra (linalg.cu)
 bem_status gemv_setup(bem_matrix* A);
 bem_status gemv_launch(const bem_matrix* A, double a, const double* x, double b, double* y,

@@ -84,6 +84,7 @@ struct MomArgs {
 // NEAR: touching sub-pairs are skipped (k_sing adds them) and the order follows the distance.
 struct SubPair {
   Seg X, Y;
+  int pi, qi, nchain;       // element indices of X and Y in their closed chain of nchain elements
   int q;
   int side;                 // K: 0 = gamma_{n-1} (hat rising), 1 = gamma_n (falling)
   double sa, sb;            // weight scales of the two families
@@ -98,6 +99,9 @@ __device__ __forceinline__ void for_subpairs(const MomArgs& M, int I, int J, Fn&
     if (NEAR && chain_rel(I, J, ng)) return;
     sp.X = M.seg[I];
     sp.Y = M.seg[J];
+    sp.pi = I;
+    sp.qi = J;
+    sp.nchain = ng;
     sp.q = NEAR ? near_order(sp.X, sp.Y, M.qfar) : M.q;
     sp.sa = sp.X.h * sp.Y.h / (4.0 * STB_PI);
     sp.sb = 0.0;
@@ -108,6 +112,9 @@ __device__ __forceinline__ void for_subpairs(const MomArgs& M, int I, int J, Fn&
     for (int side = 0; side < 2; ++side) {
       const int j = side == 0 ? (J - 1 + ng) % ng : J;
       sp.Y = M.seg[j];
+      sp.pi = I;
+      sp.qi = j;
+      sp.nchain = ng;
       if (collinear(sp.X, sp.Y)) continue;
       if (NEAR && chain_rel(I, j, ng)) continue;
       sp.q = NEAR ? near_order(sp.X, sp.Y, M.qfar) : M.q;
@@ -131,6 +138,9 @@ __device__ __forceinline__ void for_subpairs(const MomArgs& M, int I, int J, Fn&
         const int qh = (2 * J - 1 + n + nh) % nh;
         if (NEAR && chain_rel(p, qh, nh)) continue;
         sp.Y = M.half[qh];
+        sp.pi = p;
+        sp.qi = qh;
+        sp.nchain = nh;
         sp.q = NEAR ? near_order(sp.X, sp.Y, M.qfar) : M.q;
         const double dvk = n < 2 ? 1.0 / dk.Lm : -1.0 / dk.Lp;
         sp.k0 = n == 0 ? 0.0 : (n == 1 ? dk.vm : (n == 2 ? 1.0 : dk.vp));
@@ -629,6 +639,170 @@ __global__ void __launch_bounds__(128) k_near_m(BlockArgs B, MomArgs M, int chun
   }
   if (!valid) nA = nB = nZ = nC = 0;
   count_regimes(M.counters, nA, nB, nZ, nC);
+}
+
+// ------------------------------------------------------------- touching sub-pairs (d <= 1)
+// The touching (identical or vertex-sharing) sub-pairs of entry (I, J) with the singular rules
+// of order n: identical elements by the 1-D reduction
+// int int f(|x - y|) = int_0^h f(w) G(w) dw, vertex pairs by the Duffy map at the shared vertex,
+// the logarithm split as ln c = lnA + 2 ln rho with the ln rho part on log-weighted Gauss rules:
+//   int W F(c)       = sum wa F(c)
+//   int W F(c) ln c  = sum [wa lnA + 2 wla] F(c)
+// vis(c, lnA, wa, wb, wla, wlb) for the two families (weights include the kernel prefactors).
+__device__ __forceinline__ double lin1(double v0, double v1, double f) { return fma(v1 - v0, f, v0); }
+
+template <int KIND, class Vis>
+__device__ __forceinline__ void for_touch_points(const MomArgs& M, int I, int J, int n, Vis&& vis) {
+  const double alpha = M.alpha;
+  for_subpairs<KIND, false>(M, I, J, [&](const SubPair& sp) {
+    const int rel = chain_rel(sp.pi, sp.qi, sp.nchain);
+    if (!rel) return;
+    const Seg &X = sp.X, &Y = sp.Y;
+    const double hh = X.h * Y.h;
+    const double wsa = sp.sa / hh, wsb = sp.sb / hh;
+    // shapes on X and Y of family a (K: the primal hat on Y) and family b (D normal: psi_l, psi_k)
+    const double ax0 = 1.0, ax1 = 1.0;
+    const double ay0 = KIND == STB_K ? (sp.side == 0 ? 0.0 : 1.0) : 1.0;
+    const double ay1 = KIND == STB_K ? (sp.side == 0 ? 1.0 : 0.0) : 1.0;
+    const double bx0 = sp.l0, bx1 = sp.l1, by0 = sp.k0, by1 = sp.k1;
+    if (rel == 1) {
+      if (KIND == STB_K) return;  // dot = 0 on a straight element
+      const double h = X.h;
+      const double L0 = log(0.25 * alpha) + 2.0 * log(h);
+      for (int k = 0; k < n; ++k) {
+        const double rho = c_gx[n][k], w = h * rho, len = h - w;
+        // G(w) = int_0^{h-w} [Sx(v+w) Sy(v) + Sx(v) Sy(v+w)] dv (quadratic: 2-point Gauss exact)
+        double Ga = 0.0, Gb = 0.0;
+        for (int r = 0; r < 2; ++r) {
+          const double v = len * c_gx[2][r];
+          Ga += c_gw[2][r] * (lin1(ax0, ax1, (v + w) / h) * lin1(ay0, ay1, v / h) +
+                              lin1(ax0, ax1, v / h) * lin1(ay0, ay1, (v + w) / h));
+          if (KIND == STB_D)
+            Gb += c_gw[2][r] * (lin1(bx0, bx1, (v + w) / h) * lin1(by0, by1, v / h) +
+                                lin1(bx0, bx1, v / h) * lin1(by0, by1, (v + w) / h));
+        }
+        Ga *= len * h * wsa;
+        Gb *= len * h * wsb;
+        vis(0.25 * alpha * w * w, L0, Ga * c_gw[n][k], Gb * c_gw[n][k], Ga * c_glw[n][k], Gb * c_glw[n][k]);
+      }
+    } else {
+      const double h1 = X.h, h2 = Y.h;
+      double e1x, e1y, e2x, e2y;
+      double axV, axF, ayV, ayF, bxV, bxF, byV, byF;
+      if (rel == 2) {   // X.end == Y.start
+        e1x = -X.tx; e1y = -X.ty; e2x = Y.tx; e2y = Y.ty;
+        axV = ax1; axF = ax0; ayV = ay0; ayF = ay1;
+        bxV = bx1; bxF = bx0; byV = by0; byF = by1;
+      } else {          // X.start == Y.end
+        e1x = X.tx; e1y = X.ty; e2x = -Y.tx; e2y = -Y.ty;
+        axV = ax0; axF = ax1; ayV = ay1; ayF = ay0;
+        bxV = bx0; bxF = bx1; byV = by1; byF = by0;
+      }
+      const double cth = e1x * e2x + e1y * e2y;
+      const double e1n = e1x * Y.nx + e1y * Y.ny;
+      for (int tri = 0; tri < 2; ++tri)
+        for (int ie = 0; ie < n; ++ie)
+          for (int ir = 0; ir < n; ++ir) {
+            const double eta = c_gx[n][ie], rho = c_gx[n][ir];
+            const double A = tri == 0 ? (h1 * h1 + h2 * h2 * eta * eta - 2.0 * h1 * h2 * eta * cth)
+                                      : (h1 * h1 * eta * eta + h2 * h2 - 2.0 * h1 * h2 * eta * cth);
+            const double u = tri == 0 ? h1 * rho : h1 * rho * eta;
+            const double v = tri == 0 ? h2 * rho * eta : h2 * rho;
+            const double jac = h1 * h2 * rho;
+            double fa = lin1(axV, axF, u / h1) * lin1(ayV, ayF, v / h2) * jac * wsa;
+            if (KIND == STB_K) fa *= u * e1n;   // (x - y).n_y = u e1.n_y at the shared vertex
+            const double fb = KIND == STB_D ? lin1(bxV, bxF, u / h1) * lin1(byV, byF, v / h2) * jac * wsb : 0.0;
+            const double wr = c_gw[n][ie] * c_gw[n][ir], wl = c_gw[n][ie] * c_glw[n][ir];
+            vis(0.25 * alpha * rho * rho * A, log(0.25 * alpha * A), fa * wr, fb * wr, fa * wl, fb * wl);
+          }
+    }
+  });
+}
+
+// sing records: entry-level pairs (I, J = I + jo - 2), jo = 0..4, with touching sub-pairs; the
+// touching parts only, regime-A data and the affine constants (same layout as the pair records)
+template <int KIND>
+__global__ void __launch_bounds__(128) k_sing_records(MomArgs M, int nsing) {
+  const long long rid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (rid >= M.npairs) return;
+  const int I = (int)(rid / 5), jo = (int)(rid % 5);
+  const int J = (I + jo - 2 + M.ng) % M.ng;
+  double* rec = M.rec + rid;
+  const long long S = M.npairs;
+  double cmax = 0.0;
+  for_touch_points<KIND>(M, I, J, nsing, [&](double c, double, double, double, double, double) {
+    cmax = fmax(cmax, c);
+  });
+  rec[RF_CMAX * S] = cmax;
+  rec[RF_CMIN * S] = 0.0;
+  rec[RF_C0 * S] = 0.0;
+  rec[RF_KB * S] = 0.0;
+#pragma unroll 1
+  for (int slot = 0; slot < Fams<KIND>::n; ++slot) {
+    const int fam = slot == 0 ? Fams<KIND>::f0 : Fams<KIND>::f1;
+    double* R = rec + (RF_COMMON + slot * FAMSZ) * S;
+    double mk[MKA + 1];
+#pragma unroll
+    for (int k = 0; k <= MKA; ++k) mk[k] = 0.0;
+    double C0 = 0.0, C1 = 0.0;
+    for_touch_points<KIND>(M, I, J, nsing, [&](double c, double lnA, double wa, double wb, double wla, double wlb) {
+      const double w = slot == 0 ? wa : wb, wl = slot == 0 ? wla : wlb;
+      double pw = w;
+#pragma unroll
+      for (int k = 0; k <= MKA; ++k) {
+        mk[k] += pw;
+        pw *= c;
+      }
+      // int W (gamma + ln c) and int W c (gamma + ln c); Q: int W / c (regular after Duffy)
+      const double wlog = fma(w, STB_GAMMA + lnA, 2.0 * wl);
+      C0 += wlog;
+      C1 += fam == FAM_Q ? w / c : wlog * c;
+    });
+#pragma unroll
+    for (int k = 0; k <= MKA; ++k) R[(FA + k) * S] = mpoly(fam, k) * mk[k];
+    R[FM0 * S] = mk[0];
+    R[FM1 * S] = mk[1];
+#pragma unroll
+    for (int k = 0; k <= MKB; ++k) R[(FB + k) * S] = 0.0;
+    R[FC0 * S] = C0;
+    R[FC1 * S] = C1;
+  }
+}
+
+// touching contributions to the near cells, added onto the near-kernel values: thread = (sing
+// record, chunk of test steps); regime A only (the host checks c_max / min lag < 4 before it
+// chooses this path; a violation is counted in counters[3] and fails the assembly)
+template <int KIND>
+__global__ void __launch_bounds__(128) k_sing_m(BlockArgs B, MomArgs M, int chunk) {
+  const long long rid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (rid >= M.npairs) return;
+  const int I = (int)(rid / 5), jo = (int)(rid % 5);
+  if ((KIND == STB_V && (jo == 0 || jo == 4)) || (KIND == STB_K && jo == 0)) return;
+  const int J = (I + jo - 2 + M.ng) % M.ng;
+  const int a_beg = B.a0 + blockIdx.y * chunk;
+  const int a_end = min(B.a1, a_beg + chunk);
+  const long long S = M.npairs;
+  const double* rec = M.rec + rid;
+  RegA<KIND> A;
+  A.load(rec, S);
+  unsigned long long bad = 0;
+  auto node = [&](int x, int y) -> double {
+    const double4 nd = B.lag[x * B.ldlag + y];
+    bad += !(A.cmax * nd.z < STB_MXA);
+    return A.eval(nd.x, nd.y, nd.z) - affine_part<KIND>(rec, S, nd.x);
+  };
+  double prev = 0.0;
+  if (a_beg < a_end && a_beg >= 1 && a_beg - 1 >= B.b0 && a_beg - 1 < B.b1) prev = node(a_beg, a_beg - 1);
+#pragma unroll 1
+  for (int a = a_beg; a < a_end; ++a) {
+    const bool d0 = a >= B.b0 && a < B.b1, d1 = a - 1 >= B.b0 && a - 1 < B.b1;
+    double p10 = 0.0;
+    if (d0 || d1) p10 = node(a + 1, a);
+    if (d0) *entry_ptr(B, a, I, a, J) += p10;
+    if (d1) *entry_ptr(B, a, I, a - 1, J) += node(a + 1, a - 1) - prev - p10;
+    prev = p10;
+  }
+  if (bad && M.counters) atomicAdd(M.counters + 3, bad);
 }
 
 }  // namespace stb

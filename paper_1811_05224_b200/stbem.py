@@ -57,13 +57,16 @@ class SolveReport(ctypes.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+QUAD_LEGACY_SING = 1   # bem_quad_opts.flags: touching pairs by the per-lag singular kernel
+
+
 class AssemblyStats(ctypes.Structure):
     _fields_ = [("ms_bulk", ctypes.c_double), ("ms_near", ctypes.c_double), ("ms_sing", ctypes.c_double),
                 ("evals_bulk", ctypes.c_longlong), ("evals_near", ctypes.c_longlong),
                 ("q_bulk", ctypes.c_int), ("q_sing", ctypes.c_int), ("launches", ctypes.c_int),
                 ("entries", ctypes.c_longlong), ("flops_bulk", ctypes.c_double),
                 ("ms_records", ctypes.c_double), ("nodes_bulk", ctypes.c_longlong * 4),
-                ("nodes_near", ctypes.c_longlong * 4)]
+                ("nodes_near", ctypes.c_longlong * 4), ("fused_sing", ctypes.c_int)]
 
     def as_dict(self):
         out = {}
@@ -240,8 +243,8 @@ class Mesh:
         except Exception:
             pass
 
-    def _assemble(self, fn, q_bulk=0, q_sing=0, stream=None):
-        o = QuadOpts(q_bulk, q_sing, 0)
+    def _assemble(self, fn, q_bulk=0, q_sing=0, legacy_sing=False, stream=None):
+        o = QuadOpts(q_bulk, q_sing, QUAD_LEGACY_SING if legacy_sing else 0)
         h = ctypes.c_void_p()
         check(fn(self.h, ctypes.byref(o), _stream(stream), ctypes.byref(h)))
         return Matrix(h, self)

@@ -234,3 +234,18 @@ def test_gmres_c2_against_golden(precond):
     wv, rep = solve("C2", precond, 1e-10)
     assert rep["converged"] and rep["iterations"] <= 30, rep
     assert relmax(wv, wd) <= W_TOL
+
+
+@pytest.mark.parametrize("name", ["T8", "LT"])
+def test_touching_pairs_both_paths(name):
+    """touching pairs through moment records (default where alpha (h_X+h_Y)^2 / (4 min h_t) < 4)
+    and through the per-lag singular kernel (BEM_QUAD_LEGACY_SING) agree with the oracle"""
+    w = W.get(name)
+    m = S.Mesh.from_workload(w)
+    for kind in "VKD":
+        ref = oracle_dense(name, kind)
+        fused = getattr(m, f"assemble_{kind}")()
+        legacy = getattr(m, f"assemble_{kind}")(legacy_sing=True)
+        assert fused.stats()["fused_sing"] == 1 and legacy.stats()["fused_sing"] == 0
+        for A in (fused, legacy):
+            assert relmax(A.dense(), ref) <= MAT_TOL, (kind, relmax(A.dense(), ref))
