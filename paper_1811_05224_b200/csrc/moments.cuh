@@ -36,9 +36,11 @@ constexpr int MKB = 32;          // regime-B maximum Taylor order
 constexpr double MRHO = 0.3;     // regime-B cluster bound (c_max - c0 <= MRHO c0)
 constexpr double MXZ = 50.0;     // regime Z threshold on x_min
 // record layout (field-major, stride npairs): common fields, then one block per family
-enum { RF_CMAX = 0, RF_CMIN = 1, RF_C0 = 2, RF_KB = 3, RF_COMMON = 4 };
-enum { FA = 0, FM0 = MKA + 1, FM1 = MKA + 2, FB = MKA + 3, FC0 = MKA + MKB + 4, FC1 = MKA + MKB + 5,
-       FAMSZ = MKA + MKB + 6 };
+enum { RF_CMAX = 0, RF_CMIN = 1, RF_C0 = 2, RF_KB = 3, RF_IC0 = 4, RF_COMMON = 5 };
+// per family: A[0..MKA] = poly_k M_k, M0, M1, the regime-B arrays B1, B2 (scaled shifted
+// moments, see phi_bz), the affine constants C0, C1
+enum { FA = 0, FM0 = MKA + 1, FM1 = MKA + 2, FB1 = MKA + 3, FB2 = FB1 + MKB + 1, FC0 = FB2 + MKB + 1,
+       FC1 = FC0 + 1, FAMSZ = FC1 + 1 };
 enum { FAM_H = 0, FAM_F = 1, FAM_Q = 2 };
 
 template <int KIND> struct Fams;
@@ -52,6 +54,8 @@ static __device__ __constant__ const double STB_INV[MKB + 2] = {
     1.0 / 9,  1.0 / 10, 1.0 / 11, 1.0 / 12, 1.0 / 13, 1.0 / 14, 1.0 / 15, 1.0 / 16, 1.0 / 17,
     1.0 / 18, 1.0 / 19, 1.0 / 20, 1.0 / 21, 1.0 / 22, 1.0 / 23, 1.0 / 24, 1.0 / 25, 1.0 / 26,
     1.0 / 27, 1.0 / 28, 1.0 / 29, 1.0 / 30, 1.0 / 31, 1.0 / 32, 1.0 / 33};
+
+#define STB_INV_H STB_INV
 
 __device__ __forceinline__ double mpoly(int fam, int k) {
   if (fam == FAM_H) return STB_MGH[k];
@@ -232,6 +236,7 @@ __global__ void __launch_bounds__(128) k_records(MomArgs M) {
   rec[RF_CMIN * S] = cmin;
   rec[RF_C0 * S] = c0;
   rec[RF_KB * S] = (double)kb;
+  rec[RF_IC0 * S] = okB ? 1.0 / c0 : 0.0;
 #pragma unroll 1
   for (int slot = 0; slot < Fams<KIND>::n; ++slot) {
     const int fam = slot == 0 ? Fams<KIND>::f0 : Fams<KIND>::f1;
@@ -270,7 +275,11 @@ __global__ void __launch_bounds__(128) k_records(MomArgs M) {
       });
     }
 #pragma unroll
-    for (int k = 0; k <= MKB; ++k) R[(FB + k) * S] = mb[k];
+    for (int k = 0; k <= MKB; ++k) {
+      // B1[k] = m_k / k (B1[0] = m_0); B2: H m_k / ((k-1) k) (B2[1] = m_1), Q m_k, F unused
+      R[(FB1 + k) * S] = k == 0 ? mb[0] : mb[k] * STB_INV_H[k];
+      R[(FB2 + k) * S] = fam == FAM_Q ? mb[k] : (fam == FAM_H ? (k == 0 ? 0.0 : (k == 1 ? mb[1] : mb[k] * STB_INV_H[k - 1] * STB_INV_H[k])) : 0.0);
+    }
     // affine constants (all points at c > 0)
     double C0 = 0.0, C1 = 0.0;
     if (cmin > 0.0) {
@@ -344,73 +353,85 @@ __device__ __forceinline__ double pt_q(double c, double s, double lns, double u)
   return k - s / c - (STB_GAMMA + log(c));
 }
 
-// regimes B and Z (out of line: rare); *regime = 1 (B), 2 (Z) or 3 (C: not evaluated here)
+// regimes B and Z (out of line: rare); *regime = 1 (B), 2 (Z) or 3 (C: not evaluated here).
+// Regime B in scaled form (x0 = c0 u): e^_j = u^j e_j = e^{-x0} (-u)^j / j!,
+// a^_j = u^{j+1} a_j = (e^_j - a^_{j-1}) / c0 (Taylor coefficients a_j of e^{-x}/x at x0), so that
+//   F: sum_k c_k u^k m_k = E1 m_0 - S1
+//   H: ... = h(x0) m_0 + E1 u m_1 - S1 - u S2
+//   Q: ... = -E1 m_0 + (a^_0 m_0 + S3) / u + S1
+// with S1 = sum_{k>=1} a^_{k-1} B1[k], S2 = sum_{k>=2} a^_{k-2} B2[k], S3 = sum_{k>=1} a^_k B2[k]
+// (B1[k] = m_k / k; H: B2[k] = m_k / ((k-1) k); Q: B2[k] = m_k): two multiplies for e^, one
+// add and one multiply for a^, one FMA per family sum.
+// per-lane constants of regimes B and Z, loaded once per thread
 template <int KIND>
-__device__ __noinline__ double phi_bz(const MomArgs M, long long pair, double s, double u, int* regime) {
-  const long long S = M.npairs;
-  const double* rec = M.rec + pair;
-  const double cmin = rec[RF_CMIN * S], c0 = rec[RF_C0 * S];
-  const bool zz = cmin > 0.0 && cmin * u >= MXZ;
-  if (!zz && !(c0 > 0.0)) {
+struct RegBZ {
+  double c0, ic0, cmin;
+  int kb;
+  double m0[Fams<KIND>::n], m1, C0[Fams<KIND>::n], C1[Fams<KIND>::n];
+  __device__ __forceinline__ void load(const double* __restrict__ rec, long long S) {
+    c0 = rec[RF_C0 * S];
+    ic0 = rec[RF_IC0 * S];
+    cmin = rec[RF_CMIN * S];
+    kb = (int)rec[RF_KB * S];
+#pragma unroll
+    for (int f = 0; f < Fams<KIND>::n; ++f) {
+      const double* R = rec + (RF_COMMON + f * FAMSZ) * S;
+      m0[f] = R[FB1 * S];
+      C0[f] = R[FC0 * S];
+      C1[f] = R[FC1 * S];
+    }
+    m1 = rec[(RF_COMMON + FB2 + 1) * S];   // H: m_1 (B2[1])
+  }
+};
+
+template <int KIND>
+__device__ __forceinline__ double phi_bz(const double* __restrict__ rec, long long S, const RegBZ<KIND>& z,
+                                         double s, double u, int* regime) {
+  const bool zz = z.cmin > 0.0 && z.cmin * u >= MXZ;
+  if (!zz && !(z.c0 > 0.0)) {
     *regime = 3;
     return 0.0;
   }
   double T[2] = {0.0, 0.0};
   if (!zz) {
-    // Taylor coefficients at x0 of e^{-x}/x: a_j = (e_j - a_{j-1}) / x0, e_j = e^{-x0}(-1)^j/j!
-    const int kb = (int)rec[RF_KB * S];
-    const double x0 = c0 * u, ix0 = 1.0 / x0, ex = exp(-x0);
-    const double E1 = x0 < STB_XSPLIT ? ein_poly(x0) - (STB_GAMMA + log(x0)) : e1_large(ix0, ex);
-    double ej = ex, am2 = 0.0, am1 = ex * ix0;  // a_{k-2}, a_{k-1} at k = 1
-    double upk = 1.0;
-    double acc0 = 0.0, acc1 = 0.0;
-#pragma unroll 1
-    for (int k = 0; k <= kb; ++k) {
-      double c_0 = 0.0, c_1 = 0.0;   // coefficient of u^k m_k for the two families
-      double ak = 0.0;               // a_k (k >= 1)
-      if (k >= 1) {
-        ej = -ej * STB_INV[k];
-        ak = (ej - am1) * ix0;
-      }
-#pragma unroll
-      for (int f = 0; f < Fams<KIND>::n; ++f) {
-        const int fam = f == 0 ? Fams<KIND>::f0 : Fams<KIND>::f1;
-        double cf;
-        if (fam == FAM_H) {
-          // h(x0+d) = h(x0) + h'(x0) d + sum_{j>=0} b_j d^{j+2} / ((j+1)(j+2)), b_j = -(j+1)a_{j+1} - a_j
-          if (k == 0) cf = fma(1.0 + x0, E1, -ex);
-          else if (k == 1) cf = E1 - am1;
-          else cf = (-(k - 1) * am1 - am2) * (STB_INV[k - 1] * STB_INV[k]);
-        } else if (fam == FAM_F) {
-          cf = k == 0 ? E1 : -am1 * STB_INV[k];               // E1' = -e^{-x}/x
-        } else {
-          // (e^{-x}/x - E1)' = -e^{-x}/x^2: coefficient -b_{k-1}/k
-          cf = k == 0 ? am1 - E1 : fma(k, ak, am1) * STB_INV[k];
-        }
-        if (f == 0) c_0 = cf; else c_1 = cf;
-      }
-      const double* R0 = rec + (RF_COMMON + FB + k) * S;
-      acc0 = fma(c_0 * upk, R0[0], acc0);
-      if (Fams<KIND>::n == 2) acc1 = fma(c_1 * upk, R0[FAMSZ * S], acc1);
-      upk *= u;
-      if (k >= 1) {
-        am2 = am1;
-        am1 = ak;
-      }
+    // x0 = c0 u >= 4 / (1 + MRHO) > 3: E1(x0) = e^{-x0} t GB3(t), t = 1/x0 = s / c0
+    const double x0 = z.c0 * u, ic0 = z.ic0, ex = exp(-x0);
+    const double E1 = ex * (ic0 * s) * gb3_poly(ic0 * s);
+    const double* R0 = rec + (RF_COMMON + 0 * FAMSZ) * S;
+    const double* R1 = rec + (RF_COMMON + 1 * FAMSZ) * S;
+    double e = ex, ap = ex * ic0, app = 0.0;        // e^_{k-1}, a^_{k-1}, a^_{k-2}
+    const double a0 = ap;
+    double S1a = 0.0, S2a = 0.0, S1b = 0.0;
+    const double* p1 = R0 + (FB1 + 1) * S;
+    const double* p2 = R0 + (FB2 + 1) * S;
+    const double* p3 = R1 + (FB1 + 1) * S;
+#pragma unroll 2
+    for (int k = 1; k <= z.kb; ++k) {
+      e = -e * (u * STB_INV[k]);
+      const double ak = (e - ap) * ic0;
+      S1a = fma(ap, *p1, S1a);
+      if (Fams<KIND>::f0 == FAM_H) S2a = fma(app, *p2, S2a);
+      else S2a = fma(ak, *p2, S2a);   // Q: S3
+      if (Fams<KIND>::n == 2) S1b = fma(ap, *p3, S1b);
+      p1 += S;
+      p2 += S;
+      p3 += S;
+      app = ap;
+      ap = ak;
     }
-    T[0] = acc0;
-    T[1] = acc1;
+    const double m0 = z.m0[0];
+    if (Fams<KIND>::f0 == FAM_H) T[0] = fma(fma(1.0 + x0, E1, -ex), m0, fma(E1 * u, z.m1, -fma(u, S2a, S1a)));
+    else T[0] = fma(-E1, m0, fma(a0, m0, S2a) / u + S1a);
+    if (Fams<KIND>::n == 2) T[1] = fma(E1, z.m0[1], -S1b);
   }
   *regime = zz ? 2 : 1;
   double out = 0.0;
 #pragma unroll
   for (int f = 0; f < Fams<KIND>::n; ++f) {
     const int fam = f == 0 ? Fams<KIND>::f0 : Fams<KIND>::f1;
-    const double* R = rec + (RF_COMMON + f * FAMSZ) * S;
-    const double C0 = R[FC0 * S], C1 = R[FC1 * S];
-    if (fam == FAM_H) out += fma(s, T[f] + C0, C1);
-    else if (fam == FAM_F) out += T[f] + C0;
-    else out += T[f] - fma(s, C1, C0);
+    if (fam == FAM_H) out += fma(s, T[f] + z.C0[f], z.C1[f]);
+    else if (fam == FAM_F) out += T[f] + z.C0[f];
+    else out += T[f] - fma(s, z.C1[f], z.C0[f]);
   }
   return out;
 }
@@ -492,50 +513,59 @@ __global__ void __launch_bounds__(128) k_bulk_m(BlockArgs B, MomArgs M) {
   if (bmax < B.b0) return;                        // CTA-uniform
   const long long pair = (long long)I * ng + J;
   const long long S = M.npairs;
+  // row offsets of the band rows a = r_lo + r for this warp's row I (panel offset + I * ld),
+  // shared by the warp: a store is then one LDS + one address add
+  __shared__ long long s_row[4][R];
+  long long* srow = s_row[threadIdx.x >> 5];
+  if (lane < R) {
+    const int a = min(r_lo + lane, r_hi - 1);
+    srow[lane] = B.poff[a - B.a0] + (long long)I * pad4((long long)panel_nb(a, B.b0, B.b1) * ng);
+  }
+  __syncwarp();
   RegA<KIND> A;
   A.load(M.rec + pair, S);
+  RegBZ<KIND> Z;
+  Z.load(M.rec + pair, S);
   unsigned long long nA = 0, nB = 0, nZ = 0, nC = 0;
   double Gp[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) Gp[r] = 0.0;
   for (int y = B.b0; y <= bmax + 1; ++y) {
+    // every node of the column by the regime-A form, branch-free (clamped into the lag table,
+    // invalid nodes zeroed) so that the R+1 Horner chains interleave; then the nodes of lanes
+    // outside regime A are overwritten (B / Z per lane, C warp-cooperatively)
     double phi[R + 1];
-    const int xf = max(r_lo, y + 1);
-    const double umax = B.lag[xf * B.ldlag + y].z;
-    if (__all_sync(0xffffffffu, A.cmax * umax < STB_MXA)) {
+    double4 nd[R + 1];
 #pragma unroll
-      for (int r = 0; r <= R; ++r) {
-        const int x = r_lo + r;
-        phi[r] = 0.0;
-        if (x <= r_hi && x > y) {
-          const double4 nd = B.lag[x * B.ldlag + y];
-          phi[r] = A.eval(nd.x, nd.y, nd.z);
-          ++nA;
-        }
-      }
-    } else {
+    for (int r = 0; r <= R; ++r) nd[r] = B.lag[min(r_lo + r, r_hi) * B.ldlag + y];
+    unsigned bmask = 0;
+#pragma unroll
+    for (int r = 0; r <= R; ++r) {
+      const int x = r_lo + r;
+      const double v = A.eval(nd[r].x, nd[r].y, nd[r].z);
+      const bool ok = x <= r_hi && x > y;
+      const bool inA = A.cmax * nd[r].z < STB_MXA;
+      phi[r] = ok ? v : 0.0;
+      nA += ok && inA;
+      if (ok && !inA) bmask |= 1u << r;
+    }
+    if (__any_sync(0xffffffffu, bmask != 0)) {
       unsigned cmask = 0;   // nodes r of this lane left to regime C
-#pragma unroll
-      for (int r = 0; r <= R; ++r) {
-        const int x = r_lo + r;
-        double v = 0.0;
-        if (x <= r_hi && x > y) {
-          const double4 nd = B.lag[x * B.ldlag + y];
-          if (A.cmax * nd.z < STB_MXA) {
-            v = A.eval(nd.x, nd.y, nd.z);
-            ++nA;
-          } else {
-            int reg = 0;
-            v = phi_bz<KIND>(M, pair, nd.x, nd.z, &reg);
-            nB += reg == 1;
-            nZ += reg == 2;
-            if (reg == 3) {
-              cmask |= 1u << r;
-              ++nC;
-            }
-          }
+      while (bmask) {
+        const int r = __ffs(bmask) - 1;
+        bmask &= bmask - 1;
+        const double4 q = B.lag[(r_lo + r) * B.ldlag + y];
+        int reg = 0;
+        const double v = phi_bz<KIND>(M.rec + pair, S, Z, q.x, q.z, &reg);
+        nB += reg == 1;
+        nZ += reg == 2;
+        if (reg == 3) {
+          cmask |= 1u << r;
+          ++nC;
         }
-        phi[r] = v;
+#pragma unroll
+        for (int rr = 0; rr <= R; ++rr)
+          if (rr == r) phi[rr] = v;
       }
       unsigned lanes = __ballot_sync(0xffffffffu, cmask != 0);
       while (lanes) {                                   // warp-uniform
@@ -546,8 +576,8 @@ __global__ void __launch_bounds__(128) k_bulk_m(BlockArgs B, MomArgs M) {
         while (cm) {
           const int r = __ffs(cm) - 1;
           cm &= cm - 1;
-          const double4 nd = B.lag[(r_lo + r) * B.ldlag + y];
-          const double v = phi_c_warp<KIND, false>(M, Is, Js, nd.x, nd.y, nd.z);
+          const double4 q = B.lag[(r_lo + r) * B.ldlag + y];
+          const double v = phi_c_warp<KIND, false>(M, Is, Js, q.x, q.y, q.z);
           if (lane == src) {
 #pragma unroll
             for (int rr = 0; rr <= R; ++rr)
@@ -558,11 +588,12 @@ __global__ void __launch_bounds__(128) k_bulk_m(BlockArgs B, MomArgs M) {
     }
     if (y > B.b0) {
       const int b = y - 1;
+      double* col = B.out + ((long long)(b - B.b0) * ng + J);
 #pragma unroll
       for (int r = 1; r <= R; ++r) {
         const int a = r_lo + r - 1;
         const double G = phi[r] - phi[r - 1];
-        if (valid && a < r_hi && a - b >= 2) *entry_ptr(B, a, I, b, J) = Gp[r - 1] - G;
+        if (valid && a < r_hi && a - b >= 2) col[srow[r - 1]] = Gp[r - 1] - G;
         Gp[r - 1] = G;
       }
     } else {
@@ -594,6 +625,8 @@ __global__ void __launch_bounds__(128) k_near_m(BlockArgs B, MomArgs M, int chun
   const double* rec = M.rec + pair;
   RegA<KIND> A;
   A.load(rec, S);
+  RegBZ<KIND> Z;
+  Z.load(rec, S);
   unsigned long long nA = 0, nB = 0, nZ = 0, nC = 0;
   // node value for every lane (warp-uniform call: regime C is computed cooperatively)
   auto node = [&](int x, int y) -> double {
@@ -605,7 +638,7 @@ __global__ void __launch_bounds__(128) k_near_m(BlockArgs B, MomArgs M, int chun
       ++nA;
     } else {
       int reg = 0;
-      v = phi_bz<KIND>(M, pair, nd.x, nd.z, &reg);
+      v = phi_bz<KIND>(rec, S, Z, nd.x, nd.z, &reg);
       nB += reg == 1;
       nZ += reg == 2;
       if (reg == 3) {
@@ -737,6 +770,7 @@ __global__ void __launch_bounds__(128) k_sing_records(MomArgs M, int nsing) {
   rec[RF_CMIN * S] = 0.0;
   rec[RF_C0 * S] = 0.0;
   rec[RF_KB * S] = 0.0;
+  rec[RF_IC0 * S] = 0.0;
 #pragma unroll 1
   for (int slot = 0; slot < Fams<KIND>::n; ++slot) {
     const int fam = slot == 0 ? Fams<KIND>::f0 : Fams<KIND>::f1;
@@ -763,7 +797,7 @@ __global__ void __launch_bounds__(128) k_sing_records(MomArgs M, int nsing) {
     R[FM0 * S] = mk[0];
     R[FM1 * S] = mk[1];
 #pragma unroll
-    for (int k = 0; k <= MKB; ++k) R[(FB + k) * S] = 0.0;
+    for (int k = 0; k <= MKB; ++k) R[(FB1 + k) * S] = R[(FB2 + k) * S] = 0.0;
     R[FC0 * S] = C0;
     R[FC1 * S] = C1;
   }
