@@ -41,15 +41,27 @@ __global__ void __launch_bounds__(GEMV_WARPS * 32) k_gemv(const double* __restri
     const double* __restrict__ row = A + S.off + (long long)i * S.ld + col0;
     const double* __restrict__ xx = x + S.xoff + col0;
     double acc0 = 0.0, acc1 = 0.0;
-    // rows are 32-byte aligned (padded stride, aligned panel offsets); x is read as doubles
+    // rows are 32-byte aligned (padded stride, aligned panel offsets) and x offsets are even
+    // (b0 * ng + c * GEMV_CH, ng even; odd ng falls back to scalar x loads): A and x as double2
     const int nv = len / 2;
     const double2* __restrict__ row2 = reinterpret_cast<const double2*>(row);
     int k = lane;
+    if ((((size_t)xx) & 15) == 0) {
+      const double2* __restrict__ x2 = reinterpret_cast<const double2*>(xx);
 #pragma unroll 4
-    for (; k < nv; k += 32) {
-      const double2 av = __ldcs(row2 + k);   // streamed once: evict-first
-      acc0 = fma(av.x, __ldg(xx + 2 * k), acc0);
-      acc1 = fma(av.y, __ldg(xx + 2 * k + 1), acc1);
+      for (; k < nv; k += 32) {
+        const double2 av = __ldcs(row2 + k);   // streamed once: evict-first
+        const double2 xv = __ldg(x2 + k);
+        acc0 = fma(av.x, xv.x, acc0);
+        acc1 = fma(av.y, xv.y, acc1);
+      }
+    } else {
+#pragma unroll 4
+      for (; k < nv; k += 32) {
+        const double2 av = __ldcs(row2 + k);
+        acc0 = fma(av.x, __ldg(xx + 2 * k), acc0);
+        acc1 = fma(av.y, __ldg(xx + 2 * k + 1), acc1);
+      }
     }
     if ((len & 1) && lane == 0) acc0 = fma(__ldcs(row + len - 1), __ldg(xx + len - 1), acc0);
     double acc = acc0 + acc1;
@@ -154,12 +166,25 @@ static int num_sms() {
   return g_num_sms;
 }
 
+// persistent grid: exactly the CTAs that are resident at once (a second partial wave of a
+// grid-stride kernel would run at reduced occupancy)
+static int g_gemv_ctas_per_sm = 0;
+static int gemv_ctas_per_sm() {
+  if (!g_gemv_ctas_per_sm) {
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_gemv, GEMV_WARPS * 32, 0) != cudaSuccess || n <= 0) n = 4;
+    g_gemv_ctas_per_sm = n;
+  }
+  return g_gemv_ctas_per_sm;
+}
+
 bem_status gemv_launch(const bem_matrix* A, double a, const double* x, double b, double* y,
                        cudaStream_t st) {
   const bem_mesh* m = A->mesh;
   const long long n = (long long)m->ng * m->nt;
   if (A->n_items > 0) {
-    long long blocks = std::min<long long>((A->n_items + GEMV_WARPS - 1) / GEMV_WARPS, (long long)num_sms() * 8);
+    long long blocks = std::min<long long>((A->n_items + GEMV_WARPS - 1) / GEMV_WARPS,
+                                           (long long)num_sms() * gemv_ctas_per_sm());
     k_gemv<<<(unsigned)blocks, GEMV_WARPS * 32, 0, st>>>(A->data, A->d_segs, (int)A->segs.size(), A->n_items, m->ng, x, A->d_partials);
     count_launch();
   }
