@@ -199,8 +199,11 @@ def native(args):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     phases, reps, stats = [], [], None
+    step_wall = []
     for _ in range(args.steps):
+        t_s = time.perf_counter()
         ph, rep, stats, info = step(False)
+        step_wall.append(1e3 * (time.perf_counter() - t_s))
         phases.append(ph)
         reps.append(rep)
     e1.record()
@@ -212,8 +215,11 @@ def native(args):
     barrier()
     e2 = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     e2[0].record()
+    e2e_wall = []
     for _ in range(args.steps):
+        t_s = time.perf_counter()
         step(True)
+        e2e_wall.append(1e3 * (time.perf_counter() - t_s))
     e2[1].record()
     barrier()
     t_e2e = e2[0].elapsed_time(e2[1]) / 1e3
@@ -237,20 +243,44 @@ def native(args):
     peaks = json.load(open(PEAKS_PATH)) if os.path.exists(PEAKS_PATH) else {}
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     gemv_gbs = bytes_per_gemv / gemv_s / 1e9 if gemv_s > 0 else None
-    # dominant kernel: the longest assembly kernel family of the step
+    # assembly roofline: the longest bulk kernel (k_bulk_m<KIND>), FP64 flops from the exact
+    # per-regime node counts x the static FP64 counts of the shipped forms,
+    # and its store stream (8 B per stored entry)
     fam = []
     for k in "VKD":
         st = stats[k]
         fam.append((st["ms_bulk"], k, "bulk", st))
     ms_dom, kdom, _, st = max(fam)
     flops = st["flops_bulk"]
-    traffic = None
+    achieved = flops / (ms_dom * 1e-3) / 1e12
+    bulk_entries = info["entries_owned"] - 2 * w.n_gamma ** 2 * w.n_steps + w.n_gamma ** 2  # cells d >= 2
+    store_gbs = 8.0 * bulk_entries / (ms_dom * 1e-3) / 1e9
+    traffic = {}
     tpath = os.path.join(ROOT, "profiles", "r01_traffic.json")
     if os.path.exists(tpath):
-        tj = json.load(open(tpath)).get(f"k_bulk_{kdom}")
-        if tj and tj.get("config") == args.config:
-            traffic = tj["traffic_bytes_per_launch"]
-    achieved = flops / (ms_dom * 1e-3) / 1e12
+        for kname, tj in json.load(open(tpath)).items():
+            if tj.get("config") == args.config:
+                traffic[kname] = tj["traffic_bytes_per_launch"]
+    roof_asm = {"bound": "alu", "kernel": f"k_bulk_m<{kdom}>", "achieved": achieved, "peak": FP64_PEAK_DERIVED,
+                "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_DERIVED,
+                "traffic": traffic.get(f"k_bulk_m<{kdom}>"),
+                "store_gbs": store_gbs, "store_frac_of_hbm": store_gbs / hbm_peak,
+                "peak_note": "FP64 DFMA: 148 SM x 64 FMA/clk x 2 x 1.965 GHz (derived from the guide's unit counts "
+                             "and MEASURED_PEAKS sm_max_mhz); tools/fp64_peak.cu measured 34.1 TFLOP/s",
+                "flops_per_launch": flops, "node_evals_per_launch": st["evals_bulk"],
+                "nodes_by_regime_ABZC": st["nodes_bulk"],
+                "flops_note": "algorithmic: exact per-regime node counts x static FP64 flops of the shipped "
+                              "moment forms (DFMA = 2), DESIGN.md section 6"}
+    roof_gemv = {"bound": "hbm", "kernel": "k_gemv", "achieved": gemv_gbs, "peak": hbm_peak, "unit": "GB/s",
+                 "frac": (gemv_gbs / hbm_peak) if gemv_gbs else None, "traffic": traffic.get("k_gemv"),
+                 "bytes_per_launch": bytes_per_gemv,
+                 "peak_note": "MEASURED_PEAKS.json hbm_gbs (driver-measured copy bandwidth)",
+                 "bytes_note": "algorithmic: 8 B per stored entry (block lower triangle only) + 16 N"}
+    # the dominant kernel of the step by device time: the GEMV (all products of the solve) or the
+    # longest assembly kernel
+    gemv_total_ms = 1e3 * rep["seconds_matvec"]
+    roofline = roof_gemv if gemv_total_ms >= ms_dom else roof_asm
+    roofline = dict(roofline, share_of_step=(gemv_total_ms if roofline is roof_gemv else ms_dom) / ms)
     asm_s = ph["assemble_V"] + ph["assemble_K"] + ph["assemble_D"]
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -268,16 +298,12 @@ def native(args):
             "gmres_true_rel_residual": rep["true_rel_residual"], "time_to_solution_s": ph["total"],
             "kernel_ms": {k: {"bulk": stats[k]["ms_bulk"], "near": stats[k]["ms_near"], "sing": stats[k]["ms_sing"]} for k in "VKD"},
         },
-        "roofline": {"bound": "alu", "kernel": f"k_bulk_{kdom}", "achieved": achieved, "peak": FP64_PEAK_DERIVED,
-                     "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_DERIVED, "traffic": traffic,
-                     "traffic_note": "dram read+write bytes per launch from ncu --set full (profiles/r01_ncu_bulkD_C3.txt); the kernel is FP64-bound, traffic = the matrix stores",
-                     "peak_note": "FP64 DFMA: 148 SM x 64 FMA/clk x 2 x 1.965 GHz (derived); measured 34.1 TFLOP/s",
-                     "flops_per_launch": flops, "evals_per_launch": st["evals_bulk"],
-                     "flops_note": "algorithmic: evaluations x static FP64 flops of the small-x path (DFMA=2), DESIGN.md section 6"},
-        "roofline_gemv": {"bound": "hbm", "achieved": gemv_gbs, "peak": hbm_peak, "unit": "GB/s",
-                          "frac": (gemv_gbs / hbm_peak) if gemv_gbs else None, "bytes_per_launch": bytes_per_gemv},
+        "roofline": roofline,
+        "roofline_gemv": roof_gemv,
+        "roofline_assembly": roof_asm,
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n},
         "gpu_launches": int(launches),
+        "host_step_ms": {"device_timed": [round(x, 2) for x in step_wall], "e2e": [round(x, 2) for x in e2e_wall]},
         "clocks": ck,
         "wall_s": wall,
     }

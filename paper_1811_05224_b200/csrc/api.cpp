@@ -17,10 +17,11 @@ namespace {
 
 inline cudaStream_t S(bem_stream s) { return reinterpret_cast<cudaStream_t>(s); }
 
-bem_matrix* new_dense(const bem_mesh* m, int kind, bem_status* st) {
+bem_matrix* new_dense(const bem_mesh* m, int kind, cudaStream_t stream, bem_status* st) {
   bem_matrix* A = new bem_matrix_s();
   A->kind = kind;
   A->mesh = m;
+  A->stream = stream;
   const int ng = m->ng;
   long long off = 0;
   for (size_t bi = 0; bi < m->blocks.size(); ++bi) {
@@ -43,8 +44,7 @@ bem_matrix* new_dense(const bem_mesh* m, int kind, bem_status* st) {
     }
     pool_ready = true;
   }
-  cudaError_t e = cudaMallocAsync(&A->data, sizeof(double) * std::max<long long>(off, 4), (cudaStream_t)0);
-  if (e == cudaSuccess) e = cudaStreamSynchronize((cudaStream_t)0);
+  cudaError_t e = cudaMallocAsync(&A->data, sizeof(double) * std::max<long long>(off, 4), stream);
   if (e != cudaSuccess) {
     *st = BEM_E_NOMEM;
     set_error(std::string("matrix allocation of ") + std::to_string(8.0 * off / 1e9) + " GB failed: " + cudaGetErrorString(e));
@@ -66,10 +66,10 @@ bem_status assemble(int kind, const bem_mesh* m, const bem_quad_opts* o, bem_str
   if (m->ng < 6) { set_error("bem_assemble: N_Gamma >= 6 required"); return BEM_E_INVALID; }
   cudaSetDevice(m->device);
   bem_status st;
-  bem_matrix* A = new_dense(m, kind, &st);
+  bem_matrix* A = new_dense(m, kind, S(s), &st);
   if (!A) return st;
-  cudaError_t e = cudaMemsetAsync(A->data, 0, sizeof(double) * A->entries, S(s));
-  if (e != cudaSuccess) { bem_matrix_destroy(A); return cuda_fail(e, "bem_assemble/memset"); }
+  // no memset: the bulk kernel writes every entry of the cells d >= 2 and the near kernel every
+  // entry of the cells d <= 1 (the row padding is never read)
   st = launch_assembly(kind, m, A, q_bulk, q_sing, o ? o->flags : 0, S(s));
   if (st == BEM_OK) st = gemv_setup(A);
   if (st != BEM_OK) { bem_matrix_destroy(A); return st; }
@@ -120,13 +120,13 @@ bem_status bem_assemble_D(const bem_mesh* m, const bem_quad_opts* o, bem_stream 
 }
 
 bem_status bem_assemble_M(const bem_mesh* m, bem_mass_kind kind, bem_stream s, bem_matrix** out) {
-  (void)s;
   if (!m || !out) { set_error("bem_assemble_M: null argument"); return BEM_E_INVALID; }
   if (kind < BEM_MASS_PRIMAL || kind > BEM_MASS_DUAL_LUMPED) { set_error("bem_assemble_M: bad kind"); return BEM_E_INVALID; }
   cudaSetDevice(m->device);
   bem_matrix* M = new bem_matrix_s();
   M->kind = STB_MASS;
   M->mesh = m;
+  M->stream = S(s);
   bem_status st = mass_setup(M, kind);
   if (st != BEM_OK) { bem_matrix_destroy(M); return st; }
   *out = M;
@@ -394,6 +394,8 @@ bem_status bem_matrix_get(const bem_matrix* A, long long r0, long long nr, long 
 
 bem_status bem_matrix_stats(const bem_matrix* A, bem_assembly_stats* o) {
   if (!A || !o) { set_error("bem_matrix_stats: null"); return BEM_E_INVALID; }
+  bem_status fs = finalize_assembly_stats(const_cast<bem_matrix*>(A));
+  if (fs != BEM_OK) return fs;
   o->ms_bulk = A->ms_bulk;
   o->ms_near = A->ms_near;
   o->ms_sing = A->ms_sing;
@@ -434,19 +436,14 @@ bem_status bem_matrix_info(const bem_matrix* A, int* kind, long long* entries, l
 
 void bem_matrix_destroy(bem_matrix* A) {
   if (!A) return;
-  if (A->data) {
-    cudaFreeAsync(A->data, (cudaStream_t)0);
-    cudaStreamSynchronize((cudaStream_t)0);
-  }
-  cudaFree(A->d_segs);
-  cudaFree(A->d_partials);
-  cudaFree(A->d_row_pbase);
-  cudaFree(A->d_row_pstride);
-  cudaFree(A->d_ysum);
-  cudaFree(A->d_lo);
-  cudaFree(A->d_di);
-  cudaFree(A->d_up);
-  cudaFree(A->d_work);
+  // stream-ordered: the storage returns to the pool after the work queued on the matrix's
+  // stream (callers that used the matrix on another stream synchronise that stream first)
+  const cudaStream_t st = A->stream;
+  for (void* p : {(void*)A->data, (void*)A->d_segs, (void*)A->d_partials, (void*)A->d_row_pbase,
+                  (void*)A->d_row_pstride, (void*)A->d_ysum, (void*)A->d_lo, (void*)A->d_di,
+                  (void*)A->d_up, (void*)A->d_work, (void*)A->d_ctr})
+    if (p) cudaFreeAsync(p, st);
+  for (auto x : A->ev) cudaEventDestroy(x);
   delete A;
 }
 

@@ -312,10 +312,10 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bul
                            int flags, cudaStream_t st) {
   const int ng = m->ng;
   long long* d_poff = nullptr;
-  cudaError_t e = cudaMalloc(&d_poff, sizeof(long long) * std::max<size_t>(1, A->poff.size()));
+  cudaError_t e = cudaMallocAsync((void**)&d_poff, sizeof(long long) * std::max<size_t>(1, A->poff.size()), st);
   if (e != cudaSuccess) return cuda_fail(e, "assemble/poff");
   e = cudaMemcpyAsync(d_poff, A->poff.data(), sizeof(long long) * A->poff.size(), cudaMemcpyHostToDevice, st);
-  if (e != cudaSuccess) { cudaFree(d_poff); return cuda_fail(e, "assemble/poff copy"); }
+  if (e != cudaSuccess) { cudaFreeAsync(d_poff, st); return cuda_fail(e, "assemble/poff copy"); }
   // pair records (bulk order and near orders) and regime counters, stream-ordered
   const long long npairs = (long long)ng * ng;
   const long long nsrec = 5LL * ng;
@@ -329,20 +329,23 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bul
   double* d_rec = nullptr;
   unsigned long long* d_ctr = nullptr;
   if ((e = cudaMallocAsync((void**)&d_rec, sizeof(double) * nf * (2 * npairs + nsrec), st)) != cudaSuccess ||
-      (e = cudaMallocAsync((void**)&d_ctr, sizeof(unsigned long long) * 12, st)) != cudaSuccess ||
-      (e = cudaMemsetAsync(d_ctr, 0, sizeof(unsigned long long) * 12, st)) != cudaSuccess) {
-    cudaFree(d_poff);
+      (e = cudaMallocAsync((void**)&d_ctr, sizeof(unsigned long long) * 15, st)) != cudaSuccess ||
+      (e = cudaMemsetAsync(d_ctr, 0, sizeof(unsigned long long) * 15, st)) != cudaSuccess) {
+    cudaFreeAsync(d_poff, st);
     return cuda_fail(e, "assemble/records");
   }
-  // CUDA events on the launching stream around each kernel family, per block
-  std::vector<cudaEvent_t> ev;
+  // CUDA events on the launching stream around each kernel family, per block; read (with the
+  // counters) on the first statistics query, so that the assembly never blocks the host
+  A->d_ctr = d_ctr;
+  A->stats_ready = false;
+  std::vector<cudaEvent_t>& ev = A->ev;
   auto mark = [&]() {
     cudaEvent_t x;
     cudaEventCreate(&x);
     cudaEventRecord(x, st);
     ev.push_back(x);
   };
-  std::vector<int> fam;  // family of the interval ending at ev[k+1]: 0 bulk, 1 near, 2 sing, 3 records
+  std::vector<int>& fam = A->ev_fam;  // family of the interval ending at ev[k+1]: 0 bulk, 1 near, 2 sing, 3 records
   A->q_bulk = q_bulk;
   A->q_sing = q_sing;
   A->launches = 0;
@@ -350,11 +353,11 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bul
   MomArgs MB{d_rec, npairs, m->d_seg, m->d_half, m->d_dual, m->alpha, ng, q_bulk, qfar, d_ctr};
   MomArgs MN = MB;
   MN.rec = d_rec + (long long)nf * npairs;
-  MN.counters = d_ctr + 4;
+  MN.counters = d_ctr + 5;
   MomArgs MS = MB;
   MS.rec = d_rec + 2LL * nf * npairs;
   MS.npairs = nsrec;
-  MS.counters = d_ctr + 8;
+  MS.counters = d_ctr + 10;
   mark();
   if (kind == STB_V) launch_records<STB_V>(MB, MN, fused_sing ? &MS : nullptr, q_sing, st);
   else if (kind == STB_K) launch_records<STB_K>(MB, MN, fused_sing ? &MS : nullptr, q_sing, st);
@@ -412,41 +415,50 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bul
       A->launches += 2;
     }
   }
-  e = cudaGetLastError();
-  unsigned long long ctr[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
-  cudaError_t e2 = cudaMemcpyAsync(ctr, d_ctr, sizeof(ctr), cudaMemcpyDeviceToHost, st);
   cudaFreeAsync(d_rec, st);
-  cudaFreeAsync(d_ctr, st);
-  cudaStreamSynchronize(st);
-  if (e == cudaSuccess) e = e2;
+  cudaFreeAsync(d_poff, st);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "assemble/launch");
+  return BEM_OK;
+}
+
+bem_status finalize_assembly_stats(bem_matrix* A) {
+  if (A->stats_ready) return BEM_OK;
+  A->stats_ready = true;
+  if (!A->ev.empty()) cudaEventSynchronize(A->ev.back());
+  unsigned long long ctr[15] = {0};
+  cudaError_t e = cudaMemcpy(ctr, A->d_ctr, sizeof(ctr), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail(e, "assembly stats");
   for (int k = 0; k < 4; ++k) {
     A->nodes_bulk[k] = (long long)ctr[k];
-    A->nodes_near[k] = (long long)ctr[4 + k];
+    A->nodes_near[k] = (long long)ctr[5 + k];
   }
   A->ms_bulk = A->ms_near = A->ms_sing = A->ms_records = 0.0;
-  for (size_t k = 0; k + 1 < ev.size(); ++k) {
+  for (size_t k = 0; k + 1 < A->ev.size(); ++k) {
     float ms = 0.0f;
-    cudaEventElapsedTime(&ms, ev[k], ev[k + 1]);
-    (fam[k] == 0 ? A->ms_bulk : fam[k] == 1 ? A->ms_near : fam[k] == 2 ? A->ms_sing : A->ms_records) += ms;
+    cudaEventElapsedTime(&ms, A->ev[k], A->ev[k + 1]);
+    const int f = A->ev_fam[k];
+    (f == 0 ? A->ms_bulk : f == 1 ? A->ms_near : f == 2 ? A->ms_sing : A->ms_records) += ms;
   }
-  // algorithmic FP64 flops of the bulk kernel: static counts per node of
-  // the regime-A Horner forms (V 40, K 37, D 77) and of the regime-B Taylor form
-  const double fA = kind == STB_V ? 40.0 : (kind == STB_K ? 37.0 : 77.0);
-  const double fB = kind == STB_D ? 2.0 * 21 * 6 + 40.0 : 21 * 6 + 30.0;
-  A->flops_bulk = fA * (double)A->nodes_bulk[0] + fB * (double)A->nodes_bulk[1];
+  for (auto x : A->ev) cudaEventDestroy(x);
+  A->ev.clear();
+  // algorithmic FP64 flops of the bulk kernel, static counts of the shipped
+  // forms (DFMA = 2): regime A per node V 40, K 36, D 76 (17-step Horner per family + log terms);
+  // regime B per node 61 (E1 / GB3 and the closing terms, exp not counted) + per Taylor order
+  // V, K 8, D 10 (two multiplies for e^, add + multiply for a^, one or two FMAs)
+  const int kind = A->kind;
+  const double fA = kind == STB_V ? 40.0 : (kind == STB_K ? 36.0 : 76.0);
+  const double fK = kind == STB_D ? 10.0 : 8.0;
+  A->flops_bulk = fA * (double)A->nodes_bulk[0] + 61.0 * (double)A->nodes_bulk[1] + fK * (double)ctr[4];
   A->ev_bulk = A->nodes_bulk[0] + A->nodes_bulk[1] + A->nodes_bulk[2] + A->nodes_bulk[3];
   A->ev_near = A->nodes_near[0] + A->nodes_near[1] + A->nodes_near[2] + A->nodes_near[3];
-  for (auto x : ev) cudaEventDestroy(x);
-  cudaFree(d_poff);
-  if (e != cudaSuccess) return cuda_fail(e, "assemble/launch");
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return cuda_fail(e, "assemble/kernels");
+  // self-checks of the kernels' coverage
   if (A->ev_bulk != A->nodes_expected) {
-    set_error("assemble: bulk node count mismatch");
+    set_error("assembly stats: bulk node count mismatch");
     return BEM_E_CUDA;
   }
-  if (ctr[11] != 0) {
-    set_error("assemble: touching-pair moment record outside regime A (use BEM_QUAD_LEGACY_SING)");
+  if (ctr[13] != 0) {
+    set_error("assembly stats: touching-pair moment record outside regime A");
     return BEM_E_CUDA;
   }
   return BEM_OK;

@@ -83,6 +83,14 @@ enum { STB_V = 0, STB_K = 1, STB_D = 2, STB_MASS = 3 };
 struct bem_matrix_s {
   int kind = 0;
   const bem_mesh* mesh = nullptr;
+  // every device buffer of the matrix is allocated and freed stream-ordered on this stream (the
+  // stream of bem_assemble_*): assembly, setup and destroy never block the host
+  cudaStream_t stream = nullptr;
+  // lazily finalised assembly statistics (events + counters read on the first stats query)
+  std::vector<cudaEvent_t> ev;
+  std::vector<int> ev_fam;
+  unsigned long long* d_ctr = nullptr;
+  bool stats_ready = true;
   // dense block-lower-triangular storage (V, K, D)
   double* data = nullptr;
   long long entries = 0;       // stored doubles (with row padding)
@@ -147,6 +155,7 @@ bem_status gemv_setup(bem_matrix* A);
 bem_status gemv_launch(const bem_matrix* A, double a, const double* x, double b, double* y,
                        cudaStream_t st);
 bem_status mass_setup(bem_matrix* M, int kind);
+bem_status finalize_assembly_stats(bem_matrix* A);
 bem_status mass_apply(const bem_matrix* M, double a, const double* x, double b, double* y,
                       cudaStream_t st);
 bem_status mass_solve(const bem_matrix* M, int transpose, const double* x, double* y,

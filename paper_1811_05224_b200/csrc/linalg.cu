@@ -141,16 +141,17 @@ bem_status gemv_setup(bem_matrix* A) {
   }
   A->n_items = item;
   cudaError_t e;
+  const cudaStream_t st = A->stream;
   size_t nseg = std::max<size_t>(1, A->segs.size());
-  if ((e = cudaMalloc(&A->d_segs, sizeof(GSeg) * nseg)) != cudaSuccess) return cuda_fail(e, "gemv_setup");
-  if ((e = cudaMemcpy(A->d_segs, A->segs.data(), sizeof(GSeg) * A->segs.size(), cudaMemcpyHostToDevice)) != cudaSuccess) return cuda_fail(e, "gemv_setup");
-  if ((e = cudaMalloc(&A->d_partials, sizeof(double) * std::max<long long>(1, A->n_partials))) != cudaSuccess) return cuda_fail(e, "gemv_setup");
-  if ((e = cudaMalloc(&A->d_row_pbase, sizeof(long long) * nt)) != cudaSuccess) return cuda_fail(e, "gemv_setup");
-  if ((e = cudaMalloc(&A->d_row_pstride, sizeof(int) * nt)) != cudaSuccess) return cuda_fail(e, "gemv_setup");
-  if ((e = cudaMemcpy(A->d_row_pbase, A->row_pbase.data(), sizeof(long long) * nt, cudaMemcpyHostToDevice)) != cudaSuccess) return cuda_fail(e, "gemv_setup");
-  if ((e = cudaMemcpy(A->d_row_pstride, A->row_pstride.data(), sizeof(int) * nt, cudaMemcpyHostToDevice)) != cudaSuccess) return cuda_fail(e, "gemv_setup");
+  if ((e = cudaMallocAsync((void**)&A->d_segs, sizeof(GSeg) * nseg, st)) != cudaSuccess) return cuda_fail(e, "gemv_setup");
+  if ((e = cudaMemcpyAsync(A->d_segs, A->segs.data(), sizeof(GSeg) * A->segs.size(), cudaMemcpyHostToDevice, st)) != cudaSuccess) return cuda_fail(e, "gemv_setup");
+  if ((e = cudaMallocAsync((void**)&A->d_partials, sizeof(double) * std::max<long long>(1, A->n_partials), st)) != cudaSuccess) return cuda_fail(e, "gemv_setup");
+  if ((e = cudaMallocAsync((void**)&A->d_row_pbase, sizeof(long long) * nt, st)) != cudaSuccess) return cuda_fail(e, "gemv_setup");
+  if ((e = cudaMallocAsync((void**)&A->d_row_pstride, sizeof(int) * nt, st)) != cudaSuccess) return cuda_fail(e, "gemv_setup");
+  if ((e = cudaMemcpyAsync(A->d_row_pbase, A->row_pbase.data(), sizeof(long long) * nt, cudaMemcpyHostToDevice, st)) != cudaSuccess) return cuda_fail(e, "gemv_setup");
+  if ((e = cudaMemcpyAsync(A->d_row_pstride, A->row_pstride.data(), sizeof(int) * nt, cudaMemcpyHostToDevice, st)) != cudaSuccess) return cuda_fail(e, "gemv_setup");
   if (m->nranks > 1) {
-    if ((e = cudaMalloc(&A->d_ysum, sizeof(double) * (size_t)ng * nt)) != cudaSuccess) return cuda_fail(e, "gemv_setup");
+    if ((e = cudaMallocAsync((void**)&A->d_ysum, sizeof(double) * (size_t)ng * nt, st)) != cudaSuccess) return cuda_fail(e, "gemv_setup");
   }
   return BEM_OK;
 }
@@ -236,14 +237,15 @@ bem_status mass_setup(bem_matrix* M, int kind) {
   const long long n = (long long)m->ng * m->nt;
   M->mass_kind = kind;
   cudaError_t e;
-  if ((e = cudaMalloc(&M->d_lo, sizeof(double) * n)) != cudaSuccess ||
-      (e = cudaMalloc(&M->d_di, sizeof(double) * n)) != cudaSuccess ||
-      (e = cudaMalloc(&M->d_up, sizeof(double) * n)) != cudaSuccess ||
-      (e = cudaMalloc(&M->d_work, sizeof(double) * 3 * n)) != cudaSuccess)
+  const cudaStream_t st = M->stream;
+  if ((e = cudaMallocAsync((void**)&M->d_lo, sizeof(double) * n, st)) != cudaSuccess ||
+      (e = cudaMallocAsync((void**)&M->d_di, sizeof(double) * n, st)) != cudaSuccess ||
+      (e = cudaMallocAsync((void**)&M->d_up, sizeof(double) * n, st)) != cudaSuccess ||
+      (e = cudaMallocAsync((void**)&M->d_work, sizeof(double) * 3 * n, st)) != cudaSuccess)
     return cuda_fail(e, "bem_assemble_M");
-  k_mass_fill<<<(unsigned)((n + 255) / 256), 256>>>(kind, m->d_seg, m->d_dual, m->d_t, m->ng, m->nt, M->d_lo, M->d_di, M->d_up);
+  k_mass_fill<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(kind, m->d_seg, m->d_dual, m->d_t, m->ng, m->nt, M->d_lo, M->d_di, M->d_up);
   count_launch();
-  e = cudaDeviceSynchronize();
+  e = cudaGetLastError();
   return e == cudaSuccess ? BEM_OK : cuda_fail(e, "bem_assemble_M");
 }
 

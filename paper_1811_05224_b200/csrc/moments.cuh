@@ -471,10 +471,10 @@ __device__ __forceinline__ double affine_part(const double* __restrict__ rec, lo
   return out;
 }
 
-// warp-aggregated regime counters
+// warp-aggregated regime counters: [A, B, Z, C, sum of the regime-B Taylor orders]
 __device__ __forceinline__ void count_regimes(unsigned long long* ctr, unsigned long long nA,
                                               unsigned long long nB, unsigned long long nZ,
-                                              unsigned long long nC) {
+                                              unsigned long long nC, unsigned long long nK) {
   if (!ctr) return;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -482,12 +482,14 @@ __device__ __forceinline__ void count_regimes(unsigned long long* ctr, unsigned 
     nB += __shfl_xor_sync(0xffffffffu, nB, o);
     nZ += __shfl_xor_sync(0xffffffffu, nZ, o);
     nC += __shfl_xor_sync(0xffffffffu, nC, o);
+    nK += __shfl_xor_sync(0xffffffffu, nK, o);
   }
   if ((threadIdx.x & 31) == 0) {
     atomicAdd(ctr + 0, nA);
     if (nB) atomicAdd(ctr + 1, nB);
     if (nZ) atomicAdd(ctr + 2, nZ);
     if (nC) atomicAdd(ctr + 3, nC);
+    if (nK) atomicAdd(ctr + 4, nK);
   }
 }
 
@@ -526,7 +528,7 @@ __global__ void __launch_bounds__(128) k_bulk_m(BlockArgs B, MomArgs M) {
   A.load(M.rec + pair, S);
   RegBZ<KIND> Z;
   Z.load(M.rec + pair, S);
-  unsigned long long nA = 0, nB = 0, nZ = 0, nC = 0;
+  unsigned long long nA = 0, nB = 0, nZ = 0, nC = 0, nK = 0;
   double Gp[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) Gp[r] = 0.0;
@@ -558,6 +560,7 @@ __global__ void __launch_bounds__(128) k_bulk_m(BlockArgs B, MomArgs M) {
         int reg = 0;
         const double v = phi_bz<KIND>(M.rec + pair, S, Z, q.x, q.z, &reg);
         nB += reg == 1;
+        nK += reg == 1 ? Z.kb : 0;
         nZ += reg == 2;
         if (reg == 3) {
           cmask |= 1u << r;
@@ -601,8 +604,8 @@ __global__ void __launch_bounds__(128) k_bulk_m(BlockArgs B, MomArgs M) {
       for (int r = 1; r <= R; ++r) Gp[r - 1] = phi[r] - phi[r - 1];
     }
   }
-  if (!valid) nA = nB = nZ = nC = 0;
-  count_regimes(M.counters, nA, nB, nZ, nC);
+  if (!valid) nA = nB = nZ = nC = nK = 0;
+  count_regimes(M.counters, nA, nB, nZ, nC, nK);
 }
 
 // ------------------------------------------------------------- near cells (d <= 1)
@@ -627,7 +630,7 @@ __global__ void __launch_bounds__(128) k_near_m(BlockArgs B, MomArgs M, int chun
   A.load(rec, S);
   RegBZ<KIND> Z;
   Z.load(rec, S);
-  unsigned long long nA = 0, nB = 0, nZ = 0, nC = 0;
+  unsigned long long nA = 0, nB = 0, nZ = 0, nC = 0, nK = 0;
   // node value for every lane (warp-uniform call: regime C is computed cooperatively)
   auto node = [&](int x, int y) -> double {
     const double4 nd = B.lag[x * B.ldlag + y];
@@ -640,6 +643,7 @@ __global__ void __launch_bounds__(128) k_near_m(BlockArgs B, MomArgs M, int chun
       int reg = 0;
       v = phi_bz<KIND>(rec, S, Z, nd.x, nd.z, &reg);
       nB += reg == 1;
+        nK += reg == 1 ? Z.kb : 0;
       nZ += reg == 2;
       if (reg == 3) {
         needC = true;
@@ -670,8 +674,8 @@ __global__ void __launch_bounds__(128) k_near_m(BlockArgs B, MomArgs M, int chun
     }
     prev = p10;
   }
-  if (!valid) nA = nB = nZ = nC = 0;
-  count_regimes(M.counters, nA, nB, nZ, nC);
+  if (!valid) nA = nB = nZ = nC = nK = 0;
+  count_regimes(M.counters, nA, nB, nZ, nC, nK);
 }
 
 // ------------------------------------------------------------- touching sub-pairs (d <= 1)
@@ -836,7 +840,7 @@ __global__ void __launch_bounds__(128) k_sing_m(BlockArgs B, MomArgs M, int chun
     if (d1) *entry_ptr(B, a, I, a - 1, J) += node(a + 1, a - 1) - prev - p10;
     prev = p10;
   }
-  if (bad && M.counters) atomicAdd(M.counters + 3, bad);
+  if (bad && M.counters) atomicAdd(M.counters + 3, bad);   // regime C slot of the sing counters
 }
 
 }  // namespace stb
