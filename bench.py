@@ -304,6 +304,7 @@ def native(args):
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n},
         "gpu_launches": int(launches),
         "host_step_ms": {"device_timed": [round(x, 2) for x in step_wall], "e2e": [round(x, 2) for x in e2e_wall]},
+        "phases_ms": [{k: round(1e3 * v, 2) for k, v in p.items()} for p in phases],
         "clocks": ck,
         "wall_s": wall,
     }

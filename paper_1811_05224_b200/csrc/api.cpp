@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <mutex>
 #include <cstring>
 #include <vector>
 
@@ -187,24 +188,48 @@ bem_status bem_solve_gmres(const bem_matrix* V, const bem_matrix* D, const bem_m
   const int kmax = opts->max_iter;
   cudaStream_t st = S(stream);
   double *Q = nullptr, *tmp = nullptr, *u = nullptr, *v = nullptr, *dh = nullptr, *wk = nullptr;
-  double* hpin = nullptr;  // pinned host copy of the Hessenberg column
+  double* hpin = nullptr;  // pinned host copy of the Hessenberg column (persistent, grow-only)
   cudaError_t e;
+  static std::mutex pin_mu;
+  static double* pin_buf = nullptr;
+  static size_t pin_n = 0;
+  std::lock_guard<std::mutex> pin_lock(pin_mu);   // one solve at a time uses the pinned buffer
+  if (pin_n < (size_t)2 * (kmax + 2)) {
+    if (pin_buf) cudaFreeHost(pin_buf);
+    pin_buf = nullptr;
+    pin_n = 0;
+    if (cudaMallocHost(&pin_buf, sizeof(double) * 2 * (kmax + 2)) != cudaSuccess) {
+      cudaGetLastError();
+      set_error("bem_solve_gmres: pinned allocation failed");
+      return BEM_E_NOMEM;
+    }
+    pin_n = (size_t)2 * (kmax + 2);
+  }
+  hpin = pin_buf;
+  mesh_wait(m, st);
   // stream-ordered allocations: no device-wide synchronisation
   if ((e = cudaMallocAsync(&Q, sizeof(double) * n * (kmax + 1), st)) != cudaSuccess ||
       (e = cudaMallocAsync(&tmp, sizeof(double) * n, st)) != cudaSuccess ||
       (e = cudaMallocAsync(&u, sizeof(double) * n, st)) != cudaSuccess ||
       (e = cudaMallocAsync(&v, sizeof(double) * n, st)) != cudaSuccess ||
       (e = cudaMallocAsync(&wk, sizeof(double) * n, st)) != cudaSuccess ||
-      (e = cudaMallocAsync(&dh, sizeof(double) * 2 * (kmax + 2), st)) != cudaSuccess ||
-      (e = cudaMallocHost(&hpin, sizeof(double) * 2 * (kmax + 2))) != cudaSuccess) {
+      (e = cudaMallocAsync(&dh, sizeof(double) * 2 * (kmax + 2), st)) != cudaSuccess) {
     cudaFreeAsync(Q, st); cudaFreeAsync(tmp, st); cudaFreeAsync(u, st); cudaFreeAsync(v, st);
-    cudaFreeAsync(wk, st); cudaFreeAsync(dh, st); cudaFreeHost(hpin);
+    cudaFreeAsync(wk, st); cudaFreeAsync(dh, st);
     cudaGetLastError();
     set_error("bem_solve_gmres: allocation failed");
     return BEM_E_NOMEM;
   }
-  cudaEvent_t e0, e1, mv0, mv1;
-  cudaEventCreate(&e0); cudaEventCreate(&e1); cudaEventCreate(&mv0); cudaEventCreate(&mv1);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0); cudaEventCreate(&e1);
+  // GEMV timing: an event pair per product, read once after the solve (no host sync per product)
+  std::vector<cudaEvent_t> mvev;
+  auto mv_mark = [&]() {
+    cudaEvent_t x;
+    cudaEventCreate(&x);
+    cudaEventRecord(x, st);
+    mvev.push_back(x);
+  };
   double t_mv = 0.0;
   int nmv_V = 0, nmv_D = 0;
   cudaEventRecord(e0, st);
@@ -216,26 +241,18 @@ bem_status bem_solve_gmres(const bem_matrix* V, const bem_matrix* D, const bem_m
     }
     bem_status s1 = mass_solve(M, 1, r, u, st);
     if (s1 != BEM_OK) return s1;
-    cudaEventRecord(mv0, st);
+    mv_mark();
     s1 = gemv_launch(D, 1.0, u, 0.0, v, st);
     ++nmv_D;
-    cudaEventRecord(mv1, st);
+    mv_mark();
     if (s1 != BEM_OK) return s1;
-    cudaEventSynchronize(mv1);
-    float ms = 0;
-    cudaEventElapsedTime(&ms, mv0, mv1);
-    t_mv += ms * 1e-3;
     return mass_solve(M, 0, v, out, st);
   };
   auto apply_V = [&](const double* x, double* out) -> bem_status {
-    cudaEventRecord(mv0, st);
+    mv_mark();
     bem_status s1 = gemv_launch(V, 1.0, x, 0.0, out, st);
     ++nmv_V;
-    cudaEventRecord(mv1, st);
-    cudaEventSynchronize(mv1);
-    float ms = 0;
-    cudaEventElapsedTime(&ms, mv0, mv1);
-    t_mv += ms * 1e-3;
+    mv_mark();
     return s1;
   };
   auto norm = [&](const double* x) -> double {
@@ -263,16 +280,18 @@ bem_status bem_solve_gmres(const bem_matrix* V, const bem_matrix* D, const bem_m
       double* qk = Q + (long long)k * n;
       if ((status = apply_V(qk, tmp)) != BEM_OK) break;
       if ((status = apply_C(tmp, wk)) != BEM_OK) break;
-      // classical Gram-Schmidt with one re-orthogonalisation (CGS2)
+      // classical Gram-Schmidt with one re-orthogonalisation (CGS2); both coefficient passes and
+      // ||w||^2 land contiguously in dh and come back in one copy (one host sync per iteration)
       vec_dots(Q, n, k + 1, wk, n, dh, st);
       vec_update(wk, Q, n, k + 1, dh, n, st);
-      vec_dots(Q, n, k + 1, wk, n, dh + (kmax + 2), st);
-      vec_update(wk, Q, n, k + 1, dh + (kmax + 2), n, st);
-      cudaMemcpyAsync(hcol, dh, sizeof(double) * (k + 1), cudaMemcpyDeviceToHost, st);
-      cudaMemcpyAsync(hcol + (kmax + 2), dh + (kmax + 2), sizeof(double) * (k + 1), cudaMemcpyDeviceToHost, st);
-      double hk1 = norm(wk);  // synchronises
+      vec_dots(Q, n, k + 1, wk, n, dh + (k + 1), st);
+      vec_update(wk, Q, n, k + 1, dh + (k + 1), n, st);
+      vec_dots(wk, 0, 1, wk, n, dh + 2 * (k + 1), st);
+      cudaMemcpyAsync(hcol, dh, sizeof(double) * (2 * k + 3), cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      const double hk1 = std::sqrt(hcol[2 * k + 2]);
       double* Hk = &H[(size_t)k * (kmax + 1)];
-      for (int j = 0; j <= k; ++j) Hk[j] = hcol[j] + hcol[(kmax + 2) + j];
+      for (int j = 0; j <= k; ++j) Hk[j] = hcol[j] + hcol[(k + 1) + j];
       Hk[k + 1] = hk1;
       if (hk1 > 1e-300) vec_scale(Q + (long long)(k + 1) * n, wk, 1.0 / hk1, n, st);
       for (int j = 0; j < k; ++j) {
@@ -319,12 +338,17 @@ bem_status bem_solve_gmres(const bem_matrix* V, const bem_matrix* D, const bem_m
   cudaEventSynchronize(e1);
   float ms_total = 0;
   cudaEventElapsedTime(&ms_total, e0, e1);
+  for (size_t k = 0; k + 1 < mvev.size(); k += 2) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, mvev[k], mvev[k + 1]);
+    t_mv += ms * 1e-3;
+  }
+  for (auto x : mvev) cudaEventDestroy(x);
   e = cudaGetLastError();
   cudaFreeAsync(Q, st); cudaFreeAsync(tmp, st); cudaFreeAsync(u, st); cudaFreeAsync(v, st);
   cudaFreeAsync(wk, st); cudaFreeAsync(dh, st);
   cudaStreamSynchronize(st);
-  cudaFreeHost(hpin);
-  cudaEventDestroy(e0); cudaEventDestroy(e1); cudaEventDestroy(mv0); cudaEventDestroy(mv1);
+  cudaEventDestroy(e0); cudaEventDestroy(e1);
   if (e != cudaSuccess) return cuda_fail(e, "bem_solve_gmres");
   if (rep) {
     rep->iterations = iters;

@@ -311,6 +311,7 @@ static long long bulk_nodes(const Block& b, int R) {
 bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bulk, int q_sing,
                            int flags, cudaStream_t st) {
   const int ng = m->ng;
+  mesh_wait(m, st);
   long long* d_poff = nullptr;
   cudaError_t e = cudaMallocAsync((void**)&d_poff, sizeof(long long) * std::max<size_t>(1, A->poff.size()), st);
   if (e != cudaSuccess) return cuda_fail(e, "assemble/poff");

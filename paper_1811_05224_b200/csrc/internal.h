@@ -74,7 +74,7 @@ struct bem_mesh_s {
   stb::Seg* d_half = nullptr;
   stb::Dual* d_dual = nullptr;
   double4* d_lag = nullptr;       // (s, ln s, 1/s, 0) for time nodes x > y: index x*(nt+1)+y
-  cudaStream_t stream = nullptr;  // internal stream (solver)
+  cudaEvent_t ready = nullptr;    // the uploads above are complete (waited on by every user stream)
 };
 
 // matrix kinds
@@ -135,6 +135,10 @@ struct bem_matrix_s {
 namespace stb {
 // error handling
 void set_error(const std::string& msg);
+// the mesh's device data are ready on stream st (stream-ordered wait on the upload event)
+inline void mesh_wait(const bem_mesh* m, cudaStream_t st) {
+  if (m && m->ready) cudaStreamWaitEvent(st, m->ready, 0);
+}
 bem_status cuda_fail(cudaError_t e, const char* where);
 void count_launch(long long k = 1);
 

@@ -238,6 +238,7 @@ bem_status mass_setup(bem_matrix* M, int kind) {
   M->mass_kind = kind;
   cudaError_t e;
   const cudaStream_t st = M->stream;
+  mesh_wait(m, st);
   if ((e = cudaMallocAsync((void**)&M->d_lo, sizeof(double) * n, st)) != cudaSuccess ||
       (e = cudaMallocAsync((void**)&M->d_di, sizeof(double) * n, st)) != cudaSuccess ||
       (e = cudaMallocAsync((void**)&M->d_up, sizeof(double) * n, st)) != cudaSuccess ||
@@ -337,28 +338,55 @@ bem_status mass_solve(const bem_matrix* M, int transpose, const double* x, doubl
 
 // ------------------------------------------------------------------ vector kernels
 // out[j] = sum_n Q[j*ldq + n] w[n] for j < k: one CTA per j, fixed-order tree reduction
+// out[j] = <Q_j, w> for j < k: 2-D grid (vector j, chunk c) writes partials, k_dots_sum adds the
+// chunks in fixed order (deterministic; enough CTAs to stream the k+1 vectors at HBM speed)
+constexpr int DOT_CHUNK = 8192;
+constexpr int DOT_MAXCH = 1024;
 __global__ void k_dots(const double* __restrict__ Q, long long ldq, const double* __restrict__ w,
-                       long long n, double* __restrict__ out) {
-  __shared__ double red[32];
-  const int j = blockIdx.x;
+                       long long n, long long chunk, double* __restrict__ part) {
+  __shared__ double red[8];
+  const int j = blockIdx.x, c = blockIdx.y;
   const double* q = Q + (long long)j * ldq;
+  const long long r0 = (long long)c * chunk, r1 = min(n, r0 + chunk);
   double s = 0.0;
-  for (long long r = threadIdx.x; r < n; r += blockDim.x) s = fma(q[r], w[r], s);
+  for (long long r = r0 + threadIdx.x; r < r1; r += blockDim.x) s = fma(q[r], w[r], s);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
   __syncthreads();
-  if (threadIdx.x < 32) {
-    s = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : 0.0;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (threadIdx.x == 0) out[j] = s;
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += red[k];
+    part[(long long)j * gridDim.y + c] = t;
   }
 }
+__global__ void k_dots_sum(const double* __restrict__ part, int nch, int k, double* __restrict__ out) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= k) return;
+  double s = 0.0;
+  for (int c = 0; c < nch; ++c) s += part[(long long)j * nch + c];
+  out[j] = s;
+}
+static double* g_dot_part[64] = {nullptr};
+static size_t g_dot_part_n[64] = {0};
 void vec_dots(const double* Q, long long ldq, int k, const double* w, long long n, double* out,
               cudaStream_t st) {
-  k_dots<<<k, 1024, 0, st>>>(Q, ldq, w, n, out);
-  count_launch();
+  const int nch = (int)std::max<long long>(1, std::min<long long>(DOT_MAXCH, (n + DOT_CHUNK - 1) / DOT_CHUNK));
+  const long long chunk = (n + nch - 1) / nch;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  dev &= 63;
+  const size_t need = (size_t)k * nch;
+  if (need > g_dot_part_n[dev]) {
+    // per-device scratch, grows rarely (largest k seen); stream-ordered free / allocation
+    if (g_dot_part[dev]) cudaFreeAsync(g_dot_part[dev], st);
+    g_dot_part_n[dev] = std::max<size_t>(need, 64 * 1024);
+    cudaMallocAsync((void**)&g_dot_part[dev], sizeof(double) * g_dot_part_n[dev], st);
+  }
+  dim3 grid(k, nch);
+  k_dots<<<grid, 256, 0, st>>>(Q, ldq, w, n, chunk, g_dot_part[dev]);
+  k_dots_sum<<<(k + 127) / 128, 128, 0, st>>>(g_dot_part[dev], nch, k, out);
+  count_launch(2);
 }
 
 // w[n] -= sum_j h[j] Q[j][n]

@@ -373,17 +373,20 @@ bem_status bem_mesh_create(const bem_mesh_desc* d, bem_comm* comm, bem_mesh** ou
     }
   bem_status st = upload_rules();
   if (st != BEM_OK) { delete m; return st; }
+  // stream-ordered uploads from the device pool on the legacy default stream; every call that
+  // uses the mesh on some stream first waits on m->ready (no host synchronisation here)
   auto up = [&](void** dst, const void* src, size_t bytes) -> cudaError_t {
-    cudaError_t r = cudaMalloc(dst, bytes);
+    cudaError_t r = cudaMallocAsync(dst, bytes, (cudaStream_t)0);
     if (r != cudaSuccess) return r;
-    return cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice);
+    return cudaMemcpyAsync(*dst, src, bytes, cudaMemcpyHostToDevice, (cudaStream_t)0);
   };
   if ((e = up((void**)&m->d_t, m->t.data(), sizeof(double) * m->t.size())) != cudaSuccess ||
       (e = up((void**)&m->d_seg, m->seg.data(), sizeof(Seg) * ng)) != cudaSuccess ||
       (e = up((void**)&m->d_half, m->half.data(), sizeof(Seg) * 2 * ng)) != cudaSuccess ||
       (e = up((void**)&m->d_dual, m->dual.data(), sizeof(Dual) * ng)) != cudaSuccess ||
       (e = up((void**)&m->d_lag, lagtab.data(), sizeof(double4) * lagtab.size())) != cudaSuccess ||
-      (e = cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking)) != cudaSuccess) {
+      (e = cudaEventCreateWithFlags(&m->ready, cudaEventDisableTiming)) != cudaSuccess ||
+      (e = cudaEventRecord(m->ready, (cudaStream_t)0)) != cudaSuccess) {
     bem_mesh_destroy(m);
     return cuda_fail(e, "bem_mesh_create/upload");
   }
@@ -410,12 +413,11 @@ bem_status bem_mesh_info_get(const bem_mesh* m, bem_mesh_info* info) {
 
 void bem_mesh_destroy(bem_mesh* m) {
   if (!m) return;
-  cudaFree(m->d_t);
-  cudaFree(m->d_seg);
-  cudaFree(m->d_half);
-  cudaFree(m->d_dual);
-  cudaFree(m->d_lag);
-  if (m->stream) cudaStreamDestroy(m->stream);
+  // stream-ordered on the legacy default stream (callers that used the mesh on another stream
+  // synchronise that stream first)
+  for (void* p : {(void*)m->d_t, (void*)m->d_seg, (void*)m->d_half, (void*)m->d_dual, (void*)m->d_lag})
+    if (p) cudaFreeAsync(p, (cudaStream_t)0);
+  if (m->ready) cudaEventDestroy(m->ready);
   delete m;
 }
 
