@@ -67,7 +67,11 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+            self.rows.append([time.perf_counter()] + [x.strip() for x in line.split(",")])
+
+    def window(self, t0, t1):
+        """keep only the samples taken inside [t0, t1] (the timed region)"""
+        self.t0, self.t1 = t0, t1
 
     def stop(self):
         if not self.proc:
@@ -77,7 +81,8 @@ class ClockSampler:
             self.proc.wait(timeout=5)
         except Exception:
             self.proc.kill()
-        rows = [r for r in self.rows if len(r) >= 7]
+        t0, t1 = getattr(self, "t0", -1e30), getattr(self, "t1", 1e30)
+        rows = [r[1:] for r in self.rows if len(r) >= 8 and t0 <= r[0] <= t1]
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
         sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
@@ -187,12 +192,14 @@ def native(args):
         mesh.close()
         return ph, rep, stats, info
 
-    for _ in range(args.warmup):
-        step(False)
-    barrier()
+    # the clock sampler (nvidia-smi) starts before the warm-up: its start-up stalls the driver for
+    # ~0.1 s, which must not land in the timed region; only samples inside the region are kept
     clocks = ClockSampler(local)
     if rank == 0:
         clocks.start()
+    for _ in range(args.warmup):
+        step(False)
+    barrier()
     S.launch_count(reset=True)
     barrier()
     t_wall = time.perf_counter()
@@ -223,6 +230,8 @@ def native(args):
     e2[1].record()
     barrier()
     t_e2e = e2[0].elapsed_time(e2[1]) / 1e3
+    if rank == 0:
+        clocks.window(t_wall, time.perf_counter())
     ck = clocks.stop() if rank == 0 else None
     if world > 1:
         tt = torch.tensor([t_dev, t_e2e], dtype=torch.float64, device=dev)
@@ -276,6 +285,24 @@ def native(args):
                  "bytes_per_launch": bytes_per_gemv,
                  "peak_note": "MEASURED_PEAKS.json hbm_gbs (driver-measured copy bandwidth)",
                  "bytes_note": "algorithmic: 8 B per stored entry (block lower triangle only) + 16 N"}
+    # context for the HBM roofline: MEASURED_PEAKS hbm_gbs is a copy (read + write) figure; a pure
+    # streaming read (torch.sum over 8 GiB, after the timed region) can exceed it
+    try:
+        buf = torch.empty(1024 ** 3, dtype=torch.float64, device=dev).fill_(1.0)
+        for _ in range(2):
+            buf.sum()
+        r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        r0.record()
+        for _ in range(5):
+            buf.sum()
+        r1.record()
+        r1.synchronize()
+        read_gbs = 5 * buf.numel() * 8 / (r0.elapsed_time(r1) * 1e-3) / 1e9
+        del buf
+    except Exception:
+        read_gbs = None
+    roof_gemv["read_peak_live_gbs"] = read_gbs
+    roof_gemv["frac_of_read_peak"] = (gemv_gbs / read_gbs) if (gemv_gbs and read_gbs) else None
     # the dominant kernel of the step by device time: the GEMV (all products of the solve) or the
     # longest assembly kernel
     gemv_total_ms = 1e3 * rep["seconds_matvec"]
