@@ -186,6 +186,8 @@ def native(args):
         ph["solve"] = ev[4].elapsed_time(ev[5]) / 1e3
         ph["total"] = ev[0].elapsed_time(ev[5]) / 1e3
         stats = {k: A.stats() for k, A in zip("VKD", (V, K, D))}
+        for k in "VKD":
+            ph[f"kern_{k}"] = (stats[k]["ms_records"] + stats[k]["ms_bulk"] + stats[k]["ms_near"] + stats[k]["ms_sing"]) / 1e3
         info = {f: getattr(mesh.info, f) for f, _ in mesh.info._fields_}
         for A in (V, K, D, Mp) + ((Mc,) if Mc else ()):
             A.close()
@@ -201,6 +203,11 @@ def native(args):
         step(False)
     barrier()
     S.launch_count(reset=True)
+    # host jitter: a Python garbage collection during the timed steps stalls the enqueueing thread
+    # (observed 70-130 ms once per run); collect now and pause the collector until the end
+    import gc
+    gc.collect()
+    gc.disable()
     barrier()
     t_wall = time.perf_counter()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -230,6 +237,7 @@ def native(args):
     e2[1].record()
     barrier()
     t_e2e = e2[0].elapsed_time(e2[1]) / 1e3
+    gc.enable()
     if rank == 0:
         clocks.window(t_wall, time.perf_counter())
     ck = clocks.stop() if rank == 0 else None

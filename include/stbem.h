@@ -210,6 +210,10 @@ bem_status bem_matrix_get_entries(const bem_matrix* A, long long count, const lo
 bem_status bem_matrix_info(const bem_matrix* A, int* kind, long long* entries, long long* bytes);
 bem_status bem_matrix_stats(const bem_matrix* A, bem_assembly_stats* out);
 void bem_matrix_destroy(bem_matrix* A);
+/* Dense matrix storage is cached by the library after bem_matrix_destroy and reused (stream-
+ * ordered) by the next assembly of a size that fits (<= 25% larger).  This returns every cached
+ * block to the CUDA device pool (synchronising with the pending frees).  Always BEM_OK. */
+bem_status bem_release_storage(void);
 
 /* ---------------------------------------------------------- diagnostics */
 /* device evaluation of the special functions used by the kernels (for the GPU pins):

@@ -14,6 +14,82 @@
 
 using namespace stb;
 
+namespace stb {
+
+// ---------------------------------------------------------------- matrix storage cache
+// Dense matrix storage (tens of GB per matrix) is kept by the library when a matrix is destroyed
+// and handed to the next assembly of a size that fits (at most 25% larger): repeated solves then
+// neither map new physical memory nor depend on the stream-ordered pool's fragmentation (which
+// cost a 65-130 ms stall about once per five C3 steps).  Reuse is stream-ordered: the destroy
+// records an event on the matrix's stream and the next user's stream waits on it.
+// bem_release_storage() returns the cached blocks to the device pool.
+struct CachedBlock {
+  void* ptr;
+  size_t bytes;
+  cudaEvent_t freed;
+};
+static std::mutex g_cache_mu;
+static std::vector<CachedBlock> g_cache[64];
+
+void pool_setup(int device) {
+  static bool ready[64] = {false};
+  if (ready[device & 63]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    unsigned long long thr = ~0ULL;   // keep freed pool memory mapped (no re-mapping cost)
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  ready[device & 63] = true;
+}
+
+constexpr size_t CACHE_MIN_BYTES = 1 << 20;
+
+cudaError_t storage_acquire(int device, size_t bytes, cudaStream_t st, void** out) {
+  pool_setup(device);
+  if (bytes < CACHE_MIN_BYTES) return cudaMallocAsync(out, bytes, st);
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    auto& c = g_cache[device & 63];
+    int best = -1;
+    for (int k = 0; k < (int)c.size(); ++k)
+      if (c[k].bytes >= bytes && c[k].bytes <= bytes + bytes / 4 && (best < 0 || c[k].bytes < c[best].bytes)) best = k;
+    if (best >= 0) {
+      CachedBlock b = c[best];
+      c.erase(c.begin() + best);
+      cudaStreamWaitEvent(st, b.freed, 0);
+      cudaEventDestroy(b.freed);
+      *out = b.ptr;
+      return cudaSuccess;
+    }
+  }
+  cudaError_t e = cudaMallocAsync(out, bytes, st);
+  if (e == cudaErrorMemoryAllocation) {
+    // release the cache to the pool and retry once
+    cudaGetLastError();
+    bem_release_storage();
+    e = cudaMallocAsync(out, bytes, st);
+  }
+  return e;
+}
+
+void storage_release(int device, void* ptr, size_t bytes, cudaStream_t st) {
+  if (!ptr) return;
+  if (bytes < CACHE_MIN_BYTES) {
+    cudaFreeAsync(ptr, st);
+    return;
+  }
+  cudaEvent_t ev;
+  if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess || cudaEventRecord(ev, st) != cudaSuccess) {
+    cudaGetLastError();
+    cudaFreeAsync(ptr, st);
+    return;
+  }
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  g_cache[device & 63].push_back({ptr, bytes, ev});
+}
+
+}  // namespace stb
+
 namespace {
 
 inline cudaStream_t S(bem_stream s) { return reinterpret_cast<cudaStream_t>(s); }
@@ -34,18 +110,8 @@ bem_matrix* new_dense(const bem_mesh* m, int kind, cudaStream_t stream, bem_stat
     }
   }
   A->entries = off;
-  // stream-ordered allocation from the device pool, which keeps freed matrix storage for the
-  // next assembly (repeated solves do not pay cudaMalloc / cudaFree of tens of GB)
-  static bool pool_ready = false;
-  if (!pool_ready) {
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, m->device) == cudaSuccess) {
-      unsigned long long thr = ~0ULL;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-    pool_ready = true;
-  }
-  cudaError_t e = cudaMallocAsync(&A->data, sizeof(double) * std::max<long long>(off, 4), stream);
+  const size_t bytes = sizeof(double) * std::max<long long>(off, 4);
+  cudaError_t e = storage_acquire(m->device, bytes, stream, (void**)&A->data);
   if (e != cudaSuccess) {
     *st = BEM_E_NOMEM;
     set_error(std::string("matrix allocation of ") + std::to_string(8.0 * off / 1e9) + " GB failed: " + cudaGetErrorString(e));
@@ -53,6 +119,7 @@ bem_matrix* new_dense(const bem_mesh* m, int kind, cudaStream_t stream, bem_stat
     delete A;
     return nullptr;
   }
+  A->data_bytes = bytes;
   *st = BEM_OK;
   return A;
 }
@@ -208,13 +275,14 @@ bem_status bem_solve_gmres(const bem_matrix* V, const bem_matrix* D, const bem_m
   hpin = pin_buf;
   mesh_wait(m, st);
   // stream-ordered allocations: no device-wide synchronisation
-  if ((e = cudaMallocAsync(&Q, sizeof(double) * n * (kmax + 1), st)) != cudaSuccess ||
+  const size_t q_bytes = sizeof(double) * n * (kmax + 1);
+  if ((e = storage_acquire(m->device, q_bytes, st, (void**)&Q)) != cudaSuccess ||
       (e = cudaMallocAsync(&tmp, sizeof(double) * n, st)) != cudaSuccess ||
       (e = cudaMallocAsync(&u, sizeof(double) * n, st)) != cudaSuccess ||
       (e = cudaMallocAsync(&v, sizeof(double) * n, st)) != cudaSuccess ||
       (e = cudaMallocAsync(&wk, sizeof(double) * n, st)) != cudaSuccess ||
       (e = cudaMallocAsync(&dh, sizeof(double) * 2 * (kmax + 2), st)) != cudaSuccess) {
-    cudaFreeAsync(Q, st); cudaFreeAsync(tmp, st); cudaFreeAsync(u, st); cudaFreeAsync(v, st);
+    storage_release(m->device, Q, q_bytes, st); cudaFreeAsync(tmp, st); cudaFreeAsync(u, st); cudaFreeAsync(v, st);
     cudaFreeAsync(wk, st); cudaFreeAsync(dh, st);
     cudaGetLastError();
     set_error("bem_solve_gmres: allocation failed");
@@ -345,7 +413,7 @@ bem_status bem_solve_gmres(const bem_matrix* V, const bem_matrix* D, const bem_m
   }
   for (auto x : mvev) cudaEventDestroy(x);
   e = cudaGetLastError();
-  cudaFreeAsync(Q, st); cudaFreeAsync(tmp, st); cudaFreeAsync(u, st); cudaFreeAsync(v, st);
+  storage_release(m->device, Q, q_bytes, st); cudaFreeAsync(tmp, st); cudaFreeAsync(u, st); cudaFreeAsync(v, st);
   cudaFreeAsync(wk, st); cudaFreeAsync(dh, st);
   cudaStreamSynchronize(st);
   cudaEventDestroy(e0); cudaEventDestroy(e1);
@@ -458,12 +526,27 @@ bem_status bem_matrix_info(const bem_matrix* A, int* kind, long long* entries, l
   return BEM_OK;
 }
 
+bem_status bem_release_storage(void) {
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  for (auto& c : g_cache)
+    for (auto& b : c) {
+      cudaEventSynchronize(b.freed);
+      cudaEventDestroy(b.freed);
+      cudaFree(b.ptr);
+    }
+  for (auto& c : g_cache) c.clear();
+  cudaGetLastError();
+  return BEM_OK;
+}
+
 void bem_matrix_destroy(bem_matrix* A) {
   if (!A) return;
   // stream-ordered: the storage returns to the pool after the work queued on the matrix's
   // stream (callers that used the matrix on another stream synchronise that stream first)
   const cudaStream_t st = A->stream;
-  for (void* p : {(void*)A->data, (void*)A->d_segs, (void*)A->d_partials, (void*)A->d_row_pbase,
+  if (A->data) storage_release(A->mesh ? A->mesh->device : 0, A->data, A->data_bytes, st);
+  storage_release(A->mesh ? A->mesh->device : 0, A->d_partials, A->partials_bytes, st);
+  for (void* p : {(void*)A->d_segs, (void*)A->d_row_pbase,
                   (void*)A->d_row_pstride, (void*)A->d_ysum, (void*)A->d_lo, (void*)A->d_di,
                   (void*)A->d_up, (void*)A->d_work, (void*)A->d_ctr})
     if (p) cudaFreeAsync(p, st);

@@ -329,7 +329,8 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bul
   A->fused_sing = fused_sing ? 1 : 0;
   double* d_rec = nullptr;
   unsigned long long* d_ctr = nullptr;
-  if ((e = cudaMallocAsync((void**)&d_rec, sizeof(double) * nf * (2 * npairs + nsrec), st)) != cudaSuccess ||
+  const size_t rec_bytes = sizeof(double) * nf * (2 * npairs + nsrec);
+  if ((e = storage_acquire(m->device, rec_bytes, st, (void**)&d_rec)) != cudaSuccess ||
       (e = cudaMallocAsync((void**)&d_ctr, sizeof(unsigned long long) * 15, st)) != cudaSuccess ||
       (e = cudaMemsetAsync(d_ctr, 0, sizeof(unsigned long long) * 15, st)) != cudaSuccess) {
     cudaFreeAsync(d_poff, st);
@@ -416,7 +417,7 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bul
       A->launches += 2;
     }
   }
-  cudaFreeAsync(d_rec, st);
+  storage_release(m->device, d_rec, rec_bytes, st);
   cudaFreeAsync(d_poff, st);
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "assemble/launch");

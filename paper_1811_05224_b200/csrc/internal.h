@@ -93,6 +93,7 @@ struct bem_matrix_s {
   bool stats_ready = true;
   // dense block-lower-triangular storage (V, K, D)
   double* data = nullptr;
+  size_t data_bytes = 0;       // size of the storage block (>= 8 * entries; cached on destroy)
   long long entries = 0;       // stored doubles (with row padding)
   std::vector<long long> poff; // per block, per local test step: panel offset (flattened)
   std::vector<int> poff_base;  // per block: index of its first panel in poff
@@ -117,6 +118,7 @@ struct bem_matrix_s {
   long long* d_row_pbase = nullptr;
   int* d_row_pstride = nullptr;
   double* d_partials = nullptr;
+  size_t partials_bytes = 0;
   double* d_ysum = nullptr;  // multi-GPU partial y
   // mass matrices: three cyclic diagonals per row (lower = col i-1, diag, upper = col i+1)
   int mass_kind = -1;
@@ -150,6 +152,11 @@ struct Rules {
 };
 const Rules& host_rules();
 bem_status upload_rules();  // copy to __constant__ memory (per device, once)
+
+// device storage (api.cpp): blocks >= 1 MB are cached after release and reused stream-ordered by
+// the next acquire of a size that fits (<= 25% larger); smaller ones use the device pool
+cudaError_t storage_acquire(int device, size_t bytes, cudaStream_t st, void** out);
+void storage_release(int device, void* ptr, size_t bytes, cudaStream_t st);
 
 // kernels (assemble.cu)
 bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bulk, int q_sing,

@@ -150,7 +150,8 @@ bem_status gemv_setup(bem_matrix* A) {
   size_t nseg = std::max<size_t>(1, A->segs.size());
   if ((e = cudaMallocAsync((void**)&A->d_segs, sizeof(GSeg) * nseg, st)) != cudaSuccess) return cuda_fail(e, "gemv_setup");
   if ((e = cudaMemcpyAsync(A->d_segs, A->segs.data(), sizeof(GSeg) * A->segs.size(), cudaMemcpyHostToDevice, st)) != cudaSuccess) return cuda_fail(e, "gemv_setup");
-  if ((e = cudaMallocAsync((void**)&A->d_partials, sizeof(double) * std::max<long long>(1, A->n_partials), st)) != cudaSuccess) return cuda_fail(e, "gemv_setup");
+  A->partials_bytes = sizeof(double) * std::max<long long>(1, A->n_partials);
+  if ((e = storage_acquire(m->device, A->partials_bytes, st, (void**)&A->d_partials)) != cudaSuccess) return cuda_fail(e, "gemv_setup");
   if ((e = cudaMallocAsync((void**)&A->d_row_pbase, sizeof(long long) * nt, st)) != cudaSuccess) return cuda_fail(e, "gemv_setup");
   if ((e = cudaMallocAsync((void**)&A->d_row_pstride, sizeof(int) * nt, st)) != cudaSuccess) return cuda_fail(e, "gemv_setup");
   if ((e = cudaMemcpyAsync(A->d_row_pbase, A->row_pbase.data(), sizeof(long long) * nt, cudaMemcpyHostToDevice, st)) != cudaSuccess) return cuda_fail(e, "gemv_setup");

@@ -110,6 +110,7 @@ _SIGS = {
     "bem_matrix_info": (I, [P, P, P, P]),
     "bem_matrix_stats": (I, [P, ctypes.POINTER(AssemblyStats)]),
     "bem_matrix_destroy": (None, [P]),
+    "bem_release_storage": (I, []),
     "bem_eval_special": (I, [I, LL, P, P, P]),
 }
 
