@@ -186,6 +186,8 @@ def native(args):
         ph["solve"] = ev[4].elapsed_time(ev[5]) / 1e3
         ph["total"] = ev[0].elapsed_time(ev[5]) / 1e3
         stats = {k: A.stats() for k, A in zip("VKD", (V, K, D))}
+        for k, A in zip("VKD", (V, K, D)):
+            stats[k]["bytes"] = A.info()["bytes"]
         for k in "VKD":
             ph[f"kern_{k}"] = (stats[k]["ms_records"] + stats[k]["ms_bulk"] + stats[k]["ms_near"] + stats[k]["ms_sing"]) / 1e3
         info = {f: getattr(mesh.info, f) for f, _ in mesh.info._fields_}
@@ -246,7 +248,11 @@ def native(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_dev, t_e2e = tt.tolist()
     entries_total = info["entries_total"]
-    units_per_step = 3 * entries_total                     # V, K, D entries (element-pair integrals)
+    # units: the distinct element-pair integrals computed and stored per step (V_h and D_h keep the
+    # upper 32 x 32 tile triangle of their symmetric spatial blocks, K_h all entries); the matrix
+    # entries they represent (3 x entries_total) are reported beside
+    units_per_step = sum(stats[k]["entries"] for k in "VKD")
+    represented_per_step = 3 * entries_total
     ms = 1e3 * t_dev / args.steps
     value = units_per_step * args.steps / t_dev
     e2e = units_per_step * args.steps / t_e2e
@@ -254,7 +260,9 @@ def native(args):
     rep = reps[-1]
     # GEMV bandwidth: algorithmic bytes per product = 8 * stored entries (owned) + 16 N
     n = w.n
-    bytes_per_gemv = 8 * info["entries_owned"] + 16 * n
+    # bytes actually read per product of the solve (V_h and D_h alternate) + x and y
+    bytes_per_gemv = (rep["n_matvec_V"] * stats["V"]["bytes"] + rep["n_matvec_D"] * stats["D"]["bytes"]) / \
+        max(1, rep["n_matvec_V"] + rep["n_matvec_D"]) + 16 * n
     n_mv = rep["n_matvec_V"] + rep["n_matvec_D"]
     gemv_s = rep["seconds_matvec"] / max(1, n_mv)
     peaks = json.load(open(PEAKS_PATH)) if os.path.exists(PEAKS_PATH) else {}
@@ -270,7 +278,9 @@ def native(args):
     ms_dom, kdom, _, st = max(fam)
     flops = st["flops_bulk"]
     achieved = flops / (ms_dom * 1e-3) / 1e12
-    bulk_entries = info["entries_owned"] - 2 * w.n_gamma ** 2 * w.n_steps + w.n_gamma ** 2  # cells d >= 2
+    nt_ = w.n_steps
+    cells = nt_ * (nt_ + 1) / 2
+    bulk_entries = stats[kdom]["entries"] * (cells - (2 * nt_ - 1)) / cells   # stored entries of cells d >= 2
     store_gbs = 8.0 * bulk_entries / (ms_dom * 1e-3) / 1e9
     traffic = {}
     tpath = os.path.join(ROOT, "profiles", "r01_traffic.json")
@@ -292,7 +302,8 @@ def native(args):
                  "frac": (gemv_gbs / hbm_peak) if gemv_gbs else None, "traffic": traffic.get("k_gemv"),
                  "bytes_per_launch": bytes_per_gemv,
                  "peak_note": "MEASURED_PEAKS.json hbm_gbs (driver-measured copy bandwidth)",
-                 "bytes_note": "algorithmic: 8 B per stored entry (block lower triangle only) + 16 N"}
+                 "bytes_note": "algorithmic: 8 B per stored double of the product's matrix (block lower "
+                               "triangle; V_h / D_h symmetric packed spatial blocks) + 16 N"}
     # context for the HBM roofline: MEASURED_PEAKS hbm_gbs is a copy (read + write) figure; a pure
     # streaming read (torch.sum over 8 GiB, after the timed region) can exceed it
     try:
@@ -327,6 +338,9 @@ def native(args):
                    "l2": "inputs larger than L2 (each matrix 17 GB >> 126 MB)"},
         "components": {
             "assembly_pairs_per_s": units_per_step / asm_s,
+            "integrals_per_step": {k: stats[k]["entries"] for k in "VKD"},
+            "matrix_entries_represented_per_s": represented_per_step / (1e-3 * ms),
+            "storage": "V_h, D_h: symmetric packed spatial blocks (upper 32x32 tile triangle); K_h full",
             "assembly_s": {"V": ph["assemble_V"], "K": ph["assemble_K"], "D": ph["assemble_D"]},
             "matvec_gbs": gemv_gbs, "matvec_frac_of_hbm": (gemv_gbs / hbm_peak) if gemv_gbs else None,
             "gmres_solve_s": ph["solve"], "gmres_iterations": rep["iterations"],

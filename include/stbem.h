@@ -76,6 +76,9 @@ typedef struct {
                    of moment records; 0 = records whenever alpha (h_X+h_Y)^2 / (4 min h_t) < 4 */
 } bem_quad_opts;
 #define BEM_QUAD_LEGACY_SING 1
+/* V_h and D_h store their symmetric spatial blocks packed (upper 32 x 32 tile triangle, about
+ * half the bytes and half the assembly work); this flag stores them full */
+#define BEM_QUAD_FULL_STORAGE 2
 
 typedef enum {
   BEM_MASS_PRIMAL = 0,      /* M_h of eq. (4): <phi^10_(a,n), phi^0_(a,i)> */

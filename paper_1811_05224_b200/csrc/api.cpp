@@ -94,19 +94,22 @@ namespace {
 
 inline cudaStream_t S(bem_stream s) { return reinterpret_cast<cudaStream_t>(s); }
 
-bem_matrix* new_dense(const bem_mesh* m, int kind, cudaStream_t stream, bem_status* st) {
+bem_matrix* new_dense(const bem_mesh* m, int kind, bool sym, cudaStream_t stream, bem_status* st) {
   bem_matrix* A = new bem_matrix_s();
   A->kind = kind;
   A->mesh = m;
   A->stream = stream;
+  A->sym = sym ? 1 : 0;
   const int ng = m->ng;
+  A->blk_elems = sym ? sym_blk_elems(ng) : 0;
   long long off = 0;
   for (size_t bi = 0; bi < m->blocks.size(); ++bi) {
     const Block& b = m->blocks[bi];
     A->poff_base.push_back((int)A->poff.size());
     for (int a = b.a0; a < b.a1; ++a) {
       A->poff.push_back(off);
-      off += (long long)ng * pad4((long long)panel_nb(a, b.b0, b.b1) * ng);
+      off += sym ? (long long)panel_nb(a, b.b0, b.b1) * A->blk_elems
+                 : (long long)ng * pad4((long long)panel_nb(a, b.b0, b.b1) * ng);
     }
   }
   A->entries = off;
@@ -134,7 +137,9 @@ bem_status assemble(int kind, const bem_mesh* m, const bem_quad_opts* o, bem_str
   if (m->ng < 6) { set_error("bem_assemble: N_Gamma >= 6 required"); return BEM_E_INVALID; }
   cudaSetDevice(m->device);
   bem_status st;
-  bem_matrix* A = new_dense(m, kind, S(s), &st);
+  // V_h and D_h: symmetric packed spatial blocks unless BEM_QUAD_FULL_STORAGE
+  const bool sym = (kind == STB_V || kind == STB_D) && !(o && (o->flags & BEM_QUAD_FULL_STORAGE));
+  bem_matrix* A = new_dense(m, kind, sym, S(s), &st);
   if (!A) return st;
   // no memset: the bulk kernel writes every entry of the cells d >= 2 and the near kernel every
   // entry of the cells d <= 1 (the row padding is never read)
@@ -158,8 +163,13 @@ long long entry_offset(const bem_matrix* A, int a, int i, int b, int j) {
   for (size_t bi = 0; bi < m->blocks.size(); ++bi) {
     const Block& B = m->blocks[bi];
     if (B.I == I && B.J == J) {
+      const long long p0 = A->poff[A->poff_base[bi] + (a - B.a0)];
+      if (A->sym) {
+        if (i / SYM_TS > j / SYM_TS) std::swap(i, j);   // the lower tile triangle mirrors the upper
+        return p0 + (long long)(b - B.b0) * A->blk_elems + sym_in_block(i, j, sym_nt(m->ng));
+      }
       long long ld = pad4((long long)panel_nb(a, B.b0, B.b1) * m->ng);
-      return A->poff[A->poff_base[bi] + (a - B.a0)] + (long long)i * ld + (long long)(b - B.b0) * m->ng + j;
+      return p0 + (long long)i * ld + (long long)(b - B.b0) * m->ng + j;
     }
   }
   return -1;
@@ -515,9 +525,15 @@ bem_status bem_matrix_info(const bem_matrix* A, int* kind, long long* entries, l
   if (kind) *kind = A->kind;
   long long ent = 0;
   if (A->kind != STB_MASS) {
+    // distinct stored entries (sym: the entries (i, j) with i / 32 <= j / 32, i, j < N_Gamma)
     const bem_mesh* m = A->mesh;
+    long long per_block = (long long)m->ng * m->ng;
+    if (A->sym) {
+      per_block = 0;
+      for (int i = 0; i < m->ng; ++i) per_block += m->ng - (i / SYM_TS) * SYM_TS;
+    }
     for (auto& b : m->blocks)
-      for (int a = b.a0; a < b.a1; ++a) ent += (long long)m->ng * m->ng * panel_nb(a, b.b0, b.b1);
+      for (int a = b.a0; a < b.a1; ++a) ent += per_block * panel_nb(a, b.b0, b.b1);
   } else {
     ent = 3LL * A->mesh->ng * A->mesh->nt;
   }

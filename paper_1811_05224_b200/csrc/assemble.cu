@@ -56,9 +56,14 @@ struct BlockArgs {
   const double4* lag;     // (s, ln s, 1/s) per time-node pair
   int ldlag;              // n_steps + 1
   int qfar;               // near-cell Gauss order for well-separated pairs
+  int sym;                // symmetric packed spatial blocks (only tiles ti <= tj are written)
+  int nt;                 // sym: tiles per block side
+  long long blk;          // sym: stored doubles per (a,b) block
 };
 
+// sym: the caller guarantees i / 32 <= j / 32 (the upper tile triangle)
 __device__ __forceinline__ double* entry_ptr(const BlockArgs& B, int a, int i, int b, int j) {
+  if (B.sym) return B.out + B.poff[a - B.a0] + (long long)(b - B.b0) * B.blk + sym_in_block(i, j, B.nt);
   long long ld = pad4((long long)panel_nb(a, B.b0, B.b1) * B.ng);
   return B.out + B.poff[a - B.a0] + (long long)i * ld + (long long)(b - B.b0) * B.ng + j;
 }
@@ -260,7 +265,7 @@ __global__ void __launch_bounds__(128) k_sing(BlockArgs B, const Seg* __restrict
           add += nn * pair_touching<1>(X, Y, rel, Lg, alpha, nsing, vl[m][0], vl[m][1], vk[nn_][0], vk[nn_][1]);
       }
   }
-  if ((threadIdx.x & 31) == 0) *entry_ptr(B, a, i, b, jcol) += add;
+  if ((threadIdx.x & 31) == 0 && !(B.sym && i / SYM_TS > jcol / SYM_TS)) *entry_ptr(B, a, i, b, jcol) += add;
 }
 
 // ================================================================= launch
@@ -368,6 +373,11 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bul
   fam.push_back(3);
   A->launches += 2;
   A->nodes_expected = 0;
+  long long npairs_computed = npairs;   // sym: the pairs (I, J) of the upper tile triangle
+  if (A->sym) {
+    npairs_computed = 0;
+    for (int i = 0; i < ng; ++i) npairs_computed += ng - (i / SYM_TS) * SYM_TS;
+  }
   for (size_t bi = 0; bi < m->blocks.size(); ++bi) {
     const Block& blk = m->blocks[bi];
     BlockArgs BA;
@@ -378,6 +388,9 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bul
     BA.lag = m->d_lag;
     BA.ldlag = m->nt + 1;
     BA.qfar = qfar;
+    BA.sym = A->sym;
+    BA.nt = sym_nt(ng);
+    BA.blk = A->blk_elems;
     const int R = 8;
     const int nband = (blk.a1 - blk.a0 + R - 1) / R;
     if (blk.a1 - 1 - blk.b0 >= 2) {
@@ -387,7 +400,7 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bul
       mark();
       fam.push_back(0);
       A->launches++;
-      A->nodes_expected += bulk_nodes(blk, R) * npairs;
+      A->nodes_expected += bulk_nodes(blk, R) * npairs_computed;
     }
     const bool has_near = blk.b1 - 1 >= blk.a0 - 1 && blk.b0 <= blk.a1 - 1;
     if (has_near) {

@@ -40,6 +40,24 @@ inline __host__ __device__ int panel_nb(int a, int b0, int b1) {
 }
 inline __host__ __device__ long long pad4(long long v) { return (v + 3) & ~3LL; }
 
+// symmetric packed storage of the spatial blocks of V_h and D_h (V_ab(i,j) = V_ab(j,i): the
+// kernels of P:86 and P:123 depend on |x - y| and on (x, y) symmetrically, test and trial spaces
+// coincide).  Each N_Gamma x N_Gamma block (a,b) keeps the tiles (ti <= tj) of its upper tile
+// triangle, 32 x 32 row-major each (diagonal tiles full), in row-major tile order.
+constexpr int SYM_TS = 32;
+inline __host__ __device__ int sym_nt(int ng) { return (ng + SYM_TS - 1) / SYM_TS; }
+inline __host__ __device__ long long sym_blk_elems(int ng) {
+  const long long nt = sym_nt(ng);
+  return nt * (nt + 1) / 2 * SYM_TS * SYM_TS;
+}
+inline __host__ __device__ long long sym_tile_index(int ti, int tj, int nt) {
+  return (long long)ti * nt - (long long)ti * (ti - 1) / 2 + (tj - ti);
+}
+// offset inside a block of entry (i, j) with i / 32 <= j / 32
+inline __host__ __device__ long long sym_in_block(int i, int j, int nt) {
+  return sym_tile_index(i / SYM_TS, j / SYM_TS, nt) * (SYM_TS * SYM_TS) + (i % SYM_TS) * SYM_TS + (j % SYM_TS);
+}
+
 // flat description of the quadrature rules on the device
 constexpr int QMAX = 16;
 constexpr int QSING_MAX = 16;
@@ -93,6 +111,8 @@ struct bem_matrix_s {
   bool stats_ready = true;
   // dense block-lower-triangular storage (V, K, D)
   double* data = nullptr;
+  int sym = 0;                 // symmetric packed spatial blocks (V, D)
+  long long blk_elems = 0;     // sym: stored doubles per (a,b) block
   size_t data_bytes = 0;       // size of the storage block (>= 8 * entries; cached on destroy)
   long long entries = 0;       // stored doubles (with row padding)
   std::vector<long long> poff; // per block, per local test step: panel offset (flattened)

@@ -76,6 +76,84 @@ __global__ void __launch_bounds__(GEMV_WARPS * 32) k_gemv(const double* __restri
   }
 }
 
+// ---------------------------------------------------------------- symmetric packed blocks
+// reduce-scatter of 32 per-lane values over the warp: lane r returns sum over lanes of v[r]
+__device__ __forceinline__ double reduce_scatter32(double (&v)[32], int lane) {
+#pragma unroll
+  for (int h = 16; h >= 1; h >>= 1) {
+    const bool up = (lane & h) != 0;
+#pragma unroll
+    for (int r = 0; r < h; ++r) {
+      const double keep = up ? v[r + h] : v[r];
+      const double send = up ? v[r] : v[r + h];
+      v[r] = keep + __shfl_xor_sync(0xffffffffu, send, h);
+    }
+  }
+  return v[0];
+}
+
+// SYMV of the packed block-lower-triangular matrix: one CTA per (a, b) block, its upper-triangle
+// tiles dealt to the warps; an off-diagonal tile T = V_ab[ti, tj] contributes T x_b[tj] to
+// y_a[ti] (row sums: a warp reduce-scatter) and T^T x_b[ti] to y_a[tj] (column sums, lane-local);
+// each warp accumulates into its own shared-memory copy of y_a, summed in fixed order into one
+// partial per (row, b) (deterministic).  Every stored double is read once from HBM.
+constexpr int SYMV_WARPS = 4;
+__global__ void __launch_bounds__(SYMV_WARPS * 32) k_gemv_sym(const double* __restrict__ A,
+                                                             const GSeg* __restrict__ segs, int nseg,
+                                                             long long n_items, int ng, long long blk,
+                                                             const double* __restrict__ x,
+                                                             double* __restrict__ partial) {
+  extern __shared__ double sm[];
+  const int nt = sym_nt(ng), L = nt * SYM_TS, ntp = nt * (nt + 1) / 2;
+  double* xs = sm;
+  double* ys = sm + L;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double* yw = ys + w * L;
+  for (long long it = blockIdx.x; it < n_items; it += gridDim.x) {
+    int lo = 0, hi = nseg - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (segs[mid].item0 <= it) lo = mid; else hi = mid - 1;
+    }
+    const GSeg S = segs[lo];
+    const int bl = (int)(it - S.item0);               // b - b0
+    const double* __restrict__ blkp = A + S.off + (long long)bl * blk;
+    const double* __restrict__ xb = x + S.xoff + (long long)bl * ng;
+    __syncthreads();                                   // the previous item's y is written out
+    for (int k = threadIdx.x; k < L; k += blockDim.x) xs[k] = k < ng ? xb[k] : 0.0;
+    for (int k = threadIdx.x; k < SYMV_WARPS * L; k += blockDim.x) ys[k] = 0.0;
+    __syncthreads();
+    int ti = 0, tj = w;                                // tile t = w in row-major upper order
+    while (tj >= nt) { tj -= nt - ti - 1; ++ti; }
+    for (int t = w; t < ntp; t += SYMV_WARPS) {
+      const double* __restrict__ tp = blkp + (long long)t * (SYM_TS * SYM_TS);
+      const bool cok = tj * SYM_TS + lane < ng;
+      double v[32];
+#pragma unroll
+      for (int r = 0; r < 32; ++r) v[r] = (cok && ti * SYM_TS + r < ng) ? __ldcs(tp + r * SYM_TS + lane) : 0.0;
+      if (ti != tj) {
+        double s = 0.0;
+#pragma unroll
+        for (int r = 0; r < 32; ++r) s = fma(v[r], xs[ti * SYM_TS + r], s);
+        yw[tj * SYM_TS + lane] += s;
+      }
+      const double xj = xs[tj * SYM_TS + lane];
+#pragma unroll
+      for (int r = 0; r < 32; ++r) v[r] *= xj;
+      yw[ti * SYM_TS + lane] += reduce_scatter32(v, lane);
+      tj += SYMV_WARPS;                                 // advance to tile t + SYMV_WARPS
+      while (tj >= nt && ti < nt) { tj -= nt - ti - 1; ++ti; }
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < ng; k += blockDim.x) {
+      double y = 0.0;
+#pragma unroll
+      for (int ww = 0; ww < SYMV_WARPS; ++ww) y += ys[ww * L + k];
+      partial[S.pbase + (long long)k * S.pstride + bl] = y;
+    }
+  }
+}
+
 // y[a*ng + i] = alpha * sum_k partial[row_pbase[a] + i*stride + k] + beta * y
 __global__ void k_gemv_reduce(const double* __restrict__ partial, const long long* __restrict__ pbase,
                               const int* __restrict__ pstride, int ng, int nt, double alpha,
@@ -102,7 +180,8 @@ bem_status gemv_setup(bem_matrix* A) {
     for (int a = b.a0; a < b.a1; ++a) {
       long long len = (long long)panel_nb(a, b.b0, b.b1) * ng;
       if (len <= 0) continue;
-      int nch = (int)((len + gemv_ch() - 1) / gemv_ch());
+      // full storage: chunks of GEMV_CH columns; sym: one partial per trial block b
+      int nch = A->sym ? panel_nb(a, b.b0, b.b1) : (int)((len + gemv_ch() - 1) / gemv_ch());
       blk_of_a[a].push_back({(int)bi, nch});
     }
   }
@@ -123,7 +202,7 @@ bem_status gemv_setup(bem_matrix* A) {
     for (int a = b.a0; a < b.a1; ++a) {
       long long len = (long long)panel_nb(a, b.b0, b.b1) * ng;
       if (len <= 0) continue;
-      int nch = (int)((len + gemv_ch() - 1) / gemv_ch());
+      int nch = A->sym ? panel_nb(a, b.b0, b.b1) : (int)((len + gemv_ch() - 1) / gemv_ch());
       int cbase = 0;
       for (auto& pr : blk_of_a[a]) {
         if (pr.first == (int)bi) break;
@@ -141,7 +220,7 @@ bem_status gemv_setup(bem_matrix* A) {
       s.a = a;
       s.pad = 0;
       A->segs.push_back(s);
-      item += (long long)ng * nch;
+      item += A->sym ? (long long)nch : (long long)ng * nch;   // sym: one item per (a, b) block
     }
   }
   A->n_items = item;
@@ -189,7 +268,12 @@ bem_status gemv_launch(const bem_matrix* A, double a, const double* x, double b,
                        cudaStream_t st) {
   const bem_mesh* m = A->mesh;
   const long long n = (long long)m->ng * m->nt;
-  if (A->n_items > 0) {
+  if (A->n_items > 0 && A->sym) {
+    const size_t smem = sizeof(double) * (1 + SYMV_WARPS) * sym_nt(m->ng) * SYM_TS;
+    const long long blocks = std::min<long long>(A->n_items, 1LL << 30);
+    k_gemv_sym<<<(unsigned)blocks, SYMV_WARPS * 32, smem, st>>>(A->data, A->d_segs, (int)A->segs.size(), A->n_items, m->ng, A->blk_elems, x, A->d_partials);
+    count_launch();
+  } else if (A->n_items > 0) {
     long long blocks = std::min<long long>((A->n_items + GEMV_WARPS - 1) / GEMV_WARPS,
                                            (long long)num_sms() * gemv_ctas_per_sm());
     k_gemv<GEMV_UNROLL><<<(unsigned)blocks, GEMV_WARPS * 32, 0, st>>>(A->data, A->d_segs, (int)A->segs.size(), A->n_items, m->ng, x, A->d_partials, gemv_ch());

@@ -513,17 +513,24 @@ __global__ void __launch_bounds__(128) k_bulk_m(BlockArgs B, MomArgs M) {
   if (r_hi <= r_lo) return;                       // CTA-uniform
   const int bmax = min(B.b1 - 1, r_hi - 1 - 2);
   if (bmax < B.b0) return;                        // CTA-uniform
+  // sym: the CTA's 4 rows lie in tile row (4 blockIdx.y) / 32, its 32 columns in tile column
+  // blockIdx.x; tiles below the tile diagonal are the mirror images of stored ones
+  const int ti = (blockIdx.y * 4) / SYM_TS, tj = blockIdx.x;
+  if (B.sym && ti > tj) return;                   // CTA-uniform
   const long long pair = (long long)I * ng + J;
   const long long S = M.npairs;
-  // row offsets of the band rows a = r_lo + r for this warp's row I (panel offset + I * ld),
-  // shared by the warp: a store is then one LDS + one address add
+  // row offsets of the band rows a = r_lo + r for this warp's row I (panel offset + I * ld, or
+  // the tile's offset + (I mod 32) * 32), shared by the warp: a store is one LDS + one address add
   __shared__ long long s_row[4][R];
   long long* srow = s_row[threadIdx.x >> 5];
   if (lane < R) {
     const int a = min(r_lo + lane, r_hi - 1);
-    srow[lane] = B.poff[a - B.a0] + (long long)I * pad4((long long)panel_nb(a, B.b0, B.b1) * ng);
+    srow[lane] = B.poff[a - B.a0] + (B.sym ? sym_tile_index(ti, tj, B.nt) * (SYM_TS * SYM_TS) + (long long)(I % SYM_TS) * SYM_TS
+                                           : (long long)I * pad4((long long)panel_nb(a, B.b0, B.b1) * ng));
   }
   __syncwarp();
+  const long long cstride = B.sym ? B.blk : (long long)ng;   // per trial step b
+  const int jcol = B.sym ? J % SYM_TS : J;
   RegA<KIND> A;
   A.load(M.rec + pair, S);
   RegBZ<KIND> Z;
@@ -591,7 +598,7 @@ __global__ void __launch_bounds__(128) k_bulk_m(BlockArgs B, MomArgs M) {
     }
     if (y > B.b0) {
       const int b = y - 1;
-      double* col = B.out + ((long long)(b - B.b0) * ng + J);
+      double* col = B.out + ((long long)(b - B.b0) * cstride + jcol);
 #pragma unroll
       for (int r = 1; r <= R; ++r) {
         const int a = r_lo + r - 1;
@@ -623,6 +630,7 @@ __global__ void __launch_bounds__(128) k_near_m(BlockArgs B, MomArgs M, int chun
   const int I = min(I0, ng - 1), J = min(J0, ng - 1);
   const int a_beg = B.a0 + blockIdx.z * chunk;
   const int a_end = min(B.a1, a_beg + chunk);
+  if (B.sym && (int)(blockIdx.y * 4) / SYM_TS > (int)blockIdx.x) return;   // CTA-uniform (mirror tiles)
   const long long pair = (long long)I * ng + J;
   const long long S = M.npairs;
   const double* rec = M.rec + pair;
@@ -817,6 +825,7 @@ __global__ void __launch_bounds__(128) k_sing_m(BlockArgs B, MomArgs M, int chun
   const int I = (int)(rid / 5), jo = (int)(rid % 5);
   if ((KIND == STB_V && (jo == 0 || jo == 4)) || (KIND == STB_K && jo == 0)) return;
   const int J = (I + jo - 2 + M.ng) % M.ng;
+  if (B.sym && I / SYM_TS > J / SYM_TS) return;   // mirror of the stored entry (J, I)
   const int a_beg = B.a0 + blockIdx.y * chunk;
   const int a_end = min(B.a1, a_beg + chunk);
   const long long S = M.npairs;

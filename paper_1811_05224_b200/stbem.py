@@ -58,6 +58,7 @@ class SolveReport(ctypes.Structure):
 
 
 QUAD_LEGACY_SING = 1   # bem_quad_opts.flags: touching pairs by the per-lag singular kernel
+QUAD_FULL_STORAGE = 2  # bem_quad_opts.flags: V_h / D_h stored full instead of symmetric packed
 
 
 class AssemblyStats(ctypes.Structure):
@@ -244,8 +245,8 @@ class Mesh:
         except Exception:
             pass
 
-    def _assemble(self, fn, q_bulk=0, q_sing=0, legacy_sing=False, stream=None):
-        o = QuadOpts(q_bulk, q_sing, QUAD_LEGACY_SING if legacy_sing else 0)
+    def _assemble(self, fn, q_bulk=0, q_sing=0, legacy_sing=False, full_storage=False, stream=None):
+        o = QuadOpts(q_bulk, q_sing, (QUAD_LEGACY_SING if legacy_sing else 0) | (QUAD_FULL_STORAGE if full_storage else 0))
         h = ctypes.c_void_p()
         check(fn(self.h, ctypes.byref(o), _stream(stream), ctypes.byref(h)))
         return Matrix(h, self)

@@ -249,3 +249,33 @@ def test_touching_pairs_both_paths(name):
         assert fused.stats()["fused_sing"] == 1 and legacy.stats()["fused_sing"] == 0
         for A in (fused, legacy):
             assert relmax(A.dense(), ref) <= MAT_TOL, (kind, relmax(A.dense(), ref))
+
+
+@pytest.mark.parametrize("name", ["LT", "C1", "S32"])
+def test_symmetric_packed_storage(name):
+    """V_h, D_h with symmetric packed spatial blocks (default) against full storage: the same
+    entries (the mirrored half is the same integral with the roles of the points exchanged) and
+    the same products"""
+    w = W.get(name)
+    m = S.Mesh.from_workload(w)
+    x = W.random_vector(w.n)
+    for kind in "VD":
+        P = getattr(m, f"assemble_{kind}")()
+        F = getattr(m, f"assemble_{kind}")(full_storage=True)
+        dp, df = P.dense(), F.dense()
+        assert relmax(dp, df) <= 1e-13
+        ng = w.n_gamma
+        scale = np.abs(dp).max()
+        for a in range(w.n_steps):   # every spatial block of the packed matrix is symmetric
+            blk = dp[a * ng:(a + 1) * ng, :(a + 1) * ng].reshape(ng, a + 1, ng)
+            # off-diagonal 32 x 32 tiles are mirrored (exactly symmetric); diagonal tiles hold both
+            # triangles, computed separately (symmetric to rounding)
+            assert np.abs(blk - blk.transpose(2, 1, 0)).max() <= 1e-14 * scale
+        yp = torch.empty(w.n, dtype=torch.float64, device="cuda")
+        yf = torch.empty_like(yp)
+        P.matvec(cuda(x), yp)
+        F.matvec(cuda(x), yf)
+        assert relmax(yp.cpu().numpy(), yf.cpu().numpy()) <= 1e-13
+        assert relmax(yp.cpu().numpy(), dp @ x) <= 1e-13
+        # packed: fewer distinct stored entries once N_Gamma spans more than one 32-wide tile
+        assert P.stats()["entries"] < F.stats()["entries"] if ng > 32 else P.stats()["entries"] == F.stats()["entries"]
