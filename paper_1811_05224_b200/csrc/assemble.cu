@@ -285,7 +285,7 @@ static void launch_records(const MomArgs& MB, const MomArgs& MN, const MomArgs* 
   k_records<KIND, true><<<nblk, 128, 0, st>>>(MN);
   count_launch(2);
   if (MS) {
-    k_sing_records<KIND><<<(unsigned)((MS->npairs + 127) / 128), 128, 0, st>>>(*MS, q_sing);
+    k_sing_records<KIND><<<(unsigned)((MS->npairs * 32 + 127) / 128), 128, 0, st>>>(*MS, q_sing);   // warp per record
     count_launch();
   }
 }

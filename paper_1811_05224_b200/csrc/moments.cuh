@@ -295,6 +295,12 @@ __global__ void __launch_bounds__(128) k_records(MomArgs M) {
   }
 }
 
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
 // ------------------------------------------------------------- node evaluation
 // regime A from registers
 template <int KIND>
@@ -697,7 +703,8 @@ __global__ void __launch_bounds__(128) k_near_m(BlockArgs B, MomArgs M, int chun
 __device__ __forceinline__ double lin1(double v0, double v1, double f) { return fma(v1 - v0, f, v0); }
 
 template <int KIND, class Vis>
-__device__ __forceinline__ void for_touch_points(const MomArgs& M, int I, int J, int n, Vis&& vis) {
+__device__ __forceinline__ void for_touch_points(const MomArgs& M, int I, int J, int n, int lane, int nl,
+                                                 Vis&& vis) {
   const double alpha = M.alpha;
   for_subpairs<KIND, false>(M, I, J, [&](const SubPair& sp) {
     const int rel = chain_rel(sp.pi, sp.qi, sp.nchain);
@@ -714,7 +721,7 @@ __device__ __forceinline__ void for_touch_points(const MomArgs& M, int I, int J,
       if (KIND == STB_K) return;  // dot = 0 on a straight element
       const double h = X.h;
       const double L0 = log(0.25 * alpha) + 2.0 * log(h);
-      for (int k = 0; k < n; ++k) {
+      for (int k = lane; k < n; k += nl) {
         const double rho = c_gx[n][k], w = h * rho, len = h - w;
         // G(w) = int_0^{h-w} [Sx(v+w) Sy(v) + Sx(v) Sy(v+w)] dv (quadratic: 2-point Gauss exact)
         double Ga = 0.0, Gb = 0.0;
@@ -745,9 +752,8 @@ __device__ __forceinline__ void for_touch_points(const MomArgs& M, int I, int J,
       }
       const double cth = e1x * e2x + e1y * e2y;
       const double e1n = e1x * Y.nx + e1y * Y.ny;
-      for (int tri = 0; tri < 2; ++tri)
-        for (int ie = 0; ie < n; ++ie)
-          for (int ir = 0; ir < n; ++ir) {
+      for (int idx = lane; idx < 2 * n * n; idx += nl) {
+            const int tri = idx / (n * n), ie = (idx / n) % n, ir = idx % n;
             const double eta = c_gx[n][ie], rho = c_gx[n][ir];
             const double A = tri == 0 ? (h1 * h1 + h2 * h2 * eta * eta - 2.0 * h1 * h2 * eta * cth)
                                       : (h1 * h1 * eta * eta + h2 * h2 - 2.0 * h1 * h2 * eta * cth);
@@ -768,21 +774,26 @@ __device__ __forceinline__ void for_touch_points(const MomArgs& M, int I, int J,
 // touching parts only, regime-A data and the affine constants (same layout as the pair records)
 template <int KIND>
 __global__ void __launch_bounds__(128) k_sing_records(MomArgs M, int nsing) {
-  const long long rid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (rid >= M.npairs) return;
+  const long long rid = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;   // warp per record
+  if (rid >= M.npairs) return;                    // warp-uniform
+  const int lane = threadIdx.x & 31;
   const int I = (int)(rid / 5), jo = (int)(rid % 5);
   const int J = (I + jo - 2 + M.ng) % M.ng;
   double* rec = M.rec + rid;
   const long long S = M.npairs;
   double cmax = 0.0;
-  for_touch_points<KIND>(M, I, J, nsing, [&](double c, double, double, double, double, double) {
+  for_touch_points<KIND>(M, I, J, nsing, lane, 32, [&](double c, double, double, double, double, double) {
     cmax = fmax(cmax, c);
   });
-  rec[RF_CMAX * S] = cmax;
-  rec[RF_CMIN * S] = 0.0;
-  rec[RF_C0 * S] = 0.0;
-  rec[RF_KB * S] = 0.0;
-  rec[RF_IC0 * S] = 0.0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cmax = fmax(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
+  if (lane == 0) {
+    rec[RF_CMAX * S] = cmax;
+    rec[RF_CMIN * S] = 0.0;
+    rec[RF_C0 * S] = 0.0;
+    rec[RF_KB * S] = 0.0;
+    rec[RF_IC0 * S] = 0.0;
+  }
 #pragma unroll 1
   for (int slot = 0; slot < Fams<KIND>::n; ++slot) {
     const int fam = slot == 0 ? Fams<KIND>::f0 : Fams<KIND>::f1;
@@ -791,7 +802,7 @@ __global__ void __launch_bounds__(128) k_sing_records(MomArgs M, int nsing) {
 #pragma unroll
     for (int k = 0; k <= MKA; ++k) mk[k] = 0.0;
     double C0 = 0.0, C1 = 0.0;
-    for_touch_points<KIND>(M, I, J, nsing, [&](double c, double lnA, double wa, double wb, double wla, double wlb) {
+    for_touch_points<KIND>(M, I, J, nsing, lane, 32, [&](double c, double lnA, double wa, double wb, double wla, double wlb) {
       const double w = slot == 0 ? wa : wb, wl = slot == 0 ? wla : wlb;
       double pw = w;
 #pragma unroll
@@ -805,13 +816,19 @@ __global__ void __launch_bounds__(128) k_sing_records(MomArgs M, int nsing) {
       C1 += fam == FAM_Q ? w / c : wlog * c;
     });
 #pragma unroll
-    for (int k = 0; k <= MKA; ++k) R[(FA + k) * S] = mpoly(fam, k) * mk[k];
-    R[FM0 * S] = mk[0];
-    R[FM1 * S] = mk[1];
+    for (int k = 0; k <= MKA; ++k) mk[k] = warp_sum(mk[k]);
+    C0 = warp_sum(C0);
+    C1 = warp_sum(C1);
+    if (lane == 0) {
 #pragma unroll
-    for (int k = 0; k <= MKB; ++k) R[(FB1 + k) * S] = R[(FB2 + k) * S] = 0.0;
-    R[FC0 * S] = C0;
-    R[FC1 * S] = C1;
+      for (int k = 0; k <= MKA; ++k) R[(FA + k) * S] = mpoly(fam, k) * mk[k];
+      R[FM0 * S] = mk[0];
+      R[FM1 * S] = mk[1];
+#pragma unroll
+      for (int k = 0; k <= MKB; ++k) R[(FB1 + k) * S] = R[(FB2 + k) * S] = 0.0;
+      R[FC0 * S] = C0;
+      R[FC1 * S] = C1;
+    }
   }
 }
 
