@@ -187,6 +187,16 @@ bem_status bem_mass_solve(const bem_matrix* M, int transpose, const double* x_de
 /* right-hand side of eq. (4) with u0 = 0: b = 1/2 M_primal g + K g */
 bem_status bem_rhs(const bem_matrix* K, const bem_matrix* M_primal, const double* g_dev,
                    double* b_dev, bem_stream stream);
+/* b = 1/2 M_h g + K_h g (eq. 4, u0 = 0) WITHOUT storing K_h ("fused K g"):
+ * every entry of K_h is computed by the same kernels and quadrature as bem_assemble_K and is
+ * multiplied by g at once; per (test row, trial tile) sums go to fixed partial slots (deterministic)
+ * and are reduced in fixed order.  Multi-GPU: each rank sums its owned blocks, then one NCCL
+ * all-reduce.  Meshes whose touching pairs fall outside regime A (alpha (h_X+h_Y)^2 / (4 min h_t) >= 4)
+ * fall back to bem_assemble_K + bem_rhs.  g_dev, b_dev: device, N doubles, must not alias; stats
+ * (host, may be NULL) receives the statistics of the K_h kernels (synchronises the stream).
+ * Errors: BEM_E_INVALID (null / aliasing / options), BEM_E_STATE (M not primal), BEM_E_CUDA. */
+bem_status bem_rhs_fused(const bem_mesh* mesh, const bem_quad_opts* opts, const bem_matrix* M_primal,
+                         const double* g_dev, double* b_dev, bem_assembly_stats* stats, bem_stream stream);
 
 /* ----------------------------------------------------------------- solver */
 /* Preconditioned full GMRES for V w = b with left preconditioner

@@ -238,6 +238,42 @@ bem_status bem_rhs(const bem_matrix* K, const bem_matrix* Mp, const double* g, d
   return mass_apply(Mp, 0.5, g, 1.0, b, S(s));
 }
 
+bem_status bem_rhs_fused(const bem_mesh* m, const bem_quad_opts* o, const bem_matrix* Mp,
+                         const double* g, double* b, bem_assembly_stats* stats, bem_stream s) {
+  if (!m || !Mp || !g || !b) { set_error("bem_rhs_fused: null argument"); return BEM_E_INVALID; }
+  if (g == b) { set_error("bem_rhs_fused: g and b must not alias"); return BEM_E_INVALID; }
+  if (Mp->kind != STB_MASS || Mp->mass_kind != BEM_MASS_PRIMAL) { set_error("bem_rhs_fused: needs the primal mass matrix"); return BEM_E_STATE; }
+  const int flags = o ? o->flags : 0;
+  if (!touching_records_ok(STB_K, m, flags)) {
+    // large kappa: the per-lag singular kernel needs stored entries; assemble K_h, multiply
+    bem_matrix* K = nullptr;
+    bem_status st = assemble(STB_K, m, o, s, &K);
+    if (st == BEM_OK) st = bem_rhs(K, Mp, g, b, s);
+    if (st == BEM_OK && stats) st = bem_matrix_stats(K, stats);
+    bem_matrix_destroy(K);
+    return st;
+  }
+  int q_bulk = (o && o->q_bulk > 0) ? o->q_bulk : m->q_bulk;
+  int q_sing = (o && o->q_sing > 0) ? o->q_sing : 12;
+  if (q_bulk < 3 || q_bulk > 8 || q_bulk == 7) { set_error("bem_rhs_fused: q_bulk must be one of 3,4,5,6,8"); return BEM_E_INVALID; }
+  if (q_sing < 4 || q_sing > QSING_MAX) { set_error("bem_rhs_fused: q_sing must be in [4,16]"); return BEM_E_INVALID; }
+  cudaSetDevice(m->device);
+  bem_matrix* A = new bem_matrix_s();   // statistics only: K_h is never stored
+  A->kind = STB_K;
+  A->mesh = m;
+  A->stream = S(s);
+  for (size_t bi = 0; bi < m->blocks.size(); ++bi) {
+    A->poff_base.push_back((int)A->poff.size());
+    for (int a = m->blocks[bi].a0; a < m->blocks[bi].a1; ++a) A->poff.push_back(0);
+  }
+  bem_status st = launch_assembly(STB_K, m, A, q_bulk, q_sing, flags, S(s), g, b);
+  if (st == BEM_OK && m->nranks > 1) st = allreduce_sum(m, b, (long long)m->ng * m->nt, S(s));
+  if (st == BEM_OK) st = mass_apply(Mp, 0.5, g, 1.0, b, S(s));
+  if (st == BEM_OK && stats) st = bem_matrix_stats(A, stats);
+  bem_matrix_destroy(A);
+  return st;
+}
+
 bem_status bem_eval_special(int which, long long count, const double* x, double* out, bem_stream s) {
   if (which < 0 || which > 3 || count < 0) { set_error("bem_eval_special: bad argument"); return BEM_E_INVALID; }
   return eval_special(which, count, x, out, S(s));

@@ -59,6 +59,12 @@ struct BlockArgs {
   int sym;                // symmetric packed spatial blocks (only tiles ti <= tj are written)
   int nt;                 // sym: tiles per block side
   long long blk;          // sym: stored doubles per (a,b) block
+  // product mode (K_h g, K_h not stored): trial vector and partial sums
+  const double* g;
+  double* part;           // partials of this block: [(a - a0) * ng + i] * pslots + slot
+  long long pbase;
+  int pslots;             // 2 * ntile + 5: bulk trial tiles, near trial tiles, touching records
+  int ntile;              // ceil(ng / 32)
 };
 
 // sym: the caller guarantees i / 32 <= j / 32 (the upper tile triangle)
@@ -269,13 +275,29 @@ __global__ void __launch_bounds__(128) k_sing(BlockArgs B, const Seg* __restrict
 }
 
 // ================================================================= launch
-template <int KIND>
+template <int KIND, bool PROD = false>
 static void launch_kind(int which, const BlockArgs& BA, const MomArgs& M, int ng, int nband_or_chunk,
                         int nz, cudaStream_t st) {
   dim3 grid((ng + 31) / 32, (ng + 3) / 4, nz);
-  if (which == 0) k_bulk_m<KIND, 8><<<grid, 128, 0, st>>>(BA, M);
-  else k_near_m<KIND><<<grid, 128, 0, st>>>(BA, M, nband_or_chunk);
+  if (which == 0) k_bulk_m<KIND, 8, PROD><<<grid, 128, 0, st>>>(BA, M);
+  else k_near_m<KIND, PROD><<<grid, 128, 0, st>>>(BA, M, nband_or_chunk);
   count_launch();
+}
+
+// product mode: y[a ng + i] = sum over the owned blocks containing test step a of the partials
+// (bulk trial tiles, near trial tiles, touching records) in fixed order
+__global__ void k_prod_reduce(const double* __restrict__ part, const int* __restrict__ rstart,
+                              const long long* __restrict__ roff, int ng, int nt, int pslots,
+                              double* __restrict__ y) {
+  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= (long long)ng * nt) return;
+  const int a = (int)(r / ng);
+  double s = 0.0;
+  for (int k = rstart[a]; k < rstart[a + 1]; ++k) {
+    const double* p = part + roff[k] + r * pslots;
+    for (int q = 0; q < pslots; ++q) s += p[q];
+  }
+  y[r] = s;
 }
 template <int KIND>
 static void launch_records(const MomArgs& MB, const MomArgs& MN, const MomArgs* MS, int q_sing,
@@ -289,11 +311,11 @@ static void launch_records(const MomArgs& MB, const MomArgs& MN, const MomArgs* 
     count_launch();
   }
 }
-template <int KIND>
+template <int KIND, bool PROD = false>
 static void launch_sing_m(const BlockArgs& BA, const MomArgs& MS, int nsteps, cudaStream_t st) {
   const int chunk = 16;
   dim3 grid((unsigned)((MS.npairs + 127) / 128), (nsteps + chunk - 1) / chunk);
-  k_sing_m<KIND><<<grid, 128, 0, st>>>(BA, MS, chunk);
+  k_sing_m<KIND, PROD><<<grid, 128, 0, st>>>(BA, MS, chunk);
   count_launch();
 }
 
@@ -314,8 +336,10 @@ static long long bulk_nodes(const Block& b, int R) {
 }
 
 bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bulk, int q_sing,
-                           int flags, cudaStream_t st) {
+                           int flags, cudaStream_t st, const double* prod_g, double* prod_y) {
   const int ng = m->ng;
+  const bool prod = prod_g != nullptr;
+  if (prod && kind != STB_K) { set_error("assemble: product mode is K_h only"); return BEM_E_INVALID; }
   mesh_wait(m, st);
   long long* d_poff = nullptr;
   cudaError_t e = cudaMallocAsync((void**)&d_poff, sizeof(long long) * std::max<size_t>(1, A->poff.size()), st);
@@ -328,10 +352,27 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bul
   const int nf = kind == STB_D ? rec_fields<STB_D>() : rec_fields<STB_V>();
   // touching pairs through moment records (regime A) when every touching sub-pair satisfies
   // c_max / min h_t < 4 with c_max <= alpha (h_X + h_Y)^2 / 4; otherwise the per-lag k_sing
-  const double hpair = (kind == STB_D ? 1.0 : 2.0) * m->hmax;
-  const bool fused_sing = !(flags & BEM_QUAD_LEGACY_SING) &&
-                          0.25 * m->alpha * hpair * hpair / m->htmin < 0.99 * 4.0;
+  const bool fused_sing = touching_records_ok(kind, m, flags);
   A->fused_sing = fused_sing ? 1 : 0;
+  if (prod && !fused_sing) { set_error("assemble: product mode needs the touching-pair records"); return BEM_E_STATE; }
+  // product mode: partial sums per block, row (a, i) and slot (bulk / near trial tiles, records)
+  const int ntile = (ng + 31) / 32, pslots = 2 * ntile + 5;
+  double* d_part = nullptr;
+  size_t part_bytes = 0;
+  std::vector<long long> pbase(m->blocks.size(), 0);
+  if (prod) {
+    long long tot = 0;
+    for (size_t bi = 0; bi < m->blocks.size(); ++bi) {
+      pbase[bi] = tot;
+      tot += (long long)(m->blocks[bi].a1 - m->blocks[bi].a0) * ng * pslots;
+    }
+    part_bytes = sizeof(double) * std::max<long long>(1, tot);
+    if ((e = storage_acquire(m->device, part_bytes, st, (void**)&d_part)) != cudaSuccess ||
+        (e = cudaMemsetAsync(d_part, 0, part_bytes, st)) != cudaSuccess) {
+      cudaFreeAsync(d_poff, st);
+      return cuda_fail(e, "assemble/partials");
+    }
+  }
   double* d_rec = nullptr;
   unsigned long long* d_ctr = nullptr;
   const size_t rec_bytes = sizeof(double) * nf * (2 * npairs + nsrec);
@@ -391,10 +432,16 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bul
     BA.sym = A->sym;
     BA.nt = sym_nt(ng);
     BA.blk = A->blk_elems;
+    BA.g = prod_g;
+    BA.part = d_part;
+    BA.pbase = pbase[bi];
+    BA.pslots = pslots;
+    BA.ntile = ntile;
     const int R = 8;
     const int nband = (blk.a1 - blk.a0 + R - 1) / R;
     if (blk.a1 - 1 - blk.b0 >= 2) {
-      if (kind == STB_V) launch_kind<STB_V>(0, BA, MB, ng, nband, nband, st);
+      if (prod) launch_kind<STB_K, true>(0, BA, MB, ng, nband, nband, st);
+      else if (kind == STB_V) launch_kind<STB_V>(0, BA, MB, ng, nband, nband, st);
       else if (kind == STB_K) launch_kind<STB_K>(0, BA, MB, ng, nband, nband, st);
       else launch_kind<STB_D>(0, BA, MB, ng, nband, nband, st);
       mark();
@@ -406,13 +453,15 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bul
     if (has_near) {
       const int chunk = 16;
       const int nz = (blk.a1 - blk.a0 + chunk - 1) / chunk;
-      if (kind == STB_V) launch_kind<STB_V>(1, BA, MN, ng, chunk, nz, st);
+      if (prod) launch_kind<STB_K, true>(1, BA, MN, ng, chunk, nz, st);
+      else if (kind == STB_V) launch_kind<STB_V>(1, BA, MN, ng, chunk, nz, st);
       else if (kind == STB_K) launch_kind<STB_K>(1, BA, MN, ng, chunk, nz, st);
       else launch_kind<STB_D>(1, BA, MN, ng, chunk, nz, st);
       mark();
       fam.push_back(1);
       if (fused_sing) {
-        if (kind == STB_V) launch_sing_m<STB_V>(BA, MS, blk.a1 - blk.a0, st);
+        if (prod) launch_sing_m<STB_K, true>(BA, MS, blk.a1 - blk.a0, st);
+        else if (kind == STB_V) launch_sing_m<STB_V>(BA, MS, blk.a1 - blk.a0, st);
         else if (kind == STB_K) launch_sing_m<STB_K>(BA, MS, blk.a1 - blk.a0, st);
         else launch_sing_m<STB_D>(BA, MS, blk.a1 - blk.a0, st);
       } else {
@@ -429,6 +478,31 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bul
       fam.push_back(2);
       A->launches += 2;
     }
+  }
+  if (prod) {
+    // y = sum of the partials of the owned blocks of each test step (fixed order)
+    std::vector<int> rstart(m->nt + 1, 0);
+    std::vector<long long> roff;
+    for (int a = 0; a < m->nt; ++a) {
+      rstart[a] = (int)roff.size();
+      for (size_t bi = 0; bi < m->blocks.size(); ++bi)
+        if (m->blocks[bi].a0 <= a && a < m->blocks[bi].a1)
+          roff.push_back(pbase[bi] - (long long)m->blocks[bi].a0 * ng * pslots);
+    }
+    rstart[m->nt] = (int)roff.size();
+    int* d_rs = nullptr;
+    long long* d_ro = nullptr;
+    if ((e = cudaMallocAsync((void**)&d_rs, sizeof(int) * rstart.size(), st)) != cudaSuccess ||
+        (e = cudaMallocAsync((void**)&d_ro, sizeof(long long) * std::max<size_t>(1, roff.size()), st)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(d_rs, rstart.data(), sizeof(int) * rstart.size(), cudaMemcpyHostToDevice, st)) != cudaSuccess ||
+        (roff.size() && (e = cudaMemcpyAsync(d_ro, roff.data(), sizeof(long long) * roff.size(), cudaMemcpyHostToDevice, st)) != cudaSuccess))
+      return cuda_fail(e, "assemble/product reduce");
+    const long long n = (long long)ng * m->nt;
+    k_prod_reduce<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(d_part, d_rs, d_ro, ng, m->nt, pslots, prod_y);
+    count_launch();
+    cudaFreeAsync(d_rs, st);
+    cudaFreeAsync(d_ro, st);
+    storage_release(m->device, d_part, part_bytes, st);
   }
   storage_release(m->device, d_rec, rec_bytes, st);
   cudaFreeAsync(d_poff, st);

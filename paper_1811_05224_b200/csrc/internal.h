@@ -179,8 +179,17 @@ cudaError_t storage_acquire(int device, size_t bytes, cudaStream_t st, void** ou
 void storage_release(int device, void* ptr, size_t bytes, cudaStream_t st);
 
 // kernels (assemble.cu)
+// touching pairs through moment records (regime A) whenever every touching sub-pair satisfies
+// c_max / min h_t < 4 with c_max <= alpha (h_X + h_Y)^2 / 4
+inline bool touching_records_ok(int kind, const bem_mesh* m, int flags) {
+  const double hpair = (kind == STB_D ? 1.0 : 2.0) * m->hmax;
+  return !(flags & BEM_QUAD_LEGACY_SING) && 0.25 * m->alpha * hpair * hpair / m->htmin < 0.99 * 4.0;
+}
+// prod_g != nullptr: product mode (K_h only): prod_y = K_h prod_g over the owned blocks, K_h is
+// not stored (A carries statistics only)
 bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bulk, int q_sing,
-                           int flags, cudaStream_t st);
+                           int flags, cudaStream_t st, const double* prod_g = nullptr,
+                           double* prod_y = nullptr);
 // linear algebra (linalg.cu)
 bem_status gemv_setup(bem_matrix* A);
 bem_status gemv_launch(const bem_matrix* A, double a, const double* x, double b, double* y,

@@ -505,7 +505,10 @@ __device__ __forceinline__ void count_regimes(unsigned long long* ctr, unsigned 
 // once each (1.125 node evaluations per entry at R = 8).  Column fast path: when the node with
 // the smallest lag is in regime A for every lane, all R+1 nodes are (s grows with x), and the
 // R+1 Horner chains run unrolled and interleaved.
-template <int KIND, int R>
+// PROD (product mode, K_h g without storing K_h): each entry is multiplied by g at its trial
+// index and summed over the thread's columns; one warp sum per (test row, trial tile) is written
+// to the block's partial buffer (fixed slots: deterministic)
+template <int KIND, int R, bool PROD = false>
 __global__ void __launch_bounds__(128) k_bulk_m(BlockArgs B, MomArgs M) {
   const int ng = B.ng;
   const int lane = threadIdx.x & 31;
@@ -529,7 +532,7 @@ __global__ void __launch_bounds__(128) k_bulk_m(BlockArgs B, MomArgs M) {
   // the tile's offset + (I mod 32) * 32), shared by the warp: a store is one LDS + one address add
   __shared__ long long s_row[4][R];
   long long* srow = s_row[threadIdx.x >> 5];
-  if (lane < R) {
+  if (!PROD && lane < R) {
     const int a = min(r_lo + lane, r_hi - 1);
     srow[lane] = B.poff[a - B.a0] + (B.sym ? sym_tile_index(ti, tj, B.nt) * (SYM_TS * SYM_TS) + (long long)(I % SYM_TS) * SYM_TS
                                            : (long long)I * pad4((long long)panel_nb(a, B.b0, B.b1) * ng));
@@ -542,6 +545,9 @@ __global__ void __launch_bounds__(128) k_bulk_m(BlockArgs B, MomArgs M) {
   RegBZ<KIND> Z;
   Z.load(M.rec + pair, S);
   unsigned long long nA = 0, nB = 0, nZ = 0, nC = 0, nK = 0;
+  double accp[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) accp[r] = 0.0;
   double Gp[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) Gp[r] = 0.0;
@@ -604,17 +610,37 @@ __global__ void __launch_bounds__(128) k_bulk_m(BlockArgs B, MomArgs M) {
     }
     if (y > B.b0) {
       const int b = y - 1;
-      double* col = B.out + ((long long)(b - B.b0) * cstride + jcol);
+      if (PROD) {
+        const double gv = valid ? B.g[(long long)b * ng + J] : 0.0;
 #pragma unroll
-      for (int r = 1; r <= R; ++r) {
-        const int a = r_lo + r - 1;
-        const double G = phi[r] - phi[r - 1];
-        if (valid && a < r_hi && a - b >= 2) col[srow[r - 1]] = Gp[r - 1] - G;
-        Gp[r - 1] = G;
+        for (int r = 1; r <= R; ++r) {
+          const int a = r_lo + r - 1;
+          const double G = phi[r] - phi[r - 1];
+          if (a < r_hi && a - b >= 2) accp[r - 1] = fma(Gp[r - 1] - G, gv, accp[r - 1]);
+          Gp[r - 1] = G;
+        }
+      } else {
+        double* col = B.out + ((long long)(b - B.b0) * cstride + jcol);
+#pragma unroll
+        for (int r = 1; r <= R; ++r) {
+          const int a = r_lo + r - 1;
+          const double G = phi[r] - phi[r - 1];
+          if (valid && a < r_hi && a - b >= 2) col[srow[r - 1]] = Gp[r - 1] - G;
+          Gp[r - 1] = G;
+        }
       }
     } else {
 #pragma unroll
       for (int r = 1; r <= R; ++r) Gp[r - 1] = phi[r] - phi[r - 1];
+    }
+  }
+  if (PROD) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const double sum = warp_sum(accp[r]);
+      const int a = r_lo + r;
+      if (lane == 0 && a < r_hi && I0 < ng)
+        B.part[B.pbase + ((long long)(a - B.a0) * ng + I) * B.pslots + blockIdx.x] = sum;
     }
   }
   if (!valid) nA = nB = nZ = nC = nK = 0;
@@ -626,7 +652,7 @@ __global__ void __launch_bounds__(128) k_bulk_m(BlockArgs B, MomArgs M) {
 // entry (a, a-1) = Phi(a+1, a-1) - Phi(a, a-1) - Phi(a+1, a) (Phi(a, a) = 0: G vanishes at s = 0),
 // with the true node values Phi = Phi~ - affine part (the affine terms do not cancel here).
 // Touching sub-pairs are excluded from the near records; k_sing adds them afterwards.
-template <int KIND>
+template <int KIND, bool PROD = false>
 __global__ void __launch_bounds__(128) k_near_m(BlockArgs B, MomArgs M, int chunk) {
   const int ng = B.ng;
   const int lane = threadIdx.x & 31;
@@ -681,10 +707,22 @@ __global__ void __launch_bounds__(128) k_near_m(BlockArgs B, MomArgs M, int chun
     const bool d0 = a >= B.b0 && a < B.b1, d1 = a - 1 >= B.b0 && a - 1 < B.b1;
     double p10 = 0.0;
     if (d0 || d1) p10 = node(a + 1, a);
-    if (d0 && valid) *entry_ptr(B, a, I, a, J) = p10;
-    if (d1) {
-      const double p20 = node(a + 1, a - 1);
-      if (valid) *entry_ptr(B, a, I, a - 1, J) = p20 - prev - p10;
+    if (PROD) {
+      double c = 0.0;
+      if (d0 && valid) c = p10 * B.g[(long long)a * ng + J];
+      if (d1) {
+        const double p20 = node(a + 1, a - 1);
+        if (valid) c = fma(p20 - prev - p10, B.g[(long long)(a - 1) * ng + J], c);
+      }
+      c = warp_sum(c);
+      if (lane == 0 && (d0 || d1) && I0 < ng)
+        B.part[B.pbase + ((long long)(a - B.a0) * ng + I) * B.pslots + B.ntile + blockIdx.x] = c;
+    } else {
+      if (d0 && valid) *entry_ptr(B, a, I, a, J) = p10;
+      if (d1) {
+        const double p20 = node(a + 1, a - 1);
+        if (valid) *entry_ptr(B, a, I, a - 1, J) = p20 - prev - p10;
+      }
     }
     prev = p10;
   }
@@ -835,7 +873,7 @@ __global__ void __launch_bounds__(128) k_sing_records(MomArgs M, int nsing) {
 // touching contributions to the near cells, added onto the near-kernel values: thread = (sing
 // record, chunk of test steps); regime A only (the host checks c_max / min lag < 4 before it
 // chooses this path; a violation is counted in counters[3] and fails the assembly)
-template <int KIND>
+template <int KIND, bool PROD = false>
 __global__ void __launch_bounds__(128) k_sing_m(BlockArgs B, MomArgs M, int chunk) {
   const long long rid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (rid >= M.npairs) return;
@@ -862,8 +900,15 @@ __global__ void __launch_bounds__(128) k_sing_m(BlockArgs B, MomArgs M, int chun
     const bool d0 = a >= B.b0 && a < B.b1, d1 = a - 1 >= B.b0 && a - 1 < B.b1;
     double p10 = 0.0;
     if (d0 || d1) p10 = node(a + 1, a);
-    if (d0) *entry_ptr(B, a, I, a, J) += p10;
-    if (d1) *entry_ptr(B, a, I, a - 1, J) += node(a + 1, a - 1) - prev - p10;
+    if (PROD) {
+      double c = 0.0;
+      if (d0) c = p10 * B.g[(long long)a * M.ng + J];
+      if (d1) c = fma(node(a + 1, a - 1) - prev - p10, B.g[(long long)(a - 1) * M.ng + J], c);
+      if (d0 || d1) B.part[B.pbase + ((long long)(a - B.a0) * M.ng + I) * B.pslots + 2 * B.ntile + jo] = c;
+    } else {
+      if (d0) *entry_ptr(B, a, I, a, J) += p10;
+      if (d1) *entry_ptr(B, a, I, a - 1, J) += node(a + 1, a - 1) - prev - p10;
+    }
     prev = p10;
   }
   if (bad && M.counters) atomicAdd(M.counters + 3, bad);   // regime C slot of the sing counters

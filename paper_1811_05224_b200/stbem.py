@@ -105,6 +105,7 @@ _SIGS = {
     "bem_matvec": (I, [P, D, P, D, P, P]),
     "bem_mass_solve": (I, [P, I, P, P, P]),
     "bem_rhs": (I, [P, P, P, P, P]),
+    "bem_rhs_fused": (I, [P, P, P, P, P, P, P]),
     "bem_solve_gmres": (I, [P, P, P, P, P, ctypes.POINTER(GmresOpts), ctypes.POINTER(SolveReport), P, P]),
     "bem_matrix_get": (I, [P, LL, LL, LL, LL, P]),
     "bem_matrix_get_entries": (I, [P, LL, P, P, P]),
@@ -320,6 +321,16 @@ class Matrix:
 def rhs(K, Mp, g, b, stream=None):
     check(lib().bem_rhs(K.h, Mp.h, _ptr(g), _ptr(b), _stream(stream)))
     return b
+
+
+def rhs_fused(mesh, Mp, g, b, q_bulk=0, q_sing=0, legacy_sing=False, stats=False, stream=None):
+    """b = 1/2 M g + K g with K_h computed on the fly and never stored (bem_rhs_fused); returns
+    the K_h kernel statistics when stats=True (synchronises), else b"""
+    o = QuadOpts(q_bulk, q_sing, QUAD_LEGACY_SING if legacy_sing else 0)
+    st = AssemblyStats() if stats else None
+    check(lib().bem_rhs_fused(mesh.h, ctypes.byref(o), Mp.h, _ptr(g), _ptr(b),
+                              ctypes.byref(st) if stats else None, _stream(stream)))
+    return st.as_dict() if stats else b
 
 
 def solve_gmres(V, b, w, D=None, M=None, rel_tol=1e-10, max_iter=500, precond=0, history=True, stream=None):

@@ -279,3 +279,23 @@ def test_symmetric_packed_storage(name):
         assert relmax(yp.cpu().numpy(), dp @ x) <= 1e-13
         # packed: fewer distinct stored entries once N_Gamma spans more than one 32-wide tile
         assert P.stats()["entries"] < F.stats()["entries"] if ng > 32 else P.stats()["entries"] == F.stats()["entries"]
+
+
+@pytest.mark.parametrize("name,n_slices", [("C1", 1), ("LT", 1), ("C1", 3), ("S32", 2)])
+def test_rhs_fused(name, n_slices):
+    """b = 1/2 M g + K g with K_h never stored (bem_rhs_fused) against the stored K_h product and
+    the oracle's right-hand side"""
+    w = W.get(name)
+    m = S.Mesh.from_workload(w, n_slices=n_slices)
+    g = cuda(W.dirichlet_data(w))
+    Mp = m.assemble_M(S.MASS_PRIMAL)
+    b_stored = torch.empty_like(g)
+    S.rhs(m.assemble_K(), Mp, g, b_stored)
+    b_fused = torch.empty_like(g)
+    st = S.rhs_fused(m, Mp, g, b_fused, stats=True)
+    bf, bs = b_fused.cpu().numpy(), b_stored.cpu().numpy()
+    assert relmax(bf, bs) <= 1e-13, relmax(bf, bs)
+    om = O.OracleMesh(w)
+    ref = om.rhs(oracle_dense(name, "K") if name in ("C1", "LT") else om.dense("K"), W.dirichlet_data(w))
+    assert relmax(bf, ref) <= 1e-11
+    assert st["fused_sing"] == 1 and st["evals_bulk"] > 0
