@@ -442,6 +442,93 @@ __device__ __forceinline__ double phi_bz(const double* __restrict__ rec, long lo
   return out;
 }
 
+// two nodes of the same pair at once (the bulk columns usually hold several regime-B nodes per
+// lane): the two Taylor recurrences interleave (ILP 2 on a latency-bound chain) and share the
+// moment loads.  reg1 / reg2 as in phi_bz.
+template <int KIND>
+__device__ __forceinline__ void phi_bz2(const double* __restrict__ rec, long long S, const RegBZ<KIND>& z,
+                                        double s1, double u1, double s2, double u2, double& v1,
+                                        double& v2, int* reg1, int* reg2) {
+  if (!(z.c0 > 0.0)) {   // no cluster: Z or C per node
+    v1 = phi_bz<KIND>(rec, S, z, s1, u1, reg1);
+    v2 = phi_bz<KIND>(rec, S, z, s2, u2, reg2);
+    return;
+  }
+  const bool zz1 = z.cmin > 0.0 && z.cmin * u1 >= MXZ, zz2 = z.cmin > 0.0 && z.cmin * u2 >= MXZ;
+  const double ic0 = z.ic0;
+  const double x01 = z.c0 * u1, x02 = z.c0 * u2;
+  const double ex1 = exp(-x01), ex2 = exp(-x02);
+  const double E11 = ex1 * (ic0 * s1) * gb3_poly(ic0 * s1), E12 = ex2 * (ic0 * s2) * gb3_poly(ic0 * s2);
+  const double* R0 = rec + (RF_COMMON + 0 * FAMSZ) * S;
+  const double* R1 = rec + (RF_COMMON + 1 * FAMSZ) * S;
+  double e1 = ex1, ap1 = ex1 * ic0, app1 = 0.0, e2 = ex2, ap2 = ex2 * ic0, app2 = 0.0;
+  const double a01 = ap1, a02 = ap2;
+  double S1a1 = 0.0, S2a1 = 0.0, S1b1 = 0.0, S1a2 = 0.0, S2a2 = 0.0, S1b2 = 0.0;
+  const double* p1 = R0 + (FB1 + 1) * S;
+  const double* p2 = R0 + (FB2 + 1) * S;
+  const double* p3 = R1 + (FB1 + 1) * S;
+#pragma unroll 2
+  for (int k = 1; k <= z.kb; ++k) {
+    const double ik = STB_INV[k];
+    const double m1 = *p1, m2 = *p2;
+    e1 = -e1 * (u1 * ik);
+    e2 = -e2 * (u2 * ik);
+    const double ak1 = (e1 - ap1) * ic0, ak2 = (e2 - ap2) * ic0;
+    S1a1 = fma(ap1, m1, S1a1);
+    S1a2 = fma(ap2, m1, S1a2);
+    if (Fams<KIND>::f0 == FAM_H) {
+      S2a1 = fma(app1, m2, S2a1);
+      S2a2 = fma(app2, m2, S2a2);
+    } else {
+      S2a1 = fma(ak1, m2, S2a1);
+      S2a2 = fma(ak2, m2, S2a2);
+    }
+    if (Fams<KIND>::n == 2) {
+      const double m3 = *p3;
+      S1b1 = fma(ap1, m3, S1b1);
+      S1b2 = fma(ap2, m3, S1b2);
+    }
+    p1 += S;
+    p2 += S;
+    p3 += S;
+    app1 = ap1;
+    ap1 = ak1;
+    app2 = ap2;
+    ap2 = ak2;
+  }
+  const double m0 = z.m0[0];
+  double T1[2], T2[2];
+  if (Fams<KIND>::f0 == FAM_H) {
+    T1[0] = fma(fma(1.0 + x01, E11, -ex1), m0, fma(E11 * u1, z.m1, -fma(u1, S2a1, S1a1)));
+    T2[0] = fma(fma(1.0 + x02, E12, -ex2), m0, fma(E12 * u2, z.m1, -fma(u2, S2a2, S1a2)));
+  } else {
+    T1[0] = fma(-E11, m0, fma(a01, m0, S2a1) / u1 + S1a1);
+    T2[0] = fma(-E12, m0, fma(a02, m0, S2a2) / u2 + S1a2);
+  }
+  if (Fams<KIND>::n == 2) {
+    T1[1] = fma(E11, z.m0[1], -S1b1);
+    T2[1] = fma(E12, z.m0[1], -S1b2);
+  }
+  v1 = v2 = 0.0;
+#pragma unroll
+  for (int f = 0; f < Fams<KIND>::n; ++f) {
+    const int fam = f == 0 ? Fams<KIND>::f0 : Fams<KIND>::f1;
+    const double t1 = zz1 ? 0.0 : T1[f], t2 = zz2 ? 0.0 : T2[f];
+    if (fam == FAM_H) {
+      v1 += fma(s1, t1 + z.C0[f], z.C1[f]);
+      v2 += fma(s2, t2 + z.C0[f], z.C1[f]);
+    } else if (fam == FAM_F) {
+      v1 += t1 + z.C0[f];
+      v2 += t2 + z.C0[f];
+    } else {
+      v1 += t1 - fma(s1, z.C1[f], z.C0[f]);
+      v2 += t2 - fma(s2, z.C1[f], z.C0[f]);
+    }
+  }
+  *reg1 = zz1 ? 2 : 1;
+  *reg2 = zz2 ? 2 : 1;
+}
+
 // regime C, warp-cooperative: every lane evaluates its round-robin share of the points of
 // entry (I, J) at node (s, u) (all lanes pass the same arguments); returns the warp sum
 template <int KIND, bool NEAR>
@@ -576,18 +663,33 @@ __global__ void __launch_bounds__(128) k_bulk_m(BlockArgs B, MomArgs M) {
         const int r = __ffs(bmask) - 1;
         bmask &= bmask - 1;
         const double4 q = B.lag[(r_lo + r) * B.ldlag + y];
-        int reg = 0;
-        const double v = phi_bz<KIND>(M.rec + pair, S, Z, q.x, q.z, &reg);
-        nB += reg == 1;
-        nK += reg == 1 ? Z.kb : 0;
-        nZ += reg == 2;
+        int reg = 0, reg2 = 0;
+        double v = 0.0, v2 = 0.0;
+        int r2 = -1;
+        if (bmask) {             // a second node of the same lane: evaluate both together
+          r2 = __ffs(bmask) - 1;
+          bmask &= bmask - 1;
+          const double4 q2 = B.lag[(r_lo + r2) * B.ldlag + y];
+          phi_bz2<KIND>(M.rec + pair, S, Z, q.x, q.z, q2.x, q2.z, v, v2, &reg, &reg2);
+        } else {
+          v = phi_bz<KIND>(M.rec + pair, S, Z, q.x, q.z, &reg);
+        }
+        nB += (reg == 1) + (reg2 == 1);
+        nK += (reg == 1 ? Z.kb : 0) + (reg2 == 1 ? Z.kb : 0);
+        nZ += (reg == 2) + (reg2 == 2);
         if (reg == 3) {
           cmask |= 1u << r;
           ++nC;
         }
+        if (reg2 == 3) {
+          cmask |= 1u << r2;
+          ++nC;
+        }
 #pragma unroll
-        for (int rr = 0; rr <= R; ++rr)
+        for (int rr = 0; rr <= R; ++rr) {
           if (rr == r) phi[rr] = v;
+          if (rr == r2) phi[rr] = v2;
+        }
       }
       unsigned lanes = __ballot_sync(0xffffffffu, cmask != 0);
       while (lanes) {                                   // warp-uniform
