@@ -299,8 +299,8 @@ def native(args):
                 "nodes_by_regime_ABZC": st["nodes_bulk"],
                 "flops_note": "algorithmic: exact per-regime node counts x static FP64 flops of the shipped "
                               "moment forms (DFMA = 2), DESIGN.md section 6"}
-    roof_gemv = {"bound": "hbm", "kernel": "k_gemv", "achieved": gemv_gbs, "peak": hbm_peak, "unit": "GB/s",
-                 "frac": (gemv_gbs / hbm_peak) if gemv_gbs else None, "traffic": traffic.get("k_gemv"),
+    roof_gemv = {"bound": "hbm", "kernel": "k_gemv_sym", "achieved": gemv_gbs, "peak": hbm_peak, "unit": "GB/s",
+                 "frac": (gemv_gbs / hbm_peak) if gemv_gbs else None, "traffic": traffic.get("k_gemv_sym"),
                  "bytes_per_launch": bytes_per_gemv,
                  "peak_note": "MEASURED_PEAKS.json hbm_gbs (driver-measured copy bandwidth)",
                  "bytes_note": "algorithmic: 8 B per stored double of the product's matrix (block lower "
