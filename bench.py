@@ -252,7 +252,11 @@ def native(args):
     # units: the distinct element-pair integrals computed and stored per step (V_h and D_h keep the
     # upper 32 x 32 tile triangle of their symmetric spatial blocks, K_h all entries); the matrix
     # entries they represent (3 x entries_total) are reported beside
-    units_per_step = sum(stats[k]["entries"] for k in "VKD")
+    units_per_step = sum(stats[k]["entries"] for k in "VKD")   # this rank's owned blocks
+    if world > 1:   # whole-job units: every rank computes the integrals of its own blocks
+        uu = torch.tensor([float(units_per_step)], dtype=torch.float64, device=dev)
+        dist.all_reduce(uu, op=dist.ReduceOp.SUM)
+        units_per_step = uu.item()
     represented_per_step = 3 * entries_total
     ms = 1e3 * t_dev / args.steps
     value = units_per_step * args.steps / t_dev
