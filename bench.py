@@ -36,7 +36,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--config", default="C3")
-    ap.add_argument("--precond", type=int, default=1)
+    # 2: exact dual mass (cyclic-tridiagonal solves on the device, the north star's "sparse
+    # mass-matrix solves"); 1: the lumped diagonal of P:185 (study in DESIGN.md section 6.2)
+    ap.add_argument("--precond", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     return ap.parse_args()
