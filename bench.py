@@ -40,6 +40,8 @@ def parse():
     # mass-matrix solves"); 1: the lumped diagonal of P:185 (study in DESIGN.md section 6.2)
     ap.add_argument("--precond", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    # uniform time steps only; avoids the dense work, reported as its own metric
+    ap.add_argument("--variant", default="dense", choices=["dense", "toeplitz"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     return ap.parse_args()
 
@@ -165,14 +167,21 @@ def native(args):
         if e2e:
             gg = torch.empty_like(g)
             gg.copy_(g_host, non_blocking=True)
-        V = mesh.assemble_V()
+        toep = args.variant == "toeplitz"
+        V = mesh.assemble_toeplitz("V") if toep else mesh.assemble_V()
         ev[1].record()
-        D = mesh.assemble_D()
+        D = mesh.assemble_toeplitz("D") if toep else mesh.assemble_D()
         ev[2].record()
         Mp = mesh.assemble_M(S.MASS_PRIMAL)
         Mc = mesh.assemble_M(Mkind) if args.precond else None
-        # K_h is computed entry by entry and multiplied by g on the fly (never stored)
-        st_K = S.rhs_fused(mesh, Mp, gg, b, stats=True)
+        if toep:
+            Kt = mesh.assemble_toeplitz("K")
+            S.rhs(Kt, Mp, gg, b)
+            st_K = Kt.stats()
+            Kt.close()
+        else:
+            # K_h is computed entry by entry and multiplied by g on the fly (never stored)
+            st_K = S.rhs_fused(mesh, Mp, gg, b, stats=True)
         ev[3].record()
         ev[4].record()
         rep = S.solve_gmres(V, b, wv, D=D if args.precond else None, M=Mc, rel_tol=tol, max_iter=200,
@@ -336,10 +345,12 @@ def native(args):
     roofline = dict(roofline, share_of_step=(gemv_total_ms if roofline is roof_gemv else ms_dom) / ms)
     asm_s = ph["assemble_V"] + ph["assemble_K"] + ph["assemble_D"]
     out = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "metric": METRIC + (" [block-Toeplitz variant, SURVEY 8(f) f3]" if args.variant == "toeplitz" else ""),
+        "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"BJ configs[2] ({w.name}): {w.note}", "n_gamma": w.n_gamma, "n_steps": w.n_steps,
+        "config": {"workload": f"BJ configs[{'C1 C2 C3 C4 C5'.split().index(w.name) if w.name in 'C1 C2 C3 C4 C5'.split() else '-'}] ({w.name}): {w.note}",
+                   "variant": args.variant, "n_gamma": w.n_gamma, "n_steps": w.n_steps,
                    "N": n, "alpha": w.alpha, "slices_P": P, "gmres_tol": tol, "precond": ["none", "lumped", "exact"][args.precond],
                    "parallelism": f"cyclic K_P blocks over {world} GPU" + ("s" if world > 1 else ""),
                    "l2": "inputs larger than L2 (each matrix 17 GB >> 126 MB)"},
@@ -397,7 +408,8 @@ def reference(args):
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.median(secs)),
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "impl": "reference",
-           "config": {"workload": f"BJ configs[2] ({w.name}): {w.note}", "n_gamma": w.n_gamma, "n_steps": w.n_steps, "N": w.n},
+           "config": {"workload": f"BJ configs[{'C1 C2 C3 C4 C5'.split().index(w.name) if w.name in 'C1 C2 C3 C4 C5'.split() else '-'}] ({w.name}): {w.note}",
+                   "variant": args.variant, "n_gamma": w.n_gamma, "n_steps": w.n_steps, "N": w.n},
            "cpu_baseline": {"value": v, "unit": UNIT, "cores": r["cores"], "kind": "oracle", "sample": r["sample"]},
            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)

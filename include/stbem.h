@@ -171,6 +171,17 @@ bem_status bem_assemble_K(const bem_mesh* mesh, const bem_quad_opts* opts, bem_s
 bem_status bem_assemble_D(const bem_mesh* mesh, const bem_quad_opts* opts, bem_stream stream,
                           bem_matrix** out);
 /* mass matrices (block diagonal in time): see bem_mass_kind */
+/* Block-Toeplitz variant (uniform time steps only): on equal steps the
+ * entries depend on the test and trial steps through d = a - b only, A(a, b) = T_d.  Assembles
+ * the first block column T_d = A(d, 0), d = 0 .. N_I - 1 (N_I N_Gamma^2 entries instead of
+ * N_Gamma^2 N_I (N_I + 1) / 2) with the kernels and quadrature of bem_assemble_*; bem_matvec then
+ * evaluates y_a = sum_{d <= a} T_d x_{a-d} as one FP64 GEMM over the stacked index (d, j), and
+ * bem_solve_gmres / bem_rhs / bem_matrix_get_entries accept the result like a dense matrix.
+ * This avoids the dense work the paper does: report its rates separately.  kind: 0 V_h, 1 K_h,
+ * 2 D_h.  Errors: BEM_E_STATE (non-uniform steps, more than one process), BEM_E_INVALID
+ * (options), BEM_E_NOMEM, BEM_E_CUDA. */
+bem_status bem_assemble_toeplitz(const bem_mesh* mesh, int kind, const bem_quad_opts* opts,
+                                 bem_stream stream, bem_matrix** out);
 bem_status bem_assemble_M(const bem_mesh* mesh, bem_mass_kind kind, bem_stream stream,
                           bem_matrix** out);
 

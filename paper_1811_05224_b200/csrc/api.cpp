@@ -94,17 +94,29 @@ namespace {
 
 inline cudaStream_t S(bem_stream s) { return reinterpret_cast<cudaStream_t>(s); }
 
-bem_matrix* new_dense(const bem_mesh* m, int kind, bool sym, cudaStream_t stream, bem_status* st) {
+bem_matrix* new_dense(const bem_mesh* m, int kind, bool sym, cudaStream_t stream, bem_status* st,
+                      bool toeplitz = false) {
   bem_matrix* A = new bem_matrix_s();
   A->kind = kind;
   A->mesh = m;
   A->stream = stream;
+  if (toeplitz) {
+    // the first block column: T_d = A(d, 0), d = 0 .. N_I - 1 (one temporal "block" (a in [0, N_I),
+    // b in [0, 1)) of the assembly machinery)
+    A->toeplitz = 1;
+    Block b;
+    b.I = b.J = 0;
+    b.a0 = 0; b.a1 = m->nt; b.b0 = 0; b.b1 = 1;
+    b.off = 0;
+    A->own_blocks.push_back(b);
+    sym = false;
+  }
   A->sym = sym ? 1 : 0;
   const int ng = m->ng;
   A->blk_elems = sym ? sym_blk_elems(ng) : 0;
   long long off = 0;
-  for (size_t bi = 0; bi < m->blocks.size(); ++bi) {
-    const Block& b = m->blocks[bi];
+  for (size_t bi = 0; bi < blocks_of(A).size(); ++bi) {
+    const Block& b = blocks_of(A)[bi];
     A->poff_base.push_back((int)A->poff.size());
     for (int a = b.a0; a < b.a1; ++a) {
       A->poff.push_back(off);
@@ -159,6 +171,10 @@ int slice_of(const bem_mesh* m, int a) {
 long long entry_offset(const bem_matrix* A, int a, int i, int b, int j) {
   const bem_mesh* m = A->mesh;
   if (b > a) return -1;
+  if (A->toeplitz) {   // T_{a-b}(i, j)
+    const int d = a - b;
+    return A->poff[d] + (long long)i * pad4((long long)m->ng) + j;
+  }
   const int I = slice_of(m, a), J = slice_of(m, b);
   for (size_t bi = 0; bi < m->blocks.size(); ++bi) {
     const Block& B = m->blocks[bi];
@@ -186,6 +202,27 @@ bem_status gather_entries(const double* data, const long long* offs_dev, long lo
 }
 
 extern "C" {
+
+bem_status bem_assemble_toeplitz(const bem_mesh* m, int kind, const bem_quad_opts* o, bem_stream s,
+                                 bem_matrix** out) {
+  if (!m || !out) { set_error("bem_assemble_toeplitz: null argument"); return BEM_E_INVALID; }
+  *out = nullptr;
+  if (kind < STB_V || kind > STB_D) { set_error("bem_assemble_toeplitz: kind must be 0 (V), 1 (K) or 2 (D)"); return BEM_E_INVALID; }
+  if (!m->uniform) { set_error("bem_assemble_toeplitz: needs equal time steps"); return BEM_E_STATE; }
+  if (m->nranks > 1) { set_error("bem_assemble_toeplitz: one process (the Toeplitz blocks are replicated)"); return BEM_E_STATE; }
+  int q_bulk = (o && o->q_bulk > 0) ? o->q_bulk : (kind == STB_D ? m->q_bulk_d : m->q_bulk);
+  int q_sing = (o && o->q_sing > 0) ? o->q_sing : 12;
+  if (q_bulk < 3 || q_bulk > 8 || q_bulk == 7) { set_error("bem_assemble_toeplitz: q_bulk must be one of 3,4,5,6,8"); return BEM_E_INVALID; }
+  if (q_sing < 4 || q_sing > QSING_MAX) { set_error("bem_assemble_toeplitz: q_sing must be in [4,16]"); return BEM_E_INVALID; }
+  cudaSetDevice(m->device);
+  bem_status st;
+  bem_matrix* A = new_dense(m, kind, false, S(s), &st, true);
+  if (!A) return st;
+  st = launch_assembly(kind, m, A, q_bulk, q_sing, o ? o->flags : 0, S(s));
+  if (st != BEM_OK) { bem_matrix_destroy(A); return st; }
+  *out = A;
+  return BEM_OK;
+}
 
 bem_status bem_assemble_V(const bem_mesh* m, const bem_quad_opts* o, bem_stream s, bem_matrix** out) {
   return assemble(STB_V, m, o, s, out);
@@ -568,7 +605,7 @@ bem_status bem_matrix_info(const bem_matrix* A, int* kind, long long* entries, l
       per_block = 0;
       for (int i = 0; i < m->ng; ++i) per_block += m->ng - (i / SYM_TS) * SYM_TS;
     }
-    for (auto& b : m->blocks)
+    for (auto& b : blocks_of(A))
       for (int a = b.a0; a < b.a1; ++a) ent += per_block * panel_nb(a, b.b0, b.b1);
   } else {
     ent = 3LL * A->mesh->ng * A->mesh->nt;

@@ -359,12 +359,12 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bul
   const int ntile = (ng + 31) / 32, pslots = 2 * ntile + 5;
   double* d_part = nullptr;
   size_t part_bytes = 0;
-  std::vector<long long> pbase(m->blocks.size(), 0);
+  std::vector<long long> pbase(blocks_of(A).size(), 0);
   if (prod) {
     long long tot = 0;
-    for (size_t bi = 0; bi < m->blocks.size(); ++bi) {
+    for (size_t bi = 0; bi < blocks_of(A).size(); ++bi) {
       pbase[bi] = tot;
-      tot += (long long)(m->blocks[bi].a1 - m->blocks[bi].a0) * ng * pslots;
+      tot += (long long)(blocks_of(A)[bi].a1 - blocks_of(A)[bi].a0) * ng * pslots;
     }
     part_bytes = sizeof(double) * std::max<long long>(1, tot);
     if ((e = storage_acquire(m->device, part_bytes, st, (void**)&d_part)) != cudaSuccess ||
@@ -419,8 +419,8 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bul
     npairs_computed = 0;
     for (int i = 0; i < ng; ++i) npairs_computed += ng - (i / SYM_TS) * SYM_TS;
   }
-  for (size_t bi = 0; bi < m->blocks.size(); ++bi) {
-    const Block& blk = m->blocks[bi];
+  for (size_t bi = 0; bi < blocks_of(A).size(); ++bi) {
+    const Block& blk = blocks_of(A)[bi];
     BlockArgs BA;
     BA.out = A->data;
     BA.poff = d_poff + A->poff_base[bi];
@@ -485,9 +485,9 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bul
     std::vector<long long> roff;
     for (int a = 0; a < m->nt; ++a) {
       rstart[a] = (int)roff.size();
-      for (size_t bi = 0; bi < m->blocks.size(); ++bi)
-        if (m->blocks[bi].a0 <= a && a < m->blocks[bi].a1)
-          roff.push_back(pbase[bi] - (long long)m->blocks[bi].a0 * ng * pslots);
+      for (size_t bi = 0; bi < blocks_of(A).size(); ++bi)
+        if (blocks_of(A)[bi].a0 <= a && a < blocks_of(A)[bi].a1)
+          roff.push_back(pbase[bi] - (long long)blocks_of(A)[bi].a0 * ng * pslots);
     }
     rstart[m->nt] = (int)roff.size();
     int* d_rs = nullptr;

@@ -82,6 +82,7 @@ struct bem_mesh_s {
   std::vector<stb::Block> blocks; // blocks owned by this rank
   long long entries_owned = 0;
   double hmax = 0, htmin = 0, kappa = 0;
+  bool uniform = false;           // equal time steps (block-Toeplitz variant allowed)
   int q_bulk = 4;     // V_h, K_h (primal segments)
   int q_bulk_d = 4;   // D_h (half segments)
   bem_comm* comm = nullptr;
@@ -112,6 +113,8 @@ struct bem_matrix_s {
   // dense block-lower-triangular storage (V, K, D)
   double* data = nullptr;
   int sym = 0;                 // symmetric packed spatial blocks (V, D)
+  int toeplitz = 0;            // block-Toeplitz variant: stores T_d = A(d, 0), d < N_I (full blocks)
+  std::vector<stb::Block> own_blocks;   // toeplitz: the single first-block-column block
   long long blk_elems = 0;     // sym: stored doubles per (a,b) block
   size_t data_bytes = 0;       // size of the storage block (>= 8 * entries; cached on destroy)
   long long entries = 0;       // stored doubles (with row padding)
@@ -155,6 +158,7 @@ struct bem_matrix_s {
 };
 
 namespace stb {
+inline const std::vector<Block>& blocks_of(const bem_matrix_s* A);
 // error handling
 void set_error(const std::string& msg);
 // the mesh's device data are ready on stream st (stream-ordered wait on the upload event)
@@ -213,4 +217,13 @@ void vec_combine(double* out, const double* Q, long long ldq, int k, const doubl
 void vec_mul(double* y, const double* d, const double* x, long long n, cudaStream_t st);
 // collectives (comm.cpp)
 bem_status allreduce_sum(const bem_mesh* m, double* buf, long long n, cudaStream_t st);
+}  // namespace stb
+
+namespace stb {
+// the temporal blocks a matrix stores: the mesh's owned blocks, or the toeplitz matrix's own
+inline const std::vector<Block>& blocks_of(const bem_matrix_s* A) {
+  return A->toeplitz ? A->own_blocks : A->mesh->blocks;
+}
+bem_status toeplitz_gemv(const bem_matrix* A, double a, const double* x, double b, double* y,
+                         cudaStream_t st);
 }  // namespace stb

@@ -266,6 +266,7 @@ static int gemv_ctas_per_sm() {
 
 bem_status gemv_launch(const bem_matrix* A, double a, const double* x, double b, double* y,
                        cudaStream_t st) {
+  if (A->toeplitz) return toeplitz_gemv(A, a, x, b, y, st);
   const bem_mesh* m = A->mesh;
   const long long n = (long long)m->ng * m->nt;
   if (A->n_items > 0 && A->sym) {
@@ -293,6 +294,102 @@ bem_status gemv_launch(const bem_matrix* A, double a, const double* x, double b,
   }
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? BEM_OK : cuda_fail(e, "bem_matvec");
+}
+
+
+// ---------------------------------------------------------------- block-Toeplitz variant
+// Uniform time steps: A(a, b) = T_{a-b}.  Y[i, a] = sum_{d <= a} sum_j T_d[i, j] X[j, a - d] with
+// X[j, b] = x[b ng + j]: one GEMM over the stacked contraction index k = d ng + j (SURVEY 8(f) row
+// f3) — a genuine contraction (many right-hand sides through the Toeplitz shift).  CTA tile
+// 64 rows i x 64 columns a, K split into chunks (fixed partial slots, reduced in fixed order);
+// register tile 4 x 4 per thread, DFMA (FP64 tensor cores are not faster on B200).
+constexpr int TZ_TI = 64, TZ_TA = 64, TZ_TK = 32, TZ_KSPLIT = 4096;
+__global__ void __launch_bounds__(256) k_toeplitz_mm(const double* __restrict__ T, long long ldT_d,
+                                                    int ldT, const double* __restrict__ x, int ng, int nt,
+                                                    double* __restrict__ part) {
+  __shared__ double Tt[TZ_TK][TZ_TI + 2];   // transposed T tile: Tt[jj][ii]
+  __shared__ double Xs[TZ_TK][TZ_TA + 2];
+  const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
+  const int i0 = blockIdx.x * TZ_TI, a0 = blockIdx.y * TZ_TA;
+  // K chunk z: the time lags d in [z dpz, (z + 1) dpz), all trial elements j of each
+  const int dpz = max(1, TZ_KSPLIT / ng);
+  const int d0 = blockIdx.z * dpz, d1 = min(nt, d0 + dpz);
+  double acc[4][4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
+  for (int d = d0; d < d1 && d <= a0 + TZ_TA - 1; ++d) {   // d > a for every column a: nothing left
+    for (int j0 = 0; j0 < ng; j0 += TZ_TK) {
+      __syncthreads();
+      // T_d[i0 + ii][j0 + jj] -> Tt[jj][ii]   (2048 doubles, 8 per thread, coalesced along jj)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int e = tid + q * 256, ii = e / TZ_TK, jj = e % TZ_TK;
+        const int i = i0 + ii, j = j0 + jj;
+        Tt[jj][ii] = (i < ng && j < ng) ? T[(long long)d * ldT_d + (long long)i * ldT + j] : 0.0;
+      }
+      // X[j0 + jj][a0 + aa - d] -> Xs[jj][aa]
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int e = tid + q * 256, jj = e / TZ_TA, aa = e % TZ_TA;
+        const int j = j0 + jj, b = a0 + aa - d;
+        Xs[jj][aa] = (j < ng && b >= 0 && b < nt) ? x[(long long)b * ng + j] : 0.0;
+      }
+      __syncthreads();
+#pragma unroll 8
+      for (int jj = 0; jj < TZ_TK; ++jj) {
+        double tv[4], xv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) tv[u] = Tt[jj][ty * 4 + u];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) xv[v] = Xs[jj][tx * 4 + v];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) acc[u][v] = fma(tv[u], xv[v], acc[u][v]);
+      }
+    }
+  }
+  // partial Y tile of this K chunk: part[z][a][i]
+  const long long n = (long long)nt * ng;
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int i = i0 + ty * 4 + u, a = a0 + tx * 4 + v;
+      if (i < ng && a < nt) part[(long long)blockIdx.z * n + (long long)a * ng + i] = acc[u][v];
+    }
+}
+__global__ void k_toeplitz_reduce(const double* __restrict__ part, int nsplit, long long n, double alpha,
+                                  double beta, double* __restrict__ y) {
+  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  double s = 0.0;
+  for (int z = 0; z < nsplit; ++z) s += part[(long long)z * n + r];
+  y[r] = (beta == 0.0) ? alpha * s : fma(alpha, s, beta * y[r]);
+}
+
+bem_status toeplitz_gemv(const bem_matrix* A, double a, const double* x, double b, double* y,
+                         cudaStream_t st) {
+  const bem_mesh* m = A->mesh;
+  const int ng = m->ng, nt = m->nt;
+  const long long n = (long long)ng * nt;
+  const int dpz = std::max(1, TZ_KSPLIT / ng);
+  const int nsplit = (nt + dpz - 1) / dpz;
+  double* part = nullptr;
+  const size_t bytes = sizeof(double) * n * nsplit;
+  cudaError_t e = storage_acquire(m->device, bytes, st, (void**)&part);
+  if (e != cudaSuccess) return cuda_fail(e, "toeplitz product");
+  e = cudaMemsetAsync(part, 0, bytes, st);   // chunks that break early leave their slots zero
+  dim3 grid((ng + TZ_TI - 1) / TZ_TI, (nt + TZ_TA - 1) / TZ_TA, nsplit);
+  k_toeplitz_mm<<<grid, 256, 0, st>>>(A->data, A->poff.size() > 1 ? A->poff[1] - A->poff[0] : 0,
+                                      (int)pad4(ng), x, ng, nt, part);
+  k_toeplitz_reduce<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(part, nsplit, n, a, b, y);
+  count_launch(2);
+  storage_release(m->device, part, bytes, st);
+  e = cudaGetLastError();
+  return e == cudaSuccess ? BEM_OK : cuda_fail(e, "toeplitz product");
 }
 
 // ------------------------------------------------------------------ mass matrices

@@ -326,6 +326,9 @@ bem_status bem_mesh_create(const bem_mesh_desc* d, bem_comm* comm, bem_mesh** ou
   m->htmin = 1e300;
   for (int a = 0; a < m->nt; ++a) m->htmin = std::min(m->htmin, m->t[a + 1] - m->t[a]);
   m->kappa = m->alpha * m->hmax * m->hmax / (4.0 * m->htmin);
+  m->uniform = true;
+  for (int a = 0; a < m->nt; ++a)
+    if (std::fabs((m->t[a + 1] - m->t[a]) - (m->t[1] - m->t[0])) > 1e-13 * (m->t[1] - m->t[0])) m->uniform = false;
   // Gauss order for the bulk (d >= 2) from the measured error table
   m->q_bulk = m->kappa <= 0.065 ? 4 : (m->kappa <= 0.3 ? 5 : (m->kappa <= 1.0 ? 6 : 8));
   {  // half segments: kappa / 4

@@ -106,6 +106,7 @@ _SIGS = {
     "bem_mass_solve": (I, [P, I, P, P, P]),
     "bem_rhs": (I, [P, P, P, P, P]),
     "bem_rhs_fused": (I, [P, P, P, P, P, P, P]),
+    "bem_assemble_toeplitz": (I, [P, I, P, P, PP]),
     "bem_solve_gmres": (I, [P, P, P, P, P, ctypes.POINTER(GmresOpts), ctypes.POINTER(SolveReport), P, P]),
     "bem_matrix_get": (I, [P, LL, LL, LL, LL, P]),
     "bem_matrix_get_entries": (I, [P, LL, P, P, P]),
@@ -260,6 +261,13 @@ class Mesh:
 
     def assemble_D(self, **kw):
         return self._assemble(lib().bem_assemble_D, **kw)
+
+    def assemble_toeplitz(self, kind, q_bulk=0, q_sing=0, stream=None):
+        """block-Toeplitz variant (uniform steps): kind 'V', 'K' or 'D' -> T_d = A(d, 0)"""
+        o = QuadOpts(q_bulk, q_sing, 0)
+        h = ctypes.c_void_p()
+        check(lib().bem_assemble_toeplitz(self.h, "VKD".index(kind), ctypes.byref(o), _stream(stream), ctypes.byref(h)))
+        return Matrix(h, self)
 
     def assemble_M(self, kind, stream=None):
         h = ctypes.c_void_p()

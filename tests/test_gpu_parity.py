@@ -299,3 +299,44 @@ def test_rhs_fused(name, n_slices):
     ref = om.rhs(oracle_dense(name, "K") if name in ("C1", "LT") else om.dense("K"), W.dirichlet_data(w))
     assert relmax(bf, ref) <= 1e-11
     assert st["fused_sing"] == 1 and st["evals_bulk"] > 0
+
+
+@pytest.mark.parametrize("name", ["C1", "S32"])
+def test_block_toeplitz_variant(name):
+    """row f3: on equal time steps the first block column T_d = A(d, 0) reproduces every entry
+    (A(a, b) = T_{a-b}), the Toeplitz GEMM product equals the dense product, and GMRES with the
+    Toeplitz V_h and D_h returns the dense solution"""
+    w = W.get(name)
+    m = S.Mesh.from_workload(w)
+    x = W.random_vector(w.n)
+    mats = {}
+    for kind in "VKD":
+        T = m.assemble_toeplitz(kind)
+        Dn = getattr(m, f"assemble_{kind}")()
+        dT, dD = T.dense(), Dn.dense()
+        assert relmax(dT, dD) <= 1e-13, (kind, relmax(dT, dD))
+        assert relmax(dT, oracle_dense(name, kind) if name == "C1" else dD) <= 1e-11
+        yT = torch.empty(w.n, dtype=torch.float64, device="cuda")
+        yD = torch.empty_like(yT)
+        T.matvec(cuda(x), yT)
+        Dn.matvec(cuda(x), yD)
+        assert relmax(yT.cpu().numpy(), yD.cpu().numpy()) <= 1e-13
+        assert T.stats()["entries"] == w.n_steps * w.n_gamma ** 2
+        mats[kind] = (T, Dn)
+    g = cuda(W.dirichlet_data(w))
+    Mp, Me = m.assemble_M(S.MASS_PRIMAL), m.assemble_M(S.MASS_DUAL)
+    sols = []
+    for i in (0, 1):
+        b = torch.empty_like(g)
+        S.rhs(mats["K"][i], Mp, g, b)
+        wv = torch.zeros_like(g)
+        rep = S.solve_gmres(mats["V"][i], b, wv, D=mats["D"][i], M=Me, rel_tol=1e-10, max_iter=200, precond=2)
+        assert rep["converged"]
+        sols.append(wv.cpu().numpy())
+    assert relmax(sols[0], sols[1]) <= 1e-9
+
+
+def test_block_toeplitz_needs_uniform_steps():
+    m = S.Mesh.from_workload(W.get("LT"))      # graded steps
+    with pytest.raises(S.BemError):
+        m.assemble_toeplitz("V")
