@@ -15,12 +15,12 @@
 //   A  x_max = c_max/s < 4: the polynomials of moment_coeffs.h in x, so the sum over points is
 //      sum_k f_k s^{-k} M_k with time-independent moments M_k = sum_p W_p c_p^k: one Horner
 //      chain in u = 1/s per kernel family, independent of the number of quadrature points.
-//   B  the points are clustered, rho = (c_max - c0)/c0 <= 0.3: Taylor expansion in c around c0
+//   B  the points are clustered, rho = (c_max - c0)/c0 <= 0.5: Taylor expansion in c around c0
 //      with shifted moments m_k = sum_p W_p (c_p - c0)^k; the node-dependent Taylor
 //      coefficients of E1 / (1+x)E1 - e^{-x} / e^{-x}/x - E1 come from the recurrence for
 //      e^{-x}/x (x f = e^{-x}).  The remainder is bounded by rho^K (the pole of E1' at c = 0)
 //      and e^{-x0} (rho x0)^K / K! <= rho^K / sqrt(2 pi K) (the exponential), so the order per
-//      pair is K = min(32, ceil(ln 1e-17 / ln rho)) (relative error below 1e-17 sum |W|).
+//      pair is K = min(56, ceil(ln 1e-17 / ln rho)) (relative error ~1e-17..1e-16 sum |W|).
 //   Z  x_min >= 50: the E1 / exp parts are below 1e-23; only the affine constants remain.
 //   C  otherwise: the point-by-point sum (same quadrature), dealt over the 32 lanes of the warp.
 // The records (moments and constants) depend on the spatial pair only: built once per
@@ -32,8 +32,8 @@
 namespace stb {
 
 constexpr int MKA = 17;          // regime-A polynomial degree (MGH, MEIN; MPSI padded)
-constexpr int MKB = 32;          // regime-B maximum Taylor order
-constexpr double MRHO = 0.3;     // regime-B cluster bound (c_max - c0 <= MRHO c0)
+constexpr int MKB = 56;          // regime-B maximum Taylor order
+constexpr double MRHO = 0.5;     // regime-B cluster bound (c_max - c0 <= MRHO c0)
 constexpr double MXZ = 50.0;     // regime Z threshold on x_min
 // record layout (field-major, stride npairs): common fields, then one block per family
 enum { RF_CMAX = 0, RF_CMIN = 1, RF_C0 = 2, RF_KB = 3, RF_IC0 = 4, RF_COMMON = 5 };
@@ -50,10 +50,14 @@ template <> struct Fams<STB_D> { static constexpr int n = 2, f0 = FAM_H, f1 = FA
 template <int KIND> constexpr int rec_fields() { return RF_COMMON + Fams<KIND>::n * FAMSZ; }
 
 static __device__ __constant__ const double STB_INV[MKB + 2] = {
-    0.0,      1.0,      1.0 / 2,  1.0 / 3,  1.0 / 4,  1.0 / 5,  1.0 / 6,  1.0 / 7,  1.0 / 8,
-    1.0 / 9,  1.0 / 10, 1.0 / 11, 1.0 / 12, 1.0 / 13, 1.0 / 14, 1.0 / 15, 1.0 / 16, 1.0 / 17,
-    1.0 / 18, 1.0 / 19, 1.0 / 20, 1.0 / 21, 1.0 / 22, 1.0 / 23, 1.0 / 24, 1.0 / 25, 1.0 / 26,
-    1.0 / 27, 1.0 / 28, 1.0 / 29, 1.0 / 30, 1.0 / 31, 1.0 / 32, 1.0 / 33};
+    0.0, 1.0, 1.0 / 2, 1.0 / 3, 1.0 / 4, 1.0 / 5, 1.0 / 6, 1.0 / 7,
+    1.0 / 8, 1.0 / 9, 1.0 / 10, 1.0 / 11, 1.0 / 12, 1.0 / 13, 1.0 / 14, 1.0 / 15,
+    1.0 / 16, 1.0 / 17, 1.0 / 18, 1.0 / 19, 1.0 / 20, 1.0 / 21, 1.0 / 22, 1.0 / 23,
+    1.0 / 24, 1.0 / 25, 1.0 / 26, 1.0 / 27, 1.0 / 28, 1.0 / 29, 1.0 / 30, 1.0 / 31,
+    1.0 / 32, 1.0 / 33, 1.0 / 34, 1.0 / 35, 1.0 / 36, 1.0 / 37, 1.0 / 38, 1.0 / 39,
+    1.0 / 40, 1.0 / 41, 1.0 / 42, 1.0 / 43, 1.0 / 44, 1.0 / 45, 1.0 / 46, 1.0 / 47,
+    1.0 / 48, 1.0 / 49, 1.0 / 50, 1.0 / 51, 1.0 / 52, 1.0 / 53, 1.0 / 54, 1.0 / 55,
+    1.0 / 56, 1.0 / 57};
 
 #define STB_INV_H STB_INV
 
