@@ -148,7 +148,7 @@ struct bem_matrix_s {
   double* d_lo = nullptr;
   double* d_di = nullptr;
   double* d_up = nullptr;
-  double* d_work = nullptr;  // tridiagonal solve scratch (3 n)
+  double* d_work = nullptr;  // dual mass: cyclic-tridiagonal factors, 2 x N_I x (4 N_Gamma + 2)
   // assembly statistics
   double ms_bulk = 0, ms_near = 0, ms_sing = 0, ms_records = 0;
   long long ev_bulk = 0, ev_near = 0, nodes_expected = 0;

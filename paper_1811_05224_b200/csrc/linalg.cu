@@ -419,6 +419,9 @@ __global__ void k_mass_fill(int kind, const Seg* __restrict__ seg, const Dual* _
   }
 }
 
+__global__ void k_cyclic_factor(const double* __restrict__ lo, const double* __restrict__ di,
+                                const double* __restrict__ up, int ng, int nt, double* __restrict__ fac);
+
 bem_status mass_setup(bem_matrix* M, int kind) {
   const bem_mesh* m = M->mesh;
   const long long n = (long long)m->ng * m->nt;
@@ -429,10 +432,14 @@ bem_status mass_setup(bem_matrix* M, int kind) {
   if ((e = cudaMallocAsync((void**)&M->d_lo, sizeof(double) * n, st)) != cudaSuccess ||
       (e = cudaMallocAsync((void**)&M->d_di, sizeof(double) * n, st)) != cudaSuccess ||
       (e = cudaMallocAsync((void**)&M->d_up, sizeof(double) * n, st)) != cudaSuccess ||
-      (e = cudaMallocAsync((void**)&M->d_work, sizeof(double) * 3 * n, st)) != cudaSuccess)
+      (e = cudaMallocAsync((void**)&M->d_work, sizeof(double) * 2 * (4 * n + 2LL * m->nt), st)) != cudaSuccess)
     return cuda_fail(e, "bem_assemble_M");
   k_mass_fill<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(kind, m->d_seg, m->d_dual, m->d_t, m->ng, m->nt, M->d_lo, M->d_di, M->d_up);
   count_launch();
+  if (kind == BEM_MASS_DUAL) {   // factorisation for both transpose flags, once per matrix
+    k_cyclic_factor<<<(2 * m->nt + 63) / 64, 64, 0, st>>>(M->d_lo, M->d_di, M->d_up, m->ng, m->nt, M->d_work);
+    count_launch();
+  }
   e = cudaGetLastError();
   return e == cudaSuccess ? BEM_OK : cuda_fail(e, "bem_assemble_M");
 }
@@ -460,47 +467,83 @@ bem_status mass_apply(const bem_matrix* M, double a, const double* x, double b, 
 
 // cyclic tridiagonal solve per time step (Sherman-Morrison around the Thomas algorithm).
 // Row l of the (transposed) system: sub s_l at column l-1, diag d_l, super p_l at column l+1.
-__global__ void k_cyclic_solve(const double* __restrict__ lo, const double* __restrict__ di,
-                               const double* __restrict__ up, int ng, int nt, int transpose,
-                               const double* __restrict__ x, double* __restrict__ y,
-                               double* __restrict__ work) {
-  const int a = blockIdx.x * blockDim.x + threadIdx.x;
-  if (a >= nt) return;
+// Cyclic tridiagonal dual mass (one system of N_Gamma unknowns per time step): the
+// factorisation does not depend on the right-hand side, so it is computed once per matrix and
+// transpose flag (k_cyclic_factor: Thomas on the first / last diagonal modified system plus the
+// Sherman-Morrison vector z), and a solve is a forward / backward substitution with precomputed
+// multipliers: one warp per time step stages x and the factors in shared memory (coalesced),
+// lane 0 runs the two FMA recurrences, the warp writes y = yy - fact z.
+// factor layout per (transpose t, step a): [sl, inv, cp, zz] x ng, then 2 scalars (alpha/gam, den)
+__global__ void k_cyclic_factor(const double* __restrict__ lo, const double* __restrict__ di,
+                                const double* __restrict__ up, int ng, int nt, double* __restrict__ fac) {
+  const int id = blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= 2 * nt) return;
+  const int transpose = id / nt, a = id % nt;
   const long long base = (long long)a * ng;
-  auto sub = [&](int l) -> double {   // coefficient at column l-1 of row l
-    return transpose ? up[base + (l - 1 + ng) % ng] : lo[base + l];
-  };
-  auto sup = [&](int l) -> double {   // coefficient at column l+1 of row l
-    return transpose ? lo[base + (l + 1) % ng] : up[base + l];
-  };
+  auto sub = [&](int l) -> double { return transpose ? up[base + (l - 1 + ng) % ng] : lo[base + l]; };
+  auto sup = [&](int l) -> double { return transpose ? lo[base + (l + 1) % ng] : up[base + l]; };
   auto dia = [&](int l) -> double { return di[base + l]; };
-  double* cp = work + 3 * base;       // modified super-diagonal
-  double* yy = cp + ng;               // solution of T y = rhs
-  double* zz = yy + ng;               // solution of T z = u
+  double* F = fac + (long long)id * (4LL * ng + 2);
+  double* sl = F;
+  double* inv = F + ng;
+  double* cp = F + 2 * ng;
+  double* zz = F + 3 * ng;
   const double alpha_c = sub(0);      // row 0, column ng-1
   const double beta_c = sup(ng - 1);  // row ng-1, column 0
   const double gam = -dia(0);
-  // Thomas for T (first / last diagonal modified) with two right-hand sides
-  double b0 = dia(0) - gam;
-  cp[0] = sup(0) / b0;
-  yy[0] = x[base] / b0;
-  zz[0] = gam / b0;
+  double den = dia(0) - gam;
+  sl[0] = 0.0;
+  inv[0] = 1.0 / den;
+  cp[0] = sup(0) * inv[0];
+  zz[0] = gam * inv[0];
   for (int l = 1; l < ng; ++l) {
     double bl = dia(l);
     if (l == ng - 1) bl -= alpha_c * beta_c / gam;
-    const double sl = sub(l);
-    const double den = bl - sl * cp[l - 1];
-    cp[l] = (l < ng - 1) ? sup(l) / den : 0.0;
-    yy[l] = (x[base + l] - sl * yy[l - 1]) / den;
+    sl[l] = sub(l);
+    den = bl - sl[l] * cp[l - 1];
+    inv[l] = 1.0 / den;
+    cp[l] = (l < ng - 1) ? sup(l) * inv[l] : 0.0;
     const double ul = (l == ng - 1) ? beta_c : 0.0;
-    zz[l] = (ul - sl * zz[l - 1]) / den;
+    zz[l] = (ul - sl[l] * zz[l - 1]) * inv[l];
   }
-  for (int l = ng - 2; l >= 0; --l) {
-    yy[l] -= cp[l] * yy[l + 1];
-    zz[l] -= cp[l] * zz[l + 1];
+  for (int l = ng - 2; l >= 0; --l) zz[l] -= cp[l] * zz[l + 1];
+  F[4 * ng] = alpha_c / gam;
+  F[4 * ng + 1] = 1.0 + zz[0] + (alpha_c / gam) * zz[ng - 1];
+}
+
+__global__ void __launch_bounds__(32) k_cyclic_solve(const double* __restrict__ fac, int ng, int nt,
+                                                    int transpose, const double* __restrict__ x,
+                                                    double* __restrict__ y) {
+  extern __shared__ double sm[];   // x / yy, sl, inv, cp  (4 ng)
+  const int a = blockIdx.x, lane = threadIdx.x;
+  const long long base = (long long)a * ng;
+  const double* F = fac + ((long long)transpose * nt + a) * (4LL * ng + 2);
+  double* yy = sm;
+  double* sl = sm + ng;
+  double* inv = sm + 2 * ng;
+  double* cp = sm + 3 * ng;
+  for (int l = lane; l < ng; l += 32) {
+    yy[l] = x[base + l];
+    sl[l] = F[l];
+    inv[l] = F[ng + l];
+    cp[l] = F[2 * ng + l];
   }
-  const double fact = (yy[0] + alpha_c * yy[ng - 1] / gam) / (1.0 + zz[0] + alpha_c * zz[ng - 1] / gam);
-  for (int l = 0; l < ng; ++l) y[base + l] = yy[l] - fact * zz[l];
+  __syncwarp();
+  if (lane == 0) {
+    double v = yy[0] * inv[0];
+    yy[0] = v;
+    for (int l = 1; l < ng; ++l) {
+      v = (yy[l] - sl[l] * v) * inv[l];
+      yy[l] = v;
+    }
+    for (int l = ng - 2; l >= 0; --l) {
+      v = yy[l] - cp[l] * v;
+      yy[l] = v;
+    }
+  }
+  __syncwarp();
+  const double fact = (yy[0] + F[4 * ng] * yy[ng - 1]) / F[4 * ng + 1];
+  for (int l = lane; l < ng; l += 32) y[base + l] = yy[l] - fact * F[3 * ng + l];
 }
 
 __global__ void k_diag_solve(const double* __restrict__ di, long long n, const double* __restrict__ x,
@@ -516,7 +559,7 @@ bem_status mass_solve(const bem_matrix* M, int transpose, const double* x, doubl
   if (M->mass_kind == BEM_MASS_DUAL_LUMPED) {
     k_diag_solve<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(M->d_di, n, x, y);
   } else {
-    k_cyclic_solve<<<(m->nt + 63) / 64, 64, 0, st>>>(M->d_lo, M->d_di, M->d_up, m->ng, m->nt, transpose, x, y, M->d_work);
+    k_cyclic_solve<<<m->nt, 32, sizeof(double) * 4 * m->ng, st>>>(M->d_work, m->ng, m->nt, transpose ? 1 : 0, x, y);
   }
   count_launch();
   cudaError_t e = cudaGetLastError();
