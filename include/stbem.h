@@ -218,6 +218,14 @@ bem_status bem_rhs_fused(const bem_mesh* mesh, const bem_quad_opts* opts, const 
  * already queued there, e.g. the right-hand side) and synchronises it once per iteration (the
  * Hessenberg column goes to the host for the Givens rotation).  Returns BEM_E_NOT_CONVERGED /
  * BEM_E_BREAKDOWN with w and the report filled. */
+/* Representation formula in the space-time cylinder (eq. 2), u0 = 0:
+ * u(x,t) = (Vt w)(x,t) - (W g)(x,t) for the Neumann density w (piecewise constant, as solved by
+ * bem_solve_gmres) and the Dirichlet data g (nodal, as in bem_rhs).  Time integrals exact, Gauss
+ * order per element from the distance (16 / 12 / 8).  pts_dev: npts x 3 doubles (x1, x2, t),
+ * device; u_dev: npts doubles, device; w_dev, g_dev: N doubles, device.  Synchronises the stream.
+ * Errors: BEM_E_INVALID (bad argument, or a point closer than h_max to Gamma), BEM_E_CUDA. */
+bem_status bem_eval_potential(const bem_mesh* mesh, const double* w_dev, const double* g_dev,
+                              long long npts, const double* pts_dev, double* u_dev, bem_stream stream);
 bem_status bem_solve_gmres(const bem_matrix* V, const bem_matrix* D, const bem_matrix* M,
                            const double* b_dev, double* w_dev, const bem_gmres_opts* opts,
                            bem_solve_report* report, double* res_hist_host, bem_stream stream);

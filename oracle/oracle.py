@@ -13,7 +13,8 @@ module adds, in plain numpy and in the paper's order:
     C_V^{-1} = M_h^{-1} D_h M_h^{-T} (lumped or exact), stopping on the
     Givens estimate of the preconditioned relative residual (P:98-99, P:182);
   * the block forward substitution of the block-lower-triangular V_h (P:151-159);
-  * the L2(Sigma) error of w_h against the exact Neumann datum.
+  * the L2(Sigma) error of w_h against the exact Neumann datum;
+  * the representation formula u = Vt w - W g at interior points (eq. 2; row f2, C code).
 """
 import ctypes
 import os
@@ -66,6 +67,7 @@ def lib():
         L.ora_num_threads.restype = i
         L.ora_pair.restype = d
         L.ora_pair.argtypes = [p, i, i, i, i, i, i, d, d, d, d]
+        L.ora_potential.argtypes = [p, p, p, ll, p, i, p]
         _lib = L
     return _lib
 
@@ -167,6 +169,18 @@ class OracleMesh:
     def rhs(self, K, g):
         """(1/2 M_h + K_h) g (eq. 4) with u0 = 0"""
         return 0.5 * self.mass_primal() @ g + K @ g
+
+    # ------------------------------------------------ representation formula (f2)
+    def potential(self, w, g, pts, q=20):
+        """u(x,t) = (Vt w)(x,t) - (W g)(x,t) at interior points pts[k] = (x1, x2, t), u0 = 0
+        (eq. 2; time integrals exact, Gauss q per element: stbem_oracle.c)"""
+        w = np.ascontiguousarray(w, dtype=np.float64)
+        g = np.ascontiguousarray(g, dtype=np.float64)
+        pts = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1, 3)
+        out = np.empty(len(pts))
+        lib().ora_potential(self.h, w.ctypes.data, g.ctypes.data, len(pts), pts.ctypes.data, int(q),
+                            out.ctypes.data)
+        return out
 
     # ---------------------------------------------------------- L2 error
     def l2_error(self, wh, nq=10):

@@ -595,3 +595,52 @@ int ora_num_threads(void) {
   return 1;
 #endif
 }
+
+/* ------------------------------------------------ representation formula --- */
+/* Row f2: the solution in Q by the representation formula (eq. 2) with
+ * u0 = 0:   u(x,t) = (Vt w)(x,t) - (W g)(x,t)
+ *   (Vt w)(x,t) = (1/alpha) int_Sigma U*(x-y, t-tau) w(y,tau) ds_y dtau
+ *   (W g)(x,t)  = (1/alpha) int_Sigma d_{n_y} U*(x-y, t-tau) g(y,tau) ds_y dtau
+ * w piecewise constant (element j, step b: w[b*ng + j]); g piecewise linear in space (nodal
+ * values, hat phi_n) and constant in time on each step (g[b*ng + n]) -- the discrete spaces of
+ * eq. (4).  Time integrals exact (U* of P:48-54, s = t - tau):
+ *   int (1/alpha) U* dtau       = (1/(4 pi)) [E1(c/s_hi) - E1(c/s_lo)]
+ *   int (1/alpha) d_ny U* dtau  = ((x-y).n_y / (2 pi r^2)) [exp(-c/s_hi) - exp(-c/s_lo)]
+ * with c = alpha r^2/4, s_hi = t - t_b, s_lo = max(0, t - t_{b+1}) (terms with s_lo = 0 vanish).
+ * Space: Gauss-Legendre with q points per element (the caller keeps the points away from Gamma).
+ * pts[3k] = (x1, x2, t).  OpenMP over points. */
+void ora_potential(const ora_mesh* m, const double* w, const double* g, long long npts,
+                   const double* pts, int q, double* out) {
+  init_rules();
+  const ora_rule* R = &RULES[q];
+  const int ng = m->ng, nt = m->nt;
+  const double alpha = m->alpha;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (long long k = 0; k < npts; ++k) {
+    const double x1 = pts[3 * k], x2 = pts[3 * k + 1], t = pts[3 * k + 2];
+    double vw = 0.0, wg = 0.0;
+    for (int b = 0; b < nt && m->t[b] < t; ++b) {
+      const double s_hi = t - m->t[b];
+      const double s_lo = t - m->t[b + 1] > 0.0 ? t - m->t[b + 1] : 0.0;
+      for (int j = 0; j < ng; ++j) {
+        const ora_seg* S = &m->seg[j];
+        const double g0 = g[(long long)b * ng + j], g1 = g[(long long)b * ng + (j + 1) % ng];
+        double sv = 0.0, sw = 0.0;
+        for (int u = 0; u < q; ++u) {
+          const double f = R->x[u];
+          const double y1 = S->ax + f * (S->bx - S->ax), y2 = S->ay + f * (S->by - S->ay);
+          const double d1 = x1 - y1, d2 = x2 - y2;
+          const double r2 = d1 * d1 + d2 * d2;
+          const double c = 0.25 * alpha * r2;
+          const double ev = ora_e1(c / s_hi) - (s_lo > 0.0 ? ora_e1(c / s_lo) : 0.0);
+          const double ex = exp(-c / s_hi) - (s_lo > 0.0 ? exp(-c / s_lo) : 0.0);
+          sv += R->w[u] * ev;
+          sw += R->w[u] * (d1 * S->nx + d2 * S->ny) / r2 * ex * (g0 + f * (g1 - g0));
+        }
+        vw += S->h * w[(long long)b * ng + j] * sv / (4.0 * ORA_PI);
+        wg += S->h * sw / (2.0 * ORA_PI);
+      }
+    }
+    out[k] = vw - wg;
+  }
+}

@@ -311,6 +311,13 @@ bem_status bem_rhs_fused(const bem_mesh* m, const bem_quad_opts* o, const bem_ma
   return st;
 }
 
+bem_status bem_eval_potential(const bem_mesh* m, const double* w, const double* g, long long npts,
+                              const double* pts, double* u, bem_stream s) {
+  if (!m || !w || !g || (npts > 0 && (!pts || !u)) || npts < 0) { set_error("bem_eval_potential: bad argument"); return BEM_E_INVALID; }
+  cudaSetDevice(m->device);
+  return eval_potential(m, w, g, npts, pts, u, S(s));
+}
+
 bem_status bem_eval_special(int which, long long count, const double* x, double* out, bem_stream s) {
   if (which < 0 || which > 3 || count < 0) { set_error("bem_eval_special: bad argument"); return BEM_E_INVALID; }
   return eval_special(which, count, x, out, S(s));

@@ -130,6 +130,7 @@ __host__ __device__ inline bool collinear(const Seg& X, const Seg& Y) {
 }  // namespace stb
 
 #include "moments.cuh"
+#include "potential.cuh"
 
 namespace stb {
 
@@ -549,6 +550,31 @@ bem_status finalize_assembly_stats(bem_matrix* A) {
   if (ctr[13] != 0) {
     set_error("assembly stats: touching-pair moment record outside regime A");
     return BEM_E_CUDA;
+  }
+  return BEM_OK;
+}
+
+// representation formula (row f2): u = Vt w - W g at npts interior points (device arrays)
+bem_status eval_potential(const bem_mesh* m, const double* w, const double* g, long long npts,
+                          const double* pts, double* out, cudaStream_t st) {
+  if (npts <= 0) return BEM_OK;
+  mesh_wait(m, st);
+  int* d_bad = nullptr;
+  cudaError_t e;
+  if ((e = cudaMallocAsync((void**)&d_bad, sizeof(int), st)) != cudaSuccess ||
+      (e = cudaMemsetAsync(d_bad, 0, sizeof(int), st)) != cudaSuccess)
+    return cuda_fail(e, "eval_potential");
+  const unsigned nblk = (unsigned)((npts * 32 + 127) / 128);
+  k_potential<<<nblk, 128, 0, st>>>(m->d_seg, m->d_t, m->ng, m->nt, m->alpha, m->hmax, w, g, npts, pts, out, d_bad);
+  count_launch();
+  int bad = 0;
+  cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(d_bad, st);
+  e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "eval_potential");
+  if (bad) {
+    set_error("bem_eval_potential: a point is closer than h_max to Gamma (the interior quadrature needs distance >= h_max)");
+    return BEM_E_INVALID;
   }
   return BEM_OK;
 }

@@ -107,6 +107,7 @@ _SIGS = {
     "bem_rhs": (I, [P, P, P, P, P]),
     "bem_rhs_fused": (I, [P, P, P, P, P, P, P]),
     "bem_assemble_toeplitz": (I, [P, I, P, P, PP]),
+    "bem_eval_potential": (I, [P, P, P, LL, P, P, P]),
     "bem_solve_gmres": (I, [P, P, P, P, P, ctypes.POINTER(GmresOpts), ctypes.POINTER(SolveReport), P, P]),
     "bem_matrix_get": (I, [P, LL, LL, LL, LL, P]),
     "bem_matrix_get_entries": (I, [P, LL, P, P, P]),
@@ -339,6 +340,16 @@ def rhs_fused(mesh, Mp, g, b, q_bulk=0, q_sing=0, legacy_sing=False, stats=False
     check(lib().bem_rhs_fused(mesh.h, ctypes.byref(o), Mp.h, _ptr(g), _ptr(b),
                               ctypes.byref(st) if stats else None, _stream(stream)))
     return st.as_dict() if stats else b
+
+
+def eval_potential(mesh, w, g, pts, out=None, stream=None):
+    """u = Vt w - W g at interior points pts (npts x 3: x1, x2, t), u0 = 0 (bem_eval_potential)"""
+    import torch
+    pts = pts if isinstance(pts, torch.Tensor) else torch.tensor(pts, dtype=torch.float64, device=w.device)
+    pts = pts.contiguous().reshape(-1, 3)
+    out = out if out is not None else torch.empty(pts.shape[0], dtype=torch.float64, device=w.device)
+    check(lib().bem_eval_potential(mesh.h, _ptr(w), _ptr(g), pts.shape[0], _ptr(pts), _ptr(out), _stream(stream)))
+    return out
 
 
 def solve_gmres(V, b, w, D=None, M=None, rel_tol=1e-10, max_iter=500, precond=0, history=True, stream=None):

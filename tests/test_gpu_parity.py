@@ -340,3 +340,51 @@ def test_block_toeplitz_needs_uniform_steps():
     m = S.Mesh.from_workload(W.get("LT"))      # graded steps
     with pytest.raises(S.BemError):
         m.assemble_toeplitz("V")
+
+
+POT_PTS = np.array([[0.5, 0.5, 0.5], [0.25, 0.5, 1.0], [0.5, 0.75, 0.75], [0.3, 0.3, 0.25],
+                    [0.6, 0.35, 0.9], [0.4, 0.65, 0.6], [0.45, 0.5, 0.125], [0.7, 0.7, 0.33]])
+
+
+@pytest.mark.parametrize("name", ["C1", "S32"])
+def test_potential_parity(name):
+    """row f2: the representation formula on the GPU against the oracle's (same w, g)"""
+    w = W.get(name)
+    om = O.OracleMesh(w)
+    g = W.dirichlet_data(w)
+    wh = W.random_vector(w.n)          # any density: the map (w, g) -> u is what is compared
+    m = S.Mesh.from_workload(w)
+    got = S.eval_potential(m, cuda(wh), cuda(g), POT_PTS).cpu().numpy()
+    ref = om.potential(wh, g, POT_PTS)
+    assert relmax(got, ref) <= 1e-11, relmax(got, ref)
+
+
+def test_potential_after_solve_converges():
+    """GPU solve then representation formula: the error against u = U*(x - x*, t) at interior
+    points falls under refinement C1 -> C2 -> C3"""
+    errs = []
+    for name in ("C1", "C2", "C3"):
+        wv, rep = solve(name, 2, 1e-10) if name != "C3" else (None, None)
+        w = W.get(name)
+        if name == "C3":
+            m = S.Mesh.from_workload(w)
+            V, Dm = m.assemble_V(), m.assemble_D()
+            gg = cuda(W.dirichlet_data(w))
+            b = torch.empty_like(gg)
+            S.rhs_fused(m, m.assemble_M(S.MASS_PRIMAL), gg, b)
+            wt = torch.zeros_like(gg)
+            S.solve_gmres(V, b, wt, D=Dm, M=m.assemble_M(S.MASS_DUAL), rel_tol=1e-10, max_iter=200, precond=2)
+            wv = wt.cpu().numpy()
+        m = S.Mesh.from_workload(w)
+        u = S.eval_potential(m, cuda(wv), cuda(W.dirichlet_data(w)), POT_PTS).cpu().numpy()
+        ex = W.exact_solution(w, POT_PTS[:, :2], POT_PTS[:, 2])
+        errs.append(float(np.abs(u - ex).max() / np.abs(ex).max()))
+    print("potential errors", errs)
+    assert errs[0] > errs[1] > errs[2] and errs[2] < 1e-4, errs
+
+
+def test_potential_rejects_boundary_points():
+    w = W.get("C1")
+    m = S.Mesh.from_workload(w)
+    with pytest.raises(S.BemError):
+        S.eval_potential(m, cuda(np.zeros(w.n)), cuda(np.zeros(w.n)), np.array([[0.01, 0.5, 0.5]]))

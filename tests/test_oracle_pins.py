@@ -295,3 +295,92 @@ def test_w_converges_under_refinement():
         errs.append(e / r)
     assert errs[0] == pytest.approx(0.330, abs=0.01)                # prototype: 0.330 -> 0.154
     assert errs[1] < errs[0] / 1.8
+
+
+# ---------------------------------------------------------------- representation formula (f2)
+def _brute_potential(w, j, b, x, t, kind, q=30):
+    """mpmath: (1/alpha) int_{t_b}^{min(t_{b+1}, t)} int_{gamma_j} K(x - y, t - tau) phi(y) ds dtau,
+    kind 'V' (U*, phi = 1) or 'W' (d_ny U*, phi = the hat of node j+1 rising along gamma_j)"""
+    mp.mp.dps = 30
+    nodes = W.data.nodes(w)
+    a, c = nodes[j], nodes[(j + 1) % len(nodes)]
+    h = float(np.hypot(*(c - a)))
+    tan = (c - a) / h
+    nrm = np.array([tan[1], -tan[0]])
+    al = w.alpha
+    t0, t1 = w.t_breaks[b], min(w.t_breaks[b + 1], t)
+
+    def f(sarc, tau):
+        y = a + float(sarc) * tan
+        d = np.asarray(x) - y
+        r2 = mp.mpf(float(d @ d))
+        s = t - tau
+        us = al / (4 * mp.pi * s) * mp.exp(-al * r2 / (4 * s))
+        if kind == "V":
+            return us / al
+        return (us * al * float(d @ nrm) / (2 * s)) / al * (mp.mpf(sarc) / h)
+    return float(mp.quad(f, [0, h], [t0, t1]))
+
+
+@pytest.mark.parametrize("kind", ["V", "W"])
+def test_potential_single_element_brute_force(kind):
+    """one element, one time step: the closed-form time integrals and the Gauss rule of
+    ora_potential against a 2-D mpmath quadrature of the kernel of eq. (2)"""
+    w = W.get("T8")
+    om = O.OracleMesh(w)
+    n = w.n
+    j, b = 3, 2
+    dens = np.zeros(n)
+    pts = np.array([[0.55, 0.4, float(w.t_breaks[b + 1]) + 0.03], [0.35, 0.6, float(w.t_breaks[b]) + 0.05]])
+    if kind == "V":
+        dens[b * w.n_gamma + j] = 1.0
+        got = om.potential(dens, np.zeros(n), pts)
+    else:   # g = hat of node j+1 in step b: rises along gamma_j, falls along gamma_{j+1}
+        g = np.zeros(n)
+        g[b * w.n_gamma + (j + 1)] = 1.0
+        got = om.potential(np.zeros(n), g, pts)
+    for k, (x1, x2, t) in enumerate(pts):
+        ref = _brute_potential(w, j, b, (x1, x2), t, kind)
+        if kind == "W":
+            # -W g: rising part on gamma_j + falling part on gamma_{j+1} (= constant - rising)
+            ref_next_full = _brute_potential_const(w, j + 1, b, (x1, x2), t)
+            ref_next_rise = _brute_potential(w, j + 1, b, (x1, x2), t, "W")
+            ref = -(ref + ref_next_full - ref_next_rise)
+        assert abs(got[k] - ref) <= 1e-12 * max(1e-6, abs(ref)), (kind, k, got[k], ref)
+
+
+def _brute_potential_const(w, j, b, x, t):
+    """W-kernel with phi = 1 on gamma_j"""
+    mp.mp.dps = 30
+    nodes = W.data.nodes(w)
+    a, c = nodes[j], nodes[(j + 1) % len(nodes)]
+    h = float(np.hypot(*(c - a)))
+    tan = (c - a) / h
+    nrm = np.array([tan[1], -tan[0]])
+    al = w.alpha
+    t0, t1 = w.t_breaks[b], min(w.t_breaks[b + 1], t)
+
+    def f(sarc, tau):
+        y = a + float(sarc) * tan
+        d = np.asarray(x) - y
+        r2 = mp.mpf(float(d @ d))
+        s = t - tau
+        us = al / (4 * mp.pi * s) * mp.exp(-al * r2 / (4 * s))
+        return us * float(d @ nrm) / (2 * s)
+    return float(mp.quad(f, [0, h], [t0, t1]))
+
+
+def test_potential_converges_to_manufactured_solution():
+    """u_h = Vt w_h - W g_h at interior points tends to u = U*(x - x*, t) under refinement
+    (T8 -> C1 -> S32; w_h from the oracle's own V_h, K_h and block forward substitution)"""
+    pts = np.array([[0.5, 0.5, 0.5], [0.25, 0.5, 1.0], [0.5, 0.75, 0.75], [0.3, 0.3, 0.25]])
+    errs = []
+    for name in ("T8", "C1", "S32"):
+        w = W.get(name)
+        om = O.OracleMesh(w)
+        g = W.dirichlet_data(w)
+        wh = O.block_forward_solve(om.dense("V"), om.rhs(om.dense("K"), g), om.ng)
+        ex = W.exact_solution(w, pts[:, :2], pts[:, 2])
+        errs.append(np.abs(om.potential(wh, g, pts) - ex).max() / np.abs(ex).max())
+    assert errs[0] > 2.0 * errs[1] > 4.0 * errs[2] * 0.5, errs
+    assert errs[2] < 2e-3, errs

@@ -7,4 +7,4 @@ seeded random vectors.  Both `oracle/` and `paper_1811_05224_b200/` consume it;
 neither imports the other.
 """
 from .configs import CONFIGS, Workload, get  # noqa: F401
-from .data import dirichlet_data, exact_neumann, random_vector  # noqa: F401
+from .data import dirichlet_data, exact_neumann, exact_solution, random_vector  # noqa: F401

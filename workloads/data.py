@@ -46,6 +46,13 @@ def exact_neumann(w: Workload, x: np.ndarray, nrm: np.ndarray, t: np.ndarray) ->
     return -(w.alpha / (2 * t)) * np.sum(d * nrm, axis=-1) * us
 
 
+def exact_solution(w: Workload, x: np.ndarray, t: np.ndarray) -> np.ndarray:
+    """u(x, t) = U*(x - x*, t) (the manufactured solution of the BJ configs), vectorised"""
+    d = np.asarray(x) - np.asarray(w.x_star)
+    r2 = np.sum(d * d, axis=-1)
+    return w.alpha / (4 * np.pi * t) * np.exp(-w.alpha * r2 / (4 * t))
+
+
 def random_vector(n: int, seed: int = 1811) -> np.ndarray:
     """x ~ U(-1, 1), numpy default_rng(seed)"""
     return np.random.default_rng(seed).uniform(-1.0, 1.0, n)
