@@ -68,6 +68,7 @@ def lib():
         L.ora_pair.restype = d
         L.ora_pair.argtypes = [p, i, i, i, i, i, i, d, d, d, d]
         L.ora_potential.argtypes = [p, p, p, ll, p, i, p]
+        L.ora_initial_rhs.argtypes = [p, i, p, i, p, p, i, i, i, p]
         _lib = L
     return _lib
 
@@ -182,10 +183,24 @@ class OracleMesh:
                             out.ctypes.data)
         return out
 
+    # ------------------------------------------------ initial potential (f1)
+    def initial_rhs(self, nodes, tris, u0, qx=4, qt_far=3, qt_near=8):
+        """M_h^0 u0 (P:83, P:89): u0 nodal on the triangulation (nodes (M,2), tris (T,3));
+        exact time integrals, Gauss / collapsed-Gauss in space (stbem_oracle.c)"""
+        nodes = np.ascontiguousarray(nodes, dtype=np.float64)
+        tris = np.ascontiguousarray(tris, dtype=np.int32)
+        u0 = np.ascontiguousarray(u0, dtype=np.float64)
+        out = np.empty(self.n)
+        lib().ora_initial_rhs(self.h, len(nodes), nodes.ctypes.data, len(tris), tris.ctypes.data,
+                              u0.ctypes.data, int(qx), int(qt_far), int(qt_near), out.ctypes.data)
+        return out
+
     # ---------------------------------------------------------- L2 error
-    def l2_error(self, wh, nq=10):
-        """|| w_h - w ||_{L2(Sigma)} and ||w||, Gauss nq x nq per element"""
-        from workloads.data import exact_neumann
+    def l2_error(self, wh, nq=10, exact=None):
+        """|| w_h - w ||_{L2(Sigma)} and ||w||, Gauss nq x nq per element; exact(x, n, t) = d_n u
+        (default: the BJ manufactured solution)"""
+        from workloads.data import exact_neumann as bj_neumann
+        exact_neumann = (lambda w_, x, n, t: exact(x, n, t)) if exact else bj_neumann
         xg, wg = np.polynomial.legendre.leggauss(nq)
         xg, wg = 0.5 * (xg + 1), 0.5 * wg
         t = self._t

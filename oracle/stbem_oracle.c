@@ -644,3 +644,117 @@ void ora_potential(const ora_mesh* m, const double* w, const double* g, long lon
     out[k] = vw - wg;
   }
 }
+
+/* ------------------------------------------------------ initial potential --- */
+/* Row f1: M_h^0 u0 of eq. (4) for the paper's own experiment:
+ *   f[(a,i)] = <M_0 u0_h, phi^0_(a,i)> = int_{t_a}^{t_{a+1}} int_{gamma_i} int_Omega U*(x-y,t) u0_h(y) dy ds_x dt,
+ * u0_h in S_h^1(Omega_h) (nodal values on a triangulation).  Time integral exact:
+ *   int_{t_a}^{t_{a+1}} U*(x-y,t) dt = (alpha/(4 pi)) [E1(c/t_{a+1}) - E1(c/t_a)],  E1(c/0) := 0.
+ * Space: qx Gauss points on gamma_i; per triangle the collapsed (Duffy) tensor Gauss rule
+ *   y = v0 + u (v1-v0) + v (v2-v0), u = xi (1-eta), v = xi eta, dy = 2|tau| xi dxi deta,
+ * with qt_near^2 points when the distance from gamma_i to the triangle's centroid is below
+ * 2 max(h_i, longest edge), else qt_far^2 (reading R22).  OpenMP over elements i. */
+static double seg_point_dist(const ora_seg* S, double px, double py) {
+  double f = (px - S->ax) * S->tx + (py - S->ay) * S->ty;
+  if (f < 0.0) f = 0.0;
+  if (f > S->h) f = S->h;
+  double qx = S->ax + f * S->tx - px, qy = S->ay + f * S->ty - py;
+  return sqrt(qx * qx + qy * qy);
+}
+
+/* integral of F over the triangle (A,B,C) split at the apex P into (P,A,B), (P,B,C), (P,C,A)
+ * with signed areas (P inside, on an edge or outside), each by the collapsed rule with the apex
+ * at P: y = P + xi [(1-eta)(V1-P) + eta (V2-P)], dy = 2 area xi dxi deta; xi on a geometric
+ * composite Gauss rule (ratio 0.15, 10 levels, 8 points each) so that the log singularity of
+ * E1(c/t_1) at y = P is resolved; eta by 12-point Gauss. */
+static void apex_rule_accumulate(double px, double py, const double* V, const double* uv,
+                                 double alpha, double t1, double wx, double* acc) {
+  const ora_rule* RE = &RULES[12];
+  const ora_rule* RR = &RULES[8];
+  for (int s = 0; s < 3; ++s) {
+    const double v1x = V[2 * s], v1y = V[2 * s + 1], v2x = V[2 * ((s + 1) % 3)], v2y = V[2 * ((s + 1) % 3) + 1];
+    const double u1 = uv[s], u2 = uv[(s + 1) % 3];
+    const double e1x = v1x - px, e1y = v1y - py, e2x = v2x - px, e2y = v2y - py;
+    const double area2 = e1x * e2y - e1y * e2x;          /* signed */
+    if (fabs(area2) < 1e-300) continue;
+    double hi = 1.0;
+    for (int lev = 0; lev <= 10; ++lev) {
+      const double lo = lev < 10 ? hi * 0.15 : 0.0;
+      for (int r = 0; r < RR->n; ++r) {
+        const double xi = lo + (hi - lo) * RR->x[r], wxi = (hi - lo) * RR->w[r];
+        for (int e = 0; e < RE->n; ++e) {
+          const double eta = RE->x[e];
+          const double yx = px + xi * ((1.0 - eta) * e1x + eta * e2x);
+          const double yy = py + xi * ((1.0 - eta) * e1y + eta * e2y);
+          /* u0_h at y: the linear interpolant of the triangle's three values */
+          const double uh = uv[3] * 0.0 + (1.0 - xi) * uv[4] + xi * ((1.0 - eta) * u1 + eta * u2);
+          const double dx = px - yx, dy = py - yy;
+          const double c = 0.25 * alpha * (dx * dx + dy * dy);
+          *acc += wx * area2 * xi * wxi * RE->w[e] * uh * ora_e1(c / t1);
+        }
+      }
+      hi = lo;
+    }
+  }
+}
+
+void ora_initial_rhs(const ora_mesh* m, int nnode, const double* nodes, int ntri, const int* tri,
+                     const double* u0, int qx, int qt_far, int qt_near, double* out) {
+  init_rules();
+  (void)nnode;
+  const int ng = m->ng, nt = m->nt;
+  const double alpha = m->alpha;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int i = 0; i < ng; ++i) {
+    const ora_seg* S = &m->seg[i];
+    double* node_sum = (double*)calloc((size_t)(nt + 1), sizeof(double));   /* N(i, n), regular rule */
+    double first = 0.0;                                                       /* step a = 0 */
+    for (int k = 0; k < ntri; ++k) {
+      const int i0 = tri[3 * k], i1 = tri[3 * k + 1], i2 = tri[3 * k + 2];
+      const double ax = nodes[2 * i0], ay = nodes[2 * i0 + 1];
+      const double e1x = nodes[2 * i1] - ax, e1y = nodes[2 * i1 + 1] - ay;
+      const double e2x = nodes[2 * i2] - ax, e2y = nodes[2 * i2 + 1] - ay;
+      const double area2 = fabs(e1x * e2y - e1y * e2x);
+      const double gx = ax + (e1x + e2x) / 3.0, gy = ay + (e1y + e2y) / 3.0;
+      double le = sqrt(e1x * e1x + e1y * e1y);
+      double l2 = sqrt(e2x * e2x + e2y * e2y), l3 = sqrt((e2x - e1x) * (e2x - e1x) + (e2y - e1y) * (e2y - e1y));
+      if (l2 > le) le = l2;
+      if (l3 > le) le = l3;
+      const double hm = S->h > le ? S->h : le;
+      const int near = seg_point_dist(S, gx, gy) < 2.0 * hm;
+      const int qt = near ? qt_near : qt_far;
+      const ora_rule* RT = &RULES[qt];
+      const ora_rule* RX = &RULES[qx];
+      for (int p = 0; p < qx; ++p) {
+        const double xx = S->ax + RX->x[p] * (S->bx - S->ax), xy = S->ay + RX->x[p] * (S->by - S->ay);
+        double first_p = 0.0;
+        for (int a1 = 0; a1 < qt; ++a1)
+          for (int a2 = 0; a2 < qt; ++a2) {
+            const double xi = RT->x[a1], eta = RT->x[a2];
+            const double u = xi * (1.0 - eta), v = xi * eta;
+            const double yx = ax + u * e1x + v * e2x, yy = ay + u * e1y + v * e2y;
+            const double uh = (1.0 - u - v) * u0[i0] + u * u0[i1] + v * u0[i2];
+            const double W = RX->w[p] * S->h * area2 * xi * RT->w[a1] * RT->w[a2] * uh;
+            const double dx = xx - yx, dy = xy - yy;
+            const double c = 0.25 * alpha * (dx * dx + dy * dy);
+            for (int n = 1; n <= nt; ++n) node_sum[n] += W * ora_e1(c / m->t[n]);
+            if (!near) first_p += W * ora_e1(c / m->t[1]);
+          }
+        if (near) {
+          /* step 0 kernel E1(c/t_1) is log singular at y = x: apex-split rule at x */
+          const double V[6] = {ax, ay, ax + e1x, ay + e1y, ax + e2x, ay + e2y};
+          /* uv[0..2] vertex values, uv[4] = value at the apex x (linear extension) */
+          const double det = e1x * e2y - e1y * e2x;
+          const double uu = ((xx - ax) * e2y - (xy - ay) * e2x) / det, vv = ((xy - ay) * e1x - (xx - ax) * e1y) / det;
+          const double uv[5] = {u0[i0], u0[i1], u0[i2], 0.0, (1.0 - uu - vv) * u0[i0] + uu * u0[i1] + vv * u0[i2]};
+          apex_rule_accumulate(xx, xy, V, uv, alpha, m->t[1], RX->w[p] * S->h, &first_p);
+        }
+        first += first_p;
+      }
+    }
+    out[i] = alpha / (4.0 * ORA_PI) * first;
+    for (int a = 1; a < nt; ++a)
+      out[(long long)a * ng + i] = alpha / (4.0 * ORA_PI) * (node_sum[a + 1] - node_sum[a]);
+    free(node_sum);
+  }
+}

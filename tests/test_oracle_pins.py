@@ -384,3 +384,44 @@ def test_potential_converges_to_manufactured_solution():
         errs.append(np.abs(om.potential(wh, g, pts) - ex).max() / np.abs(ex).max())
     assert errs[0] > 2.0 * errs[1] > 4.0 * errs[2] * 0.5, errs
     assert errs[2] < 2e-3, errs
+
+
+# ------------------------------------------------------ initial potential M_h^0 u0 (f1)
+def test_initial_potential_closed_form_constant_u0():
+    """u0 = 1: (M_0 1)(x,t) = int_(0,1)^2 U*(x-y,t) dy = prod_k (erf((1-x_k)/s) + erf(x_k/s)) / 2,
+    s = sqrt(4t/alpha) (U* factorises); its integral over gamma_i x [t_a, t_{a+1}] by scipy
+    against the oracle's M_h^0 1 (exact time integrals, Gauss / collapsed Gauss / apex-split rule)"""
+    from scipy import integrate
+    from scipy.special import erf
+    import workloads.table1 as T
+    w = T.table1(3)
+    om = O.OracleMesh(w)
+    nodes, tris = T.triangulation(w)
+    f = om.initial_rhs(nodes, tris, np.ones(len(nodes)), 8, 6, 16)
+    al = w.alpha
+
+    def m0one(x, t):
+        s = np.sqrt(4 * t / al)
+        return np.prod([0.5 * (erf((1 - xk) / s) + erf(xk / s)) for xk in x])
+    for a, i, tol in [(0, 1, 5e-6), (0, 6, 5e-6), (1, 5, 1e-11), (5, 9, 1e-11), (20, 12, 1e-11), (31, 15, 1e-11)]:
+        A, B, h = om.seg_a[i], om.seg_b[i], om.seg_h[i]
+        ref, _ = integrate.dblquad(lambda s, t: m0one(A + s * (B - A), t) * h, w.t_breaks[a],
+                                   w.t_breaks[a + 1], 0, 1, epsabs=1e-16, epsrel=1e-13)
+        assert abs(f[a * om.ng + i] - ref) <= tol * abs(ref), (a, i, f[a * om.ng + i], ref)
+
+
+def test_table1_density_converges():
+    """the paper's experiment: V_h w = (1/2 M_h + K_h) g - M_h^0 u0 solved by block
+    forward substitution; the L2(Sigma) error of w_h against d_n u falls under refinement"""
+    import workloads.table1 as T
+    errs = []
+    for L in (2, 3, 4):
+        w = T.table1(L)
+        om = O.OracleMesh(w)
+        nodes, tris = T.triangulation(w)
+        g = T.dirichlet_data(w)
+        b = om.rhs(om.dense("K"), g) - om.initial_rhs(nodes, tris, T.initial_nodes(w), 4, 4, 12)
+        wh = O.block_forward_solve(om.dense("V"), b, om.ng)
+        err, ref = om.l2_error(wh, exact=lambda x, n, t: T.exact_neumann(x, n, t))
+        errs.append(err / ref)
+    assert errs[0] > 1.5 * errs[1] > 2.25 * errs[2], errs
