@@ -218,6 +218,16 @@ bem_status bem_rhs_fused(const bem_mesh* mesh, const bem_quad_opts* opts, const 
  * already queued there, e.g. the right-hand side) and synchronises it once per iteration (the
  * Hessenberg column goes to the host for the Givens rotation).  Returns BEM_E_NOT_CONVERGED /
  * BEM_E_BREAKDOWN with w and the report filled. */
+/* Initial potential term of eq. (4): b <- b - M_h^0 u0 with
+ * M_h^0[(a,i), j] = <M_0 phi^1_j, phi^0_(a,i)>, u0 in S_h^1(Omega_h) given by its nodal values on a
+ * triangulation of Omega (nodes_xy: n_nodes x 2, tris: n_tri x 3 node indices, both HOST; u0_dev,
+ * b_dev: device).  Exact time integrals; qx Gauss points per boundary element, qt_far^2 /
+ * qt_near^2 collapsed Gauss points per triangle, the log-singular first step by an apex-split rule
+ * (reading R22); 0 selects the defaults 4 / 4 / 12 (<= 16 each).  M_h^0 is never
+ * stored (its product only).  One process.  Errors: BEM_E_INVALID, BEM_E_STATE, BEM_E_CUDA. */
+bem_status bem_rhs_initial(const bem_mesh* mesh, int n_nodes, const double* nodes_xy, int n_tri,
+                           const int* tris, const double* u0_dev, int qx, int qt_far, int qt_near,
+                           double* b_dev, bem_stream stream);
 /* Representation formula in the space-time cylinder (eq. 2), u0 = 0:
  * u(x,t) = (Vt w)(x,t) - (W g)(x,t) for the Neumann density w (piecewise constant, as solved by
  * bem_solve_gmres) and the Dirichlet data g (nodal, as in bem_rhs).  Time integrals exact, Gauss

@@ -311,6 +311,21 @@ bem_status bem_rhs_fused(const bem_mesh* m, const bem_quad_opts* o, const bem_ma
   return st;
 }
 
+bem_status bem_rhs_initial(const bem_mesh* m, int n_nodes, const double* nodes_xy, int n_tri,
+                           const int* tris, const double* u0, int qx, int qt_far, int qt_near,
+                           double* b, bem_stream s) {
+  if (!m || n_nodes < 3 || n_tri < 1 || !nodes_xy || !tris || !u0 || !b) { set_error("bem_rhs_initial: bad argument"); return BEM_E_INVALID; }
+  if (qx <= 0) qx = 4;
+  if (qt_far <= 0) qt_far = 4;
+  if (qt_near <= 0) qt_near = 12;
+  if (qx > QMAX || qt_far > QMAX || qt_near > QMAX) { set_error("bem_rhs_initial: orders must be <= 16"); return BEM_E_INVALID; }
+  for (int k = 0; k < 3 * n_tri; ++k)
+    if (tris[k] < 0 || tris[k] >= n_nodes) { set_error("bem_rhs_initial: triangle index out of range"); return BEM_E_INVALID; }
+  if (m->nranks > 1) { set_error("bem_rhs_initial: one process"); return BEM_E_STATE; }
+  cudaSetDevice(m->device);
+  return initial_rhs(m, n_nodes, nodes_xy, n_tri, tris, u0, qx, qt_far, qt_near, b, S(s));
+}
+
 bem_status bem_eval_potential(const bem_mesh* m, const double* w, const double* g, long long npts,
                               const double* pts, double* u, bem_stream s) {
   if (!m || !w || !g || (npts > 0 && (!pts || !u)) || npts < 0) { set_error("bem_eval_potential: bad argument"); return BEM_E_INVALID; }

@@ -131,6 +131,7 @@ __host__ __device__ inline bool collinear(const Seg& X, const Seg& Y) {
 
 #include "moments.cuh"
 #include "potential.cuh"
+#include "initial.cuh"
 
 namespace stb {
 
@@ -577,6 +578,34 @@ bem_status eval_potential(const bem_mesh* m, const double* w, const double* g, l
     return BEM_E_INVALID;
   }
   return BEM_OK;
+}
+
+// row f1: b <- b - M_h^0 u0 (eq. 4); nodes / tris on the host, u0 and b on the device
+bem_status initial_rhs(const bem_mesh* m, int nnode, const double* nodes, int ntri, const int* tris,
+                       const double* u0, int qx, int qtf, int qtn, double* b, cudaStream_t st) {
+  mesh_wait(m, st);
+  double* d_nodes = nullptr;
+  int* d_tris = nullptr;
+  double* d_part = nullptr;
+  const int nch = (ntri + 255) / 256;
+  const size_t part_bytes = sizeof(double) * (size_t)m->ng * nch * (m->nt + 2);
+  cudaError_t e;
+  if ((e = cudaMallocAsync((void**)&d_nodes, sizeof(double) * 2 * nnode, st)) != cudaSuccess ||
+      (e = cudaMallocAsync((void**)&d_tris, sizeof(int) * 3 * ntri, st)) != cudaSuccess ||
+      (e = storage_acquire(m->device, part_bytes, st, (void**)&d_part)) != cudaSuccess ||
+      (e = cudaMemcpyAsync(d_nodes, nodes, sizeof(double) * 2 * nnode, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
+      (e = cudaMemcpyAsync(d_tris, tris, sizeof(int) * 3 * ntri, cudaMemcpyHostToDevice, st)) != cudaSuccess)
+    return cuda_fail(e, "initial_rhs");
+  dim3 grid(m->ng, nch);
+  k_initial<<<grid, 256, 0, st>>>(m->d_seg, m->d_t, m->ng, m->nt, m->alpha, d_nodes, d_tris, ntri, u0, qx, qtf, qtn, d_part);
+  const long long n = (long long)m->ng * m->nt;
+  k_initial_finish<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(d_part, m->ng, m->nt, nch, m->alpha, b);
+  count_launch(2);
+  cudaFreeAsync(d_nodes, st);
+  cudaFreeAsync(d_tris, st);
+  storage_release(m->device, d_part, part_bytes, st);
+  e = cudaGetLastError();
+  return e == cudaSuccess ? BEM_OK : cuda_fail(e, "initial_rhs");
 }
 
 }  // namespace stb

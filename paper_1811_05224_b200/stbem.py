@@ -108,6 +108,7 @@ _SIGS = {
     "bem_rhs_fused": (I, [P, P, P, P, P, P, P]),
     "bem_assemble_toeplitz": (I, [P, I, P, P, PP]),
     "bem_eval_potential": (I, [P, P, P, LL, P, P, P]),
+    "bem_rhs_initial": (I, [P, I, P, I, P, P, I, I, I, P, P]),
     "bem_solve_gmres": (I, [P, P, P, P, P, ctypes.POINTER(GmresOpts), ctypes.POINTER(SolveReport), P, P]),
     "bem_matrix_get": (I, [P, LL, LL, LL, LL, P]),
     "bem_matrix_get_entries": (I, [P, LL, P, P, P]),
@@ -340,6 +341,15 @@ def rhs_fused(mesh, Mp, g, b, q_bulk=0, q_sing=0, legacy_sing=False, stats=False
     check(lib().bem_rhs_fused(mesh.h, ctypes.byref(o), Mp.h, _ptr(g), _ptr(b),
                               ctypes.byref(st) if stats else None, _stream(stream)))
     return st.as_dict() if stats else b
+
+
+def rhs_initial(mesh, nodes, tris, u0, b, qx=0, qt_far=0, qt_near=0, stream=None):
+    """b <- b - M_h^0 u0 (bem_rhs_initial); nodes (M, 2) and tris (T, 3) host arrays, u0, b device"""
+    nodes = np.ascontiguousarray(nodes, dtype=np.float64)
+    tris = np.ascontiguousarray(tris, dtype=np.int32)
+    check(lib().bem_rhs_initial(mesh.h, len(nodes), nodes.ctypes.data, len(tris), tris.ctypes.data, _ptr(u0),
+                                int(qx), int(qt_far), int(qt_near), _ptr(b), _stream(stream)))
+    return b
 
 
 def eval_potential(mesh, w, g, pts, out=None, stream=None):

@@ -388,3 +388,19 @@ def test_potential_rejects_boundary_points():
     m = S.Mesh.from_workload(w)
     with pytest.raises(S.BemError):
         S.eval_potential(m, cuda(np.zeros(w.n)), cuda(np.zeros(w.n)), np.array([[0.01, 0.5, 0.5]]))
+
+
+@pytest.mark.parametrize("L,orders", [(2, (4, 4, 12)), (3, (8, 6, 16)), (4, (4, 4, 12))])
+def test_initial_potential_parity(L, orders):
+    """row f1: b - M_h^0 u0 on the GPU against the oracle's M_h^0 u0 (paper's Table-1 workload)"""
+    import workloads.table1 as T
+    w = T.table1(L)
+    om = O.OracleMesh(w)
+    nodes, tris = T.triangulation(w)
+    u0 = T.initial_nodes(w)
+    ref = om.initial_rhs(nodes, tris, u0, *orders)
+    m = S.Mesh.from_workload(w)
+    b = torch.zeros(w.n, dtype=torch.float64, device="cuda")
+    S.rhs_initial(m, nodes, tris, cuda(u0), b, *orders)
+    got = -b.cpu().numpy()
+    assert relmax(got, ref) <= 1e-11, relmax(got, ref)
