@@ -303,61 +303,77 @@ bem_status gemv_launch(const bem_matrix* A, double a, const double* x, double b,
 // f3) — a genuine contraction (many right-hand sides through the Toeplitz shift).  CTA tile
 // 64 rows i x 64 columns a, K split into chunks (fixed partial slots, reduced in fixed order);
 // register tile 4 x 4 per thread, DFMA (FP64 tensor cores are not faster on B200).
-constexpr int TZ_TI = 64, TZ_TA = 64, TZ_TK = 32, TZ_KSPLIT = 4096;
+constexpr int TZ_TI = 128, TZ_TA = 128, TZ_TK = 16;
+// CTA tile 128 rows i x 128 columns a, 256 threads as 16 x 16, 8 x 8 accumulators per thread
+// (rows ty*8 + u: broadcast reads of the T tile; columns 32 k + 2 tx + e: conflict-free 16-byte
+// reads of the X tile), K steps of 16 with the next step's tiles prefetched into registers while
+// the current one is multiplied from shared memory.
 __global__ void __launch_bounds__(256) k_toeplitz_mm(const double* __restrict__ T, long long ldT_d,
                                                     int ldT, const double* __restrict__ x, int ng, int nt,
-                                                    double* __restrict__ part) {
-  __shared__ double Tt[TZ_TK][TZ_TI + 2];   // transposed T tile: Tt[jj][ii]
-  __shared__ double Xs[TZ_TK][TZ_TA + 2];
+                                                    int dpz, double* __restrict__ part) {
+  __shared__ __align__(16) double Tt[TZ_TK][TZ_TI + 2];   // Tt[jj][ii] = T_d[i0 + ii][j0 + jj]
+  __shared__ __align__(16) double Xs[TZ_TK][TZ_TA + 2];   // Xs[jj][aa] = X[j0 + jj][a0 + aa - d]
   const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
   const int i0 = blockIdx.x * TZ_TI, a0 = blockIdx.y * TZ_TA;
-  // K chunk z: the time lags d in [z dpz, (z + 1) dpz), all trial elements j of each
-  const int dpz = max(1, TZ_KSPLIT / ng);
-  const int d0 = blockIdx.z * dpz, d1 = min(nt, d0 + dpz);
-  double acc[4][4];
+  const int d0 = blockIdx.z * dpz, d1 = min(min(nt, d0 + dpz), a0 + TZ_TA);   // d > a: nothing
+  const int nj = (ng + TZ_TK - 1) / TZ_TK;
+  const int nsteps = max(0, d1 - d0) * nj;
+  double acc[8][8];
 #pragma unroll
-  for (int u = 0; u < 4; ++u)
+  for (int u = 0; u < 8; ++u)
 #pragma unroll
-    for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
-  for (int d = d0; d < d1 && d <= a0 + TZ_TA - 1; ++d) {   // d > a for every column a: nothing left
-    for (int j0 = 0; j0 < ng; j0 += TZ_TK) {
-      __syncthreads();
-      // T_d[i0 + ii][j0 + jj] -> Tt[jj][ii]   (2048 doubles, 8 per thread, coalesced along jj)
+    for (int v = 0; v < 8; ++v) acc[u][v] = 0.0;
+  double rt[8], rx[8];
+  auto fetch = [&](int step) {
+    const int d = d0 + step / nj, j0 = (step % nj) * TZ_TK;
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int e = tid + q * 256, ii = e / TZ_TK, jj = e % TZ_TK;
-        const int i = i0 + ii, j = j0 + jj;
-        Tt[jj][ii] = (i < ng && j < ng) ? T[(long long)d * ldT_d + (long long)i * ldT + j] : 0.0;
+    for (int q = 0; q < 8; ++q) {
+      const int e = tid + q * 256, ii = e / TZ_TK, jj = e % TZ_TK;
+      const int i = i0 + ii, j = j0 + jj;
+      rt[q] = (i < ng && j < ng) ? T[(long long)d * ldT_d + (long long)i * ldT + j] : 0.0;
+      const int aa = ii, b = a0 + aa - d;
+      rx[q] = (j < ng && b >= 0 && b < nt) ? x[(long long)b * ng + j] : 0.0;
+    }
+  };
+  if (nsteps > 0) fetch(0);
+  for (int step = 0; step < nsteps; ++step) {
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int e = tid + q * 256, ii = e / TZ_TK, jj = e % TZ_TK;
+      Tt[jj][ii] = rt[q];
+      Xs[jj][ii] = rx[q];
+    }
+    __syncthreads();
+    if (step + 1 < nsteps) fetch(step + 1);
+#pragma unroll 4
+    for (int jj = 0; jj < TZ_TK; ++jj) {
+      double tv[8], xv[8];
+#pragma unroll
+      for (int u = 0; u < 8; u += 2) {
+        const double2 t2 = *reinterpret_cast<const double2*>(&Tt[jj][ty * 8 + u]);
+        tv[u] = t2.x;
+        tv[u + 1] = t2.y;
       }
-      // X[j0 + jj][a0 + aa - d] -> Xs[jj][aa]
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int e = tid + q * 256, jj = e / TZ_TA, aa = e % TZ_TA;
-        const int j = j0 + jj, b = a0 + aa - d;
-        Xs[jj][aa] = (j < ng && b >= 0 && b < nt) ? x[(long long)b * ng + j] : 0.0;
+      for (int k = 0; k < 4; ++k) {
+        const double2 x2 = *reinterpret_cast<const double2*>(&Xs[jj][32 * k + 2 * tx]);
+        xv[2 * k] = x2.x;
+        xv[2 * k + 1] = x2.y;
       }
-      __syncthreads();
-#pragma unroll 8
-      for (int jj = 0; jj < TZ_TK; ++jj) {
-        double tv[4], xv[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) tv[u] = Tt[jj][ty * 4 + u];
+      for (int u = 0; u < 8; ++u)
 #pragma unroll
-        for (int v = 0; v < 4; ++v) xv[v] = Xs[jj][tx * 4 + v];
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-#pragma unroll
-          for (int v = 0; v < 4; ++v) acc[u][v] = fma(tv[u], xv[v], acc[u][v]);
-      }
+        for (int v = 0; v < 8; ++v) acc[u][v] = fma(tv[u], xv[v], acc[u][v]);
     }
   }
-  // partial Y tile of this K chunk: part[z][a][i]
+  // partial Y tile of this lag range: part[z][a][i]
   const long long n = (long long)nt * ng;
 #pragma unroll
-  for (int u = 0; u < 4; ++u)
+  for (int u = 0; u < 8; ++u)
 #pragma unroll
-    for (int v = 0; v < 4; ++v) {
-      const int i = i0 + ty * 4 + u, a = a0 + tx * 4 + v;
+    for (int v = 0; v < 8; ++v) {
+      const int i = i0 + ty * 8 + u, a = a0 + 32 * (v / 2) + 2 * tx + (v % 2);
       if (i < ng && a < nt) part[(long long)blockIdx.z * n + (long long)a * ng + i] = acc[u][v];
     }
 }
@@ -375,16 +391,19 @@ bem_status toeplitz_gemv(const bem_matrix* A, double a, const double* x, double 
   const bem_mesh* m = A->mesh;
   const int ng = m->ng, nt = m->nt;
   const long long n = (long long)ng * nt;
-  const int dpz = std::max(1, TZ_KSPLIT / ng);
+  // lag ranges per CTA: enough CTAs for two waves of the 148 SMs over the output tiles
+  const int tiles = ((ng + TZ_TI - 1) / TZ_TI) * ((nt + TZ_TA - 1) / TZ_TA);
+  const int want = std::max(1, (2 * num_sms() + tiles - 1) / tiles);
+  const int dpz = std::max(1, (nt + want - 1) / want);
   const int nsplit = (nt + dpz - 1) / dpz;
   double* part = nullptr;
   const size_t bytes = sizeof(double) * n * nsplit;
   cudaError_t e = storage_acquire(m->device, bytes, st, (void**)&part);
   if (e != cudaSuccess) return cuda_fail(e, "toeplitz product");
-  e = cudaMemsetAsync(part, 0, bytes, st);   // chunks that break early leave their slots zero
+  e = cudaMemsetAsync(part, 0, bytes, st);   // lag ranges beyond a tile's columns leave their slots zero
   dim3 grid((ng + TZ_TI - 1) / TZ_TI, (nt + TZ_TA - 1) / TZ_TA, nsplit);
   k_toeplitz_mm<<<grid, 256, 0, st>>>(A->data, A->poff.size() > 1 ? A->poff[1] - A->poff[0] : 0,
-                                      (int)pad4(ng), x, ng, nt, part);
+                                      (int)pad4(ng), x, ng, nt, dpz, part);
   k_toeplitz_reduce<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(part, nsplit, n, a, b, y);
   count_launch(2);
   storage_release(m->device, part, bytes, st);
