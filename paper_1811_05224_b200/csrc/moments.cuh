@@ -716,23 +716,43 @@ __global__ void __launch_bounds__(128, KIND == STB_D ? 2 : 3) k_bulk_m(BlockArgs
     }
     if (y > B.b0) {
       const int b = y - 1;
+      // interior column: every band row is a full bulk cell (no per-row conditions)
+      const bool interior = b <= r_lo - 2 && r_hi - r_lo == R;
       if (PROD) {
         const double gv = valid ? B.g[(long long)b * ng + J] : 0.0;
+        if (interior) {
 #pragma unroll
-        for (int r = 1; r <= R; ++r) {
-          const int a = r_lo + r - 1;
-          const double G = phi[r] - phi[r - 1];
-          if (a < r_hi && a - b >= 2) accp[r - 1] = fma(Gp[r - 1] - G, gv, accp[r - 1]);
-          Gp[r - 1] = G;
+          for (int r = 1; r <= R; ++r) {
+            const double G = phi[r] - phi[r - 1];
+            accp[r - 1] = fma(Gp[r - 1] - G, gv, accp[r - 1]);
+            Gp[r - 1] = G;
+          }
+        } else {
+#pragma unroll
+          for (int r = 1; r <= R; ++r) {
+            const int a = r_lo + r - 1;
+            const double G = phi[r] - phi[r - 1];
+            if (a < r_hi && a - b >= 2) accp[r - 1] = fma(Gp[r - 1] - G, gv, accp[r - 1]);
+            Gp[r - 1] = G;
+          }
         }
       } else {
         double* col = B.out + ((long long)(b - B.b0) * cstride + jcol);
+        if (interior && valid) {
 #pragma unroll
-        for (int r = 1; r <= R; ++r) {
-          const int a = r_lo + r - 1;
-          const double G = phi[r] - phi[r - 1];
-          if (valid && a < r_hi && a - b >= 2) col[srow[r - 1]] = Gp[r - 1] - G;
-          Gp[r - 1] = G;
+          for (int r = 1; r <= R; ++r) {
+            const double G = phi[r] - phi[r - 1];
+            col[srow[r - 1]] = Gp[r - 1] - G;
+            Gp[r - 1] = G;
+          }
+        } else {
+#pragma unroll
+          for (int r = 1; r <= R; ++r) {
+            const int a = r_lo + r - 1;
+            const double G = phi[r] - phi[r - 1];
+            if (valid && a < r_hi && a - b >= 2) col[srow[r - 1]] = Gp[r - 1] - G;
+            Gp[r - 1] = G;
+          }
         }
       }
     } else {
