@@ -404,3 +404,48 @@ def test_initial_potential_parity(L, orders):
     S.rhs_initial(m, nodes, tris, cuda(u0), b, *orders)
     got = -b.cpu().numpy()
     assert relmax(got, ref) <= 1e-11, relmax(got, ref)
+
+
+def test_large_kappa_falls_back_to_legacy_touching_path():
+    """kappa = alpha h^2 / (4 min h_t) beyond the records' regime A: the touching pairs go through
+    the per-lag singular kernel (fused_sing = 0) and bem_rhs_fused falls back to assemble + GEMV"""
+    from workloads.configs import square
+    w = square(2, 64, name="K64", tol=1e-10)      # h = 0.5, h_t = 1/64: kappa = 1
+    m = S.Mesh.from_workload(w)
+    assert m.info.kappa >= 1.0
+    om = O.OracleMesh(w)
+    rows = np.arange(0, w.n, 7)
+    for kind in "VKD":
+        A = getattr(m, f"assemble_{kind}")()
+        assert A.stats()["fused_sing"] == 0
+        cols = (rows // w.n_gamma) * w.n_gamma + (rows * 3) % w.n_gamma    # same test step, varied j
+        ref = om.entries(kind, rows, cols)
+        got = A.entries(rows, cols)
+        assert float(np.abs(got - ref).max() / np.abs(ref).max()) <= MAT_TOL
+    g = cuda(W.dirichlet_data(w))
+    Mp = m.assemble_M(S.MASS_PRIMAL)
+    b1, b2 = torch.empty_like(g), torch.empty_like(g)
+    S.rhs(m.assemble_K(), Mp, g, b1)
+    st = S.rhs_fused(m, Mp, g, b2, stats=True)
+    assert st["fused_sing"] == 0
+    assert relmax(b2.cpu().numpy(), b1.cpu().numpy()) <= 1e-14
+
+
+def test_c4_sampled_entries_block_toeplitz():
+    """BJ configs[3] (C4, N = 262 144, the largest): its dense matrices need 8 GPUs, the uniform
+    steps let the block-Toeplitz variant hold every entry on one GPU; sampled entries (diagonal,
+    near and random cells) against the oracle"""
+    w = W.get("C4")
+    m = S.Mesh.from_workload(w)
+    rng = np.random.default_rng(1811)
+    rows, cols = sample_entries(w, rng, n_random=300, rows_per=2)
+    om = O.OracleMesh(w)
+    for kind in "VKD":
+        T = m.assemble_toeplitz(kind)
+        r_, c_ = (rows[::4], cols[::4]) if kind == "D" else (rows[::2], cols[::2])
+        ref = om.entries(kind, r_, c_)
+        got = T.entries(r_, c_)
+        err = float(np.abs(got - ref).max() / np.abs(ref).max())
+        print(f"C4 {kind} sampled rel max-norm error {err:.3e} over {len(r_)} entries")
+        assert err <= MAT_TOL
+        T.close()
