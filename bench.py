@@ -32,7 +32,7 @@ FP64_PEAK_DERIVED = 148 * 64 * 2 * 1.965e9 / 1e12
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=10)   # ~0.75 s timed: several nvidia-smi samples
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--config", default="C3")
