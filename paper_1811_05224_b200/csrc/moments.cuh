@@ -306,37 +306,49 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 // ------------------------------------------------------------- node evaluation
-// regime A from registers
+// regime A from registers.  The s factor of the H family is folded into the Horner chain:
+//   s sum_k P_k u^k = s P_0 + sum_{k>=0} P_{k+1} u^k   (u = 1/s),
+// so V_h runs one chain of 17 steps and D_h merges its two families into ONE chain over
+//   Pc_k = P^H_{k+1} + P^F_k,   Phi~ = s P^H_0 + sum_k Pc_k u^k + ln s (s M0^H + M1^H + M0^F)
+// (the same terms re-associated).
 template <int KIND>
 struct RegA {
-  double P[Fams<KIND>::n][MKA + 1];
-  double M0[Fams<KIND>::n], M1[Fams<KIND>::n];
+  static constexpr int NC = KIND == STB_K ? MKA + 1 : (KIND == STB_V ? MKA : MKA + 1);
+  double P[NC];      // the chain's coefficients (highest degree last)
+  double e0;         // V, D: s P^H_0 term; K: unused
+  double l0, l1;     // V, D: ln s (s l0 + l1);  K: -ln s l0
   double cmax;
   __device__ __forceinline__ void load(const double* __restrict__ rec, long long S) {
     cmax = rec[RF_CMAX * S];
+    const double* R0 = rec + (RF_COMMON + 0 * FAMSZ) * S;
+    if (KIND == STB_K) {
 #pragma unroll
-    for (int f = 0; f < Fams<KIND>::n; ++f) {
-      const double* R = rec + (RF_COMMON + f * FAMSZ) * S;
+      for (int k = 0; k <= MKA; ++k) P[k] = R0[(FA + k) * S];
+      e0 = 0.0;
+      l0 = R0[FM0 * S];
+      l1 = 0.0;
+    } else if (KIND == STB_V) {
 #pragma unroll
-      for (int k = 0; k <= MKA; ++k) P[f][k] = R[(FA + k) * S];
-      M0[f] = R[FM0 * S];
-      M1[f] = R[FM1 * S];
+      for (int k = 0; k < MKA; ++k) P[k] = R0[(FA + k + 1) * S];
+      e0 = R0[FA * S];
+      l0 = R0[FM0 * S];
+      l1 = R0[FM1 * S];
+    } else {
+      const double* R1 = rec + (RF_COMMON + 1 * FAMSZ) * S;
+#pragma unroll
+      for (int k = 0; k <= MKA; ++k) P[k] = (k < MKA ? R0[(FA + k + 1) * S] : 0.0) + R1[(FA + k) * S];
+      e0 = R0[FA * S];
+      l0 = R0[FM0 * S];
+      l1 = R0[FM1 * S] + R1[FM0 * S];
     }
   }
   // Phi~ at the node (s, ln s, u = 1/s)
   __device__ __forceinline__ double eval(double s, double lns, double u) const {
-    double out = 0.0;
+    double acc = P[NC - 1];
 #pragma unroll
-    for (int f = 0; f < Fams<KIND>::n; ++f) {
-      const int fam = f == 0 ? Fams<KIND>::f0 : Fams<KIND>::f1;
-      double acc = P[f][MKA];
-#pragma unroll
-      for (int k = MKA - 1; k >= 0; --k) acc = fma(acc, u, P[f][k]);
-      if (fam == FAM_H) out += fma(s, fma(lns, M0[f], acc), lns * M1[f]);
-      else if (fam == FAM_F) out += fma(lns, M0[f], acc);
-      else out += fma(-lns, M0[f], acc);
-    }
-    return out;
+    for (int k = NC - 2; k >= 0; --k) acc = fma(acc, u, P[k]);
+    if (KIND == STB_K) return fma(-lns, l0, acc);
+    return fma(s, fma(lns, l0, e0), fma(lns, l1, acc));
   }
 };
 
