@@ -241,27 +241,44 @@ __global__ void __launch_bounds__(128) k_records(MomArgs M) {
   rec[RF_C0 * S] = c0;
   rec[RF_KB * S] = (double)kb;
   rec[RF_IC0 * S] = okB ? 1.0 / c0 : 0.0;
-#pragma unroll 1
-  for (int slot = 0; slot < Fams<KIND>::n; ++slot) {
-    const int fam = slot == 0 ? Fams<KIND>::f0 : Fams<KIND>::f1;
-    double* R = rec + (RF_COMMON + slot * FAMSZ) * S;
-    // regime A: M_k = sum W c^k
-    double mk[MKA + 1];
+  // regime-A moments M_k = sum W c^k and the affine constants of both families in one pass
+  constexpr int NF = Fams<KIND>::n;
+  double mk[NF][MKA + 1], C0[NF], C1[NF];
 #pragma unroll
-    for (int k = 0; k <= MKA; ++k) mk[k] = 0.0;
-    for_points<KIND, NEAR>(M, I, J, [&](double c, double wa, double wb) {
-      const double w = slot == 0 ? wa : wb;
+  for (int f = 0; f < NF; ++f) {
+    C0[f] = C1[f] = 0.0;
+#pragma unroll
+    for (int k = 0; k <= MKA; ++k) mk[f][k] = 0.0;
+  }
+  const bool lg = cmin > 0.0;   // the affine constants need c > 0 at every point
+  for_points<KIND, NEAR>(M, I, J, [&](double c, double wa, double wb) {
+    const double g = lg ? STB_GAMMA + log(c) : 0.0;
+#pragma unroll
+    for (int f = 0; f < NF; ++f) {
+      const int fam = f == 0 ? Fams<KIND>::f0 : Fams<KIND>::f1;
+      const double w = f == 0 ? wa : wb;
       double pw = w;
 #pragma unroll
       for (int k = 0; k <= MKA; ++k) {
-        mk[k] += pw;
+        mk[f][k] += pw;
         pw *= c;
       }
-    });
+      if (lg) {
+        C0[f] = fma(w, g, C0[f]);
+        C1[f] += fam == FAM_Q ? w / c : w * c * g;
+      }
+    }
+  });
+#pragma unroll 1
+  for (int slot = 0; slot < NF; ++slot) {
+    const int fam = slot == 0 ? Fams<KIND>::f0 : Fams<KIND>::f1;
+    double* R = rec + (RF_COMMON + slot * FAMSZ) * S;
 #pragma unroll
-    for (int k = 0; k <= MKA; ++k) R[(FA + k) * S] = mpoly(fam, k) * mk[k];
-    R[FM0 * S] = mk[0];
-    R[FM1 * S] = mk[1];
+    for (int k = 0; k <= MKA; ++k) R[(FA + k) * S] = mpoly(fam, k) * mk[slot][k];
+    R[FM0 * S] = mk[slot][0];
+    R[FM1 * S] = mk[slot][1];
+    R[FC0 * S] = C0[slot];
+    R[FC1 * S] = C1[slot];
     // regime B: m_k = sum W (c - c0)^k
     double mb[MKB + 1];
 #pragma unroll
@@ -284,18 +301,6 @@ __global__ void __launch_bounds__(128) k_records(MomArgs M) {
       R[(FB1 + k) * S] = k == 0 ? mb[0] : mb[k] * STB_INV_H[k];
       R[(FB2 + k) * S] = fam == FAM_Q ? mb[k] : (fam == FAM_H ? (k == 0 ? 0.0 : (k == 1 ? mb[1] : mb[k] * STB_INV_H[k - 1] * STB_INV_H[k])) : 0.0);
     }
-    // affine constants (all points at c > 0)
-    double C0 = 0.0, C1 = 0.0;
-    if (cmin > 0.0) {
-      for_points<KIND, NEAR>(M, I, J, [&](double c, double wa, double wb) {
-        const double w = slot == 0 ? wa : wb;
-        const double g = STB_GAMMA + log(c);
-        C0 = fma(w, g, C0);
-        C1 += fam == FAM_Q ? w / c : w * c * g;
-      });
-    }
-    R[FC0 * S] = C0;
-    R[FC1 * S] = C1;
   }
 }
 
