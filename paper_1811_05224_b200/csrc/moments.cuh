@@ -650,6 +650,27 @@ __global__ void __launch_bounds__(128, KIND == STB_D ? 2 : 3) k_bulk_m(BlockArgs
   const int jcol = B.sym ? J % SYM_TS : J;
   RegA<KIND> A;
   A.load(M.rec + pair, S);
+  // pairs without quadrature points (K_h on collinear elements: the kernel vanishes) hold
+  // only zero entries: a warp of them writes zeros (or, in product mode, nothing) and skips the
+  // node evaluations, counted as regime A
+  if (__all_sync(0xffffffffu, A.cmax == 0.0 && A.P[0] == 0.0 && A.l0 == 0.0)) {
+    unsigned long long nz = 0;
+    for (int y = B.b0; y <= bmax + 1; ++y) {
+#pragma unroll
+      for (int r = 0; r <= R; ++r) nz += (r_lo + r <= r_hi && r_lo + r > y);
+      if (!PROD && y > B.b0) {
+        const int b = y - 1;
+        double* col = B.out + ((long long)(b - B.b0) * cstride + jcol);
+#pragma unroll
+        for (int r = 1; r <= R; ++r) {
+          const int a = r_lo + r - 1;
+          if (valid && a < r_hi && a - b >= 2) col[srow[r - 1]] = 0.0;
+        }
+      }
+    }
+    count_regimes(M.counters, valid ? nz : 0, 0, 0, 0, 0);
+    return;
+  }
   RegBZ<KIND> Z;
   Z.load(M.rec + pair, S);
   unsigned long long nA = 0, nB = 0, nZ = 0, nC = 0, nK = 0;
