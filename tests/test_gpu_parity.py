@@ -449,3 +449,26 @@ def test_c4_sampled_entries_block_toeplitz():
         print(f"C4 {kind} sampled rel max-norm error {err:.3e} over {len(r_)} entries")
         assert err <= MAT_TOL
         T.close()
+
+
+def test_ragged_tiles_and_many_slices():
+    """N_Gamma = 40 (a full 32-wide tile and a ragged one of 8) with the maximum number of temporal
+    slices (P = N_I): symmetric packed storage, products and the fused RHS against the oracle"""
+    from workloads.configs import square
+    w = square(10, 12, name="R40", tol=1e-10)
+    om = O.OracleMesh(w)
+    x = W.random_vector(w.n)
+    g = W.dirichlet_data(w)
+    for P in (1, 12):
+        m = S.Mesh.from_workload(w, n_slices=P)
+        for kind in "VKD":
+            A = getattr(m, f"assemble_{kind}")()
+            ref = om.dense(kind)
+            dA = A.dense()
+            assert relmax(dA, ref) <= MAT_TOL, (P, kind, relmax(dA, ref))
+            y = torch.empty(w.n, dtype=torch.float64, device="cuda")
+            A.matvec(cuda(x), y)
+            assert relmax(y.cpu().numpy(), dA @ x) <= 1e-13
+        b = torch.empty(w.n, dtype=torch.float64, device="cuda")
+        S.rhs_fused(m, m.assemble_M(S.MASS_PRIMAL), cuda(g), b)
+        assert relmax(b.cpu().numpy(), om.rhs(om.dense("K"), g)) <= 1e-11
