@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(128) k_records(MomArgs M) {
   const bool okB = cmin > 0.0 && (cmax - c0m) <= MRHO * c0m;
   const double c0 = okB ? c0m : 0.0;
   const double rho = okB ? (cmax - c0m) / c0m : 1.0;
-  const int kb = rho <= 1e-6 ? 3 : min(MKB, max(3, (int)ceil(log(1e-17) / log(rho))));
+  const int kb = rho <= 1e-6 ? 3 : min(MKB, max(3, (int)ceil(log(1e-16) / log(rho))));
   rec[RF_CMAX * S] = cmax;
   rec[RF_CMIN * S] = cmin;
   rec[RF_C0 * S] = c0;
@@ -411,6 +411,11 @@ struct RegBZ {
   }
 };
 
+// the GB3 coefficients as a (non-const) constant-bank array: read as c[bank][offset] operands of
+// the Horner DFMAs instead of being materialised as immediates on every regime-B evaluation
+static __device__ __constant__ double STB_GB3_CB[STB_GB3_DEG + 1] = STB_GB3_INIT;
+__device__ __forceinline__ double gb3_cb(double t) { return horner<STB_GB3_DEG>(STB_GB3_CB, fma(t, 6.0, -1.0)); }
+
 template <int KIND>
 __device__ __forceinline__ double phi_bz(const double* __restrict__ rec, long long S, const RegBZ<KIND>& z,
                                          double s, double u, int* regime) {
@@ -423,7 +428,7 @@ __device__ __forceinline__ double phi_bz(const double* __restrict__ rec, long lo
   if (!zz) {
     // x0 = c0 u >= 4 / (1 + MRHO) > 3: E1(x0) = e^{-x0} t GB3(t), t = 1/x0 = s / c0
     const double x0 = z.c0 * u, ic0 = z.ic0, ex = exp(-x0);
-    const double E1 = ex * (ic0 * s) * gb3_poly(ic0 * s);
+    const double E1 = ex * (ic0 * s) * gb3_cb(ic0 * s);
     const double* R0 = rec + (RF_COMMON + 0 * FAMSZ) * S;
     const double* R1 = rec + (RF_COMMON + 1 * FAMSZ) * S;
     double e = ex, ap = ex * ic0, app = 0.0;        // e^_{k-1}, a^_{k-1}, a^_{k-2}
@@ -479,7 +484,7 @@ __device__ __forceinline__ void phi_bz2(const double* __restrict__ rec, long lon
   const double ic0 = z.ic0;
   const double x01 = z.c0 * u1, x02 = z.c0 * u2;
   const double ex1 = exp(-x01), ex2 = exp(-x02);
-  const double E11 = ex1 * (ic0 * s1) * gb3_poly(ic0 * s1), E12 = ex2 * (ic0 * s2) * gb3_poly(ic0 * s2);
+  const double E11 = ex1 * (ic0 * s1) * gb3_cb(ic0 * s1), E12 = ex2 * (ic0 * s2) * gb3_cb(ic0 * s2);
   const double* R0 = rec + (RF_COMMON + 0 * FAMSZ) * S;
   const double* R1 = rec + (RF_COMMON + 1 * FAMSZ) * S;
   double e1 = ex1, ap1 = ex1 * ic0, app1 = 0.0, e2 = ex2, ap2 = ex2 * ic0, app2 = 0.0;
