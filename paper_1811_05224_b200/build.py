@@ -11,7 +11,8 @@ CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libstbem.so")
 SOURCES = ["mesh.cpp", "api.cpp", "comm.cpp", "assemble.cu", "linalg.cu"]
-HEADERS = ["internal.h", "special.cuh", "special_coeffs.h", "moments.cuh", "moment_coeffs.h"]
+HEADERS = ["internal.h", "special.cuh", "special_coeffs.h", "moments.cuh", "moment_coeffs.h", "potential.cuh",
+           "initial.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",

@@ -587,8 +587,12 @@ bem_status initial_rhs(const bem_mesh* m, int nnode, const double* nodes, int nt
   double* d_nodes = nullptr;
   int* d_tris = nullptr;
   double* d_part = nullptr;
-  const int nch = (ntri + 255) / 256;
-  const size_t part_bytes = sizeof(double) * (size_t)m->ng * nch * (m->nt + 2);
+  // chunks per element: enough CTAs for 8 per SM, each looping over its interleaved triangle batches
+  const int nbt_all = (ntri + 255) / 256;
+  const int nch = std::max(1, std::min(nbt_all, (8 * 148 + m->ng - 1) / m->ng));
+  const int nbatch = (nbt_all + nch - 1) / nch;
+  static const int use_moments = getenv("BEM_INITIAL_DIRECT") ? 0 : 1;
+  const size_t part_bytes = sizeof(double) * (size_t)m->ng * nch * 8 * (m->nt + 2);   // one row per warp
   cudaError_t e;
   if ((e = cudaMallocAsync((void**)&d_nodes, sizeof(double) * 2 * nnode, st)) != cudaSuccess ||
       (e = cudaMallocAsync((void**)&d_tris, sizeof(int) * 3 * ntri, st)) != cudaSuccess ||
@@ -597,7 +601,12 @@ bem_status initial_rhs(const bem_mesh* m, int nnode, const double* nodes, int nt
       (e = cudaMemcpyAsync(d_tris, tris, sizeof(int) * 3 * ntri, cudaMemcpyHostToDevice, st)) != cudaSuccess)
     return cuda_fail(e, "initial_rhs");
   dim3 grid(m->ng, nch);
-  k_initial<<<grid, 256, 0, st>>>(m->d_seg, m->d_t, m->ng, m->nt, m->alpha, d_nodes, d_tris, ntri, u0, qx, qtf, qtn, d_part);
+  // the warps' node accumulators in shared memory when 8 (nt + 2) doubles fit, else in their rows
+  const size_t wacc_bytes = sizeof(double) * 8 * (size_t)(m->nt + 2);
+  const int use_wacc = wacc_bytes <= 160 * 1024;
+  if (use_wacc) cudaFuncSetAttribute(k_initial, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wacc_bytes);
+  k_initial<<<grid, 256, use_wacc ? wacc_bytes : 0, st>>>(m->d_seg, m->d_t, m->ng, m->nt, m->alpha, d_nodes, d_tris, ntri,
+                                                          u0, qx, qtf, qtn, use_moments, nbatch, use_wacc, d_part);
   const long long n = (long long)m->ng * m->nt;
   k_initial_finish<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(d_part, m->ng, m->nt, nch, m->alpha, b);
   count_launch(2);

@@ -9,22 +9,11 @@
 // (a = 0: E1(c/t_1) alone is log singular at y = x) uses on the near triangles the apex-split rule
 // at each x point: the three sub-triangles (x, V_k, V_k+1) with signed areas, radial coordinate on a
 // geometric composite Gauss rule (ratio 0.15, 10 levels x 8 points), angular 12-point Gauss
-// (reading R22).  CTA = (element i, chunk of 256 triangles), thread = triangle, one block
-// sum per time node into fixed partial slots, k_initial_finish sums the chunks in fixed order.
+// (reading R22).  Node values from the moments of each warp's 32-triangle point cluster
+// (initial_warp); per-warp partial rows, k_initial_finish sums them in fixed order.
 #pragma once
 
 namespace stb {
-
-__device__ __forceinline__ double block_sum256(double v, double* red) {
-  v = warp_sum(v);
-  __syncthreads();
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-  __syncthreads();
-  double s = 0.0;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) s += red[k];
-  return s;
-}
 
 __device__ double apex_split(double px, double py, const double (&V)[6], const double (&uv)[3],
                              double u_apex, double alpha, double t1) {
@@ -56,18 +45,63 @@ __device__ double apex_split(double px, double py, const double (&V)[6], const d
   return acc;
 }
 
-__global__ void __launch_bounds__(256) k_initial(const Seg* __restrict__ seg, const double* __restrict__ tg,
-                                                int ng, int nt, double alpha,
-                                                const double* __restrict__ nodes, const int* __restrict__ tris,
-                                                int ntri, const double* __restrict__ u0, int qx, int qtf, int qtn,
-                                                double* __restrict__ part) {
-  __shared__ double red[8];
-  const int i = blockIdx.x, k = blockIdx.y * 256 + threadIdx.x;
+// the quadrature points of (gamma_i x triangle): x Gauss on gamma_i, the collapsed Duffy rule on the
+// triangle; vis(c, W) with c = alpha |x - y|^2 / 4 and the full weight W (h area2 xi w w u0_h(y))
+template <class F>
+__device__ __forceinline__ void for_tri_points(const Seg& S, const double (&V)[6], const double (&uv)[3],
+                                               int qx, int qt, double alpha, F&& vis) {
+  const double e1x = V[2] - V[0], e1y = V[3] - V[1], e2x = V[4] - V[0], e2y = V[5] - V[1];
+  const double area2 = fabs(e1x * e2y - e1y * e2x);
+  for (int p = 0; p < qx; ++p) {
+    const double xx = fma(c_gx[qx][p], S.bx - S.ax, S.ax), xy = fma(c_gx[qx][p], S.by - S.ay, S.ay);
+    const double wp = c_gw[qx][p] * S.h * area2;
+    for (int a1 = 0; a1 < qt; ++a1) {
+      const double xi = c_gx[qt][a1];
+      for (int a2 = 0; a2 < qt; ++a2) {
+        const double eta = c_gx[qt][a2];
+        const double u = xi * (1.0 - eta), v = xi * eta;
+        const double yx = V[0] + u * e1x + v * e2x, yy = V[1] + u * e1y + v * e2y;
+        const double uh = (1.0 - u - v) * uv[0] + u * uv[1] + v * uv[2];
+        const double dx = xx - yx, dy = xy - yy;
+        vis(0.25 * alpha * (dx * dx + dy * dy), wp * xi * c_gw[qt][a1] * c_gw[qt][a2] * uh);
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ double warp_min(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// One warp = 32 triangles of a batch against element i.  The node values
+//   N(t_n) = sum_{p in the warp's points} W_p E1(c_p / t_n)
+// are evaluated on the moments of the WARP's joint point cluster (row f1):
+//   regime A (c_max u < 4):  sum_k MEIN_k u^k M_k - gamma M_0 - L_0 - ln(u) M_0,
+//                            M_k = sum W c^k, L_0 = sum W ln c           (E1 = Ein - gamma - ln x)
+//   regime B (rho <= 1/2):   E1(x0) m_0 - sum_k a_{k-1} m_k / k, m_k = sum W (c - c0)^k (as phi_bz)
+// -- algebraic identities of the point sum of each triangle's own rule (qt_far^2 or qt_near^2
+// points), so the moments are summed over the 32 lanes once and each lane then evaluates its own
+// nodes n = 1 + lane, 1 + lane + 32, ...  Nodes in neither regime (a prefix n < n_A of small t,
+// only when the cluster is wide) take the per-lane point sum.  Step 0 (the log-singular E1(c/t_1)
+// alone): the apex-split rule on near triangles, the regular rule on far ones.
+// acc: this warp's row of nt + 2 node accumulators (shared or global), owned by the warp;
+// sm: the warp's moment slots in shared memory (MKA + MKB + 2 doubles).
+__device__ __forceinline__ void initial_warp(const Seg& S, const double* __restrict__ tg, int k, int nt,
+                                             double alpha, const double* __restrict__ nodes,
+                                             const int* __restrict__ tris, int ntri,
+                                             const double* __restrict__ u0, int qx, int qtf, int qtn,
+                                             int use_moments, double* acc, double* sm) {
+  const int lane = threadIdx.x & 31;
   const bool valid = k < ntri;
-  const Seg S = seg[i];
   double V[6] = {0, 0, 0, 0, 0, 0}, uv[3] = {0, 0, 0};
   bool near = false;
-  double cmin = 1e300;
   if (valid) {
 #pragma unroll
     for (int v = 0; v < 3; ++v) {
@@ -77,27 +111,22 @@ __global__ void __launch_bounds__(256) k_initial(const Seg* __restrict__ seg, co
       uv[v] = u0[id];
     }
     const double gx = (V[0] + V[2] + V[4]) / 3.0, gy = (V[1] + V[3] + V[5]) / 3.0;
-    double le = 0.0, rad = 0.0;
+    double le = 0.0;
 #pragma unroll
     for (int v = 0; v < 3; ++v) {
       const double ex = V[2 * ((v + 1) % 3)] - V[2 * v], ey = V[2 * ((v + 1) % 3) + 1] - V[2 * v + 1];
       le = fmax(le, sqrt(ex * ex + ey * ey));
-      rad = fmax(rad, sqrt((V[2 * v] - gx) * (V[2 * v] - gx) + (V[2 * v + 1] - gy) * (V[2 * v + 1] - gy)));
     }
     double f0 = (gx - S.ax) * S.tx + (gy - S.ay) * S.ty;
     f0 = fmin(fmax(f0, 0.0), S.h);
     const double qx0 = S.ax + f0 * S.tx - gx, qy0 = S.ay + f0 * S.ty - gy;
-    const double dist = sqrt(qx0 * qx0 + qy0 * qy0);
-    near = dist < 2.0 * fmax(S.h, le);
-    const double dmin = fmax(0.0, dist - rad);
-    cmin = 0.25 * alpha * dmin * dmin;    // lower bound of c over the triangle x gamma_i
+    near = sqrt(qx0 * qx0 + qy0 * qy0) < 2.0 * fmax(S.h, le);
   }
-  const double e1x = V[2] - V[0], e1y = V[3] - V[1], e2x = V[4] - V[0], e2y = V[5] - V[1];
-  const double area2 = fabs(e1x * e2y - e1y * e2x);
   const int qt = near ? qtn : qtf;
+  // step 0
   double first = 0.0;
   if (valid && near) {
-    // step 0 on a near triangle: the apex-split rule at every x point
+    const double e1x = V[2] - V[0], e1y = V[3] - V[1], e2x = V[4] - V[0], e2y = V[5] - V[1];
     const double det = e1x * e2y - e1y * e2x;
     for (int p = 0; p < qx; ++p) {
       const double xx = fma(c_gx[qx][p], S.bx - S.ax, S.ax), xy = fma(c_gx[qx][p], S.by - S.ay, S.ay);
@@ -106,36 +135,146 @@ __global__ void __launch_bounds__(256) k_initial(const Seg* __restrict__ seg, co
       const double ua = (1.0 - uu - vv) * uv[0] + uu * uv[1] + vv * uv[2];
       first = fma(c_gw[qx][p] * S.h, apex_split(xx, xy, V, uv, ua, alpha, tg[1]), first);
     }
+  } else if (valid) {
+    const double it = 1.0 / tg[1];
+    for_tri_points(S, V, uv, qx, qt, alpha, [&](double c, double W) { first = fma(W, dev_e1(c * it), first); });
   }
-  const long long base = ((long long)blockIdx.x * gridDim.y + blockIdx.y) * (nt + 2);
-  for (int n = 1; n <= nt; ++n) {
+  first = warp_sum(first);
+  if (lane == 0) acc[0] += first;
+
+  // the warp's joint moments (all lanes hold the sums)
+  double P[MKA + 1], mb[MKB + 1];
+#pragma unroll
+  for (int q = 0; q <= MKA; ++q) P[q] = 0.0;
+#pragma unroll
+  for (int q = 0; q <= MKB; ++q) mb[q] = 0.0;
+  double L0 = 0.0, cmn = 1e300, cmx = 0.0;
+  if (valid && use_moments)
+    for_tri_points(S, V, uv, qx, qt, alpha, [&](double c, double W) {
+      cmn = fmin(cmn, c);
+      cmx = fmax(cmx, c);
+      L0 = fma(W, log(c), L0);
+      double pw = W;
+#pragma unroll
+      for (int q = 0; q <= MKA; ++q) {
+        P[q] += pw;
+        pw *= c;
+      }
+    });
+  const double cmin = warp_min(valid ? cmn : 1e300), cmax = warp_max(valid ? cmx : 0.0);
+  const double c0 = 0.5 * (cmin + cmax);
+  const bool okB = use_moments && cmin > 0.0 && cmin < 1e300 && (cmax - c0) <= MRHO * c0;
+  const double ic0 = okB ? 1.0 / c0 : 0.0;
+  int kb = 0;
+  if (okB) {
+    const double rho = (cmax - c0) / c0;
+    kb = rho <= 1e-6 ? 3 : min(MKB, max(3, (int)ceil(log(1e-16) / log(rho))));
+    if (valid)
+      for_tri_points(S, V, uv, qx, qt, alpha, [&](double c, double W) {
+        const double d = c - c0;
+        double pw = W;
+#pragma unroll
+        for (int q = 0; q <= MKB; ++q) {
+          mb[q] += pw;
+          pw *= d;
+        }
+      });
+#pragma unroll
+    for (int q = 0; q <= MKB; ++q)
+      if (q <= kb) {                                      // kb warp-uniform
+        const double v = warp_sum(mb[q]);
+        if (lane == 0) sm[MKA + 1 + q] = q == 0 ? v : v * STB_INV[q];
+      }
+  }
+  if (use_moments) {
+    L0 = warp_sum(L0);
+#pragma unroll
+    for (int q = 0; q <= MKA; ++q) P[q] = warp_sum(P[q]);
+    if (lane == 0) {
+      sm[0] = P[0];
+#pragma unroll
+      for (int q = 1; q <= MKA; ++q) sm[q] = P[q] * STB_MEIN[q];
+    }
+    L0 = fma(STB_GAMMA, P[0], L0);                         // gamma M_0 + L_0
+  }
+  __syncwarp();
+  const double* Pm = sm;                                   // joint moments, broadcast reads
+  const double* mbm = sm + MKA + 1;
+  // joint regimes; n_A = first node in regime A (t grows with n)
+  int nA = nt + 1;
+  if (use_moments) {
+    for (int n = 1; n <= nt; ++n)
+      if (cmax < 4.0 * tg[n]) {
+        nA = n;
+        break;
+      }
+  }
+  const int nlane = use_moments && okB ? 1 : nA;          // nodes [1, nlane) take per-lane point sums
+  for (int n = 1 + lane; n <= nt; n += 32) {
+    if (n < nlane) continue;
     const double it = 1.0 / tg[n];
     double s = 0.0;
-    if (valid && cmin * it <= STB_XUNDER) {
-      for (int p = 0; p < qx; ++p) {
-        const double xx = fma(c_gx[qx][p], S.bx - S.ax, S.ax), xy = fma(c_gx[qx][p], S.by - S.ay, S.ay);
-        double sp = 0.0;
-        for (int a1 = 0; a1 < qt; ++a1) {
-          const double xi = c_gx[qt][a1];
-          for (int a2 = 0; a2 < qt; ++a2) {
-            const double eta = c_gx[qt][a2];
-            const double u = xi * (1.0 - eta), v = xi * eta;
-            const double yx = V[0] + u * e1x + v * e2x, yy = V[1] + u * e1y + v * e2y;
-            const double uh = (1.0 - u - v) * uv[0] + u * uv[1] + v * uv[2];
-            const double dx = xx - yx, dy = xy - yy;
-            const double c = 0.25 * alpha * (dx * dx + dy * dy);
-            sp = fma(xi * c_gw[qt][a1] * c_gw[qt][a2] * uh, dev_e1(c * it), sp);
-          }
-        }
-        s = fma(c_gw[qx][p] * S.h * area2, sp, s);
+    if (cmin * it > STB_XUNDER) {
+      s = 0.0;
+    } else if (n >= nA) {
+      double h = Pm[MKA];
+#pragma unroll
+      for (int q = MKA - 1; q >= 1; --q) h = fma(h, it, Pm[q]);
+      s = fma(h, it, -fma(log(it), Pm[0], L0));
+    } else {
+      const double x0 = c0 * it, ex = exp(-x0), tt = ic0 * tg[n];
+      const double E1 = ex * tt * gb3_cb(tt);
+      double e = ex, ap = ex * ic0, S1 = 0.0;
+      for (int q = 1; q <= kb; ++q) {
+        e = -e * (it * STB_INV[q]);
+        S1 = fma(ap, mbm[q], S1);
+        ap = (e - ap) * ic0;
       }
+      s = fma(E1, mbm[0], -S1);
     }
-    if (n == 1 && !near) first += s;         // far triangles: the regular rule serves step 0 too
-    const double tot = block_sum256(s, red);
-    if (threadIdx.x == 0) part[base + n] = tot;
+    acc[n] += s;
   }
-  const double tf = block_sum256(first, red);
-  if (threadIdx.x == 0) part[base] = tf;
+  for (int n = 1; n < nlane; ++n) {                       // per-lane point sums (rare with moments)
+    const double it = 1.0 / tg[n];
+    double s = 0.0;
+    if (valid)
+      for_tri_points(S, V, uv, qx, qt, alpha, [&](double c, double W) {
+        if (c * it <= STB_XUNDER) s = fma(W, dev_e1(c * it), s);
+      });
+    s = warp_sum(s);
+    if (lane == 0) acc[n] += s;
+  }
+}
+
+// CTA = (element i, chunk), 8 warps: the chunk's triangle batches k = (bt * nch + chunk) * 256 + tid
+// are interleaved over the chunks (balance of the near triangles); every warp accumulates its node
+// values into its own row (shared memory when 8 (nt + 2) doubles fit, else its global partial row)
+// in batch order; k_initial_finish sums the rows in fixed order (deterministic).
+__global__ void __launch_bounds__(256) k_initial(const Seg* __restrict__ seg, const double* __restrict__ tg,
+                                                int ng, int nt, double alpha,
+                                                const double* __restrict__ nodes, const int* __restrict__ tris,
+                                                int ntri, const double* __restrict__ u0, int qx, int qtf, int qtn,
+                                                int use_moments, int nbatch, int use_smem,
+                                                double* __restrict__ part) {
+  extern __shared__ double acc_s[];
+  __shared__ double msh[8][MKA + MKB + 2];               // each warp's joint moments
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long row = (((long long)blockIdx.x * gridDim.y + blockIdx.y) * 8 + warp) * (nt + 2);
+  double* acc = use_smem ? acc_s + warp * (nt + 2) : part + row;
+  for (int r = lane; r < nt + 2; r += 32) acc[r] = 0.0;
+  __syncwarp();
+  const Seg S = seg[blockIdx.x];
+  for (int bt = 0; bt < nbatch; ++bt) {
+    const int k0 = (bt * gridDim.y + blockIdx.y) * 256;
+    if (k0 >= ntri) break;                                // CTA-uniform
+    initial_warp(S, tg, k0 + threadIdx.x, nt, alpha, nodes, tris, ntri, u0, qx, qtf, qtn, use_moments, acc,
+                 msh[warp]);
+    __syncwarp();
+  }
+  if (use_smem) {
+    __syncwarp();
+    for (int r = lane; r < nt + 2; r += 32) part[row + r] = acc[r];
+  }
 }
 
 __global__ void k_initial_finish(const double* __restrict__ part, int ng, int nt, int nch, double alpha,
@@ -144,8 +283,8 @@ __global__ void k_initial_finish(const double* __restrict__ part, int ng, int nt
   if (r >= (long long)ng * nt) return;
   const int a = (int)(r / ng), i = (int)(r % ng);
   double v = 0.0;
-  for (int ch = 0; ch < nch; ++ch) {
-    const double* p = part + ((long long)i * nch + ch) * (nt + 2);
+  for (int row = 0; row < nch * 8; ++row) {       // chunk-major, warp-minor: fixed order
+    const double* p = part + ((long long)i * nch * 8 + row) * (nt + 2);
     v += a == 0 ? p[0] : p[a + 1] - p[a];
   }
   b[r] -= alpha / (4.0 * STB_PI) * v;    // b <- b - M_h^0 u0 (eq. 4)

@@ -414,7 +414,7 @@ struct RegBZ {
 // the GB3 coefficients as a (non-const) constant-bank array: read as c[bank][offset] operands of
 // the Horner DFMAs instead of being materialised as immediates on every regime-B evaluation
 static __device__ __constant__ double STB_GB3_CB[STB_GB3_DEG + 1] = STB_GB3_INIT;
-__device__ __forceinline__ double gb3_cb(double t) { return horner<STB_GB3_DEG>(STB_GB3_CB, fma(t, 6.0, -1.0)); }
+__device__ __forceinline__ double gb3_cb(double t) { return horner<STB_GB3_DEG>(STB_GB3_CB, fma(t, STB_GB3_YS, -1.0)); }
 
 template <int KIND>
 __device__ __forceinline__ double phi_bz(const double* __restrict__ rec, long long S, const RegBZ<KIND>& z,
@@ -426,7 +426,7 @@ __device__ __forceinline__ double phi_bz(const double* __restrict__ rec, long lo
   }
   double T[2] = {0.0, 0.0};
   if (!zz) {
-    // x0 = c0 u >= 4 / (1 + MRHO) > 3: E1(x0) = e^{-x0} t GB3(t), t = 1/x0 = s / c0
+    // x0 = c0 u >= 4 / (1 + MRHO) = 8/3 (the GB3 fit range): E1(x0) = e^{-x0} t GB3(t), t = 1/x0 = s / c0
     const double x0 = z.c0 * u, ic0 = z.ic0, ex = exp(-x0);
     const double E1 = ex * (ic0 * s) * gb3_cb(ic0 * s);
     const double* R0 = rec + (RF_COMMON + 0 * FAMSZ) * S;

@@ -1,0 +1,79 @@
+"""The polynomial constants the CUDA kernels evaluate (csrc/special_coeffs.h, moment_coeffs.h),
+checked against scipy's E1 over the whole range the kernels use them on (no GPU needed).
+
+The ranges come from the kernel sources themselves: regime B of the moment forms evaluates
+E1(x0) = e^{-x0} t GB3(t), t = 1/x0, for every x0 >= 4 / (1 + MRHO), so the
+GB3 fit must cover t <= (1 + MRHO) / 4 -- a fit on a shorter interval extrapolates (the r01 bug:
+fit on t <= 1/3 while MRHO = 0.5 needs 3/8, 2.5e-8 relative error at x0 = 8/3).
+"""
+import os
+import re
+
+import numpy as np
+import pytest
+from scipy.special import exp1
+
+CSRC = os.path.join(os.path.dirname(__file__), "..", "paper_1811_05224_b200", "csrc")
+EULER = 0.57721566490153286061
+
+
+def _coeffs(header, name):
+    s = open(os.path.join(CSRC, header)).read()
+    m = re.search(r"STB_%s\[\d+\] = \{([^}]*)\}" % name, s)
+    assert m, name
+    return np.array([float(v) for v in m.group(1).split(",")])
+
+
+def _define(header, name):
+    s = open(os.path.join(CSRC, header)).read()
+    m = re.search(r"#define STB_%s (\S+)" % name, s)
+    assert m, name
+    return float(m.group(1))
+
+
+def _constexpr(name):
+    s = open(os.path.join(CSRC, "moments.cuh")).read()
+    m = re.search(r"constexpr (?:double|int) %s = ([0-9.eE+-]+);" % name, s)
+    assert m, name
+    return float(m.group(1))
+
+
+def _horner(c, y):
+    r = np.zeros_like(y)
+    for v in c[::-1]:
+        r = r * y + v
+    return r
+
+
+def test_gb3_covers_regime_b():
+    c = _coeffs("special_coeffs.h", "GB3")
+    ys = _define("special_coeffs.h", "GB3_YS")
+    rho = _constexpr("MRHO")
+    tmax = (1.0 + rho) / 4.0              # x0 >= 4 / (1 + rho)
+    assert 2.0 / ys >= tmax * (1 - 1e-15), "GB3 fit interval shorter than regime B's t range"
+    t = np.linspace(2e-3, tmax, 4001)
+    x = 1.0 / t
+    e1 = np.exp(-x) * t * _horner(c, t * ys - 1.0)
+    rel = np.abs(e1 / exp1(x) - 1.0)
+    assert rel.max() < 5e-14, rel.max()
+
+
+def test_gb_large_x():
+    c = _coeffs("special_coeffs.h", "GB")
+    t = np.linspace(2e-3, 0.25, 2001)
+    x = 1.0 / t
+    rel = np.abs(np.exp(-x) * t * _horner(c, 8.0 * t - 1.0) / exp1(x) - 1.0)
+    assert rel.max() < 5e-14, rel.max()
+
+
+@pytest.mark.parametrize("name", ["MEIN", "MGH", "MPSI"])
+def test_moment_polynomials(name):
+    """the regime-A polynomials in x on [0, 4] (MKA = their degree bound)"""
+    c = _coeffs("moment_coeffs.h", name)
+    assert len(c) - 1 <= _constexpr("MKA")
+    x = np.linspace(1e-6, 4.0, 4001)
+    ein = exp1(x) + EULER + np.log(x)
+    ref = {"MEIN": ein, "MGH": (1 + x) * ein - np.exp(-x), "MPSI": np.expm1(-x) / x - ein}[name]
+    scale = _horner(np.abs(c), x)          # sum |c_k| x^k: the rounding scale of the Horner sum
+    err = np.abs(_horner(c, x) - ref) / np.maximum(scale, 1.0)
+    assert err.max() < 2e-15, err.max()

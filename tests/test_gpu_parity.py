@@ -390,7 +390,7 @@ def test_potential_rejects_boundary_points():
         S.eval_potential(m, cuda(np.zeros(w.n)), cuda(np.zeros(w.n)), np.array([[0.01, 0.5, 0.5]]))
 
 
-@pytest.mark.parametrize("L,orders", [(2, (4, 4, 12)), (3, (8, 6, 16)), (4, (4, 4, 12))])
+@pytest.mark.parametrize("L,orders", [(2, (4, 4, 12)), (3, (8, 6, 16)), (4, (4, 4, 12)), (5, (4, 4, 12))])
 def test_initial_potential_parity(L, orders):
     """row f1: b - M_h^0 u0 on the GPU against the oracle's M_h^0 u0 (paper's Table-1 workload)"""
     import workloads.table1 as T

@@ -2,7 +2,7 @@
 alpha = 10, u = exp(-t/alpha) sin(x . d), u0 != 0: b = (1/2 M_h + K_h) g - M_h^0 u0 (fused K g,
 bem_rhs_initial), GMRES to 1e-8 without and with the lumped preconditioner (the paper's choice,
 P:185) and with the exact dual mass; the L2(Sigma) error of w_h against d_n u.  Levels 2..7 on the
-dense path, level 8 (N = 262 144) on the block-Toeplitz variant (the dense matrices need 8 GPUs).
+dense path, levels 8 and 9 (N = 262 144, 1 048 576: the paper's largest) on the block-Toeplitz variant.
 Prints one JSON line per level."""
 import json, os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -37,7 +37,7 @@ def l2_error(w, wh, nq=6):
     return float(np.sqrt(err2 / ref2))
 
 
-for L in [int(v) for v in (sys.argv[1:] or "2 3 4 5 6 7 8".split())]:
+for L in [int(v) for v in (sys.argv[1:] or "2 3 4 5 6 7 8 9".split())]:
     w = T.table1(L)
     toep = L >= 8
     m = S.Mesh.from_workload(w)
