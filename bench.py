@@ -27,6 +27,7 @@ PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 # FP64 DFMA peak: 148 SMs x 64 FP64 FMA/clk x 2 flop x 1.965 GHz (B200_PROFILING.md unit counts,
 # MEASURED_PEAKS sm_max_mhz); tools/fp64_peak.cu measured 34.1 TFLOP/s on this pool (profiles/).
 FP64_PEAK_DERIVED = 148 * 64 * 2 * 1.965e9 / 1e12
+FP64_TC_PEAK = 37.1   # measured DMMA m8n8k4 throughput, profiles/r01_dmma_peak.txt
 
 
 def parse():
@@ -320,9 +321,24 @@ def native(args):
                  "peak_note": "MEASURED_PEAKS.json hbm_gbs (driver-measured copy bandwidth)",
                  "bytes_note": "algorithmic: 8 B per stored double of the product's matrix (block lower "
                                "triangle; V_h / D_h symmetric packed spatial blocks) + 16 N"}
+    if args.variant == "toeplitz":
+        # the product is the FP64 tensor-core GEMM k_toeplitz_mm: algorithmic flops per product
+        # 2 ng^2 sum_a (a + 1) (the block lower triangle of lags) against the measured DMMA peak
+        ng_, nt_t = w.n_gamma, w.n_steps
+        fl = 2.0 * ng_ * ng_ * nt_t * (nt_t + 1) / 2
+        tf = fl / gemv_s / 1e12 if gemv_s > 0 else None
+        roof_gemv = {"bound": "tensor", "kernel": "k_toeplitz_mm", "achieved": tf, "peak": FP64_TC_PEAK,
+                     "unit": "TFLOP/s", "frac": (tf / FP64_TC_PEAK) if tf else None, "traffic": None,
+                     "flops_per_launch": fl,
+                     "peak_note": "FP64 tensor cores (DMMA m8n8k4) measured 37.1 TFLOP/s on this pool's B200 "
+                                  "(profiles/r01_dmma_peak.txt; DFMA 34.1)",
+                     "flops_note": "algorithmic: 2 ng^2 per (row block a, lag d <= a) pair, per product; "
+                                   "time = the solve's products incl. the fixed-order partial reduction"}
     # context for the HBM roofline: MEASURED_PEAKS hbm_gbs is a copy (read + write) figure; a pure
     # streaming read (torch.sum over 8 GiB, after the timed region) can exceed it
     try:
+        if args.variant == "toeplitz":
+            raise RuntimeError("no HBM roofline for the tensor-bound variant")
         buf = torch.empty(1024 ** 3, dtype=torch.float64, device=dev).fill_(1.0)
         for _ in range(2):
             buf.sum()
@@ -353,7 +369,7 @@ def native(args):
                    "variant": args.variant, "n_gamma": w.n_gamma, "n_steps": w.n_steps,
                    "N": n, "alpha": w.alpha, "slices_P": P, "gmres_tol": tol, "precond": ["none", "lumped", "exact"][args.precond],
                    "parallelism": f"cyclic K_P blocks over {world} GPU" + ("s" if world > 1 else ""),
-                   "l2": "inputs larger than L2 (each matrix 17 GB >> 126 MB)"},
+                   "l2": "inputs larger than L2 (V_h %.1f GB, D_h %.1f GB >> 126 MB)" % (stats["V"]["bytes"] / 1e9, stats["D"]["bytes"] / 1e9)},
         "components": {
             "assembly_pairs_per_s": units_per_step / asm_s,
             "integrals_per_step": {k: stats[k]["entries"] for k in "VKD"},

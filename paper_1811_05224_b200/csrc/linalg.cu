@@ -301,28 +301,47 @@ bem_status gemv_launch(const bem_matrix* A, double a, const double* x, double b,
 // Uniform time steps: A(a, b) = T_{a-b}.  Y[i, a] = sum_{d <= a} sum_j T_d[i, j] X[j, a - d] with
 // X[j, b] = x[b ng + j]: one GEMM over the stacked contraction index k = d ng + j (SURVEY 8(f) row
 // f3) — a genuine contraction (many right-hand sides through the Toeplitz shift).  CTA tile
-// 64 rows i x 64 columns a, K split into chunks (fixed partial slots, reduced in fixed order);
-// register tile 4 x 4 per thread, DFMA (FP64 tensor cores are not faster on B200).
-constexpr int TZ_TI = 128, TZ_TA = 128, TZ_TK = 16;
-// CTA tile 128 rows i x 128 columns a, 256 threads as 16 x 16, 8 x 8 accumulators per thread
-// (rows ty*8 + u: broadcast reads of the T tile; columns 32 k + 2 tx + e: conflict-free 16-byte
-// reads of the X tile), K steps of 16 with the next step's tiles prefetched into registers while
-// the current one is multiplied from shared memory.
+// 128 rows i x 128 columns a, K split into lag ranges (fixed partial slots, reduced in fixed order).
+// The multiply runs on the FP64 tensor cores (DMMA m8n8k4): their peak is only ~9% above the DFMA
+// peak on B200 (37.1 vs 34.1 TFLOP/s, profiles/r01_fp64_peak.txt, r01_dmma_peak.txt) but one
+// DMMA does 256 FMAs per warp from 2 operand registers per lane, so the tile loop is no longer
+// bound by shared-memory operand loads and issue slots as the 8 x 8 DFMA register tile was.
+constexpr int TZ_TI = 128, TZ_TA = 128, TZ_TK = 16, TZ_LD = TZ_TI + 4;
+// 8 warps as 2 (i) x 4 (a), warp tile 64 i x 32 a = 8 x 4 DMMA tiles, 64 accumulators per lane.
+// Shared tiles k-major with row stride 132 doubles and column index ii ^ (jj / 4): the fragment
+// loads (lane -> k = lane % 4, m / n = lane / 4) and the tile stores (16 consecutive jj of one ii)
+// both hit 16 distinct 8-byte bank pairs per half warp.  The next K step's tiles are
+// prefetched into registers while the current one is multiplied from shared memory.
+__device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d[0]), "+d"(d[1]) : "d"(a), "d"(b));
+}
+// Work units (1-D grid): a-tile at (in order), then chunk of dpz lags within the tile's lag range
+// [0, min(nt, a0 + 128)) (lags beyond the tile's last column contribute nothing), then i-tile: all
+// units but a tile's last chunk cost the same, and the host sizes dpz for whole waves of the SMs.
 __global__ void __launch_bounds__(256) k_toeplitz_mm(const double* __restrict__ T, long long ldT_d,
                                                     int ldT, const double* __restrict__ x, int ng, int nt,
                                                     int dpz, double* __restrict__ part) {
-  __shared__ __align__(16) double Tt[TZ_TK][TZ_TI + 2];   // Tt[jj][ii] = T_d[i0 + ii][j0 + jj]
-  __shared__ __align__(16) double Xs[TZ_TK][TZ_TA + 2];   // Xs[jj][aa] = X[j0 + jj][a0 + aa - d]
-  const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
-  const int i0 = blockIdx.x * TZ_TI, a0 = blockIdx.y * TZ_TA;
-  const int d0 = blockIdx.z * dpz, d1 = min(min(nt, d0 + dpz), a0 + TZ_TA);   // d > a: nothing
+  __shared__ __align__(16) double Tt[TZ_TK][TZ_LD];   // Tt[jj][ii] = T_d[i0 + ii][j0 + jj]
+  __shared__ __align__(16) double Xs[TZ_TK][TZ_LD];   // Xs[jj][aa] = X[j0 + jj][a0 + aa - d]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wi = (warp & 1) * 64, wa = (warp >> 1) * 32, fr = lane & 3, fc = lane >> 2;
+  const int nti = (ng + TZ_TI - 1) / TZ_TI;
+  int r = blockIdx.x, at = 0;
+  for (;; ++at) {
+    const int cnt = nti * ((min(nt, (at + 1) * TZ_TA) + dpz - 1) / dpz);
+    if (r < cnt) break;
+    r -= cnt;
+  }
+  const int chunk = r / nti, i0 = (r % nti) * TZ_TI, a0 = at * TZ_TA;
+  const int d0 = chunk * dpz, d1 = min(min(nt, d0 + dpz), a0 + TZ_TA);   // d > a: nothing
   const int nj = (ng + TZ_TK - 1) / TZ_TK;
   const int nsteps = max(0, d1 - d0) * nj;
-  double acc[8][8];
+  double acc[8][4][2];
 #pragma unroll
   for (int u = 0; u < 8; ++u)
 #pragma unroll
-    for (int v = 0; v < 8; ++v) acc[u][v] = 0.0;
+    for (int v = 0; v < 4; ++v) acc[u][v][0] = acc[u][v][1] = 0.0;
   double rt[8], rx[8];
   auto fetch = [&](int step) {
     const int d = d0 + step / nj, j0 = (step % nj) * TZ_TK;
@@ -341,41 +360,35 @@ __global__ void __launch_bounds__(256) k_toeplitz_mm(const double* __restrict__ 
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const int e = tid + q * 256, ii = e / TZ_TK, jj = e % TZ_TK;
-      Tt[jj][ii] = rt[q];
-      Xs[jj][ii] = rx[q];
+      Tt[jj][ii ^ (jj >> 2)] = rt[q];     // XOR swizzle: conflict-free stores (16 jj of one ii)
+      Xs[jj][ii ^ (jj >> 2)] = rx[q];
     }
     __syncthreads();
     if (step + 1 < nsteps) fetch(step + 1);
-#pragma unroll 4
-    for (int jj = 0; jj < TZ_TK; ++jj) {
-      double tv[8], xv[8];
 #pragma unroll
-      for (int u = 0; u < 8; u += 2) {
-        const double2 t2 = *reinterpret_cast<const double2*>(&Tt[jj][ty * 8 + u]);
-        tv[u] = t2.x;
-        tv[u + 1] = t2.y;
-      }
+    for (int kk = 0; kk < TZ_TK; kk += 4) {
+      double af[8], bf[4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const double2 x2 = *reinterpret_cast<const double2*>(&Xs[jj][32 * k + 2 * tx]);
-        xv[2 * k] = x2.x;
-        xv[2 * k + 1] = x2.y;
-      }
+      for (int u = 0; u < 8; ++u) af[u] = Tt[kk + fr][(wi + 8 * u + fc) ^ (kk >> 2)];
+#pragma unroll
+      for (int v = 0; v < 4; ++v) bf[v] = Xs[kk + fr][(wa + 8 * v + fc) ^ (kk >> 2)];
 #pragma unroll
       for (int u = 0; u < 8; ++u)
 #pragma unroll
-        for (int v = 0; v < 8; ++v) acc[u][v] = fma(tv[u], xv[v], acc[u][v]);
+        for (int v = 0; v < 4; ++v) dmma_8x8x4(acc[u][v], af[u], bf[v]);
     }
   }
-  // partial Y tile of this lag range: part[z][a][i]
+  // partial Y tile of this lag range: part[z][a][i]; lane holds D[fc][2 fr + e] of each tile
   const long long n = (long long)nt * ng;
 #pragma unroll
   for (int u = 0; u < 8; ++u)
 #pragma unroll
-    for (int v = 0; v < 8; ++v) {
-      const int i = i0 + ty * 8 + u, a = a0 + 32 * (v / 2) + 2 * tx + (v % 2);
-      if (i < ng && a < nt) part[(long long)blockIdx.z * n + (long long)a * ng + i] = acc[u][v];
-    }
+    for (int v = 0; v < 4; ++v)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int i = i0 + wi + 8 * u + fc, a = a0 + wa + 8 * v + 2 * fr + e;
+        if (i < ng && a < nt) part[(long long)chunk * n + (long long)a * ng + i] = acc[u][v][e];
+      }
 }
 __global__ void k_toeplitz_reduce(const double* __restrict__ part, int nsplit, long long n, double alpha,
                                   double beta, double* __restrict__ y) {
@@ -391,18 +404,28 @@ bem_status toeplitz_gemv(const bem_matrix* A, double a, const double* x, double 
   const bem_mesh* m = A->mesh;
   const int ng = m->ng, nt = m->nt;
   const long long n = (long long)ng * nt;
-  // lag ranges per CTA: enough CTAs for two waves of the 148 SMs over the output tiles
-  const int tiles = ((ng + TZ_TI - 1) / TZ_TI) * ((nt + TZ_TA - 1) / TZ_TA);
-  const int want = std::max(1, (2 * num_sms() + tiles - 1) / tiles);
-  const int dpz = std::max(1, (nt + want - 1) / want);
+  // lag chunk dpz: minimise (waves of the SMs at one CTA each) x dpz, the critical path of equal units
+  const int nti = (ng + TZ_TI - 1) / TZ_TI, nta = (nt + TZ_TA - 1) / TZ_TA, sms = num_sms();
+  auto units = [&](int dz) {
+    long long u = 0;
+    for (int at = 0; at < nta; ++at) u += (long long)nti * ((std::min(nt, (at + 1) * TZ_TA) + dz - 1) / dz);
+    return u;
+  };
+  int dpz = nt;
+  double best = 1e300;
+  for (int dz = std::min(nt, 8); dz <= nt; ++dz) {
+    const long long u = units(dz);
+    const double cost = (double)((u + sms - 1) / sms) * (dz + 4);   // + 4: per-unit fill / epilogue
+    if (cost < best) best = cost, dpz = dz;
+  }
+  const long long nunits = units(dpz);
   const int nsplit = (nt + dpz - 1) / dpz;
   double* part = nullptr;
   const size_t bytes = sizeof(double) * n * nsplit;
   cudaError_t e = storage_acquire(m->device, bytes, st, (void**)&part);
   if (e != cudaSuccess) return cuda_fail(e, "toeplitz product");
   e = cudaMemsetAsync(part, 0, bytes, st);   // lag ranges beyond a tile's columns leave their slots zero
-  dim3 grid((ng + TZ_TI - 1) / TZ_TI, (nt + TZ_TA - 1) / TZ_TA, nsplit);
-  k_toeplitz_mm<<<grid, 256, 0, st>>>(A->data, A->poff.size() > 1 ? A->poff[1] - A->poff[0] : 0,
+  k_toeplitz_mm<<<(unsigned)nunits, 256, 0, st>>>(A->data, A->poff.size() > 1 ? A->poff[1] - A->poff[0] : 0,
                                       (int)pad4(ng), x, ng, nt, dpz, part);
   k_toeplitz_reduce<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(part, nsplit, n, a, b, y);
   count_launch(2);
