@@ -79,6 +79,11 @@ typedef struct {
 /* V_h and D_h store their symmetric spatial blocks packed (upper 32 x 32 tile triangle, about
  * half the bytes and half the assembly work); this flag stores them full */
 #define BEM_QUAD_FULL_STORAGE 2
+/* Bulk time cells (d >= 2): regime-A node values as a contraction on the FP64 tensor cores
+ * (k_bulk_t, DMMA m8n8k4) instead of the default Horner-chain DFMA kernel k_bulk_m (same regimes,
+ * results to rounding).  Opt-in: DMMA and DFMA share the FP64 units on B200 and k_bulk_t measured
+ * slower on C3 */
+#define BEM_QUAD_BULK_MMA 4
 
 typedef enum {
   BEM_MASS_PRIMAL = 0,      /* M_h of eq. (4): <phi^10_(a,n), phi^0_(a,i)> */

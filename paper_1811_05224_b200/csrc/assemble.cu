@@ -277,11 +277,14 @@ __global__ void __launch_bounds__(128) k_sing(BlockArgs B, const Seg* __restrict
 }
 
 // ================================================================= launch
+// which: 0 bulk (DMMA k_bulk_t with the basis table bas, or the DFMA k_bulk_m when bas is null),
+// 1 near cells
 template <int KIND, bool PROD = false>
 static void launch_kind(int which, const BlockArgs& BA, const MomArgs& M, int ng, int nband_or_chunk,
-                        int nz, cudaStream_t st) {
+                        int nz, cudaStream_t st, const double* bas = nullptr) {
   dim3 grid((ng + 31) / 32, (ng + 3) / 4, nz);
-  if (which == 0) k_bulk_m<KIND, 8, PROD><<<grid, 128, 0, st>>>(BA, M);
+  if (which == 0 && bas) k_bulk_t<KIND, PROD><<<grid, 128, 0, st>>>(BA, M, bas);
+  else if (which == 0) k_bulk_m<KIND, 8, PROD><<<grid, 128, 0, st>>>(BA, M);
   else k_near_m<KIND, PROD><<<grid, 128, 0, st>>>(BA, M, nband_or_chunk);
   count_launch();
 }
@@ -408,6 +411,26 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bul
   MS.rec = d_rec + 2LL * nf * npairs;
   MS.npairs = nsrec;
   MS.counters = d_ctr + 10;
+  // opt-in DMMA bulk kernel (BEM_QUAD_BULK_MMA or env BEM_BULK_MMA for the probes) and its basis
+  // table: (n_steps + 1)^2 nodes x 4 KS doubles
+  static const bool env_mma = getenv("BEM_BULK_MMA") != nullptr;
+  const bool use_mma = (flags & BEM_QUAD_BULK_MMA) || env_mma;
+  double* d_bas = nullptr;
+  const long long nnode = (long long)(m->nt + 1) * (m->nt + 1);
+  const size_t bas_bytes = use_mma ? sizeof(double) * nnode * 4 * (kind == STB_D ? BasisK<STB_D>::KS : BasisK<STB_V>::KS) : 0;
+  if (use_mma) {
+    if ((e = storage_acquire(m->device, bas_bytes, st, (void**)&d_bas)) != cudaSuccess) {
+      storage_release(m->device, d_rec, rec_bytes, st);
+      cudaFreeAsync(d_poff, st);
+      return cuda_fail(e, "assemble/basis");
+    }
+    const unsigned nb = (unsigned)((nnode + 255) / 256);
+    if (kind == STB_V) k_basis<STB_V><<<nb, 256, 0, st>>>(m->d_lag, m->nt + 1, d_bas);
+    else if (kind == STB_K) k_basis<STB_K><<<nb, 256, 0, st>>>(m->d_lag, m->nt + 1, d_bas);
+    else k_basis<STB_D><<<nb, 256, 0, st>>>(m->d_lag, m->nt + 1, d_bas);
+    count_launch();
+    A->launches++;
+  }
   mark();
   if (kind == STB_V) launch_records<STB_V>(MB, MN, fused_sing ? &MS : nullptr, q_sing, st);
   else if (kind == STB_K) launch_records<STB_K>(MB, MN, fused_sing ? &MS : nullptr, q_sing, st);
@@ -439,13 +462,13 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bul
     BA.pbase = pbase[bi];
     BA.pslots = pslots;
     BA.ntile = ntile;
-    const int R = 8;
+    const int R = use_mma ? 7 : 8;    // test steps per band (k_bulk_t: 8 nodes = one DMMA N tile)
     const int nband = (blk.a1 - blk.a0 + R - 1) / R;
     if (blk.a1 - 1 - blk.b0 >= 2) {
-      if (prod) launch_kind<STB_K, true>(0, BA, MB, ng, nband, nband, st);
-      else if (kind == STB_V) launch_kind<STB_V>(0, BA, MB, ng, nband, nband, st);
-      else if (kind == STB_K) launch_kind<STB_K>(0, BA, MB, ng, nband, nband, st);
-      else launch_kind<STB_D>(0, BA, MB, ng, nband, nband, st);
+      if (prod) launch_kind<STB_K, true>(0, BA, MB, ng, nband, nband, st, d_bas);
+      else if (kind == STB_V) launch_kind<STB_V>(0, BA, MB, ng, nband, nband, st, d_bas);
+      else if (kind == STB_K) launch_kind<STB_K>(0, BA, MB, ng, nband, nband, st, d_bas);
+      else launch_kind<STB_D>(0, BA, MB, ng, nband, nband, st, d_bas);
       mark();
       fam.push_back(0);
       A->launches++;
@@ -507,6 +530,7 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bul
     storage_release(m->device, d_part, part_bytes, st);
   }
   storage_release(m->device, d_rec, rec_bytes, st);
+  if (d_bas) storage_release(m->device, d_bas, bas_bytes, st);
   cudaFreeAsync(d_poff, st);
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "assemble/launch");

@@ -816,6 +816,305 @@ __global__ void __launch_bounds__(128, KIND == STB_D ? 2 : 3) k_bulk_m(BlockArgs
   count_regimes(M.counters, nA, nB, nZ, nC, nK);
 }
 
+// ------------------------------------------------------------- bulk cells on the FP64 tensor cores
+// Regime A node values are a contraction: Phi~(pair, node) = sum_k C[pair][k] Bas[k][node] with
+// the pair's coefficients C (premultiplied moments, the ln s / s terms of RegA) and the node's
+// basis Bas = (u^0 .. u^(NU-1), s, s ln s, ln s) (V: NU = 17, K: 18 + ln s, D: 18 + 3; padded to
+// 4 KS columns).  k_bulk_t evaluates it with DMMA m8n8k4 (M = 8 pairs, N = 8 nodes, K = 4 basis
+// terms): warp = test element I, 32 trial elements J as 4 M tiles; band of R = 7 test steps whose
+// 8 nodes x = r_lo .. r_lo + 7 at trial node y form the N tile.  DMMA and DFMA share the FP64 units
+// on B200 (profiles/r01_dmma_peak.txt: both at once 32.3 TFLOP/s, DMMA alone 37.1, DFMA alone
+// 34.1), so the contraction costs the same pipe time as the Horner chains (K = 20 vs 17-18
+// terms) but 8x fewer issued instructions: the regime fix-ups, second differences and stores run
+// beside it.  Lane (g = lane / 4, q = lane % 4) holds A[pair 8 mt + g][k = 4 ks + q] (its pairs'
+// coefficients, loaded once), B[k = 4 ks + q][node g] per trial node, and D[pair 8 mt + g][nodes
+// 2q, 2q+1].  Nodes outside regime A are overwritten by regimes B / Z (per lane) and C (warp).
+template <int KIND> struct BasisK;
+template <> struct BasisK<STB_V> { static constexpr int KS = 5, NU = 17; };
+template <> struct BasisK<STB_K> { static constexpr int KS = 5, NU = 18; };
+template <> struct BasisK<STB_D> { static constexpr int KS = 6, NU = 18; };
+
+// basis rows per node (x, y), zero for x <= y
+template <int KIND>
+__global__ void k_basis(const double4* __restrict__ lag, int ld, double* __restrict__ bas) {
+  constexpr int KB = 4 * BasisK<KIND>::KS, NU = BasisK<KIND>::NU;
+  const long long node = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (node >= (long long)ld * ld) return;
+  const double4 q = lag[node];
+  double* out = bas + node * KB;
+  const bool ok = q.x > 0.0;
+  double p = 1.0;
+  for (int k = 0; k < NU; ++k) {
+    out[k] = ok ? p : 0.0;
+    p *= q.z;
+  }
+  if (KIND == STB_K) {
+    out[NU] = ok ? q.y : 0.0;
+    for (int k = NU + 1; k < KB; ++k) out[k] = 0.0;
+  } else {
+    out[NU] = ok ? q.x : 0.0;
+    out[NU + 1] = ok ? q.x * q.y : 0.0;
+    out[NU + 2] = ok ? q.y : 0.0;
+    for (int k = NU + 3; k < KB; ++k) out[k] = 0.0;
+  }
+}
+
+// coefficient k (basis order) of the pair at rec (= M.rec + pair)
+template <int KIND>
+__device__ __forceinline__ double basis_coef(const double* __restrict__ rec, long long S, int k) {
+  constexpr int NU = BasisK<KIND>::NU;
+  const double* R0 = rec + (RF_COMMON + 0 * FAMSZ) * S;
+  if (KIND == STB_V) {
+    if (k < NU) return R0[(FA + k + 1) * S];
+    if (k == NU) return R0[FA * S];
+    if (k == NU + 1) return R0[FM0 * S];
+    if (k == NU + 2) return R0[FM1 * S];
+    return 0.0;
+  } else if (KIND == STB_K) {
+    if (k < NU) return R0[(FA + k) * S];
+    if (k == NU) return -R0[FM0 * S];
+    return 0.0;
+  } else {
+    const double* R1 = rec + (RF_COMMON + 1 * FAMSZ) * S;
+    if (k < NU) return (k < MKA ? R0[(FA + k + 1) * S] : 0.0) + R1[(FA + k) * S];
+    if (k == NU) return R0[FA * S];
+    if (k == NU + 1) return R0[FM0 * S];
+    if (k == NU + 2) return R0[FM1 * S] + R1[FM0 * S];
+    return 0.0;
+  }
+}
+
+__device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d[0]), "+d"(d[1]) : "d"(a), "d"(b));
+}
+
+template <int KIND, bool PROD = false>
+__global__ void __launch_bounds__(128, 3) k_bulk_t(BlockArgs B, MomArgs M, const double* __restrict__ bas) {
+  constexpr int R = 7, KS = BasisK<KIND>::KS, KB = 4 * KS;
+  const int ng = B.ng;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, q = lane & 3, g = lane >> 2;
+  const int I0 = blockIdx.y * 4 + warp, Jb = blockIdx.x * 32;
+  const bool rowok = I0 < ng;
+  const int I = min(I0, ng - 1);
+  const int band = blockIdx.z;
+  const int r_hi = B.a1 - R * band;
+  const int r_lo = max(B.a0, r_hi - R);
+  if (r_hi <= r_lo) return;                       // CTA-uniform
+  const int bmax = min(B.b1 - 1, r_hi - 1 - 2);
+  if (bmax < B.b0) return;                        // CTA-uniform
+  const int ti = (blockIdx.y * 4) / SYM_TS, tj = blockIdx.x;
+  if (B.sym && ti > tj) return;                   // CTA-uniform
+  const long long S = M.npairs;
+  __shared__ long long s_row[4][R];
+  long long* srow = s_row[warp];
+  if (!PROD && lane < R) {
+    const int a = min(r_lo + lane, r_hi - 1);
+    srow[lane] = B.poff[a - B.a0] + (B.sym ? sym_tile_index(ti, tj, B.nt) * (SYM_TS * SYM_TS) + (long long)(I % SYM_TS) * SYM_TS
+                                           : (long long)I * pad4((long long)panel_nb(a, B.b0, B.b1) * ng));
+  }
+  __syncwarp();
+  const long long cstride = B.sym ? B.blk : (long long)ng;
+  // this lane's pairs (I, J[mt]) and their coefficients
+  int Jm[4];
+  bool pv[4];
+  double af[4][KS], cmx[4];
+  bool nonzero = false;
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt) {
+    const int J0 = Jb + 8 * mt + g;
+    pv[mt] = rowok && J0 < ng;
+    Jm[mt] = min(J0, ng - 1);
+    const double* rec = M.rec + (long long)I * ng + Jm[mt];
+    cmx[mt] = rec[RF_CMAX * S];
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      af[mt][ks] = basis_coef<KIND>(rec, S, 4 * ks + q);
+      nonzero |= af[mt][ks] != 0.0;
+    }
+    nonzero |= cmx[mt] != 0.0;
+  }
+  // warps whose pairs hold no quadrature points (K_h, collinear elements) write zeros and skip
+  if (!__any_sync(0xffffffffu, nonzero)) {
+    unsigned long long nz = 0;
+    for (int y = B.b0; y <= bmax + 1; ++y) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int x = r_lo + 2 * q + e;
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) nz += pv[mt] && x <= r_hi && x > y;
+      }
+      if (!PROD && y > B.b0) {
+        const int b = y - 1;
+        double* col = B.out + (long long)(b - B.b0) * cstride;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int j = 2 * q + e - 1, a = r_lo + j;   // entry row index j = r - 1
+          if (j < 0 || a >= r_hi || a - b < 2) continue;
+#pragma unroll
+          for (int mt = 0; mt < 4; ++mt)
+            if (pv[mt]) col[srow[j] + (B.sym ? Jm[mt] % SYM_TS : Jm[mt])] = 0.0;
+        }
+      }
+    }
+    count_regimes(M.counters, nz, 0, 0, 0, 0);
+    return;
+  }
+  unsigned long long nA = 0, nB = 0, nZ = 0, nC = 0, nK = 0;
+  double Gp[4][2], accp[4][2];
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt) Gp[mt][0] = Gp[mt][1] = accp[mt][0] = accp[mt][1] = 0.0;
+  const int xg = min(r_lo + g, r_hi);             // this lane's B-fragment node row
+  for (int y = B.b0; y <= bmax + 1; ++y) {
+    const double* bp = bas + ((long long)xg * B.ldlag + y) * KB + q;
+    double bf[KS];
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) bf[ks] = bp[4 * ks];
+    double phi[4][2];
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) phi[mt][0] = phi[mt][1] = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) dmma884(phi[mt], af[mt][ks], bf[ks]);
+    // this lane's nodes r = 2q + e: validity and regime A
+    double4 nd[2];
+    bool ok[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int x = r_lo + 2 * q + e;
+      ok[e] = x <= r_hi && x > y;
+      nd[e] = B.lag[min(x, r_hi) * B.ldlag + y];
+    }
+    unsigned fix = 0;                             // bit 2 mt + e: node outside regime A
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const bool live = ok[e] && pv[mt];
+        const bool inA = cmx[mt] * nd[e].z < STB_MXA;
+        if (!ok[e]) phi[mt][e] = 0.0;
+        nA += live && inA;
+        if (live && !inA) fix |= 1u << (2 * mt + e);
+      }
+    if (__any_sync(0xffffffffu, fix != 0)) {
+      unsigned cmask = 0;
+      // one copy of the regime-B / Z code: the lane's flagged pairs in turn (values moved in and
+      // out of the register arrays by unrolled selects, no local-memory indexing)
+      unsigned todo = fix;
+#pragma unroll 1
+      while (todo) {
+        const int mt = (__ffs(todo) - 1) >> 1;
+        const unsigned f2 = (fix >> (2 * mt)) & 3u;
+        todo &= ~(3u << (2 * mt));
+        int Jsel = Jm[0];
+        double v0 = phi[0][0], v1 = phi[0][1];
+#pragma unroll
+        for (int m2 = 1; m2 < 4; ++m2)
+          if (m2 == mt) Jsel = Jm[m2], v0 = phi[m2][0], v1 = phi[m2][1];
+        const double* rec = M.rec + (long long)I * ng + Jsel;
+        RegBZ<KIND> Z;
+        Z.load(rec, S);
+        int reg0 = 0, reg1 = 0;
+        if (f2 == 3u) {
+          phi_bz2<KIND>(rec, S, Z, nd[0].x, nd[0].z, nd[1].x, nd[1].z, v0, v1, &reg0, &reg1);
+        } else if (f2 == 1u) {
+          v0 = phi_bz<KIND>(rec, S, Z, nd[0].x, nd[0].z, &reg0);
+        } else {
+          v1 = phi_bz<KIND>(rec, S, Z, nd[1].x, nd[1].z, &reg1);
+        }
+        nB += (reg0 == 1) + (reg1 == 1);
+        nK += (reg0 == 1 ? Z.kb : 0) + (reg1 == 1 ? Z.kb : 0);
+        nZ += (reg0 == 2) + (reg1 == 2);
+        if (reg0 == 3) { cmask |= 1u << (2 * mt); ++nC; }
+        if (reg1 == 3) { cmask |= 1u << (2 * mt + 1); ++nC; }
+#pragma unroll
+        for (int m2 = 0; m2 < 4; ++m2)
+          if (m2 == mt) {
+            if (f2 & 1u) phi[m2][0] = v0;
+            if (f2 & 2u) phi[m2][1] = v1;
+          }
+      }
+      unsigned lanes = __ballot_sync(0xffffffffu, cmask != 0);
+      while (lanes) {                             // warp-uniform
+        const int src = __ffs(lanes) - 1;
+        lanes &= lanes - 1;
+        unsigned cm = __shfl_sync(0xffffffffu, cmask, src);
+        while (cm) {
+          const int bit = __ffs(cm) - 1;
+          cm &= cm - 1;
+          const int mt = bit >> 1, e = bit & 1;
+          int Jsel = Jm[0];
+#pragma unroll
+          for (int m2 = 1; m2 < 4; ++m2)
+            if (m2 == mt) Jsel = Jm[m2];
+          const int Js = __shfl_sync(0xffffffffu, Jsel, src);
+          const int xs = r_lo + 2 * (src & 3) + e;
+          const double4 qd = B.lag[xs * B.ldlag + y];
+          const double v = phi_c_warp<KIND, false>(M, I, Js, qd.x, qd.y, qd.z);
+          if (lane == src) {
+#pragma unroll
+            for (int m2 = 0; m2 < 4; ++m2)
+#pragma unroll
+              for (int e2 = 0; e2 < 2; ++e2)
+                if (m2 == mt && e2 == e) phi[m2][e2] = v;
+          }
+        }
+      }
+    }
+    // differences along x: G[r] = Phi[r] - Phi[r-1]; lane q holds r = 2q (from lane - 1) and 2q + 1
+    double G[4][2];
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) {
+      const double prev = __shfl_up_sync(0xffffffffu, phi[mt][1], 1);
+      G[mt][0] = q > 0 ? phi[mt][0] - prev : 0.0;
+      G[mt][1] = phi[mt][1] - phi[mt][0];
+    }
+    if (y > B.b0) {
+      const int b = y - 1;
+      double gv[4];
+      if (PROD) {
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) gv[mt] = pv[mt] ? B.g[(long long)b * ng + Jm[mt]] : 0.0;
+      }
+      double* col = B.out + (long long)(b - B.b0) * cstride;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int j = 2 * q + e - 1, a = r_lo + j;   // entry row (r = j + 1)
+        const bool rok = j >= 0 && a < r_hi && a - b >= 2;
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) {
+          const double v = Gp[mt][e] - G[mt][e];
+          if (PROD) {
+            if (rok) accp[mt][e] = fma(v, gv[mt], accp[mt][e]);
+          } else if (rok && pv[mt]) {
+            col[srow[j] + (B.sym ? Jm[mt] % SYM_TS : Jm[mt])] = v;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) {
+      Gp[mt][0] = G[mt][0];
+      Gp[mt][1] = G[mt][1];
+    }
+  }
+  if (PROD) {
+    // row sums over the 32 trial elements: the 4 M tiles in the lane, then the 8 lanes of equal q
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      double sum = (accp[0][e] + accp[1][e]) + (accp[2][e] + accp[3][e]);
+      sum += __shfl_xor_sync(0xffffffffu, sum, 4);
+      sum += __shfl_xor_sync(0xffffffffu, sum, 8);
+      sum += __shfl_xor_sync(0xffffffffu, sum, 16);
+      const int j = 2 * q + e - 1, a = r_lo + j;
+      if (g == 0 && j >= 0 && a < r_hi && rowok)
+        B.part[B.pbase + ((long long)(a - B.a0) * ng + I) * B.pslots + blockIdx.x] = sum;
+    }
+  }
+  count_regimes(M.counters, nA, nB, nZ, nC, nK);
+}
+
 // ------------------------------------------------------------- near cells (d <= 1)
 // thread = entry-level pair; it walks the test steps a of its chunk: entry (a, a) = Phi(a+1, a),
 // entry (a, a-1) = Phi(a+1, a-1) - Phi(a, a-1) - Phi(a+1, a) (Phi(a, a) = 0: G vanishes at s = 0),

@@ -59,6 +59,7 @@ class SolveReport(ctypes.Structure):
 
 QUAD_LEGACY_SING = 1   # bem_quad_opts.flags: touching pairs by the per-lag singular kernel
 QUAD_FULL_STORAGE = 2  # bem_quad_opts.flags: V_h / D_h stored full instead of symmetric packed
+QUAD_BULK_MMA = 4      # bem_quad_opts.flags: bulk cells by the DMMA kernel k_bulk_t (opt-in)
 
 
 class AssemblyStats(ctypes.Structure):
@@ -249,8 +250,9 @@ class Mesh:
         except Exception:
             pass
 
-    def _assemble(self, fn, q_bulk=0, q_sing=0, legacy_sing=False, full_storage=False, stream=None):
-        o = QuadOpts(q_bulk, q_sing, (QUAD_LEGACY_SING if legacy_sing else 0) | (QUAD_FULL_STORAGE if full_storage else 0))
+    def _assemble(self, fn, q_bulk=0, q_sing=0, legacy_sing=False, full_storage=False, bulk_mma=False, stream=None):
+        o = QuadOpts(q_bulk, q_sing, (QUAD_LEGACY_SING if legacy_sing else 0) | (QUAD_FULL_STORAGE if full_storage else 0)
+                     | (QUAD_BULK_MMA if bulk_mma else 0))
         h = ctypes.c_void_p()
         check(fn(self.h, ctypes.byref(o), _stream(stream), ctypes.byref(h)))
         return Matrix(h, self)

@@ -98,6 +98,23 @@ def test_matrix_full_parity(name, kind):
         assert np.all(got[a * ng:(a + 1) * ng, (a + 1) * ng:] == 0.0)
 
 
+@pytest.mark.parametrize("name", ["LT", "C1", "C2"])
+@pytest.mark.parametrize("kind", ["V", "K", "D"])
+def test_bulk_mma_kernel(name, kind):
+    """the opt-in DMMA bulk kernel k_bulk_t (BEM_QUAD_BULK_MMA): oracle parity and agreement with
+    the default DFMA kernel to rounding"""
+    w = W.get(name)
+    m = S.Mesh.from_workload(w)
+    A = getattr(m, f"assemble_{kind}")(bulk_mma=True)
+    B = getattr(m, f"assemble_{kind}")()
+    got, dflt = A.dense(), B.dense()
+    if name != "C2":
+        assert relmax(got, oracle_dense(name, kind)) <= MAT_TOL
+    assert relmax(got, dflt) <= 1e-13
+    st = A.stats()
+    assert sum(st["nodes_bulk"]) > 0
+
+
 def sample_entries(w, rng, n_random=1500, rows_per=6):
     ng, nt = w.n_gamma, w.n_steps
     rows, cols = [], []
