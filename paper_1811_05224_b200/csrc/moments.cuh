@@ -822,13 +822,15 @@ __global__ void __launch_bounds__(128, KIND == STB_D ? 2 : 3) k_bulk_m(BlockArgs
 // basis Bas = (u^0 .. u^(NU-1), s, s ln s, ln s) (V: NU = 17, K: 18 + ln s, D: 18 + 3; padded to
 // 4 KS columns).  k_bulk_t evaluates it with DMMA m8n8k4 (M = 8 pairs, N = 8 nodes, K = 4 basis
 // terms): warp = test element I, 32 trial elements J as 4 M tiles; band of R = 7 test steps whose
-// 8 nodes x = r_lo .. r_lo + 7 at trial node y form the N tile.  DMMA and DFMA share the FP64 units
+// 8 nodes x = r_lo .. r_lo + 7 at trial node y form the N tile.  The accumulator tile is
+// transposed through shared memory so that lane j continues with the 8 node values of its own pair
+// (I, Jb + j) exactly as k_bulk_m does (regime fix-ups with the lane's RegBZ, differences, stores).  DMMA and DFMA share the FP64 units
 // on B200 (profiles/r01_dmma_peak.txt: both at once 32.3 TFLOP/s, DMMA alone 37.1, DFMA alone
 // 34.1), so the contraction costs the same pipe time as the Horner chains (K = 20 vs 17-18
 // terms) but 8x fewer issued instructions: the regime fix-ups, second differences and stores run
 // beside it.  Lane (g = lane / 4, q = lane % 4) holds A[pair 8 mt + g][k = 4 ks + q] (its pairs'
 // coefficients, loaded once), B[k = 4 ks + q][node g] per trial node, and D[pair 8 mt + g][nodes
-// 2q, 2q+1].  Nodes outside regime A are overwritten by regimes B / Z (per lane) and C (warp).
+// 2q, 2q+1].
 template <int KIND> struct BasisK;
 template <> struct BasisK<STB_V> { static constexpr int KS = 5, NU = 17; };
 template <> struct BasisK<STB_K> { static constexpr int KS = 5, NU = 18; };
@@ -895,8 +897,9 @@ __global__ void __launch_bounds__(128, 3) k_bulk_t(BlockArgs B, MomArgs M, const
   const int ng = B.ng;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, q = lane & 3, g = lane >> 2;
   const int I0 = blockIdx.y * 4 + warp, Jb = blockIdx.x * 32;
-  const bool rowok = I0 < ng;
-  const int I = min(I0, ng - 1);
+  const int J0 = Jb + lane;
+  const bool valid = I0 < ng && J0 < ng;
+  const int I = min(I0, ng - 1), J = min(J0, ng - 1);
   const int band = blockIdx.z;
   const int r_hi = B.a1 - R * band;
   const int r_lo = max(B.a0, r_hi - R);
@@ -906,8 +909,11 @@ __global__ void __launch_bounds__(128, 3) k_bulk_t(BlockArgs B, MomArgs M, const
   const int ti = (blockIdx.y * 4) / SYM_TS, tj = blockIdx.x;
   if (B.sym && ti > tj) return;                   // CTA-uniform
   const long long S = M.npairs;
+  const long long pair = (long long)I * ng + J;
   __shared__ long long s_row[4][R];
+  __shared__ double s_tr[4][32 * 9];              // per warp: node values [pair][node], row stride 9
   long long* srow = s_row[warp];
+  double* tr = s_tr[warp];
   if (!PROD && lane < R) {
     const int a = min(r_lo + lane, r_hi - 1);
     srow[lane] = B.poff[a - B.a0] + (B.sym ? sym_tile_index(ti, tj, B.nt) * (SYM_TS * SYM_TS) + (long long)(I % SYM_TS) * SYM_TS
@@ -915,203 +921,163 @@ __global__ void __launch_bounds__(128, 3) k_bulk_t(BlockArgs B, MomArgs M, const
   }
   __syncwarp();
   const long long cstride = B.sym ? B.blk : (long long)ng;
-  // this lane's pairs (I, J[mt]) and their coefficients
-  int Jm[4];
-  bool pv[4];
-  double af[4][KS], cmx[4];
-  bool nonzero = false;
+  const int jcol = B.sym ? J % SYM_TS : J;
+  // A fragments: coefficient k = 4 ks + q of the pairs (I, Jb + 8 mt + g)
+  double af[4][KS];
 #pragma unroll
   for (int mt = 0; mt < 4; ++mt) {
-    const int J0 = Jb + 8 * mt + g;
-    pv[mt] = rowok && J0 < ng;
-    Jm[mt] = min(J0, ng - 1);
-    const double* rec = M.rec + (long long)I * ng + Jm[mt];
-    cmx[mt] = rec[RF_CMAX * S];
+    const double* rec = M.rec + (long long)I * ng + min(Jb + 8 * mt + g, ng - 1);
 #pragma unroll
-    for (int ks = 0; ks < KS; ++ks) {
-      af[mt][ks] = basis_coef<KIND>(rec, S, 4 * ks + q);
-      nonzero |= af[mt][ks] != 0.0;
-    }
-    nonzero |= cmx[mt] != 0.0;
+    for (int ks = 0; ks < KS; ++ks) af[mt][ks] = basis_coef<KIND>(rec, S, 4 * ks + q);
   }
-  // warps whose pairs hold no quadrature points (K_h, collinear elements) write zeros and skip
-  if (!__any_sync(0xffffffffu, nonzero)) {
+  // this lane's own pair (I, J): regime constants
+  const double cmax = M.rec[RF_CMAX * S + pair];
+  bool nonzero = cmax != 0.0;
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) nonzero |= af[mt][ks] != 0.0;
+  if (!__any_sync(0xffffffffu, nonzero)) {        // K_h collinear elements: zeros, no node work
     unsigned long long nz = 0;
     for (int y = B.b0; y <= bmax + 1; ++y) {
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int x = r_lo + 2 * q + e;
-#pragma unroll
-        for (int mt = 0; mt < 4; ++mt) nz += pv[mt] && x <= r_hi && x > y;
-      }
+      for (int r = 0; r <= R; ++r) nz += (r_lo + r <= r_hi && r_lo + r > y);
       if (!PROD && y > B.b0) {
         const int b = y - 1;
-        double* col = B.out + (long long)(b - B.b0) * cstride;
+        double* col = B.out + ((long long)(b - B.b0) * cstride + jcol);
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int j = 2 * q + e - 1, a = r_lo + j;   // entry row index j = r - 1
-          if (j < 0 || a >= r_hi || a - b < 2) continue;
-#pragma unroll
-          for (int mt = 0; mt < 4; ++mt)
-            if (pv[mt]) col[srow[j] + (B.sym ? Jm[mt] % SYM_TS : Jm[mt])] = 0.0;
+        for (int r = 1; r <= R; ++r) {
+          const int a = r_lo + r - 1;
+          if (valid && a < r_hi && a - b >= 2) col[srow[r - 1]] = 0.0;
         }
       }
     }
-    count_regimes(M.counters, nz, 0, 0, 0, 0);
+    count_regimes(M.counters, valid ? nz : 0, 0, 0, 0, 0);
     return;
   }
+  RegBZ<KIND> Z;
+  Z.load(M.rec + pair, S);
   unsigned long long nA = 0, nB = 0, nZ = 0, nC = 0, nK = 0;
-  double Gp[4][2], accp[4][2];
+  double accp[R], Gp[R];
 #pragma unroll
-  for (int mt = 0; mt < 4; ++mt) Gp[mt][0] = Gp[mt][1] = accp[mt][0] = accp[mt][1] = 0.0;
-  const int xg = min(r_lo + g, r_hi);             // this lane's B-fragment node row
+  for (int r = 0; r < R; ++r) accp[r] = Gp[r] = 0.0;
+  const int xg = min(r_lo + g, r_hi);             // B-fragment node row of this lane
   for (int y = B.b0; y <= bmax + 1; ++y) {
     const double* bp = bas + ((long long)xg * B.ldlag + y) * KB + q;
     double bf[KS];
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) bf[ks] = bp[4 * ks];
-    double phi[4][2];
+    double d[4][2];
 #pragma unroll
-    for (int mt = 0; mt < 4; ++mt) phi[mt][0] = phi[mt][1] = 0.0;
+    for (int mt = 0; mt < 4; ++mt) d[mt][0] = d[mt][1] = 0.0;
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks)
 #pragma unroll
-      for (int mt = 0; mt < 4; ++mt) dmma884(phi[mt], af[mt][ks], bf[ks]);
-    // this lane's nodes r = 2q + e: validity and regime A
-    double4 nd[2];
-    bool ok[2];
+      for (int mt = 0; mt < 4; ++mt) dmma884(d[mt], af[mt][ks], bf[ks]);
+    // transpose through shared memory: lane j takes the 8 node values of its own pair j
 #pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int x = r_lo + 2 * q + e;
-      ok[e] = x <= r_hi && x > y;
-      nd[e] = B.lag[min(x, r_hi) * B.ldlag + y];
+    for (int mt = 0; mt < 4; ++mt) {
+      tr[(8 * mt + g) * 9 + 2 * q] = d[mt][0];
+      tr[(8 * mt + g) * 9 + 2 * q + 1] = d[mt][1];
     }
-    unsigned fix = 0;                             // bit 2 mt + e: node outside regime A
+    __syncwarp();
+    double phi[R + 1];
+    unsigned bmask = 0;
 #pragma unroll
-    for (int mt = 0; mt < 4; ++mt)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const bool live = ok[e] && pv[mt];
-        const bool inA = cmx[mt] * nd[e].z < STB_MXA;
-        if (!ok[e]) phi[mt][e] = 0.0;
-        nA += live && inA;
-        if (live && !inA) fix |= 1u << (2 * mt + e);
-      }
-    if (__any_sync(0xffffffffu, fix != 0)) {
+    for (int r = 0; r <= R; ++r) {
+      const int x = r_lo + r;
+      const bool ok = x <= r_hi && x > y;
+      const double u = B.lag[min(x, r_hi) * B.ldlag + y].z;
+      const bool inA = cmax * u < STB_MXA;
+      phi[r] = ok ? tr[lane * 9 + r] : 0.0;
+      nA += ok && inA;
+      if (ok && !inA) bmask |= 1u << r;
+    }
+    __syncwarp();
+    if (__any_sync(0xffffffffu, bmask != 0)) {
       unsigned cmask = 0;
-      // one copy of the regime-B / Z code: the lane's flagged pairs in turn (values moved in and
-      // out of the register arrays by unrolled selects, no local-memory indexing)
-      unsigned todo = fix;
-#pragma unroll 1
-      while (todo) {
-        const int mt = (__ffs(todo) - 1) >> 1;
-        const unsigned f2 = (fix >> (2 * mt)) & 3u;
-        todo &= ~(3u << (2 * mt));
-        int Jsel = Jm[0];
-        double v0 = phi[0][0], v1 = phi[0][1];
-#pragma unroll
-        for (int m2 = 1; m2 < 4; ++m2)
-          if (m2 == mt) Jsel = Jm[m2], v0 = phi[m2][0], v1 = phi[m2][1];
-        const double* rec = M.rec + (long long)I * ng + Jsel;
-        RegBZ<KIND> Z;
-        Z.load(rec, S);
-        int reg0 = 0, reg1 = 0;
-        if (f2 == 3u) {
-          phi_bz2<KIND>(rec, S, Z, nd[0].x, nd[0].z, nd[1].x, nd[1].z, v0, v1, &reg0, &reg1);
-        } else if (f2 == 1u) {
-          v0 = phi_bz<KIND>(rec, S, Z, nd[0].x, nd[0].z, &reg0);
+      while (bmask) {
+        const int r = __ffs(bmask) - 1;
+        bmask &= bmask - 1;
+        const double4 qd = B.lag[(r_lo + r) * B.ldlag + y];
+        int reg = 0, reg2 = 0;
+        double v = 0.0, v2 = 0.0;
+        int r2 = -1;
+        if (bmask) {
+          r2 = __ffs(bmask) - 1;
+          bmask &= bmask - 1;
+          const double4 q2 = B.lag[(r_lo + r2) * B.ldlag + y];
+          phi_bz2<KIND>(M.rec + pair, S, Z, qd.x, qd.z, q2.x, q2.z, v, v2, &reg, &reg2);
         } else {
-          v1 = phi_bz<KIND>(rec, S, Z, nd[1].x, nd[1].z, &reg1);
+          v = phi_bz<KIND>(M.rec + pair, S, Z, qd.x, qd.z, &reg);
         }
-        nB += (reg0 == 1) + (reg1 == 1);
-        nK += (reg0 == 1 ? Z.kb : 0) + (reg1 == 1 ? Z.kb : 0);
-        nZ += (reg0 == 2) + (reg1 == 2);
-        if (reg0 == 3) { cmask |= 1u << (2 * mt); ++nC; }
-        if (reg1 == 3) { cmask |= 1u << (2 * mt + 1); ++nC; }
+        nB += (reg == 1) + (reg2 == 1);
+        nK += (reg == 1 ? Z.kb : 0) + (reg2 == 1 ? Z.kb : 0);
+        nZ += (reg == 2) + (reg2 == 2);
+        if (reg == 3) { cmask |= 1u << r; ++nC; }
+        if (reg2 == 3) { cmask |= 1u << r2; ++nC; }
 #pragma unroll
-        for (int m2 = 0; m2 < 4; ++m2)
-          if (m2 == mt) {
-            if (f2 & 1u) phi[m2][0] = v0;
-            if (f2 & 2u) phi[m2][1] = v1;
-          }
+        for (int rr = 0; rr <= R; ++rr) {
+          if (rr == r) phi[rr] = v;
+          if (rr == r2) phi[rr] = v2;
+        }
       }
       unsigned lanes = __ballot_sync(0xffffffffu, cmask != 0);
       while (lanes) {                             // warp-uniform
         const int src = __ffs(lanes) - 1;
         lanes &= lanes - 1;
         unsigned cm = __shfl_sync(0xffffffffu, cmask, src);
+        const int Js = __shfl_sync(0xffffffffu, J, src);
         while (cm) {
-          const int bit = __ffs(cm) - 1;
+          const int r = __ffs(cm) - 1;
           cm &= cm - 1;
-          const int mt = bit >> 1, e = bit & 1;
-          int Jsel = Jm[0];
-#pragma unroll
-          for (int m2 = 1; m2 < 4; ++m2)
-            if (m2 == mt) Jsel = Jm[m2];
-          const int Js = __shfl_sync(0xffffffffu, Jsel, src);
-          const int xs = r_lo + 2 * (src & 3) + e;
-          const double4 qd = B.lag[xs * B.ldlag + y];
+          const double4 qd = B.lag[(r_lo + r) * B.ldlag + y];
           const double v = phi_c_warp<KIND, false>(M, I, Js, qd.x, qd.y, qd.z);
           if (lane == src) {
 #pragma unroll
-            for (int m2 = 0; m2 < 4; ++m2)
-#pragma unroll
-              for (int e2 = 0; e2 < 2; ++e2)
-                if (m2 == mt && e2 == e) phi[m2][e2] = v;
+            for (int rr = 0; rr <= R; ++rr)
+              if (rr == r) phi[rr] = v;
           }
         }
       }
-    }
-    // differences along x: G[r] = Phi[r] - Phi[r-1]; lane q holds r = 2q (from lane - 1) and 2q + 1
-    double G[4][2];
-#pragma unroll
-    for (int mt = 0; mt < 4; ++mt) {
-      const double prev = __shfl_up_sync(0xffffffffu, phi[mt][1], 1);
-      G[mt][0] = q > 0 ? phi[mt][0] - prev : 0.0;
-      G[mt][1] = phi[mt][1] - phi[mt][0];
     }
     if (y > B.b0) {
       const int b = y - 1;
-      double gv[4];
+      const bool interior = b <= r_lo - 2 && r_hi - r_lo == R;
       if (PROD) {
+        const double gv = valid ? B.g[(long long)b * ng + J] : 0.0;
 #pragma unroll
-        for (int mt = 0; mt < 4; ++mt) gv[mt] = pv[mt] ? B.g[(long long)b * ng + Jm[mt]] : 0.0;
-      }
-      double* col = B.out + (long long)(b - B.b0) * cstride;
+        for (int r = 1; r <= R; ++r) {
+          const int a = r_lo + r - 1;
+          const double G = phi[r] - phi[r - 1];
+          if (interior || (a < r_hi && a - b >= 2)) accp[r - 1] = fma(Gp[r - 1] - G, gv, accp[r - 1]);
+          Gp[r - 1] = G;
+        }
+      } else {
+        double* col = B.out + ((long long)(b - B.b0) * cstride + jcol);
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int j = 2 * q + e - 1, a = r_lo + j;   // entry row (r = j + 1)
-        const bool rok = j >= 0 && a < r_hi && a - b >= 2;
-#pragma unroll
-        for (int mt = 0; mt < 4; ++mt) {
-          const double v = Gp[mt][e] - G[mt][e];
-          if (PROD) {
-            if (rok) accp[mt][e] = fma(v, gv[mt], accp[mt][e]);
-          } else if (rok && pv[mt]) {
-            col[srow[j] + (B.sym ? Jm[mt] % SYM_TS : Jm[mt])] = v;
-          }
+        for (int r = 1; r <= R; ++r) {
+          const int a = r_lo + r - 1;
+          const double G = phi[r] - phi[r - 1];
+          if (valid && (interior || (a < r_hi && a - b >= 2))) col[srow[r - 1]] = Gp[r - 1] - G;
+          Gp[r - 1] = G;
         }
       }
-    }
+    } else {
 #pragma unroll
-    for (int mt = 0; mt < 4; ++mt) {
-      Gp[mt][0] = G[mt][0];
-      Gp[mt][1] = G[mt][1];
+      for (int r = 1; r <= R; ++r) Gp[r - 1] = phi[r] - phi[r - 1];
     }
   }
   if (PROD) {
-    // row sums over the 32 trial elements: the 4 M tiles in the lane, then the 8 lanes of equal q
 #pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      double sum = (accp[0][e] + accp[1][e]) + (accp[2][e] + accp[3][e]);
-      sum += __shfl_xor_sync(0xffffffffu, sum, 4);
-      sum += __shfl_xor_sync(0xffffffffu, sum, 8);
-      sum += __shfl_xor_sync(0xffffffffu, sum, 16);
-      const int j = 2 * q + e - 1, a = r_lo + j;
-      if (g == 0 && j >= 0 && a < r_hi && rowok)
+    for (int r = 0; r < R; ++r) {
+      const double sum = warp_sum(accp[r]);
+      const int a = r_lo + r;
+      if (lane == 0 && a < r_hi && I0 < ng)
         B.part[B.pbase + ((long long)(a - B.a0) * ng + I) * B.pslots + blockIdx.x] = sum;
     }
   }
+  if (!valid) nA = nB = nZ = nC = nK = 0;
   count_regimes(M.counters, nA, nB, nZ, nC, nK);
 }
 
