@@ -622,7 +622,7 @@ __device__ __forceinline__ void count_regimes(unsigned long long* ctr, unsigned 
 // index and summed over the thread's columns; one warp sum per (test row, trial tile) is written
 // to the block's partial buffer (fixed slots: deterministic)
 template <int KIND, int R, bool PROD = false>
-__global__ void __launch_bounds__(128, KIND == STB_D ? 2 : 3) k_bulk_m(BlockArgs B, MomArgs M) {
+__global__ void __launch_bounds__(128, (KIND == STB_D || PROD) ? 2 : 3) k_bulk_m(BlockArgs B, MomArgs M) {
   const int ng = B.ng;
   const int lane = threadIdx.x & 31;
   const int J0 = blockIdx.x * 32 + lane;
