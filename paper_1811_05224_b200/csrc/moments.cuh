@@ -257,11 +257,15 @@ __global__ void __launch_bounds__(128) k_records(MomArgs M) {
     for (int f = 0; f < NF; ++f) {
       const int fam = f == 0 ? Fams<KIND>::f0 : Fams<KIND>::f1;
       const double w = f == 0 ? wa : wb;
-      double pw = w;
+      // two independent power chains (even / odd orders)
+      const double c2 = c * c;
+      double pe = w, po = w * c;
 #pragma unroll
-      for (int k = 0; k <= MKA; ++k) {
-        mk[f][k] += pw;
-        pw *= c;
+      for (int k = 0; k <= MKA; k += 2) {
+        mk[f][k] += pe;
+        if (k + 1 <= MKA) mk[f][k + 1] += po;
+        pe *= c2;
+        po *= c2;
       }
       if (lg) {
         C0[f] = fma(w, g, C0[f]);
@@ -269,35 +273,55 @@ __global__ void __launch_bounds__(128) k_records(MomArgs M) {
       }
     }
   });
+  // regime-A fields of both families (static indices: the moments stay in registers)
+#pragma unroll
+  for (int f = 0; f < NF; ++f) {
+    const int fam = f == 0 ? Fams<KIND>::f0 : Fams<KIND>::f1;
+    double* R = rec + (RF_COMMON + f * FAMSZ) * S;
+#pragma unroll
+    for (int k = 0; k <= MKA; ++k) R[(FA + k) * S] = mpoly(fam, k) * mk[f][k];
+    R[FM0 * S] = mk[f][0];
+    R[FM1 * S] = mk[f][1];
+    R[FC0 * S] = C0[f];
+    R[FC1 * S] = C1[f];
+  }
 #pragma unroll 1
   for (int slot = 0; slot < NF; ++slot) {
     const int fam = slot == 0 ? Fams<KIND>::f0 : Fams<KIND>::f1;
     double* R = rec + (RF_COMMON + slot * FAMSZ) * S;
-#pragma unroll
-    for (int k = 0; k <= MKA; ++k) R[(FA + k) * S] = mpoly(fam, k) * mk[slot][k];
-    R[FM0 * S] = mk[slot][0];
-    R[FM1 * S] = mk[slot][1];
-    R[FC0 * S] = C0[slot];
-    R[FC1 * S] = C1[slot];
-    // regime B: m_k = sum W (c - c0)^k
+    // regime B: m_k = sum W (c - c0)^k, only the orders the evaluation reads (k <= kb): chunks of
+    // 8 with a per-thread exit, four independent power chains
     double mb[MKB + 1];
 #pragma unroll
     for (int k = 0; k <= MKB; ++k) mb[k] = 0.0;
     if (okB) {
       for_points<KIND, NEAR>(M, I, J, [&](double c, double wa, double wb) {
         const double w = slot == 0 ? wa : wb;
-        const double d = c - c0;
-        double pw = w;
+        const double d = c - c0, d2 = d * d, d4 = d2 * d2;
+        double p0 = w, p1 = w * d, p2 = w * d2, p3 = p1 * d2;
 #pragma unroll
-        for (int k = 0; k <= MKB; ++k) {
-          mb[k] += pw;
-          pw *= d;
+        for (int kc = 0; kc <= MKB / 8; ++kc) {
+          if (kc * 8 > kb) break;
+#pragma unroll
+          for (int j = 0; j < 8; j += 4) {
+            const int k = kc * 8 + j;
+            if (k <= MKB) mb[k] += p0;
+            if (k + 1 <= MKB) mb[k + 1] += p1;
+            if (k + 2 <= MKB) mb[k + 2] += p2;
+            if (k + 3 <= MKB) mb[k + 3] += p3;
+            p0 *= d4;
+            p1 *= d4;
+            p2 *= d4;
+            p3 *= d4;
+          }
         }
       });
     }
 #pragma unroll
     for (int k = 0; k <= MKB; ++k) {
-      // B1[k] = m_k / k (B1[0] = m_0); B2: H m_k / ((k-1) k) (B2[1] = m_1), Q m_k, F unused
+      // B1[k] = m_k / k (B1[0] = m_0); B2: H m_k / ((k-1) k) (B2[1] = m_1), Q m_k, F unused;
+      // orders above kb are never read
+      if (k > kb && k > 1) break;
       R[(FB1 + k) * S] = k == 0 ? mb[0] : mb[k] * STB_INV_H[k];
       R[(FB2 + k) * S] = fam == FAM_Q ? mb[k] : (fam == FAM_H ? (k == 0 ? 0.0 : (k == 1 ? mb[1] : mb[k] * STB_INV_H[k - 1] * STB_INV_H[k])) : 0.0);
     }
