@@ -328,7 +328,8 @@ def native(args):
         fl = 2.0 * ng_ * ng_ * nt_t * (nt_t + 1) / 2
         tf = fl / gemv_s / 1e12 if gemv_s > 0 else None
         roof_gemv = {"bound": "tensor", "kernel": "k_toeplitz_mm", "achieved": tf, "peak": FP64_TC_PEAK,
-                     "unit": "TFLOP/s", "frac": (tf / FP64_TC_PEAK) if tf else None, "traffic": None,
+                     "unit": "TFLOP/s", "frac": (tf / FP64_TC_PEAK) if tf else None,
+                     "traffic": traffic.get("k_toeplitz_mm"),
                      "flops_per_launch": fl,
                      "peak_note": "FP64 tensor cores (DMMA m8n8k4) measured 37.1 TFLOP/s on this pool's B200 "
                                   "(profiles/r01_dmma_peak.txt; DFMA 34.1)",

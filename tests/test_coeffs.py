@@ -77,3 +77,36 @@ def test_moment_polynomials(name):
     scale = _horner(np.abs(c), x)          # sum |c_k| x^k: the rounding scale of the Horner sum
     err = np.abs(_horner(c, x) - ref) / np.maximum(scale, 1.0)
     assert err.max() < 2e-15, err.max()
+
+
+def test_regime_b_taylor_truncation():
+    """regime B restated (scaled recurrence of the Taylor coefficients of e^{-x}/x about x0, order
+    K = ceil(ln 1e-16 / ln rho) capped at MKB) for the F family, against mpmath E1 point sums, over
+    the whole regime: rho up to MRHO, x0 from 4 / (1 + rho) up to x_min = MXZ (regime Z beyond).
+    The error is measured against sum |W| -- the scale of the node values Phi~ (the affine constants
+    sum W (gamma + ln c) are of that size) whose second differences are the entries: at large x0
+    the truncated series is relatively inaccurate for the exponentially small E1 sum itself
+    (the exponential's Taylor terms (rho x0)^k / k!), but absolutely below e^{-x0 (1 - rho)}"""
+    import math
+    import mpmath as mp
+    rho_max, kmax = _constexpr("MRHO"), int(_constexpr("MKB"))
+    rng = np.random.default_rng(1811)
+    worst = 0.0
+    for rho in (0.05, 0.2, 0.35, rho_max):
+        K = min(kmax, max(3, math.ceil(math.log(1e-16) / math.log(rho))))
+        for x0 in (4.0 / (1.0 + rho), 3.5, 8.0, 40.0, _constexpr("MXZ") / (1.0 - rho)):
+            c0, u = 1.0, x0
+            c = c0 * (1.0 + rho * rng.uniform(-1.0, 1.0, 24))
+            c[0], c[1] = c0 * (1 - rho), c0 * (1 + rho)
+            W = rng.uniform(-1.0, 1.0, 24)
+            m = [float(np.sum(W * (c - c0) ** k)) for k in range(K + 1)]
+            ex = math.exp(-x0)
+            e, ap, S1 = ex, ex / c0, 0.0
+            for k in range(1, K + 1):
+                e = -e * (u / k)
+                S1 += ap * m[k] / k
+                ap = (e - ap) / c0
+            got = float(mp.e1(x0)) * m[0] - S1
+            ref = float(mp.fsum(mp.mpf(w) * mp.e1(mp.mpf(ci) * u) for w, ci in zip(W, c)))
+            worst = max(worst, abs(got - ref) / float(np.sum(np.abs(W))))
+    assert worst < 1e-16, worst
