@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(128) k_records(MomArgs M) {
   const bool okB = cmin > 0.0 && (cmax - c0m) <= MRHO * c0m;
   const double c0 = okB ? c0m : 0.0;
   const double rho = okB ? (cmax - c0m) / c0m : 1.0;
-  const int kb = rho <= 1e-6 ? 3 : min(MKB, max(3, (int)ceil(log(1e-16) / log(rho))));
+  const int kb = (!okB || rho <= 1e-6) ? 3 : min(MKB, max(3, (int)ceil(log(1e-16) / log(rho))));
   rec[RF_CMAX * S] = cmax;
   rec[RF_CMIN * S] = cmin;
   rec[RF_C0 * S] = c0;
@@ -317,13 +317,36 @@ __global__ void __launch_bounds__(128) k_records(MomArgs M) {
         }
       });
     }
+    // regime-B polynomial coefficients: every Taylor sum of phi_bz is
+    // e^{-x0} sum_i coef_i (-u)^i with per-pair coefficients from backward recurrences over the
+    // shifted moments (B1_k = m_k / k, B2_k = m_k / ((k-1) k)):
+    //   S1:     G_i = (B1_{i+1} - G_{i+1}) / c0,  G_kb = 0,      coef G_i / i!  -> FB1[i], i < kb
+    //   S2 (H): H_i = (B2_{i+2} - H_{i+1}) / c0,  H_{kb-1} = 0,  coef H_i / i!  -> FB2[i], i < kb
+    //   S3 (Q): Q_i = (m_i - Q_{i+1}) / c0 (i >= 1), Q_0 = -Q_1 / c0, Q_{kb+1} = 0  -> FB2[i], i <= kb
+    //   m_0 -> FB1[MKB], m_1 -> FB2[MKB] (H)
+    {
+      const double ic0 = okB ? 1.0 / c0 : 0.0;
+      double G = 0.0, H2 = 0.0, Q3 = 0.0;
 #pragma unroll
-    for (int k = 0; k <= MKB; ++k) {
-      // B1[k] = m_k / k (B1[0] = m_0); B2: H m_k / ((k-1) k) (B2[1] = m_1), Q m_k, F unused;
-      // orders above kb are never read
-      if (k > kb && k > 1) break;
-      R[(FB1 + k) * S] = k == 0 ? mb[0] : mb[k] * STB_INV_H[k];
-      R[(FB2 + k) * S] = fam == FAM_Q ? mb[k] : (fam == FAM_H ? (k == 0 ? 0.0 : (k == 1 ? mb[1] : mb[k] * STB_INV_H[k - 1] * STB_INV_H[k])) : 0.0);
+      for (int i = MKB; i >= 0; --i) {
+        if (fam == FAM_Q && i <= kb) {
+          Q3 = ((i >= 1 ? mb[i] : 0.0) - Q3) * ic0;
+          R[(FB2 + i) * S] = Q3 * STB_INVFACT[i];
+        }
+        if (i <= kb - 1) {
+          G = (mb[i + 1 <= MKB ? i + 1 : MKB] * STB_INV_H[i + 1 <= MKB ? i + 1 : MKB] - G) * ic0;
+          R[(FB1 + i) * S] = G * STB_INVFACT[i];
+          if (fam == FAM_H) {
+            if (i <= kb - 2) {
+              const int k2 = i + 2 <= MKB ? i + 2 : MKB;
+              H2 = (mb[k2] * STB_INV_H[k2 - 1] * STB_INV_H[k2] - H2) * ic0;
+            }
+            R[(FB2 + i) * S] = i <= kb - 2 ? H2 * STB_INVFACT[i] : 0.0;
+          }
+        }
+      }
+      R[(FB1 + MKB) * S] = mb[0];
+      if (fam == FAM_H) R[(FB2 + MKB) * S] = mb[1];
     }
   }
 }
@@ -427,11 +450,11 @@ struct RegBZ {
 #pragma unroll
     for (int f = 0; f < Fams<KIND>::n; ++f) {
       const double* R = rec + (RF_COMMON + f * FAMSZ) * S;
-      m0[f] = R[FB1 * S];
+      m0[f] = R[(FB1 + MKB) * S];
       C0[f] = R[FC0 * S];
       C1[f] = R[FC1 * S];
     }
-    m1 = rec[(RF_COMMON + FB2 + 1) * S];   // H: m_1 (B2[1])
+    m1 = rec[(RF_COMMON + FB2 + MKB) * S];   // H: m_1
   }
 };
 
@@ -455,26 +478,20 @@ __device__ __forceinline__ double phi_bz(const double* __restrict__ rec, long lo
     const double E1 = ex * (ic0 * s) * gb3_cb(ic0 * s);
     const double* R0 = rec + (RF_COMMON + 0 * FAMSZ) * S;
     const double* R1 = rec + (RF_COMMON + 1 * FAMSZ) * S;
-    double e = ex, ap = ex * ic0, app = 0.0;        // e^_{k-1}, a^_{k-1}, a^_{k-2}
-    const double a0 = ap;
-    double S1a = 0.0, S2a = 0.0, S1b = 0.0;
-    const double* p1 = R0 + (FB1 + 1) * S;
-    const double* p2 = R0 + (FB2 + 1) * S;
-    const double* p3 = R1 + (FB1 + 1) * S;
+    // the Taylor sums as polynomials in z = -u (coefficients from k_records), Horner from the top
+    const double zu = -u;
+    const double* p1 = R0 + FB1 * S;
+    const double* p2 = R0 + FB2 * S;
+    const double* p3 = R1 + FB1 * S;
+    double h1 = 0.0, h2 = Fams<KIND>::f0 == FAM_Q ? p2[(long long)z.kb * S] : 0.0, h3 = 0.0;
 #pragma unroll 2
-    for (int k = 1; k <= z.kb; ++k) {
-      e = -e * (u * STB_INV[k]);
-      const double ak = (e - ap) * ic0;
-      S1a = fma(ap, *p1, S1a);
-      if (Fams<KIND>::f0 == FAM_H) S2a = fma(app, *p2, S2a);
-      else S2a = fma(ak, *p2, S2a);   // Q: S3
-      if (Fams<KIND>::n == 2) S1b = fma(ap, *p3, S1b);
-      p1 += S;
-      p2 += S;
-      p3 += S;
-      app = ap;
-      ap = ak;
+    for (int i = z.kb - 1; i >= 0; --i) {
+      h1 = fma(h1, zu, p1[(long long)i * S]);
+      if (Fams<KIND>::f0 != FAM_F) h2 = fma(h2, zu, p2[(long long)i * S]);
+      if (Fams<KIND>::n == 2) h3 = fma(h3, zu, p3[(long long)i * S]);
     }
+    const double S1a = ex * h1, S2a = ex * h2, S1b = ex * h3;
+    const double a0 = ex * ic0;
     const double m0 = z.m0[0];
     if (Fams<KIND>::f0 == FAM_H) T[0] = fma(fma(1.0 + x0, E1, -ex), m0, fma(E1 * u, z.m1, -fma(u, S2a, S1a)));
     else T[0] = fma(-E1, m0, fma(a0, m0, S2a) / u + S1a);
@@ -511,41 +528,32 @@ __device__ __forceinline__ void phi_bz2(const double* __restrict__ rec, long lon
   const double E11 = ex1 * (ic0 * s1) * gb3_cb(ic0 * s1), E12 = ex2 * (ic0 * s2) * gb3_cb(ic0 * s2);
   const double* R0 = rec + (RF_COMMON + 0 * FAMSZ) * S;
   const double* R1 = rec + (RF_COMMON + 1 * FAMSZ) * S;
-  double e1 = ex1, ap1 = ex1 * ic0, app1 = 0.0, e2 = ex2, ap2 = ex2 * ic0, app2 = 0.0;
-  const double a01 = ap1, a02 = ap2;
-  double S1a1 = 0.0, S2a1 = 0.0, S1b1 = 0.0, S1a2 = 0.0, S2a2 = 0.0, S1b2 = 0.0;
-  const double* p1 = R0 + (FB1 + 1) * S;
-  const double* p2 = R0 + (FB2 + 1) * S;
-  const double* p3 = R1 + (FB1 + 1) * S;
+  // both nodes' Taylor sums as polynomials in -u (shared coefficient loads, 2 x 1-3 Horner chains)
+  const double z1 = -u1, z2 = -u2;
+  const double* p1 = R0 + FB1 * S;
+  const double* p2 = R0 + FB2 * S;
+  const double* p3 = R1 + FB1 * S;
+  const double top = Fams<KIND>::f0 == FAM_Q ? p2[(long long)z.kb * S] : 0.0;
+  double h11 = 0.0, h21 = top, h31 = 0.0, h12 = 0.0, h22 = top, h32 = 0.0;
 #pragma unroll 2
-  for (int k = 1; k <= z.kb; ++k) {
-    const double ik = STB_INV[k];
-    const double m1 = *p1, m2 = *p2;
-    e1 = -e1 * (u1 * ik);
-    e2 = -e2 * (u2 * ik);
-    const double ak1 = (e1 - ap1) * ic0, ak2 = (e2 - ap2) * ic0;
-    S1a1 = fma(ap1, m1, S1a1);
-    S1a2 = fma(ap2, m1, S1a2);
-    if (Fams<KIND>::f0 == FAM_H) {
-      S2a1 = fma(app1, m2, S2a1);
-      S2a2 = fma(app2, m2, S2a2);
-    } else {
-      S2a1 = fma(ak1, m2, S2a1);
-      S2a2 = fma(ak2, m2, S2a2);
+  for (int i = z.kb - 1; i >= 0; --i) {
+    const double c1 = p1[(long long)i * S];
+    h11 = fma(h11, z1, c1);
+    h12 = fma(h12, z2, c1);
+    if (Fams<KIND>::f0 != FAM_F) {
+      const double c2 = p2[(long long)i * S];
+      h21 = fma(h21, z1, c2);
+      h22 = fma(h22, z2, c2);
     }
     if (Fams<KIND>::n == 2) {
-      const double m3 = *p3;
-      S1b1 = fma(ap1, m3, S1b1);
-      S1b2 = fma(ap2, m3, S1b2);
+      const double c3 = p3[(long long)i * S];
+      h31 = fma(h31, z1, c3);
+      h32 = fma(h32, z2, c3);
     }
-    p1 += S;
-    p2 += S;
-    p3 += S;
-    app1 = ap1;
-    ap1 = ak1;
-    app2 = ap2;
-    ap2 = ak2;
   }
+  const double S1a1 = ex1 * h11, S2a1 = ex1 * h21, S1b1 = ex1 * h31;
+  const double S1a2 = ex2 * h12, S2a2 = ex2 * h22, S1b2 = ex2 * h32;
+  const double a01 = ex1 * ic0, a02 = ex2 * ic0;
   const double m0 = z.m0[0];
   double T1[2], T2[2];
   if (Fams<KIND>::f0 == FAM_H) {

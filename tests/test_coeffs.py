@@ -79,34 +79,73 @@ def test_moment_polynomials(name):
     assert err.max() < 2e-15, err.max()
 
 
-def test_regime_b_taylor_truncation():
-    """regime B restated (scaled recurrence of the Taylor coefficients of e^{-x}/x about x0, order
-    K = ceil(ln 1e-16 / ln rho) capped at MKB) for the F family, against mpmath E1 point sums, over
-    the whole regime: rho up to MRHO, x0 from 4 / (1 + rho) up to x_min = MXZ (regime Z beyond).
-    The error is measured against sum |W| -- the scale of the node values Phi~ (the affine constants
+def _regime_b_poly(W, c, c0, u, K, fam):
+    """regime B as the kernels evaluate it (k_records + phi_bz): Taylor sums about c0 written as
+    e^{-x0} times polynomials in -u whose coefficients follow from backward recurrences over the
+    shifted moments m_k = sum W (c - c0)^k"""
+    import math
+    import mpmath as mp
+    x0 = c0 * u
+    ex, E1 = math.exp(-x0), float(mp.e1(x0))
+    m = [float(np.sum(W * (c - c0) ** k)) for k in range(K + 1)]
+
+    def horner(co, z):
+        r = 0.0
+        for v in reversed(co):
+            r = r * z + v
+        return r
+
+    G = [0.0] * (K + 1)                                    # S1: B1_k = m_k / k
+    for i in range(K - 1, -1, -1):
+        G[i] = (m[i + 1] / (i + 1) - G[i + 1]) / c0
+    S1 = ex * horner([G[i] / math.factorial(i) for i in range(K)], -u)
+    if fam == "F":                                         # sum W E1(c u)
+        return E1 * m[0] - S1
+    if fam == "H":                                         # sum W [(1 + x) E1(x) - e^{-x}]
+        H = [0.0] * (K + 1)
+        for i in range(K - 2, -1, -1):
+            H[i] = (m[i + 2] / ((i + 1) * (i + 2)) - H[i + 1]) / c0
+        S2 = ex * horner([H[i] / math.factorial(i) for i in range(K - 1)], -u)
+        return ((1 + x0) * E1 - ex) * m[0] + E1 * u * m[1] - S1 - u * S2
+    Q = [0.0] * (K + 2)                                    # sum W [e^{-x}/x - E1(x)]
+    for i in range(K, 0, -1):
+        Q[i] = (m[i] - Q[i + 1]) / c0
+    Q[0] = -Q[1] / c0
+    S3 = ex * horner([Q[i] / math.factorial(i) for i in range(K + 1)], -u)
+    return -E1 * m[0] + (ex / c0 * m[0] + S3) / u + S1
+
+
+@pytest.mark.parametrize("fam", ["F", "H", "Q"])
+def test_regime_b_taylor_truncation(fam):
+    """regime B restated (order K = ceil(ln 1e-16 / ln rho) capped at MKB) for the three kernel
+    families against mpmath point sums, over the whole regime: rho up to MRHO, x0 from
+    4 / (1 + rho) up to x_min = MXZ (regime Z beyond), cluster centres 1e-3 .. 30.  The error is
+    measured against sum |W| -- the scale of the node values Phi~ (the affine constants
     sum W (gamma + ln c) are of that size) whose second differences are the entries: at large x0
-    the truncated series is relatively inaccurate for the exponentially small E1 sum itself
+    the truncated series is relatively inaccurate for the exponentially small sums themselves
     (the exponential's Taylor terms (rho x0)^k / k!), but absolutely below e^{-x0 (1 - rho)}"""
     import math
     import mpmath as mp
-    rho_max, kmax = _constexpr("MRHO"), int(_constexpr("MKB"))
+    rho_max, kmax, mxz = _constexpr("MRHO"), int(_constexpr("MKB")), _constexpr("MXZ")
     rng = np.random.default_rng(1811)
+
+    def truth(W, c, u):
+        out = mp.mpf(0)
+        for w, ci in zip(W, c):
+            x = mp.mpf(ci) * u
+            v = mp.e1(x) if fam == "F" else ((1 + x) * mp.e1(x) - mp.exp(-x) if fam == "H" else mp.exp(-x) / x - mp.e1(x))
+            out += mp.mpf(w) * v
+        return float(out)
+
     worst = 0.0
     for rho in (0.05, 0.2, 0.35, rho_max):
         K = min(kmax, max(3, math.ceil(math.log(1e-16) / math.log(rho))))
-        for x0 in (4.0 / (1.0 + rho), 3.5, 8.0, 40.0, _constexpr("MXZ") / (1.0 - rho)):
-            c0, u = 1.0, x0
-            c = c0 * (1.0 + rho * rng.uniform(-1.0, 1.0, 24))
-            c[0], c[1] = c0 * (1 - rho), c0 * (1 + rho)
-            W = rng.uniform(-1.0, 1.0, 24)
-            m = [float(np.sum(W * (c - c0) ** k)) for k in range(K + 1)]
-            ex = math.exp(-x0)
-            e, ap, S1 = ex, ex / c0, 0.0
-            for k in range(1, K + 1):
-                e = -e * (u / k)
-                S1 += ap * m[k] / k
-                ap = (e - ap) / c0
-            got = float(mp.e1(x0)) * m[0] - S1
-            ref = float(mp.fsum(mp.mpf(w) * mp.e1(mp.mpf(ci) * u) for w, ci in zip(W, c)))
-            worst = max(worst, abs(got - ref) / float(np.sum(np.abs(W))))
+        for x0 in (4.0 / (1.0 + rho), 3.5, 8.0, 40.0, mxz / (1.0 - rho)):
+            for c0 in (1e-3, 1.0, 30.0):
+                u = x0 / c0
+                c = c0 * (1.0 + rho * rng.uniform(-1.0, 1.0, 24))
+                c[0], c[1] = c0 * (1 - rho), c0 * (1 + rho)
+                W = rng.uniform(-1.0, 1.0, 24)
+                got = _regime_b_poly(W, c, c0, u, K, fam)
+                worst = max(worst, abs(got - truth(W, c, u)) / float(np.sum(np.abs(W))))
     assert worst < 1e-16, worst

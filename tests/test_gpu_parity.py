@@ -489,3 +489,38 @@ def test_ragged_tiles_and_many_slices():
         b = torch.empty(w.n, dtype=torch.float64, device="cuda")
         S.rhs_fused(m, m.assemble_M(S.MASS_PRIMAL), cuda(g), b)
         assert relmax(b.cpu().numpy(), om.rhs(om.dense("K"), g)) <= 1e-11
+
+
+def test_api_misuse_reports_errors():
+    """the C-ABI's documented error returns (include/stbem.h) surface as BemError, nothing launches
+    on bad input: wrong matrix kinds, missing or mismatched preconditioner parts, product mode on
+    V_h, out-of-range triangle indices, orders above the tables"""
+    import workloads.table1 as T
+    w = W.get("T8")
+    m = S.Mesh.from_workload(w)
+    V, K, D = m.assemble_V(), m.assemble_K(), m.assemble_D()
+    Ml, Md = m.assemble_M(S.MASS_DUAL_LUMPED), m.assemble_M(S.MASS_DUAL)
+    b = cuda(np.ones(w.n))
+    x = torch.zeros_like(b)
+    with pytest.raises(S.BemError):
+        S.solve_gmres(K, b, x)                              # first matrix must be V_h
+    with pytest.raises(S.BemError):
+        S.solve_gmres(V, b, x, precond=2)                   # D_h and M missing
+    with pytest.raises(S.BemError):
+        S.solve_gmres(V, b, x, D=D, M=Ml, precond=2)        # exact precond needs the dual mass
+    with pytest.raises(S.BemError):
+        S.solve_gmres(V, b, x, D=V, M=Md, precond=2)        # D slot holds V_h
+    rep = S.solve_gmres(V, b, x, D=D, M=Md, precond=2, rel_tol=1e-10)
+    assert rep["status"] == "OK"
+    wt = T.table1(2)
+    mt = S.Mesh.from_workload(wt)
+    nodes, tris = T.triangulation(wt)
+    u0 = cuda(T.initial_nodes(wt))
+    bt = torch.zeros(wt.n, dtype=torch.float64, device="cuda")
+    bad = tris.copy()
+    bad[0, 0] = len(nodes)
+    with pytest.raises(S.BemError):
+        S.rhs_initial(mt, nodes, bad, u0, bt)
+    with pytest.raises(S.BemError):
+        S.rhs_initial(mt, nodes, tris, u0, bt, qx=40)
+    assert float(bt.abs().max()) == 0.0                     # nothing was written
