@@ -136,7 +136,11 @@ long long bem_launch_count(int reset);
 /* ----------------------------------------------------------- multi-GPU (NCCL) */
 /* rank 0 creates the 128-byte NCCL unique id; the caller broadcasts it (torch.distributed). */
 bem_status bem_nccl_get_unique_id(void* out128_host);
-/* collective over nranks: one rank per GPU; cuda_device is this rank's device ordinal. */
+/* collective over nranks: one rank per GPU; cuda_device is this rank's device ordinal.  A mesh
+ * created with a communicator runs the distributed code path (owned blocks of the cyclic plan,
+ * partial products summed by ncclAllReduce on the caller's stream) -- also for nranks = 1, where
+ * the all-reduce runs on a real one-rank communicator; a mesh without one never calls NCCL.
+ * Errors: BEM_E_INVALID (arguments), BEM_E_NCCL (libnccl.so.2 not loadable or NCCL failure). */
 bem_status bem_comm_create(const void* unique_id128_host, int nranks, int rank, int cuda_device,
                            bem_comm** out);
 void bem_comm_destroy(bem_comm* comm);

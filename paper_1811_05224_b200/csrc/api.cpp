@@ -304,7 +304,7 @@ bem_status bem_rhs_fused(const bem_mesh* m, const bem_quad_opts* o, const bem_ma
     for (int a = m->blocks[bi].a0; a < m->blocks[bi].a1; ++a) A->poff.push_back(0);
   }
   bem_status st = launch_assembly(STB_K, m, A, q_bulk, q_sing, flags, S(s), g, b);
-  if (st == BEM_OK && m->nranks > 1) st = allreduce_sum(m, b, (long long)m->ng * m->nt, S(s));
+  if (st == BEM_OK && m->comm) st = allreduce_sum(m, b, (long long)m->ng * m->nt, S(s));
   if (st == BEM_OK) st = mass_apply(Mp, 0.5, g, 1.0, b, S(s));
   if (st == BEM_OK && stats) st = bem_matrix_stats(A, stats);
   bem_matrix_destroy(A);

@@ -51,7 +51,7 @@ bem_status nccl_fail(ncclResult_t r, const char* where) {
 
 namespace stb {
 bem_status allreduce_sum(const bem_mesh* m, double* buf, long long n, cudaStream_t st) {
-  if (!m->comm || m->comm->nranks == 1) return BEM_OK;
+  if (!m->comm) return BEM_OK;
   if (!nccl()) return BEM_E_NCCL;
   ncclResult_t r = g_nccl.AllReduce(buf, buf, (size_t)n, ncclDouble, ncclSum, (ncclComm_t)m->comm->nccl, st);
   if (r != ncclSuccess) return nccl_fail(r, "ncclAllReduce");
@@ -81,7 +81,7 @@ bem_status bem_comm_create(const void* id128, int nranks, int rank, int cuda_dev
   c->nranks = nranks;
   c->rank = rank;
   c->device = cuda_device;
-  if (nranks > 1) {
+  {   // also for one rank: the distributed code path then runs on a real (1-rank) communicator
     if (!nccl()) { delete c; return BEM_E_NCCL; }
     ncclUniqueId id;
     std::memcpy(&id, id128, sizeof(id));

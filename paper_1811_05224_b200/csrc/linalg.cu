@@ -235,7 +235,7 @@ bem_status gemv_setup(bem_matrix* A) {
   if ((e = cudaMallocAsync((void**)&A->d_row_pstride, sizeof(int) * nt, st)) != cudaSuccess) return cuda_fail(e, "gemv_setup");
   if ((e = cudaMemcpyAsync(A->d_row_pbase, A->row_pbase.data(), sizeof(long long) * nt, cudaMemcpyHostToDevice, st)) != cudaSuccess) return cuda_fail(e, "gemv_setup");
   if ((e = cudaMemcpyAsync(A->d_row_pstride, A->row_pstride.data(), sizeof(int) * nt, cudaMemcpyHostToDevice, st)) != cudaSuccess) return cuda_fail(e, "gemv_setup");
-  if (m->nranks > 1) {
+  if (m->comm) {   // distributed mode (any communicator, also one rank)
     if ((e = cudaMallocAsync((void**)&A->d_ysum, sizeof(double) * (size_t)ng * nt, st)) != cudaSuccess) return cuda_fail(e, "gemv_setup");
   }
   return BEM_OK;
@@ -280,7 +280,7 @@ bem_status gemv_launch(const bem_matrix* A, double a, const double* x, double b,
     k_gemv<GEMV_UNROLL><<<(unsigned)blocks, GEMV_WARPS * 32, 0, st>>>(A->data, A->d_segs, (int)A->segs.size(), A->n_items, m->ng, x, A->d_partials, gemv_ch());
     count_launch();
   }
-  if (m->nranks > 1) {
+  if (m->comm) {   // distributed mode (any communicator, also one rank)
     // partial y over the owned blocks, summed over ranks (NCCL all-reduce = reduce-scatter +
     // all-gather), then y = a * ysum + b * y
     k_gemv_reduce<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(A->d_partials, A->d_row_pbase, A->d_row_pstride, m->ng, m->nt, 1.0, 0.0, A->d_ysum);

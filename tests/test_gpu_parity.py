@@ -524,3 +524,34 @@ def test_api_misuse_reports_errors():
     with pytest.raises(S.BemError):
         S.rhs_initial(mt, nodes, tris, u0, bt, qx=40)
     assert float(bt.abs().max()) == 0.0                     # nothing was written
+
+
+def test_distributed_path_on_a_one_rank_nccl_communicator():
+    """the multi-GPU code path (owned blocks, partial products + ncclAllReduce on the stream,
+    all-reduced fused RHS) on a real one-rank NCCL communicator against the plain path: same
+    matrices, products, RHS and GMRES solution (one GPU: no ranks waiting on each other)"""
+    import ctypes
+    uid = ctypes.create_string_buffer(128)
+    S.check(S.lib().bem_nccl_get_unique_id(uid))
+    comm = S.Comm(0, 1, 0, unique_id=bytes(uid.raw))
+    w = W.get("C1")
+    out = []
+    for cm in (comm, None):
+        m = S.Mesh.from_workload(w, n_slices=2, comm=cm)
+        V, D = m.assemble_V(), m.assemble_D()
+        Mp, Md = m.assemble_M(S.MASS_PRIMAL), m.assemble_M(S.MASS_DUAL)
+        g = cuda(W.dirichlet_data(w))
+        b = torch.empty_like(g)
+        S.rhs_fused(m, Mp, g, b)
+        x = cuda(W.random_vector(w.n))
+        y = torch.empty_like(x)
+        V.matvec(x, y)
+        wv = torch.zeros_like(g)
+        rep = S.solve_gmres(V, b, wv, D=D, M=Md, precond=2, rel_tol=1e-10)
+        assert rep["status"] == "OK"
+        out.append((b.cpu().numpy(), y.cpu().numpy(), wv.cpu().numpy(), V.dense()))
+    comm.close()
+    (b1, y1, w1, V1), (b0, y0, w0, V0) = out
+    assert np.array_equal(V1, V0)
+    assert relmax(y1, y0) <= 1e-14 and relmax(b1, b0) <= 1e-14
+    assert relmax(w1, w0) <= 1e-12
