@@ -658,7 +658,7 @@ void bem_matrix_destroy(bem_matrix* A) {
   if (A->data) storage_release(A->mesh ? A->mesh->device : 0, A->data, A->data_bytes, st);
   storage_release(A->mesh ? A->mesh->device : 0, A->d_partials, A->partials_bytes, st);
   for (void* p : {(void*)A->d_segs, (void*)A->d_row_pbase,
-                  (void*)A->d_row_pstride, (void*)A->d_ysum, (void*)A->d_lo, (void*)A->d_di,
+                  (void*)A->d_row_pstride, (void*)A->d_ysum, (void*)A->d_rowcnt, (void*)A->d_lo, (void*)A->d_di,
                   (void*)A->d_up, (void*)A->d_work, (void*)A->d_ctr})
     if (p) cudaFreeAsync(p, st);
   for (auto x : A->ev) cudaEventDestroy(x);

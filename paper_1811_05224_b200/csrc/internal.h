@@ -143,6 +143,8 @@ struct bem_matrix_s {
   double* d_partials = nullptr;
   size_t partials_bytes = 0;
   double* d_ysum = nullptr;  // multi-GPU partial y
+  int* d_rowcnt = nullptr;   // SYMV: finished blocks per row (last block reduces; self-resetting)
+  bool empty_rows = false;   // some test step owns no block here (multi-GPU): y = b y there
   // mass matrices: three cyclic diagonals per row (lower = col i-1, diag, upper = col i+1)
   int mass_kind = -1;
   double* d_lo = nullptr;

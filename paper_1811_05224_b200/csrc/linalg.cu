@@ -98,11 +98,20 @@ __device__ __forceinline__ double reduce_scatter32(double (&v)[32], int lane) {
 // each warp accumulates into its own shared-memory copy of y_a, summed in fixed order into one
 // partial per (row, b) (deterministic).  Every stored double is read once from HBM.
 constexpr int SYMV_WARPS = 4;
+// The row reduction is fused: the partials of block (a, b) go to partial[rpbase[a] + b' ng + i]
+// (b' = the block's index in its row); the CTA that completes a row (device-scope counter per row,
+// reset by it) sums the row's partials in b' order -- fixed, so the result is deterministic -- and
+// writes y_a = alpha sum + beta y_a.
 __global__ void __launch_bounds__(SYMV_WARPS * 32) k_gemv_sym(const double* __restrict__ A,
                                                              const GSeg* __restrict__ segs, int nseg,
                                                              long long n_items, int ng, long long blk,
                                                              const double* __restrict__ x,
-                                                             double* __restrict__ partial) {
+                                                             double* __restrict__ partial,
+                                                             const long long* __restrict__ rpbase,
+                                                             const int* __restrict__ rpstride,
+                                                             int* __restrict__ rowcnt, double alpha,
+                                                             double beta, double* __restrict__ y) {
+  __shared__ int s_last;
   extern __shared__ double sm[];
   const int nt = sym_nt(ng), L = nt * SYM_TS, ntp = nt * (nt + 1) / 2;
   double* xs = sm;
@@ -146,12 +155,35 @@ __global__ void __launch_bounds__(SYMV_WARPS * 32) k_gemv_sym(const double* __re
     }
     __syncthreads();
     for (int k = threadIdx.x; k < ng; k += blockDim.x) {
-      double y = 0.0;
+      double yv = 0.0;
 #pragma unroll
-      for (int ww = 0; ww < SYMV_WARPS; ++ww) y += ys[ww * L + k];
-      partial[S.pbase + (long long)k * S.pstride + bl] = y;
+      for (int ww = 0; ww < SYMV_WARPS; ++ww) yv += ys[ww * L + k];
+      partial[S.pbase + (long long)bl * ng + k] = yv;
+    }
+    __threadfence();                                   // this block's partials, device-wide
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(rowcnt + S.a, 1) == rpstride[S.a] - 1;
+    __syncthreads();
+    if (s_last) {                                      // the row is complete: reduce it
+      __threadfence();
+      const double* __restrict__ pr = partial + rpbase[S.a];
+      const int nb = rpstride[S.a];
+      for (int k = threadIdx.x; k < ng; k += blockDim.x) {
+        double sum = 0.0;
+        for (int j = 0; j < nb; ++j) sum += __ldcg(pr + (long long)j * ng + k);
+        double* yp = y + (long long)S.a * ng + k;
+        *yp = (beta == 0.0) ? alpha * sum : fma(alpha, sum, beta * *yp);
+      }
+      if (threadIdx.x == 0) rowcnt[S.a] = 0;
     }
   }
+}
+
+// rows without any owned block (multi-GPU): y = beta y (the fused SYMV reduction never visits them)
+__global__ void k_empty_rows(const int* __restrict__ pstride, int ng, int nt, double beta, double* __restrict__ y) {
+  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= (long long)ng * nt || pstride[r / ng] != 0) return;
+  y[r] = beta == 0.0 ? 0.0 : beta * y[r];
 }
 
 // y[a*ng + i] = alpha * sum_k partial[row_pbase[a] + i*stride + k] + beta * y
@@ -194,6 +226,8 @@ bem_status gemv_setup(bem_matrix* A) {
     pb += (long long)st * ng;
   }
   A->n_partials = pb;
+  A->empty_rows = false;
+  for (int a = 0; a < nt; ++a) A->empty_rows |= A->row_pstride[a] == 0;
   // segments in memory order (block, a)
   A->segs.clear();
   long long item = 0;
@@ -214,7 +248,8 @@ bem_status gemv_setup(bem_matrix* A) {
       s.ld = pad4(len);
       s.len = len;
       s.xoff = (long long)b.b0 * ng;
-      s.pbase = A->row_pbase[a] + cbase;
+      // full storage: partial[pbase + i * pstride + chunk]; sym: partial[pbase + b * ng + i]
+      s.pbase = A->row_pbase[a] + (A->sym ? (long long)cbase * ng : cbase);
       s.nch = nch;
       s.pstride = A->row_pstride[a];
       s.a = a;
@@ -237,6 +272,10 @@ bem_status gemv_setup(bem_matrix* A) {
   if ((e = cudaMemcpyAsync(A->d_row_pstride, A->row_pstride.data(), sizeof(int) * nt, cudaMemcpyHostToDevice, st)) != cudaSuccess) return cuda_fail(e, "gemv_setup");
   if (m->comm) {   // distributed mode (any communicator, also one rank)
     if ((e = cudaMallocAsync((void**)&A->d_ysum, sizeof(double) * (size_t)ng * nt, st)) != cudaSuccess) return cuda_fail(e, "gemv_setup");
+  }
+  if (A->sym) {
+    if ((e = cudaMallocAsync((void**)&A->d_rowcnt, sizeof(int) * nt, st)) != cudaSuccess ||
+        (e = cudaMemsetAsync(A->d_rowcnt, 0, sizeof(int) * nt, st)) != cudaSuccess) return cuda_fail(e, "gemv_setup");
   }
   return BEM_OK;
 }
@@ -272,8 +311,23 @@ bem_status gemv_launch(const bem_matrix* A, double a, const double* x, double b,
   if (A->n_items > 0 && A->sym) {
     const size_t smem = sizeof(double) * (1 + SYMV_WARPS) * sym_nt(m->ng) * SYM_TS;
     const long long blocks = std::min<long long>(A->n_items, 1LL << 30);
-    k_gemv_sym<<<(unsigned)blocks, SYMV_WARPS * 32, smem, st>>>(A->data, A->d_segs, (int)A->segs.size(), A->n_items, m->ng, A->blk_elems, x, A->d_partials);
+    // fused row reduction: into y (or the distributed partial sum ysum)
+    const bool dist = m->comm != nullptr;
+    k_gemv_sym<<<(unsigned)blocks, SYMV_WARPS * 32, smem, st>>>(A->data, A->d_segs, (int)A->segs.size(), A->n_items, m->ng, A->blk_elems, x, A->d_partials,
+                                                                A->d_row_pbase, A->d_row_pstride, A->d_rowcnt,
+                                                                dist ? 1.0 : a, dist ? 0.0 : b, dist ? A->d_ysum : y);
     count_launch();
+    if (A->empty_rows) {
+      k_empty_rows<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(A->d_row_pstride, m->ng, m->nt, dist ? 0.0 : b, dist ? A->d_ysum : y);
+      count_launch();
+    }
+    if (dist) {
+      bem_status s = allreduce_sum(m, A->d_ysum, n, st);
+      if (s != BEM_OK) return s;
+      vec_axpby(y, a, A->d_ysum, b, n, st);
+    }
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? BEM_OK : cuda_fail(e, "bem_matvec");
   } else if (A->n_items > 0) {
     long long blocks = std::min<long long>((A->n_items + GEMV_WARPS - 1) / GEMV_WARPS,
                                            (long long)num_sms() * gemv_ctas_per_sm());
