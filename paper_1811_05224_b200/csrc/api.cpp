@@ -366,16 +366,17 @@ bem_status bem_solve_gmres(const bem_matrix* V, const bem_matrix* D, const bem_m
   static double* pin_buf = nullptr;
   static size_t pin_n = 0;
   std::lock_guard<std::mutex> pin_lock(pin_mu);   // one solve at a time uses the pinned buffer
-  if (pin_n < (size_t)2 * (kmax + 2)) {
+  const size_t slot = (size_t)2 * (kmax + 2);      // one Hessenberg column copy
+  if (pin_n < 3 * slot) {                          // slots 0, 1 (alternating iterations), 2 (misc)
     if (pin_buf) cudaFreeHost(pin_buf);
     pin_buf = nullptr;
     pin_n = 0;
-    if (cudaMallocHost(&pin_buf, sizeof(double) * 2 * (kmax + 2)) != cudaSuccess) {
+    if (cudaMallocHost(&pin_buf, sizeof(double) * 3 * slot) != cudaSuccess) {
       cudaGetLastError();
       set_error("bem_solve_gmres: pinned allocation failed");
       return BEM_E_NOMEM;
     }
-    pin_n = (size_t)2 * (kmax + 2);
+    pin_n = 3 * slot;
   }
   hpin = pin_buf;
   mesh_wait(m, st);
@@ -430,12 +431,32 @@ bem_status bem_solve_gmres(const bem_matrix* V, const bem_matrix* D, const bem_m
   };
   auto norm = [&](const double* x) -> double {
     vec_dots(x, 0, 1, x, n, dh, st);
-    cudaMemcpyAsync(hpin + 2 * (kmax + 2) - 1, dh, sizeof(double), cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(hpin + 2 * slot, dh, sizeof(double), cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
-    return std::sqrt(hpin[2 * (kmax + 2) - 1]);
+    return std::sqrt(hpin[2 * slot]);
+  };
+  // one Arnoldi step k, enqueued only (no host wait): w = C V q_k, CGS2 against q_0..q_k with
+  // both coefficient passes and ||w||^2 in dh, their copy to pinned slot k % 2 + an event, and
+  // q_{k+1} = w / ||w|| scaled on the device
+  cudaEvent_t hev[2];
+  cudaEventCreateWithFlags(&hev[0], cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&hev[1], cudaEventDisableTiming);
+  auto enqueue_step = [&](int k) -> bem_status {
+    double* qk = Q + (long long)k * n;
+    bem_status s1 = apply_V(qk, tmp);
+    if (s1 == BEM_OK) s1 = apply_C(tmp, wk);
+    if (s1 != BEM_OK) return s1;
+    vec_dots(Q, n, k + 1, wk, n, dh, st);
+    vec_update(wk, Q, n, k + 1, dh, n, st);
+    vec_dots(Q, n, k + 1, wk, n, dh + (k + 1), st);
+    vec_update(wk, Q, n, k + 1, dh + (k + 1), n, st);
+    vec_dots(wk, 0, 1, wk, n, dh + 2 * (k + 1), st);
+    cudaMemcpyAsync(hpin + (k & 1) * slot, dh, sizeof(double) * (2 * k + 3), cudaMemcpyDeviceToHost, st);
+    cudaEventRecord(hev[k & 1], st);
+    if (k + 1 <= kmax) vec_scale_rnorm(Q + (long long)(k + 1) * n, wk, dh + 2 * (k + 1), n, st);
+    return BEM_OK;
   };
   std::vector<double> H((size_t)(kmax + 1) * kmax, 0.0), cs(kmax), sn(kmax), g(kmax + 1, 0.0);
-  double* hcol = hpin;
   int iters = 0;
   bool converged = false, breakdown = false;
   double resid = 1.0;
@@ -449,24 +470,25 @@ bem_status bem_solve_gmres(const bem_matrix* V, const bem_matrix* D, const bem_m
   } else if (status == BEM_OK) {
     vec_scale(Q, Q, 1.0 / beta, n, st);
     g[0] = beta;
-    for (int k = 0; k < kmax; ++k) {
-      double* qk = Q + (long long)k * n;
-      if ((status = apply_V(qk, tmp)) != BEM_OK) break;
-      if ((status = apply_C(tmp, wk)) != BEM_OK) break;
-      // classical Gram-Schmidt with one re-orthogonalisation (CGS2); both coefficient passes and
-      // ||w||^2 land contiguously in dh and come back in one copy (one host sync per iteration)
-      vec_dots(Q, n, k + 1, wk, n, dh, st);
-      vec_update(wk, Q, n, k + 1, dh, n, st);
-      vec_dots(Q, n, k + 1, wk, n, dh + (k + 1), st);
-      vec_update(wk, Q, n, k + 1, dh + (k + 1), n, st);
-      vec_dots(wk, 0, 1, wk, n, dh + 2 * (k + 1), st);
-      cudaMemcpyAsync(hcol, dh, sizeof(double) * (2 * k + 3), cudaMemcpyDeviceToHost, st);
-      cudaStreamSynchronize(st);
+    // Pipelined Arnoldi: step k + 1 is enqueued before the host waits for step k's Hessenberg
+    // column (its vector q_{k+1} is scaled on the device), so the GPU never idles across the host's
+    // Givens update -- unless the residual trend predicts that step k converges, in which case
+    // the speculative step (one V and one D product) would be wasted and is not enqueued.
+    int enq = -1;                                    // last enqueued step
+    double r_prev = 1.0, r_prev2 = 1.0;
+    if ((status = enqueue_step(0)) == BEM_OK) enq = 0;
+    for (int k = 0; k < kmax && status == BEM_OK; ++k) {
+      const double pred = k >= 2 ? r_prev * (r_prev / r_prev2) : 1.0;
+      if (enq == k && k + 1 < kmax && pred > 2.0 * opts->rel_tol) {
+        if ((status = enqueue_step(k + 1)) != BEM_OK) break;
+        enq = k + 1;
+      }
+      cudaEventSynchronize(hev[k & 1]);
+      const double* hcol = hpin + (k & 1) * slot;
       const double hk1 = std::sqrt(hcol[2 * k + 2]);
       double* Hk = &H[(size_t)k * (kmax + 1)];
       for (int j = 0; j <= k; ++j) Hk[j] = hcol[j] + hcol[(k + 1) + j];
       Hk[k + 1] = hk1;
-      if (hk1 > 1e-300) vec_scale(Q + (long long)(k + 1) * n, wk, 1.0 / hk1, n, st);
       for (int j = 0; j < k; ++j) {
         double t1 = cs[j] * Hk[j] + sn[j] * Hk[j + 1];
         Hk[j + 1] = -sn[j] * Hk[j] + cs[j] * Hk[j + 1];
@@ -484,6 +506,12 @@ bem_status bem_solve_gmres(const bem_matrix* V, const bem_matrix* D, const bem_m
       if (hist) hist[k + 1] = resid;
       if (resid <= opts->rel_tol) { converged = true; break; }
       if (hk1 <= 1e-300) { breakdown = true; break; }
+      r_prev2 = r_prev;
+      r_prev = resid;
+      if (enq == k && k + 1 < kmax) {               // not speculated: enqueue the next step now
+        if ((status = enqueue_step(k + 1)) != BEM_OK) break;
+        enq = k + 1;
+      }
     }
     if (status == BEM_OK && iters > 0) {
       std::vector<double> y(iters);
@@ -492,8 +520,10 @@ bem_status bem_solve_gmres(const bem_matrix* V, const bem_matrix* D, const bem_m
         for (int j = i + 1; j < iters; ++j) s -= H[(size_t)j * (kmax + 1) + i] * y[j];
         y[i] = s / H[(size_t)i * (kmax + 1) + i];
       }
-      for (int i = 0; i < iters; ++i) hpin[i] = y[i];
-      cudaMemcpyAsync(dh, hpin, sizeof(double) * iters, cudaMemcpyHostToDevice, st);
+      // slot 2: a speculative step may still be copying its column into slot 0 or 1
+      double* ypin = hpin + 2 * slot;
+      for (int i = 0; i < iters; ++i) ypin[i] = y[i];
+      cudaMemcpyAsync(dh, ypin, sizeof(double) * iters, cudaMemcpyHostToDevice, st);
       vec_combine(w, Q, n, iters, dh, n, st);
     }
   }
@@ -522,6 +552,7 @@ bem_status bem_solve_gmres(const bem_matrix* V, const bem_matrix* D, const bem_m
   cudaFreeAsync(wk, st); cudaFreeAsync(dh, st);
   cudaStreamSynchronize(st);
   cudaEventDestroy(e0); cudaEventDestroy(e1);
+  cudaEventDestroy(hev[0]); cudaEventDestroy(hev[1]);
   if (e != cudaSuccess) return cuda_fail(e, "bem_solve_gmres");
   if (rep) {
     rep->iterations = iters;

@@ -217,6 +217,7 @@ void vec_dots(const double* Q, long long ldq, int k, const double* w, long long 
 void vec_update(double* w, const double* Q, long long ldq, int k, const double* h, long long n,
                 cudaStream_t st);
 void vec_scale(double* y, const double* x, double s, long long n, cudaStream_t st);
+void vec_scale_rnorm(double* y, const double* x, const double* nrm2_dev, long long n, cudaStream_t st);
 void vec_axpby(double* y, double a, const double* x, double b, long long n, cudaStream_t st);
 void vec_combine(double* out, const double* Q, long long ldq, int k, const double* coef,
                  long long n, cudaStream_t st);

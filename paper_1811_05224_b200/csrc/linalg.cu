@@ -751,6 +751,18 @@ void vec_scale(double* y, const double* x, double s, long long n, cudaStream_t s
   k_scale<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(y, x, s, n);
   count_launch();
 }
+// y = x / sqrt(*nrm2) (the next Arnoldi vector, scaled on the device so that the host need not
+// read the norm first); left untouched on breakdown (sqrt(*nrm2) <= 1e-300)
+__global__ void k_scale_rnorm(double* __restrict__ y, const double* __restrict__ x, const double* __restrict__ nrm2,
+                              long long n) {
+  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const double h = sqrt(*nrm2);
+  if (r < n && h > 1e-300) y[r] = (1.0 / h) * x[r];
+}
+void vec_scale_rnorm(double* y, const double* x, const double* nrm2_dev, long long n, cudaStream_t st) {
+  k_scale_rnorm<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(y, x, nrm2_dev, n);
+  count_launch();
+}
 __global__ void k_axpby(double* __restrict__ y, double a, const double* __restrict__ x, double b, long long n) {
   const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (r < n) y[r] = (b == 0.0) ? a * x[r] : fma(a, x[r], b * y[r]);
