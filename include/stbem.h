@@ -168,7 +168,10 @@ bem_status bem_mesh_info_get(const bem_mesh* mesh, bem_mesh_info* info);
 void bem_mesh_destroy(bem_mesh* mesh);
 
 /* ------------------------------------------------------------ assembly */
-/* V_h[(a,i),(b,j)] = <V phi^0_(b,j), phi^0_(a,i)> with (1/alpha) U* (P:43).
+/* All three need N_Gamma >= 6 (the touching-pair enumeration of the dual half segments assumes
+ * distinct neighbours); smaller boundaries return BEM_E_INVALID.  Any kappa = alpha h^2 /
+ * (4 min h_t): above 1 the elements are integrated with composite rules (reading R24).
+ * V_h[(a,i),(b,j)] = <V phi^0_(b,j), phi^0_(a,i)> with (1/alpha) U* (P:43).
  * Stored entries: owned blocks, b <= a, packed row panels. */
 bem_status bem_assemble_V(const bem_mesh* mesh, const bem_quad_opts* opts, bem_stream stream,
                           bem_matrix** out);

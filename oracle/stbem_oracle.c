@@ -248,6 +248,7 @@ typedef struct {
   ora_seg* seg;            /* ng primal segments */
   ora_seg* half;           /* 2 ng half segments: 2i=[x_i,m_i], 2i+1=[m_i,x_{i+1}] */
   int q_far, q_near, q_sing, q_log;
+  double ell;              /* sqrt(4 min h_t / alpha) (reading R24) */
 } ora_mesh;
 
 static ora_seg make_seg(double ax, double ay, double bx, double by) {
@@ -297,6 +298,9 @@ ora_mesh* ora_mesh_new(int nv, const double* vxy, const int* segs_per_side, int 
   }
   free(nodes);
   m->q_far = 10; m->q_near = 16; m->q_sing = 16; m->q_log = 8;
+  double htmin = t[1] - t[0];
+  for (int a = 1; a < nt; ++a) if (t[a + 1] - t[a] < htmin) htmin = t[a + 1] - t[a];
+  m->ell = sqrt(4.0 * htmin / alpha);
   return m;
 }
 
@@ -330,25 +334,36 @@ typedef struct { double sx0, sx1, sy0, sy1; } ora_shape;
 
 static double lin(double v0, double v1, double f) { return v0 + (v1 - v0) * f; }
 
+/* Composite rules (reading R24): U* varies on the length ell = sqrt(4 min h_t / alpha)
+ * at the smallest lag; elements longer than ell are integrated with ns = ceil(h / ell) equal cells
+ * per direction (a Gauss rule of the given order in each cell). */
+static int ora_cells(const ora_mesh* m, const ora_seg* X, const ora_seg* Y) {
+  double hm = X->h > Y->h ? X->h : Y->h;
+  if (!(m->ell > 0.0) || hm <= m->ell) return 1;
+  int ns = (int)ceil(hm / m->ell);
+  return ns > 24 ? 24 : ns;
+}
+
 static double pair_disjoint(const ora_mesh* m, int ker, const ora_lags* L, const ora_seg* X,
                             const ora_seg* Y, const ora_shape* sh, int q) {
   const ora_rule* R = &RULES[q];
+  const int ns = ora_cells(m, X, Y);
   double acc = 0.0;
-  for (int p = 0; p < q; ++p) {
-    double fu = R->x[p];
+  for (int p = 0; p < q * ns; ++p) {
+    double fu = (p / q + R->x[p % q]) / ns, wu = R->w[p % q] / ns;
     double x0 = X->ax + fu * (X->bx - X->ax), x1 = X->ay + fu * (X->by - X->ay);
     double su = lin(sh->sx0, sh->sx1, fu);
     double inner = 0.0;
-    for (int r = 0; r < q; ++r) {
-      double fv = R->x[r];
+    for (int r = 0; r < q * ns; ++r) {
+      double fv = (r / q + R->x[r % q]) / ns, wv = R->w[r % q] / ns;
       double y0 = Y->ax + fv * (Y->bx - Y->ax), y1 = Y->ay + fv * (Y->by - Y->ay);
       double dx = x0 - y0, dy = x1 - y1;
       double c = m->alpha * (dx * dx + dy * dy) / 4.0;
       double k = ker_direct(ker, L, m->alpha, c);
       if (ker == KER_Q) k *= dx * Y->nx + dy * Y->ny;
-      inner += R->w[r] * lin(sh->sy0, sh->sy1, fv) * k;
+      inner += wv * lin(sh->sy0, sh->sy1, fv) * k;
     }
-    acc += R->w[p] * su * inner;
+    acc += wu * su * inner;
   }
   return acc * X->h * Y->h;
 }
@@ -364,22 +379,14 @@ static double pair_identical(const ora_mesh* m, int ker, const ora_lags* L, cons
   /* G(w) = int_0^{h-w} [Sx(v+w) Sy(v) + Sx(v) Sy(v+w)] dv, shapes in arc length */
 #define SHX(u) lin(sh->sx0, sh->sx1, (u) / h)
 #define SHY(u) lin(sh->sy0, sh->sy1, (u) / h)
-  double acc_reg = 0.0, acc_log = 0.0;
-  for (int p = 0; p < Rr->n; ++p) {
-    double w = h * Rr->x[p], len = h - w, G = 0.0;
-    for (int r = 0; r < Rv->n; ++r) {
-      double v = len * Rv->x[r];
-      G += Rv->w[r] * (SHX(v + w) * SHY(v) + SHX(v) * SHY(v + w));
-    }
-    G *= len;
-    double c = alpha * w * w / 4.0, Rk, Pk;
-    ker_split(ker, L, alpha, c, &Rk, &Pk);
-    acc_reg += Rr->w[p] * G * (Rk + Pk * (log(alpha / 4.0) + 2.0 * log(h)));
-  }
-  /* 2 int_0^1 P(c(h rho)) G(h rho) ln rho d rho = -2 int int P G (h rho tau) */
-  for (int p = 0; p < Rl->n; ++p)
-    for (int q = 0; q < Rl->n; ++q) {
-      double w = h * Rl->x[p] * Rl->x[q], len = h - w, G = 0.0;
+  /* composite in rho = w / h (R24): cell 0 = [0, 1/ns] with the split treatment below (rho = t/ns,
+   * ln rho = ln t - ln ns), cells k >= 1 by plain Gauss with ln c evaluated */
+  const int ns = ora_cells(m, X, X);
+  const double lns = log((double)ns);
+  double acc_reg = 0.0, acc_log = 0.0, acc_out = 0.0;
+  for (int cell = 1; cell < ns; ++cell)
+    for (int p = 0; p < Rr->n; ++p) {
+      double w = h * (cell + Rr->x[p]) / ns, len = h - w, G = 0.0;
       for (int r = 0; r < Rv->n; ++r) {
         double v = len * Rv->x[r];
         G += Rv->w[r] * (SHX(v + w) * SHY(v) + SHX(v) * SHY(v + w));
@@ -387,11 +394,35 @@ static double pair_identical(const ora_mesh* m, int ker, const ora_lags* L, cons
       G *= len;
       double c = alpha * w * w / 4.0, Rk, Pk;
       ker_split(ker, L, alpha, c, &Rk, &Pk);
-      acc_log += Rl->w[p] * Rl->w[q] * Pk * G;
+      acc_out += Rr->w[p] / ns * G * (Rk + Pk * log(c));
+    }
+  for (int p = 0; p < Rr->n; ++p) {
+    double w = h * Rr->x[p] / ns, len = h - w, G = 0.0;
+    for (int r = 0; r < Rv->n; ++r) {
+      double v = len * Rv->x[r];
+      G += Rv->w[r] * (SHX(v + w) * SHY(v) + SHX(v) * SHY(v + w));
+    }
+    G *= len;
+    double c = alpha * w * w / 4.0, Rk, Pk;
+    ker_split(ker, L, alpha, c, &Rk, &Pk);
+    acc_reg += Rr->w[p] / ns * G * (Rk + Pk * (log(alpha / 4.0) + 2.0 * log(h) - 2.0 * lns));
+  }
+  /* 2 int_0^1 P(c(h t/ns)) G(h t/ns) ln t dt / ns = -2 int int P G (h t tau / ns) / ns */
+  for (int p = 0; p < Rl->n; ++p)
+    for (int q = 0; q < Rl->n; ++q) {
+      double w = h * Rl->x[p] * Rl->x[q] / ns, len = h - w, G = 0.0;
+      for (int r = 0; r < Rv->n; ++r) {
+        double v = len * Rv->x[r];
+        G += Rv->w[r] * (SHX(v + w) * SHY(v) + SHX(v) * SHY(v + w));
+      }
+      G *= len;
+      double c = alpha * w * w / 4.0, Rk, Pk;
+      ker_split(ker, L, alpha, c, &Rk, &Pk);
+      acc_log += Rl->w[p] * Rl->w[q] / ns * Pk * G;
     }
 #undef SHX
 #undef SHY
-  return h * (acc_reg - 2.0 * acc_log);
+  return h * (acc_reg - 2.0 * acc_log + acc_out);
 }
 
 /* segments sharing one vertex V: x = V + u e1 (u in [0,h1]), y = V + v e2 (v in [0,h2]);
@@ -414,37 +445,52 @@ static double pair_vertex(const ora_mesh* m, int ker, const ora_lags* L, const o
   if (ker == KER_Q && fabs(e1n) < 1e-14) return 0.0;   /* collinear: exactly 0 */
   const ora_rule* Rr = &RULES[m->q_sing];
   const ora_rule* Rl = &RULES[m->q_log];
+  /* composite (R24): eta by plain Gauss in ns cells; rho in ns cells, cell 0 with the split
+   * treatment (rho = t/ns), cells k >= 1 by plain Gauss with ln c evaluated */
+  const int ns = ora_cells(m, X, Y);
+  const double lns = log((double)ns);
   double total = 0.0;
   for (int tri = 0; tri < 2; ++tri) {
-    for (int ie = 0; ie < Rr->n; ++ie) {
-      double eta = Rr->x[ie];
+    for (int ie = 0; ie < Rr->n * ns; ++ie) {
+      double eta = (ie / Rr->n + Rr->x[ie % Rr->n]) / ns, weta = Rr->w[ie % Rr->n] / ns;
       /* r^2 = rho^2 A(eta) */
       double A = (tri == 0) ? (h1 * h1 + h2 * h2 * eta * eta - 2.0 * h1 * h2 * eta * cth)
                             : (h1 * h1 * eta * eta + h2 * h2 - 2.0 * h1 * h2 * eta * cth);
       double lnA = log(alpha * A / 4.0);
-      double reg = 0.0, lg = 0.0;
-      for (int ir = 0; ir < Rr->n; ++ir) {
-        double rho = Rr->x[ir];
-        double u = (tri == 0) ? h1 * rho : h1 * rho * eta;
-        double v = (tri == 0) ? h2 * rho * eta : h2 * rho;
-        double f = lin(sxV, sxF, u / h1) * lin(syV, syF, v / h2) * h1 * h2 * rho;
-        double c = alpha * rho * rho * A / 4.0, Rk, Pk;
-        ker_split(ker, L, alpha, c, &Rk, &Pk);
-        if (ker == KER_Q) f *= u * e1n;
-        reg += Rr->w[ir] * f * (Rk + Pk * lnA);
-      }
-      for (int ir = 0; ir < Rl->n; ++ir)
-        for (int it = 0; it < Rl->n; ++it) {
-          double rho = Rl->x[ir] * Rl->x[it];
+      double reg = 0.0, lg = 0.0, out = 0.0;
+      for (int cell = 1; cell < ns; ++cell)
+        for (int ir = 0; ir < Rr->n; ++ir) {
+          double rho = (cell + Rr->x[ir]) / ns;
           double u = (tri == 0) ? h1 * rho : h1 * rho * eta;
           double v = (tri == 0) ? h2 * rho * eta : h2 * rho;
           double f = lin(sxV, sxF, u / h1) * lin(syV, syF, v / h2) * h1 * h2 * rho;
           double c = alpha * rho * rho * A / 4.0, Rk, Pk;
           ker_split(ker, L, alpha, c, &Rk, &Pk);
           if (ker == KER_Q) f *= u * e1n;
-          lg += Rl->w[ir] * Rl->w[it] * f * Pk;
+          out += Rr->w[ir] / ns * f * (Rk + Pk * log(c));
         }
-      total += Rr->w[ie] * (reg - 2.0 * lg);
+      for (int ir = 0; ir < Rr->n; ++ir) {
+        double rho = Rr->x[ir] / ns;
+        double u = (tri == 0) ? h1 * rho : h1 * rho * eta;
+        double v = (tri == 0) ? h2 * rho * eta : h2 * rho;
+        double f = lin(sxV, sxF, u / h1) * lin(syV, syF, v / h2) * h1 * h2 * rho;
+        double c = alpha * rho * rho * A / 4.0, Rk, Pk;
+        ker_split(ker, L, alpha, c, &Rk, &Pk);
+        if (ker == KER_Q) f *= u * e1n;
+        reg += Rr->w[ir] / ns * f * (Rk + Pk * (lnA - 2.0 * lns));
+      }
+      for (int ir = 0; ir < Rl->n; ++ir)
+        for (int it = 0; it < Rl->n; ++it) {
+          double rho = Rl->x[ir] * Rl->x[it] / ns;
+          double u = (tri == 0) ? h1 * rho : h1 * rho * eta;
+          double v = (tri == 0) ? h2 * rho * eta : h2 * rho;
+          double f = lin(sxV, sxF, u / h1) * lin(syV, syF, v / h2) * h1 * h2 * rho;
+          double c = alpha * rho * rho * A / 4.0, Rk, Pk;
+          ker_split(ker, L, alpha, c, &Rk, &Pk);
+          if (ker == KER_Q) f *= u * e1n;
+          lg += Rl->w[ir] * Rl->w[it] / ns * f * Pk;
+        }
+      total += weta * (reg - 2.0 * lg + out);
     }
   }
   return total;

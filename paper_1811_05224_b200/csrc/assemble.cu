@@ -65,6 +65,7 @@ struct BlockArgs {
   long long pbase;
   int pslots;             // 2 * ntile + 5: bulk trial tiles, near trial tiles, touching records
   int ntile;              // ceil(ng / 32)
+  double ell;             // sqrt(4 min h_t / alpha): composite singular rules when h > ell
 };
 
 // sym: the caller guarantees i / 32 <= j / 32 (the upper tile triangle)
@@ -164,15 +165,23 @@ __device__ __forceinline__ double lin(double v0, double v1, double f) { return f
 // warp-cooperative integral over a touching pair; the result is valid in all lanes
 template <int KER>
 __device__ double pair_touching(const Seg& X, const Seg& Y, int rel, const Lags& Lg, double alpha,
-                                int n, double sx0, double sx1, double sy0, double sy1) {
+                                int n, double sx0, double sx1, double sy0, double sy1, double ell) {
   const int lane = threadIdx.x & 31;
   double acc = 0.0;
+  // composite in the radial coordinate (and in eta for vertex pairs) when the elements are longer
+  // than ell = sqrt(4 min h_t / alpha), the length on which the kernel varies at the smallest lag:
+  // cell 0 keeps the log-weighted rule (scaled: ln rho = ln t - ln ns), the other cells take plain
+  // Gauss with ln rho evaluated
+  const double hmax = fmax(X.h, Y.h);
+  const int ns = (ell > 0.0 && hmax > ell) ? min(24, (int)ceil(hmax / ell)) : 1;
+  const double ins = 1.0 / ns, lnns = log((double)ns);
   if (rel == 1) {
     if (KER == 2) return 0.0;  // dot = 0 on a straight segment
     const double h = X.h;
     const double L0 = log(0.25 * alpha) + 2.0 * log(h);
-    for (int k = lane; k < n; k += 32) {
-      const double rho = c_gx[n][k], w = h * rho, len = h - w;
+    for (int idx = lane; idx < ns * n; idx += 32) {
+      const int cell = idx / n, k = idx % n;
+      const double rho = (cell + c_gx[n][k]) * ins, w = h * rho, len = h - w;
       // G(w) = int_0^{h-w} [Sx(v+w) Sy(v) + Sx(v) Sy(v+w)] dv (quadratic integrand: 2-point Gauss)
       double G = 0.0;
       for (int r = 0; r < 2; ++r) {
@@ -184,7 +193,9 @@ __device__ double pair_touching(const Seg& X, const Seg& Y, int rel, const Lags&
       const double c = 0.25 * alpha * w * w;
       double R, P;
       split_RP<KER>(Lg, alpha, c, log(c), R, P);
-      acc += G * (c_gw[n][k] * (R + P * L0) + 2.0 * c_glw[n][k] * P);
+      const double wt = cell == 0 ? c_gw[n][k] * (R + P * (L0 - 2.0 * lnns)) + 2.0 * c_glw[n][k] * P
+                                  : c_gw[n][k] * (R + P * (L0 + 2.0 * log(rho)));
+      acc += G * ins * wt;
     }
     acc *= h;
   } else {
@@ -200,10 +211,12 @@ __device__ double pair_touching(const Seg& X, const Seg& Y, int rel, const Lags&
     const double cth = e1x * e2x + e1y * e2y;
     const double e1n = e1x * Y.nx + e1y * Y.ny;
     if (KER == 2 && fabs(e1n) < 1e-14) return 0.0;
-    const int npts = 2 * n * n;
+    const int nq = ns * n, npts = 2 * nq * nq;
     for (int idx = lane; idx < npts; idx += 32) {
-      const int tri = idx / (n * n), ie = (idx / n) % n, ir = idx % n;
-      const double eta = c_gx[n][ie], rho = c_gx[n][ir];
+      const int tri = idx / (nq * nq), ie = (idx / nq) % nq, ir = idx % nq;
+      const int rc = ir / n, rk = ir % n;
+      const double eta = (ie / n + c_gx[n][ie % n]) * ins, weta = c_gw[n][ie % n] * ins;
+      const double rho = (rc + c_gx[n][rk]) * ins;
       const double A = tri == 0 ? (h1 * h1 + h2 * h2 * eta * eta - 2.0 * h1 * h2 * eta * cth)
                                 : (h1 * h1 * eta * eta + h2 * h2 - 2.0 * h1 * h2 * eta * cth);
       const double u = tri == 0 ? h1 * rho : h1 * rho * eta;
@@ -214,7 +227,9 @@ __device__ double pair_touching(const Seg& X, const Seg& Y, int rel, const Lags&
       const double lnA = log(0.25 * alpha * A);
       double R, P;
       split_RP<KER>(Lg, alpha, c, lnA + 2.0 * log(rho), R, P);
-      acc += c_gw[n][ie] * f * (c_gw[n][ir] * (R + P * lnA) + 2.0 * c_glw[n][ir] * P);
+      const double wr = rc == 0 ? c_gw[n][rk] * (R + P * (lnA - 2.0 * lnns)) + 2.0 * c_glw[n][rk] * P
+                                : c_gw[n][rk] * (R + P * (lnA + 2.0 * log(rho)));
+      acc += weta * f * ins * wr;
     }
   }
 #pragma unroll
@@ -245,13 +260,13 @@ __global__ void __launch_bounds__(128) k_sing(BlockArgs B, const Seg* __restrict
   if (KIND == STB_V) {
     jcol = ((i + off - 1) % ng + ng) % ng;       // i-1, i, i+1
     const int rel = chain_rel(i, jcol, ng);
-    add = pair_touching<0>(seg[i], seg[jcol], rel, Lg, alpha, nsing, 1, 1, 1, 1);
+    add = pair_touching<0>(seg[i], seg[jcol], rel, Lg, alpha, nsing, 1, 1, 1, 1, B.ell);
   } else if (KIND == STB_K) {
     jcol = ((i + off - 1) % ng + ng) % ng;       // n = i-1 .. i+2
     const int jl = (jcol - 1 + ng) % ng;
     const int rl = chain_rel(i, jl, ng), rr = chain_rel(i, jcol, ng);
-    if (rl) add += pair_touching<2>(seg[i], seg[jl], rl, Lg, alpha, nsing, 1, 1, 0, 1);
-    if (rr) add += pair_touching<2>(seg[i], seg[jcol], rr, Lg, alpha, nsing, 1, 1, 1, 0);
+    if (rl) add += pair_touching<2>(seg[i], seg[jl], rl, Lg, alpha, nsing, 1, 1, 0, 1, B.ell);
+    if (rr) add += pair_touching<2>(seg[i], seg[jcol], rr, Lg, alpha, nsing, 1, 1, 1, 0, B.ell);
   } else {
     const int l = i;
     jcol = ((l + off - 2) % ng + ng) % ng;       // k = l-2 .. l+2
@@ -267,10 +282,10 @@ __global__ void __launch_bounds__(128) k_sing(BlockArgs B, const Seg* __restrict
         const int rel = chain_rel(p, q, nh);
         if (!rel) continue;
         const Seg X = half[p], Y = half[q];
-        add += dvl[m] * dvk[nn_] * pair_touching<0>(X, Y, rel, Lg, alpha, nsing, 1, 1, 1, 1);
+        add += dvl[m] * dvk[nn_] * pair_touching<0>(X, Y, rel, Lg, alpha, nsing, 1, 1, 1, 1, B.ell);
         const double nn = X.nx * Y.nx + X.ny * Y.ny;
         if (nn != 0.0)
-          add += nn * pair_touching<1>(X, Y, rel, Lg, alpha, nsing, vl[m][0], vl[m][1], vk[nn_][0], vk[nn_][1]);
+          add += nn * pair_touching<1>(X, Y, rel, Lg, alpha, nsing, vl[m][0], vl[m][1], vk[nn_][0], vk[nn_][1], B.ell);
       }
   }
   if ((threadIdx.x & 31) == 0 && !(B.sym && i / SYM_TS > jcol / SYM_TS)) *entry_ptr(B, a, i, b, jcol) += add;
@@ -404,6 +419,7 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bul
   A->launches = 0;
   const int qfar = std::min(6, q_bulk + 1);
   MomArgs MB{d_rec, npairs, m->d_seg, m->d_half, m->d_dual, m->alpha, ng, q_bulk, qfar, d_ctr};
+  MB.ell = m->htmin > 0.0 ? std::sqrt(4.0 * m->htmin / m->alpha) : 0.0;
   MomArgs MN = MB;
   MN.rec = d_rec + (long long)nf * npairs;
   MN.counters = d_ctr + 5;
@@ -462,6 +478,7 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bul
     BA.pbase = pbase[bi];
     BA.pslots = pslots;
     BA.ntile = ntile;
+    BA.ell = MB.ell;
     const int R = use_mma ? 7 : 8;    // test steps per band (k_bulk_t: 8 nodes = one DMMA N tile)
     const int nband = (blk.a1 - blk.a0 + R - 1) / R;
     if (blk.a1 - 1 - blk.b0 >= 2) {

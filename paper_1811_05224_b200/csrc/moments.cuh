@@ -78,7 +78,18 @@ struct MomArgs {
   int q;                  // bulk Gauss order (bulk records)
   int qfar;               // near-cell order of well-separated pairs (near records)
   unsigned long long* counters;  // node evaluations per regime: A, B, Z, C
+  double ell;             // sqrt(4 min h_t / alpha): the length on which U* varies at the
+                          // smallest lag; sub-pairs closer than 8 ell get composite rules with
+                          // cells of at most ell (no subdivision while kappa <= 1)
 };
+
+// composite subdivision of a sub-pair: cells per direction
+__device__ __forceinline__ int composite_cells(const Seg& X, const Seg& Y, double ell) {
+  if (!(ell > 0.0)) return 1;
+  const double hm = fmax(X.h, Y.h);
+  if (hm <= ell || seg_dist(X, Y) >= 8.0 * ell) return 1;
+  return min(24, (int)ceil(hm / ell));
+}
 
 // ------------------------------------------------------------- point enumeration
 // Visits every quadrature point of the (half-)segment pairs that make up entry (I, J) with its
@@ -94,6 +105,7 @@ struct SubPair {
   Seg X, Y;
   int pi, qi, nchain;       // element indices of X and Y in their closed chain of nchain elements
   int q;
+  int ns;                   // composite cells per direction (1 = plain tensor Gauss)
   int side;                 // K: 0 = gamma_{n-1} (hat rising), 1 = gamma_n (falling)
   double sa, sb;            // weight scales of the two families
   double l0, l1, k0, k1;    // D: psi_l on X and psi_k on Y, linear from (l0 / k0) to (l1 / k1)
@@ -111,6 +123,7 @@ __device__ __forceinline__ void for_subpairs(const MomArgs& M, int I, int J, Fn&
     sp.qi = J;
     sp.nchain = ng;
     sp.q = NEAR ? near_order(sp.X, sp.Y, M.qfar) : M.q;
+    sp.ns = composite_cells(sp.X, sp.Y, M.ell);
     sp.sa = sp.X.h * sp.Y.h / (4.0 * STB_PI);
     sp.sb = 0.0;
     fn(sp);
@@ -126,6 +139,7 @@ __device__ __forceinline__ void for_subpairs(const MomArgs& M, int I, int J, Fn&
       if (collinear(sp.X, sp.Y)) continue;
       if (NEAR && chain_rel(I, j, ng)) continue;
       sp.q = NEAR ? near_order(sp.X, sp.Y, M.qfar) : M.q;
+      sp.ns = composite_cells(sp.X, sp.Y, M.ell);
       sp.side = side;
       sp.sa = M.alpha / (8.0 * STB_PI) * sp.X.h * sp.Y.h;
       sp.sb = 0.0;
@@ -150,6 +164,7 @@ __device__ __forceinline__ void for_subpairs(const MomArgs& M, int I, int J, Fn&
         sp.qi = qh;
         sp.nchain = nh;
         sp.q = NEAR ? near_order(sp.X, sp.Y, M.qfar) : M.q;
+        sp.ns = composite_cells(sp.X, sp.Y, M.ell);
         const double dvk = n < 2 ? 1.0 / dk.Lm : -1.0 / dk.Lp;
         sp.k0 = n == 0 ? 0.0 : (n == 1 ? dk.vm : (n == 2 ? 1.0 : dk.vp));
         sp.k1 = n == 0 ? dk.vm : (n == 1 ? 1.0 : (n == 2 ? dk.vp : 0.0));
@@ -163,16 +178,18 @@ __device__ __forceinline__ void for_subpairs(const MomArgs& M, int I, int J, Fn&
 }
 
 // quadrature point (u, v) of a sub-pair: c = alpha r^2 / 4 and the two family weights
+// (composite cell cu, node uu) x (cell cv, node vv); cells of width 1 / ns on [0, 1]
 template <int KIND>
-__device__ __forceinline__ void sub_point(const SubPair& sp, double alpha, int u, int v, double& c,
-                                          double& wa, double& wb) {
+__device__ __forceinline__ void sub_point(const SubPair& sp, double alpha, int cu, int uu, int cv, int vv,
+                                          double& c, double& wa, double& wb) {
   const int q = sp.q;
-  const double fu = c_gx[q][u], fv = c_gx[q][v];
+  const double ins = sp.ns == 1 ? 1.0 : 1.0 / sp.ns;
+  const double fu = (cu + c_gx[q][uu]) * ins, fv = (cv + c_gx[q][vv]) * ins;
   const double px = fma(fu, sp.X.bx - sp.X.ax, sp.X.ax), py = fma(fu, sp.X.by - sp.X.ay, sp.X.ay);
   const double qx = fma(fv, sp.Y.bx - sp.Y.ax, sp.Y.ax), qy = fma(fv, sp.Y.by - sp.Y.ay, sp.Y.ay);
   const double dx = px - qx, dy = py - qy;
   c = 0.25 * alpha * (dx * dx + dy * dy);
-  const double w = c_gw[q][u] * c_gw[q][v];
+  const double w = c_gw[q][uu] * c_gw[q][vv] * (ins * ins);
   if (KIND == STB_V) {
     wa = sp.sa * w;
     wb = 0.0;
@@ -188,12 +205,14 @@ __device__ __forceinline__ void sub_point(const SubPair& sp, double alpha, int u
 template <int KIND, bool NEAR, class Vis>
 __device__ __forceinline__ void for_points(const MomArgs& M, int I, int J, Vis&& vis) {
   for_subpairs<KIND, NEAR>(M, I, J, [&](const SubPair& sp) {
-    for (int u = 0; u < sp.q; ++u)
-      for (int v = 0; v < sp.q; ++v) {
-        double c, wa, wb;
-        sub_point<KIND>(sp, M.alpha, u, v, c, wa, wb);
-        vis(c, wa, wb);
-      }
+    for (int cu = 0; cu < sp.ns; ++cu)
+      for (int u = 0; u < sp.q; ++u)
+        for (int cv = 0; cv < sp.ns; ++cv)
+          for (int v = 0; v < sp.q; ++v) {
+            double c, wa, wb;
+            sub_point<KIND>(sp, M.alpha, cu, u, cv, v, c, wa, wb);
+            vis(c, wa, wb);
+          }
   });
 }
 
@@ -202,10 +221,11 @@ template <int KIND, bool NEAR, class Vis>
 __device__ __forceinline__ void for_points_lane(const MomArgs& M, int I, int J, int lane, Vis&& vis) {
   int base = 0;
   for_subpairs<KIND, NEAR>(M, I, J, [&](const SubPair& sp) {
-    const int n = sp.q * sp.q;
+    const int nq = sp.q * sp.ns, n = nq * nq;
     for (int idx = (lane - base) & 31; idx < n; idx += 32) {
       double c, wa, wb;
-      sub_point<KIND>(sp, M.alpha, idx / sp.q, idx % sp.q, c, wa, wb);
+      const int iu = idx / nq, iv = idx % nq;
+      sub_point<KIND>(sp, M.alpha, iu / sp.q, iu % sp.q, iv / sp.q, iv % sp.q, c, wa, wb);
       vis(c, wa, wb);
     }
     base = (base + n) & 31;
@@ -427,6 +447,27 @@ __device__ __forceinline__ double pt_q(double c, double s, double lns, double u)
   return k - s / c - (STB_GAMMA + log(c));
 }
 
+// the same point contributions without the affine terms (the true node values of the near
+// cells): computing them directly avoids subtracting two large affine sums when c >> s
+__device__ __forceinline__ double pt_h_true(double c, double s, double lns, double u) {
+  const double x = c * u;
+  if (x < STB_XSPLIT) return fma(s, gh_poly(x), (s + c) * (lns - STB_GAMMA - log(c)));
+  const double e = x > STB_XUNDER ? 0.0 : exp(-x);
+  return x > STB_XUNDER ? 0.0 : s * fma(1.0 + x, e1_large(1.0 / x, e), -e);
+}
+__device__ __forceinline__ double pt_f_true(double c, double lns, double u) {
+  const double x = c * u;
+  if (x < STB_XSPLIT) return ein_poly(x) + lns - STB_GAMMA - log(c);
+  return x > STB_XUNDER ? 0.0 : e1_large(1.0 / x, exp(-x));
+}
+__device__ __forceinline__ double pt_q_true(double c, double s, double lns, double u) {
+  const double x = c * u;
+  if (x < STB_XSPLIT) return psi_poly(x) - lns + s / c + STB_GAMMA + log(c);
+  const double t = 1.0 / x;
+  const double e = x > STB_XUNDER ? 0.0 : exp(-x);
+  return x > STB_XUNDER ? 0.0 : e * t - e1_large(t, e);
+}
+
 // regimes B and Z (out of line: rare); *regime = 1 (B), 2 (Z) or 3 (C: not evaluated here).
 // Regime B in scaled form (x0 = c0 u): e^_j = u^j e_j = e^{-x0} (-u)^j / j!,
 // a^_j = u^{j+1} a_j = (e^_j - a^_{j-1}) / c0 (Taylor coefficients a_j of e^{-x}/x at x0), so that
@@ -463,7 +504,9 @@ struct RegBZ {
 static __device__ __constant__ double STB_GB3_CB[STB_GB3_DEG + 1] = STB_GB3_INIT;
 __device__ __forceinline__ double gb3_cb(double t) { return horner<STB_GB3_DEG>(STB_GB3_CB, fma(t, STB_GB3_YS, -1.0)); }
 
-template <int KIND>
+// TRUEV: return the true node value (near cells: without the affine terms, which then need not be
+// added here and subtracted again by the caller)
+template <int KIND, bool TRUEV = false>
 __device__ __forceinline__ double phi_bz(const double* __restrict__ rec, long long S, const RegBZ<KIND>& z,
                                          double s, double u, int* regime) {
   const bool zz = z.cmin > 0.0 && z.cmin * u >= MXZ;
@@ -502,7 +545,8 @@ __device__ __forceinline__ double phi_bz(const double* __restrict__ rec, long lo
 #pragma unroll
   for (int f = 0; f < Fams<KIND>::n; ++f) {
     const int fam = f == 0 ? Fams<KIND>::f0 : Fams<KIND>::f1;
-    if (fam == FAM_H) out += fma(s, T[f] + z.C0[f], z.C1[f]);
+    if (TRUEV) out += fam == FAM_H ? s * T[f] : T[f];
+    else if (fam == FAM_H) out += fma(s, T[f] + z.C0[f], z.C1[f]);
     else if (fam == FAM_F) out += T[f] + z.C0[f];
     else out += T[f] - fma(s, z.C1[f], z.C0[f]);
   }
@@ -589,16 +633,17 @@ __device__ __forceinline__ void phi_bz2(const double* __restrict__ rec, long lon
 
 // regime C, warp-cooperative: every lane evaluates its round-robin share of the points of
 // entry (I, J) at node (s, u) (all lanes pass the same arguments); returns the warp sum
+// (NEAR: the true node value, without the affine terms)
 template <int KIND, bool NEAR>
 __device__ __noinline__ double phi_c_warp(const MomArgs M, int I, int J, double s, double lns, double u) {
   const int lane = threadIdx.x & 31;
   double out = 0.0;
   for_points_lane<KIND, NEAR>(M, I, J, lane, [&](double c, double wa, double wb) {
-    if (KIND == STB_V) out = fma(wa, pt_h(c, s, lns, u), out);
-    else if (KIND == STB_K) out = fma(wa, pt_q(c, s, lns, u), out);
+    if (KIND == STB_V) out = fma(wa, NEAR ? pt_h_true(c, s, lns, u) : pt_h(c, s, lns, u), out);
+    else if (KIND == STB_K) out = fma(wa, NEAR ? pt_q_true(c, s, lns, u) : pt_q(c, s, lns, u), out);
     else {
-      out = fma(wa, pt_h(c, s, lns, u), out);
-      if (wb != 0.0) out = fma(wb, pt_f(c, lns, u), out);
+      out = fma(wa, NEAR ? pt_h_true(c, s, lns, u) : pt_h(c, s, lns, u), out);
+      if (wb != 0.0) out = fma(wb, NEAR ? pt_f_true(c, lns, u) : pt_f(c, lns, u), out);
     }
   });
 #pragma unroll
@@ -1141,13 +1186,14 @@ __global__ void __launch_bounds__(128) k_near_m(BlockArgs B, MomArgs M, int chun
   auto node = [&](int x, int y) -> double {
     const double4 nd = B.lag[x * B.ldlag + y];
     double v = 0.0;
-    bool needC = false;
+    bool needC = false, inA = false;
     if (A.cmax * nd.z < STB_MXA) {
       v = A.eval(nd.x, nd.y, nd.z);
+      inA = true;
       ++nA;
     } else {
       int reg = 0;
-      v = phi_bz<KIND>(rec, S, Z, nd.x, nd.z, &reg);
+      v = phi_bz<KIND, true>(rec, S, Z, nd.x, nd.z, &reg);
       nB += reg == 1;
         nK += reg == 1 ? Z.kb : 0;
       nZ += reg == 2;
@@ -1164,7 +1210,8 @@ __global__ void __launch_bounds__(128) k_near_m(BlockArgs B, MomArgs M, int chun
       const double c = phi_c_warp<KIND, true>(M, Is, Js, nd.x, nd.y, nd.z);
       if (lane == src) v = c;
     }
-    return v - affine_part<KIND>(rec, S, nd.x);
+    // regime A gives the regularised value; B, Z and C return the true value directly
+    return inA ? v - affine_part<KIND>(rec, S, nd.x) : v;
   };
   double prev = 0.0;  // Phi(a, a-1)
   if (a_beg < a_end && a_beg >= 1 && a_beg - 1 >= B.b0 && a_beg - 1 < B.b1) prev = node(a_beg, a_beg - 1);

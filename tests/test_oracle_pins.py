@@ -118,6 +118,32 @@ def test_pair_integrals_brute_force(c1, case):
     assert got == pytest.approx(ref, rel=1e-12, abs=1e-18)
 
 
+# large kappa = alpha h^2 / (4 min h_t) (here 44): U* varies on ell = sqrt(4 min h_t / alpha) =
+# h / 6.7, the composite rules of DESIGN.md reading R24 resolve it (touching pairs near the
+# singularity, the identical pair in a bulk cell, a 2-D integrand at the corner)
+LK_CASES = [
+    # ker, a, b, p, q, rel, sx, sy
+    (0, 1, 0, 2, 1, 3, (1, 1), (1, 1)),      # V vertex pair at the corner (1,0), d = 1
+    (0, 2, 0, 2, 2, 1, (1, 1), (1, 1)),      # V identical, bulk cell d = 2
+    (2, 1, 0, 2, 3, 2, (1, 1), (1, 0)),      # K vertex pair, falling hat, d = 1
+    (1, 1, 0, 4, 4, 1, (0.5, 1), (1, 0.5)),  # F identical, linear shapes
+]
+
+
+@pytest.mark.parametrize("case", LK_CASES)
+def test_large_kappa_pair_integrals_brute_force(case):
+    from workloads.configs import Workload, uniform_times
+    sq = [(0.0, 0.0), (1.0, 0.0), (1.0, 1.0), (0.0, 1.0)]
+    w = Workload("alpha_large", sq, [3, 3, 3, 3], uniform_times(8), 200.0, (1.5, 1.5), 1e-10)
+    m = O.OracleMesh(w)
+    ker, a, b, p, q, rel, sx, sy = case
+    X = (tuple(m.seg_a[p]), tuple(m.seg_b[p]))
+    Y = (tuple(m.seg_a[q]), tuple(m.seg_b[q]))
+    ref = float(B.pair(ker, w.alpha, w.t_breaks, a, b, X, Y, m.seg_n[q], sx, sy, rel))
+    got = m.pair(ker, 0, a, b, p, q, sx, sy)
+    assert got == pytest.approx(ref, rel=1e-11, abs=1e-18)
+
+
 def test_half_segment_pairs_brute_force():
     """half segments on the L-shape (re-entrant corner, graded steps, alpha = 1/2)"""
     w = W.get("LT")
