@@ -562,34 +562,13 @@ def test_distributed_path_on_a_one_rank_nccl_communicator():
     assert relmax(w1, w0) <= 1e-12
 
 
-def _edge_workloads():
-    from workloads.configs import Workload, graded_times, uniform_times
-    sq = [(0.0, 0.0), (1.0, 0.0), (1.0, 1.0), (0.0, 1.0)]
-    return {
-        # the smallest boundary the API accepts (N_Gamma = 6): every pair is at most two
-        # elements apart (identical, adjacent, second neighbours through a corner)
-        "triangle6": Workload("triangle6", [(0.0, 0.0), (1.0, 0.0), (0.3, 0.8)], [2, 2, 2],
-                              uniform_times(5), 1.0, (1.5, 1.5), 1e-10),
-        # one time step: only the d = 0 cell exists
-        "onestep": Workload("onestep", sq, [2, 2, 2, 2], uniform_times(1), 1.0, (1.5, 1.5), 1e-10),
-        # 33 elements: one full 32-wide tile and a ragged tile of one (symmetric packing, bulk
-        # column tiles, SYMV)
-        "ragged33": Workload("ragged33", sq, [9, 8, 8, 8], uniform_times(6), 1.0, (1.5, 1.5), 1e-10),
-        # steps graded by 2: the first step is 1/1023, kappa = 61 (per-lag singular kernel,
-        # large bulk order) next to steps of 1/2
-        "grade2": Workload("grade2", sq, [2, 2, 2, 2], graded_times(10, 2.0), 1.0, (1.5, 1.5), 1e-10),
-        # heat capacity extremes (c = alpha r^2 / 4): nearly every node in regime A / in regime Z
-        "alpha_small": Workload("alpha_small", sq, [3, 3, 3, 3], uniform_times(8), 1e-3, (1.5, 1.5), 1e-10),
-        "alpha_large": Workload("alpha_large", sq, [3, 3, 3, 3], uniform_times(8), 200.0, (1.5, 1.5), 1e-10),
-    }
-
-
 @pytest.mark.parametrize("name", ["triangle6", "onestep", "ragged33", "grade2", "alpha_small", "alpha_large"])
 def test_edge_case_meshes_full_parity(name):
     """degenerate and extreme inputs (minimal boundary, one step, ragged tiles, strong grading,
     alpha extremes): V_h, K_h, D_h in full against the oracle, causality zeros, and V_h's spatial
     blocks symmetric"""
-    w = _edge_workloads()[name]
+    from workloads.edge import edge_workloads
+    w = edge_workloads()[name]
     om = O.OracleMesh(w)
     m = S.Mesh.from_workload(w)
     ng = w.n_gamma

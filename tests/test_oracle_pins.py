@@ -132,9 +132,8 @@ LK_CASES = [
 
 @pytest.mark.parametrize("case", LK_CASES)
 def test_large_kappa_pair_integrals_brute_force(case):
-    from workloads.configs import Workload, uniform_times
-    sq = [(0.0, 0.0), (1.0, 0.0), (1.0, 1.0), (0.0, 1.0)]
-    w = Workload("alpha_large", sq, [3, 3, 3, 3], uniform_times(8), 200.0, (1.5, 1.5), 1e-10)
+    from workloads.edge import edge_workloads
+    w = edge_workloads()["alpha_large"]
     m = O.OracleMesh(w)
     ker, a, b, p, q, rel, sx, sy = case
     X = (tuple(m.seg_a[p]), tuple(m.seg_b[p]))

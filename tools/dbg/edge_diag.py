@@ -3,14 +3,11 @@ import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 import torch
-src = open(os.path.join(os.path.dirname(__file__), "..", "..", "tests", "test_gpu_parity.py")).read()
-i = src.index("def _edge_workloads"); j = src.index('@pytest.mark.parametrize("name", ["triangle6"')
-ns = {}
-exec(src[i:j], ns)
+from workloads.edge import edge_workloads
 from oracle import oracle as O
 from paper_1811_05224_b200 import stbem as S
 for name in sys.argv[1:]:
-    w = ns["_edge_workloads"]()[name]
+    w = edge_workloads()[name]
     om = O.OracleMesh(w)
     m = S.Mesh.from_workload(w)
     ng = w.n_gamma
