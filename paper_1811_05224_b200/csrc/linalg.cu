@@ -360,24 +360,37 @@ bem_status gemv_launch(const bem_matrix* A, double a, const double* x, double b,
 // peak on B200 (37.1 vs 34.1 TFLOP/s, profiles/r01_fp64_peak.txt, r01_dmma_peak.txt) but one
 // DMMA does 256 FMAs per warp from 2 operand registers per lane, so the tile loop is no longer
 // bound by shared-memory operand loads and issue slots as the 8 x 8 DFMA register tile was.
-constexpr int TZ_TI = 128, TZ_TA = 128, TZ_TK = 16, TZ_LD = TZ_TI + 4;
+constexpr int TZ_TI = 128, TZ_TA = 128, TZ_TK = 16, TZ_LDK = TZ_TK + 4, TZ_STAGES = 3;
+constexpr size_t TZ_SMEM = sizeof(double) * TZ_STAGES * 2 * TZ_TI * TZ_LDK;
 // 8 warps as 2 (i) x 4 (a), warp tile 64 i x 32 a = 8 x 4 DMMA tiles, 64 accumulators per lane.
-// Shared tiles k-major with row stride 132 doubles and column index ii ^ (jj / 4): the fragment
-// loads (lane -> k = lane % 4, m / n = lane / 4) and the tile stores (16 consecutive jj of one ii)
-// both hit 16 distinct 8-byte bank pairs per half warp.  The next K step's tiles are
-// prefetched into registers while the current one is multiplied from shared memory.
+// Shared tiles row-major [i or a][k] with row stride 20 doubles: the fragment loads (lane -> k =
+// lane % 4, m / n = lane / 4) hit 16 distinct 8-byte bank pairs per half warp.  Global -> shared
+// by cp.async (zero-filled outside the matrix) in a 3-stage pipeline: the tiles of the next two
+// K steps are in flight while the current one is multiplied.
 __device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(d[0]), "+d"(d[1]) : "d"(a), "d"(b));
 }
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int bytes) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" :: "r"(sa), "l"(gmem), "r"(bytes));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, int bytes) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" :: "r"(sa), "l"(gmem), "r"(bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" :: "n"(N)); }
 // Work units (1-D grid): a-tile at (in order), then chunk of dpz lags within the tile's lag range
 // [0, min(nt, a0 + 128)) (lags beyond the tile's last column contribute nothing), then i-tile: all
 // units but a tile's last chunk cost the same, and the host sizes dpz for whole waves of the SMs.
 __global__ void __launch_bounds__(256) k_toeplitz_mm(const double* __restrict__ T, long long ldT_d,
                                                     int ldT, const double* __restrict__ x, int ng, int nt,
                                                     int dpz, double* __restrict__ part) {
-  __shared__ __align__(16) double Tt[TZ_TK][TZ_LD];   // Tt[jj][ii] = T_d[i0 + ii][j0 + jj]
-  __shared__ __align__(16) double Xs[TZ_TK][TZ_LD];   // Xs[jj][aa] = X[j0 + jj][a0 + aa - d]
+  extern __shared__ __align__(16) double tz_sm[];
+  // stage s: Ts = tz_sm + s * 2 * TI * LDK  ([ii][jj] = T_d[i0 + ii][j0 + jj]),
+  //          Xs = Ts + TI * LDK            ([aa][jj] = X[j0 + jj][a0 + aa - d] = x[(a0 + aa - d) ng + j0 + jj])
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wi = (warp & 1) * 64, wa = (warp >> 1) * 32, fr = lane & 3, fc = lane >> 2;
   const int nti = (ng + TZ_TI - 1) / TZ_TI;
@@ -396,42 +409,53 @@ __global__ void __launch_bounds__(256) k_toeplitz_mm(const double* __restrict__ 
   for (int u = 0; u < 8; ++u)
 #pragma unroll
     for (int v = 0; v < 4; ++v) acc[u][v][0] = acc[u][v][1] = 0.0;
-  double rt[8], rx[8];
-  auto fetch = [&](int step) {
+  auto issue = [&](int step) {
+    double* Ts = tz_sm + (step % TZ_STAGES) * (2 * TZ_TI * TZ_LDK);
+    double* Xs = Ts + TZ_TI * TZ_LDK;
     const int d = d0 + step / nj, j0 = (step % nj) * TZ_TK;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int e = tid + q * 256, ii = e / TZ_TK, jj = e % TZ_TK;
+    for (int q = 0; q < 4; ++q) {            // T: 128 rows x 8 chunks of 16 bytes
+      const int e = tid + q * 256, ii = e >> 3, jj = (e & 7) * 2;
       const int i = i0 + ii, j = j0 + jj;
-      rt[q] = (i < ng && j < ng) ? T[(long long)d * ldT_d + (long long)i * ldT + j] : 0.0;
-      const int aa = ii, b = a0 + aa - d;
-      rx[q] = (j < ng && b >= 0 && b < nt) ? x[(long long)b * ng + j] : 0.0;
+      const int bytes = (i < ng && j < ng) ? (j + 1 < ng ? 16 : 8) : 0;
+      const double* src = T + (long long)d * ldT_d + (long long)min(i, ng - 1) * ldT + (bytes ? j : 0);
+      cp_async16(Ts + ii * TZ_LDK + jj, src, bytes);
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {            // X: 128 columns x 16 doubles (rows of x need not be 16-B aligned)
+      const int e = tid + q * 256, aa = e >> 4, jj = e & 15;
+      const int b = a0 + aa - d, j = j0 + jj;
+      const bool ok = j < ng && b >= 0 && b < nt;
+      cp_async8(Xs + aa * TZ_LDK + jj, x + (ok ? (long long)b * ng + j : 0), ok ? 8 : 0);
     }
   };
-  if (nsteps > 0) fetch(0);
-  for (int step = 0; step < nsteps; ++step) {
-    __syncthreads();
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int e = tid + q * 256, ii = e / TZ_TK, jj = e % TZ_TK;
-      Tt[jj][ii ^ (jj >> 2)] = rt[q];     // XOR swizzle: conflict-free stores (16 jj of one ii)
-      Xs[jj][ii ^ (jj >> 2)] = rx[q];
-    }
-    __syncthreads();
-    if (step + 1 < nsteps) fetch(step + 1);
+  for (int sgi = 0; sgi < TZ_STAGES - 1; ++sgi) {
+    if (sgi < nsteps) issue(sgi);
+    cp_async_commit();
+  }
+  for (int step = 0; step < nsteps; ++step) {
+    cp_async_wait<TZ_STAGES - 2>();
+    __syncthreads();                         // stage step % STAGES complete for all threads; the
+                                             // stage refilled below was last read in step - 1
+    if (step + TZ_STAGES - 1 < nsteps) issue(step + TZ_STAGES - 1);
+    cp_async_commit();
+    const double* Ts = tz_sm + (step % TZ_STAGES) * (2 * TZ_TI * TZ_LDK);
+    const double* Xs = Ts + TZ_TI * TZ_LDK;
 #pragma unroll
     for (int kk = 0; kk < TZ_TK; kk += 4) {
       double af[8], bf[4];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) af[u] = Tt[kk + fr][(wi + 8 * u + fc) ^ (kk >> 2)];
+      for (int u = 0; u < 8; ++u) af[u] = Ts[(wi + 8 * u + fc) * TZ_LDK + kk + fr];
 #pragma unroll
-      for (int v = 0; v < 4; ++v) bf[v] = Xs[kk + fr][(wa + 8 * v + fc) ^ (kk >> 2)];
+      for (int v = 0; v < 4; ++v) bf[v] = Xs[(wa + 8 * v + fc) * TZ_LDK + kk + fr];
 #pragma unroll
       for (int u = 0; u < 8; ++u)
 #pragma unroll
         for (int v = 0; v < 4; ++v) dmma_8x8x4(acc[u][v], af[u], bf[v]);
     }
   }
+  cp_async_wait<0>();
   // partial Y tile of this lag range: part[z][a][i]; lane holds D[fc][2 fr + e] of each tile
   const long long n = (long long)nt * ng;
 #pragma unroll
@@ -479,7 +503,12 @@ bem_status toeplitz_gemv(const bem_matrix* A, double a, const double* x, double 
   cudaError_t e = storage_acquire(m->device, bytes, st, (void**)&part);
   if (e != cudaSuccess) return cuda_fail(e, "toeplitz product");
   e = cudaMemsetAsync(part, 0, bytes, st);   // lag ranges beyond a tile's columns leave their slots zero
-  k_toeplitz_mm<<<(unsigned)nunits, 256, 0, st>>>(A->data, A->poff.size() > 1 ? A->poff[1] - A->poff[0] : 0,
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_toeplitz_mm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TZ_SMEM);
+    attr = true;
+  }
+  k_toeplitz_mm<<<(unsigned)nunits, 256, TZ_SMEM, st>>>(A->data, A->poff.size() > 1 ? A->poff[1] - A->poff[0] : 0,
                                       (int)pad4(ng), x, ng, nt, dpz, part);
   k_toeplitz_reduce<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(part, nsplit, n, a, b, y);
   count_launch(2);
