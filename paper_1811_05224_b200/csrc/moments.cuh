@@ -527,11 +527,19 @@ __device__ __forceinline__ double phi_bz(const double* __restrict__ rec, long lo
     const double* p2 = R0 + FB2 * S;
     const double* p3 = R1 + FB1 * S;
     double h1 = 0.0, h2 = Fams<KIND>::f0 == FAM_Q ? p2[(long long)z.kb * S] : 0.0, h3 = 0.0;
+    // coefficient pointers walked down by the record stride (no index multiply per load)
+    const long long top = (long long)(z.kb - 1) * S;
+    const double* q1 = p1 + top;
+    const double* q2 = p2 + top;
+    const double* q3 = p3 + top;
 #pragma unroll 2
     for (int i = z.kb - 1; i >= 0; --i) {
-      h1 = fma(h1, zu, p1[(long long)i * S]);
-      if (Fams<KIND>::f0 != FAM_F) h2 = fma(h2, zu, p2[(long long)i * S]);
-      if (Fams<KIND>::n == 2) h3 = fma(h3, zu, p3[(long long)i * S]);
+      h1 = fma(h1, zu, *q1);
+      if (Fams<KIND>::f0 != FAM_F) h2 = fma(h2, zu, *q2);
+      if (Fams<KIND>::n == 2) h3 = fma(h3, zu, *q3);
+      q1 -= S;
+      q2 -= S;
+      q3 -= S;
     }
     const double S1a = ex * h1, S2a = ex * h2, S1b = ex * h3;
     const double a0 = ex * ic0;
@@ -579,21 +587,28 @@ __device__ __forceinline__ void phi_bz2(const double* __restrict__ rec, long lon
   const double* p3 = R1 + FB1 * S;
   const double top = Fams<KIND>::f0 == FAM_Q ? p2[(long long)z.kb * S] : 0.0;
   double h11 = 0.0, h21 = top, h31 = 0.0, h12 = 0.0, h22 = top, h32 = 0.0;
+  const long long off = (long long)(z.kb - 1) * S;
+  const double* q1 = p1 + off;
+  const double* q2 = p2 + off;
+  const double* q3 = p3 + off;
 #pragma unroll 2
   for (int i = z.kb - 1; i >= 0; --i) {
-    const double c1 = p1[(long long)i * S];
+    const double c1 = *q1;
     h11 = fma(h11, z1, c1);
     h12 = fma(h12, z2, c1);
     if (Fams<KIND>::f0 != FAM_F) {
-      const double c2 = p2[(long long)i * S];
+      const double c2 = *q2;
       h21 = fma(h21, z1, c2);
       h22 = fma(h22, z2, c2);
     }
     if (Fams<KIND>::n == 2) {
-      const double c3 = p3[(long long)i * S];
+      const double c3 = *q3;
       h31 = fma(h31, z1, c3);
       h32 = fma(h32, z2, c3);
     }
+    q1 -= S;
+    q2 -= S;
+    q3 -= S;
   }
   const double S1a1 = ex1 * h11, S2a1 = ex1 * h21, S1b1 = ex1 * h31;
   const double S1a2 = ex2 * h12, S2a2 = ex2 * h22, S1b2 = ex2 * h32;
