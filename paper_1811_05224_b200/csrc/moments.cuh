@@ -736,6 +736,7 @@ __global__ void __launch_bounds__(128, (KIND == STB_D || PROD) ? 2 : 3) k_bulk_m
   // row offsets of the band rows a = r_lo + r for this warp's row I (panel offset + I * ld, or
   // the tile's offset + (I mod 32) * 32), shared by the warp: a store is one LDS + one address add
   __shared__ long long s_row[4][R];
+  __shared__ double s_phi[(R + 1) * 128];       // per-thread node values during the fix-ups
   long long* srow = s_row[threadIdx.x >> 5];
   if (!PROD && lane < R) {
     const int a = min(r_lo + lane, r_hi - 1);
@@ -797,6 +798,11 @@ __global__ void __launch_bounds__(128, (KIND == STB_D || PROD) ? 2 : 3) k_bulk_m
       if (ok && !inA) bmask |= 1u << r;
     }
     if (__any_sync(0xffffffffu, bmask != 0)) {
+      // the node values pass through shared memory while lanes overwrite their B / Z / C nodes
+      // (dynamic node index without register-array selects)
+      double* sp = s_phi + threadIdx.x;
+#pragma unroll
+      for (int r = 0; r <= R; ++r) sp[r * 128] = phi[r];
       unsigned cmask = 0;   // nodes r of this lane left to regime C
       while (bmask) {
         const int r = __ffs(bmask) - 1;
@@ -824,11 +830,8 @@ __global__ void __launch_bounds__(128, (KIND == STB_D || PROD) ? 2 : 3) k_bulk_m
           cmask |= 1u << r2;
           ++nC;
         }
-#pragma unroll
-        for (int rr = 0; rr <= R; ++rr) {
-          if (rr == r) phi[rr] = v;
-          if (rr == r2) phi[rr] = v2;
-        }
+        sp[r * 128] = v;
+        if (r2 >= 0) sp[r2 * 128] = v2;
       }
       unsigned lanes = __ballot_sync(0xffffffffu, cmask != 0);
       while (lanes) {                                   // warp-uniform
@@ -841,13 +844,11 @@ __global__ void __launch_bounds__(128, (KIND == STB_D || PROD) ? 2 : 3) k_bulk_m
           cm &= cm - 1;
           const double4 q = B.lag[(r_lo + r) * B.ldlag + y];
           const double v = phi_c_warp<KIND, false>(M, Is, Js, q.x, q.y, q.z);
-          if (lane == src) {
-#pragma unroll
-            for (int rr = 0; rr <= R; ++rr)
-              if (rr == r) phi[rr] = v;
-          }
+          if (lane == src) sp[r * 128] = v;
         }
       }
+#pragma unroll
+      for (int r = 0; r <= R; ++r) phi[r] = sp[r * 128];
     }
     if (y > B.b0) {
       const int b = y - 1;
