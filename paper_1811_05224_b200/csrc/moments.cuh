@@ -243,25 +243,8 @@ __global__ void __launch_bounds__(128) k_records(MomArgs M) {
   const int I = (int)(pair / M.ng), J = (int)(pair % M.ng);
   double* rec = M.rec + pair;
   const long long S = M.npairs;
-  double cmin = 1e300, cmax = 0.0;
-  int npts = 0;
-  for_points<KIND, NEAR>(M, I, J, [&](double c, double, double) {
-    cmin = fmin(cmin, c);
-    cmax = fmax(cmax, c);
-    ++npts;
-  });
-  if (npts == 0) cmin = 0.0;
-  const double c0m = 0.5 * (cmin + cmax);
-  const bool okB = cmin > 0.0 && (cmax - c0m) <= MRHO * c0m;
-  const double c0 = okB ? c0m : 0.0;
-  const double rho = okB ? (cmax - c0m) / c0m : 1.0;
-  const int kb = (!okB || rho <= 1e-6) ? 3 : min(MKB, max(3, (int)ceil(log(1e-16) / log(rho))));
-  rec[RF_CMAX * S] = cmax;
-  rec[RF_CMIN * S] = cmin;
-  rec[RF_C0 * S] = c0;
-  rec[RF_KB * S] = (double)kb;
-  rec[RF_IC0 * S] = okB ? 1.0 / c0 : 0.0;
-  // regime-A moments M_k = sum W c^k and the affine constants of both families in one pass
+  // one pass: c range, regime-A moments M_k = sum W c^k and the affine constants of both
+  // families (the constants need c > 0 at every point: dropped at the end if one c is 0)
   constexpr int NF = Fams<KIND>::n;
   double mk[NF][MKA + 1], C0[NF], C1[NF];
 #pragma unroll
@@ -270,9 +253,14 @@ __global__ void __launch_bounds__(128) k_records(MomArgs M) {
 #pragma unroll
     for (int k = 0; k <= MKA; ++k) mk[f][k] = 0.0;
   }
-  const bool lg = cmin > 0.0;   // the affine constants need c > 0 at every point
+  double cmin = 1e300, cmax = 0.0;
+  int npts = 0;
   for_points<KIND, NEAR>(M, I, J, [&](double c, double wa, double wb) {
-    const double g = lg ? STB_GAMMA + log(c) : 0.0;
+    cmin = fmin(cmin, c);
+    cmax = fmax(cmax, c);
+    ++npts;
+    const bool pos = c > 0.0;
+    const double g = pos ? STB_GAMMA + log(c) : 0.0;
 #pragma unroll
     for (int f = 0; f < NF; ++f) {
       const int fam = f == 0 ? Fams<KIND>::f0 : Fams<KIND>::f1;
@@ -287,12 +275,27 @@ __global__ void __launch_bounds__(128) k_records(MomArgs M) {
         pe *= c2;
         po *= c2;
       }
-      if (lg) {
+      if (pos) {
         C0[f] = fma(w, g, C0[f]);
         C1[f] += fam == FAM_Q ? w / c : w * c * g;
       }
     }
   });
+  if (npts == 0) cmin = 0.0;
+  if (!(cmin > 0.0)) {
+#pragma unroll
+    for (int f = 0; f < NF; ++f) C0[f] = C1[f] = 0.0;
+  }
+  const double c0m = 0.5 * (cmin + cmax);
+  const bool okB = cmin > 0.0 && (cmax - c0m) <= MRHO * c0m;
+  const double c0 = okB ? c0m : 0.0;
+  const double rho = okB ? (cmax - c0m) / c0m : 1.0;
+  const int kb = (!okB || rho <= 1e-6) ? 3 : min(MKB, max(3, (int)ceil(log(1e-16) / log(rho))));
+  rec[RF_CMAX * S] = cmax;
+  rec[RF_CMIN * S] = cmin;
+  rec[RF_C0 * S] = c0;
+  rec[RF_KB * S] = (double)kb;
+  rec[RF_IC0 * S] = okB ? 1.0 / c0 : 0.0;
   // regime-A fields of both families (static indices: the moments stay in registers)
 #pragma unroll
   for (int f = 0; f < NF; ++f) {
