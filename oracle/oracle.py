@@ -162,6 +162,42 @@ class OracleMesh:
                 M[r, a * ng + (l + 1) % ng] += self.ht[a] * hp * vp / 4
         return M
 
+    def dual_gram(self):
+        """spatial Gram matrix G_Y[l, k] = int_Gamma psi_l psi_k of the dual hats (R6): on each half
+        segment two hats are linear, int f g = L/6 (2 f0 g0 + f0 g1 + f1 g0 + 2 f1 g1)"""
+        ng, h = self.ng, self.seg_h
+        G = np.zeros((ng, ng))
+
+        def add(l, k, L, f0, f1, g0, g1):
+            v = L / 6.0 * (2 * f0 * g0 + f0 * g1 + f1 * g0 + 2 * f1 * g1)
+            G[l % ng, k % ng] += v
+
+        for i in range(ng):
+            vm = h[(i - 1) % ng] / (h[(i - 1) % ng] + h[i])      # psi_i(x_i)
+            vp = h[(i + 1) % ng] / (h[i] + h[(i + 1) % ng])      # psi_i(x_{i+1})
+            L = h[i] / 2.0
+            left = [(i, vm, 1.0), (i - 1, 1.0 - vm, 0.0)]        # [x_i, m_i]
+            right = [(i, 1.0, vp), (i + 1, 0.0, 1.0 - vp)]       # [m_i, x_{i+1}]
+            for half in (left, right):
+                for (l, f0, f1) in half:
+                    for (k, g0, g1) in half:
+                        add(l, k, L, f0, f1, g0, g1)
+        return G
+
+    def stability_ratio(self):
+        """the discrete inf-sup constant of the pairing <tau_h, v_h> between X^{0,0}(Sigma_h) and
+        Y_h (eq. 5, P:124; SPEC's stability surrogate): the time factors h_t(a) and the H^{+-1/2, +-1/4}
+        scalings cancel between the pairing and the two norms, leaving the spatial L^2 inf-sup
+        sigma_min(G_Y^{-1/2} M_s G_X^{-1/2}) with M_s[l, k] = int psi_l phi_k (the dual mass of one
+        step / h_t), G_X = diag(h_k), G_Y the dual-hat Gram matrix.  Returns (ratio, sigma_min(M_s))."""
+        ng = self.ng
+        Ms = self.mass_dual()[:ng, :ng] / self.ht[0]
+        gx = 1.0 / np.sqrt(self.seg_h)
+        wy, Uy = np.linalg.eigh(self.dual_gram())
+        Gy = Uy @ np.diag(1.0 / np.sqrt(wy)) @ Uy.T
+        B = Gy @ Ms @ np.diag(gx)
+        return float(np.linalg.svd(B, compute_uv=False).min()), float(np.linalg.svd(Ms, compute_uv=False).min())
+
     def lumped_dual(self):
         """row sums of the dual mass: d_(a,l) = h_t(a)(h_{l-1} + 2 h_l + h_{l+1})/4"""
         return self.mass_dual().sum(axis=1)

@@ -584,3 +584,27 @@ def test_edge_case_meshes_full_parity(name):
                 for b in range(a + 1):
                     blk = got[a * ng:(a + 1) * ng, b * ng:(b + 1) * ng]
                     assert np.allclose(blk, blk.T, rtol=0, atol=MAT_TOL * np.abs(got).max())
+
+
+@pytest.mark.parametrize("name", ["C1", "LT"])
+def test_dual_pairing_inf_sup_from_gpu_mass(name):
+    """row f4, SPEC's stability surrogate (eq. 5): the pairing block of the first time step
+    read back from the GPU dual mass matrix (matvec on unit vectors) gives the oracle's discrete
+    inf-sup constant sqrt(3)/2 (equal elements: C1 and LT both have h = 1/4 on every side)"""
+    w = W.get(name)
+    om = O.OracleMesh(w)
+    m = S.Mesh.from_workload(w)
+    Md = m.assemble_M(S.MASS_DUAL)
+    ng = w.n_gamma
+    cols = []
+    for k in range(ng):
+        e = torch.zeros(w.n, dtype=torch.float64, device="cuda")
+        e[k] = 1.0
+        y = torch.empty_like(e)
+        Md.matvec(e, y)
+        cols.append(y[:ng].cpu().numpy())
+    Ms = np.stack(cols, 1) / (w.t_breaks[1] - w.t_breaks[0])
+    np.testing.assert_allclose(Ms, om.mass_dual()[:ng, :ng] / om.ht[0], rtol=1e-14, atol=1e-16)
+    wy, Uy = np.linalg.eigh(om.dual_gram())
+    B = (Uy @ np.diag(wy ** -0.5) @ Uy.T) @ Ms @ np.diag(om.seg_h ** -0.5)
+    assert np.linalg.svd(B, compute_uv=False).min() == pytest.approx(np.sqrt(3.0) / 2.0, rel=1e-12)
