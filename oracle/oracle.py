@@ -69,6 +69,7 @@ def lib():
         L.ora_pair.argtypes = [p, i, i, i, i, i, i, d, d, d, d]
         L.ora_potential.argtypes = [p, p, p, ll, p, i, p]
         L.ora_initial_rhs.argtypes = [p, i, p, i, p, p, i, i, i, p]
+        L.ora_potential_initial.argtypes = [p, i, p, i, p, p, ll, p, i, p]
         _lib = L
     return _lib
 
@@ -217,6 +218,18 @@ class OracleMesh:
         out = np.empty(len(pts))
         lib().ora_potential(self.h, w.ctypes.data, g.ctypes.data, len(pts), pts.ctypes.data, int(q),
                             out.ctypes.data)
+        return out
+
+    def potential_initial(self, nodes, tris, u0, pts, q=8):
+        """(M~_0 u0)(x,t) = int_Omega U*(x - y, t) u0_h(y) dy at points pts[k] = (x1, x2, t) (eq. 2,
+        P:37-46): the initial-potential term of the representation formula (stbem_oracle.c)"""
+        nodes = np.ascontiguousarray(nodes, dtype=np.float64)
+        tris = np.ascontiguousarray(tris, dtype=np.int32)
+        u0 = np.ascontiguousarray(u0, dtype=np.float64)
+        pts = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1, 3)
+        out = np.empty(len(pts))
+        lib().ora_potential_initial(self.h, len(nodes), nodes.ctypes.data, len(tris), tris.ctypes.data,
+                                    u0.ctypes.data, len(pts), pts.ctypes.data, int(q), out.ctypes.data)
         return out
 
     # ------------------------------------------------ initial potential (f1)

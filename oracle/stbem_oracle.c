@@ -804,3 +804,55 @@ void ora_initial_rhs(const ora_mesh* m, int nnode, const double* nodes, int ntri
     free(node_sum);
   }
 }
+
+
+/* ------------------------------------------- initial potential in Q (row f2) --- */
+/* (M~_0 u0)(x, t) = int_Omega U*(x - y, t) u0_h(y) dy (eq. 2), U*(z, t) =
+ * alpha / (4 pi t) exp(-alpha |z|^2 / (4 t)), u0_h linear on each triangle.  Every
+ * triangle V0 + u e1 + v e2 by the collapsed map u = xi (1 - eta), v = xi eta (Jacobian xi)
+ * with q x q Gauss points on each of ns x ns equal cells of [0,1]^2, ns = ceil(2 l / ell),
+ * l = longest edge, ell = sqrt(4 t / alpha) (the Gaussian's width; reading R24).  No
+ * truncation.  out[k] = value at pts[k] = (x1, x2, t), t > 0. */
+void ora_potential_initial(const ora_mesh* m, int nnode, const double* nodes, int ntri, const int* tri,
+                           const double* u0, long long npts, const double* pts, int q, double* out) {
+  (void)nnode;
+  init_rules();
+  const ora_rule* R = &RULES[q];
+  const double alpha = m->alpha;
+#pragma omp parallel for schedule(dynamic)
+  for (long long k = 0; k < npts; ++k) {
+    const double x1 = pts[3 * k], x2 = pts[3 * k + 1], t = pts[3 * k + 2];
+    const double ell = sqrt(4.0 * t / alpha), pref = alpha / (4.0 * ORA_PI * t);
+    double acc = 0.0;
+    for (int e = 0; e < ntri; ++e) {
+      const int i0 = tri[3 * e], i1 = tri[3 * e + 1], i2 = tri[3 * e + 2];
+      const double ax = nodes[2 * i0], ay = nodes[2 * i0 + 1];
+      const double e1x = nodes[2 * i1] - ax, e1y = nodes[2 * i1 + 1] - ay;
+      const double e2x = nodes[2 * i2] - ax, e2y = nodes[2 * i2 + 1] - ay;
+      const double area2 = fabs(e1x * e2y - e1y * e2x);
+      double l = sqrt(e1x * e1x + e1y * e1y);
+      double l2 = sqrt(e2x * e2x + e2y * e2y), l3 = sqrt((e2x - e1x) * (e2x - e1x) + (e2y - e1y) * (e2y - e1y));
+      if (l2 > l) l = l2;
+      if (l3 > l) l = l3;
+      int ns = (int)ceil(2.0 * l / ell);
+      if (ns < 1) ns = 1;
+      double tri_sum = 0.0;
+      for (int cx = 0; cx < ns; ++cx)
+        for (int a1 = 0; a1 < q; ++a1) {
+          const double xi = (cx + R->x[a1]) / ns;
+          for (int cy = 0; cy < ns; ++cy)
+            for (int a2 = 0; a2 < q; ++a2) {
+              const double eta = (cy + R->x[a2]) / ns;
+              const double u = xi * (1.0 - eta), v = xi * eta;
+              const double yx = ax + u * e1x + v * e2x, yy = ay + u * e1y + v * e2y;
+              const double uh = (1.0 - u - v) * u0[i0] + u * u0[i1] + v * u0[i2];
+              const double dx = x1 - yx, dy = x2 - yy;
+              tri_sum += R->w[a1] * R->w[a2] / ((double)ns * ns) * xi * uh *
+                         exp(-alpha * (dx * dx + dy * dy) / (4.0 * t));
+            }
+        }
+      acc += area2 * tri_sum;
+    }
+    out[k] = pref * acc;
+  }
+}

@@ -450,3 +450,35 @@ def test_table1_density_converges():
         err, ref = om.l2_error(wh, exact=lambda x, n, t: T.exact_neumann(x, n, t))
         errs.append(err / ref)
     assert errs[0] > 1.5 * errs[1] > 2.25 * errs[2], errs
+
+
+# ------------------------------------------- initial potential in Q (row f2, u0 != 0)
+def _gauss_moments(x, sigma):
+    """int_0^1 N(y; x, sigma^2) dy and int_0^1 y N(y; x, sigma^2) dy (closed forms)"""
+    from scipy.special import erf
+    s2 = np.sqrt(2.0) * sigma
+    P = 0.5 * (erf((1.0 - x) / s2) + erf(x / s2))
+    m1 = x * P + sigma / np.sqrt(2.0 * np.pi) * (np.exp(-x * x / (2 * sigma * sigma)) - np.exp(-(1 - x) ** 2 / (2 * sigma * sigma)))
+    return P, m1
+
+
+@pytest.mark.parametrize("t", [0.5, 0.05, 0.002])
+def test_initial_potential_in_Q_closed_forms(t):
+    """(M~_0 u0)(x, t) = int_Omega U*(x - y, t) u0(y) dy on the unit square for u0 = 1 and u0 = y1
+    (both in S_h^1, so the triangulation is exact): U* is the product of two 1-D Gaussians of
+    variance 2t/alpha, the integrals are erf products and first Gaussian moments; small t makes
+    the Gaussian narrower than the triangles (composite cells)"""
+    import workloads.table1 as T
+    w = T.table1(3)
+    om = O.OracleMesh(w)
+    nodes, tris = T.triangulation(w)
+    alpha = w.alpha
+    sigma = np.sqrt(2.0 * t / alpha)
+    pts = np.array([[0.5, 0.5, t], [0.3, 0.8, t], [0.05, 0.6, t]])
+    one = om.potential_initial(nodes, tris, np.ones(len(nodes)), pts)
+    lin = om.potential_initial(nodes, tris, nodes[:, 0].copy(), pts)
+    for k, (x1, x2, _) in enumerate(pts):
+        P1, M1 = _gauss_moments(x1, sigma)
+        P2, _ = _gauss_moments(x2, sigma)
+        assert one[k] == pytest.approx(P1 * P2, rel=1e-12), (t, k)
+        assert lin[k] == pytest.approx(M1 * P2, rel=1e-11, abs=1e-15), (t, k)
