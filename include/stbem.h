@@ -248,6 +248,17 @@ bem_status bem_rhs_initial(const bem_mesh* mesh, int n_nodes, const double* node
  * Errors: BEM_E_INVALID (bad argument, or a point closer than h_max to Gamma), BEM_E_CUDA. */
 bem_status bem_eval_potential(const bem_mesh* mesh, const double* w_dev, const double* g_dev,
                               long long npts, const double* pts_dev, double* u_dev, bem_stream stream);
+/* Initial potential of the representation formula (eq. 2; row f2 with u0 != 0):
+ * u_dev[k] += (M~_0 u0)(x_k, t_k) = int_Omega U*(x_k - y, t_k) u0_h(y) dy, U*(z,t) = alpha/(4 pi t)
+ * exp(-alpha |z|^2 / (4t)), u0_h in S_h^1 on the triangulation (nodes_xy, tris: host, as in
+ * bem_rhs_initial; u0_dev: device, one value per node).  Add it to the result of
+ * bem_eval_potential for the full u = M~_0 u0 + Vt w - W g.  pts_dev: npts x 3 (x1, x2, t > 0),
+ * device.  Collapsed Gauss (order 6) per triangle on ceil(l / ell)^2 cells, ell = sqrt(4 t/alpha)
+ * (reading R24); triangles farther than 7 ell skipped.  Synchronises the stream.
+ * Errors: BEM_E_INVALID (bad argument, index out of range, t <= 0), BEM_E_CUDA. */
+bem_status bem_eval_potential_initial(const bem_mesh* mesh, int n_nodes, const double* nodes_xy, int n_tri,
+                                      const int* tris, const double* u0_dev, long long npts,
+                                      const double* pts_dev, double* u_dev, bem_stream stream);
 bem_status bem_solve_gmres(const bem_matrix* V, const bem_matrix* D, const bem_matrix* M,
                            const double* b_dev, double* w_dev, const bem_gmres_opts* opts,
                            bem_solve_report* report, double* res_hist_host, bem_stream stream);

@@ -333,6 +333,19 @@ bem_status bem_eval_potential(const bem_mesh* m, const double* w, const double* 
   return eval_potential(m, w, g, npts, pts, u, S(s));
 }
 
+bem_status bem_eval_potential_initial(const bem_mesh* m, int n_nodes, const double* nodes_xy, int n_tri,
+                                      const int* tris, const double* u0, long long npts, const double* pts,
+                                      double* u, bem_stream s) {
+  if (!m || n_nodes < 3 || n_tri < 1 || !nodes_xy || !tris || !u0 || npts < 0 || (npts > 0 && (!pts || !u))) {
+    set_error("bem_eval_potential_initial: bad argument");
+    return BEM_E_INVALID;
+  }
+  for (int k = 0; k < 3 * n_tri; ++k)
+    if (tris[k] < 0 || tris[k] >= n_nodes) { set_error("bem_eval_potential_initial: triangle index out of range"); return BEM_E_INVALID; }
+  cudaSetDevice(m->device);
+  return eval_potential_initial(m, n_nodes, nodes_xy, n_tri, tris, u0, npts, pts, u, S(s));
+}
+
 bem_status bem_eval_special(int which, long long count, const double* x, double* out, bem_stream s) {
   if (which < 0 || which > 3 || count < 0) { set_error("bem_eval_special: bad argument"); return BEM_E_INVALID; }
   return eval_special(which, count, x, out, S(s));

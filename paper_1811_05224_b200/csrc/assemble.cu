@@ -621,6 +621,40 @@ bem_status eval_potential(const bem_mesh* m, const double* w, const double* g, l
   return BEM_OK;
 }
 
+// row f2 with u0 != 0: u += (M~_0 u0)(x, t) at interior points; nodes / tris on the host
+bem_status eval_potential_initial(const bem_mesh* m, int nnode, const double* nodes, int ntri, const int* tris,
+                                  const double* u0, long long npts, const double* pts, double* out,
+                                  cudaStream_t st) {
+  if (npts <= 0) return BEM_OK;
+  mesh_wait(m, st);
+  double* d_nodes = nullptr;
+  int* d_tris = nullptr;
+  int* d_bad = nullptr;
+  cudaError_t e;
+  if ((e = cudaMallocAsync((void**)&d_nodes, sizeof(double) * 2 * nnode, st)) != cudaSuccess ||
+      (e = cudaMallocAsync((void**)&d_tris, sizeof(int) * 3 * ntri, st)) != cudaSuccess ||
+      (e = cudaMallocAsync((void**)&d_bad, sizeof(int), st)) != cudaSuccess ||
+      (e = cudaMemsetAsync(d_bad, 0, sizeof(int), st)) != cudaSuccess ||
+      (e = cudaMemcpyAsync(d_nodes, nodes, sizeof(double) * 2 * nnode, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
+      (e = cudaMemcpyAsync(d_tris, tris, sizeof(int) * 3 * ntri, cudaMemcpyHostToDevice, st)) != cudaSuccess)
+    return cuda_fail(e, "eval_potential_initial");
+  const unsigned nblk = (unsigned)((npts * 32 + 127) / 128);
+  k_potential_initial<<<nblk, 128, 0, st>>>(d_nodes, d_tris, ntri, u0, m->alpha, npts, pts, out, d_bad);
+  count_launch();
+  int bad = 0;
+  cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(d_nodes, st);
+  cudaFreeAsync(d_tris, st);
+  cudaFreeAsync(d_bad, st);
+  e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "eval_potential_initial");
+  if (bad) {
+    set_error("bem_eval_potential_initial: a point has t <= 0");
+    return BEM_E_INVALID;
+  }
+  return BEM_OK;
+}
+
 // row f1: b <- b - M_h^0 u0 (eq. 4); nodes / tris on the host, u0 and b on the device
 bem_status initial_rhs(const bem_mesh* m, int nnode, const double* nodes, int ntri, const int* tris,
                        const double* u0, int qx, int qtf, int qtn, double* b, cudaStream_t st) {

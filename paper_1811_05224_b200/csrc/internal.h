@@ -207,6 +207,9 @@ bem_status mass_apply(const bem_matrix* M, double a, const double* x, double b, 
 bem_status mass_solve(const bem_matrix* M, int transpose, const double* x, double* y,
                       cudaStream_t st);
 bem_status eval_special(int which, long long n, const double* x, double* out, cudaStream_t st);
+bem_status eval_potential_initial(const bem_mesh* m, int nnode, const double* nodes, int ntri, const int* tris,
+                                  const double* u0, long long npts, const double* pts, double* out,
+                                  cudaStream_t st);
 bem_status initial_rhs(const bem_mesh* m, int nnode, const double* nodes, int ntri, const int* tris,
                        const double* u0, int qx, int qtf, int qtn, double* b, cudaStream_t st);
 bem_status eval_potential(const bem_mesh* m, const double* w, const double* g, long long npts,

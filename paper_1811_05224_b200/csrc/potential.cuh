@@ -87,4 +87,62 @@ __global__ void __launch_bounds__(128) k_potential(const Seg* __restrict__ seg, 
   if (lane == 0) out[k] = vw - wg;
 }
 
+// Initial potential of the representation formula (eq. 2; row f2 with u0 != 0):
+//   u(x,t) += (M~_0 u0)(x,t) = int_Omega U*(x - y, t) u0_h(y) dy,  U*(z,t) = alpha/(4 pi t) e^{-alpha |z|^2/(4t)}.
+// Warp per point, lanes over the triangles.  Each triangle by the collapsed Gauss rule of order 6 on
+// ns x ns cells, ns = ceil(l / ell), ell = sqrt(4 t / alpha) the Gaussian's width (reading R24);
+// triangles whose distance from x exceeds 7 ell are skipped (their integrand is below
+// e^{-49} = 5e-22 of the peak).  Points with t <= 0 set *bad.
+__global__ void __launch_bounds__(128) k_potential_initial(const double* __restrict__ nodes,
+                                                          const int* __restrict__ tris, int ntri,
+                                                          const double* __restrict__ u0, double alpha,
+                                                          long long npts, const double* __restrict__ pts,
+                                                          double* __restrict__ out, int* bad) {
+  const long long p = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (p >= npts) return;                                  // warp-uniform
+  const double x1 = pts[3 * p], x2 = pts[3 * p + 1], t = pts[3 * p + 2];
+  if (!(t > 0.0)) {
+    if (lane == 0) atomicExch(bad, 1);
+    return;
+  }
+  constexpr int Q = 6;
+  const double ell = sqrt(4.0 * t / alpha), ia = alpha / (4.0 * t);
+  double acc = 0.0;
+  for (int e = lane; e < ntri; e += 32) {
+    const int i0 = tris[3 * e], i1 = tris[3 * e + 1], i2 = tris[3 * e + 2];
+    const double ax = nodes[2 * i0], ay = nodes[2 * i0 + 1];
+    const double e1x = nodes[2 * i1] - ax, e1y = nodes[2 * i1 + 1] - ay;
+    const double e2x = nodes[2 * i2] - ax, e2y = nodes[2 * i2 + 1] - ay;
+    const double l = sqrt(fmax(fmax(e1x * e1x + e1y * e1y, e2x * e2x + e2y * e2y),
+                               (e2x - e1x) * (e2x - e1x) + (e2y - e1y) * (e2y - e1y)));
+    // distance from x to the triangle >= distance to the centroid - circumradius bound (l)
+    const double gx = ax + (e1x + e2x) / 3.0 - x1, gy = ay + (e1y + e2y) / 3.0 - x2;
+    if (sqrt(gx * gx + gy * gy) - l > 7.0 * ell) continue;
+    const double u0a = u0[i0], u0b = u0[i1], u0c = u0[i2];
+    const int ns = min(64, max(1, (int)ceil(l / ell)));
+    const double ins = 1.0 / ns;
+    double ts = 0.0;
+    for (int cx = 0; cx < ns; ++cx)
+#pragma unroll
+      for (int a1 = 0; a1 < Q; ++a1) {
+        const double xi = (cx + c_gx[Q][a1]) * ins, wx = c_gw[Q][a1] * xi;
+        double row = 0.0;
+        for (int cy = 0; cy < ns; ++cy)
+#pragma unroll
+          for (int a2 = 0; a2 < Q; ++a2) {
+            const double eta = (cy + c_gx[Q][a2]) * ins;
+            const double u = xi * (1.0 - eta), v = xi * eta;
+            const double dx = x1 - (ax + u * e1x + v * e2x), dy = x2 - (ay + u * e1y + v * e2y);
+            const double uh = fma(u, u0b - u0a, fma(v, u0c - u0a, u0a));
+            row = fma(c_gw[Q][a2] * uh, exp(-ia * (dx * dx + dy * dy)), row);
+          }
+        ts = fma(wx, row, ts);
+      }
+    acc = fma(fabs(e1x * e2y - e1y * e2x) * ins * ins, ts, acc);
+  }
+  acc = warp_sum(acc);
+  if (lane == 0) out[p] += alpha / (4.0 * STB_PI * t) * acc;
+}
+
 }  // namespace stb

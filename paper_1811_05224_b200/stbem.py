@@ -109,6 +109,7 @@ _SIGS = {
     "bem_rhs_fused": (I, [P, P, P, P, P, P, P]),
     "bem_assemble_toeplitz": (I, [P, I, P, P, PP]),
     "bem_eval_potential": (I, [P, P, P, LL, P, P, P]),
+    "bem_eval_potential_initial": (I, [P, I, P, I, P, P, LL, P, P, P]),
     "bem_rhs_initial": (I, [P, I, P, I, P, P, I, I, I, P, P]),
     "bem_solve_gmres": (I, [P, P, P, P, P, ctypes.POINTER(GmresOpts), ctypes.POINTER(SolveReport), P, P]),
     "bem_matrix_get": (I, [P, LL, LL, LL, LL, P]),
@@ -361,6 +362,19 @@ def eval_potential(mesh, w, g, pts, out=None, stream=None):
     pts = pts.contiguous().reshape(-1, 3)
     out = out if out is not None else torch.empty(pts.shape[0], dtype=torch.float64, device=w.device)
     check(lib().bem_eval_potential(mesh.h, _ptr(w), _ptr(g), pts.shape[0], _ptr(pts), _ptr(out), _stream(stream)))
+    return out
+
+
+def eval_potential_initial(mesh, nodes, tris, u0, pts, out, stream=None):
+    """out += (M~_0 u0)(x, t) at points pts (npts x 3: x1, x2, t > 0) (bem_eval_potential_initial);
+    nodes (M, 2), tris (T, 3) host arrays, u0 nodal on the device"""
+    import torch
+    nodes = np.ascontiguousarray(nodes, dtype=np.float64)
+    tris = np.ascontiguousarray(tris, dtype=np.int32)
+    pts = pts if isinstance(pts, torch.Tensor) else torch.tensor(pts, dtype=torch.float64, device=out.device)
+    pts = pts.contiguous().reshape(-1, 3)
+    check(lib().bem_eval_potential_initial(mesh.h, len(nodes), nodes.ctypes.data, len(tris), tris.ctypes.data,
+                                           _ptr(u0), pts.shape[0], _ptr(pts), _ptr(out), _stream(stream)))
     return out
 
 

@@ -608,3 +608,50 @@ def test_dual_pairing_inf_sup_from_gpu_mass(name):
     wy, Uy = np.linalg.eigh(om.dual_gram())
     B = (Uy @ np.diag(wy ** -0.5) @ Uy.T) @ Ms @ np.diag(om.seg_h ** -0.5)
     assert np.linalg.svd(B, compute_uv=False).min() == pytest.approx(np.sqrt(3.0) / 2.0, rel=1e-12)
+
+
+@pytest.mark.parametrize("t", [0.5, 0.05, 0.002])
+def test_potential_initial_parity(t):
+    """row f2 with u0 != 0: the initial potential (M~_0 u0)(x, t) of the representation formula on
+    the GPU against the oracle (the paper's u0 on the Table-1 triangulation, L = 3); small t makes
+    the Gaussian narrower than the triangles (composite cells)"""
+    import workloads.table1 as T
+    w = T.table1(3)
+    om = O.OracleMesh(w)
+    nodes, tris = T.triangulation(w)
+    u0 = T.initial_nodes(w)
+    pts = np.array([[0.5, 0.5, t], [0.3, 0.8, t], [0.05, 0.6, t], [0.9, 0.1, t]])
+    ref = om.potential_initial(nodes, tris, u0, pts)
+    m = S.Mesh.from_workload(w)
+    out = torch.zeros(len(pts), dtype=torch.float64, device="cuda")
+    S.eval_potential_initial(m, nodes, tris, cuda(u0), cuda(pts), out)
+    assert relmax(out.cpu().numpy(), ref) <= 1e-11
+    with pytest.raises(S.BemError):
+        S.eval_potential_initial(m, nodes, tris, cuda(u0), cuda(np.array([[0.5, 0.5, 0.0]])), out[:1])
+
+
+def test_representation_formula_with_initial_datum_converges():
+    """SPEC's evaluate_interior example on the paper's Table-1 problem: u_h(x, t) =
+    (M~_0 u0)(x,t) + (Vt w_h)(x,t) - (W g)(x,t) at x = (0.5, 0.5), t = 0.5 after the solve approaches
+    u = e^{-t/alpha} sin(x . d) as L grows"""
+    import workloads.table1 as T
+    errs = []
+    for L in (2, 3, 4, 5):
+        w = T.table1(L)
+        m = S.Mesh.from_workload(w)
+        V, D, Mp, Md = m.assemble_V(), m.assemble_D(), m.assemble_M(S.MASS_PRIMAL), m.assemble_M(S.MASS_DUAL)
+        nodes, tris = T.triangulation(w)
+        u0 = cuda(T.initial_nodes(w))
+        g = cuda(T.dirichlet_data(w))
+        b = torch.empty_like(g)
+        S.rhs_fused(m, Mp, g, b)
+        S.rhs_initial(m, nodes, tris, u0, b)
+        wv = torch.zeros_like(g)
+        rep = S.solve_gmres(V, b, wv, D=D, M=Md, precond=2, rel_tol=1e-10, history=False)
+        assert rep["status"] == "OK"
+        pts = np.array([[0.5, 0.5, 0.5]])
+        u = S.eval_potential(m, wv, g, pts)
+        S.eval_potential_initial(m, nodes, tris, u0, cuda(pts), u)
+        exact = float(T.exact(pts[:, :2], 0.5)[0])
+        errs.append(abs(float(u.cpu().numpy()[0]) - exact) / abs(exact))
+    assert errs[-1] < 0.25 * errs[0] and all(b < a for a, b in zip(errs, errs[1:])), errs
