@@ -337,9 +337,27 @@ static double lin(double v0, double v1, double f) { return v0 + (v1 - v0) * f; }
 /* Composite rules (reading R24): U* varies on the length ell = sqrt(4 min h_t / alpha)
  * at the smallest lag; elements longer than ell are integrated with ns = ceil(h / ell) equal cells
  * per direction (a Gauss rule of the given order in each cell). */
+static double pt_seg_dist(double px, double py, const ora_seg* S) {
+  double dx = S->bx - S->ax, dy = S->by - S->ay;
+  double f = ((px - S->ax) * dx + (py - S->ay) * dy) / (dx * dx + dy * dy);
+  if (f < 0.0) f = 0.0;
+  if (f > 1.0) f = 1.0;
+  double qx = S->ax + f * dx - px, qy = S->ay + f * dy - py;
+  return sqrt(qx * qx + qy * qy);
+}
+/* distance of two non-crossing segments: the smallest endpoint-to-segment distance */
+static double seg_seg_dist(const ora_seg* X, const ora_seg* Y) {
+  double d = pt_seg_dist(X->ax, X->ay, Y), e;
+  if ((e = pt_seg_dist(X->bx, X->by, Y)) < d) d = e;
+  if ((e = pt_seg_dist(Y->ax, Y->ay, X)) < d) d = e;
+  if ((e = pt_seg_dist(Y->bx, Y->by, X)) < d) d = e;
+  return d;
+}
+/* pairs farther apart than 8 ell keep the plain rule: U* there is below e^{-64} of its peak at
+ * the smallest lag and varies on the scale of its distance at the larger ones */
 static int ora_cells(const ora_mesh* m, const ora_seg* X, const ora_seg* Y) {
   double hm = X->h > Y->h ? X->h : Y->h;
-  if (!(m->ell > 0.0) || hm <= m->ell) return 1;
+  if (!(m->ell > 0.0) || hm <= m->ell || seg_seg_dist(X, Y) >= 8.0 * m->ell) return 1;
   int ns = (int)ceil(hm / m->ell);
   return ns > 24 ? 24 : ns;
 }
