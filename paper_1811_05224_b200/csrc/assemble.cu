@@ -370,6 +370,7 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bul
   const long long npairs = (long long)ng * ng;
   const long long nsrec = 5LL * ng;
   const int nf = kind == STB_D ? rec_fields<STB_D>() : rec_fields<STB_V>();
+  const int nfn = kind == STB_D ? rec_fields_near<STB_D>() : rec_fields_near<STB_V>();   // + regime B2
   // touching pairs through moment records (regime A) when every touching sub-pair satisfies
   // c_max / min h_t < 4 with c_max <= alpha (h_X + h_Y)^2 / 4; otherwise the per-lag k_sing
   const bool fused_sing = touching_records_ok(kind, m, flags);
@@ -395,7 +396,7 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bul
   }
   double* d_rec = nullptr;
   unsigned long long* d_ctr = nullptr;
-  const size_t rec_bytes = sizeof(double) * nf * (2 * npairs + nsrec);
+  const size_t rec_bytes = sizeof(double) * ((size_t)nf * (npairs + nsrec) + (size_t)nfn * npairs);
   if ((e = storage_acquire(m->device, rec_bytes, st, (void**)&d_rec)) != cudaSuccess ||
       (e = cudaMallocAsync((void**)&d_ctr, sizeof(unsigned long long) * 15, st)) != cudaSuccess ||
       (e = cudaMemsetAsync(d_ctr, 0, sizeof(unsigned long long) * 15, st)) != cudaSuccess) {
@@ -422,9 +423,19 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bul
   MB.ell = m->htmin > 0.0 ? std::sqrt(4.0 * m->htmin / m->alpha) : 0.0;
   MomArgs MN = MB;
   MN.rec = d_rec + (long long)nf * npairs;
+  // the near cells' nodes: s = t_{a+1} - t_a and t_{a+1} - t_{a-1} (and t_a - t_{a-1})
+  {
+    double smin = 1e300, smax = 0.0;
+    for (int a = 0; a < m->nt; ++a) {
+      smin = std::min(smin, m->t[a + 1] - m->t[a]);
+      smax = std::max(smax, m->t[a + 1] - m->t[a > 0 ? a - 1 : a]);
+    }
+    MN.u_near[0] = 1.0 / smax;
+    MN.u_near[1] = 1.0 / smin;
+  }
   MN.counters = d_ctr + 5;
   MomArgs MS = MB;
-  MS.rec = d_rec + 2LL * nf * npairs;
+  MS.rec = d_rec + (long long)nf * npairs + (long long)nfn * npairs;
   MS.npairs = nsrec;
   MS.counters = d_ctr + 10;
   // opt-in DMMA bulk kernel (BEM_QUAD_BULK_MMA or env BEM_BULK_MMA for the probes) and its basis

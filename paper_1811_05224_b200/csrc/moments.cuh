@@ -26,6 +26,7 @@
 // The records (moments and constants) depend on the spatial pair only: built once per
 // assembly by k_records, reused by every block, band and time node.
 #pragma once
+#include <type_traits>
 
 #include "moment_coeffs.h"
 
@@ -48,6 +49,12 @@ template <> struct Fams<STB_V> { static constexpr int n = 1, f0 = FAM_H, f1 = -1
 template <> struct Fams<STB_K> { static constexpr int n = 1, f0 = FAM_Q, f1 = -1; };
 template <> struct Fams<STB_D> { static constexpr int n = 2, f0 = FAM_H, f1 = FAM_F; };
 template <int KIND> constexpr int rec_fields() { return RF_COMMON + Fams<KIND>::n * FAMSZ; }
+// near records append a second regime-B cluster (regime B2): c0, 1/c0, order and
+// split point c_s of the cluster c > c_s, then per family its two coefficient arrays (m_0 and m_1
+// in their last slots, as for the first cluster)
+enum { R2_C0 = 0, R2_IC0 = 1, R2_KB = 2, R2_CS = 3, R2_FAM = 4, R2_FAMSZ = 2 * (MKB + 1) };
+template <int KIND> constexpr int rec2_base() { return rec_fields<KIND>(); }
+template <int KIND> constexpr int rec_fields_near() { return rec_fields<KIND>() + R2_FAM + Fams<KIND>::n * R2_FAMSZ; }
 
 static __device__ __constant__ const double STB_INV[MKB + 2] = {
     0.0, 1.0, 1.0 / 2, 1.0 / 3, 1.0 / 4, 1.0 / 5, 1.0 / 6, 1.0 / 7,
@@ -78,6 +85,7 @@ struct MomArgs {
   int q;                  // bulk Gauss order (bulk records)
   int qfar;               // near-cell order of well-separated pairs (near records)
   unsigned long long* counters;  // node evaluations per regime: A, B, Z, C
+  double u_near[2];       // near records: smallest and largest 1/s of the near-cell nodes
   double ell;             // sqrt(4 min h_t / alpha): the length on which U* varies at the
                           // smallest lag; sub-pairs closer than 8 ell get composite rules with
                           // cells of at most ell (no subdivision while kappa <= 1)
@@ -286,11 +294,32 @@ __global__ void __launch_bounds__(128) k_records(MomArgs M) {
 #pragma unroll
     for (int f = 0; f < NF; ++f) C0[f] = C1[f] = 0.0;
   }
-  const double c0m = 0.5 * (cmin + cmax);
-  const bool okB = cmin > 0.0 && (cmax - c0m) <= MRHO * c0m;
+  double c0m = 0.5 * (cmin + cmax);
+  bool okB = cmin > 0.0 && (cmax - c0m) <= MRHO * c0m;
+  // near records: a cluster too wide for one Taylor centre (c_max > 3 c_min) but within 9 c_min is
+  // split at c_s = sqrt(c_min c_max) into two clusters of ratio <= 3 each (regime B2)
+  // (only when a near-cell node can fall between regime A and regime Z for this pair)
+  const bool two = NEAR && !okB && cmin > 0.0 && cmax <= 8.99 * cmin && cmax * M.u_near[1] >= STB_MXA &&
+                   cmin * M.u_near[0] < MXZ;
+  const double cs = two ? sqrt(cmin * cmax) : 0.0;
+  if (two) {
+    c0m = 0.5 * (cmin + cs);
+    okB = true;
+  }
   const double c0 = okB ? c0m : 0.0;
-  const double rho = okB ? (cmax - c0m) / c0m : 1.0;
+  const double cup = two ? cs : cmax;                       // upper end of the first cluster
+  const double rho = okB ? (cup - c0m) / c0m : 1.0;
   const int kb = (!okB || rho <= 1e-6) ? 3 : min(MKB, max(3, (int)ceil(log(1e-16) / log(rho))));
+  const double c0b = two ? 0.5 * (cs + cmax) : 0.0;
+  const double rhob = two ? (cmax - c0b) / c0b : 1.0;
+  const int kbb = two ? (rhob <= 1e-6 ? 3 : min(MKB, max(3, (int)ceil(log(1e-16) / log(rhob))))) : 0;
+  if (NEAR) {
+    double* R2 = rec + (long long)rec2_base<KIND>() * S;
+    R2[R2_C0 * S] = c0b;
+    R2[R2_IC0 * S] = two ? 1.0 / c0b : 0.0;
+    R2[R2_KB * S] = (double)kbb;
+    R2[R2_CS * S] = cs;
+  }
   rec[RF_CMAX * S] = cmax;
   rec[RF_CMIN * S] = cmin;
   rec[RF_C0 * S] = c0;
@@ -308,23 +337,30 @@ __global__ void __launch_bounds__(128) k_records(MomArgs M) {
     R[FC0 * S] = C0[f];
     R[FC1 * S] = C1[f];
   }
-#pragma unroll 1
-  for (int slot = 0; slot < NF; ++slot) {
+  // one pass per family and cluster (CL: 0 = c <= c_s or the only cluster, 1 = c > c_s)
+  auto bpass = [&](const int slot, auto CLc) {
+    constexpr int cl = decltype(CLc)::value;
     const int fam = slot == 0 ? Fams<KIND>::f0 : Fams<KIND>::f1;
-    double* R = rec + (RF_COMMON + slot * FAMSZ) * S;
-    // regime B: m_k = sum W (c - c0)^k, only the orders the evaluation reads (k <= kb): chunks of
-    // 8 with a per-thread exit, four independent power chains
+    // coefficient arrays: FB1 / FB2 of the family (cluster 0) or of the B2 block (cluster 1)
+    double* P1 = cl == 0 ? rec + (RF_COMMON + slot * FAMSZ + FB1) * S
+                         : rec + (long long)(rec2_base<KIND>() + R2_FAM + slot * R2_FAMSZ) * S;
+    double* P2 = cl == 0 ? rec + (RF_COMMON + slot * FAMSZ + FB2) * S : P1 + (long long)(MKB + 1) * S;
+    const double cc0 = cl == 0 ? c0 : c0b;
+    const int ckb = cl == 0 ? kb : kbb;
+    // regime B: m_k = sum W (c - c0)^k over the cluster's points, only the orders the evaluation
+    // reads (k <= kb): chunks of 8 with a per-thread exit, four independent power chains
     double mb[MKB + 1];
 #pragma unroll
     for (int k = 0; k <= MKB; ++k) mb[k] = 0.0;
     if (okB) {
       for_points<KIND, NEAR>(M, I, J, [&](double c, double wa, double wb) {
+        if (cl == 1 ? !(c > cs) : (two && c > cs)) return;
         const double w = slot == 0 ? wa : wb;
-        const double d = c - c0, d2 = d * d, d4 = d2 * d2;
+        const double d = c - cc0, d2 = d * d, d4 = d2 * d2;
         double p0 = w, p1 = w * d, p2 = w * d2, p3 = p1 * d2;
 #pragma unroll
         for (int kc = 0; kc <= MKB / 8; ++kc) {
-          if (kc * 8 > kb) break;
+          if (kc * 8 > ckb) break;
 #pragma unroll
           for (int j = 0; j < 8; j += 4) {
             const int k = kc * 8 + j;
@@ -343,34 +379,40 @@ __global__ void __launch_bounds__(128) k_records(MomArgs M) {
     // regime-B polynomial coefficients: every Taylor sum of phi_bz is
     // e^{-x0} sum_i coef_i (-u)^i with per-pair coefficients from backward recurrences over the
     // shifted moments (B1_k = m_k / k, B2_k = m_k / ((k-1) k)):
-    //   S1:     G_i = (B1_{i+1} - G_{i+1}) / c0,  G_kb = 0,      coef G_i / i!  -> FB1[i], i < kb
-    //   S2 (H): H_i = (B2_{i+2} - H_{i+1}) / c0,  H_{kb-1} = 0,  coef H_i / i!  -> FB2[i], i < kb
-    //   S3 (Q): Q_i = (m_i - Q_{i+1}) / c0 (i >= 1), Q_0 = -Q_1 / c0, Q_{kb+1} = 0  -> FB2[i], i <= kb
-    //   m_0 -> FB1[MKB], m_1 -> FB2[MKB] (H)
+    //   S1:     G_i = (B1_{i+1} - G_{i+1}) / c0,  G_kb = 0,      coef G_i / i!  -> P1[i], i < kb
+    //   S2 (H): H_i = (B2_{i+2} - H_{i+1}) / c0,  H_{kb-1} = 0,  coef H_i / i!  -> P2[i], i < kb
+    //   S3 (Q): Q_i = (m_i - Q_{i+1}) / c0 (i >= 1), Q_0 = -Q_1 / c0, Q_{kb+1} = 0  -> P2[i], i <= kb
+    //   m_0 -> P1[MKB], m_1 -> P2[MKB] (H)
     {
-      const double ic0 = okB ? 1.0 / c0 : 0.0;
+      const double ic0 = okB ? 1.0 / cc0 : 0.0;
       double G = 0.0, H2 = 0.0, Q3 = 0.0;
 #pragma unroll
       for (int i = MKB; i >= 0; --i) {
-        if (fam == FAM_Q && i <= kb) {
+        if (fam == FAM_Q && i <= ckb) {
           Q3 = ((i >= 1 ? mb[i] : 0.0) - Q3) * ic0;
-          R[(FB2 + i) * S] = Q3 * STB_INVFACT[i];
+          P2[i * S] = Q3 * STB_INVFACT[i];
         }
-        if (i <= kb - 1) {
+        if (i <= ckb - 1) {
           G = (mb[i + 1 <= MKB ? i + 1 : MKB] * STB_INV_H[i + 1 <= MKB ? i + 1 : MKB] - G) * ic0;
-          R[(FB1 + i) * S] = G * STB_INVFACT[i];
+          P1[i * S] = G * STB_INVFACT[i];
           if (fam == FAM_H) {
-            if (i <= kb - 2) {
+            if (i <= ckb - 2) {
               const int k2 = i + 2 <= MKB ? i + 2 : MKB;
               H2 = (mb[k2] * STB_INV_H[k2 - 1] * STB_INV_H[k2] - H2) * ic0;
             }
-            R[(FB2 + i) * S] = i <= kb - 2 ? H2 * STB_INVFACT[i] : 0.0;
+            P2[i * S] = i <= ckb - 2 ? H2 * STB_INVFACT[i] : 0.0;
           }
         }
       }
-      R[(FB1 + MKB) * S] = mb[0];
-      if (fam == FAM_H) R[(FB2 + MKB) * S] = mb[1];
+      P1[MKB * S] = mb[0];
+      if (fam == FAM_H) P2[MKB * S] = mb[1];
     }
+  };
+#pragma unroll 1
+  for (int slot = 0; slot < NF; ++slot) bpass(slot, std::integral_constant<int, 0>{});
+  if (NEAR && two) {
+#pragma unroll 1
+    for (int slot = 0; slot < NF; ++slot) bpass(slot, std::integral_constant<int, 1>{});
   }
 }
 
@@ -509,6 +551,43 @@ __device__ __forceinline__ double gb3_cb(double t) { return horner<STB_GB3_DEG>(
 
 // TRUEV: return the true node value (near cells: without the affine terms, which then need not be
 // added here and subtracted again by the caller)
+// The Taylor sums of one regime-B cluster (centre c0, order kb, coefficient arrays p1 / p2 of the
+// first family and p3 of the second, m_0 / m_1 in their last slots): the non-affine node parts
+// T[f].  E1(x0) by the GB3 form for x0 >= 8/3 (every single-cluster node: x0 >= x_max / (1 + MRHO)),
+// by the general E1 below (the clusters of regime B2 may sit lower).
+template <int KIND>
+__device__ __forceinline__ void bz_T(const double* __restrict__ p1, const double* __restrict__ p2,
+                                     const double* __restrict__ p3, long long S, double c0, double ic0,
+                                     int kb, double s, double u, double (&T)[2]) {
+  const double x0 = c0 * u, ex = exp(-x0);
+  const double E1 = x0 >= 8.0 / 3.0 ? ex * (ic0 * s) * gb3_cb(ic0 * s) : dev_e1(x0);
+  // the Taylor sums as polynomials in z = -u (coefficients from k_records), Horner from the top
+  const double zu = -u;
+  double h1 = 0.0, h2 = Fams<KIND>::f0 == FAM_Q ? p2[(long long)kb * S] : 0.0, h3 = 0.0;
+  // coefficient pointers walked down by the record stride (no index multiply per load)
+  const long long top = (long long)(kb - 1) * S;
+  const double* q1 = p1 + top;
+  const double* q2 = p2 + top;
+  const double* q3 = p3 + top;
+#pragma unroll 2
+  for (int i = kb - 1; i >= 0; --i) {
+    h1 = fma(h1, zu, *q1);
+    if (Fams<KIND>::f0 != FAM_F) h2 = fma(h2, zu, *q2);
+    if (Fams<KIND>::n == 2) h3 = fma(h3, zu, *q3);
+    q1 -= S;
+    q2 -= S;
+    q3 -= S;
+  }
+  const double S1a = ex * h1, S2a = ex * h2, S1b = ex * h3;
+  const double a0 = ex * ic0;
+  const double m0 = p1[(long long)MKB * S];
+  if (Fams<KIND>::f0 == FAM_H) T[0] = fma(fma(1.0 + x0, E1, -ex), m0, fma(E1 * u, p2[(long long)MKB * S], -fma(u, S2a, S1a)));
+  else T[0] = fma(-E1, m0, fma(a0, m0, S2a) / u + S1a);
+  if (Fams<KIND>::n == 2) T[1] = fma(E1, p3[(long long)MKB * S], -S1b);
+}
+
+// TRUEV: return the true node value (near cells: without the affine terms, which then need not be
+// added here and subtracted again by the caller)
 template <int KIND, bool TRUEV = false>
 __device__ __forceinline__ double phi_bz(const double* __restrict__ rec, long long S, const RegBZ<KIND>& z,
                                          double s, double u, int* regime) {
@@ -519,37 +598,9 @@ __device__ __forceinline__ double phi_bz(const double* __restrict__ rec, long lo
   }
   double T[2] = {0.0, 0.0};
   if (!zz) {
-    // x0 = c0 u >= 4 / (1 + MRHO) = 8/3 (the GB3 fit range): E1(x0) = e^{-x0} t GB3(t), t = 1/x0 = s / c0
-    const double x0 = z.c0 * u, ic0 = z.ic0, ex = exp(-x0);
-    const double E1 = ex * (ic0 * s) * gb3_cb(ic0 * s);
     const double* R0 = rec + (RF_COMMON + 0 * FAMSZ) * S;
     const double* R1 = rec + (RF_COMMON + 1 * FAMSZ) * S;
-    // the Taylor sums as polynomials in z = -u (coefficients from k_records), Horner from the top
-    const double zu = -u;
-    const double* p1 = R0 + FB1 * S;
-    const double* p2 = R0 + FB2 * S;
-    const double* p3 = R1 + FB1 * S;
-    double h1 = 0.0, h2 = Fams<KIND>::f0 == FAM_Q ? p2[(long long)z.kb * S] : 0.0, h3 = 0.0;
-    // coefficient pointers walked down by the record stride (no index multiply per load)
-    const long long top = (long long)(z.kb - 1) * S;
-    const double* q1 = p1 + top;
-    const double* q2 = p2 + top;
-    const double* q3 = p3 + top;
-#pragma unroll 2
-    for (int i = z.kb - 1; i >= 0; --i) {
-      h1 = fma(h1, zu, *q1);
-      if (Fams<KIND>::f0 != FAM_F) h2 = fma(h2, zu, *q2);
-      if (Fams<KIND>::n == 2) h3 = fma(h3, zu, *q3);
-      q1 -= S;
-      q2 -= S;
-      q3 -= S;
-    }
-    const double S1a = ex * h1, S2a = ex * h2, S1b = ex * h3;
-    const double a0 = ex * ic0;
-    const double m0 = z.m0[0];
-    if (Fams<KIND>::f0 == FAM_H) T[0] = fma(fma(1.0 + x0, E1, -ex), m0, fma(E1 * u, z.m1, -fma(u, S2a, S1a)));
-    else T[0] = fma(-E1, m0, fma(a0, m0, S2a) / u + S1a);
-    if (Fams<KIND>::n == 2) T[1] = fma(E1, z.m0[1], -S1b);
+    bz_T<KIND>(R0 + FB1 * S, R0 + FB2 * S, R1 + FB1 * S, S, z.c0, z.ic0, z.kb, s, u, T);
   }
   *regime = zz ? 2 : 1;
   double out = 0.0;
@@ -560,6 +611,44 @@ __device__ __forceinline__ double phi_bz(const double* __restrict__ rec, long lo
     else if (fam == FAM_H) out += fma(s, T[f] + z.C0[f], z.C1[f]);
     else if (fam == FAM_F) out += T[f] + z.C0[f];
     else out += T[f] - fma(s, z.C1[f], z.C0[f]);
+  }
+  return out;
+}
+
+// regime B2 (near records): the two clusters c <= c_s and c > c_s, each with its own centre and
+// its own regime Z test; returns the true node value
+struct RegB2 {
+  double c0, ic0, cs;
+  int kb;
+  template <int KIND>
+  __device__ __forceinline__ void load(const double* __restrict__ rec, long long S) {
+    const double* R2 = rec + (long long)rec2_base<KIND>() * S;
+    c0 = R2[R2_C0 * S];
+    ic0 = R2[R2_IC0 * S];
+    kb = (int)R2[R2_KB * S];
+    cs = R2[R2_CS * S];
+  }
+};
+template <int KIND>
+__device__ __forceinline__ double phi_b2(const double* __restrict__ rec, long long S, const RegBZ<KIND>& z,
+                                         const RegB2& z2, double s, double u, int* regime) {
+  const bool zz1 = z.cmin * u >= MXZ, zz2 = z2.cs * u >= MXZ;
+  double T[2] = {0.0, 0.0}, T2[2] = {0.0, 0.0};
+  if (!zz1) {
+    const double* R0 = rec + (RF_COMMON + 0 * FAMSZ) * S;
+    const double* R1 = rec + (RF_COMMON + 1 * FAMSZ) * S;
+    bz_T<KIND>(R0 + FB1 * S, R0 + FB2 * S, R1 + FB1 * S, S, z.c0, z.ic0, z.kb, s, u, T);
+  }
+  if (!zz2) {
+    const double* B = rec + (long long)(rec2_base<KIND>() + R2_FAM) * S;
+    bz_T<KIND>(B, B + (long long)(MKB + 1) * S, B + (long long)R2_FAMSZ * S, S, z2.c0, z2.ic0, z2.kb, s, u, T2);
+  }
+  *regime = (zz1 && zz2) ? 2 : 1;
+  double out = 0.0;
+#pragma unroll
+  for (int f = 0; f < Fams<KIND>::n; ++f) {
+    const int fam = f == 0 ? Fams<KIND>::f0 : Fams<KIND>::f1;
+    out += fam == FAM_H ? s * (T[f] + T2[f]) : T[f] + T2[f];
   }
   return out;
 }
@@ -1200,6 +1289,8 @@ __global__ void __launch_bounds__(128) k_near_m(BlockArgs B, MomArgs M, int chun
   A.load(rec, S);
   RegBZ<KIND> Z;
   Z.load(rec, S);
+  RegB2 Z2;
+  Z2.load<KIND>(rec, S);
   unsigned long long nA = 0, nB = 0, nZ = 0, nC = 0, nK = 0;
   // node value for every lane (warp-uniform call: regime C is computed cooperatively)
   auto node = [&](int x, int y) -> double {
@@ -1212,9 +1303,9 @@ __global__ void __launch_bounds__(128) k_near_m(BlockArgs B, MomArgs M, int chun
       ++nA;
     } else {
       int reg = 0;
-      v = phi_bz<KIND, true>(rec, S, Z, nd.x, nd.z, &reg);
+      v = Z2.kb > 0 ? phi_b2<KIND>(rec, S, Z, Z2, nd.x, nd.z, &reg) : phi_bz<KIND, true>(rec, S, Z, nd.x, nd.z, &reg);
       nB += reg == 1;
-        nK += reg == 1 ? Z.kb : 0;
+        nK += reg == 1 ? Z.kb + Z2.kb : 0;
       nZ += reg == 2;
       if (reg == 3) {
         needC = true;
