@@ -43,6 +43,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     # uniform time steps only; avoids the dense work, reported as its own metric
     ap.add_argument("--variant", default="dense", choices=["dense", "toeplitz"])
+    ap.add_argument("--overlap", type=int, default=1)   # V_h, D_h assembled on side streams
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     return ap.parse_args()
 
@@ -155,6 +156,7 @@ def native(args):
     wv = torch.empty_like(g)
     tol = w.tol
     Mkind = S.MASS_DUAL_LUMPED if args.precond == 1 else S.MASS_DUAL
+    side = (torch.cuda.Stream(), torch.cuda.Stream())
 
     def barrier():
         if world > 1:
@@ -172,10 +174,21 @@ def native(args):
             gg = torch.empty_like(g)
             gg.copy_(g_host, non_blocking=True)
         toep = args.variant == "toeplitz"
-        V = mesh.assemble_toeplitz("V") if toep else mesh.assemble_V()
-        ev[1].record()
-        D = mesh.assemble_toeplitz("D") if toep else mesh.assemble_D()
-        ev[2].record()
+        cur = torch.cuda.current_stream()
+        if args.overlap:
+            # V_h and D_h on two side streams, concurrently with K_h g on the main stream: the
+            # three assemblies are independent; the solve waits for all of them
+            side[0].wait_stream(cur)
+            side[1].wait_stream(cur)
+            V = mesh.assemble_toeplitz("V", stream=side[0]) if toep else mesh.assemble_V(stream=side[0])
+            D = mesh.assemble_toeplitz("D", stream=side[1]) if toep else mesh.assemble_D(stream=side[1])
+            ev[1].record()
+            ev[2].record()
+        else:
+            V = mesh.assemble_toeplitz("V") if toep else mesh.assemble_V()
+            ev[1].record()
+            D = mesh.assemble_toeplitz("D") if toep else mesh.assemble_D()
+            ev[2].record()
         Mp = mesh.assemble_M(S.MASS_PRIMAL)
         Mc = mesh.assemble_M(Mkind) if args.precond else None
         if toep:
@@ -187,6 +200,9 @@ def native(args):
             # K_h is computed entry by entry and multiplied by g on the fly (never stored)
             st_K = S.rhs_fused(mesh, Mp, gg, b, stats=True)
         ev[3].record()
+        if args.overlap:
+            cur.wait_stream(side[0])
+            cur.wait_stream(side[1])
         ev[4].record()
         rep = S.solve_gmres(V, b, wv, D=D if args.precond else None, M=Mc, rel_tol=tol, max_iter=200,
                             precond=args.precond, history=False)
@@ -197,7 +213,8 @@ def native(args):
         ph["assemble_V"] = ev[0].elapsed_time(ev[1]) / 1e3
         ph["assemble_D"] = ev[1].elapsed_time(ev[2]) / 1e3
         ph["assemble_K"] = ev[2].elapsed_time(ev[3]) / 1e3     # fused K g (+ mass matrices)
-        ph["rhs"] = ev[3].elapsed_time(ev[4]) / 1e3
+        ph["rhs"] = ev[3].elapsed_time(ev[4]) / 1e3            # overlap: the wait for V_h, D_h
+        ph["assembly"] = ev[0].elapsed_time(ev[4]) / 1e3
         ph["solve"] = ev[4].elapsed_time(ev[5]) / 1e3
         ph["total"] = ev[0].elapsed_time(ev[5]) / 1e3
         stats = {k: A.stats() for k, A in zip("VD", (V, D))}
@@ -363,7 +380,7 @@ def native(args):
     gemv_total_ms = 1e3 * rep["seconds_matvec"]
     roofline = roof_gemv if gemv_total_ms >= ms_dom else roof_asm
     roofline = dict(roofline, share_of_step=(gemv_total_ms if roofline is roof_gemv else ms_dom) / ms)
-    asm_s = ph["assemble_V"] + ph["assemble_K"] + ph["assemble_D"]
+    asm_s = ph["assembly"]          # mesh -> V_h, D_h, K_h g all done (overlapped or not)
     out = {
         "metric": METRIC + (" [block-Toeplitz variant, SURVEY 8(f) f3]" if args.variant == "toeplitz" else ""),
         "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -380,7 +397,9 @@ def native(args):
             "matrix_entries_represented_per_s": represented_per_step / (1e-3 * ms),
             "storage": "V_h, D_h: symmetric packed spatial blocks (upper 32x32 tile triangle); K_h computed "
                        "and applied to g on the fly (bem_rhs_fused), never stored",
-            "assembly_s": {"V": ph["assemble_V"], "K": ph["assemble_K"], "D": ph["assemble_D"]},
+            "assembly_s": {"V": ph["assemble_V"], "K": ph["assemble_K"], "D": ph["assemble_D"], "all": ph["assembly"],
+                           "note": ("V_h and D_h on side streams concurrently with K_h g: the per-matrix "
+                                    "phases are enqueue marks, 'all' is the assembly time") if args.overlap else ""},
             "matvec_gbs": gemv_gbs, "matvec_frac_of_hbm": (gemv_gbs / hbm_peak) if gemv_gbs else None,
             "gmres_solve_s": ph["solve"], "gmres_iterations": rep["iterations"],
             "gmres_true_rel_residual": rep["true_rel_residual"], "time_to_solution_s": ph["total"],
