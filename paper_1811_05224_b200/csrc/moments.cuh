@@ -879,15 +879,25 @@ __global__ void __launch_bounds__(128, (KIND == STB_D || PROD) ? 2 : 3) k_bulk_m
 #pragma unroll
     for (int r = 0; r <= R; ++r) nd[r] = B.lag[min(r_lo + r, r_hi) * B.ldlag + y];
     unsigned bmask = 0;
+    // full columns (every band node above the trial node) whose smallest-lag node is in regime A
+    // for every lane: all nodes are (s grows with x), no masks or regime tests per node
+    // (not for V_h: its 3-CTA register budget would spill)
+    const bool full = KIND != STB_V && r_lo > y && r_hi - r_lo == R;       // CTA-uniform
+    if (full && __all_sync(0xffffffffu, A.cmax * nd[0].z < STB_MXA)) {
 #pragma unroll
-    for (int r = 0; r <= R; ++r) {
-      const int x = r_lo + r;
-      const double v = A.eval(nd[r].x, nd[r].y, nd[r].z);
-      const bool ok = x <= r_hi && x > y;
-      const bool inA = A.cmax * nd[r].z < STB_MXA;
-      phi[r] = ok ? v : 0.0;
-      nA += ok && inA;
-      if (ok && !inA) bmask |= 1u << r;
+      for (int r = 0; r <= R; ++r) phi[r] = A.eval(nd[r].x, nd[r].y, nd[r].z);
+      nA += R + 1;
+    } else {
+#pragma unroll
+      for (int r = 0; r <= R; ++r) {
+        const int x = r_lo + r;
+        const double v = A.eval(nd[r].x, nd[r].y, nd[r].z);
+        const bool ok = x <= r_hi && x > y;
+        const bool inA = A.cmax * nd[r].z < STB_MXA;
+        phi[r] = ok ? v : 0.0;
+        nA += ok && inA;
+        if (ok && !inA) bmask |= 1u << r;
+      }
     }
     if (__any_sync(0xffffffffu, bmask != 0)) {
       // the node values pass through shared memory while lanes overwrite their B / Z / C nodes
