@@ -655,3 +655,31 @@ def test_representation_formula_with_initial_datum_converges():
         exact = float(T.exact(pts[:, :2], 0.5)[0])
         errs.append(abs(float(u.cpu().numpy()[0]) - exact) / abs(exact))
     assert errs[-1] < 0.25 * errs[0] and all(b < a for a, b in zip(errs, errs[1:])), errs
+
+
+def test_bench_step_configuration_against_golden():
+    """the step exactly as bench.py launches it -- V_h and D_h assembled on two side streams while
+    K_h g runs fused on the main stream, exact dual-mass preconditioning, solve after both streams
+    are joined -- on C2 against the oracle's golden density"""
+    path = os.path.join(GOLDEN, "C2_oracle_w.npy")
+    if not os.path.exists(path):
+        pytest.skip("tests/golden/C2_oracle_w.npy missing")
+    wd = np.load(path)
+    w = W.get("C2")
+    m = S.Mesh.from_workload(w)
+    side = (torch.cuda.Stream(), torch.cuda.Stream())
+    cur = torch.cuda.current_stream()
+    for s_ in side:
+        s_.wait_stream(cur)
+    V = m.assemble_V(stream=side[0])
+    D = m.assemble_D(stream=side[1])
+    Mp, Md = m.assemble_M(S.MASS_PRIMAL), m.assemble_M(S.MASS_DUAL)
+    g = cuda(W.dirichlet_data(w))
+    b = torch.empty_like(g)
+    S.rhs_fused(m, Mp, g, b)
+    for s_ in side:
+        cur.wait_stream(s_)
+    wv = torch.zeros_like(g)
+    rep = S.solve_gmres(V, b, wv, D=D, M=Md, precond=2, rel_tol=w.tol, history=False)
+    assert rep["status"] == "OK"
+    assert relmax(wv.cpu().numpy(), wd) <= W_TOL
