@@ -683,3 +683,33 @@ def test_bench_step_configuration_against_golden():
     rep = S.solve_gmres(V, b, wv, D=D, M=Md, precond=2, rel_tol=w.tol, history=False)
     assert rep["status"] == "OK"
     assert relmax(wv.cpu().numpy(), wd) <= W_TOL
+
+
+@pytest.mark.parametrize("name", ["C3", "C5"])
+def test_full_size_step_properties(name):
+    """BJ configs at full size in the bench's launch configuration, checked through properties
+    that hold at any size: GMRES converges within the preconditioned iteration band of §6.2, the
+    true preconditioned residual meets the tolerance, and the density approaches the exact
+    Neumann datum (first order in h: relative L2(Sigma) error below that of C2)"""
+    w = W.get(name)
+    m = S.Mesh.from_workload(w)
+    side = (torch.cuda.Stream(), torch.cuda.Stream())
+    cur = torch.cuda.current_stream()
+    for s_ in side:
+        s_.wait_stream(cur)
+    V = m.assemble_V(stream=side[0])
+    D = m.assemble_D(stream=side[1])
+    Mp, Md = m.assemble_M(S.MASS_PRIMAL), m.assemble_M(S.MASS_DUAL)
+    g = cuda(W.dirichlet_data(w))
+    b = torch.empty_like(g)
+    S.rhs_fused(m, Mp, g, b)
+    for s_ in side:
+        cur.wait_stream(s_)
+    wv = torch.zeros_like(g)
+    rep = S.solve_gmres(V, b, wv, D=D, M=Md, precond=2, rel_tol=w.tol, history=False)
+    assert rep["status"] == "OK" and rep["iterations"] <= 16, rep
+    assert rep["true_rel_residual"] <= 2.0 * w.tol, rep
+    err, nrm = O.OracleMesh(w).l2_error(wv.cpu().numpy(), nq=4)
+    assert err / nrm < 0.0798, (err, nrm)          # C2: 0.0798 (P11)
+    for A in (V, D, Mp, Md):
+        A.close()
