@@ -71,7 +71,7 @@ typedef struct {
 /* Quadrature options; NULL = documented defaults.  0 = default. */
 typedef struct {
   int q_bulk;   /* Gauss order per direction for time cells d >= 2; 0 = chosen from kappa */
-  int q_sing;   /* order of the Duffy / 1-D reduction rules for touching pairs (default 12) */
+  int q_sing;   /* order of the Duffy / 1-D reduction rules for touching pairs (default 16) */
   int flags;    /* BEM_QUAD_LEGACY_SING: touching pairs by per-lag singular rules (k_sing) instead
                    of moment records; 0 = records whenever alpha (h_X+h_Y)^2 / (4 min h_t) < 4 */
 } bem_quad_opts;

@@ -362,10 +362,23 @@ static int ora_cells(const ora_mesh* m, const ora_seg* X, const ora_seg* Y) {
   return ns > 24 ? 24 : ns;
 }
 
+/* near cells (d <= 1) of disjoint pairs closer than their length (reading R25): the true kernel
+ * keeps its ln c and 1/c parts, which vary on the scale of the distance -- cells of that size */
+static int ora_near_cells(const ora_seg* X, const ora_seg* Y) {
+  double hm = X->h > Y->h ? X->h : Y->h, d = seg_seg_dist(X, Y);
+  if (d >= hm) return 1;
+  int ns = (int)ceil(2.0 * hm / d);
+  return ns > 16 ? 16 : ns;
+}
+
 static double pair_disjoint(const ora_mesh* m, int ker, const ora_lags* L, const ora_seg* X,
                             const ora_seg* Y, const ora_shape* sh, int q) {
   const ora_rule* R = &RULES[q];
-  const int ns = ora_cells(m, X, Y);
+  int ns = ora_cells(m, X, Y);
+  if (L->d <= 1) {
+    int nn = ora_near_cells(X, Y);
+    if (nn > ns) ns = nn;
+  }
   double acc = 0.0;
   for (int p = 0; p < q * ns; ++p) {
     double fu = (p / q + R->x[p % q]) / ns, wu = R->w[p % q] / ns;
@@ -467,10 +480,19 @@ static double pair_vertex(const ora_mesh* m, int ker, const ora_lags* L, const o
    * treatment (rho = t/ns), cells k >= 1 by plain Gauss with ln c evaluated */
   const int ns = ora_cells(m, X, Y);
   const double lns = log((double)ns);
+  /* acute angle (cos > 1/2, reading R25): A(eta) dips to sin^2(theta) h^2 near eta* = cos(theta)
+   * h1/h2 and its complex zeros approach [0,1]: eta in cells of width about sin(theta)/1.5 */
+  int nea = 1;
+  if (cth > 0.5) {
+    double sth = sqrt(1.0 - cth * cth);
+    nea = (int)ceil(1.5 / (sth > 1e-6 ? sth : 1e-6));
+    if (nea > 16) nea = 16;
+  }
+  const int ne = ns * nea;
   double total = 0.0;
   for (int tri = 0; tri < 2; ++tri) {
-    for (int ie = 0; ie < Rr->n * ns; ++ie) {
-      double eta = (ie / Rr->n + Rr->x[ie % Rr->n]) / ns, weta = Rr->w[ie % Rr->n] / ns;
+    for (int ie = 0; ie < Rr->n * ne; ++ie) {
+      double eta = (ie / Rr->n + Rr->x[ie % Rr->n]) / ne, weta = Rr->w[ie % Rr->n] / ne;
       /* r^2 = rho^2 A(eta) */
       double A = (tri == 0) ? (h1 * h1 + h2 * h2 * eta * eta - 2.0 * h1 * h2 * eta * cth)
                             : (h1 * h1 * eta * eta + h2 * h2 - 2.0 * h1 * h2 * eta * cth);

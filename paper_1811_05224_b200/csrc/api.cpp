@@ -143,7 +143,7 @@ bem_status assemble(int kind, const bem_mesh* m, const bem_quad_opts* o, bem_str
   if (!m || !out) { set_error("bem_assemble: null argument"); return BEM_E_INVALID; }
   *out = nullptr;
   int q_bulk = (o && o->q_bulk > 0) ? o->q_bulk : (kind == STB_D ? m->q_bulk_d : m->q_bulk);
-  int q_sing = (o && o->q_sing > 0) ? o->q_sing : 12;
+  int q_sing = (o && o->q_sing > 0) ? o->q_sing : 16;
   if (q_bulk < 3 || q_bulk > 8 || q_bulk == 7) { set_error("bem_assemble: q_bulk must be one of 3,4,5,6,8"); return BEM_E_INVALID; }
   if (q_sing < 4 || q_sing > QSING_MAX) { set_error("bem_assemble: q_sing must be in [4,16]"); return BEM_E_INVALID; }
   if (m->ng < 6) { set_error("bem_assemble: N_Gamma >= 6 required"); return BEM_E_INVALID; }
@@ -211,7 +211,7 @@ bem_status bem_assemble_toeplitz(const bem_mesh* m, int kind, const bem_quad_opt
   if (!m->uniform) { set_error("bem_assemble_toeplitz: needs equal time steps"); return BEM_E_STATE; }
   if (m->nranks > 1) { set_error("bem_assemble_toeplitz: one process (the Toeplitz blocks are replicated)"); return BEM_E_STATE; }
   int q_bulk = (o && o->q_bulk > 0) ? o->q_bulk : (kind == STB_D ? m->q_bulk_d : m->q_bulk);
-  int q_sing = (o && o->q_sing > 0) ? o->q_sing : 12;
+  int q_sing = (o && o->q_sing > 0) ? o->q_sing : 16;
   if (q_bulk < 3 || q_bulk > 8 || q_bulk == 7) { set_error("bem_assemble_toeplitz: q_bulk must be one of 3,4,5,6,8"); return BEM_E_INVALID; }
   if (q_sing < 4 || q_sing > QSING_MAX) { set_error("bem_assemble_toeplitz: q_sing must be in [4,16]"); return BEM_E_INVALID; }
   cudaSetDevice(m->device);
@@ -291,7 +291,7 @@ bem_status bem_rhs_fused(const bem_mesh* m, const bem_quad_opts* o, const bem_ma
     return st;
   }
   int q_bulk = (o && o->q_bulk > 0) ? o->q_bulk : m->q_bulk;
-  int q_sing = (o && o->q_sing > 0) ? o->q_sing : 12;
+  int q_sing = (o && o->q_sing > 0) ? o->q_sing : 16;
   if (q_bulk < 3 || q_bulk > 8 || q_bulk == 7) { set_error("bem_rhs_fused: q_bulk must be one of 3,4,5,6,8"); return BEM_E_INVALID; }
   if (q_sing < 4 || q_sing > QSING_MAX) { set_error("bem_rhs_fused: q_sing must be in [4,16]"); return BEM_E_INVALID; }
   cudaSetDevice(m->device);

@@ -211,11 +211,13 @@ __device__ double pair_touching(const Seg& X, const Seg& Y, int rel, const Lags&
     const double cth = e1x * e2x + e1y * e2y;
     const double e1n = e1x * Y.nx + e1y * Y.ny;
     if (KER == 2 && fabs(e1n) < 1e-14) return 0.0;
-    const int nq = ns * n, npts = 2 * nq * nq;
+    const int ne = ns * acute_cells(cth);          // eta cells: composite (R24) x acute angle (R25)
+    const double ine = 1.0 / ne;
+    const int nq = ns * n, nqe = ne * n, npts = 2 * nqe * nq;
     for (int idx = lane; idx < npts; idx += 32) {
-      const int tri = idx / (nq * nq), ie = (idx / nq) % nq, ir = idx % nq;
+      const int tri = idx / (nqe * nq), ie = (idx / nq) % nqe, ir = idx % nq;
       const int rc = ir / n, rk = ir % n;
-      const double eta = (ie / n + c_gx[n][ie % n]) * ins, weta = c_gw[n][ie % n] * ins;
+      const double eta = (ie / n + c_gx[n][ie % n]) * ine, weta = c_gw[n][ie % n] * ine;
       const double rho = (rc + c_gx[n][rk]) * ins;
       const double A = tri == 0 ? (h1 * h1 + h2 * h2 * eta * eta - 2.0 * h1 * h2 * eta * cth)
                                 : (h1 * h1 * eta * eta + h2 * h2 - 2.0 * h1 * h2 * eta * cth);

@@ -91,12 +91,30 @@ struct MomArgs {
                           // cells of at most ell (no subdivision while kappa <= 1)
 };
 
-// composite subdivision of a sub-pair: cells per direction
+// composite subdivision of a sub-pair: cells per direction.  R24: pairs
+// closer than 8 ell with elements longer than ell; R25 (NEAR: the near cells keep the ln c and 1/c
+// parts of the kernel): disjoint pairs closer than their length, cells of the distance's size
+// vertex pairs at an acute angle (cos > 1/2): the Duffy integrand's A(eta) = |x - y|^2 / rho^2 dips
+// to sin^2 of the angle, with complex zeros that close distance from [0,1]: cells in eta of about
+// sin(theta) / 1.5 (reading R25); right and obtuse angles keep one cell
+__host__ __device__ inline int acute_cells(double cth) {
+  if (!(cth > 0.5)) return 1;
+  const int ne = (int)ceil(1.5 / sqrt(fmax(1e-12, 1.0 - cth * cth)));
+  return ne > 16 ? 16 : ne;
+}
+template <bool NEAR>
 __device__ __forceinline__ int composite_cells(const Seg& X, const Seg& Y, double ell) {
-  if (!(ell > 0.0)) return 1;
   const double hm = fmax(X.h, Y.h);
-  if (hm <= ell || seg_dist(X, Y) >= 8.0 * ell) return 1;
-  return min(24, (int)ceil(hm / ell));
+  int ns = 1;
+  if (ell > 0.0 && hm > ell) {
+    const double d = seg_dist(X, Y);
+    if (d < 8.0 * ell) ns = min(24, (int)ceil(hm / ell));
+  }
+  if (NEAR) {
+    const double d = seg_dist(X, Y);
+    if (d < hm) ns = max(ns, min(16, (int)ceil(2.0 * hm / d)));
+  }
+  return ns;
 }
 
 // ------------------------------------------------------------- point enumeration
@@ -131,7 +149,7 @@ __device__ __forceinline__ void for_subpairs(const MomArgs& M, int I, int J, Fn&
     sp.qi = J;
     sp.nchain = ng;
     sp.q = NEAR ? near_order(sp.X, sp.Y, M.qfar) : M.q;
-    sp.ns = composite_cells(sp.X, sp.Y, M.ell);
+    sp.ns = composite_cells<NEAR>(sp.X, sp.Y, M.ell);
     sp.sa = sp.X.h * sp.Y.h / (4.0 * STB_PI);
     sp.sb = 0.0;
     fn(sp);
@@ -147,7 +165,7 @@ __device__ __forceinline__ void for_subpairs(const MomArgs& M, int I, int J, Fn&
       if (collinear(sp.X, sp.Y)) continue;
       if (NEAR && chain_rel(I, j, ng)) continue;
       sp.q = NEAR ? near_order(sp.X, sp.Y, M.qfar) : M.q;
-      sp.ns = composite_cells(sp.X, sp.Y, M.ell);
+      sp.ns = composite_cells<NEAR>(sp.X, sp.Y, M.ell);
       sp.side = side;
       sp.sa = M.alpha / (8.0 * STB_PI) * sp.X.h * sp.Y.h;
       sp.sb = 0.0;
@@ -172,7 +190,7 @@ __device__ __forceinline__ void for_subpairs(const MomArgs& M, int I, int J, Fn&
         sp.qi = qh;
         sp.nchain = nh;
         sp.q = NEAR ? near_order(sp.X, sp.Y, M.qfar) : M.q;
-        sp.ns = composite_cells(sp.X, sp.Y, M.ell);
+        sp.ns = composite_cells<NEAR>(sp.X, sp.Y, M.ell);
         const double dvk = n < 2 ? 1.0 / dk.Lm : -1.0 / dk.Lp;
         sp.k0 = n == 0 ? 0.0 : (n == 1 ? dk.vm : (n == 2 ? 1.0 : dk.vp));
         sp.k1 = n == 0 ? dk.vm : (n == 1 ? 1.0 : (n == 2 ? dk.vp : 0.0));
@@ -1423,9 +1441,11 @@ __device__ __forceinline__ void for_touch_points(const MomArgs& M, int I, int J,
       }
       const double cth = e1x * e2x + e1y * e2y;
       const double e1n = e1x * Y.nx + e1y * Y.ny;
-      for (int idx = lane; idx < 2 * n * n; idx += nl) {
-            const int tri = idx / (n * n), ie = (idx / n) % n, ir = idx % n;
-            const double eta = c_gx[n][ie], rho = c_gx[n][ir];
+      const int ne = acute_cells(cth);                  // eta cells (reading R25)
+      const double ine = 1.0 / ne;
+      for (int idx = lane; idx < 2 * ne * n * n; idx += nl) {
+            const int tri = idx / (ne * n * n), ie = (idx / n) % (ne * n), ir = idx % n;
+            const double eta = (ie / n + c_gx[n][ie % n]) * ine, rho = c_gx[n][ir];
             const double A = tri == 0 ? (h1 * h1 + h2 * h2 * eta * eta - 2.0 * h1 * h2 * eta * cth)
                                       : (h1 * h1 * eta * eta + h2 * h2 - 2.0 * h1 * h2 * eta * cth);
             const double u = tri == 0 ? h1 * rho : h1 * rho * eta;
@@ -1434,7 +1454,8 @@ __device__ __forceinline__ void for_touch_points(const MomArgs& M, int I, int J,
             double fa = lin1(axV, axF, u / h1) * lin1(ayV, ayF, v / h2) * jac * wsa;
             if (KIND == STB_K) fa *= u * e1n;   // (x - y).n_y = u e1.n_y at the shared vertex
             const double fb = KIND == STB_D ? lin1(bxV, bxF, u / h1) * lin1(byV, byF, v / h2) * jac * wsb : 0.0;
-            const double wr = c_gw[n][ie] * c_gw[n][ir], wl = c_gw[n][ie] * c_glw[n][ir];
+            const double we = c_gw[n][ie % n] * ine;
+            const double wr = we * c_gw[n][ir], wl = we * c_glw[n][ir];
             vis(0.25 * alpha * rho * rho * A, log(0.25 * alpha * A), fa * wr, fb * wr, fa * wl, fb * wl);
           }
     }

@@ -143,6 +143,27 @@ def test_large_kappa_pair_integrals_brute_force(case):
     assert got == pytest.approx(ref, rel=1e-11, abs=1e-18)
 
 
+# acute corner (about 25 degrees, reading R25): the vertex pair's Duffy integrand and the near
+# cell of the second neighbour across the corner (distance 0.4 h), K kernel, d = 0
+AC_CASES = [
+    (2, 2, 2, 4, 3, 3, (1, 1), (1.0, 0.0)),     # K vertex pair at the acute corner, d = 0
+    (2, 2, 2, 4, 2, 0, (1, 1), (0.0, 1.0)),     # K disjoint pair across the corner, d = 0
+]
+
+
+@pytest.mark.parametrize("case", AC_CASES)
+def test_acute_corner_pair_integrals_brute_force(case):
+    from workloads.edge import edge_workloads
+    w = edge_workloads()["acute"]
+    m = O.OracleMesh(w)
+    ker, a, b, p, q, rel, sx, sy = case
+    X = (tuple(m.seg_a[p]), tuple(m.seg_b[p]))
+    Y = (tuple(m.seg_a[q]), tuple(m.seg_b[q]))
+    ref = float(B.pair(ker, w.alpha, w.t_breaks, a, b, X, Y, m.seg_n[q], sx, sy, rel))
+    got = m.pair(ker, 0, a, b, p, q, sx, sy)
+    assert got == pytest.approx(ref, rel=1e-12, abs=1e-18)
+
+
 def test_half_segment_pairs_brute_force():
     """half segments on the L-shape (re-entrant corner, graded steps, alpha = 1/2)"""
     w = W.get("LT")

@@ -1,8 +1,9 @@
 """Edge-case workloads for the parity tests (data only: geometry, time grids, alpha).
 
 Degenerate and extreme inputs of the method: the smallest boundary the C-ABI accepts, a single
-time step, ragged 32-wide tiles, strongly graded steps (kappa = alpha h^2 / (4 min h_t) = 64) and
-heat-capacity extremes (kappa = 1e-3 .. 44); reading R24 for the large-kappa rules.
+time step, ragged 32-wide tiles, strongly graded steps (kappa = alpha h^2 / (4 min h_t) = 64),
+heat-capacity extremes (kappa = 1e-3 .. 44), an acute corner and a non-convex pentagon; DESIGN.md
+readings R24 / R25 for the large-kappa and near-singular rules.
 """
 from .configs import Workload, graded_times, uniform_times
 
@@ -27,4 +28,10 @@ def edge_workloads():
         # heat capacity extremes (c = alpha r^2 / 4): nearly every node in regime A / in regime Z
         "alpha_small": Workload("alpha_small", sq, [3, 3, 3, 3], uniform_times(8), 1e-3, (1.5, 1.5), 1e-10),
         "alpha_large": Workload("alpha_large", sq, [3, 3, 3, 3], uniform_times(8), 200.0, (1.5, 1.5), 1e-10),
+        # an acute corner (about 22 degrees): second neighbours across the corner nearly touch
+        "acute": Workload("acute", [(0.0, 0.0), (1.0, 0.0), (0.15, 0.4)], [4, 3, 3], uniform_times(6), 1.0,
+                          (1.5, 1.5), 1e-10),
+        # a non-convex pentagon with unequal sides and graded steps
+        "pentagon": Workload("pentagon", [(0.0, 0.0), (1.0, 0.1), (0.7, 0.5), (1.0, 0.9), (0.1, 0.8)],
+                             [3, 2, 2, 3, 3], graded_times(8, 1.3), 0.7, (1.5, 1.5), 1e-10),
     }
