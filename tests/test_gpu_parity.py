@@ -563,7 +563,7 @@ def test_distributed_path_on_a_one_rank_nccl_communicator():
 
 
 @pytest.mark.parametrize("name", ["triangle6", "onestep", "ragged33", "grade2", "alpha_small", "alpha_large",
-                                  "acute", "pentagon"])
+                                  "acute", "pentagon", "ratio10", "scaled"])
 def test_edge_case_meshes_full_parity(name):
     """degenerate and extreme inputs (minimal boundary, one step, ragged tiles, strong grading,
     alpha extremes): V_h, K_h, D_h in full against the oracle, causality zeros, and V_h's spatial

@@ -31,6 +31,11 @@ def edge_workloads():
         # an acute corner (about 22 degrees): second neighbours across the corner nearly touch
         "acute": Workload("acute", [(0.0, 0.0), (1.0, 0.0), (0.15, 0.4)], [4, 3, 3], uniform_times(6), 1.0,
                           (1.5, 1.5), 1e-10),
+        # neighbours whose lengths differ by 10 (one element on two sides, ten on the others)
+        "ratio10": Workload("ratio10", sq, [1, 10, 1, 10], uniform_times(6), 1.0, (1.5, 1.5), 1e-10),
+        # a domain of size 1e-2 over T = 1e-4 (the heat kernel's scaling x -> x/L, t -> t/L^2)
+        "scaled": Workload("scaled", [(0.0, 0.0), (0.01, 0.0), (0.01, 0.01), (0.0, 0.01)], [3, 3, 3, 3],
+                           uniform_times(6, 1e-4), 1.0, (0.015, 0.015), 1e-10),
         # a non-convex pentagon with unequal sides and graded steps
         "pentagon": Workload("pentagon", [(0.0, 0.0), (1.0, 0.1), (0.7, 0.5), (1.0, 0.9), (0.1, 0.8)],
                              [3, 2, 2, 3, 3], graded_times(8, 1.3), 0.7, (1.5, 1.5), 1e-10),
