@@ -318,12 +318,14 @@ def test_rhs_fused(name, n_slices):
     assert st["fused_sing"] == 1 and st["evals_bulk"] > 0
 
 
-@pytest.mark.parametrize("name", ["C1", "S32"])
+@pytest.mark.parametrize("name", ["C1", "S32", "ragged33"])
 def test_block_toeplitz_variant(name):
     """row f3: on equal time steps the first block column T_d = A(d, 0) reproduces every entry
     (A(a, b) = T_{a-b}), the Toeplitz GEMM product equals the dense product, and GMRES with the
-    Toeplitz V_h and D_h returns the dense solution"""
-    w = W.get(name)
+    Toeplitz V_h and D_h returns the dense solution (ragged33: odd N_Gamma, unaligned rows of x
+    for the cp.async staging, a ragged 128-row tile)"""
+    from workloads.edge import edge_workloads
+    w = edge_workloads()[name] if name in edge_workloads() else W.get(name)
     m = S.Mesh.from_workload(w)
     x = W.random_vector(w.n)
     mats = {}
