@@ -716,3 +716,25 @@ def test_full_size_step_properties(name):
     assert err / nrm < 0.0798, (err, nrm)          # C2: 0.0798 (P11)
     for A in (V, D, Mp, Md):
         A.close()
+
+
+@pytest.mark.parametrize("name", ["C1", "S32"])
+def test_potential_parity_hard_points(name):
+    """row f2 at the hard end of its domain: points at 1.05 h_max from Gamma (the rejection
+    distance is h_max) next to each side, times inside the first step, just after a step break
+    and at T"""
+    w = W.get(name)
+    om = O.OracleMesh(w)
+    h = max(np.hypot(*(np.asarray(w.vertices[(k + 1) % len(w.vertices)]) - np.asarray(w.vertices[k]))) / n
+            for k, n in enumerate(w.segments_per_side))
+    t = np.asarray(w.t_breaks)
+    d = 1.05 * h
+    xs = [(d, 0.3), (0.4, d), (0.5, 1.0 - d), (1.0 - d, 0.6)]
+    ts = [0.5 * t[1], t[2] + 1e-3 * (t[3] - t[2]), t[-1]]
+    pts = np.array([[x1, x2, tt] for (x1, x2) in xs for tt in ts])
+    g = W.dirichlet_data(w)
+    wh = W.random_vector(w.n)
+    m = S.Mesh.from_workload(w)
+    got = S.eval_potential(m, cuda(wh), cuda(g), pts).cpu().numpy()
+    ref = om.potential(wh, g, pts)
+    assert relmax(got, ref) <= 1e-11, relmax(got, ref)
