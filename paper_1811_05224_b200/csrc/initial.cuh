@@ -8,7 +8,9 @@
 // gamma_i to the centroid is below 2 max(h_i, longest edge), else qt_far^2); the first step
 // (a = 0: E1(c/t_1) alone is log singular at y = x) uses on the near triangles the apex-split rule
 // at each x point: the three sub-triangles (x, V_k, V_k+1) with signed areas, radial coordinate on a
-// geometric composite Gauss rule (ratio 0.15, 10 levels x 8 points), angular 12-point Gauss
+// geometric composite Gauss rule (ratio 0.15, 10 levels x 16 points: on a level [0.15 r, r] the log
+// singularity sits 0.18 of its length away, Bernstein ratio 2.26, 2.26^-32 = 5e-12), angular
+// 12-point Gauss
 // (reading R22).  Node values from the moments of each warp's 32-triangle point cluster
 // (initial_warp); per-warp partial rows, k_initial_finish sums them in fixed order.
 #pragma once
@@ -27,8 +29,8 @@ __device__ double apex_split(double px, double py, const double (&V)[6], const d
     double hi = 1.0;
     for (int lev = 0; lev <= 10; ++lev) {
       const double lo = lev < 10 ? hi * 0.15 : 0.0;
-      for (int r = 0; r < 8; ++r) {
-        const double xi = fma(hi - lo, c_gx[8][r], lo), wxi = (hi - lo) * c_gw[8][r];
+      for (int r = 0; r < 16; ++r) {
+        const double xi = fma(hi - lo, c_gx[16][r], lo), wxi = (hi - lo) * c_gw[16][r];
         double part = 0.0;
         for (int e = 0; e < 12; ++e) {
           const double eta = c_gx[12][e];
@@ -136,8 +138,29 @@ __device__ __forceinline__ void initial_warp(const Seg& S, const double* __restr
       first = fma(c_gw[qx][p] * S.h, apex_split(xx, xy, V, uv, ua, alpha, tg[1]), first);
     }
   } else if (valid) {
+    // step 0 alone on a far triangle: E1(c / t_1) varies on ell_1 = sqrt(4 t_1 / alpha); composite
+    // collapsed rule of ceil(2 l / ell_1) cells per direction (reading R24)
     const double it = 1.0 / tg[1];
-    for_tri_points(S, V, uv, qx, qt, alpha, [&](double c, double W) { first = fma(W, dev_e1(c * it), first); });
+    const double e1x = V[2] - V[0], e1y = V[3] - V[1], e2x = V[4] - V[0], e2y = V[5] - V[1];
+    const double l = sqrt(fmax(fmax(e1x * e1x + e1y * e1y, e2x * e2x + e2y * e2y),
+                               (e2x - e1x) * (e2x - e1x) + (e2y - e1y) * (e2y - e1y)));
+    const int ns = min(24, max(1, (int)ceil(2.0 * l / sqrt(4.0 * tg[1] / alpha))));
+    const double ins = 1.0 / ns, area2 = fabs(e1x * e2y - e1y * e2x);
+    for (int p = 0; p < qx; ++p) {
+      const double xx = fma(c_gx[qx][p], S.bx - S.ax, S.ax), xy = fma(c_gx[qx][p], S.by - S.ay, S.ay);
+      double sp = 0.0;
+      for (int a1 = 0; a1 < qt * ns; ++a1) {
+        const double xi = (a1 / qt + c_gx[qt][a1 % qt]) * ins;
+        for (int a2 = 0; a2 < qt * ns; ++a2) {
+          const double eta = (a2 / qt + c_gx[qt][a2 % qt]) * ins;
+          const double u = xi * (1.0 - eta), v = xi * eta;
+          const double dx = xx - (V[0] + u * e1x + v * e2x), dy = xy - (V[1] + u * e1y + v * e2y);
+          const double uh = (1.0 - u - v) * uv[0] + u * uv[1] + v * uv[2];
+          sp = fma(xi * c_gw[qt][a1 % qt] * c_gw[qt][a2 % qt] * uh, dev_e1(0.25 * alpha * (dx * dx + dy * dy) * it), sp);
+        }
+      }
+      first = fma(c_gw[qx][p] * S.h * area2 * ins * ins, sp, first);
+    }
   }
   first = warp_sum(first);
   if (lane == 0) acc[0] += first;
