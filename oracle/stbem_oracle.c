@@ -763,20 +763,44 @@ static void apex_rule_accumulate(double px, double py, const double* V, const do
     const double e1x = v1x - px, e1y = v1y - py, e2x = v2x - px, e2y = v2y - py;
     const double area2 = e1x * e2y - e1y * e2x;          /* signed */
     if (fabs(area2) < 1e-300) continue;
+    /* eta rule along the far side v1 -> v2: the xi-integrated kernel behaves like log rho(eta),
+     * rho = |y(1, eta) - p|, near-singular at an end where the apex sits close to that vertex
+     * (x near a corner of the triangle, reading R22): grade eta geometrically (ratio 0.15, 8 points
+     * per level) toward that end down to the scale |p - v| / |v1 - v2|; else 12 Gauss points */
+    const double l1 = sqrt(e1x * e1x + e1y * e1y), l2 = sqrt(e2x * e2x + e2y * e2y);
+    const double lside = sqrt((v2x - v1x) * (v2x - v1x) + (v2y - v1y) * (v2y - v1y));
+    const double dmin = l1 < l2 ? l1 : l2;
+    double es[128], ew[128];
+    int ne = 0;
+    if (dmin < 0.15 * lside) {
+      const int at0 = l1 < l2;                     /* grade toward eta = 0 (v1) or eta = 1 (v2) */
+      int nlev = (int)ceil(log(dmin / lside) / log(0.15)) + 1;
+      if (nlev > 14) nlev = 14;
+      double top = 1.0;
+      for (int lev = 0; lev < nlev; ++lev) {
+        const double bot = lev == nlev - 1 ? 0.0 : 0.15 * top;
+        for (int q = 0; q < 8; ++q) {
+          const double d = bot + (top - bot) * RULES[8].x[q];
+          es[ne] = at0 ? d : 1.0 - d; ew[ne] = (top - bot) * RULES[8].w[q]; ++ne;
+        }
+        top = bot;
+      }
+    } else {
+      for (int q = 0; q < RE->n; ++q) { es[ne] = RE->x[q]; ew[ne] = RE->w[q]; ++ne; }
+    }
     double hi = 1.0;
     for (int lev = 0; lev <= 10; ++lev) {
       const double lo = lev < 10 ? hi * 0.15 : 0.0;
       for (int r = 0; r < RR->n; ++r) {
         const double xi = lo + (hi - lo) * RR->x[r], wxi = (hi - lo) * RR->w[r];
-        for (int e = 0; e < RE->n; ++e) {
-          const double eta = RE->x[e];
-          const double yx = px + xi * ((1.0 - eta) * e1x + eta * e2x);
-          const double yy = py + xi * ((1.0 - eta) * e1y + eta * e2y);
+        for (int e = 0; e < ne; ++e) {
+          const double eta = es[e];
           /* u0_h at y: the linear interpolant of the triangle's three values */
           const double uh = uv[3] * 0.0 + (1.0 - xi) * uv[4] + xi * ((1.0 - eta) * u1 + eta * u2);
-          const double dx = px - yx, dy = py - yy;
+          /* y - p formed directly: p - y would cancel to 0 where y is within rounding of p */
+          const double dx = xi * ((1.0 - eta) * e1x + eta * e2x), dy = xi * ((1.0 - eta) * e1y + eta * e2y);
           const double c = 0.25 * alpha * (dx * dx + dy * dy);
-          *acc += wx * area2 * xi * wxi * RE->w[e] * uh * ora_e1(c / t1);
+          *acc += wx * area2 * xi * wxi * ew[e] * uh * ora_e1(c / t1);
         }
       }
       hi = lo;
@@ -795,6 +819,41 @@ void ora_initial_rhs(const ora_mesh* m, int nnode, const double* nodes, int ntri
     const ora_seg* S = &m->seg[i];
     double* node_sum = (double*)calloc((size_t)(nt + 1), sizeof(double));   /* N(i, n), regular rule */
     double first = 0.0;                                                       /* step a = 0 */
+    /* x rule of the step-0 terms (reading R22): the step-0 column is log-singular in x where the
+     * element meets a corner of Gamma (the data density jumps there), so a half of the element
+     * that ends at a corner takes 8 geometrically graded levels (ratio 0.15 toward the corner,
+     * the last level reaching it) of 8 Gauss points; other halves 16 Gauss points; an element
+     * with no corner end keeps the plain qx-point rule */
+    const ora_seg* Sp = &m->seg[(i + ng - 1) % ng];
+    const ora_seg* Sn = &m->seg[(i + 1) % ng];
+    const int c_a = S->tx * Sp->tx + S->ty * Sp->ty < 1.0 - 1e-12;   /* corner at the start a */
+    const int c_b = S->tx * Sn->tx + S->ty * Sn->ty < 1.0 - 1e-12;   /* corner at the end b */
+    double xs[160], xw[160];
+    int nx0 = 0;
+    if (!c_a && !c_b) {
+      for (int p = 0; p < qx; ++p) { xs[nx0] = RULES[qx].x[p]; xw[nx0] = RULES[qx].w[p]; ++nx0; }
+    } else {
+      for (int half = 0; half < 2; ++half) {
+        const int graded = half == 0 ? c_a : c_b;
+        /* d = distance from the half's element end (0 at the corner end) in [0, 1/2] */
+        if (!graded) {
+          for (int p = 0; p < 16; ++p) {
+            const double d = 0.5 * RULES[16].x[p];
+            xs[nx0] = half == 0 ? d : 1.0 - d; xw[nx0] = 0.5 * RULES[16].w[p]; ++nx0;
+          }
+        } else {
+          double top = 0.5;
+          for (int lev = 0; lev < 8; ++lev) {
+            const double bot = lev == 7 ? 0.0 : 0.15 * top;
+            for (int p = 0; p < 8; ++p) {
+              const double d = bot + (top - bot) * RULES[8].x[p];
+              xs[nx0] = half == 0 ? d : 1.0 - d; xw[nx0] = (top - bot) * RULES[8].w[p]; ++nx0;
+            }
+            top = bot;
+          }
+        }
+      }
+    }
     for (int k = 0; k < ntri; ++k) {
       const int i0 = tri[3 * k], i1 = tri[3 * k + 1], i2 = tri[3 * k + 2];
       const double ax = nodes[2 * i0], ay = nodes[2 * i0 + 1];
@@ -813,7 +872,6 @@ void ora_initial_rhs(const ora_mesh* m, int nnode, const double* nodes, int ntri
       const ora_rule* RX = &RULES[qx];
       for (int p = 0; p < qx; ++p) {
         const double xx = S->ax + RX->x[p] * (S->bx - S->ax), xy = S->ay + RX->x[p] * (S->by - S->ay);
-        double first_p = 0.0;
         for (int a1 = 0; a1 < qt; ++a1)
           for (int a2 = 0; a2 < qt; ++a2) {
             const double xi = RT->x[a1], eta = RT->x[a2];
@@ -825,6 +883,14 @@ void ora_initial_rhs(const ora_mesh* m, int nnode, const double* nodes, int ntri
             const double c = 0.25 * alpha * (dx * dx + dy * dy);
             for (int n = 1; n <= nt; ++n) node_sum[n] += W * ora_e1(c / m->t[n]);
           }
+      }
+      /* far triangles: the step-0 term is smooth in x (Gauss qx on gamma_i, corner or not); near
+       * ones: the apex split at every point of the x rule above */
+      const int npx = near ? nx0 : qx;
+      for (int p = 0; p < npx; ++p) {
+        const double xp = near ? xs[p] : RX->x[p], wxp = near ? xw[p] : RX->w[p];
+        const double xx = S->ax + xp * (S->bx - S->ax), xy = S->ay + xp * (S->by - S->ay);
+        double first_p = 0.0;
         if (!near) {
           /* step 0 alone (no difference of two nodes): E1(c/t_1) varies on ell_1 = sqrt(4 t_1 /
            * alpha); triangles longer than that by composite collapsed rules of ceil(2 l / ell_1)
@@ -839,7 +905,7 @@ void ora_initial_rhs(const ora_mesh* m, int nnode, const double* nodes, int ntri
               const double u = xi * (1.0 - eta), v = xi * eta;
               const double yx = ax + u * e1x + v * e2x, yy = ay + u * e1y + v * e2y;
               const double uh = (1.0 - u - v) * u0[i0] + u * u0[i1] + v * u0[i2];
-              const double W = RX->w[p] * S->h * area2 * xi * RT->w[a1 % qt] * RT->w[a2 % qt] / ((double)ns * ns) * uh;
+              const double W = wxp * S->h * area2 * xi * RT->w[a1 % qt] * RT->w[a2 % qt] / ((double)ns * ns) * uh;
               const double dx = xx - yx, dy = xy - yy;
               first_p += W * ora_e1(0.25 * alpha * (dx * dx + dy * dy) / m->t[1]);
             }
@@ -851,7 +917,7 @@ void ora_initial_rhs(const ora_mesh* m, int nnode, const double* nodes, int ntri
           const double det = e1x * e2y - e1y * e2x;
           const double uu = ((xx - ax) * e2y - (xy - ay) * e2x) / det, vv = ((xy - ay) * e1x - (xx - ax) * e1y) / det;
           const double uv[5] = {u0[i0], u0[i1], u0[i2], 0.0, (1.0 - uu - vv) * u0[i0] + uu * u0[i1] + vv * u0[i2]};
-          apex_rule_accumulate(xx, xy, V, uv, alpha, m->t[1], RX->w[p] * S->h, &first_p);
+          apex_rule_accumulate(xx, xy, V, uv, alpha, m->t[1], wxp * S->h, &first_p);
         }
         first += first_p;
       }

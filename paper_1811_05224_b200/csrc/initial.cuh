@@ -17,31 +17,86 @@
 
 namespace stb {
 
-__device__ double apex_split(double px, double py, const double (&V)[6], const double (&uv)[3],
-                             double u_apex, double alpha, double t1) {
+// x points of the first step on gamma_i (parameter f in [0, 1] and weight): 2 x 16 Gauss points on
+// the halves of the element; a half that ends at a corner of Gamma (tangent change) gets geometric
+// levels toward it instead (ratio 0.15, 8 levels x 8 points): the log kernel's potential over the
+// domain is singular in x at a corner (reading R22)
+struct XRule {
+  int n0, n1, qx;
+  bool plain;                                       // no corner: Gauss qx on the element
+  __device__ __forceinline__ XRule(bool c0, bool c1, int q) : n0(c0 ? 64 : 16), n1(c1 ? 64 : 16), qx(q), plain(!c0 && !c1) {}
+  __device__ __forceinline__ int n() const { return plain ? qx : n0 + n1; }
+  __device__ __forceinline__ void point(int k, double& f, double& w) const {
+    if (plain) {
+      f = c_gx[qx][k];
+      w = c_gw[qx][k];
+      return;
+    }
+    const bool h1 = k >= n0;
+    const int kk = h1 ? k - n0 : k, nh = h1 ? n1 : n0;
+    double g, wg;                                   // position from the half's outer end, in [0, 1/2]
+    if (nh == 16) {
+      g = 0.5 * c_gx[16][kk];
+      wg = 0.5 * c_gw[16][kk];
+    } else {
+      const int lev = kk >> 3, r = kk & 7;
+      double hi = 0.5;
+      for (int l = 0; l < lev; ++l) hi *= 0.15;
+      const double lo = lev < 7 ? hi * 0.15 : 0.0;
+      g = fma(hi - lo, c_gx[8][r], lo);
+      wg = (hi - lo) * c_gw[8][r];
+    }
+    f = h1 ? 1.0 - g : g;
+    w = wg;
+  }
+};
+
+// one geometric xi level lev (0..10) of the sub-triangle (p, v_s, v_s+1) of the apex split
+__device__ double apex_level(double px, double py, const double (&V)[6], const double (&uv)[3],
+                             double u_apex, double alpha, double t1, int s, int lev) {
   double acc = 0.0;
-  for (int s = 0; s < 3; ++s) {
+  {
     const double e1x = V[2 * s] - px, e1y = V[2 * s + 1] - py;
     const double e2x = V[2 * ((s + 1) % 3)] - px, e2y = V[2 * ((s + 1) % 3) + 1] - py;
     const double area2 = e1x * e2y - e1y * e2x;      // signed
-    if (fabs(area2) < 1e-300) continue;
+    if (fabs(area2) < 1e-300) return 0.0;
     const double u1 = uv[s], u2 = uv[(s + 1) % 3];
+    // eta along the far side: the xi-integrated kernel ~ log rho(eta) is near-singular at a side end
+    // the apex sits close to (x near a triangle vertex): geometric levels (ratio 0.15, 8 Gauss points
+    // each) toward that end down to |p - v| / side, else 12 Gauss points (reading R22)
+    const double l1 = sqrt(e1x * e1x + e1y * e1y), l2 = sqrt(e2x * e2x + e2y * e2y);
+    const double sx = e2x - e1x, sy = e2y - e1y, ls = sqrt(sx * sx + sy * sy);
+    const double dm = fmin(l1, l2);
+    const bool grade = dm < 0.15 * ls, at0 = l1 < l2;
+    const int nlev = grade ? min(14, (int)ceil(log(dm / ls) * (1.0 / log(0.15))) + 1) : 0;
+    const int ne = grade ? 8 * nlev : 12;
     double hi = 1.0;
-    for (int lev = 0; lev <= 10; ++lev) {
+    for (int l = 0; l < lev; ++l) hi *= 0.15;
+    {
       const double lo = lev < 10 ? hi * 0.15 : 0.0;
       for (int r = 0; r < 16; ++r) {
         const double xi = fma(hi - lo, c_gx[16][r], lo), wxi = (hi - lo) * c_gw[16][r];
-        double part = 0.0;
-        for (int e = 0; e < 12; ++e) {
-          const double eta = c_gx[12][e];
-          const double dx = xi * fma(eta, e2x - e1x, e1x), dy = xi * fma(eta, e2y - e1y, e1y);
+        double part = 0.0, etop = 1.0;
+        for (int e = 0; e < ne; ++e) {
+          double eta, we;
+          if (grade) {
+            const int q = e & 7;
+            const double ebot = (e >> 3) == nlev - 1 ? 0.0 : 0.15 * etop;
+            const double d = fma(etop - ebot, c_gx[8][q], ebot);
+            eta = at0 ? d : 1.0 - d;
+            we = (etop - ebot) * c_gw[8][q];
+            if (q == 7) etop = ebot;
+          } else {
+            eta = c_gx[12][e];
+            we = c_gw[12][e];
+          }
+          const double dx = xi * fma(eta, sx, e1x), dy = xi * fma(eta, sy, e1y);
           const double uh = fma(xi, fma(eta, u2 - u1, u1) - u_apex, u_apex);
           const double c = 0.25 * alpha * (dx * dx + dy * dy);
-          part = fma(c_gw[12][e] * uh, dev_e1(c / t1), part);
+          part = fma(we * uh, dev_e1(c / t1), part);
         }
         acc = fma(area2 * xi * wxi, part, acc);
       }
-      hi = lo;
     }
   }
   return acc;
@@ -99,8 +154,9 @@ __device__ __forceinline__ void initial_warp(const Seg& S, const double* __restr
                                              double alpha, const double* __restrict__ nodes,
                                              const int* __restrict__ tris, int ntri,
                                              const double* __restrict__ u0, int qx, int qtf, int qtn,
-                                             int use_moments, double* acc, double* sm) {
+                                             int use_moments, double* acc, double* sm, bool cor0, bool cor1) {
   const int lane = threadIdx.x & 31;
+  const XRule xr(cor0, cor1, qx);
   const bool valid = k < ntri;
   double V[6] = {0, 0, 0, 0, 0, 0}, uv[3] = {0, 0, 0};
   bool near = false;
@@ -125,19 +181,33 @@ __device__ __forceinline__ void initial_warp(const Seg& S, const double* __restr
     near = sqrt(qx0 * qx0 + qy0 * qy0) < 2.0 * fmax(S.h, le);
   }
   const int qt = near ? qtn : qtf;
-  // step 0
+  // step 0.  Near triangles: the apex-split rule, work items (x point, sub-triangle, xi level) spread
+  // over the warp one near triangle at a time (a corner row's graded x rule makes them heavy)
   double first = 0.0;
-  if (valid && near) {
-    const double e1x = V[2] - V[0], e1y = V[3] - V[1], e2x = V[4] - V[0], e2y = V[5] - V[1];
+  unsigned nmask = __ballot_sync(0xffffffffu, valid && near);
+  while (nmask) {
+    const int src = __ffs(nmask) - 1;
+    nmask &= nmask - 1;
+    double Vs[6], us[3];
+#pragma unroll
+    for (int v = 0; v < 6; ++v) Vs[v] = __shfl_sync(0xffffffffu, V[v], src);
+#pragma unroll
+    for (int v = 0; v < 3; ++v) us[v] = __shfl_sync(0xffffffffu, uv[v], src);
+    const double e1x = Vs[2] - Vs[0], e1y = Vs[3] - Vs[1], e2x = Vs[4] - Vs[0], e2y = Vs[5] - Vs[1];
     const double det = e1x * e2y - e1y * e2x;
-    for (int p = 0; p < qx; ++p) {
-      const double xx = fma(c_gx[qx][p], S.bx - S.ax, S.ax), xy = fma(c_gx[qx][p], S.by - S.ay, S.ay);
-      const double uu = ((xx - V[0]) * e2y - (xy - V[1]) * e2x) / det;
-      const double vv = ((xy - V[1]) * e1x - (xx - V[0]) * e1y) / det;
-      const double ua = (1.0 - uu - vv) * uv[0] + uu * uv[1] + vv * uv[2];
-      first = fma(c_gw[qx][p] * S.h, apex_split(xx, xy, V, uv, ua, alpha, tg[1]), first);
+    const int nitem = xr.n() * 33;
+    for (int w = lane; w < nitem; w += 32) {
+      const int p = w / 33, sl = w - 33 * p;
+      double fp, wp;
+      xr.point(p, fp, wp);
+      const double xx = fma(fp, S.bx - S.ax, S.ax), xy = fma(fp, S.by - S.ay, S.ay);
+      const double uu = ((xx - Vs[0]) * e2y - (xy - Vs[1]) * e2x) / det;
+      const double vv = ((xy - Vs[1]) * e1x - (xx - Vs[0]) * e1y) / det;
+      const double ua = (1.0 - uu - vv) * us[0] + uu * us[1] + vv * us[2];
+      first = fma(wp * S.h, apex_level(xx, xy, Vs, us, ua, alpha, tg[1], sl / 11, sl % 11), first);
     }
-  } else if (valid) {
+  }
+  if (valid && !near) {
     // step 0 alone on a far triangle: E1(c / t_1) varies on ell_1 = sqrt(4 t_1 / alpha); composite
     // collapsed rule of ceil(2 l / ell_1) cells per direction (reading R24)
     const double it = 1.0 / tg[1];
@@ -146,8 +216,17 @@ __device__ __forceinline__ void initial_warp(const Seg& S, const double* __restr
                                (e2x - e1x) * (e2x - e1x) + (e2y - e1y) * (e2y - e1y)));
     const int ns = min(24, max(1, (int)ceil(2.0 * l / sqrt(4.0 * tg[1] / alpha))));
     const double ins = 1.0 / ns, area2 = fabs(e1x * e2y - e1y * e2x);
-    for (int p = 0; p < qx; ++p) {
-      const double xx = fma(c_gx[qx][p], S.bx - S.ax, S.ax), xy = fma(c_gx[qx][p], S.by - S.ay, S.ay);
+    // a triangle whose every point is beyond x = c/t_1 = 50 from gamma_i adds below e^{-50}/50
+    const double gx = V[0] + (e1x + e2x) / 3.0, gy = V[1] + (e1y + e2y) / 3.0;
+    double f0 = (gx - S.ax) * S.tx + (gy - S.ay) * S.ty;
+    f0 = fmin(fmax(f0, 0.0), S.h);
+    const double qx0 = S.ax + f0 * S.tx - gx, qy0 = S.ay + f0 * S.ty - gy;
+    const double dmin = fmax(0.0, sqrt(qx0 * qx0 + qy0 * qy0) - l);
+    // (smooth in x: Gauss qx on gamma_i also at a corner element)
+    const int np = 0.25 * alpha * dmin * dmin * it > 50.0 ? 0 : qx;
+    for (int p = 0; p < np; ++p) {
+      const double fp = c_gx[qx][p], wp = c_gw[qx][p];
+      const double xx = fma(fp, S.bx - S.ax, S.ax), xy = fma(fp, S.by - S.ay, S.ay);
       double sp = 0.0;
       for (int a1 = 0; a1 < qt * ns; ++a1) {
         const double xi = (a1 / qt + c_gx[qt][a1 % qt]) * ins;
@@ -159,7 +238,7 @@ __device__ __forceinline__ void initial_warp(const Seg& S, const double* __restr
           sp = fma(xi * c_gw[qt][a1 % qt] * c_gw[qt][a2 % qt] * uh, dev_e1(0.25 * alpha * (dx * dx + dy * dy) * it), sp);
         }
       }
-      first = fma(c_gw[qx][p] * S.h * area2 * ins * ins, sp, first);
+      first = fma(wp * S.h * area2 * ins * ins, sp, first);
     }
   }
   first = warp_sum(first);
@@ -287,11 +366,13 @@ __global__ void __launch_bounds__(256) k_initial(const Seg* __restrict__ seg, co
   for (int r = lane; r < nt + 2; r += 32) acc[r] = 0.0;
   __syncwarp();
   const Seg S = seg[blockIdx.x];
+  const Seg Sp = seg[(blockIdx.x + ng - 1) % ng], Sn = seg[(blockIdx.x + 1) % ng];
+  const bool cor0 = S.tx * Sp.tx + S.ty * Sp.ty < 1.0 - 1e-12, cor1 = S.tx * Sn.tx + S.ty * Sn.ty < 1.0 - 1e-12;
   for (int bt = 0; bt < nbatch; ++bt) {
     const int k0 = (bt * gridDim.y + blockIdx.y) * 256;
     if (k0 >= ntri) break;                                // CTA-uniform
     initial_warp(S, tg, k0 + threadIdx.x, nt, alpha, nodes, tris, ntri, u0, qx, qtf, qtn, use_moments, acc,
-                 msh[warp]);
+                 msh[warp], cor0, cor1);
     __syncwarp();
   }
   if (use_smem) {
