@@ -360,7 +360,8 @@ bem_status gemv_launch(const bem_matrix* A, double a, const double* x, double b,
 // peak on B200 (37.1 vs 34.1 TFLOP/s, profiles/r01_fp64_peak.txt, r01_dmma_peak.txt) but one
 // DMMA does 256 FMAs per warp from 2 operand registers per lane, so the tile loop is no longer
 // bound by shared-memory operand loads and issue slots as the 8 x 8 DFMA register tile was.
-constexpr int TZ_TI = 128, TZ_TA = 128, TZ_TK = 16, TZ_LDK = TZ_TK + 4, TZ_STAGES = 3;
+// row stride 18 doubles (144 B): the 16-byte fragment loads of a quarter warp hit 8 distinct bank quads
+constexpr int TZ_TI = 128, TZ_TA = 128, TZ_TK = 16, TZ_LDK = TZ_TK + 2, TZ_STAGES = 3;
 constexpr size_t TZ_SMEM = sizeof(double) * TZ_STAGES * 2 * TZ_TI * TZ_LDK;
 // 8 warps as 2 (i) x 4 (a), warp tile 64 i x 32 a = 8 x 4 DMMA tiles, 64 accumulators per lane.
 // Shared tiles row-major [i or a][k] with row stride 20 doubles: the fragment loads (lane -> k =
@@ -442,17 +443,23 @@ __global__ void __launch_bounds__(256) k_toeplitz_mm(const double* __restrict__ 
     cp_async_commit();
     const double* Ts = tz_sm + (step % TZ_STAGES) * (2 * TZ_TI * TZ_LDK);
     const double* Xs = Ts + TZ_TI * TZ_LDK;
+    // k order inside the stage: product s of lane (fc, fr) takes k = 4 fr + s (the sum over the 16
+    // k of the stage is the same), so a lane's fragments of two products are one 16-byte load
 #pragma unroll
-    for (int kk = 0; kk < TZ_TK; kk += 4) {
-      double af[8], bf[4];
+    for (int h = 0; h < TZ_TK / 8; ++h) {
+      double2 af[8], bf[4];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) af[u] = Ts[(wi + 8 * u + fc) * TZ_LDK + kk + fr];
+      for (int u = 0; u < 8; ++u) af[u] = *reinterpret_cast<const double2*>(Ts + (wi + 8 * u + fc) * TZ_LDK + 4 * fr + 2 * h);
 #pragma unroll
-      for (int v = 0; v < 4; ++v) bf[v] = Xs[(wa + 8 * v + fc) * TZ_LDK + kk + fr];
+      for (int v = 0; v < 4; ++v) bf[v] = *reinterpret_cast<const double2*>(Xs + (wa + 8 * v + fc) * TZ_LDK + 4 * fr + 2 * h);
 #pragma unroll
       for (int u = 0; u < 8; ++u)
 #pragma unroll
-        for (int v = 0; v < 4; ++v) dmma_8x8x4(acc[u][v], af[u], bf[v]);
+        for (int v = 0; v < 4; ++v) dmma_8x8x4(acc[u][v], af[u].x, bf[v].x);
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) dmma_8x8x4(acc[u][v], af[u].y, bf[v].y);
     }
   }
   cp_async_wait<0>();
