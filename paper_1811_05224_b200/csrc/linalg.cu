@@ -361,8 +361,11 @@ bem_status gemv_launch(const bem_matrix* A, double a, const double* x, double b,
 // DMMA does 256 FMAs per warp from 2 operand registers per lane, so the tile loop is no longer
 // bound by shared-memory operand loads and issue slots as the 8 x 8 DFMA register tile was.
 // row stride 18 doubles (144 B): the 16-byte fragment loads of a quarter warp hit 8 distinct bank quads
-constexpr int TZ_TI = 128, TZ_TA = 128, TZ_TK = 16, TZ_LDK = TZ_TK + 2, TZ_STAGES = 3;
-constexpr size_t TZ_SMEM = sizeof(double) * TZ_STAGES * 2 * TZ_TI * TZ_LDK;
+// a tiles of 64 columns: the lags d > a of a tile's last lag chunk (the triangle, computed on
+// zero-filled x) cost TA^2 / 2 per tile, 1/5 of the C4 products at TA = 128, 1/9 at 64;
+// 8 warps as 4 (i) x 2 (a), each 32 x 32 = 4 x 4 DMMA accumulators
+constexpr int TZ_TI = 128, TZ_TA = 64, TZ_TK = 16, TZ_LDK = TZ_TK + 2, TZ_STAGES = 3, TZ_UI = 4, TZ_VA = 4;
+constexpr size_t TZ_SMEM = sizeof(double) * TZ_STAGES * (TZ_TI + TZ_TA) * TZ_LDK;
 // 8 warps as 2 (i) x 4 (a), warp tile 64 i x 32 a = 8 x 4 DMMA tiles, 64 accumulators per lane.
 // Shared tiles row-major [i or a][k] with row stride 20 doubles: the fragment loads (lane -> k =
 // lane % 4, m / n = lane / 4) hit 16 distinct 8-byte bank pairs per half warp.  Global -> shared
@@ -386,14 +389,14 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // Work units (1-D grid): a-tile at (in order), then chunk of dpz lags within the tile's lag range
 // [0, min(nt, a0 + 128)) (lags beyond the tile's last column contribute nothing), then i-tile: all
 // units but a tile's last chunk cost the same, and the host sizes dpz for whole waves of the SMs.
-__global__ void __launch_bounds__(256) k_toeplitz_mm(const double* __restrict__ T, long long ldT_d,
+__global__ void __launch_bounds__(256, 2) k_toeplitz_mm(const double* __restrict__ T, long long ldT_d,
                                                     int ldT, const double* __restrict__ x, int ng, int nt,
                                                     int dpz, double* __restrict__ part) {
   extern __shared__ __align__(16) double tz_sm[];
   // stage s: Ts = tz_sm + s * 2 * TI * LDK  ([ii][jj] = T_d[i0 + ii][j0 + jj]),
   //          Xs = Ts + TI * LDK            ([aa][jj] = X[j0 + jj][a0 + aa - d] = x[(a0 + aa - d) ng + j0 + jj])
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wi = (warp & 1) * 64, wa = (warp >> 1) * 32, fr = lane & 3, fc = lane >> 2;
+  const int wi = (warp & 3) * (8 * TZ_UI), wa = (warp >> 2) * (8 * TZ_VA), fr = lane & 3, fc = lane >> 2;
   const int nti = (ng + TZ_TI - 1) / TZ_TI;
   int r = blockIdx.x, at = 0;
   for (;; ++at) {
@@ -405,13 +408,13 @@ __global__ void __launch_bounds__(256) k_toeplitz_mm(const double* __restrict__ 
   const int d0 = chunk * dpz, d1 = min(min(nt, d0 + dpz), a0 + TZ_TA);   // d > a: nothing
   const int nj = (ng + TZ_TK - 1) / TZ_TK;
   const int nsteps = max(0, d1 - d0) * nj;
-  double acc[8][4][2];
+  double acc[TZ_UI][TZ_VA][2];
 #pragma unroll
-  for (int u = 0; u < 8; ++u)
+  for (int u = 0; u < TZ_UI; ++u)
 #pragma unroll
-    for (int v = 0; v < 4; ++v) acc[u][v][0] = acc[u][v][1] = 0.0;
+    for (int v = 0; v < TZ_VA; ++v) acc[u][v][0] = acc[u][v][1] = 0.0;
   auto issue = [&](int step) {
-    double* Ts = tz_sm + (step % TZ_STAGES) * (2 * TZ_TI * TZ_LDK);
+    double* Ts = tz_sm + (step % TZ_STAGES) * ((TZ_TI + TZ_TA) * TZ_LDK);
     double* Xs = Ts + TZ_TI * TZ_LDK;
     const int d = d0 + step / nj, j0 = (step % nj) * TZ_TK;
 #pragma unroll
@@ -423,7 +426,7 @@ __global__ void __launch_bounds__(256) k_toeplitz_mm(const double* __restrict__ 
       cp_async16(Ts + ii * TZ_LDK + jj, src, bytes);
     }
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {            // X: 128 columns x 16 doubles (rows of x need not be 16-B aligned)
+    for (int q = 0; q < TZ_TA * 16 / 256; ++q) {  // X: TA columns x 16 doubles (rows of x need not be 16-B aligned)
       const int e = tid + q * 256, aa = e >> 4, jj = e & 15;
       const int b = a0 + aa - d, j = j0 + jj;
       const bool ok = j < ng && b >= 0 && b < nt;
@@ -441,34 +444,34 @@ __global__ void __launch_bounds__(256) k_toeplitz_mm(const double* __restrict__ 
                                              // stage refilled below was last read in step - 1
     if (step + TZ_STAGES - 1 < nsteps) issue(step + TZ_STAGES - 1);
     cp_async_commit();
-    const double* Ts = tz_sm + (step % TZ_STAGES) * (2 * TZ_TI * TZ_LDK);
+    const double* Ts = tz_sm + (step % TZ_STAGES) * ((TZ_TI + TZ_TA) * TZ_LDK);
     const double* Xs = Ts + TZ_TI * TZ_LDK;
     // k order inside the stage: product s of lane (fc, fr) takes k = 4 fr + s (the sum over the 16
     // k of the stage is the same), so a lane's fragments of two products are one 16-byte load
 #pragma unroll
     for (int h = 0; h < TZ_TK / 8; ++h) {
-      double2 af[8], bf[4];
+      double2 af[TZ_UI], bf[TZ_VA];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) af[u] = *reinterpret_cast<const double2*>(Ts + (wi + 8 * u + fc) * TZ_LDK + 4 * fr + 2 * h);
+      for (int u = 0; u < TZ_UI; ++u) af[u] = *reinterpret_cast<const double2*>(Ts + (wi + 8 * u + fc) * TZ_LDK + 4 * fr + 2 * h);
 #pragma unroll
-      for (int v = 0; v < 4; ++v) bf[v] = *reinterpret_cast<const double2*>(Xs + (wa + 8 * v + fc) * TZ_LDK + 4 * fr + 2 * h);
+      for (int v = 0; v < TZ_VA; ++v) bf[v] = *reinterpret_cast<const double2*>(Xs + (wa + 8 * v + fc) * TZ_LDK + 4 * fr + 2 * h);
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
+      for (int u = 0; u < TZ_UI; ++u)
 #pragma unroll
-        for (int v = 0; v < 4; ++v) dmma_8x8x4(acc[u][v], af[u].x, bf[v].x);
+        for (int v = 0; v < TZ_VA; ++v) dmma_8x8x4(acc[u][v], af[u].x, bf[v].x);
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
+      for (int u = 0; u < TZ_UI; ++u)
 #pragma unroll
-        for (int v = 0; v < 4; ++v) dmma_8x8x4(acc[u][v], af[u].y, bf[v].y);
+        for (int v = 0; v < TZ_VA; ++v) dmma_8x8x4(acc[u][v], af[u].y, bf[v].y);
     }
   }
   cp_async_wait<0>();
   // partial Y tile of this lag range: part[z][a][i]; lane holds D[fc][2 fr + e] of each tile
   const long long n = (long long)nt * ng;
 #pragma unroll
-  for (int u = 0; u < 8; ++u)
+  for (int u = 0; u < TZ_UI; ++u)
 #pragma unroll
-    for (int v = 0; v < 4; ++v)
+    for (int v = 0; v < TZ_VA; ++v)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int i = i0 + wi + 8 * u + fc, a = a0 + wa + 8 * v + 2 * fr + e;
@@ -489,7 +492,15 @@ bem_status toeplitz_gemv(const bem_matrix* A, double a, const double* x, double 
   const bem_mesh* m = A->mesh;
   const int ng = m->ng, nt = m->nt;
   const long long n = (long long)ng * nt;
-  // lag chunk dpz: minimise (waves of the SMs at one CTA each) x dpz, the critical path of equal units
+  static bool attr = false;
+  static int tz_ctas = 1;
+  if (!attr) {
+    cudaFuncSetAttribute(k_toeplitz_mm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TZ_SMEM);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tz_ctas, k_toeplitz_mm, 256, TZ_SMEM) != cudaSuccess || tz_ctas < 1) tz_ctas = 1;
+    attr = true;
+  }
+  // lag chunk dpz: minimise the busiest SM's time, (units per SM) x (dpz + 4), where two co-resident
+  // units share the SM's FP64 tensor pipe at ~1.15x the throughput of one (C4 measured)
   const int nti = (ng + TZ_TI - 1) / TZ_TI, nta = (nt + TZ_TA - 1) / TZ_TA, sms = num_sms();
   auto units = [&](int dz) {
     long long u = 0;
@@ -500,7 +511,8 @@ bem_status toeplitz_gemv(const bem_matrix* A, double a, const double* x, double 
   double best = 1e300;
   for (int dz = std::min(nt, 8); dz <= nt; ++dz) {
     const long long u = units(dz);
-    const double cost = (double)((u + sms - 1) / sms) * (dz + 4);   // + 4: per-unit fill / epilogue
+    const long long per_sm = (u + sms - 1) / sms;
+    const double cost = (double)per_sm * (dz + 4) / (per_sm >= 2 && tz_ctas >= 2 ? 1.15 : 1.0);   // + 4: fill / epilogue
     if (cost < best) best = cost, dpz = dz;
   }
   const long long nunits = units(dpz);
@@ -510,11 +522,6 @@ bem_status toeplitz_gemv(const bem_matrix* A, double a, const double* x, double 
   cudaError_t e = storage_acquire(m->device, bytes, st, (void**)&part);
   if (e != cudaSuccess) return cuda_fail(e, "toeplitz product");
   e = cudaMemsetAsync(part, 0, bytes, st);   // lag ranges beyond a tile's columns leave their slots zero
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_toeplitz_mm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TZ_SMEM);
-    attr = true;
-  }
   k_toeplitz_mm<<<(unsigned)nunits, 256, TZ_SMEM, st>>>(A->data, A->poff.size() > 1 ? A->poff[1] - A->poff[0] : 0,
                                       (int)pad4(ng), x, ng, nt, dpz, part);
   k_toeplitz_reduce<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(part, nsplit, n, a, b, y);
