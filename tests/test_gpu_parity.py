@@ -738,3 +738,22 @@ def test_potential_parity_hard_points(name):
     got = S.eval_potential(m, cuda(wh), cuda(g), pts).cpu().numpy()
     ref = om.potential(wh, g, pts)
     assert relmax(got, ref) <= 1e-11, relmax(got, ref)
+
+
+@pytest.mark.gpu
+def test_storage_beyond_device_memory_reports_nomem():
+    """maximum sizes: V_h of a 1024-element, 1024-step square needs ~2.2 TB even in symmetric packed
+    storage (far beyond one GPU's 180 GB): bem_assemble fails with BEM_E_NOMEM (include/stbem.h)
+    before any kernel runs, and the library stays usable -- the same process then assembles and
+    checks a small matrix"""
+    from workloads.configs import square
+    big = S.Mesh.from_workload(square(256, 1024, name="huge", tol=1e-10))
+    with pytest.raises(S.BemError) as ei:
+        big.assemble_V()
+    assert ei.value.status == 2, str(ei.value)             # BEM_E_NOMEM
+    big.close()
+    w = W.get("C1")
+    om = O.OracleMesh(w)
+    ref = om.dense("V")
+    got = S.Mesh.from_workload(w).assemble_V().dense()
+    assert relmax(got, ref) <= 1e-11
