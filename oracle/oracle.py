@@ -208,6 +208,21 @@ class OracleMesh:
         """(1/2 M_h + K_h) g (eq. 4) with u0 = 0"""
         return 0.5 * self.mass_primal() @ g + K @ g
 
+    def rhs_rows(self, rows, g):
+        """rows r = (a, i) of (1/2 M_h + K_h) g (eq. 4) without the dense matrices: K_h row
+        entries (b <= a; causal) from the C oracle, the M_h row by P:89
+        (h_t(a) h_i / 2 at columns (a, i) and (a, i + 1))"""
+        g = np.asarray(g, dtype=np.float64)
+        ng = self.ng
+        out = np.empty(len(rows))
+        for k, r in enumerate(rows):
+            a, i = divmod(int(r), ng)
+            cols = np.arange((a + 1) * ng)
+            kg = float(self.entries("K", np.full(len(cols), r), cols) @ g[cols])
+            mg = self.ht[a] * self.seg_h[i] / 2 * (g[a * ng + i] + g[a * ng + (i + 1) % ng])
+            out[k] = 0.5 * mg + kg
+        return out
+
     # ------------------------------------------------ representation formula (f2)
     def potential(self, w, g, pts, q=20):
         """u(x,t) = (Vt w)(x,t) - (W g)(x,t) at interior points pts[k] = (x1, x2, t), u0 = 0

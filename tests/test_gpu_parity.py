@@ -757,3 +757,25 @@ def test_storage_beyond_device_memory_reports_nomem():
     ref = om.dense("V")
     got = S.Mesh.from_workload(w).assemble_V().dense()
     assert relmax(got, ref) <= 1e-11
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["C3", "C5"])
+def test_rhs_fused_full_size_sampled_rows(name):
+    """BJ configs C3, C5 at full size in the bench's product mode (bem_rhs_fused: K_h g with K_h
+    never stored, one slice): rows of the first, second, middle and last test steps of
+    b = (1/2 M_h + K_h) g against the oracle row by row"""
+    w = W.get(name)
+    m = S.Mesh.from_workload(w)
+    g_h = W.dirichlet_data(w)
+    Mp = m.assemble_M(S.MASS_PRIMAL)
+    b = torch.empty(w.n, dtype=torch.float64, device="cuda")
+    S.rhs_fused(m, Mp, cuda(g_h), b)
+    got = b.cpu().numpy()
+    rng = np.random.default_rng(1811)
+    ng, nt = w.n_gamma, w.n_steps
+    rows = [a * ng + int(i) for a in (0, 1, nt // 2, nt - 1) for i in rng.choice(ng, 2, replace=False)]
+    ref = O.OracleMesh(w).rhs_rows(rows, g_h)
+    err = float(np.abs(got[rows] - ref).max() / np.abs(ref).max())
+    print(f"{name} fused rhs sampled rows rel error {err:.3e}")
+    assert err <= 1e-11

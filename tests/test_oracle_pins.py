@@ -505,3 +505,15 @@ def test_initial_potential_in_Q_closed_forms(t):
         P2, _ = _gauss_moments(x2, sigma)
         assert one[k] == pytest.approx(P1 * P2, rel=1e-12), (t, k)
         assert lin[k] == pytest.approx(M1 * P2, rel=1e-11, abs=1e-15), (t, k)
+
+
+def test_rhs_rows_equal_the_dense_rhs():
+    """oracle rhs_rows (row-wise (1/2 M_h + K_h) g for the full-size sampled tests) against the dense
+    (1/2 M_h + K_h) g on C1: the causal row range and the mass row of P:89"""
+    import workloads as W
+    w = W.get("C1")
+    om = O.OracleMesh(w)
+    g = W.dirichlet_data(w)
+    ref = om.rhs(om.dense("K"), g)
+    rows = [0, 1, w.n_gamma - 1, w.n // 2, w.n - 1]
+    assert np.abs(om.rhs_rows(rows, g) - ref[rows]).max() <= 1e-14 * np.abs(ref).max()
