@@ -208,6 +208,17 @@ class OracleMesh:
         """(1/2 M_h + K_h) g (eq. 4) with u0 = 0"""
         return 0.5 * self.mass_primal() @ g + K @ g
 
+    def matvec_rows(self, kind, rows, x):
+        """rows r = (a, i) of A x for A in {V_h, K_h, D_h}: sum over the causal columns (b <= a, P:86-88,
+        P:104) of the C oracle's entries times x"""
+        x = np.asarray(x, dtype=np.float64)
+        out = np.empty(len(rows))
+        for k, r in enumerate(rows):
+            a = int(r) // self.ng
+            cols = np.arange((a + 1) * self.ng)
+            out[k] = float(self.entries(kind, np.full(len(cols), r), cols) @ x[cols])
+        return out
+
     def rhs_rows(self, rows, g):
         """rows r = (a, i) of (1/2 M_h + K_h) g (eq. 4) without the dense matrices: K_h row
         entries (b <= a; causal) from the C oracle, the M_h row by P:89

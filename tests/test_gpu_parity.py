@@ -779,3 +779,29 @@ def test_rhs_fused_full_size_sampled_rows(name):
     err = float(np.abs(got[rows] - ref).max() / np.abs(ref).max())
     print(f"{name} fused rhs sampled rows rel error {err:.3e}")
     assert err <= 1e-11
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["C3", "C5"])
+def test_gemv_full_size_sampled_rows(name):
+    """BJ configs C3, C5 at full size: the bench's stored V_h, D_h (symmetric packed, one slice) and
+    the fused-reduction SYMV, y = A x for a seeded x, against the oracle on rows of the first,
+    second, middle and last test steps"""
+    w = W.get(name)
+    m = S.Mesh.from_workload(w)
+    x_h = np.random.default_rng(1811).standard_normal(w.n)
+    x = cuda(x_h)
+    rng = np.random.default_rng(7)
+    ng, nt = w.n_gamma, w.n_steps
+    rows = [a * ng + int(i) for a in (0, 1, nt // 2, nt - 1) for i in rng.choice(ng, 2, replace=False)]
+    om = O.OracleMesh(w)
+    for kind in "VD":
+        A = m.assemble_V() if kind == "V" else m.assemble_D()
+        y = torch.empty_like(x)
+        A.matvec(x, y)
+        got = y.cpu().numpy()[rows]
+        A.close()
+        ref = om.matvec_rows(kind, rows, x_h)
+        err = float(np.abs(got - ref).max() / np.abs(ref).max())
+        print(f"{name} {kind} product sampled rows rel error {err:.3e}")
+        assert err <= 1e-11

@@ -517,3 +517,14 @@ def test_rhs_rows_equal_the_dense_rhs():
     ref = om.rhs(om.dense("K"), g)
     rows = [0, 1, w.n_gamma - 1, w.n // 2, w.n - 1]
     assert np.abs(om.rhs_rows(rows, g) - ref[rows]).max() <= 1e-14 * np.abs(ref).max()
+
+
+def test_matvec_rows_equal_the_dense_products():
+    import workloads as W
+    w = W.get("C1")
+    om = O.OracleMesh(w)
+    x = np.random.default_rng(5).standard_normal(w.n)
+    rows = [0, 3, w.n // 2, w.n - 1]
+    for kind in "VD":
+        ref = om.dense(kind) @ x
+        assert np.abs(om.matvec_rows(kind, rows, x) - ref[rows]).max() <= 1e-14 * np.abs(ref).max()
