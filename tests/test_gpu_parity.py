@@ -451,7 +451,7 @@ def test_large_kappa_falls_back_to_legacy_touching_path():
 
 
 def test_c4_sampled_entries_block_toeplitz():
-    """BJ configs[3] (C4, N = 262 144, the largest): its dense matrices need 8 GPUs, the uniform
+    """BJ configs[3] (C4, N = 262 144, the largest): its dense V_h + D_h need 2 x 146 GB, the uniform
     steps let the block-Toeplitz variant hold every entry on one GPU; sampled entries (diagonal,
     near and random cells) against the oracle"""
     w = W.get("C4")
@@ -804,4 +804,29 @@ def test_gemv_full_size_sampled_rows(name):
         ref = om.matvec_rows(kind, rows, x_h)
         err = float(np.abs(got - ref).max() / np.abs(ref).max())
         print(f"{name} {kind} product sampled rows rel error {err:.3e}")
+        assert err <= 1e-11
+
+
+@pytest.mark.gpu
+def test_c4_toeplitz_products_sampled_rows():
+    """C4 at full size through the block-Toeplitz variant the bench times: y = T x (the DMMA GEMM over
+    the stacked lags, lag-chunk partials reduced in fixed order) for V_h and D_h, rows of the first,
+    second, middle and last test steps against the oracle's row sums"""
+    w = W.get("C4")
+    m = S.Mesh.from_workload(w)
+    x_h = np.random.default_rng(1811).standard_normal(w.n)
+    x = cuda(x_h)
+    rng = np.random.default_rng(11)
+    ng, nt = w.n_gamma, w.n_steps
+    rows = [a * ng + int(i) for a in (0, 1, nt // 2, nt - 1) for i in rng.choice(ng, 2, replace=False)]
+    om = O.OracleMesh(w)
+    for kind in "VD":
+        T = m.assemble_toeplitz(kind)
+        y = torch.empty_like(x)
+        T.matvec(x, y)
+        got = y.cpu().numpy()[rows]
+        T.close()
+        ref = om.matvec_rows(kind, rows, x_h)
+        err = float(np.abs(got - ref).max() / np.abs(ref).max())
+        print(f"C4 Toeplitz {kind} product sampled rows rel error {err:.3e}")
         assert err <= 1e-11
