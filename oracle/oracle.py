@@ -8,7 +8,9 @@ Matrix entries come from the plain C oracle (stbem_oracle.c, ctypes).  This
 module adds, in plain numpy and in the paper's order:
   * mass matrices M_h (primal, eq. 4) and M_h (dual pairing, Thm 1),
     the lumped dual mass (row sums, P:185);
-  * the right-hand side (1/2 M_h + K_h) g of eq. (4) (P:83), u0 = 0;
+  * the right-hand side (1/2 M_h + K_h) g of eq. (4), u0 = 0, dense or row by row
+    (rhs_rows), and row-wise products of V_h, K_h, D_h (matvec_rows) for the full-size sampled tests
+    (both pinned to the dense forms on C1);
   * full GMRES with modified Gram-Schmidt, x0 = 0, left preconditioning by
     C_V^{-1} = M_h^{-1} D_h M_h^{-T} (lumped or exact), stopping on the
     Givens estimate of the preconditioned relative residual (P:98-99, P:182);
