@@ -1,12 +1,15 @@
 #!/usr/bin/env python
-"""bench.py — one step = the whole hot path of arXiv:1811.05224 on one workload (BJ configs[2],
-C3: unit square, 256 segments x 256 uniform steps, N = 65536, alpha = 1):
-  mesh (a1) -> assemble V_h, K_h, D_h (a2-a5) -> mass matrices (a6) -> b = 1/2 M g + K g (a7)
-  -> preconditioned GMRES to 1e-10 (a8-a10, lumped dual mass).
+"""bench.py — one step = the whole hot path of arXiv:1811.05224 on one workload, by default the
+largest BASELINE.json configuration that fits one GPU: configs[4], C5 (L-shape, 384 segments x
+256 steps graded toward t = 0, N = 98 304, alpha = 0.5):
+  mesh (a1) -> assemble V_h, D_h (a2, a3, a5) -> mass matrices (a6) -> b = 1/2 M g + K g with K_h
+  computed and applied on the fly (a4, a7) -> GMRES to 1e-10 preconditioned by
+  M_h^{-1} D_h M_h^{-T} with the exact dual mass (a8-a10; --precond 1: the lumped mass of P:185).
 
-python bench.py [--gpus N] [--steps K] [--warmup W] [--impl native|reference] [--config C3]
-Under torchrun (N > 1) one rank per GPU; P = 2N temporal slices owned by the cyclic K_P plan.
-Prints ONE JSON line on rank 0 (contract in the task statement / DESIGN.md section 7).
+python bench.py [--gpus N] [--steps K] [--warmup W] [--impl native|reference] [--config C5]
+--gpus N > 1 without torchrun: the script re-launches itself under torch.distributed.run with N
+ranks (one per GPU); P = 2N temporal slices owned by the cyclic K_P plan.  Prints ONE JSON line on
+rank 0 (contract in the task statement / DESIGN.md section 6).
 """
 import argparse
 import json
@@ -36,7 +39,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)   # ~0.75 s timed: several nvidia-smi samples
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
-    ap.add_argument("--config", default="C3")
+    ap.add_argument("--config", default="C5")
     # 2: exact dual mass (cyclic-tridiagonal solves on the device, the north star's "sparse
     # mass-matrix solves"); 1: the lumped diagonal of P:185 (study in DESIGN.md section 6.2)
     ap.add_argument("--precond", type=int, default=2)
@@ -45,7 +48,43 @@ def parse():
     ap.add_argument("--variant", default="dense", choices=["dense", "toeplitz"])
     ap.add_argument("--overlap", type=int, default=1)   # V_h, D_h assembled on side streams
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-isolated", action="store_true")   # skip the serialised per-matrix pass
     return ap.parse_args()
+
+
+def relaunch_distributed(args):
+    """--gpus N > 1 outside torchrun: run this script under torch.distributed.run with N ranks (one
+    process per GPU, rendezvous on 127.0.0.1) and return its exit code"""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def config_of(w, args, world):
+    """the workload description shared by both arms (same keys, same values)"""
+    names = "C1 C2 C3 C4 C5".split()
+    idx = names.index(w.name) if w.name in names else "-"
+    P = 1 if world == 1 else 2 * world
+    return {"workload": f"BJ configs[{idx}] ({w.name}): {w.note}", "variant": args.variant,
+            "n_gamma": w.n_gamma, "n_steps": w.n_steps, "N": w.n, "alpha": w.alpha,
+            "slices_P": P, "gmres_tol": w.tol, "precond": ["none", "lumped", "exact"][args.precond],
+            "parallelism": f"cyclic K_P plan, P = {P} temporal slices over {world} GPU" + ("s" if world > 1 else ""),
+            "l2": "inputs larger than L2: V_h and D_h (symmetric packed) %.1f GB each >> 126 MB, streamed "
+                  "once per product" % (8e-9 * w.n_gamma * (w.n_gamma + 32) / 2 * w.n_steps * (w.n_steps + 1) / 2)}
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 # ---------------------------------------------------------------------- clocks
@@ -100,11 +139,22 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------- oracle baseline
-def cpu_baseline(w, seconds, steps=1):
-    """the oracle as it stands (oracle/stbem_oracle.c, OpenMP, all host cores) on a bounded sample
-    of the same workload: V, K, D entries of a band of test rows around a = N_I/2 (all trial steps
-    b <= a), sized to ~`seconds` of CPU work; value = entries computed per second."""
+def cpu_baseline(w, seconds, steps=1, threads=None):
+    """the oracle as it stands (oracle/stbem_oracle.c, OpenMP, all host cores or `threads`) on a
+    bounded sample of the same workload: V, K, D entries of test row a = N_I/2 (random trial
+    entries b <= a), sized to ~`seconds` of CPU work; value = entries computed per second."""
     from oracle import oracle as O
+    all_threads = O.lib().ora_num_threads()
+    if threads:
+        O.lib().omp_set_num_threads(int(threads))   # libgomp, loaded with the oracle
+    try:
+        return _cpu_baseline(O, w, seconds)
+    finally:
+        if threads:
+            O.lib().omp_set_num_threads(int(all_threads))
+
+
+def _cpu_baseline(O, w, seconds):
     m = O.OracleMesh(w)
     ng, nt = w.n_gamma, w.n_steps
     a = nt // 2
@@ -128,7 +178,8 @@ def cpu_baseline(w, seconds, steps=1):
         done += triples
     return {"value": 3 * done / dt, "unit": UNIT, "cores": O.lib().ora_num_threads(), "kind": "oracle",
             "sample": f"{done} random entries each of V_h, K_h, D_h in test row a={a} of {w.name} "
-                      f"(all b <= a), {dt:.1f} s", "seconds": dt}
+                      f"(all b <= a), {dt:.1f} s", "seconds": dt, "cpu_model": cpu_model(),
+            "host_cpus": os.cpu_count()}
 
 
 # ---------------------------------------------------------------------- native step
@@ -142,6 +193,8 @@ def native(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -273,6 +326,9 @@ def native(args):
     barrier()
     t_e2e = e2[0].elapsed_time(e2[1]) / 1e3
     gc.enable()
+    # after the timed regions: one serialised pass, each assembly alone on the GPU (the timed steps
+    # overlap V_h and D_h with K_h g), for per-matrix seconds and the isolated kernel rates
+    iso = None if args.no_isolated else isolated_pass(S, w, P, comm, g, b, args)
     if rank == 0:
         clocks.window(t_wall, time.perf_counter())
     ck = clocks.stop() if rank == 0 else None
@@ -308,13 +364,18 @@ def native(args):
     # assembly roofline: the longest bulk kernel (k_bulk_m<KIND>), FP64 flops from the exact
     # per-regime node counts x the static FP64 counts of the shipped forms,
     # and its store stream (8 B per stored entry)
+    # (the isolated pass when it ran: each assembly alone on the GPU; else the timed steps' own
+    # kernel events, taken while V_h, D_h and K_h g overlap)
+    src = iso["stats"] if iso else stats
     fam = []
     for k in "VKD":
-        st = stats[k]
+        st = src[k]
         fam.append((st["ms_bulk"], k, "bulk", st))
     ms_dom, kdom, _, st = max(fam)
     flops = st["flops_bulk"]
     achieved = flops / (ms_dom * 1e-3) / 1e12
+    all_bulk_flops = sum(src[k]["flops_bulk"] for k in "VKD")
+    all_bulk_ms = sum(src[k]["ms_bulk"] for k in "VKD")
     nt_ = w.n_steps
     cells = nt_ * (nt_ + 1) / 2
     bulk_entries = stats[kdom]["entries"] * (cells - (2 * nt_ - 1)) / cells   # stored entries of cells d >= 2
@@ -332,6 +393,10 @@ def native(args):
                 "peak_note": "FP64 DFMA: 148 SM x 64 FMA/clk x 2 x 1.965 GHz (derived from the guide's unit counts "
                              "and MEASURED_PEAKS sm_max_mhz); tools/fp64_peak.cu measured 34.1 TFLOP/s",
                 "flops_per_launch": flops, "node_evals_per_launch": st["evals_bulk"],
+                "timing": "isolated (serialised pass after the timed region)" if iso else "inside the overlapped step",
+                "all_bulk_kernels": {"flops": all_bulk_flops, "ms": all_bulk_ms,
+                                     "tflops": all_bulk_flops / (all_bulk_ms * 1e-3) / 1e12,
+                                     "frac": all_bulk_flops / (all_bulk_ms * 1e-3) / 1e12 / FP64_PEAK_DERIVED},
                 "nodes_by_regime_ABZC": st["nodes_bulk"],
                 "flops_note": "algorithmic: exact per-regime node counts x static FP64 flops of the shipped "
                               "moment forms (DFMA = 2), DESIGN.md section 6"}
@@ -386,20 +451,19 @@ def native(args):
         "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"BJ configs[{'C1 C2 C3 C4 C5'.split().index(w.name) if w.name in 'C1 C2 C3 C4 C5'.split() else '-'}] ({w.name}): {w.note}",
-                   "variant": args.variant, "n_gamma": w.n_gamma, "n_steps": w.n_steps,
-                   "N": n, "alpha": w.alpha, "slices_P": P, "gmres_tol": tol, "precond": ["none", "lumped", "exact"][args.precond],
-                   "parallelism": f"cyclic K_P blocks over {world} GPU" + ("s" if world > 1 else ""),
-                   "l2": "inputs larger than L2 (V_h %.1f GB, D_h %.1f GB >> 126 MB)" % (stats["V"]["bytes"] / 1e9, stats["D"]["bytes"] / 1e9)},
+        "config": config_of(w, args, world),
         "components": {
             "assembly_pairs_per_s": units_per_step / asm_s,
             "integrals_per_step": {k: stats[k]["entries"] for k in "VKD"},
             "matrix_entries_represented_per_s": represented_per_step / (1e-3 * ms),
             "storage": "V_h, D_h: symmetric packed spatial blocks (upper 32x32 tile triangle); K_h computed "
                        "and applied to g on the fly (bem_rhs_fused), never stored",
-            "assembly_s": {"V": ph["assemble_V"], "K": ph["assemble_K"], "D": ph["assemble_D"], "all": ph["assembly"],
-                           "note": ("V_h and D_h on side streams concurrently with K_h g: the per-matrix "
-                                    "phases are enqueue marks, 'all' is the assembly time") if args.overlap else ""},
+            "assembly_s": {"all_in_step": ph["assembly"],
+                           "isolated": iso["seconds"] if iso else None,
+                           "isolated_pairs_per_s": iso["pairs_per_s"] if iso else None,
+                           "note": "all_in_step: mesh -> V_h, D_h (side streams) and K_h g done, median of the timed "
+                                   "steps; isolated: each matrix assembled alone after the timed region (CUDA events "
+                                   "on its stream, mesh and mass matrices excluded)"},
             "matvec_gbs": gemv_gbs, "matvec_frac_of_hbm": (gemv_gbs / hbm_peak) if gemv_gbs else None,
             "gmres_solve_s": ph["solve"], "gmres_iterations": rep["iterations"],
             "gmres_true_rel_residual": rep["true_rel_residual"], "time_to_solution_s": ph["total"],
@@ -418,11 +482,44 @@ def native(args):
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline(w, args.cpu_seconds)
+            one = cpu_baseline(w, max(3.0, args.cpu_seconds / 3), threads=1)
+            out["cpu_baseline"]["single_thread"] = {"value": one["value"], "cores": 1, "sample": one["sample"]}
         print(json.dumps(out), flush=True)
     if comm:
         comm.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def isolated_pass(S, w, P, comm, g, b, args):
+    """each matrix assembled alone (serialised, synchronised), timed with CUDA events on the
+    launching stream: per-matrix seconds, pairs/s and the kernel statistics of that assembly"""
+    import torch
+    mesh = S.Mesh.from_workload(w, n_slices=P, comm=comm)
+    Mp = mesh.assemble_M(S.MASS_PRIMAL)
+    torch.cuda.synchronize()
+    out = {"seconds": {}, "pairs_per_s": {}, "stats": {}}
+    toep = args.variant == "toeplitz"
+    for k in "VDK":
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        if k == "K" and not toep:
+            st = S.rhs_fused(mesh, Mp, g, b, stats=True)      # K_h g, K_h never stored (as in the step)
+            e1.record()
+        else:
+            A = mesh.assemble_toeplitz(k) if toep else getattr(mesh, f"assemble_{k}")()
+            e1.record()
+            st = A.stats()
+            A.close()
+        e1.synchronize()
+        sec = e0.elapsed_time(e1) / 1e3
+        out["seconds"][k] = sec
+        out["pairs_per_s"][k] = st["entries"] / sec
+        out["stats"][k] = st
+    Mp.close()
+    mesh.close()
+    torch.cuda.synchronize()
+    return out
 
 
 # ---------------------------------------------------------------------- reference arm
@@ -447,15 +544,17 @@ def reference(args):
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.median(secs)),
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "impl": "reference",
-           "config": {"workload": f"BJ configs[{'C1 C2 C3 C4 C5'.split().index(w.name) if w.name in 'C1 C2 C3 C4 C5'.split() else '-'}] ({w.name}): {w.note}",
-                   "variant": args.variant, "n_gamma": w.n_gamma, "n_steps": w.n_steps, "N": w.n},
-           "cpu_baseline": {"value": v, "unit": UNIT, "cores": r["cores"], "kind": "oracle", "sample": r["sample"]},
+           "config": config_of(w, args, int(os.environ.get("WORLD_SIZE", "1"))),
+           "cpu_baseline": {"value": v, "unit": UNIT, "cores": r["cores"], "kind": "oracle", "sample": r["sample"],
+                            "cpu_model": r["cpu_model"], "host_cpus": r["host_cpus"]},
            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
 
 if __name__ == "__main__":
     a = parse()
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_distributed(a))
     if a.impl == "reference":
         reference(a)
     else:

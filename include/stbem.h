@@ -66,24 +66,32 @@ typedef struct {
   long long entries_total; /* n_gamma^2 n_steps (n_steps+1) / 2 */
   int q_bulk;              /* Gauss points per direction for d = a-b >= 2 (per mesh) */
   double kappa;            /* alpha h_max^2 / (4 min h_t): smoothness ratio choosing q_bulk */
+  int rank, nranks;        /* this process in the communicator (0, 1 without one) */
+  /* vector layout (reading R27): vectors are REPLICATED -- every rank holds all n
+   * entries, local_row0 = 0 and local_rows = n on every rank; a product's owned-block partials are
+   * summed over the ranks inside the library, so the caller never exchanges vector pieces */
+  long long local_rows, local_row0;
 } bem_mesh_info;
 
-/* Quadrature options; NULL = documented defaults.  0 = default. */
+/* Quadrature options (the paper's quadrature is unpublished, reading R1 and section
+ * 4.3); NULL or 0 in a field = the documented default.  Negative values, q_far not in
+ * {3,4,5,6,8}, q_near not in [3,16], q_sing not in [4,16] or unknown flags: BEM_E_INVALID. */
 typedef struct {
-  int q_bulk;   /* Gauss order per direction for time cells d >= 2; 0 = chosen from kappa */
+  int q_far;    /* Gauss order per direction for the time cells d = a - b >= 2; default chosen from
+                   kappa = alpha h_max^2 / (4 min h_t) (bem_mesh_info.q_bulk) */
+  int q_near;   /* time cells d <= 1, non-touching pairs at distance ratio dist / h >= near_gap;
+                   default min(6, q_far + 1) */
+  int near_gap; /* time cells d <= 1: pairs closer than near_gap element lengths take the measured
+                   orders 10 (ratio < 2.5), 8 (< 5), 6 (< near_gap); default 9 */
   int q_sing;   /* order of the Duffy / 1-D reduction rules for touching pairs (default 16) */
-  int flags;    /* BEM_QUAD_LEGACY_SING: touching pairs by per-lag singular rules (k_sing) instead
-                   of moment records; 0 = records whenever alpha (h_X+h_Y)^2 / (4 min h_t) < 4 */
+  int flags;    /* BEM_QUAD_* below */
 } bem_quad_opts;
+/* touching pairs by per-lag singular rules (k_sing) instead of moment records; without it the
+ * records are used whenever alpha (h_X + h_Y)^2 / (4 min h_t) < 4 */
 #define BEM_QUAD_LEGACY_SING 1
 /* V_h and D_h store their symmetric spatial blocks packed (upper 32 x 32 tile triangle, about
  * half the bytes and half the assembly work); this flag stores them full */
 #define BEM_QUAD_FULL_STORAGE 2
-/* Bulk time cells (d >= 2): regime-A node values as a contraction on the FP64 tensor cores
- * (k_bulk_t, DMMA m8n8k4) instead of the default Horner-chain DFMA kernel k_bulk_m (same regimes,
- * results to rounding).  Opt-in: DMMA and DFMA share the FP64 units on B200 and k_bulk_t measured
- * slower on C3 */
-#define BEM_QUAD_BULK_MMA 4
 
 typedef enum {
   BEM_MASS_PRIMAL = 0,      /* M_h of eq. (4): <phi^10_(a,n), phi^0_(a,i)> */
@@ -222,14 +230,6 @@ bem_status bem_rhs_fused(const bem_mesh* mesh, const bem_quad_opts* opts, const 
                          const double* g_dev, double* b_dev, bem_assembly_stats* stats, bem_stream stream);
 
 /* ----------------------------------------------------------------- solver */
-/* Preconditioned full GMRES (P:98-99, P:182) for V w = b with left preconditioner
- * C_V^{-1} = M^{-1} D M^{-T} (P:120); D and M are ignored when opts->precond == 0.
- * M must be BEM_MASS_DUAL_LUMPED for precond 1 and BEM_MASS_DUAL for precond 2.
- * x0 = 0.  b_dev, w_dev device vectors of length n.  res_hist_host: NULL or max_iter+1 doubles
- * (relative preconditioned residual estimates, [0] = 1).  Runs on `stream` (ordered after the work
- * already queued there, e.g. the right-hand side) and synchronises it once per iteration (the
- * Hessenberg column goes to the host for the Givens rotation).  Returns BEM_E_NOT_CONVERGED /
- * BEM_E_BREAKDOWN with w and the report filled. */
 /* Initial potential term of eq. (4): b <- b - M_h^0 u0 with
  * M_h^0[(a,i), j] = <M_0 phi^1_j, phi^0_(a,i)>, u0 in S_h^1(Omega_h) given by its nodal values on a
  * triangulation of Omega (nodes_xy: n_nodes x 2, tris: n_tri x 3 node indices, both HOST; u0_dev,
@@ -259,6 +259,14 @@ bem_status bem_eval_potential(const bem_mesh* mesh, const double* w_dev, const d
 bem_status bem_eval_potential_initial(const bem_mesh* mesh, int n_nodes, const double* nodes_xy, int n_tri,
                                       const int* tris, const double* u0_dev, long long npts,
                                       const double* pts_dev, double* u_dev, bem_stream stream);
+/* Preconditioned full GMRES (P:98-99, P:182) for V w = b with left preconditioner
+ * C_V^{-1} = M^{-1} D M^{-T} (P:120); D and M are ignored when opts->precond == 0.
+ * M must be BEM_MASS_DUAL_LUMPED for precond 1 and BEM_MASS_DUAL for precond 2.
+ * x0 = 0.  b_dev, w_dev device vectors of length n.  res_hist_host: NULL or max_iter+1 doubles
+ * (relative preconditioned residual estimates, [0] = 1).  Runs on `stream` (ordered after the work
+ * already queued there, e.g. the right-hand side) and synchronises it once per iteration (the
+ * Hessenberg column goes to the host for the Givens rotation).  Returns BEM_E_NOT_CONVERGED /
+ * BEM_E_BREAKDOWN with w and the report filled. */
 bem_status bem_solve_gmres(const bem_matrix* V, const bem_matrix* D, const bem_matrix* M,
                            const double* b_dev, double* w_dev, const bem_gmres_opts* opts,
                            bem_solve_report* report, double* res_hist_host, bem_stream stream);

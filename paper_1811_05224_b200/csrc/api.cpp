@@ -31,8 +31,11 @@ struct CachedBlock {
 static std::mutex g_cache_mu;
 static std::vector<CachedBlock> g_cache[64];
 
+static bool g_pool_ready[64] = {false};
+bool pool_ready(int device) { return g_pool_ready[device & 63]; }
+
 void pool_setup(int device) {
-  static bool ready[64] = {false};
+  bool* ready = g_pool_ready;
   if (ready[device & 63]) return;
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
@@ -142,10 +145,9 @@ bem_matrix* new_dense(const bem_mesh* m, int kind, bool sym, cudaStream_t stream
 bem_status assemble(int kind, const bem_mesh* m, const bem_quad_opts* o, bem_stream s, bem_matrix** out) {
   if (!m || !out) { set_error("bem_assemble: null argument"); return BEM_E_INVALID; }
   *out = nullptr;
-  int q_bulk = (o && o->q_bulk > 0) ? o->q_bulk : (kind == STB_D ? m->q_bulk_d : m->q_bulk);
-  int q_sing = (o && o->q_sing > 0) ? o->q_sing : 16;
-  if (q_bulk < 3 || q_bulk > 8 || q_bulk == 7) { set_error("bem_assemble: q_bulk must be one of 3,4,5,6,8"); return BEM_E_INVALID; }
-  if (q_sing < 4 || q_sing > QSING_MAX) { set_error("bem_assemble: q_sing must be in [4,16]"); return BEM_E_INVALID; }
+  QuadCfg qc;
+  bem_status qs = resolve_quad(kind, m, o, "bem_assemble", &qc);
+  if (qs != BEM_OK) return qs;
   if (m->ng < 6) { set_error("bem_assemble: N_Gamma >= 6 required"); return BEM_E_INVALID; }
   cudaSetDevice(m->device);
   bem_status st;
@@ -155,7 +157,7 @@ bem_status assemble(int kind, const bem_mesh* m, const bem_quad_opts* o, bem_str
   if (!A) return st;
   // no memset: the bulk kernel writes every entry of the cells d >= 2 and the near kernel every
   // entry of the cells d <= 1 (the row padding is never read)
-  st = launch_assembly(kind, m, A, q_bulk, q_sing, o ? o->flags : 0, S(s));
+  st = launch_assembly(kind, m, A, qc, S(s));
   if (st == BEM_OK) st = gemv_setup(A);
   if (st != BEM_OK) { bem_matrix_destroy(A); return st; }
   *out = A;
@@ -210,15 +212,16 @@ bem_status bem_assemble_toeplitz(const bem_mesh* m, int kind, const bem_quad_opt
   if (kind < STB_V || kind > STB_D) { set_error("bem_assemble_toeplitz: kind must be 0 (V), 1 (K) or 2 (D)"); return BEM_E_INVALID; }
   if (!m->uniform) { set_error("bem_assemble_toeplitz: needs equal time steps"); return BEM_E_STATE; }
   if (m->nranks > 1) { set_error("bem_assemble_toeplitz: one process (the Toeplitz blocks are replicated)"); return BEM_E_STATE; }
-  int q_bulk = (o && o->q_bulk > 0) ? o->q_bulk : (kind == STB_D ? m->q_bulk_d : m->q_bulk);
-  int q_sing = (o && o->q_sing > 0) ? o->q_sing : 16;
-  if (q_bulk < 3 || q_bulk > 8 || q_bulk == 7) { set_error("bem_assemble_toeplitz: q_bulk must be one of 3,4,5,6,8"); return BEM_E_INVALID; }
-  if (q_sing < 4 || q_sing > QSING_MAX) { set_error("bem_assemble_toeplitz: q_sing must be in [4,16]"); return BEM_E_INVALID; }
+  QuadCfg qc;
+  bem_status qs = resolve_quad(kind, m, o, "bem_assemble_toeplitz", &qc);
+  if (qs != BEM_OK) return qs;
+  qc.flags &= ~BEM_QUAD_FULL_STORAGE;   // the Toeplitz blocks are stored full anyway
+  if (m->ng < 6) { set_error("bem_assemble_toeplitz: N_Gamma >= 6 required"); return BEM_E_INVALID; }
   cudaSetDevice(m->device);
   bem_status st;
   bem_matrix* A = new_dense(m, kind, false, S(s), &st, true);
   if (!A) return st;
-  st = launch_assembly(kind, m, A, q_bulk, q_sing, o ? o->flags : 0, S(s));
+  st = launch_assembly(kind, m, A, qc, S(s));
   if (st != BEM_OK) { bem_matrix_destroy(A); return st; }
   *out = A;
   return BEM_OK;
@@ -280,7 +283,11 @@ bem_status bem_rhs_fused(const bem_mesh* m, const bem_quad_opts* o, const bem_ma
   if (!m || !Mp || !g || !b) { set_error("bem_rhs_fused: null argument"); return BEM_E_INVALID; }
   if (g == b) { set_error("bem_rhs_fused: g and b must not alias"); return BEM_E_INVALID; }
   if (Mp->kind != STB_MASS || Mp->mass_kind != BEM_MASS_PRIMAL) { set_error("bem_rhs_fused: needs the primal mass matrix"); return BEM_E_STATE; }
-  const int flags = o ? o->flags : 0;
+  if (m->ng < 6) { set_error("bem_rhs_fused: N_Gamma >= 6 required"); return BEM_E_INVALID; }
+  QuadCfg qc;
+  bem_status qs = resolve_quad(STB_K, m, o, "bem_rhs_fused", &qc);
+  if (qs != BEM_OK) return qs;
+  const int flags = qc.flags;
   if (!touching_records_ok(STB_K, m, flags)) {
     // large kappa: the per-lag singular kernel needs stored entries; assemble K_h, multiply
     bem_matrix* K = nullptr;
@@ -290,10 +297,6 @@ bem_status bem_rhs_fused(const bem_mesh* m, const bem_quad_opts* o, const bem_ma
     bem_matrix_destroy(K);
     return st;
   }
-  int q_bulk = (o && o->q_bulk > 0) ? o->q_bulk : m->q_bulk;
-  int q_sing = (o && o->q_sing > 0) ? o->q_sing : 16;
-  if (q_bulk < 3 || q_bulk > 8 || q_bulk == 7) { set_error("bem_rhs_fused: q_bulk must be one of 3,4,5,6,8"); return BEM_E_INVALID; }
-  if (q_sing < 4 || q_sing > QSING_MAX) { set_error("bem_rhs_fused: q_sing must be in [4,16]"); return BEM_E_INVALID; }
   cudaSetDevice(m->device);
   bem_matrix* A = new bem_matrix_s();   // statistics only: K_h is never stored
   A->kind = STB_K;
@@ -303,7 +306,7 @@ bem_status bem_rhs_fused(const bem_mesh* m, const bem_quad_opts* o, const bem_ma
     A->poff_base.push_back((int)A->poff.size());
     for (int a = m->blocks[bi].a0; a < m->blocks[bi].a1; ++a) A->poff.push_back(0);
   }
-  bem_status st = launch_assembly(STB_K, m, A, q_bulk, q_sing, flags, S(s), g, b);
+  bem_status st = launch_assembly(STB_K, m, A, qc, S(s), g, b);
   if (st == BEM_OK && m->comm) st = allreduce_sum(m, b, (long long)m->ng * m->nt, S(s));
   if (st == BEM_OK) st = mass_apply(Mp, 0.5, g, 1.0, b, S(s));
   if (st == BEM_OK && stats) st = bem_matrix_stats(A, stats);
@@ -599,6 +602,9 @@ bem_status bem_matrix_get_entries(const bem_matrix* A, long long count, const lo
     offs[k] = entry_offset(A, (int)(rows[k] / m->ng), (int)(rows[k] % m->ng), (int)(cols[k] / m->ng), (int)(cols[k] % m->ng));
   }
   cudaSetDevice(m->device);
+  // the matrix may have been assembled on a non-blocking stream that the legacy stream used below
+  // does not order against: wait for its assembly first
+  if (A->stream) cudaStreamSynchronize(A->stream);
   const long long CH = 1 << 22;
   long long* d_off = nullptr;
   double* d_out = nullptr;
@@ -683,13 +689,29 @@ bem_status bem_matrix_info(const bem_matrix* A, int* kind, long long* entries, l
 
 bem_status bem_release_storage(void) {
   std::lock_guard<std::mutex> lk(g_cache_mu);
-  for (auto& c : g_cache)
+  for (int dev = 0; dev < 64; ++dev) {
+    auto& c = g_cache[dev];
     for (auto& b : c) {
       cudaEventSynchronize(b.freed);
       cudaEventDestroy(b.freed);
       cudaFree(b.ptr);
     }
-  for (auto& c : g_cache) c.clear();
+    c.clear();
+  }
+  // the device pool keeps freed memory mapped (release threshold: infinite, pool_setup): hand it
+  // back to the driver so that other allocators in the process (torch) can use it
+  int cur = 0;
+  cudaGetDevice(&cur);
+  for (int dev = 0; dev < 64; ++dev) {
+    if (!pool_ready(dev)) continue;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      cudaSetDevice(dev);
+      cudaDeviceSynchronize();
+      cudaMemPoolTrimTo(pool, 0);
+    }
+  }
+  cudaSetDevice(cur);
   cudaGetLastError();
   return BEM_OK;
 }

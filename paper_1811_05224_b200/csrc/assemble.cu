@@ -55,7 +55,6 @@ struct BlockArgs {
   int ng;                 // entries per panel row block (N_Gamma)
   const double4* lag;     // (s, ln s, 1/s) per time-node pair
   int ldlag;              // n_steps + 1
-  int qfar;               // near-cell Gauss order for well-separated pairs
   int sym;                // symmetric packed spatial blocks (only tiles ti <= tj are written)
   int nt;                 // sym: tiles per block side
   long long blk;          // sym: stored doubles per (a,b) block
@@ -108,10 +107,11 @@ __host__ __device__ inline double seg_dist(const Seg& X, const Seg& Y) {
   return fmin(fmin(pd(X.ax, X.ay, Y), pd(X.bx, X.by, Y)), fmin(pd(Y.ax, Y.ay, X), pd(Y.bx, Y.by, X)));
 }
 // Gauss order for non-touching pairs in cells d <= 1 (measured table)
-// qfar: order for well-separated pairs (rho >= 9), min(6, q_bulk + 1) from the mesh's kappa
-__host__ __device__ inline int near_order(const Seg& X, const Seg& Y, int qfar) {
+// qfar: order for well-separated pairs (rho >= gap; bem_quad_opts q_near, default min(6, q_far + 1)),
+// gap: bem_quad_opts near_gap (default 9)
+__host__ __device__ inline int near_order(const Seg& X, const Seg& Y, int qfar, double gap) {
   double rho = seg_dist(X, Y) / fmax(X.h, Y.h);
-  return rho < 2.5 ? 10 : (rho < 5.0 ? 8 : (rho < 9.0 ? 6 : qfar));
+  return rho < fmin(2.5, gap) ? 10 : (rho < fmin(5.0, gap) ? 8 : (rho < gap ? 6 : qfar));
 }
 // relation of elements p, q of a closed chain of n: 0 disjoint, 1 identical,
 // 2 X.end == Y.start, 3 X.start == Y.end
@@ -294,14 +294,12 @@ __global__ void __launch_bounds__(128) k_sing(BlockArgs B, const Seg* __restrict
 }
 
 // ================================================================= launch
-// which: 0 bulk (DMMA k_bulk_t with the basis table bas, or the DFMA k_bulk_m when bas is null),
-// 1 near cells
+// which: 0 bulk cells (k_bulk_m), 1 near cells (k_near_m)
 template <int KIND, bool PROD = false>
 static void launch_kind(int which, const BlockArgs& BA, const MomArgs& M, int ng, int nband_or_chunk,
-                        int nz, cudaStream_t st, const double* bas = nullptr) {
+                        int nz, cudaStream_t st) {
   dim3 grid((ng + 31) / 32, (ng + 3) / 4, nz);
-  if (which == 0 && bas) k_bulk_t<KIND, PROD><<<grid, 128, 0, st>>>(BA, M, bas);
-  else if (which == 0) k_bulk_m<KIND, 8, PROD><<<grid, 128, 0, st>>>(BA, M);
+  if (which == 0) k_bulk_m<KIND, 8, PROD><<<grid, 128, 0, st>>>(BA, M);
   else k_near_m<KIND, PROD><<<grid, 128, 0, st>>>(BA, M, nband_or_chunk);
   count_launch();
 }
@@ -357,11 +355,34 @@ static long long bulk_nodes(const Block& b, int R) {
   return nodes;
 }
 
-bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bulk, int q_sing,
-                           int flags, cudaStream_t st, const double* prod_g, double* prod_y) {
+bem_status resolve_quad(int kind, const bem_mesh* m, const bem_quad_opts* o, const char* where, QuadCfg* out) {
+  QuadCfg q;
+  q.q_far = (o && o->q_far > 0) ? o->q_far : (kind == STB_D ? m->q_bulk_d : m->q_bulk);
+  q.q_near = (o && o->q_near > 0) ? o->q_near : std::min(6, q.q_far + 1);
+  q.near_gap = (o && o->near_gap > 0) ? (double)o->near_gap : 9.0;
+  q.q_sing = (o && o->q_sing > 0) ? o->q_sing : 16;
+  q.flags = o ? o->flags : 0;
+  if (o && (o->q_far < 0 || o->q_near < 0 || o->near_gap < 0 || o->q_sing < 0)) {
+    set_error(std::string(where) + ": negative quadrature option");
+    return BEM_E_INVALID;
+  }
+  if (q.q_far < 3 || q.q_far > 8 || q.q_far == 7) { set_error(std::string(where) + ": q_far must be one of 3,4,5,6,8"); return BEM_E_INVALID; }
+  if (q.q_near < 3 || q.q_near > QMAX) { set_error(std::string(where) + ": q_near must be in [3,16]"); return BEM_E_INVALID; }
+  if (q.q_sing < 4 || q.q_sing > QSING_MAX) { set_error(std::string(where) + ": q_sing must be in [4,16]"); return BEM_E_INVALID; }
+  if (q.flags & ~(BEM_QUAD_LEGACY_SING | BEM_QUAD_FULL_STORAGE)) { set_error(std::string(where) + ": unknown flags"); return BEM_E_INVALID; }
+  *out = q;
+  return BEM_OK;
+}
+
+bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, const QuadCfg& qc,
+                           cudaStream_t st, const double* prod_g, double* prod_y) {
+  const int q_bulk = qc.q_far, q_sing = qc.q_sing, flags = qc.flags;
   const int ng = m->ng;
   const bool prod = prod_g != nullptr;
   if (prod && kind != STB_K) { set_error("assemble: product mode is K_h only"); return BEM_E_INVALID; }
+  // the touching-pair enumeration (offsets J = I + jo - 2) needs distinct neighbours: below six
+  // elements two offsets name the same pair and its contribution would be counted twice
+  if (ng < 6) { set_error("assemble: N_Gamma >= 6 required"); return BEM_E_INVALID; }
   mesh_wait(m, st);
   long long* d_poff = nullptr;
   cudaError_t e = cudaMallocAsync((void**)&d_poff, sizeof(long long) * std::max<size_t>(1, A->poff.size()), st);
@@ -420,8 +441,9 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bul
   A->q_bulk = q_bulk;
   A->q_sing = q_sing;
   A->launches = 0;
-  const int qfar = std::min(6, q_bulk + 1);
+  const int qfar = qc.q_near;
   MomArgs MB{d_rec, npairs, m->d_seg, m->d_half, m->d_dual, m->alpha, ng, q_bulk, qfar, d_ctr};
+  MB.near_gap = qc.near_gap;
   MB.ell = m->htmin > 0.0 ? std::sqrt(4.0 * m->htmin / m->alpha) : 0.0;
   MomArgs MN = MB;
   MN.rec = d_rec + (long long)nf * npairs;
@@ -440,26 +462,6 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bul
   MS.rec = d_rec + (long long)nf * npairs + (long long)nfn * npairs;
   MS.npairs = nsrec;
   MS.counters = d_ctr + 10;
-  // opt-in DMMA bulk kernel (BEM_QUAD_BULK_MMA or env BEM_BULK_MMA for the probes) and its basis
-  // table: (n_steps + 1)^2 nodes x 4 KS doubles
-  static const bool env_mma = getenv("BEM_BULK_MMA") != nullptr;
-  const bool use_mma = (flags & BEM_QUAD_BULK_MMA) || env_mma;
-  double* d_bas = nullptr;
-  const long long nnode = (long long)(m->nt + 1) * (m->nt + 1);
-  const size_t bas_bytes = use_mma ? sizeof(double) * nnode * 4 * (kind == STB_D ? BasisK<STB_D>::KS : BasisK<STB_V>::KS) : 0;
-  if (use_mma) {
-    if ((e = storage_acquire(m->device, bas_bytes, st, (void**)&d_bas)) != cudaSuccess) {
-      storage_release(m->device, d_rec, rec_bytes, st);
-      cudaFreeAsync(d_poff, st);
-      return cuda_fail(e, "assemble/basis");
-    }
-    const unsigned nb = (unsigned)((nnode + 255) / 256);
-    if (kind == STB_V) k_basis<STB_V><<<nb, 256, 0, st>>>(m->d_lag, m->nt + 1, d_bas);
-    else if (kind == STB_K) k_basis<STB_K><<<nb, 256, 0, st>>>(m->d_lag, m->nt + 1, d_bas);
-    else k_basis<STB_D><<<nb, 256, 0, st>>>(m->d_lag, m->nt + 1, d_bas);
-    count_launch();
-    A->launches++;
-  }
   mark();
   if (kind == STB_V) launch_records<STB_V>(MB, MN, fused_sing ? &MS : nullptr, q_sing, st);
   else if (kind == STB_K) launch_records<STB_K>(MB, MN, fused_sing ? &MS : nullptr, q_sing, st);
@@ -482,7 +484,6 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bul
     BA.ng = ng;
     BA.lag = m->d_lag;
     BA.ldlag = m->nt + 1;
-    BA.qfar = qfar;
     BA.sym = A->sym;
     BA.nt = sym_nt(ng);
     BA.blk = A->blk_elems;
@@ -492,13 +493,13 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bul
     BA.pslots = pslots;
     BA.ntile = ntile;
     BA.ell = MB.ell;
-    const int R = use_mma ? 7 : 8;    // test steps per band (k_bulk_t: 8 nodes = one DMMA N tile)
+    const int R = 8;                  // test steps per band of k_bulk_m
     const int nband = (blk.a1 - blk.a0 + R - 1) / R;
     if (blk.a1 - 1 - blk.b0 >= 2) {
-      if (prod) launch_kind<STB_K, true>(0, BA, MB, ng, nband, nband, st, d_bas);
-      else if (kind == STB_V) launch_kind<STB_V>(0, BA, MB, ng, nband, nband, st, d_bas);
-      else if (kind == STB_K) launch_kind<STB_K>(0, BA, MB, ng, nband, nband, st, d_bas);
-      else launch_kind<STB_D>(0, BA, MB, ng, nband, nband, st, d_bas);
+      if (prod) launch_kind<STB_K, true>(0, BA, MB, ng, nband, nband, st);
+      else if (kind == STB_V) launch_kind<STB_V>(0, BA, MB, ng, nband, nband, st);
+      else if (kind == STB_K) launch_kind<STB_K>(0, BA, MB, ng, nband, nband, st);
+      else launch_kind<STB_D>(0, BA, MB, ng, nband, nband, st);
       mark();
       fam.push_back(0);
       A->launches++;
@@ -560,7 +561,6 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bul
     storage_release(m->device, d_part, part_bytes, st);
   }
   storage_release(m->device, d_rec, rec_bytes, st);
-  if (d_bas) storage_release(m->device, d_bas, bas_bytes, st);
   cudaFreeAsync(d_poff, st);
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "assemble/launch");

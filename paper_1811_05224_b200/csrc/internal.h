@@ -191,10 +191,20 @@ inline bool touching_records_ok(int kind, const bem_mesh* m, int flags) {
   const double hpair = (kind == STB_D ? 1.0 : 2.0) * m->hmax;
   return !(flags & BEM_QUAD_LEGACY_SING) && 0.25 * m->alpha * hpair * hpair / m->htmin < 0.99 * 4.0;
 }
+// resolved quadrature options (bem_quad_opts with the defaults applied)
+struct QuadCfg {
+  int q_far;        // Gauss order of the bulk time cells d >= 2
+  int q_near;       // near cells (d <= 1): order of the pairs at distance ratio >= near_gap
+  double near_gap;  // near cells: distance ratio below which the measured orders 10 / 8 / 6 apply
+  int q_sing;       // touching pairs: singular rules
+  int flags;
+};
+// defaults and validation of bem_quad_opts for matrix kind `kind` (BEM_E_INVALID with a message)
+bem_status resolve_quad(int kind, const bem_mesh* m, const bem_quad_opts* o, const char* where, QuadCfg* out);
 // prod_g != nullptr: product mode (K_h only): prod_y = K_h prod_g over the owned blocks, K_h is
 // not stored (A carries statistics only)
-bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, int q_bulk, int q_sing,
-                           int flags, cudaStream_t st, const double* prod_g = nullptr,
+bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, const QuadCfg& qc,
+                           cudaStream_t st, const double* prod_g = nullptr,
                            double* prod_y = nullptr);
 // linear algebra (linalg.cu)
 bem_status gemv_setup(bem_matrix* A);

@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(SYMV_WARPS * 32) k_gemv_sym(const double* __re
     for (int k = threadIdx.x; k < SYMV_WARPS * L; k += blockDim.x) ys[k] = 0.0;
     __syncthreads();
     int ti = 0, tj = w;                                // tile t = w in row-major upper order
-    while (tj >= nt) { tj -= nt - ti - 1; ++ti; }
+    while (tj >= nt && ti < nt) { tj -= nt - ti - 1; ++ti; }   // w >= ntp: ti reaches nt, no tile
     for (int t = w; t < ntp; t += SYMV_WARPS) {
       const double* __restrict__ tp = blkp + (long long)t * (SYM_TS * SYM_TS);
       const bool cok = tj * SYM_TS + lane < ng;
@@ -360,17 +360,15 @@ bem_status gemv_launch(const bem_matrix* A, double a, const double* x, double b,
 // peak on B200 (37.1 vs 34.1 TFLOP/s, profiles/r01_fp64_peak.txt, r01_dmma_peak.txt) but one
 // DMMA does 256 FMAs per warp from 2 operand registers per lane, so the tile loop is no longer
 // bound by shared-memory operand loads and issue slots as the 8 x 8 DFMA register tile was.
-// row stride 18 doubles (144 B): the 16-byte fragment loads of a quarter warp hit 8 distinct bank quads
 // a tiles of 64 columns: the lags d > a of a tile's last lag chunk (the triangle, computed on
-// zero-filled x) cost TA^2 / 2 per tile, 1/5 of the C4 products at TA = 128, 1/9 at 64;
-// 8 warps as 4 (i) x 2 (a), each 32 x 32 = 4 x 4 DMMA accumulators
+// zero-filled x) cost TA^2 / 2 per tile, 1/5 of the C4 products at TA = 128, 1/9 at 64.
+// 8 warps as 4 (i) x 2 (a), warp tile 32 x 32 = 4 x 4 DMMA tiles, 32 accumulators per lane.
+// Shared tiles row-major [i or a][k] with row stride 18 doubles (144 B): the 16-byte fragment loads
+// of a quarter warp hit 8 distinct bank quads.  Global -> shared by cp.async (zero-filled outside
+// the matrix) in a 3-stage pipeline: the tiles of the next two K steps are in flight while the
+// current one is multiplied.
 constexpr int TZ_TI = 128, TZ_TA = 64, TZ_TK = 16, TZ_LDK = TZ_TK + 2, TZ_STAGES = 3, TZ_UI = 4, TZ_VA = 4;
 constexpr size_t TZ_SMEM = sizeof(double) * TZ_STAGES * (TZ_TI + TZ_TA) * TZ_LDK;
-// 8 warps as 2 (i) x 4 (a), warp tile 64 i x 32 a = 8 x 4 DMMA tiles, 64 accumulators per lane.
-// Shared tiles row-major [i or a][k] with row stride 20 doubles: the fragment loads (lane -> k =
-// lane % 4, m / n = lane / 4) hit 16 distinct 8-byte bank pairs per half warp.  Global -> shared
-// by cp.async (zero-filled outside the matrix) in a 3-stage pipeline: the tiles of the next two
-// K steps are in flight while the current one is multiplied.
 __device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(d[0]), "+d"(d[1]) : "d"(a), "d"(b));
@@ -650,22 +648,28 @@ __global__ void k_cyclic_factor(const double* __restrict__ lo, const double* __r
   F[4 * ng + 1] = 1.0 + zz[0] + (alpha_c / gam) * zz[ng - 1];
 }
 
+// staged: x and the factors in shared memory (4 ng doubles); otherwise (N_Gamma beyond the
+// shared-memory limit) the recurrences run on y and the factors in global memory
 __global__ void __launch_bounds__(32) k_cyclic_solve(const double* __restrict__ fac, int ng, int nt,
-                                                    int transpose, const double* __restrict__ x,
-                                                    double* __restrict__ y) {
+                                                    int transpose, int staged, const double* x,
+                                                    double* y) {
   extern __shared__ double sm[];   // x / yy, sl, inv, cp  (4 ng)
   const int a = blockIdx.x, lane = threadIdx.x;
   const long long base = (long long)a * ng;
   const double* F = fac + ((long long)transpose * nt + a) * (4LL * ng + 2);
-  double* yy = sm;
-  double* sl = sm + ng;
-  double* inv = sm + 2 * ng;
-  double* cp = sm + 3 * ng;
-  for (int l = lane; l < ng; l += 32) {
-    yy[l] = x[base + l];
-    sl[l] = F[l];
-    inv[l] = F[ng + l];
-    cp[l] = F[2 * ng + l];
+  double* yy = staged ? sm : y + base;
+  const double* sl = staged ? sm + ng : F;
+  const double* inv = staged ? sm + 2 * ng : F + ng;
+  const double* cp = staged ? sm + 3 * ng : F + 2 * ng;
+  if (staged) {
+    for (int l = lane; l < ng; l += 32) {
+      yy[l] = x[base + l];
+      sm[ng + l] = F[l];
+      sm[2 * ng + l] = F[ng + l];
+      sm[3 * ng + l] = F[2 * ng + l];
+    }
+  } else if (x != y) {
+    for (int l = lane; l < ng; l += 32) yy[l] = x[base + l];
   }
   __syncwarp();
   if (lane == 0) {
@@ -682,6 +686,7 @@ __global__ void __launch_bounds__(32) k_cyclic_solve(const double* __restrict__ 
   }
   __syncwarp();
   const double fact = (yy[0] + F[4 * ng] * yy[ng - 1]) / F[4 * ng + 1];
+  __syncwarp();
   for (int l = lane; l < ng; l += 32) y[base + l] = yy[l] - fact * F[3 * ng + l];
 }
 
@@ -698,7 +703,17 @@ bem_status mass_solve(const bem_matrix* M, int transpose, const double* x, doubl
   if (M->mass_kind == BEM_MASS_DUAL_LUMPED) {
     k_diag_solve<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(M->d_di, n, x, y);
   } else {
-    k_cyclic_solve<<<m->nt, 32, sizeof(double) * 4 * m->ng, st>>>(M->d_work, m->ng, m->nt, transpose ? 1 : 0, x, y);
+    // shared staging up to the opt-in limit (N_Gamma <= 7264 at 227 KB), global memory beyond
+    static int smem_max = -1;
+    if (smem_max < 0) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      if (cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) smem_max = 48 * 1024;
+      cudaFuncSetAttribute(k_cyclic_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
+    }
+    const size_t smem = sizeof(double) * 4 * (size_t)m->ng;
+    const int staged = smem <= (size_t)smem_max;
+    k_cyclic_solve<<<m->nt, 32, staged ? smem : 0, st>>>(M->d_work, m->ng, m->nt, transpose ? 1 : 0, staged, x, y);
   }
   count_launch();
   cudaError_t e = cudaGetLastError();

@@ -411,6 +411,10 @@ bem_status bem_mesh_info_get(const bem_mesh* m, bem_mesh_info* info) {
   info->entries_total = (long long)m->ng * m->ng * m->nt * (m->nt + 1) / 2;
   info->q_bulk = m->q_bulk;
   info->kappa = m->kappa;
+  info->rank = m->rank;
+  info->nranks = m->nranks;
+  info->local_rows = (long long)m->ng * m->nt;   // replicated vectors (R27)
+  info->local_row0 = 0;
   return BEM_OK;
 }
 

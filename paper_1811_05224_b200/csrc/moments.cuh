@@ -89,6 +89,7 @@ struct MomArgs {
   double ell;             // sqrt(4 min h_t / alpha): the length on which U* varies at the
                           // smallest lag; sub-pairs closer than 8 ell get composite rules with
                           // cells of at most ell (no subdivision while kappa <= 1)
+  double near_gap;        // near records: distance ratio below which the measured orders apply
 };
 
 // composite subdivision of a sub-pair: cells per direction.  R24: pairs
@@ -148,7 +149,7 @@ __device__ __forceinline__ void for_subpairs(const MomArgs& M, int I, int J, Fn&
     sp.pi = I;
     sp.qi = J;
     sp.nchain = ng;
-    sp.q = NEAR ? near_order(sp.X, sp.Y, M.qfar) : M.q;
+    sp.q = NEAR ? near_order(sp.X, sp.Y, M.qfar, M.near_gap) : M.q;
     sp.ns = composite_cells<NEAR>(sp.X, sp.Y, M.ell);
     sp.sa = sp.X.h * sp.Y.h / (4.0 * STB_PI);
     sp.sb = 0.0;
@@ -164,7 +165,7 @@ __device__ __forceinline__ void for_subpairs(const MomArgs& M, int I, int J, Fn&
       sp.nchain = ng;
       if (collinear(sp.X, sp.Y)) continue;
       if (NEAR && chain_rel(I, j, ng)) continue;
-      sp.q = NEAR ? near_order(sp.X, sp.Y, M.qfar) : M.q;
+      sp.q = NEAR ? near_order(sp.X, sp.Y, M.qfar, M.near_gap) : M.q;
       sp.ns = composite_cells<NEAR>(sp.X, sp.Y, M.ell);
       sp.side = side;
       sp.sa = M.alpha / (8.0 * STB_PI) * sp.X.h * sp.Y.h;
@@ -189,7 +190,7 @@ __device__ __forceinline__ void for_subpairs(const MomArgs& M, int I, int J, Fn&
         sp.pi = p;
         sp.qi = qh;
         sp.nchain = nh;
-        sp.q = NEAR ? near_order(sp.X, sp.Y, M.qfar) : M.q;
+        sp.q = NEAR ? near_order(sp.X, sp.Y, M.qfar, M.near_gap) : M.q;
         sp.ns = composite_cells<NEAR>(sp.X, sp.Y, M.ell);
         const double dvk = n < 2 ? 1.0 / dk.Lm : -1.0 / dk.Lp;
         sp.k0 = n == 0 ? 0.0 : (n == 1 ? dk.vm : (n == 2 ? 1.0 : dk.vp));
@@ -1009,271 +1010,6 @@ __global__ void __launch_bounds__(128, (KIND == STB_D || PROD) ? 2 : 3) k_bulk_m
             if (valid && a < r_hi && a - b >= 2) col[srow[r - 1]] = Gp[r - 1] - G;
             Gp[r - 1] = G;
           }
-        }
-      }
-    } else {
-#pragma unroll
-      for (int r = 1; r <= R; ++r) Gp[r - 1] = phi[r] - phi[r - 1];
-    }
-  }
-  if (PROD) {
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const double sum = warp_sum(accp[r]);
-      const int a = r_lo + r;
-      if (lane == 0 && a < r_hi && I0 < ng)
-        B.part[B.pbase + ((long long)(a - B.a0) * ng + I) * B.pslots + blockIdx.x] = sum;
-    }
-  }
-  if (!valid) nA = nB = nZ = nC = nK = 0;
-  count_regimes(M.counters, nA, nB, nZ, nC, nK);
-}
-
-// ------------------------------------------------------------- bulk cells on the FP64 tensor cores
-// Regime A node values are a contraction: Phi~(pair, node) = sum_k C[pair][k] Bas[k][node] with
-// the pair's coefficients C (premultiplied moments, the ln s / s terms of RegA) and the node's
-// basis Bas = (u^0 .. u^(NU-1), s, s ln s, ln s) (V: NU = 17, K: 18 + ln s, D: 18 + 3; padded to
-// 4 KS columns).  k_bulk_t evaluates it with DMMA m8n8k4 (M = 8 pairs, N = 8 nodes, K = 4 basis
-// terms): warp = test element I, 32 trial elements J as 4 M tiles; band of R = 7 test steps whose
-// 8 nodes x = r_lo .. r_lo + 7 at trial node y form the N tile.  The accumulator tile is
-// transposed through shared memory so that lane j continues with the 8 node values of its own pair
-// (I, Jb + j) exactly as k_bulk_m does (regime fix-ups with the lane's RegBZ, differences, stores).  DMMA and DFMA share the FP64 units
-// on B200 (profiles/r01_dmma_peak.txt: both at once 32.3 TFLOP/s, DMMA alone 37.1, DFMA alone
-// 34.1), so the contraction costs the same pipe time as the Horner chains (K = 20 vs 17-18
-// terms) but 8x fewer issued instructions: the regime fix-ups, second differences and stores run
-// beside it.  Lane (g = lane / 4, q = lane % 4) holds A[pair 8 mt + g][k = 4 ks + q] (its pairs'
-// coefficients, loaded once), B[k = 4 ks + q][node g] per trial node, and D[pair 8 mt + g][nodes
-// 2q, 2q+1].
-template <int KIND> struct BasisK;
-template <> struct BasisK<STB_V> { static constexpr int KS = 5, NU = 17; };
-template <> struct BasisK<STB_K> { static constexpr int KS = 5, NU = 18; };
-template <> struct BasisK<STB_D> { static constexpr int KS = 6, NU = 18; };
-
-// basis rows per node (x, y), zero for x <= y
-template <int KIND>
-__global__ void k_basis(const double4* __restrict__ lag, int ld, double* __restrict__ bas) {
-  constexpr int KB = 4 * BasisK<KIND>::KS, NU = BasisK<KIND>::NU;
-  const long long node = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (node >= (long long)ld * ld) return;
-  const double4 q = lag[node];
-  double* out = bas + node * KB;
-  const bool ok = q.x > 0.0;
-  double p = 1.0;
-  for (int k = 0; k < NU; ++k) {
-    out[k] = ok ? p : 0.0;
-    p *= q.z;
-  }
-  if (KIND == STB_K) {
-    out[NU] = ok ? q.y : 0.0;
-    for (int k = NU + 1; k < KB; ++k) out[k] = 0.0;
-  } else {
-    out[NU] = ok ? q.x : 0.0;
-    out[NU + 1] = ok ? q.x * q.y : 0.0;
-    out[NU + 2] = ok ? q.y : 0.0;
-    for (int k = NU + 3; k < KB; ++k) out[k] = 0.0;
-  }
-}
-
-// coefficient k (basis order) of the pair at rec (= M.rec + pair)
-template <int KIND>
-__device__ __forceinline__ double basis_coef(const double* __restrict__ rec, long long S, int k) {
-  constexpr int NU = BasisK<KIND>::NU;
-  const double* R0 = rec + (RF_COMMON + 0 * FAMSZ) * S;
-  if (KIND == STB_V) {
-    if (k < NU) return R0[(FA + k + 1) * S];
-    if (k == NU) return R0[FA * S];
-    if (k == NU + 1) return R0[FM0 * S];
-    if (k == NU + 2) return R0[FM1 * S];
-    return 0.0;
-  } else if (KIND == STB_K) {
-    if (k < NU) return R0[(FA + k) * S];
-    if (k == NU) return -R0[FM0 * S];
-    return 0.0;
-  } else {
-    const double* R1 = rec + (RF_COMMON + 1 * FAMSZ) * S;
-    if (k < NU) return (k < MKA ? R0[(FA + k + 1) * S] : 0.0) + R1[(FA + k) * S];
-    if (k == NU) return R0[FA * S];
-    if (k == NU + 1) return R0[FM0 * S];
-    if (k == NU + 2) return R0[FM1 * S] + R1[FM0 * S];
-    return 0.0;
-  }
-}
-
-__device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-               : "+d"(d[0]), "+d"(d[1]) : "d"(a), "d"(b));
-}
-
-template <int KIND, bool PROD = false>
-__global__ void __launch_bounds__(128, 3) k_bulk_t(BlockArgs B, MomArgs M, const double* __restrict__ bas) {
-  constexpr int R = 7, KS = BasisK<KIND>::KS, KB = 4 * KS;
-  const int ng = B.ng;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, q = lane & 3, g = lane >> 2;
-  const int I0 = blockIdx.y * 4 + warp, Jb = blockIdx.x * 32;
-  const int J0 = Jb + lane;
-  const bool valid = I0 < ng && J0 < ng;
-  const int I = min(I0, ng - 1), J = min(J0, ng - 1);
-  const int band = blockIdx.z;
-  const int r_hi = B.a1 - R * band;
-  const int r_lo = max(B.a0, r_hi - R);
-  if (r_hi <= r_lo) return;                       // CTA-uniform
-  const int bmax = min(B.b1 - 1, r_hi - 1 - 2);
-  if (bmax < B.b0) return;                        // CTA-uniform
-  const int ti = (blockIdx.y * 4) / SYM_TS, tj = blockIdx.x;
-  if (B.sym && ti > tj) return;                   // CTA-uniform
-  const long long S = M.npairs;
-  const long long pair = (long long)I * ng + J;
-  __shared__ long long s_row[4][R];
-  __shared__ double s_tr[4][32 * 9];              // per warp: node values [pair][node], row stride 9
-  long long* srow = s_row[warp];
-  double* tr = s_tr[warp];
-  if (!PROD && lane < R) {
-    const int a = min(r_lo + lane, r_hi - 1);
-    srow[lane] = B.poff[a - B.a0] + (B.sym ? sym_tile_index(ti, tj, B.nt) * (SYM_TS * SYM_TS) + (long long)(I % SYM_TS) * SYM_TS
-                                           : (long long)I * pad4((long long)panel_nb(a, B.b0, B.b1) * ng));
-  }
-  __syncwarp();
-  const long long cstride = B.sym ? B.blk : (long long)ng;
-  const int jcol = B.sym ? J % SYM_TS : J;
-  // A fragments: coefficient k = 4 ks + q of the pairs (I, Jb + 8 mt + g)
-  double af[4][KS];
-#pragma unroll
-  for (int mt = 0; mt < 4; ++mt) {
-    const double* rec = M.rec + (long long)I * ng + min(Jb + 8 * mt + g, ng - 1);
-#pragma unroll
-    for (int ks = 0; ks < KS; ++ks) af[mt][ks] = basis_coef<KIND>(rec, S, 4 * ks + q);
-  }
-  // this lane's own pair (I, J): regime constants
-  const double cmax = M.rec[RF_CMAX * S + pair];
-  bool nonzero = cmax != 0.0;
-#pragma unroll
-  for (int mt = 0; mt < 4; ++mt)
-#pragma unroll
-    for (int ks = 0; ks < KS; ++ks) nonzero |= af[mt][ks] != 0.0;
-  if (!__any_sync(0xffffffffu, nonzero)) {        // K_h collinear elements: zeros, no node work
-    unsigned long long nz = 0;
-    for (int y = B.b0; y <= bmax + 1; ++y) {
-#pragma unroll
-      for (int r = 0; r <= R; ++r) nz += (r_lo + r <= r_hi && r_lo + r > y);
-      if (!PROD && y > B.b0) {
-        const int b = y - 1;
-        double* col = B.out + ((long long)(b - B.b0) * cstride + jcol);
-#pragma unroll
-        for (int r = 1; r <= R; ++r) {
-          const int a = r_lo + r - 1;
-          if (valid && a < r_hi && a - b >= 2) col[srow[r - 1]] = 0.0;
-        }
-      }
-    }
-    count_regimes(M.counters, valid ? nz : 0, 0, 0, 0, 0);
-    return;
-  }
-  RegBZ<KIND> Z;
-  Z.load(M.rec + pair, S);
-  unsigned long long nA = 0, nB = 0, nZ = 0, nC = 0, nK = 0;
-  double accp[R], Gp[R];
-#pragma unroll
-  for (int r = 0; r < R; ++r) accp[r] = Gp[r] = 0.0;
-  const int xg = min(r_lo + g, r_hi);             // B-fragment node row of this lane
-  for (int y = B.b0; y <= bmax + 1; ++y) {
-    const double* bp = bas + ((long long)xg * B.ldlag + y) * KB + q;
-    double bf[KS];
-#pragma unroll
-    for (int ks = 0; ks < KS; ++ks) bf[ks] = bp[4 * ks];
-    double d[4][2];
-#pragma unroll
-    for (int mt = 0; mt < 4; ++mt) d[mt][0] = d[mt][1] = 0.0;
-#pragma unroll
-    for (int ks = 0; ks < KS; ++ks)
-#pragma unroll
-      for (int mt = 0; mt < 4; ++mt) dmma884(d[mt], af[mt][ks], bf[ks]);
-    // transpose through shared memory: lane j takes the 8 node values of its own pair j
-#pragma unroll
-    for (int mt = 0; mt < 4; ++mt) {
-      tr[(8 * mt + g) * 9 + 2 * q] = d[mt][0];
-      tr[(8 * mt + g) * 9 + 2 * q + 1] = d[mt][1];
-    }
-    __syncwarp();
-    double phi[R + 1];
-    unsigned bmask = 0;
-#pragma unroll
-    for (int r = 0; r <= R; ++r) {
-      const int x = r_lo + r;
-      const bool ok = x <= r_hi && x > y;
-      const double u = B.lag[min(x, r_hi) * B.ldlag + y].z;
-      const bool inA = cmax * u < STB_MXA;
-      phi[r] = ok ? tr[lane * 9 + r] : 0.0;
-      nA += ok && inA;
-      if (ok && !inA) bmask |= 1u << r;
-    }
-    __syncwarp();
-    if (__any_sync(0xffffffffu, bmask != 0)) {
-      unsigned cmask = 0;
-      while (bmask) {
-        const int r = __ffs(bmask) - 1;
-        bmask &= bmask - 1;
-        const double4 qd = B.lag[(r_lo + r) * B.ldlag + y];
-        int reg = 0, reg2 = 0;
-        double v = 0.0, v2 = 0.0;
-        int r2 = -1;
-        if (bmask) {
-          r2 = __ffs(bmask) - 1;
-          bmask &= bmask - 1;
-          const double4 q2 = B.lag[(r_lo + r2) * B.ldlag + y];
-          phi_bz2<KIND>(M.rec + pair, S, Z, qd.x, qd.z, q2.x, q2.z, v, v2, &reg, &reg2);
-        } else {
-          v = phi_bz<KIND>(M.rec + pair, S, Z, qd.x, qd.z, &reg);
-        }
-        nB += (reg == 1) + (reg2 == 1);
-        nK += (reg == 1 ? Z.kb : 0) + (reg2 == 1 ? Z.kb : 0);
-        nZ += (reg == 2) + (reg2 == 2);
-        if (reg == 3) { cmask |= 1u << r; ++nC; }
-        if (reg2 == 3) { cmask |= 1u << r2; ++nC; }
-#pragma unroll
-        for (int rr = 0; rr <= R; ++rr) {
-          if (rr == r) phi[rr] = v;
-          if (rr == r2) phi[rr] = v2;
-        }
-      }
-      unsigned lanes = __ballot_sync(0xffffffffu, cmask != 0);
-      while (lanes) {                             // warp-uniform
-        const int src = __ffs(lanes) - 1;
-        lanes &= lanes - 1;
-        unsigned cm = __shfl_sync(0xffffffffu, cmask, src);
-        const int Js = __shfl_sync(0xffffffffu, J, src);
-        while (cm) {
-          const int r = __ffs(cm) - 1;
-          cm &= cm - 1;
-          const double4 qd = B.lag[(r_lo + r) * B.ldlag + y];
-          const double v = phi_c_warp<KIND, false>(M, I, Js, qd.x, qd.y, qd.z);
-          if (lane == src) {
-#pragma unroll
-            for (int rr = 0; rr <= R; ++rr)
-              if (rr == r) phi[rr] = v;
-          }
-        }
-      }
-    }
-    if (y > B.b0) {
-      const int b = y - 1;
-      const bool interior = b <= r_lo - 2 && r_hi - r_lo == R;
-      if (PROD) {
-        const double gv = valid ? B.g[(long long)b * ng + J] : 0.0;
-#pragma unroll
-        for (int r = 1; r <= R; ++r) {
-          const int a = r_lo + r - 1;
-          const double G = phi[r] - phi[r - 1];
-          if (interior || (a < r_hi && a - b >= 2)) accp[r - 1] = fma(Gp[r - 1] - G, gv, accp[r - 1]);
-          Gp[r - 1] = G;
-        }
-      } else {
-        double* col = B.out + ((long long)(b - B.b0) * cstride + jcol);
-#pragma unroll
-        for (int r = 1; r <= R; ++r) {
-          const int a = r_lo + r - 1;
-          const double G = phi[r] - phi[r - 1];
-          if (valid && (interior || (a < r_hi && a - b >= 2))) col[srow[r - 1]] = Gp[r - 1] - G;
-          Gp[r - 1] = G;
         }
       }
     } else {

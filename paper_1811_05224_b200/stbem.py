@@ -35,11 +35,18 @@ class MeshInfo(ctypes.Structure):
     _fields_ = [("n_gamma", ctypes.c_int), ("n_steps", ctypes.c_int), ("n", ctypes.c_longlong),
                 ("n_slices", ctypes.c_int), ("n_owned_blocks", ctypes.c_int),
                 ("entries_owned", ctypes.c_longlong), ("entries_total", ctypes.c_longlong),
-                ("q_bulk", ctypes.c_int), ("kappa", ctypes.c_double)]
+                ("q_bulk", ctypes.c_int), ("kappa", ctypes.c_double), ("rank", ctypes.c_int),
+                ("nranks", ctypes.c_int), ("local_rows", ctypes.c_longlong), ("local_row0", ctypes.c_longlong)]
 
 
 class QuadOpts(ctypes.Structure):
-    _fields_ = [("q_bulk", ctypes.c_int), ("q_sing", ctypes.c_int), ("flags", ctypes.c_int)]
+    _fields_ = [("q_far", ctypes.c_int), ("q_near", ctypes.c_int), ("near_gap", ctypes.c_int),
+                ("q_sing", ctypes.c_int), ("flags", ctypes.c_int)]
+
+
+def quad_opts(q_bulk=0, q_sing=0, flags=0, q_near=0, near_gap=0):
+    """bem_quad_opts; q_bulk is the order of the bulk time cells (the struct's q_far)"""
+    return QuadOpts(int(q_bulk), int(q_near), int(near_gap), int(q_sing), int(flags))
 
 
 class GmresOpts(ctypes.Structure):
@@ -59,7 +66,6 @@ class SolveReport(ctypes.Structure):
 
 QUAD_LEGACY_SING = 1   # bem_quad_opts.flags: touching pairs by the per-lag singular kernel
 QUAD_FULL_STORAGE = 2  # bem_quad_opts.flags: V_h / D_h stored full instead of symmetric packed
-QUAD_BULK_MMA = 4      # bem_quad_opts.flags: bulk cells by the DMMA kernel k_bulk_t (opt-in)
 
 
 class AssemblyStats(ctypes.Structure):
@@ -251,9 +257,10 @@ class Mesh:
         except Exception:
             pass
 
-    def _assemble(self, fn, q_bulk=0, q_sing=0, legacy_sing=False, full_storage=False, bulk_mma=False, stream=None):
-        o = QuadOpts(q_bulk, q_sing, (QUAD_LEGACY_SING if legacy_sing else 0) | (QUAD_FULL_STORAGE if full_storage else 0)
-                     | (QUAD_BULK_MMA if bulk_mma else 0))
+    def _assemble(self, fn, q_bulk=0, q_sing=0, legacy_sing=False, full_storage=False, q_near=0, near_gap=0,
+                  stream=None):
+        o = quad_opts(q_bulk, q_sing, (QUAD_LEGACY_SING if legacy_sing else 0) | (QUAD_FULL_STORAGE if full_storage else 0),
+                      q_near, near_gap)
         h = ctypes.c_void_p()
         check(fn(self.h, ctypes.byref(o), _stream(stream), ctypes.byref(h)))
         return Matrix(h, self)
@@ -269,7 +276,7 @@ class Mesh:
 
     def assemble_toeplitz(self, kind, q_bulk=0, q_sing=0, stream=None):
         """block-Toeplitz variant (uniform steps): kind 'V', 'K' or 'D' -> T_d = A(d, 0)"""
-        o = QuadOpts(q_bulk, q_sing, 0)
+        o = quad_opts(q_bulk, q_sing)
         h = ctypes.c_void_p()
         check(lib().bem_assemble_toeplitz(self.h, "VKD".index(kind), ctypes.byref(o), _stream(stream), ctypes.byref(h)))
         return Matrix(h, self)
@@ -339,7 +346,7 @@ def rhs(K, Mp, g, b, stream=None):
 def rhs_fused(mesh, Mp, g, b, q_bulk=0, q_sing=0, legacy_sing=False, stats=False, stream=None):
     """b = 1/2 M g + K g with K_h computed on the fly and never stored (bem_rhs_fused); returns
     the K_h kernel statistics when stats=True (synchronises), else b"""
-    o = QuadOpts(q_bulk, q_sing, QUAD_LEGACY_SING if legacy_sing else 0)
+    o = quad_opts(q_bulk, q_sing, QUAD_LEGACY_SING if legacy_sing else 0)
     st = AssemblyStats() if stats else None
     check(lib().bem_rhs_fused(mesh.h, ctypes.byref(o), Mp.h, _ptr(g), _ptr(b),
                               ctypes.byref(st) if stats else None, _stream(stream)))

@@ -98,23 +98,6 @@ def test_matrix_full_parity(name, kind):
         assert np.all(got[a * ng:(a + 1) * ng, (a + 1) * ng:] == 0.0)
 
 
-@pytest.mark.parametrize("name", ["LT", "C1", "C2"])
-@pytest.mark.parametrize("kind", ["V", "K", "D"])
-def test_bulk_mma_kernel(name, kind):
-    """the opt-in DMMA bulk kernel k_bulk_t (BEM_QUAD_BULK_MMA): oracle parity and agreement with
-    the default DFMA kernel to rounding"""
-    w = W.get(name)
-    m = S.Mesh.from_workload(w)
-    A = getattr(m, f"assemble_{kind}")(bulk_mma=True)
-    B = getattr(m, f"assemble_{kind}")()
-    got, dflt = A.dense(), B.dense()
-    if name != "C2":
-        assert relmax(got, oracle_dense(name, kind)) <= MAT_TOL
-    assert relmax(got, dflt) <= 1e-13
-    st = A.stats()
-    assert sum(st["nodes_bulk"]) > 0
-
-
 def sample_entries(w, rng, n_random=1500, rows_per=6):
     ng, nt = w.n_gamma, w.n_steps
     rows, cols = [], []
@@ -183,8 +166,14 @@ def test_gemv_c3_ragged_rows():
         assert abs(y[r] - row @ x) <= 1e-13 * np.abs(row).sum() * 1.0
 
 
-def test_mass_matrices():
-    w = W.get("C1")
+@pytest.mark.parametrize("name", ["C1", "ratio10", "pentagon", "LT"])
+def test_mass_matrices(name):
+    """primal, dual and lumped mass: products and the (transposed) cyclic
+    solves against the oracle's dense matrices -- on non-uniform boundaries too, where the dual
+    hats' node values v- != 1/2 (ratio10: neighbours of length ratio 10; pentagon and LT: unequal
+    sides, graded steps) and the dual mass is not symmetric"""
+    from workloads.edge import edge_workloads
+    w = edge_workloads()[name] if name in ("ratio10", "pentagon") else W.get(name)
     m = S.Mesh.from_workload(w)
     om = O.OracleMesh(w)
     x = W.random_vector(w.n)
@@ -660,15 +649,19 @@ def test_representation_formula_with_initial_datum_converges():
     assert errs[-1] < 0.25 * errs[0] and all(b < a for a, b in zip(errs, errs[1:])), errs
 
 
-def test_bench_step_configuration_against_golden():
+@pytest.mark.parametrize("name", ["C2", "C3"])
+def test_bench_step_configuration_against_golden(name):
     """the step exactly as bench.py launches it -- V_h and D_h assembled on two side streams while
     K_h g runs fused on the main stream, exact dual-mass preconditioning, solve after both streams
-    are joined -- on C2 against the oracle's golden density"""
-    path = os.path.join(GOLDEN, "C2_oracle_w.npy")
+    are joined -- against the oracle's golden right-hand side and density (C2: dense oracle
+    matrices; C3, N = 65 536: the oracle's first block columns, reading R26), eq. (4)
+    P:81-90 solved to the GMRES tolerance of P:182 (BJ: 1e-10)"""
+    path = os.path.join(GOLDEN, f"{name}_oracle_w.npy")
     if not os.path.exists(path):
-        pytest.skip("tests/golden/C2_oracle_w.npy missing")
+        pytest.skip(f"tests/golden/{name}_oracle_w.npy missing (python -m oracle.gen_golden {name})")
     wd = np.load(path)
-    w = W.get("C2")
+    bd = np.load(os.path.join(GOLDEN, f"{name}_oracle_b.npy"))
+    w = W.get(name)
     m = S.Mesh.from_workload(w)
     side = (torch.cuda.Stream(), torch.cuda.Stream())
     cur = torch.cuda.current_stream()
@@ -685,7 +678,10 @@ def test_bench_step_configuration_against_golden():
     wv = torch.zeros_like(g)
     rep = S.solve_gmres(V, b, wv, D=D, M=Md, precond=2, rel_tol=w.tol, history=False)
     assert rep["status"] == "OK"
+    assert relmax(b.cpu().numpy(), bd) <= MAT_TOL
     assert relmax(wv.cpu().numpy(), wd) <= W_TOL
+    for A in (V, D, Mp, Md):
+        A.close()
 
 
 @pytest.mark.parametrize("name", ["C3", "C5"])
@@ -830,3 +826,60 @@ def test_c4_toeplitz_products_sampled_rows():
         err = float(np.abs(got - ref).max() / np.abs(ref).max())
         print(f"C4 Toeplitz {kind} product sampled rows rel error {err:.3e}")
         assert err <= 1e-11
+
+
+def test_quadrature_options():
+    """bem_quad_opts (include/stbem.h): q_near / near_gap at their defaults reproduce the default
+    assembly bitwise; raised near orders keep oracle parity; invalid values are rejected"""
+    w = W.get("C1")
+    m = S.Mesh.from_workload(w)
+    for kind in "VKD":
+        A0 = getattr(m, f"assemble_{kind}")()
+        A1 = getattr(m, f"assemble_{kind}")(q_near=min(6, m.info.q_bulk + 1), near_gap=9)
+        A2 = getattr(m, f"assemble_{kind}")(q_near=8, near_gap=12)
+        d0, d1, d2 = A0.dense(), A1.dense(), A2.dense()
+        assert np.array_equal(d0, d1)
+        assert relmax(d2, oracle_dense("C1", kind)) <= MAT_TOL
+        assert not np.array_equal(d0, d2)           # the near cells did change order
+    for bad in (dict(q_bulk=7), dict(q_near=2), dict(q_near=17), dict(near_gap=-1), dict(q_sing=3)):
+        with pytest.raises(S.BemError) as e:
+            m.assemble_V(**bad)
+        assert e.value.status == S.BEM_E_INVALID
+
+
+def test_small_boundaries_rejected_everywhere():
+    """the touching-pair enumeration needs N_Gamma >= 6: every assembly entry point says INVALID"""
+    w = W.Workload("tri3", [(0.0, 0.0), (1.0, 0.0), (0.0, 1.0)], [1, 1, 1], W.configs.uniform_times(4), 1.0,
+                   (1.5, 1.5), 1e-10)
+    m = S.Mesh.from_workload(w)
+    g = cuda(np.ones(w.n))
+    b = torch.empty_like(g)
+    Mp = m.assemble_M(S.MASS_PRIMAL)
+    for call in (lambda: m.assemble_V(), lambda: m.assemble_toeplitz("K"), lambda: S.rhs_fused(m, Mp, g, b)):
+        with pytest.raises(S.BemError) as e:
+            call()
+        assert e.value.status == S.BEM_E_INVALID
+
+
+def test_cyclic_solve_beyond_shared_memory():
+    """N_Gamma = 8000 (4 N_Gamma doubles exceed the 227 KB of shared memory per CTA): the dual-mass
+    solves run from global memory and still match a dense solve"""
+    w = W.Workload("big", [(0.0, 0.0), (1.0, 0.0), (1.0, 1.0), (0.0, 1.0)], [1000, 3000, 1000, 3000],
+                   W.configs.uniform_times(2), 1.0, (1.5, 1.5), 1e-10)
+    m = S.Mesh.from_workload(w)
+    M = m.assemble_M(S.MASS_DUAL)
+    x = W.random_vector(w.n)
+    ng = w.n_gamma
+    h = np.concatenate([np.full(1000, 1e-3), np.full(3000, 1.0 / 3000), np.full(1000, 1e-3), np.full(3000, 1.0 / 3000)])
+    hm, hp = np.roll(h, 1), np.roll(h, -1)
+    vm, vp = hm / (hm + h), hp / (h + hp)
+    for a in range(2):
+        ht = 0.5
+        Md = np.diag(ht * h * (2 + vm + vp) / 4)
+        idx = np.arange(ng)
+        Md[idx, (idx - 1) % ng] += ht * hm * vm / 4
+        Md[idx, (idx + 1) % ng] += ht * hp * vp / 4
+        for tr in (False, True):
+            z = M.solve(cuda(x), torch.empty(w.n, dtype=torch.float64, device="cuda"), transpose=tr).cpu().numpy()
+            ref = np.linalg.solve(Md.T if tr else Md, x[a * ng:(a + 1) * ng])
+            assert relmax(z[a * ng:(a + 1) * ng], ref) <= 1e-12

@@ -143,6 +143,32 @@ def test_large_kappa_pair_integrals_brute_force(case):
     assert got == pytest.approx(ref, rel=1e-11, abs=1e-18)
 
 
+# large kappa, far pair (reading R24): pairs farther apart than 8 ell keep the plain Gauss rule
+# (no composite cells; U* at the smallest lag is below e^{-64} of its peak there).  Segments 1 and
+# 4 of alpha_large are sqrt(2)/3 = 9.4 ell apart; every lag d = 0 .. 7, the V, F and K kernels.
+FAR_CASES = [(ker, a) for ker in (0, 1, 2) for a in range(8)]
+
+
+@pytest.mark.parametrize("case", FAR_CASES)
+def test_large_kappa_far_pair_cutoff_brute_force(case):
+    from workloads.edge import edge_workloads
+    w = edge_workloads()["alpha_large"]
+    m = O.OracleMesh(w)
+    ker, a = case
+    p, q = 1, 4
+    ell = np.sqrt(4 * (w.t_breaks[1] - w.t_breaks[0]) / w.alpha)
+    gap = np.hypot(m.seg_a[q][0] - m.seg_b[p][0], m.seg_a[q][1] - m.seg_b[p][1])
+    assert 8 * ell < gap < 10 * ell                  # the pair sits just beyond the cutoff
+    sy = (1, 0) if ker == 2 else (1, 1)
+    X = (tuple(m.seg_a[p]), tuple(m.seg_b[p]))
+    Y = (tuple(m.seg_a[q]), tuple(m.seg_b[q]))
+    ref = float(B.pair(ker, w.alpha, w.t_breaks, a, 0, X, Y, m.seg_n[q], (1, 1), sy, 0))
+    got = m.pair(ker, 0, a, 0, p, q, (1, 1), sy)
+    # scale of the matrix: the identical pair of the same kernel at d = 0 (the max-norm entries)
+    scale = abs(m.pair(ker if ker != 2 else 0, 0, 0, 0, p, p, (1, 1), (1, 1)))
+    assert abs(got - ref) <= 1e-11 * abs(ref) + 1e-14 * scale, (got, ref, scale)
+
+
 # acute corner (about 25 degrees, reading R25): the vertex pair's Duffy integrand and the near
 # cell of the second neighbour across the corner (distance 0.4 h), K kernel, d = 0
 AC_CASES = [
@@ -458,6 +484,35 @@ def test_initial_potential_closed_form_constant_u0():
         assert abs(f[a * om.ng + i] - ref) <= tol * abs(ref), (a, i, f[a * om.ng + i], ref)
 
 
+def test_initial_rhs_closed_form_linear_u0():
+    """u0 = y1 (in S_h^1: the nodal interpolant is exact): (M_0 y1)(x,t) = int_(0,1)^2 U*(x-y,t) y1 dy
+    = m1(x1) P(x2), the first Gaussian moment and the erf integral of the two 1-D factors of U*
+    (variance 2t/alpha), integrated over gamma_i x [t_a, t_{a+1}] by scipy against the
+    oracle's M_h^0 y1: pins the barycentric interpolation of u0 and the apex-split rule with a
+    non-constant u0 (reading R22)"""
+    from scipy import integrate
+    import workloads.table1 as T
+    w = T.table1(3)
+    om = O.OracleMesh(w)
+    nodes, tris = T.triangulation(w)
+    f = om.initial_rhs(nodes, tris, nodes[:, 0].copy(), 8, 6, 16)
+    al = w.alpha
+
+    def m0y1(x, t):
+        sigma = np.sqrt(2 * t / al)
+        _, M1 = _gauss_moments(x[0], sigma)
+        P2, _ = _gauss_moments(x[1], sigma)
+        return M1 * P2
+    # elements 0, 4 start at a corner of Q (graded rules of the step-0 term); elements on the sides
+    # y1 = 0 (0..3) and y1 = 1 (4..7) see u0's extreme values
+    for a, i, tol in [(0, 0, 1e-9), (0, 4, 1e-9), (0, 5, 1e-10), (1, 0, 1e-10), (0, 9, 1e-10), (1, 5, 1e-11),
+                      (3, 2, 1e-11), (5, 9, 1e-11), (12, 12, 1e-11), (15, 6, 1e-11)]:
+        A, Bp, h = om.seg_a[i], om.seg_b[i], om.seg_h[i]
+        ref, _ = integrate.dblquad(lambda s, t: m0y1(A + s * (Bp - A), t) * h, w.t_breaks[a],
+                                   w.t_breaks[a + 1], 0, 1, epsabs=1e-17, epsrel=1e-13)
+        assert abs(f[a * om.ng + i] - ref) <= tol * max(abs(ref), 1e-3 * np.abs(f).max()), (a, i, f[a * om.ng + i], ref)
+
+
 def test_table1_density_converges():
     """the paper's experiment: V_h w = (1/2 M_h + K_h) g - M_h^0 u0 solved by block
     forward substitution; the L2(Sigma) error of w_h against d_n u falls under refinement"""
@@ -528,3 +583,22 @@ def test_matvec_rows_equal_the_dense_products():
     for kind in "VD":
         ref = om.dense(kind) @ x
         assert np.abs(om.matvec_rows(kind, rows, x) - ref[rows]).max() <= 1e-14 * np.abs(ref).max()
+
+
+def test_uniform_grid_block_toeplitz_identity():
+    """DESIGN.md reading R26 (the C3 golden density of oracle/gen_golden.py rests on it): on a
+    uniform grid t_k = k h the four lags of entry (a, b) are (d+1) h, d h, d h, (d-1) h with
+    d = a - b, so A(a, b) = A(a - b, 0); on the dyadic grids of C1-C4 the lags are the same doubles
+    and the oracle's entries agree bitwise -- random entries of C2 against the first block column"""
+    import workloads as W
+    w = W.get("C2")
+    m = O.OracleMesh(w)
+    ng, nt = m.ng, m.nt
+    rng = np.random.default_rng(26)
+    a = rng.integers(0, nt, 400)
+    b = (rng.random(400) * (a + 1)).astype(np.int64)
+    i, j = rng.integers(0, ng, 400), rng.integers(0, ng, 400)
+    for kind in "VKD":
+        full = m.entries(kind, a * ng + i, b * ng + j)
+        first = m.entries(kind, (a - b) * ng + i, j)
+        assert np.array_equal(full, first), kind

@@ -15,7 +15,8 @@ for _ in range(25):
     e0.record(); A.matvec(x, y); e1.record(); torch.cuda.synchronize()
     ts.append(e0.elapsed_time(e1))
 ms = float(np.median(ts[5:]))
-print(f"{name} gemv median {ms:.3f} ms  {8*m.info.entries_total/ms/1e6:.1f} GB/s (algorithmic bytes 8 x entries)")
+nbytes = A.info()["bytes"] + 16 * w.n
+print(f"{name} gemv median {ms:.3f} ms  {nbytes/ms/1e6:.1f} GB/s (bytes read: stored doubles of the packed V_h + 16 N)")
 # pure-read reference: torch sum over a 16 GiB FP64 buffer
 buf = torch.empty(2 * 1024**3, dtype=torch.float64, device="cuda").uniform_()
 for _ in range(3): buf.sum()

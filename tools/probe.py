@@ -20,7 +20,7 @@ for k in kinds:
     nb, nn = st["nodes_bulk"], st["nodes_near"]
     fb = [v / max(1, sum(nb)) for v in nb]
     fn = [v / max(1, sum(nn)) for v in nn]
-    print(f"assemble {k}: {dt:.3f} s  {m.info.entries_total/dt/1e9:.3f} G entries/s | ms rec {st['ms_records']:.2f} "
+    print(f"assemble {k}: {dt:.3f} s  {st['entries']/dt/1e9:.3f} G computed entries/s | ms rec {st['ms_records']:.2f} "
           f"bulk {st['ms_bulk']:.2f} near {st['ms_near']:.2f} sing {st['ms_sing']:.2f} | bulk regimes A/B/Z/C "
           f"{fb[0]:.4f}/{fb[1]:.4f}/{fb[2]:.4f}/{fb[3]:.5f} near {fn[0]:.3f}/{fn[1]:.3f}/{fn[2]:.3f}/{fn[3]:.4f}", flush=True)
 x = torch.tensor(W.random_vector(w.n), device="cuda"); y = torch.empty_like(x)
@@ -31,4 +31,5 @@ e0.record()
 for _ in range(10): A.matvec(x, y)
 e1.record(); torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / 10
-print(f"gemv {ms:.3f} ms  {8*m.info.entries_total/ms/1e6:.1f} GB/s", flush=True)
+nbytes = A.info()["bytes"] + 16 * w.n   # stored doubles (symmetric packed V_h / D_h) + x and y
+print(f"gemv {ms:.3f} ms  {nbytes/ms/1e6:.1f} GB/s (bytes read: stored entries + 16 N)", flush=True)

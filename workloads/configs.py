@@ -76,9 +76,9 @@ CONFIGS = {
     "C2": square(16, 64, name="C2", tol=1e-10, precond=1,
                  note="unit square 64 seg x 64 steps, N=4096, preconditioned GMRES 1e-10"),
     "C3": square(64, 256, name="C3", tol=1e-10, n_slices=8, precond=1,
-                 note="unit square 256 seg x 256 steps, N=65536, P=8"),
+                 note="unit square 256 seg x 256 steps, N=65536"),
     "C4": square(128, 512, name="C4", tol=1e-8, n_slices=16, precond=1,
-                 note="unit square 512 seg x 512 steps, N=262144, P=16 (8 GPUs only)"),
+                 note="unit square 512 seg x 512 steps, N=262144 (dense V_h, D_h need >= 2 GPUs)"),
     "C5": Workload(name="C5", vertices=L_SHAPE, segments_per_side=[96, 48, 48, 48, 48, 96],
                    t_breaks=graded_times(256, 1.02), alpha=0.5, x_star=(0.75, 0.75),
                    tol=1e-10, n_slices=8, precond=1,
