@@ -299,7 +299,15 @@ template <int KIND, bool PROD = false>
 static void launch_kind(int which, const BlockArgs& BA, const MomArgs& M, int ng, int nband_or_chunk,
                         int nz, cudaStream_t st) {
   dim3 grid((ng + 31) / 32, (ng + 3) / 4, nz);
-  if (which == 0) k_bulk_m<KIND, 8, PROD><<<grid, 128, 0, st>>>(BA, M);
+  if (which == 0) {
+    constexpr size_t smem = bulk_smem_bytes<KIND, 8>();
+    static bool attr = false;   // per template instance
+    if (!attr) {
+      cudaFuncSetAttribute(k_bulk_m<KIND, 8, PROD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = true;
+    }
+    k_bulk_m<KIND, 8, PROD><<<grid, 128, smem, st>>>(BA, M);
+  }
   else k_near_m<KIND, PROD><<<grid, 128, 0, st>>>(BA, M, nband_or_chunk);
   count_launch();
 }

@@ -568,48 +568,109 @@ struct RegBZ {
 static __device__ __constant__ double STB_GB3_CB[STB_GB3_DEG + 1] = STB_GB3_INIT;
 __device__ __forceinline__ double gb3_cb(double t) { return horner<STB_GB3_DEG>(STB_GB3_CB, fma(t, STB_GB3_YS, -1.0)); }
 
-// TRUEV: return the true node value (near cells: without the affine terms, which then need not be
-// added here and subtracted again by the caller)
+// Regime-B coefficient source.  The Taylor sums are Horner chains over per-pair coefficient arrays
+// p1 (S1 of the first family), p2 (S2 of H / S3 of Q) and p3 (S1 of the second family), stored
+// field-major in the records (stride S).  The bulk kernel stages the first ns coefficients of its
+// pair in shared memory once per thread (sm: [chain][i] with stride BZS_STRIDE between entries), so
+// that a node's chains read L2 only for orders >= ns: a chain walked through L2 costs one L2 round
+// trip per unrolled step, which made a regime-B node ~25x the cost of a regime-A node.
+constexpr int BZ_KBS = 12;          // staged orders per chain (kb <= 11 for ~90% of the C3 / C5 nodes)
+constexpr int BZS_STRIDE = 128;     // threads per bulk CTA: entry i of chain f at sm[(f KBS + i) 128]
+struct BzSrc {
+  const double* p1;
+  const double* p2;
+  const double* p3;
+  long long S;
+  const double* sm;   // this thread's staged coefficients (nullptr: none)
+  int ns;             // staged entries per chain (orders 0 .. ns-1; p2 also its top entry kb if kb < ns)
+};
+
+// h[c][n] = the chain sums of NN nodes (z_n = -u_n), orders kb-1 .. 0 (+ the Q top entry kb)
+template <int KIND, int NN>
+__device__ __forceinline__ void bz_chains(const BzSrc& src, int kb, const double (&z)[NN],
+                                          double (&h1)[NN], double (&h2)[NN], double (&h3)[NN]) {
+  constexpr bool C2 = Fams<KIND>::f0 != FAM_F, C3 = Fams<KIND>::n == 2;
+  double top = 0.0;
+  if (Fams<KIND>::f0 == FAM_Q) top = kb < src.ns ? src.sm[(BZ_KBS + kb) * BZS_STRIDE] : src.p2[(long long)kb * src.S];
+#pragma unroll
+  for (int n = 0; n < NN; ++n) h1[n] = h3[n] = 0.0, h2[n] = top;
+  int i = kb - 1;
+  // orders >= ns from the records (coefficient pointers walked down by the record stride)
+  if (i >= src.ns) {
+    const long long off = (long long)i * src.S;
+    const double* q1 = src.p1 + off;
+    const double* q2 = src.p2 + off;
+    const double* q3 = src.p3 + off;
+#pragma unroll 2
+    for (; i >= src.ns; --i) {
+      const double c1 = *q1;
+#pragma unroll
+      for (int n = 0; n < NN; ++n) h1[n] = fma(h1[n], z[n], c1);
+      if (C2) {
+        const double c2 = *q2;
+#pragma unroll
+        for (int n = 0; n < NN; ++n) h2[n] = fma(h2[n], z[n], c2);
+      }
+      if (C3) {
+        const double c3 = *q3;
+#pragma unroll
+        for (int n = 0; n < NN; ++n) h3[n] = fma(h3[n], z[n], c3);
+      }
+      q1 -= src.S;
+      q2 -= src.S;
+      q3 -= src.S;
+    }
+  }
+  // staged orders from shared memory
+  if (i >= 0) {
+    const double* r1 = src.sm + i * BZS_STRIDE;
+#pragma unroll 4
+    for (; i >= 0; --i) {
+      const double c1 = r1[0];
+#pragma unroll
+      for (int n = 0; n < NN; ++n) h1[n] = fma(h1[n], z[n], c1);
+      if (C2) {
+        const double c2 = r1[BZ_KBS * BZS_STRIDE];
+#pragma unroll
+        for (int n = 0; n < NN; ++n) h2[n] = fma(h2[n], z[n], c2);
+      }
+      if (C3) {
+        const double c3 = r1[2 * BZ_KBS * BZS_STRIDE];
+#pragma unroll
+        for (int n = 0; n < NN; ++n) h3[n] = fma(h3[n], z[n], c3);
+      }
+      r1 -= BZS_STRIDE;
+    }
+  }
+}
+
 // The Taylor sums of one regime-B cluster (centre c0, order kb, coefficient arrays p1 / p2 of the
 // first family and p3 of the second, m_0 / m_1 in their last slots): the non-affine node parts
 // T[f].  E1(x0) by the GB3 form for x0 >= 8/3 (every single-cluster node: x0 >= x_max / (1 + MRHO)),
 // by the general E1 below (the clusters of regime B2 may sit lower).
 template <int KIND>
-__device__ __forceinline__ void bz_T(const double* __restrict__ p1, const double* __restrict__ p2,
-                                     const double* __restrict__ p3, long long S, double c0, double ic0,
-                                     int kb, double s, double u, double (&T)[2]) {
+__device__ __forceinline__ void bz_T(const BzSrc& src, double c0, double ic0, int kb, double s, double u,
+                                     double (&T)[2]) {
   const double x0 = c0 * u, ex = exp(-x0);
   const double E1 = x0 >= 8.0 / 3.0 ? ex * (ic0 * s) * gb3_cb(ic0 * s) : dev_e1(x0);
   // the Taylor sums as polynomials in z = -u (coefficients from k_records), Horner from the top
-  const double zu = -u;
-  double h1 = 0.0, h2 = Fams<KIND>::f0 == FAM_Q ? p2[(long long)kb * S] : 0.0, h3 = 0.0;
-  // coefficient pointers walked down by the record stride (no index multiply per load)
-  const long long top = (long long)(kb - 1) * S;
-  const double* q1 = p1 + top;
-  const double* q2 = p2 + top;
-  const double* q3 = p3 + top;
-#pragma unroll 2
-  for (int i = kb - 1; i >= 0; --i) {
-    h1 = fma(h1, zu, *q1);
-    if (Fams<KIND>::f0 != FAM_F) h2 = fma(h2, zu, *q2);
-    if (Fams<KIND>::n == 2) h3 = fma(h3, zu, *q3);
-    q1 -= S;
-    q2 -= S;
-    q3 -= S;
-  }
-  const double S1a = ex * h1, S2a = ex * h2, S1b = ex * h3;
+  const double z[1] = {-u};
+  double h1[1], h2[1], h3[1];
+  bz_chains<KIND, 1>(src, kb, z, h1, h2, h3);
+  const double S1a = ex * h1[0], S2a = ex * h2[0], S1b = ex * h3[0];
   const double a0 = ex * ic0;
-  const double m0 = p1[(long long)MKB * S];
-  if (Fams<KIND>::f0 == FAM_H) T[0] = fma(fma(1.0 + x0, E1, -ex), m0, fma(E1 * u, p2[(long long)MKB * S], -fma(u, S2a, S1a)));
-  else T[0] = fma(-E1, m0, fma(a0, m0, S2a) / u + S1a);
-  if (Fams<KIND>::n == 2) T[1] = fma(E1, p3[(long long)MKB * S], -S1b);
+  const double m0 = src.p1[(long long)MKB * src.S];
+  // (the Q form divides by u: multiplied by s = 1 / u instead)
+  if (Fams<KIND>::f0 == FAM_H) T[0] = fma(fma(1.0 + x0, E1, -ex), m0, fma(E1 * u, src.p2[(long long)MKB * src.S], -fma(u, S2a, S1a)));
+  else T[0] = fma(-E1, m0, fma(fma(a0, m0, S2a), s, S1a));
+  if (Fams<KIND>::n == 2) T[1] = fma(E1, src.p3[(long long)MKB * src.S], -S1b);
 }
 
 // TRUEV: return the true node value (near cells: without the affine terms, which then need not be
 // added here and subtracted again by the caller)
 template <int KIND, bool TRUEV = false>
 __device__ __forceinline__ double phi_bz(const double* __restrict__ rec, long long S, const RegBZ<KIND>& z,
-                                         double s, double u, int* regime) {
+                                         double s, double u, int* regime, const double* sm = nullptr, int ns = 0) {
   const bool zz = z.cmin > 0.0 && z.cmin * u >= MXZ;
   if (!zz && !(z.c0 > 0.0)) {
     *regime = 3;
@@ -619,7 +680,7 @@ __device__ __forceinline__ double phi_bz(const double* __restrict__ rec, long lo
   if (!zz) {
     const double* R0 = rec + (RF_COMMON + 0 * FAMSZ) * S;
     const double* R1 = rec + (RF_COMMON + 1 * FAMSZ) * S;
-    bz_T<KIND>(R0 + FB1 * S, R0 + FB2 * S, R1 + FB1 * S, S, z.c0, z.ic0, z.kb, s, u, T);
+    bz_T<KIND>(BzSrc{R0 + FB1 * S, R0 + FB2 * S, R1 + FB1 * S, S, sm, ns}, z.c0, z.ic0, z.kb, s, u, T);
   }
   *regime = zz ? 2 : 1;
   double out = 0.0;
@@ -656,11 +717,12 @@ __device__ __forceinline__ double phi_b2(const double* __restrict__ rec, long lo
   if (!zz1) {
     const double* R0 = rec + (RF_COMMON + 0 * FAMSZ) * S;
     const double* R1 = rec + (RF_COMMON + 1 * FAMSZ) * S;
-    bz_T<KIND>(R0 + FB1 * S, R0 + FB2 * S, R1 + FB1 * S, S, z.c0, z.ic0, z.kb, s, u, T);
+    bz_T<KIND>(BzSrc{R0 + FB1 * S, R0 + FB2 * S, R1 + FB1 * S, S, nullptr, 0}, z.c0, z.ic0, z.kb, s, u, T);
   }
   if (!zz2) {
     const double* B = rec + (long long)(rec2_base<KIND>() + R2_FAM) * S;
-    bz_T<KIND>(B, B + (long long)(MKB + 1) * S, B + (long long)R2_FAMSZ * S, S, z2.c0, z2.ic0, z2.kb, s, u, T2);
+    bz_T<KIND>(BzSrc{B, B + (long long)(MKB + 1) * S, B + (long long)R2_FAMSZ * S, S, nullptr, 0}, z2.c0, z2.ic0,
+               z2.kb, s, u, T2);
   }
   *regime = (zz1 && zz2) ? 2 : 1;
   double out = 0.0;
@@ -678,7 +740,7 @@ __device__ __forceinline__ double phi_b2(const double* __restrict__ rec, long lo
 template <int KIND>
 __device__ __forceinline__ void phi_bz2(const double* __restrict__ rec, long long S, const RegBZ<KIND>& z,
                                         double s1, double u1, double s2, double u2, double& v1,
-                                        double& v2, int* reg1, int* reg2) {
+                                        double& v2, int* reg1, int* reg2, const double* sm = nullptr, int ns = 0) {
   if (!(z.c0 > 0.0)) {   // no cluster: Z or C per node
     v1 = phi_bz<KIND>(rec, S, z, s1, u1, reg1);
     v2 = phi_bz<KIND>(rec, S, z, s2, u2, reg2);
@@ -692,46 +754,20 @@ __device__ __forceinline__ void phi_bz2(const double* __restrict__ rec, long lon
   const double* R0 = rec + (RF_COMMON + 0 * FAMSZ) * S;
   const double* R1 = rec + (RF_COMMON + 1 * FAMSZ) * S;
   // both nodes' Taylor sums as polynomials in -u (shared coefficient loads, 2 x 1-3 Horner chains)
-  const double z1 = -u1, z2 = -u2;
-  const double* p1 = R0 + FB1 * S;
-  const double* p2 = R0 + FB2 * S;
-  const double* p3 = R1 + FB1 * S;
-  const double top = Fams<KIND>::f0 == FAM_Q ? p2[(long long)z.kb * S] : 0.0;
-  double h11 = 0.0, h21 = top, h31 = 0.0, h12 = 0.0, h22 = top, h32 = 0.0;
-  const long long off = (long long)(z.kb - 1) * S;
-  const double* q1 = p1 + off;
-  const double* q2 = p2 + off;
-  const double* q3 = p3 + off;
-#pragma unroll 2
-  for (int i = z.kb - 1; i >= 0; --i) {
-    const double c1 = *q1;
-    h11 = fma(h11, z1, c1);
-    h12 = fma(h12, z2, c1);
-    if (Fams<KIND>::f0 != FAM_F) {
-      const double c2 = *q2;
-      h21 = fma(h21, z1, c2);
-      h22 = fma(h22, z2, c2);
-    }
-    if (Fams<KIND>::n == 2) {
-      const double c3 = *q3;
-      h31 = fma(h31, z1, c3);
-      h32 = fma(h32, z2, c3);
-    }
-    q1 -= S;
-    q2 -= S;
-    q3 -= S;
-  }
-  const double S1a1 = ex1 * h11, S2a1 = ex1 * h21, S1b1 = ex1 * h31;
-  const double S1a2 = ex2 * h12, S2a2 = ex2 * h22, S1b2 = ex2 * h32;
+  const double zz[2] = {-u1, -u2};
+  double h1[2], h2[2], h3[2];
+  bz_chains<KIND, 2>(BzSrc{R0 + FB1 * S, R0 + FB2 * S, R1 + FB1 * S, S, sm, ns}, z.kb, zz, h1, h2, h3);
+  const double S1a1 = ex1 * h1[0], S2a1 = ex1 * h2[0], S1b1 = ex1 * h3[0];
+  const double S1a2 = ex2 * h1[1], S2a2 = ex2 * h2[1], S1b2 = ex2 * h3[1];
   const double a01 = ex1 * ic0, a02 = ex2 * ic0;
   const double m0 = z.m0[0];
   double T1[2], T2[2];
   if (Fams<KIND>::f0 == FAM_H) {
     T1[0] = fma(fma(1.0 + x01, E11, -ex1), m0, fma(E11 * u1, z.m1, -fma(u1, S2a1, S1a1)));
     T2[0] = fma(fma(1.0 + x02, E12, -ex2), m0, fma(E12 * u2, z.m1, -fma(u2, S2a2, S1a2)));
-  } else {
-    T1[0] = fma(-E11, m0, fma(a01, m0, S2a1) / u1 + S1a1);
-    T2[0] = fma(-E12, m0, fma(a02, m0, S2a2) / u2 + S1a2);
+  } else {   // the Q form's division by u as a product with s = 1 / u
+    T1[0] = fma(-E11, m0, fma(fma(a01, m0, S2a1), s1, S1a1));
+    T2[0] = fma(-E12, m0, fma(fma(a02, m0, S2a2), s2, S1a2));
   }
   if (Fams<KIND>::n == 2) {
     T1[1] = fma(E11, z.m0[1], -S1b1);
@@ -821,9 +857,25 @@ __device__ __forceinline__ void count_regimes(unsigned long long* ctr, unsigned 
 // once each (1.125 node evaluations per entry at R = 8).  Column fast path: when the node with
 // the smallest lag is in regime A for every lane, all R+1 nodes are (s grows with x), and the
 // R+1 Horner chains run unrolled and interleaved.
+// The lag-table rows of the band's nodes (shared by the whole CTA) are staged in shared memory
+// by cp.async in chunks of LAG_CH columns, double-buffered: the chunk after the current one is in
+// flight while the current one is evaluated (a global load per column left every column waiting
+// on an L2 round trip: a quarter of the kernel's stall samples).
 // PROD (product mode, K_h g without storing K_h): each entry is multiplied by g at its trial
 // index and summed over the thread's columns; one warp sum per (test row, trial tile) is written
 // to the block's partial buffer (fixed slots: deterministic)
+constexpr int LAG_CH = 16;
+template <int KIND>
+__host__ __device__ constexpr int bulk_nch() { return Fams<KIND>::n == 2 ? 3 : 2; }
+// dynamic shared memory of k_bulk_m: staged regime-B coefficients + two lag chunks
+template <int KIND, int R>
+__host__ __device__ constexpr size_t bulk_smem_bytes() {
+  return sizeof(double) * bulk_nch<KIND>() * BZ_KBS * BZS_STRIDE + sizeof(double4) * 2 * LAG_CH * (R + 1);
+}
+__device__ __forceinline__ void cp_async16_bulk(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(sa), "l"(gmem));
+}
 template <int KIND, int R, bool PROD = false>
 __global__ void __launch_bounds__(128, (KIND == STB_D || PROD) ? 2 : 3) k_bulk_m(BlockArgs B, MomArgs M) {
   const int ng = B.ng;
@@ -848,6 +900,25 @@ __global__ void __launch_bounds__(128, (KIND == STB_D || PROD) ? 2 : 3) k_bulk_m
   // the tile's offset + (I mod 32) * 32), shared by the warp: a store is one LDS + one address add
   __shared__ long long s_row[4][R];
   __shared__ double s_phi[(R + 1) * 128];       // per-thread node values during the fix-ups
+  extern __shared__ __align__(16) double bulk_dyn[];
+  constexpr int NCH = bulk_nch<KIND>();
+  double* s_bz = bulk_dyn;                                                  // [NCH][KBS][128]
+  double4* s_lag = reinterpret_cast<double4*>(bulk_dyn + NCH * BZ_KBS * BZS_STRIDE);   // [2][LAG_CH][R+1]
+  // lag chunk c: columns y = b0 + c LAG_CH + k, nodes x = min(r_lo + r, r_hi) (2 x 16 B per entry)
+  const int ncols = bmax + 2 - B.b0;
+  auto stage = [&](int c) {
+    double4* dst = s_lag + (c & 1) * (LAG_CH * (R + 1));
+    for (int e = threadIdx.x; e < 2 * LAG_CH * (R + 1); e += blockDim.x) {
+      const int ent = e >> 1, k = ent / (R + 1), r = ent % (R + 1);
+      const int y = B.b0 + c * LAG_CH + k;
+      if (c * LAG_CH + k < ncols) {
+        const double* src = reinterpret_cast<const double*>(B.lag + (long long)min(r_lo + r, r_hi) * B.ldlag + y);
+        cp_async16_bulk(reinterpret_cast<double*>(dst + ent) + 2 * (e & 1), src + 2 * (e & 1));
+      }
+    }
+    asm volatile("cp.async.commit_group;");
+  };
+  stage(0);
   long long* srow = s_row[threadIdx.x >> 5];
   if (!PROD && lane < R) {
     const int a = min(r_lo + lane, r_hi - 1);
@@ -861,27 +932,24 @@ __global__ void __launch_bounds__(128, (KIND == STB_D || PROD) ? 2 : 3) k_bulk_m
   A.load(M.rec + pair, S);
   // pairs without quadrature points (K_h on collinear elements: the kernel vanishes) hold
   // only zero entries: a warp of them writes zeros (or, in product mode, nothing) and skips the
-  // node evaluations, counted as regime A
-  if (__all_sync(0xffffffffu, A.cmax == 0.0 && A.P[0] == 0.0 && A.l0 == 0.0)) {
-    unsigned long long nz = 0;
-    for (int y = B.b0; y <= bmax + 1; ++y) {
-#pragma unroll
-      for (int r = 0; r <= R; ++r) nz += (r_lo + r <= r_hi && r_lo + r > y);
-      if (!PROD && y > B.b0) {
-        const int b = y - 1;
-        double* col = B.out + ((long long)(b - B.b0) * cstride + jcol);
-#pragma unroll
-        for (int r = 1; r <= R; ++r) {
-          const int a = r_lo + r - 1;
-          if (valid && a < r_hi && a - b >= 2) col[srow[r - 1]] = 0.0;
-        }
-      }
-    }
-    count_regimes(M.counters, valid ? nz : 0, 0, 0, 0, 0);
-    return;
-  }
+  // node evaluations, counted as regime A (warp-uniform; the warp still joins the lag staging)
+  const bool zero_warp = __all_sync(0xffffffffu, A.cmax == 0.0 && A.P[0] == 0.0 && A.l0 == 0.0);
   RegBZ<KIND> Z;
   Z.load(M.rec + pair, S);
+  // the pair's regime-B Taylor coefficients, orders < BZ_KBS (and K's top entry), staged once in
+  // shared memory: this thread's column of s_bz (only this thread reads it, no barrier needed)
+  double* sbz = s_bz + threadIdx.x;
+  int nsb = 0;
+  if (!zero_warp && Z.c0 > 0.0) {
+    const double* R0 = M.rec + pair + (RF_COMMON + 0 * FAMSZ) * S;
+    const double* R1 = M.rec + pair + (RF_COMMON + 1 * FAMSZ) * S;
+    nsb = min(Z.kb + 1, BZ_KBS);
+    for (int i = 0; i < nsb; ++i) {
+      sbz[i * BZS_STRIDE] = R0[(FB1 + i) * S];
+      if (Fams<KIND>::f0 != FAM_F) sbz[(BZ_KBS + i) * BZS_STRIDE] = R0[(FB2 + i) * S];
+      if (NCH == 3) sbz[(2 * BZ_KBS + i) * BZS_STRIDE] = R1[(FB1 + i) * S];
+    }
+  }
   unsigned long long nA = 0, nB = 0, nZ = 0, nC = 0, nK = 0;
   double accp[R];
 #pragma unroll
@@ -890,19 +958,32 @@ __global__ void __launch_bounds__(128, (KIND == STB_D || PROD) ? 2 : 3) k_bulk_m
 #pragma unroll
   for (int r = 0; r < R; ++r) Gp[r] = 0.0;
   for (int y = B.b0; y <= bmax + 1; ++y) {
+    const int kc = y - B.b0;
+    if (kc % LAG_CH == 0) {                          // CTA-uniform: chunk kc / LAG_CH is needed
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+      __syncthreads();                               // visible to all; the other buffer is free
+      if (kc + LAG_CH < ncols) stage(kc / LAG_CH + 1);
+    }
+    const double4* ndc = s_lag + ((kc / LAG_CH) & 1) * (LAG_CH * (R + 1)) + (kc % LAG_CH) * (R + 1);
     // every node of the column by the regime-A form, branch-free (clamped into the lag table,
     // invalid nodes zeroed) so that the R+1 Horner chains interleave; then the nodes of lanes
     // outside regime A are overwritten (B / Z per lane, C warp-cooperatively)
     double phi[R + 1];
     double4 nd[R + 1];
 #pragma unroll
-    for (int r = 0; r <= R; ++r) nd[r] = B.lag[min(r_lo + r, r_hi) * B.ldlag + y];
+    for (int r = 0; r <= R; ++r) nd[r] = ndc[r];
     unsigned bmask = 0;
     // full columns (every band node above the trial node) whose smallest-lag node is in regime A
     // for every lane: all nodes are (s grows with x), no masks or regime tests per node
     // (not for V_h: its 3-CTA register budget would spill)
     const bool full = KIND != STB_V && r_lo > y && r_hi - r_lo == R;       // CTA-uniform
-    if (full && __all_sync(0xffffffffu, A.cmax * nd[0].z < STB_MXA)) {
+    if (zero_warp) {
+#pragma unroll
+      for (int r = 0; r <= R; ++r) {
+        phi[r] = 0.0;
+        nA += r_lo + r <= r_hi && r_lo + r > y;
+      }
+    } else if (full && __all_sync(0xffffffffu, A.cmax * nd[0].z < STB_MXA)) {
 #pragma unroll
       for (int r = 0; r <= R; ++r) phi[r] = A.eval(nd[r].x, nd[r].y, nd[r].z);
       nA += R + 1;
@@ -925,21 +1006,18 @@ __global__ void __launch_bounds__(128, (KIND == STB_D || PROD) ? 2 : 3) k_bulk_m
 #pragma unroll
       for (int r = 0; r <= R; ++r) sp[r * 128] = phi[r];
       unsigned cmask = 0;   // nodes r of this lane left to regime C
+      // two nodes per pass (the Taylor chains interleave and share the coefficient loads); an odd
+      // last node is evaluated as a pair with itself, so that every lane runs the same code path
       while (bmask) {
         const int r = __ffs(bmask) - 1;
         bmask &= bmask - 1;
-        const double4 q = B.lag[(r_lo + r) * B.ldlag + y];
+        const int r2 = bmask ? __ffs(bmask) - 1 : r;
+        bmask &= bmask - 1;
+        const double4 q = ndc[r], q2 = ndc[r2];
         int reg = 0, reg2 = 0;
         double v = 0.0, v2 = 0.0;
-        int r2 = -1;
-        if (bmask) {             // a second node of the same lane: evaluate both together
-          r2 = __ffs(bmask) - 1;
-          bmask &= bmask - 1;
-          const double4 q2 = B.lag[(r_lo + r2) * B.ldlag + y];
-          phi_bz2<KIND>(M.rec + pair, S, Z, q.x, q.z, q2.x, q2.z, v, v2, &reg, &reg2);
-        } else {
-          v = phi_bz<KIND>(M.rec + pair, S, Z, q.x, q.z, &reg);
-        }
+        phi_bz2<KIND>(M.rec + pair, S, Z, q.x, q.z, q2.x, q2.z, v, v2, &reg, &reg2, sbz, nsb);
+        if (r2 == r) reg2 = 0;
         nB += (reg == 1) + (reg2 == 1);
         nK += (reg == 1 ? Z.kb : 0) + (reg2 == 1 ? Z.kb : 0);
         nZ += (reg == 2) + (reg2 == 2);
@@ -952,7 +1030,7 @@ __global__ void __launch_bounds__(128, (KIND == STB_D || PROD) ? 2 : 3) k_bulk_m
           ++nC;
         }
         sp[r * 128] = v;
-        if (r2 >= 0) sp[r2 * 128] = v2;
+        if (r2 != r) sp[r2 * 128] = v2;
       }
       unsigned lanes = __ballot_sync(0xffffffffu, cmask != 0);
       while (lanes) {                                   // warp-uniform
@@ -963,7 +1041,7 @@ __global__ void __launch_bounds__(128, (KIND == STB_D || PROD) ? 2 : 3) k_bulk_m
         while (cm) {
           const int r = __ffs(cm) - 1;
           cm &= cm - 1;
-          const double4 q = B.lag[(r_lo + r) * B.ldlag + y];
+          const double4 q = ndc[r];
           const double v = phi_c_warp<KIND, false>(M, Is, Js, q.x, q.y, q.z);
           if (lane == src) sp[r * 128] = v;
         }

@@ -835,8 +835,8 @@ def test_quadrature_options():
     m = S.Mesh.from_workload(w)
     for kind in "VKD":
         A0 = getattr(m, f"assemble_{kind}")()
-        A1 = getattr(m, f"assemble_{kind}")(q_near=min(6, m.info.q_bulk + 1), near_gap=9)
-        A2 = getattr(m, f"assemble_{kind}")(q_near=8, near_gap=12)
+        A1 = getattr(m, f"assemble_{kind}")(q_near=min(6, A0.stats()["q_bulk"] + 1), near_gap=9)
+        A2 = getattr(m, f"assemble_{kind}")(q_near=10, near_gap=3)
         d0, d1, d2 = A0.dense(), A1.dense(), A2.dense()
         assert np.array_equal(d0, d1)
         assert relmax(d2, oracle_dense("C1", kind)) <= MAT_TOL
