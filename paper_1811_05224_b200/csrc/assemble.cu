@@ -331,8 +331,16 @@ template <int KIND>
 static void launch_records(const MomArgs& MB, const MomArgs& MN, const MomArgs* MS, int q_sing,
                            cudaStream_t st) {
   const unsigned nblk = (unsigned)((MB.npairs + 127) / 128);
+  // D_h near records: the pairs with touching or close half-segment sub-pairs (distance-dependent
+  // orders, skipped sub-pairs) warp per pair, the others thread per pair (k_records near_special)
   k_records<KIND, false><<<nblk, 128, 0, st>>>(MB);
-  k_records<KIND, true><<<nblk, 128, 0, st>>>(MN);
+  if (KIND == STB_D) {
+    k_records<KIND, true, true><<<nblk, 128, 0, st>>>(MN);
+    k_records_warp<KIND, true, true><<<(unsigned)((MN.npairs * 32 + 127) / 128), 128, 0, st>>>(MN);
+    count_launch();
+  } else {
+    k_records<KIND, true><<<nblk, 128, 0, st>>>(MN);
+  }
   count_launch(2);
   if (MS) {
     k_sing_records<KIND><<<(unsigned)((MS->npairs * 32 + 127) / 128), 128, 0, st>>>(*MS, q_sing);   // warp per record

@@ -260,16 +260,33 @@ __device__ __forceinline__ void for_points_lane(const MomArgs& M, int I, int J, 
 }
 
 // ------------------------------------------------------------- records
-// One thread per entry-level spatial pair (I, J): c range, regime-A moments premultiplied by the
-// polynomial coefficients, regime-B shifted moments, and the affine constants
+// One entry-level spatial pair (I, J): c range, regime-A moments premultiplied by the polynomial
+// coefficients, regime-B shifted moments, and the affine constants
 //   C0 = sum W (gamma + ln c), C1 = sum W c (gamma + ln c)  (H);  C0 (F, Q);  C1 = sum W / c (Q)
-template <int KIND, bool NEAR>
-__global__ void __launch_bounds__(128) k_records(MomArgs M) {
-  const long long pair = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (pair >= M.npairs) return;
+// WARP = false: one thread per pair.  WARP = true: one warp per pair, its points dealt round-robin
+// to the lanes and the partial sums reduced by xor butterflies (every lane ends with the same
+// totals; lane 0 writes the record) -- for the pairs with many points (the near records, whose
+// orders 10 / 8 / 6 / q_near differ between neighbouring pairs, and D_h's 16 half-segment
+// sub-pairs): thread-per-pair left half of each warp idle on the divergent point counts.
+template <bool WARP>
+__device__ __forceinline__ double rsum(double v) {
+  if (WARP) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  }
+  return v;
+}
+template <int KIND, bool NEAR, bool WARP, class Vis>
+__device__ __forceinline__ void rec_points(const MomArgs& M, int I, int J, int lane, Vis&& vis) {
+  if (WARP) for_points_lane<KIND, NEAR>(M, I, J, lane, vis);
+  else for_points<KIND, NEAR>(M, I, J, vis);
+}
+template <int KIND, bool NEAR, bool WARP>
+__device__ __forceinline__ void records_body(const MomArgs& M, long long pair, int lane) {
   const int I = (int)(pair / M.ng), J = (int)(pair % M.ng);
   double* rec = M.rec + pair;
   const long long S = M.npairs;
+  const bool wr = !WARP || lane == 0;   // the lane that writes the record
   // one pass: c range, regime-A moments M_k = sum W c^k and the affine constants of both
   // families (the constants need c > 0 at every point: dropped at the end if one c is 0)
   constexpr int NF = Fams<KIND>::n;
@@ -282,7 +299,7 @@ __global__ void __launch_bounds__(128) k_records(MomArgs M) {
   }
   double cmin = 1e300, cmax = 0.0;
   int npts = 0;
-  for_points<KIND, NEAR>(M, I, J, [&](double c, double wa, double wb) {
+  rec_points<KIND, NEAR, WARP>(M, I, J, lane, [&](double c, double wa, double wb) {
     cmin = fmin(cmin, c);
     cmax = fmax(cmax, c);
     ++npts;
@@ -308,6 +325,21 @@ __global__ void __launch_bounds__(128) k_records(MomArgs M) {
       }
     }
   });
+  if (WARP) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      cmin = fmin(cmin, __shfl_xor_sync(0xffffffffu, cmin, o));
+      cmax = fmax(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
+      npts += __shfl_xor_sync(0xffffffffu, npts, o);
+    }
+#pragma unroll
+    for (int f = 0; f < NF; ++f) {
+      C0[f] = rsum<WARP>(C0[f]);
+      C1[f] = rsum<WARP>(C1[f]);
+#pragma unroll
+      for (int k = 0; k <= MKA; ++k) mk[f][k] = rsum<WARP>(mk[f][k]);
+    }
+  }
   if (npts == 0) cmin = 0.0;
   if (!(cmin > 0.0)) {
 #pragma unroll
@@ -332,21 +364,23 @@ __global__ void __launch_bounds__(128) k_records(MomArgs M) {
   const double c0b = two ? 0.5 * (cs + cmax) : 0.0;
   const double rhob = two ? (cmax - c0b) / c0b : 1.0;
   const int kbb = two ? (rhob <= 1e-6 ? 3 : min(MKB, max(3, (int)ceil(log(1e-16) / log(rhob))))) : 0;
-  if (NEAR) {
+  if (NEAR && wr) {
     double* R2 = rec + (long long)rec2_base<KIND>() * S;
     R2[R2_C0 * S] = c0b;
     R2[R2_IC0 * S] = two ? 1.0 / c0b : 0.0;
     R2[R2_KB * S] = (double)kbb;
     R2[R2_CS * S] = cs;
   }
-  rec[RF_CMAX * S] = cmax;
-  rec[RF_CMIN * S] = cmin;
-  rec[RF_C0 * S] = c0;
-  rec[RF_KB * S] = (double)kb;
-  rec[RF_IC0 * S] = okB ? 1.0 / c0 : 0.0;
+  if (wr) {
+    rec[RF_CMAX * S] = cmax;
+    rec[RF_CMIN * S] = cmin;
+    rec[RF_C0 * S] = c0;
+    rec[RF_KB * S] = (double)kb;
+    rec[RF_IC0 * S] = okB ? 1.0 / c0 : 0.0;
+  }
   // regime-A fields of both families (static indices: the moments stay in registers)
 #pragma unroll
-  for (int f = 0; f < NF; ++f) {
+  for (int f = 0; f < NF && wr; ++f) {
     const int fam = f == 0 ? Fams<KIND>::f0 : Fams<KIND>::f1;
     double* R = rec + (RF_COMMON + f * FAMSZ) * S;
 #pragma unroll
@@ -372,7 +406,7 @@ __global__ void __launch_bounds__(128) k_records(MomArgs M) {
 #pragma unroll
     for (int k = 0; k <= MKB; ++k) mb[k] = 0.0;
     if (okB) {
-      for_points<KIND, NEAR>(M, I, J, [&](double c, double wa, double wb) {
+      rec_points<KIND, NEAR, WARP>(M, I, J, lane, [&](double c, double wa, double wb) {
         if (cl == 1 ? !(c > cs) : (two && c > cs)) return;
         const double w = slot == 0 ? wa : wb;
         const double d = c - cc0, d2 = d * d, d4 = d2 * d2;
@@ -394,7 +428,17 @@ __global__ void __launch_bounds__(128) k_records(MomArgs M) {
           }
         }
       });
+      if (WARP) {
+#pragma unroll
+        for (int kc = 0; kc <= MKB / 8; ++kc) {
+          if (kc * 8 > ckb) break;
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (kc * 8 + j <= MKB) mb[kc * 8 + j] = rsum<WARP>(mb[kc * 8 + j]);
+        }
+      }
     }
+    if (!wr) return;
     // regime-B polynomial coefficients: every Taylor sum of phi_bz is
     // e^{-x0} sum_i coef_i (-u)^i with per-pair coefficients from backward recurrences over the
     // shifted moments (B1_k = m_k / k, B2_k = m_k / ((k-1) k)):
@@ -433,6 +477,33 @@ __global__ void __launch_bounds__(128) k_records(MomArgs M) {
 #pragma unroll 1
     for (int slot = 0; slot < NF; ++slot) bpass(slot, std::integral_constant<int, 1>{});
   }
+}
+// near records: a pair with a touching sub-pair or one closer than near_gap element lengths takes
+// sub-pair orders 10 / 8 / 6 next to q_near and skips its touching sub-pairs -- per lane different
+// loop nests, which serialise a thread-per-pair warp several times over; such pairs (a band along
+// the chain and the corners) go to the warp-per-pair kernel, the others to thread-per-pair
+template <int KIND>
+__device__ __forceinline__ bool near_special(const MomArgs& M, int I, int J) {
+  bool sp = false;
+  for_subpairs<KIND, false>(M, I, J, [&](const SubPair& q) {
+    sp |= chain_rel(q.pi, q.qi, q.nchain) != 0 || seg_dist(q.X, q.Y) < M.near_gap * fmax(q.X.h, q.Y.h);
+  });
+  return sp;
+}
+// SPLIT: D_h near records, pairs divided between the two kernels by near_special
+template <int KIND, bool NEAR, bool SPLIT = false>
+__global__ void __launch_bounds__(128) k_records(MomArgs M) {
+  const long long pair = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (pair >= M.npairs) return;
+  if (SPLIT && near_special<KIND>(M, (int)(pair / M.ng), (int)(pair % M.ng))) return;
+  records_body<KIND, NEAR, false>(M, pair, 0);
+}
+template <int KIND, bool NEAR, bool SPLIT = false>
+__global__ void __launch_bounds__(128) k_records_warp(MomArgs M) {
+  const long long pair = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (pair >= M.npairs) return;   // warp-uniform
+  if (SPLIT && !near_special<KIND>(M, (int)(pair / M.ng), (int)(pair % M.ng))) return;   // warp-uniform
+  records_body<KIND, NEAR, true>(M, pair, threadIdx.x & 31);
 }
 
 __device__ __forceinline__ double warp_sum(double v) {
