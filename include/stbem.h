@@ -112,7 +112,9 @@ typedef struct {
   double true_rel_residual;  /* ||C(b - V w)|| / ||C b|| recomputed at exit */
   double seconds_total;
   double seconds_matvec;     /* V and D products (device time) */
-  double seconds_comm;       /* collectives (device time, 0 on one GPU) */
+  double seconds_comm;       /* collectives: device time of the NCCL calls (CUDA events on their
+                                stream, overlapped with the GEMV where chunked), host time of the
+                                emulated ranks' all-reduces; 0 without a communicator */
   int n_matvec_V;            /* V_h products performed (incl. the true-residual check) */
   int n_matvec_D;            /* D_h products performed */
 } bem_solve_report;
@@ -151,6 +153,19 @@ bem_status bem_nccl_get_unique_id(void* out128_host);
  * Errors: BEM_E_INVALID (arguments), BEM_E_NCCL (libnccl.so.2 not loadable or NCCL failure). */
 bem_status bem_comm_create(const void* unique_id128_host, int nranks, int rank, int cuda_device,
                            bem_comm** out);
+/* Emulated ranks on ONE device, without NCCL (tests of the multi-rank path on a single GPU):
+ * writes nranks (1..16) communicator handles to out_host[0 .. nranks-1], rank r = out_host[r], all
+ * on cuda_device.  Each rank must be driven by its own host thread, SPMD, exactly as one process per
+ * GPU would (every rank calls every collective function).  A product's all-reduce synchronises the
+ * rank's stream, meets the other ranks at a host barrier, sums all ranks' partial results in rank
+ * order (identical on every rank) and copies the sum back after a second barrier -- no kernel waits
+ * on another rank's kernel.  Each handle is freed with bem_comm_destroy.
+ * Errors: BEM_E_INVALID (nranks out of range, null out_host), BEM_E_CUDA. */
+bem_status bem_comm_create_group(int nranks, int cuda_device, bem_comm** out_host);
+/* NCCL communicators: the collectives run on the communicator's own stream (a product's row
+ * chunks are all-reduced while the GEMV of the next chunk runs); every host wait of the solver polls
+ * ncclCommGetAsyncError and aborts the communicator on an asynchronous error (BEM_E_NCCL from then
+ * on).  Frees the handle (NCCL or emulated). */
 void bem_comm_destroy(bem_comm* comm);
 
 /* ----------------------------------------------------- cyclic K_P plan (host) */

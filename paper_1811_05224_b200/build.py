@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libstbem.so")
-SOURCES = ["mesh.cpp", "api.cpp", "comm.cpp", "assemble.cu", "linalg.cu"]
+SOURCES = ["mesh.cpp", "api.cpp", "comm.cu", "assemble.cu", "linalg.cu"]
 HEADERS = ["internal.h", "special.cuh", "special_coeffs.h", "moments.cuh", "moment_coeffs.h", "potential.cuh",
            "initial.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -378,23 +378,26 @@ bem_status bem_solve_gmres(const bem_matrix* V, const bem_matrix* D, const bem_m
   double *Q = nullptr, *tmp = nullptr, *u = nullptr, *v = nullptr, *dh = nullptr, *wk = nullptr;
   double* hpin = nullptr;  // pinned host copy of the Hessenberg column (persistent, grow-only)
   cudaError_t e;
-  static std::mutex pin_mu;
-  static double* pin_buf = nullptr;
-  static size_t pin_n = 0;
-  std::lock_guard<std::mutex> pin_lock(pin_mu);   // one solve at a time uses the pinned buffer
+  // per host thread (concurrent solves on several threads, e.g. emulated ranks, each own theirs)
+  struct PinBuf {
+    double* p = nullptr;
+    size_t n = 0;
+    ~PinBuf() { if (p) cudaFreeHost(p); }
+  };
+  static thread_local PinBuf pin;
   const size_t slot = (size_t)2 * (kmax + 2);      // one Hessenberg column copy
-  if (pin_n < 3 * slot) {                          // slots 0, 1 (alternating iterations), 2 (misc)
-    if (pin_buf) cudaFreeHost(pin_buf);
-    pin_buf = nullptr;
-    pin_n = 0;
-    if (cudaMallocHost(&pin_buf, sizeof(double) * 3 * slot) != cudaSuccess) {
+  if (pin.n < 3 * slot) {                          // slots 0, 1 (alternating iterations), 2 (misc)
+    if (pin.p) cudaFreeHost(pin.p);
+    pin.p = nullptr;
+    pin.n = 0;
+    if (cudaMallocHost(&pin.p, sizeof(double) * 3 * slot) != cudaSuccess) {
       cudaGetLastError();
       set_error("bem_solve_gmres: pinned allocation failed");
       return BEM_E_NOMEM;
     }
-    pin_n = 3 * slot;
+    pin.n = 3 * slot;
   }
-  hpin = pin_buf;
+  hpin = pin.p;
   mesh_wait(m, st);
   // stream-ordered allocations: no device-wide synchronisation
   const size_t q_bytes = sizeof(double) * n * (kmax + 1);
@@ -412,6 +415,8 @@ bem_status bem_solve_gmres(const bem_matrix* V, const bem_matrix* D, const bem_m
   }
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0); cudaEventCreate(&e1);
+  CommTimer ctimer;                 // device / host time of the collectives of this solve
+  comm_timer_set(m->comm ? &ctimer : nullptr);
   // GEMV timing: an event pair per product, read once after the solve (no host sync per product)
   std::vector<cudaEvent_t> mvev;
   auto mv_mark = [&]() {
@@ -445,10 +450,16 @@ bem_status bem_solve_gmres(const bem_matrix* V, const bem_matrix* D, const bem_m
     mv_mark();
     return s1;
   };
+  cudaEvent_t nev;
+  cudaEventCreateWithFlags(&nev, cudaEventDisableTiming);
   auto norm = [&](const double* x) -> double {
     vec_dots(x, 0, 1, x, n, dh, st);
     cudaMemcpyAsync(hpin + 2 * slot, dh, sizeof(double), cudaMemcpyDeviceToHost, st);
-    cudaStreamSynchronize(st);
+    cudaEventRecord(nev, st);
+    if (comm_wait_event(m, nev) != BEM_OK) {
+      status = BEM_E_NCCL;
+      return 0.0;
+    }
     return std::sqrt(hpin[2 * slot]);
   };
   // one Arnoldi step k, enqueued only (no host wait): w = C V q_k, CGS2 against q_0..q_k with
@@ -478,6 +489,7 @@ bem_status bem_solve_gmres(const bem_matrix* V, const bem_matrix* D, const bem_m
   double resid = 1.0;
   status = apply_C(b, Q);
   double beta = status == BEM_OK ? norm(Q) : 0.0;
+  if (status != BEM_OK) beta = 0.0;
   if (hist) hist[0] = 1.0;
   if (status == BEM_OK && beta == 0.0) {
     cudaMemsetAsync(w, 0, sizeof(double) * n, st);
@@ -499,7 +511,9 @@ bem_status bem_solve_gmres(const bem_matrix* V, const bem_matrix* D, const bem_m
         if ((status = enqueue_step(k + 1)) != BEM_OK) break;
         enq = k + 1;
       }
-      cudaEventSynchronize(hev[k & 1]);
+      // host wait for the column (polls NCCL for asynchronous errors: a failed peer aborts the
+      // communicator instead of hanging the solve)
+      if ((status = comm_wait_event(m, hev[k & 1])) != BEM_OK) break;
       const double* hcol = hpin + (k & 1) * slot;
       const double hk1 = std::sqrt(hcol[2 * k + 2]);
       double* Hk = &H[(size_t)k * (kmax + 1)];
@@ -550,7 +564,10 @@ bem_status bem_solve_gmres(const bem_matrix* V, const bem_matrix* D, const bem_m
     if (status == BEM_OK) {
       vec_axpby(tmp, 1.0, b, -1.0, n, st);
       status = apply_C(tmp, wk);
-      if (status == BEM_OK) true_res = norm(wk) / beta;
+      if (status == BEM_OK) {
+        const double nr = norm(wk);
+        if (status == BEM_OK) true_res = nr / beta;
+      }
     }
   }
   cudaEventRecord(e1, st);
@@ -567,7 +584,9 @@ bem_status bem_solve_gmres(const bem_matrix* V, const bem_matrix* D, const bem_m
   storage_release(m->device, Q, q_bytes, st); cudaFreeAsync(tmp, st); cudaFreeAsync(u, st); cudaFreeAsync(v, st);
   cudaFreeAsync(wk, st); cudaFreeAsync(dh, st);
   cudaStreamSynchronize(st);
-  cudaEventDestroy(e0); cudaEventDestroy(e1);
+  comm_timer_set(nullptr);
+  const double t_comm = comm_timer_seconds(&ctimer);
+  cudaEventDestroy(e0); cudaEventDestroy(e1); cudaEventDestroy(nev);
   cudaEventDestroy(hev[0]); cudaEventDestroy(hev[1]);
   if (e != cudaSuccess) return cuda_fail(e, "bem_solve_gmres");
   if (rep) {
@@ -577,7 +596,7 @@ bem_status bem_solve_gmres(const bem_matrix* V, const bem_matrix* D, const bem_m
     rep->true_rel_residual = true_res;
     rep->seconds_total = ms_total * 1e-3;
     rep->seconds_matvec = t_mv;
-    rep->seconds_comm = 0.0;
+    rep->seconds_comm = t_comm;
     rep->n_matvec_V = nmv_V;
     rep->n_matvec_D = nmv_D;
   }
@@ -723,7 +742,9 @@ void bem_matrix_destroy(bem_matrix* A) {
   const cudaStream_t st = A->stream;
   if (A->data) storage_release(A->mesh ? A->mesh->device : 0, A->data, A->data_bytes, st);
   storage_release(A->mesh ? A->mesh->device : 0, A->d_partials, A->partials_bytes, st);
-  for (void* p : {(void*)A->d_segs, (void*)A->d_row_pbase,
+  for (int c = 0; c < bem_matrix_s::COMM_CHUNKS; ++c)
+    if (A->chunk_ev[c]) cudaEventDestroy(A->chunk_ev[c]);
+  for (void* p : {(void*)A->d_segs, (void*)A->d_segs_ch, (void*)A->d_row_pbase,
                   (void*)A->d_row_pstride, (void*)A->d_ysum, (void*)A->d_rowcnt, (void*)A->d_lo, (void*)A->d_di,
                   (void*)A->d_up, (void*)A->d_work, (void*)A->d_ctr})
     if (p) cudaFreeAsync(p, st);

@@ -64,9 +64,13 @@ constexpr int QSING_MAX = 16;
 
 }  // namespace stb
 
+namespace stb { struct CommGroup; }
 struct bem_comm_s {
   int nranks = 1, rank = 0, device = 0;
-  void* nccl = nullptr;  // ncclComm_t
+  void* nccl = nullptr;            // ncclComm_t (NCCL communicator), or
+  stb::CommGroup* group = nullptr; // emulated ranks on one device (host-thread group, tests)
+  cudaStream_t stream = nullptr;   // NCCL: the collectives' stream (overlap with the GEMV)
+  bool failed = false;             // an asynchronous NCCL error was seen: the communicator is aborted
 };
 
 struct bem_mesh_s {
@@ -135,6 +139,15 @@ struct bem_matrix_s {
   };
   std::vector<GemvSeg> segs;
   GemvSeg* d_segs = nullptr;
+  // multi-GPU, symmetric packed: the same items split into row chunks (test steps), so that the
+  // all-reduce of one chunk's rows overlaps the GEMV of the next (linalg.cu)
+  static constexpr int COMM_CHUNKS = 4;
+  int nchunks = 0;
+  int chunk_seg0[COMM_CHUNKS + 1] = {0};       // segment range of chunk c in d_segs_ch
+  long long chunk_items[COMM_CHUNKS] = {0};
+  int chunk_row0[COMM_CHUNKS + 1] = {0};       // test steps [row0[c], row0[c+1])
+  GemvSeg* d_segs_ch = nullptr;
+  cudaEvent_t chunk_ev[COMM_CHUNKS] = {nullptr};
   long long n_items = 0, n_partials = 0;
   std::vector<long long> row_pbase;  // per test step: partial base, stride = row_pstride[a]
   std::vector<int> row_pstride;
@@ -237,6 +250,23 @@ void vec_combine(double* out, const double* Q, long long ldq, int k, const doubl
 void vec_mul(double* y, const double* d, const double* x, long long n, cudaStream_t st);
 // collectives (comm.cpp)
 bem_status allreduce_sum(const bem_mesh* m, double* buf, long long n, cudaStream_t st);
+// stream on which allreduce_sum_async runs the NCCL collective after waiting on `ready` (recorded
+// on the compute stream); the caller joins it back with comm_join.  Group / no communicator:
+// the plain allreduce_sum on st.
+bem_status allreduce_sum_async(const bem_mesh* m, double* buf, long long n, cudaStream_t st, cudaEvent_t ready);
+bem_status comm_join(const bem_mesh* m, cudaStream_t st);
+bool comm_overlaps(const bem_mesh* m);   // NCCL with its own collective stream
+// host wait on an event that polls the communicator for asynchronous NCCL errors (and aborts it on
+// one) instead of blocking: a failed peer cannot hang the solve.  BEM_E_NCCL on an error.
+bem_status comm_wait_event(const bem_mesh* m, cudaEvent_t ev);
+// collective timing sink of the calling thread (bem_solve_gmres): device time of the collectives
+// (CUDA events around each NCCL call on its stream) and host time of the group collectives
+struct CommTimer {
+  std::vector<cudaEvent_t> ev;   // pairs (start, end)
+  double host_s = 0.0;
+};
+void comm_timer_set(CommTimer* t);   // nullptr: off
+double comm_timer_seconds(CommTimer* t);   // sums and destroys the events
 }  // namespace stb
 
 namespace stb {

@@ -277,6 +277,33 @@ bem_status gemv_setup(bem_matrix* A) {
     if ((e = cudaMallocAsync((void**)&A->d_rowcnt, sizeof(int) * nt, st)) != cudaSuccess ||
         (e = cudaMemsetAsync(A->d_rowcnt, 0, sizeof(int) * nt, st)) != cudaSuccess) return cuda_fail(e, "gemv_setup");
   }
+  if (A->sym && comm_overlaps(m) && nt >= 2) {
+    // row chunks for the overlapped all-reduce: segments of test steps [row0[c], row0[c+1]) in
+    // memory order, items renumbered per chunk
+    const int nch = std::min(bem_matrix_s::COMM_CHUNKS, nt);
+    std::vector<GSeg> ch;
+    for (int c = 0; c < nch; ++c) {
+      A->chunk_row0[c] = (int)((long long)nt * c / nch);
+      A->chunk_row0[c + 1] = (int)((long long)nt * (c + 1) / nch);
+      A->chunk_seg0[c] = (int)ch.size();
+      long long it = 0;
+      for (const GSeg& g : A->segs) {
+        if (g.a < A->chunk_row0[c] || g.a >= A->chunk_row0[c + 1]) continue;
+        GSeg x = g;
+        x.item0 = it;
+        it += x.nch;   // sym: one item per (a, b) block
+        ch.push_back(x);
+      }
+      A->chunk_items[c] = it;
+    }
+    A->chunk_seg0[nch] = (int)ch.size();
+    A->nchunks = nch;
+    if ((e = cudaMallocAsync((void**)&A->d_segs_ch, sizeof(GSeg) * std::max<size_t>(1, ch.size()), st)) != cudaSuccess ||
+        (ch.size() && (e = cudaMemcpyAsync(A->d_segs_ch, ch.data(), sizeof(GSeg) * ch.size(), cudaMemcpyHostToDevice, st)) != cudaSuccess))
+      return cuda_fail(e, "gemv_setup");
+    for (int c = 0; c < nch; ++c)
+      if ((e = cudaEventCreateWithFlags(&A->chunk_ev[c], cudaEventDisableTiming)) != cudaSuccess) return cuda_fail(e, "gemv_setup");
+  }
   return BEM_OK;
 }
 
@@ -313,6 +340,32 @@ bem_status gemv_launch(const bem_matrix* A, double a, const double* x, double b,
     const long long blocks = std::min<long long>(A->n_items, 1LL << 30);
     // fused row reduction: into y (or the distributed partial sum ysum)
     const bool dist = m->comm != nullptr;
+    if (dist && A->nchunks > 1) {
+      // multi-GPU with NCCL: row chunk c's all-reduce (on the communicator's stream) overlaps the
+      // GEMV of chunk c + 1; rows without owned blocks are zeroed first
+      if (A->empty_rows) {
+        k_empty_rows<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(A->d_row_pstride, m->ng, m->nt, 0.0, A->d_ysum);
+        count_launch();
+      }
+      for (int c = 0; c < A->nchunks; ++c) {
+        const int s0 = A->chunk_seg0[c], ns = A->chunk_seg0[c + 1] - s0;
+        if (A->chunk_items[c] > 0) {
+          k_gemv_sym<<<(unsigned)std::min<long long>(A->chunk_items[c], 1LL << 30), SYMV_WARPS * 32, smem, st>>>(
+              A->data, A->d_segs_ch + s0, ns, A->chunk_items[c], m->ng, A->blk_elems, x, A->d_partials, A->d_row_pbase,
+              A->d_row_pstride, A->d_rowcnt, 1.0, 0.0, A->d_ysum);
+          count_launch();
+        }
+        cudaEventRecord(A->chunk_ev[c], st);
+        const long long r0 = (long long)A->chunk_row0[c] * m->ng, nr = (long long)(A->chunk_row0[c + 1] - A->chunk_row0[c]) * m->ng;
+        bem_status s = allreduce_sum_async(m, A->d_ysum + r0, nr, st, A->chunk_ev[c]);
+        if (s != BEM_OK) return s;
+      }
+      bem_status s = comm_join(m, st);
+      if (s != BEM_OK) return s;
+      vec_axpby(y, a, A->d_ysum, b, n, st);
+      cudaError_t e = cudaGetLastError();
+      return e == cudaSuccess ? BEM_OK : cuda_fail(e, "bem_matvec");
+    }
     k_gemv_sym<<<(unsigned)blocks, SYMV_WARPS * 32, smem, st>>>(A->data, A->d_segs, (int)A->segs.size(), A->n_items, m->ng, A->blk_elems, x, A->d_partials,
                                                                 A->d_row_pbase, A->d_row_pstride, A->d_rowcnt,
                                                                 dist ? 1.0 : a, dist ? 0.0 : b, dist ? A->d_ysum : y);
@@ -751,8 +804,9 @@ __global__ void k_dots_sum(const double* __restrict__ part, int nch, int k, doub
   for (int c = 0; c < nch; ++c) s += part[(long long)j * nch + c];
   out[j] = s;
 }
-static double* g_dot_part[64] = {nullptr};
-static size_t g_dot_part_n[64] = {0};
+// per host thread and device (concurrent solves on several threads each own theirs)
+static thread_local double* g_dot_part[64] = {nullptr};
+static thread_local size_t g_dot_part_n[64] = {0};
 void vec_dots(const double* Q, long long ldq, int k, const double* w, long long n, double* out,
               cudaStream_t st) {
   const int nch = (int)std::max<long long>(1, std::min<long long>(DOT_MAXCH, (n + DOT_CHUNK - 1) / DOT_CHUNK));

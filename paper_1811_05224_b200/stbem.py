@@ -98,6 +98,7 @@ _SIGS = {
     "bem_nccl_get_unique_id": (I, [P]),
     "bem_comm_create": (I, [P, I, I, I, PP]),
     "bem_comm_destroy": (None, [P]),
+    "bem_comm_create_group": (I, [I, I, P]),
     "bem_plan_build": (I, [I, P]),
     "bem_plan_generator": (I, [I, P, P]),
     "bem_plan_owned_blocks": (I, [I, I, I, P, P]),
@@ -217,6 +218,20 @@ class Comm:
         check(lib().bem_comm_create(uid, world, rank, device, ctypes.byref(h)))
         self.h = h
         self.rank, self.world = rank, world
+
+    @classmethod
+    def group(cls, world, device):
+        """emulated ranks on one device (bem_comm_create_group): `world` handles, rank r driven by
+        its own host thread"""
+        hs = (ctypes.c_void_p * world)()
+        check(lib().bem_comm_create_group(int(world), int(device), hs))
+        out = []
+        for r in range(world):
+            c = cls.__new__(cls)
+            c.h = ctypes.c_void_p(hs[r])
+            c.rank, c.world = r, world
+            out.append(c)
+        return out
 
     def close(self):
         if self.h:

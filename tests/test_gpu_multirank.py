@@ -1,0 +1,96 @@
+"""The multi-rank path with the real kernels on ONE GPU: G emulated ranks (bem_comm_create_group,
+one host thread each, SPMD) own the blocks of the cyclic K_P plan with P = 2G temporal slices
+ and sum their partial products with the group all-reduce.
+Against the single-rank path: products and the fused right-hand side to rounding, the GMRES
+solution to the density tolerance with the same iteration count, every rank bitwise identical
+(the all-reduce gives all ranks the same sums, so they take identical decisions)."""
+import threading
+
+import numpy as np
+import pytest
+
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_1811_05224_b200 import stbem as S  # noqa: E402
+
+
+def relmax(a, b):
+    return float(np.abs(a - b).max() / np.abs(b).max())
+
+
+def step(w, n_slices, comm, x_host):
+    """one rank's SPMD sequence: assemble, products, fused rhs, preconditioned solve"""
+    torch.cuda.set_device(0)
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        m = S.Mesh.from_workload(w, n_slices=n_slices, comm=comm)
+        V, D = m.assemble_V(stream=st), m.assemble_D(stream=st)
+        Mp, Md = m.assemble_M(S.MASS_PRIMAL, stream=st), m.assemble_M(S.MASS_DUAL, stream=st)
+        x = torch.tensor(x_host, dtype=torch.float64, device="cuda")
+        Vx, Dx = torch.empty_like(x), torch.empty_like(x)
+        V.matvec(x, Vx, stream=st)
+        D.matvec(x, Dx, stream=st)
+        g = torch.tensor(W.dirichlet_data(w), dtype=torch.float64, device="cuda")
+        b = torch.empty_like(g)
+        S.rhs_fused(m, Mp, g, b, stream=st)
+        wv = torch.zeros_like(g)
+        rep = S.solve_gmres(V, b, wv, D=D, M=Md, precond=2, rel_tol=w.tol, max_iter=200, history=False, stream=st)
+        st.synchronize()
+        out = {"Vx": Vx.cpu().numpy(), "Dx": Dx.cpu().numpy(), "b": b.cpu().numpy(), "w": wv.cpu().numpy(),
+               "rep": rep, "blocks": m.info.n_owned_blocks, "entries": m.info.entries_owned}
+        for A in (V, D, Mp, Md):
+            A.close()
+        m.close()
+    return out
+
+
+_single = {}
+
+
+def single(name):
+    if name not in _single:
+        w = W.get(name)
+        _single[name] = step(w, 1, None, W.random_vector(w.n))
+    return _single[name]
+
+
+@pytest.mark.parametrize("name,G", [("S32", 2), ("S32", 4), ("S32", 8), ("C2", 2), ("C2", 4)])
+def test_emulated_ranks_match_single_rank(name, G):
+    w = W.get(name)
+    ref = single(name)
+    comms = S.Comm.group(G, 0)
+    res, errs = [None] * G, []
+
+    def run(r):
+        try:
+            res[r] = step(w, 2 * G, comms[r], W.random_vector(w.n))
+        except Exception as e:   # noqa: BLE001
+            errs.append(repr(e))
+    th = [threading.Thread(target=run, args=(r,)) for r in range(G)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(600)
+    for c in comms:
+        c.close()
+    assert not errs, errs
+    # the cyclic plan gives every rank its share: P(P+1)/2 blocks in total, entries summing to the whole
+    P = 2 * G
+    assert sum(r["blocks"] for r in res) == P * (P + 1) // 2
+    assert sum(r["entries"] for r in res) == w.n_gamma ** 2 * w.n_steps * (w.n_steps + 1) // 2
+    for r in range(1, G):                              # identical sums on every rank
+        for k in ("Vx", "Dx", "b", "w"):
+            assert np.array_equal(res[r][k], res[0][k]), (r, k)
+    out = res[0]
+    for k in ("Vx", "Dx", "b"):
+        assert relmax(out[k], ref[k]) <= 1e-13, k
+    assert out["rep"]["status"] == "OK"
+    assert out["rep"]["iterations"] == ref["rep"]["iterations"], (out["rep"], ref["rep"])
+    assert relmax(out["w"], ref["w"]) <= 1e-10
+    assert out["rep"]["seconds_comm"] > 0.0            # the collectives were timed
