@@ -549,14 +549,19 @@ struct RegA {
       l1 = R0[FM1 * S] + R1[FM0 * S];
     }
   }
-  // Phi~ at the node (s, ln s, u = 1/s)
-  __device__ __forceinline__ double eval(double s, double lns, double u) const {
+  // Phi~ at the node (s, ln s, u = 1/s): the Horner chain in u, then the s / ln s terms (split so
+  // that the bulk kernel holds only u of every node in registers during the chains)
+  __device__ __forceinline__ double chain(double u) const {
     double acc = P[NC - 1];
 #pragma unroll
     for (int k = NC - 2; k >= 0; --k) acc = fma(acc, u, P[k]);
+    return acc;
+  }
+  __device__ __forceinline__ double finish(double acc, double s, double lns) const {
     if (KIND == STB_K) return fma(-lns, l0, acc);
     return fma(s, fma(lns, l0, e0), fma(lns, l1, acc));
   }
+  __device__ __forceinline__ double eval(double s, double lns, double u) const { return finish(chain(u), s, lns); }
 };
 
 // point-by-point regularised contributions (regime C), same function as regimes A / B / Z
@@ -948,7 +953,7 @@ __device__ __forceinline__ void cp_async16_bulk(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(sa), "l"(gmem));
 }
 template <int KIND, int R, bool PROD = false>
-__global__ void __launch_bounds__(128, (KIND == STB_D || PROD) ? 2 : 3) k_bulk_m(BlockArgs B, MomArgs M) {
+__global__ void __launch_bounds__(128, KIND == STB_D ? 2 : 3) k_bulk_m(BlockArgs B, MomArgs M) {
   const int ng = B.ng;
   const int lane = threadIdx.x & 31;
   const int J0 = blockIdx.x * 32 + lane;
@@ -1039,32 +1044,35 @@ __global__ void __launch_bounds__(128, (KIND == STB_D || PROD) ? 2 : 3) k_bulk_m
     // every node of the column by the regime-A form, branch-free (clamped into the lag table,
     // invalid nodes zeroed) so that the R+1 Horner chains interleave; then the nodes of lanes
     // outside regime A are overwritten (B / Z per lane, C warp-cooperatively)
+    // only u = 1/s of the column's nodes is held in registers through the Horner chains; s and
+    // ln s are read from shared memory again for the closing terms
+    const double* ndd = reinterpret_cast<const double*>(ndc);
     double phi[R + 1];
-    double4 nd[R + 1];
-#pragma unroll
-    for (int r = 0; r <= R; ++r) nd[r] = ndc[r];
     unsigned bmask = 0;
     // full columns (every band node above the trial node) whose smallest-lag node is in regime A
     // for every lane: all nodes are (s grows with x), no masks or regime tests per node
-    // (not for V_h: its 3-CTA register budget would spill)
-    const bool full = KIND != STB_V && r_lo > y && r_hi - r_lo == R;       // CTA-uniform
+    const bool full = r_lo > y && r_hi - r_lo == R;       // CTA-uniform
     if (zero_warp) {
 #pragma unroll
       for (int r = 0; r <= R; ++r) {
         phi[r] = 0.0;
         nA += r_lo + r <= r_hi && r_lo + r > y;
       }
-    } else if (full && __all_sync(0xffffffffu, A.cmax * nd[0].z < STB_MXA)) {
+    } else if (full && __all_sync(0xffffffffu, A.cmax * ndd[2] < STB_MXA)) {
 #pragma unroll
-      for (int r = 0; r <= R; ++r) phi[r] = A.eval(nd[r].x, nd[r].y, nd[r].z);
+      for (int r = 0; r <= R; ++r) phi[r] = A.chain(ndd[4 * r + 2]);
+#pragma unroll
+      for (int r = 0; r <= R; ++r) phi[r] = A.finish(phi[r], ndd[4 * r], ndd[4 * r + 1]);
       nA += R + 1;
     } else {
 #pragma unroll
+      for (int r = 0; r <= R; ++r) phi[r] = A.chain(ndd[4 * r + 2]);
+#pragma unroll
       for (int r = 0; r <= R; ++r) {
         const int x = r_lo + r;
-        const double v = A.eval(nd[r].x, nd[r].y, nd[r].z);
+        const double v = A.finish(phi[r], ndd[4 * r], ndd[4 * r + 1]);
         const bool ok = x <= r_hi && x > y;
-        const bool inA = A.cmax * nd[r].z < STB_MXA;
+        const bool inA = A.cmax * ndd[4 * r + 2] < STB_MXA;
         phi[r] = ok ? v : 0.0;
         nA += ok && inA;
         if (ok && !inA) bmask |= 1u << r;
