@@ -183,7 +183,7 @@ long long entry_offset(const bem_matrix* A, int a, int i, int b, int j) {
     if (B.I == I && B.J == J) {
       const long long p0 = A->poff[A->poff_base[bi] + (a - B.a0)];
       if (A->sym) {
-        if (i / SYM_TS > j / SYM_TS) std::swap(i, j);   // the lower tile triangle mirrors the upper
+        if (!sym_stored(i, j)) std::swap(i, j);   // the lower triangle mirrors the stored upper one
         return p0 + (long long)(b - B.b0) * A->blk_elems + sym_in_block(i, j, sym_nt(m->ng));
       }
       long long ld = pad4((long long)panel_nb(a, B.b0, B.b1) * m->ng);
@@ -692,10 +692,7 @@ bem_status bem_matrix_info(const bem_matrix* A, int* kind, long long* entries, l
     // distinct stored entries (sym: the entries (i, j) with i / 32 <= j / 32, i, j < N_Gamma)
     const bem_mesh* m = A->mesh;
     long long per_block = (long long)m->ng * m->ng;
-    if (A->sym) {
-      per_block = 0;
-      for (int i = 0; i < m->ng; ++i) per_block += m->ng - (i / SYM_TS) * SYM_TS;
-    }
+    if (A->sym) per_block = (long long)m->ng * (m->ng + 1) / 2;   // (i, j), i <= j
     for (auto& b : blocks_of(A))
       for (int a = b.a0; a < b.a1; ++a) ent += per_block * panel_nb(a, b.b0, b.b1);
   } else {

@@ -67,7 +67,7 @@ struct BlockArgs {
   double ell;             // sqrt(4 min h_t / alpha): composite singular rules when h > ell
 };
 
-// sym: the caller guarantees i / 32 <= j / 32 (the upper tile triangle)
+// sym: the caller guarantees sym_stored(i, j)
 __device__ __forceinline__ double* entry_ptr(const BlockArgs& B, int a, int i, int b, int j) {
   if (B.sym) return B.out + B.poff[a - B.a0] + (long long)(b - B.b0) * B.blk + sym_in_block(i, j, B.nt);
   long long ld = pad4((long long)panel_nb(a, B.b0, B.b1) * B.ng);
@@ -290,7 +290,7 @@ __global__ void __launch_bounds__(128) k_sing(BlockArgs B, const Seg* __restrict
           add += nn * pair_touching<1>(X, Y, rel, Lg, alpha, nsing, vl[m][0], vl[m][1], vk[nn_][0], vk[nn_][1], B.ell);
       }
   }
-  if ((threadIdx.x & 31) == 0 && !(B.sym && i / SYM_TS > jcol / SYM_TS)) *entry_ptr(B, a, i, b, jcol) += add;
+  if ((threadIdx.x & 31) == 0 && !(B.sym && !sym_stored(i, jcol))) *entry_ptr(B, a, i, b, jcol) += add;
 }
 
 // ================================================================= launch

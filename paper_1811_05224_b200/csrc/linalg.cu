@@ -135,17 +135,26 @@ __global__ void __launch_bounds__(SYMV_WARPS * 32) k_gemv_sym(const double* __re
     int ti = 0, tj = w;                                // tile t = w in row-major upper order
     while (tj >= nt && ti < nt) { tj -= nt - ti - 1; ++ti; }   // w >= ntp: ti reaches nt, no tile
     for (int t = w; t < ntp; t += SYMV_WARPS) {
-      const double* __restrict__ tp = blkp + (long long)t * (SYM_TS * SYM_TS);
+      const double* __restrict__ tp = blkp + sym_tile_offset(ti, tj, nt);
       const bool cok = tj * SYM_TS + lane < ng;
       double v[32];
-#pragma unroll
-      for (int r = 0; r < 32; ++r) v[r] = (cok && ti * SYM_TS + r < ng) ? __ldcs(tp + r * SYM_TS + lane) : 0.0;
+      double s = 0.0;
       if (ti != tj) {
-        double s = 0.0;
+#pragma unroll
+        for (int r = 0; r < 32; ++r) v[r] = (cok && ti * SYM_TS + r < ng) ? __ldcs(tp + r * SYM_TS + lane) : 0.0;
+        // T^T x_b[ti] -> y_a[tj] (column sums)
 #pragma unroll
         for (int r = 0; r < 32; ++r) s = fma(v[r], xs[ti * SYM_TS + r], s);
-        yw[tj * SYM_TS + lane] += s;
+      } else {
+        // diagonal tile, upper triangle stored (row r: columns r..31): the row sums below give
+        // sum_{c >= r} T[r][c] x[c]; the strictly upper part transposed adds sum_{r < c} T[r][c] x[r]
+#pragma unroll
+        for (int r = 0; r < 32; ++r)
+          v[r] = (cok && r <= lane && ti * SYM_TS + r < ng) ? __ldcs(tp + sym_row_base(r, true) + lane) : 0.0;
+#pragma unroll
+        for (int r = 0; r < 32; ++r) s = fma(r < lane ? v[r] : 0.0, xs[ti * SYM_TS + r], s);
       }
+      yw[tj * SYM_TS + lane] += s;
       const double xj = xs[tj * SYM_TS + lane];
 #pragma unroll
       for (int r = 0; r < 32; ++r) v[r] *= xj;

@@ -998,12 +998,14 @@ __global__ void __launch_bounds__(128, KIND == STB_D ? 2 : 3) k_bulk_m(BlockArgs
   long long* srow = s_row[threadIdx.x >> 5];
   if (!PROD && lane < R) {
     const int a = min(r_lo + lane, r_hi - 1);
-    srow[lane] = B.poff[a - B.a0] + (B.sym ? sym_tile_index(ti, tj, B.nt) * (SYM_TS * SYM_TS) + (long long)(I % SYM_TS) * SYM_TS
+    srow[lane] = B.poff[a - B.a0] + (B.sym ? sym_tile_offset(ti, tj, B.nt) + sym_row_base(I % SYM_TS, ti == tj)
                                            : (long long)I * pad4((long long)panel_nb(a, B.b0, B.b1) * ng));
   }
   __syncwarp();
   const long long cstride = B.sym ? B.blk : (long long)ng;   // per trial step b
   const int jcol = B.sym ? J % SYM_TS : J;
+  // stores: diagonal tiles of the symmetric packing keep their upper triangle only
+  const bool vst = valid && (!B.sym || ti != tj || jcol >= I % SYM_TS);
   RegA<KIND> A;
   A.load(M.rec + pair, S);
   // pairs without quadrature points (K_h on collinear elements: the kernel vanishes) hold
@@ -1152,7 +1154,7 @@ __global__ void __launch_bounds__(128, KIND == STB_D ? 2 : 3) k_bulk_m(BlockArgs
         }
       } else {
         double* col = B.out + ((long long)(b - B.b0) * cstride + jcol);
-        if (interior && valid) {
+        if (interior && vst) {
 #pragma unroll
           for (int r = 1; r <= R; ++r) {
             const double G = phi[r] - phi[r - 1];
@@ -1164,7 +1166,7 @@ __global__ void __launch_bounds__(128, KIND == STB_D ? 2 : 3) k_bulk_m(BlockArgs
           for (int r = 1; r <= R; ++r) {
             const int a = r_lo + r - 1;
             const double G = phi[r] - phi[r - 1];
-            if (valid && a < r_hi && a - b >= 2) col[srow[r - 1]] = Gp[r - 1] - G;
+            if (vst && a < r_hi && a - b >= 2) col[srow[r - 1]] = Gp[r - 1] - G;
             Gp[r - 1] = G;
           }
         }
@@ -1262,10 +1264,11 @@ __global__ void __launch_bounds__(128) k_near_m(BlockArgs B, MomArgs M, int chun
       if (lane == 0 && (d0 || d1) && I0 < ng)
         B.part[B.pbase + ((long long)(a - B.a0) * ng + I) * B.pslots + B.ntile + blockIdx.x] = c;
     } else {
-      if (d0 && valid) *entry_ptr(B, a, I, a, J) = p10;
+      const bool vst = valid && (!B.sym || sym_stored(I, J));
+      if (d0 && vst) *entry_ptr(B, a, I, a, J) = p10;
       if (d1) {
         const double p20 = node(a + 1, a - 1);
-        if (valid) *entry_ptr(B, a, I, a - 1, J) = p20 - prev - p10;
+        if (vst) *entry_ptr(B, a, I, a - 1, J) = p20 - prev - p10;
       }
     }
     prev = p10;
@@ -1427,7 +1430,7 @@ __global__ void __launch_bounds__(128) k_sing_m(BlockArgs B, MomArgs M, int chun
   const int I = (int)(rid / 5), jo = (int)(rid % 5);
   if ((KIND == STB_V && (jo == 0 || jo == 4)) || (KIND == STB_K && jo == 0)) return;
   const int J = (I + jo - 2 + M.ng) % M.ng;
-  if (B.sym && I / SYM_TS > J / SYM_TS) return;   // mirror of the stored entry (J, I)
+  if (B.sym && !sym_stored(I, J)) return;   // mirror of the stored entry (J, I)
   const int a_beg = B.a0 + blockIdx.y * chunk;
   const int a_end = min(B.a1, a_beg + chunk);
   const long long S = M.npairs;
