@@ -116,6 +116,7 @@ __global__ void __launch_bounds__(SYMV_WARPS * 32) k_gemv_sym(const double* __re
   const int nt = sym_nt(ng), L = nt * SYM_TS, ntp = nt * (nt + 1) / 2;
   double* xs = sm;
   double* ys = sm + L;
+  double* ds = ys + SYMV_WARPS * L;                    // per-warp diagonal-tile scratch (SYM_TD each)
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   double* yw = ys + w * L;
   for (long long it = blockIdx.x; it < n_items; it += gridDim.x) {
@@ -146,11 +147,19 @@ __global__ void __launch_bounds__(SYMV_WARPS * 32) k_gemv_sym(const double* __re
 #pragma unroll
         for (int r = 0; r < 32; ++r) s = fma(v[r], xs[ti * SYM_TS + r], s);
       } else {
-        // diagonal tile, upper triangle stored (row r: columns r..31): the row sums below give
-        // sum_{c >= r} T[r][c] x[c]; the strictly upper part transposed adds sum_{r < c} T[r][c] x[r]
+        // diagonal tile, upper triangle stored (row r: columns r..31): read as 17 full-warp
+        // coalesced loads into the warp's shared scratch (32 masked row loads would issue as many
+        // load instructions as a full tile for half the bytes), then row by row.  The row sums below
+        // give sum_{c >= r} T[r][c] x[c]; the strictly upper part transposed adds sum_{r < c} T[r][c] x[r]
+        double* dsm = ds + w * SYM_TD;
+#pragma unroll
+        for (int k = 0; k < (SYM_TD + 31) / 32; ++k)
+          if (k * 32 + lane < SYM_TD) dsm[k * 32 + lane] = __ldcs(tp + k * 32 + lane);
+        __syncwarp();
 #pragma unroll
         for (int r = 0; r < 32; ++r)
-          v[r] = (cok && r <= lane && ti * SYM_TS + r < ng) ? __ldcs(tp + sym_row_base(r, true) + lane) : 0.0;
+          v[r] = (cok && r <= lane && ti * SYM_TS + r < ng) ? dsm[sym_row_base(r, true) + lane] : 0.0;
+        __syncwarp();
 #pragma unroll
         for (int r = 0; r < 32; ++r) s = fma(r < lane ? v[r] : 0.0, xs[ti * SYM_TS + r], s);
       }
@@ -345,7 +354,14 @@ bem_status gemv_launch(const bem_matrix* A, double a, const double* x, double b,
   const bem_mesh* m = A->mesh;
   const long long n = (long long)m->ng * m->nt;
   if (A->n_items > 0 && A->sym) {
-    const size_t smem = sizeof(double) * (1 + SYMV_WARPS) * sym_nt(m->ng) * SYM_TS;
+    const size_t smem = sizeof(double) * ((1 + SYMV_WARPS) * sym_nt(m->ng) * SYM_TS + SYMV_WARPS * SYM_TD);
+    // x, per-warp y and diagonal scratch exceed the default 48 KB beyond N_Gamma ~ 900: opt in
+    static size_t smem_set = 48 * 1024;
+    if (smem > smem_set) {
+      if (cudaFuncSetAttribute(k_gemv_sym, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return cuda_fail(cudaGetLastError(), "bem_matvec: shared memory for this N_Gamma");
+      smem_set = smem;
+    }
     const long long blocks = std::min<long long>(A->n_items, 1LL << 30);
     // fused row reduction: into y (or the distributed partial sum ysum)
     const bool dist = m->comm != nullptr;
