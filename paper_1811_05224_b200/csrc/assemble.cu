@@ -335,8 +335,9 @@ static void launch_records(const MomArgs& MB, const MomArgs& MN, const MomArgs* 
   // orders, skipped sub-pairs) warp per pair, the others thread per pair (k_records near_special)
   k_records<KIND, false><<<nblk, 128, 0, st>>>(MB);
   if (KIND == STB_D) {
+    cudaMemsetAsync(MN.list, 0, sizeof(int), st);
     k_records<KIND, true, true><<<nblk, 128, 0, st>>>(MN);
-    k_records_warp<KIND, true, true><<<(unsigned)((MN.npairs * 32 + 127) / 128), 128, 0, st>>>(MN);
+    k_records_warp<KIND, true><<<148 * 2, 128, 0, st>>>(MN);   // persistent: the resident warps walk the list
     count_launch();
   } else {
     k_records<KIND, true><<<nblk, 128, 0, st>>>(MN);
@@ -435,6 +436,11 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, const Qua
   }
   double* d_rec = nullptr;
   unsigned long long* d_ctr = nullptr;
+  int* d_list = nullptr;   // D_h near records: the near_special pairs
+  if (kind == STB_D && (e = cudaMallocAsync((void**)&d_list, sizeof(int) * (npairs + 1), st)) != cudaSuccess) {
+    cudaFreeAsync(d_poff, st);
+    return cuda_fail(e, "assemble/list");
+  }
   const size_t rec_bytes = sizeof(double) * ((size_t)nf * (npairs + nsrec) + (size_t)nfn * npairs);
   if ((e = storage_acquire(m->device, rec_bytes, st, (void**)&d_rec)) != cudaSuccess ||
       (e = cudaMallocAsync((void**)&d_ctr, sizeof(unsigned long long) * 15, st)) != cudaSuccess ||
@@ -463,6 +469,7 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, const Qua
   MB.ell = m->htmin > 0.0 ? std::sqrt(4.0 * m->htmin / m->alpha) : 0.0;
   MomArgs MN = MB;
   MN.rec = d_rec + (long long)nf * npairs;
+  MN.list = d_list;
   // the near cells' nodes: s = t_{a+1} - t_a and t_{a+1} - t_{a-1} (and t_a - t_{a-1})
   {
     double smin = 1e300, smax = 0.0;
@@ -577,6 +584,7 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, const Qua
     storage_release(m->device, d_part, part_bytes, st);
   }
   storage_release(m->device, d_rec, rec_bytes, st);
+  if (d_list) cudaFreeAsync(d_list, st);
   cudaFreeAsync(d_poff, st);
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "assemble/launch");

@@ -90,6 +90,7 @@ struct MomArgs {
                           // smallest lag; sub-pairs closer than 8 ell get composite rules with
                           // cells of at most ell (no subdivision while kappa <= 1)
   double near_gap;        // near records: distance ratio below which the measured orders apply
+  int* list;              // D_h near records: [0] count, [1..] the near_special pairs (k_records appends)
 };
 
 // composite subdivision of a sub-pair: cells per direction.  R24: pairs
@@ -490,20 +491,25 @@ __device__ __forceinline__ bool near_special(const MomArgs& M, int I, int J) {
   });
   return sp;
 }
-// SPLIT: D_h near records, pairs divided between the two kernels by near_special
+// SPLIT: D_h near records: the thread kernel appends the near_special pairs to M.list (in any
+// order: each pair's record is computed by exactly one warp, so the results do not depend on it)
+// and the persistent warp kernel takes them from the list
 template <int KIND, bool NEAR, bool SPLIT = false>
 __global__ void __launch_bounds__(128) k_records(MomArgs M) {
   const long long pair = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (pair >= M.npairs) return;
-  if (SPLIT && near_special<KIND>(M, (int)(pair / M.ng), (int)(pair % M.ng))) return;
+  if (SPLIT && near_special<KIND>(M, (int)(pair / M.ng), (int)(pair % M.ng))) {
+    M.list[1 + atomicAdd(M.list, 1)] = (int)pair;
+    return;
+  }
   records_body<KIND, NEAR, false>(M, pair, 0);
 }
-template <int KIND, bool NEAR, bool SPLIT = false>
+template <int KIND, bool NEAR>
 __global__ void __launch_bounds__(128) k_records_warp(MomArgs M) {
-  const long long pair = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (pair >= M.npairs) return;   // warp-uniform
-  if (SPLIT && !near_special<KIND>(M, (int)(pair / M.ng), (int)(pair % M.ng))) return;   // warp-uniform
-  records_body<KIND, NEAR, true>(M, pair, threadIdx.x & 31);
+  const int nw = (int)((gridDim.x * blockDim.x) >> 5);
+  const int n = *(volatile int*)M.list;
+  for (int k = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); k < n; k += nw)   // warp-uniform
+    records_body<KIND, NEAR, true>(M, M.list[1 + k], threadIdx.x & 31);
 }
 
 __device__ __forceinline__ double warp_sum(double v) {
