@@ -380,12 +380,14 @@ def native(args):
     cells = nt_ * (nt_ + 1) / 2
     bulk_entries = stats[kdom]["entries"] * (cells - (2 * nt_ - 1)) / cells   # stored entries of cells d >= 2
     store_gbs = 8.0 * bulk_entries / (ms_dom * 1e-3) / 1e9
+    # ncu dram__bytes_read.sum + dram__bytes_write.sum per launch of the same kernel on the same
+    # config (profiles/traffic.json, from the committed ncu summaries), None where not captured
     traffic = {}
-    tpath = os.path.join(ROOT, "profiles", "r01_traffic.json")
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
-        for kname, tj in json.load(open(tpath)).items():
+        for tj in json.load(open(tpath))["entries"]:
             if tj.get("config") == args.config:
-                traffic[kname] = tj["traffic_bytes_per_launch"]
+                traffic[tj["kernel"]] = tj["traffic_bytes_per_launch"]
     roof_asm = {"bound": "alu", "kernel": f"k_bulk_m<{kdom}>", "achieved": achieved, "peak": FP64_PEAK_DERIVED,
                 "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_DERIVED,
                 "traffic": traffic.get(f"k_bulk_m<{kdom}>"),

@@ -5,7 +5,9 @@ from collections import defaultdict
 path = sys.argv[1]
 out = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(out.splitlines()))
-h = rows[1]
+hi = next(i for i, r in enumerate(rows) if "Address" in r)
+h = rows[hi]
+rows = rows[hi - 1:]
 ia, isrc = h.index("Address"), h.index("Source")
 iss, iex = h.index("Warp Stall Sampling (All Samples)"), h.index("Instructions Executed")
 recs = [(int(r[ia], 16), r[isrc].strip(), int(r[iss] or 0), int(r[iex] or 0)) for r in rows[2:] if len(r) == len(h)]
