@@ -688,6 +688,40 @@ def test_bench_step_configuration_against_golden(name):
         A.close()
 
 
+def test_c5_leading_steps_against_golden():
+    """the headline configuration (C5: L-shape, graded steps, N = 98 304) solved in the bench's
+    launch configuration, against the oracle's exact density of the first 24 time steps (block
+    forward substitution over the oracle's causal blocks, oracle/gen_golden.py C5; V_h is block
+    lower triangular, so those steps depend on nothing else): b and w of those steps"""
+    path = os.path.join(GOLDEN, "C5_oracle_w_first24.npy")
+    if not os.path.exists(path):
+        pytest.skip("tests/golden/C5_oracle_w_first24.npy missing (python -m oracle.gen_golden C5)")
+    wd = np.load(path)
+    bd = np.load(os.path.join(GOLDEN, "C5_oracle_b_first24.npy"))
+    w = W.get("C5")
+    k = len(wd)
+    m = S.Mesh.from_workload(w)
+    side = (torch.cuda.Stream(), torch.cuda.Stream())
+    cur = torch.cuda.current_stream()
+    for s_ in side:
+        s_.wait_stream(cur)
+    V = m.assemble_V(stream=side[0])
+    D = m.assemble_D(stream=side[1])
+    Mp, Md = m.assemble_M(S.MASS_PRIMAL), m.assemble_M(S.MASS_DUAL)
+    g = cuda(W.dirichlet_data(w))
+    b = torch.empty_like(g)
+    S.rhs_fused(m, Mp, g, b)
+    for s_ in side:
+        cur.wait_stream(s_)
+    wv = torch.zeros_like(g)
+    rep = S.solve_gmres(V, b, wv, D=D, M=Md, precond=2, rel_tol=w.tol, history=False)
+    assert rep["status"] == "OK"
+    assert relmax(b.cpu().numpy()[:k], bd) <= MAT_TOL
+    assert relmax(wv.cpu().numpy()[:k], wd) <= W_TOL
+    for A in (V, D, Mp, Md):
+        A.close()
+
+
 @pytest.mark.parametrize("name", ["C3", "C5"])
 def test_full_size_step_properties(name):
     """BJ configs at full size in the bench's launch configuration, checked through properties
