@@ -3,6 +3,7 @@
 //     deterministic two-level sum; no tensor cores: a single right-hand side is not a contraction)
 //   * mass matrices: apply, lumped scaling, cyclic-tridiagonal solves (one system per time step)
 //   * Krylov vector kernels (block dot products, updates) with fixed reduction order
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -554,6 +555,129 @@ __global__ void __launch_bounds__(256, 2) k_toeplitz_mm(const double* __restrict
         if (i < ng && a < nt) part[(long long)chunk * n + (long long)a * ng + i] = acc[u][v][e];
       }
 }
+// TMA version (sm_100a Tensor Memory Accelerator): the T and X tiles of a K step are fetched by
+// two cp.async.bulk.tensor copies issued by one thread, completion signalled on the stage's
+// mbarrier (expect_tx of the tile bytes; out-of-range rows / columns and the causal x columns
+// b < 0 are zero-filled by the TMA unit), 128-byte swizzled in shared memory so that the DMMA
+// fragment loads (8 rows x 16 B per quarter warp) stay conflict-free without row padding.  Same
+// tiles, work units, warp layout and k order as k_toeplitz_mm.
+constexpr int TZ_TSTAGE = (TZ_TI + TZ_TA) * TZ_TK;                 // doubles per stage
+constexpr size_t TZ_TMA_SMEM = sizeof(double) * TZ_STAGES * TZ_TSTAGE + 1024 + 64;
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" :: "r"(bar), "r"(parity) : "memory");
+}
+// element (r, k) of a swizzled tile of 16-double rows: the 16-byte chunk k / 2 XOR (r mod 8)
+__device__ __forceinline__ const double2* swz(const double* base, int r, int k) {
+  return reinterpret_cast<const double2*>(base + r * TZ_TK + ((((k >> 1) ^ (r & 7))) << 1));
+}
+__global__ void __launch_bounds__(256, 2) k_toeplitz_tma(const __grid_constant__ CUtensorMap tmT,
+                                                     const __grid_constant__ CUtensorMap tmX, int ng, int nt,
+                                                     int dpz, double* __restrict__ part) {
+  extern __shared__ __align__(16) unsigned char tz_raw[];
+  // 1024-byte aligned stages (the swizzle pattern repeats every 8 rows of 128 B)
+  double* tz = reinterpret_cast<double*>((reinterpret_cast<size_t>(tz_raw) + 1023) & ~size_t(1023));
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(tz + TZ_STAGES * TZ_TSTAGE);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wi = (warp & 3) * (8 * TZ_UI), wa = (warp >> 2) * (8 * TZ_VA), fr = lane & 3, fc = lane >> 2;
+  const int nti = (ng + TZ_TI - 1) / TZ_TI;
+  int r = blockIdx.x, at = 0;
+  for (;; ++at) {
+    const int cnt = nti * ((min(nt, (at + 1) * TZ_TA) + dpz - 1) / dpz);
+    if (r < cnt) break;
+    r -= cnt;
+  }
+  const int chunk = r / nti, i0 = (r % nti) * TZ_TI, a0 = at * TZ_TA;
+  const int d0 = chunk * dpz, d1 = min(min(nt, d0 + dpz), a0 + TZ_TA);
+  const int nj = (ng + TZ_TK - 1) / TZ_TK;
+  const int nsteps = max(0, d1 - d0) * nj;
+  if (tid == 0) {
+    for (int s = 0; s < TZ_STAGES; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_u32(bar + s)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int step) {   // thread 0
+    const int s = step % TZ_STAGES;
+    double* Ts = tz + s * TZ_TSTAGE;
+    double* Xs = Ts + TZ_TI * TZ_TK;
+    const int d = d0 + step / nj, j0 = (step % nj) * TZ_TK;
+    const unsigned b = smem_u32(bar + s);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(b), "r"((unsigned)(sizeof(double) * TZ_TSTAGE)) : "memory");
+    asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+                 :: "r"(smem_u32(Ts)), "l"(reinterpret_cast<unsigned long long>(&tmT)), "r"(j0), "r"(i0), "r"(d), "r"(b)
+                 : "memory");
+    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+                 :: "r"(smem_u32(Xs)), "l"(reinterpret_cast<unsigned long long>(&tmX)), "r"(j0), "r"(a0 - d), "r"(b)
+                 : "memory");
+  };
+  double acc[TZ_UI][TZ_VA][2];
+#pragma unroll
+  for (int u = 0; u < TZ_UI; ++u)
+#pragma unroll
+    for (int v = 0; v < TZ_VA; ++v) acc[u][v][0] = acc[u][v][1] = 0.0;
+  if (tid == 0)
+    for (int k = 0; k < TZ_STAGES - 1 && k < nsteps; ++k) issue(k);
+  for (int step = 0; step < nsteps; ++step) {
+    mbar_wait(smem_u32(bar + step % TZ_STAGES), (unsigned)((step / TZ_STAGES) & 1));
+    __syncthreads();                  // every warp is done with the stage refilled below (step - 1)
+    if (tid == 0 && step + TZ_STAGES - 1 < nsteps) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic reads before async writes
+      issue(step + TZ_STAGES - 1);
+    }
+    const double* Ts = tz + (step % TZ_STAGES) * TZ_TSTAGE;
+    const double* Xs = Ts + TZ_TI * TZ_TK;
+#pragma unroll
+    for (int h = 0; h < TZ_TK / 8; ++h) {
+      double2 af[TZ_UI], bf[TZ_VA];
+#pragma unroll
+      for (int u = 0; u < TZ_UI; ++u) af[u] = *swz(Ts, wi + 8 * u + fc, 4 * fr + 2 * h);
+#pragma unroll
+      for (int v = 0; v < TZ_VA; ++v) bf[v] = *swz(Xs, wa + 8 * v + fc, 4 * fr + 2 * h);
+#pragma unroll
+      for (int u = 0; u < TZ_UI; ++u)
+#pragma unroll
+        for (int v = 0; v < TZ_VA; ++v) dmma_8x8x4(acc[u][v], af[u].x, bf[v].x);
+#pragma unroll
+      for (int u = 0; u < TZ_UI; ++u)
+#pragma unroll
+        for (int v = 0; v < TZ_VA; ++v) dmma_8x8x4(acc[u][v], af[u].y, bf[v].y);
+    }
+  }
+  const long long n = (long long)nt * ng;
+#pragma unroll
+  for (int u = 0; u < TZ_UI; ++u)
+#pragma unroll
+    for (int v = 0; v < TZ_VA; ++v)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int i = i0 + wi + 8 * u + fc, a = a0 + wa + 8 * v + 2 * fr + e;
+        if (i < ng && a < nt) part[(long long)chunk * n + (long long)a * ng + i] = acc[u][v][e];
+      }
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+    cudaGetLastError();
+  }
+  return fn;
+}
+
 __global__ void k_toeplitz_reduce(const double* __restrict__ part, int nsplit, long long n, double alpha,
                                   double beta, double* __restrict__ y) {
   const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -598,8 +722,35 @@ bem_status toeplitz_gemv(const bem_matrix* A, double a, const double* x, double 
   cudaError_t e = storage_acquire(m->device, bytes, st, (void**)&part);
   if (e != cudaSuccess) return cuda_fail(e, "toeplitz product");
   e = cudaMemsetAsync(part, 0, bytes, st);   // lag ranges beyond a tile's columns leave their slots zero
-  k_toeplitz_mm<<<(unsigned)nunits, 256, TZ_SMEM, st>>>(A->data, A->poff.size() > 1 ? A->poff[1] - A->poff[0] : 0,
-                                      (int)pad4(ng), x, ng, nt, dpz, part);
+  const long long ldT_d = A->poff.size() > 1 ? A->poff[1] - A->poff[0] : 0;
+  // TMA path: tensor maps of T (j, i, d) and of this product's x (j, b); the strides must be
+  // multiples of 16 bytes (N_Gamma even) and x 16-byte aligned -- otherwise the cp.async kernel
+  static bool tma_attr = false;
+  static const bool no_tma = getenv("BEM_TOEPLITZ_NO_TMA") != nullptr;
+  EncodeTiledFn enc = no_tma ? nullptr : encode_tiled();
+  bool tma = enc && ng % 2 == 0 && ((size_t)x & 15) == 0 && ldT_d > 0 && nt > 1;
+  CUtensorMap tmT, tmX;
+  if (tma) {
+    const cuuint64_t gT[3] = {(cuuint64_t)ng, (cuuint64_t)ng, (cuuint64_t)nt};
+    const cuuint64_t sT[2] = {(cuuint64_t)pad4(ng) * 8, (cuuint64_t)ldT_d * 8};
+    const cuuint32_t bT[3] = {TZ_TK, TZ_TI, 1}, one3[3] = {1, 1, 1};
+    const cuuint64_t gX[2] = {(cuuint64_t)ng, (cuuint64_t)nt};
+    const cuuint64_t sX[1] = {(cuuint64_t)ng * 8};
+    const cuuint32_t bX[2] = {TZ_TK, TZ_TA}, one2[2] = {1, 1};
+    tma = enc(&tmT, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)A->data, gT, sT, bT, one3, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS &&
+          enc(&tmX, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)x, gX, sX, bX, one2, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
+  if (tma) {
+    if (!tma_attr) {
+      cudaFuncSetAttribute(k_toeplitz_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TZ_TMA_SMEM);
+      tma_attr = true;
+    }
+    k_toeplitz_tma<<<(unsigned)nunits, 256, TZ_TMA_SMEM, st>>>(tmT, tmX, ng, nt, dpz, part);
+  } else {
+    k_toeplitz_mm<<<(unsigned)nunits, 256, TZ_SMEM, st>>>(A->data, ldT_d, (int)pad4(ng), x, ng, nt, dpz, part);
+  }
   k_toeplitz_reduce<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(part, nsplit, n, a, b, y);
   count_launch(2);
   storage_release(m->device, part, bytes, st);
