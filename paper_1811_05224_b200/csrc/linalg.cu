@@ -562,7 +562,8 @@ __global__ void __launch_bounds__(256, 2) k_toeplitz_mm(const double* __restrict
 // fragment loads (8 rows x 16 B per quarter warp) stay conflict-free without row padding.  Same
 // tiles, work units, warp layout and k order as k_toeplitz_mm.
 constexpr int TZ_TSTAGE = (TZ_TI + TZ_TA) * TZ_TK;                 // doubles per stage
-constexpr size_t TZ_TMA_SMEM = sizeof(double) * TZ_STAGES * TZ_TSTAGE + 1024 + 64;
+constexpr int TZ_TSTAGES = 4;                                       // TMA pipeline depth
+constexpr size_t TZ_TMA_SMEM = sizeof(double) * TZ_TSTAGES * TZ_TSTAGE + 1024 + 128;
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
   asm volatile(
@@ -581,7 +582,8 @@ __global__ void __launch_bounds__(256, 2) k_toeplitz_tma(const __grid_constant__
   extern __shared__ __align__(16) unsigned char tz_raw[];
   // 1024-byte aligned stages (the swizzle pattern repeats every 8 rows of 128 B)
   double* tz = reinterpret_cast<double*>((reinterpret_cast<size_t>(tz_raw) + 1023) & ~size_t(1023));
-  unsigned long long* bar = reinterpret_cast<unsigned long long*>(tz + TZ_STAGES * TZ_TSTAGE);
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(tz + TZ_TSTAGES * TZ_TSTAGE);   // full
+  unsigned long long* ebar = bar + TZ_TSTAGES;                                                  // empty
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wi = (warp & 3) * (8 * TZ_UI), wa = (warp >> 2) * (8 * TZ_VA), fr = lane & 3, fc = lane >> 2;
   const int nti = (ng + TZ_TI - 1) / TZ_TI;
@@ -596,12 +598,15 @@ __global__ void __launch_bounds__(256, 2) k_toeplitz_tma(const __grid_constant__
   const int nj = (ng + TZ_TK - 1) / TZ_TK;
   const int nsteps = max(0, d1 - d0) * nj;
   if (tid == 0) {
-    for (int s = 0; s < TZ_STAGES; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_u32(bar + s)));
+    for (int s = 0; s < TZ_TSTAGES; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_u32(bar + s)));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 8;" :: "r"(smem_u32(ebar + s)));   // one arrival per warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   auto issue = [&](int step) {   // thread 0
-    const int s = step % TZ_STAGES;
+    const int s = step % TZ_TSTAGES;
     double* Ts = tz + s * TZ_TSTAGE;
     double* Xs = Ts + TZ_TI * TZ_TK;
     const int d = d0 + step / nj, j0 = (step % nj) * TZ_TK;
@@ -619,16 +624,16 @@ __global__ void __launch_bounds__(256, 2) k_toeplitz_tma(const __grid_constant__
   for (int u = 0; u < TZ_UI; ++u)
 #pragma unroll
     for (int v = 0; v < TZ_VA; ++v) acc[u][v][0] = acc[u][v][1] = 0.0;
+  // producer / consumer ring without block barriers: stage s holds step k (k mod S = s); a warp
+  // waits on full[s], multiplies, and its lane 0 arrives on empty[s]; thread 0 refills stage s with
+  // step k + S once all eight warps arrived
   if (tid == 0)
-    for (int k = 0; k < TZ_STAGES - 1 && k < nsteps; ++k) issue(k);
+    for (int k = 0; k < TZ_TSTAGES && k < nsteps; ++k) issue(k);
   for (int step = 0; step < nsteps; ++step) {
-    mbar_wait(smem_u32(bar + step % TZ_STAGES), (unsigned)((step / TZ_STAGES) & 1));
-    __syncthreads();                  // every warp is done with the stage refilled below (step - 1)
-    if (tid == 0 && step + TZ_STAGES - 1 < nsteps) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic reads before async writes
-      issue(step + TZ_STAGES - 1);
-    }
-    const double* Ts = tz + (step % TZ_STAGES) * TZ_TSTAGE;
+    const int st_ = step % TZ_TSTAGES;
+    const unsigned ph = (unsigned)((step / TZ_TSTAGES) & 1);
+    mbar_wait(smem_u32(bar + st_), ph);
+    const double* Ts = tz + (step % TZ_TSTAGES) * TZ_TSTAGE;
     const double* Xs = Ts + TZ_TI * TZ_TK;
 #pragma unroll
     for (int h = 0; h < TZ_TK / 8; ++h) {
@@ -645,6 +650,13 @@ __global__ void __launch_bounds__(256, 2) k_toeplitz_tma(const __grid_constant__
       for (int u = 0; u < TZ_UI; ++u)
 #pragma unroll
         for (int v = 0; v < TZ_VA; ++v) dmma_8x8x4(acc[u][v], af[u].y, bf[v].y);
+    }
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(ebar + st_)) : "memory");
+    if (tid == 0 && step + TZ_TSTAGES < nsteps) {
+      mbar_wait(smem_u32(ebar + st_), ph);                            // all warps are done with stage st_
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic reads before async writes
+      issue(step + TZ_TSTAGES);
     }
   }
   const long long n = (long long)nt * ng;
