@@ -793,13 +793,14 @@ struct RegB2 {
 };
 template <int KIND>
 __device__ __forceinline__ double phi_b2(const double* __restrict__ rec, long long S, const RegBZ<KIND>& z,
-                                         const RegB2& z2, double s, double u, int* regime) {
+                                         const RegB2& z2, double s, double u, int* regime,
+                                         const double* sm = nullptr, int ns = 0) {
   const bool zz1 = z.cmin * u >= MXZ, zz2 = z2.cs * u >= MXZ;
   double T[2] = {0.0, 0.0}, T2[2] = {0.0, 0.0};
   if (!zz1) {
     const double* R0 = rec + (RF_COMMON + 0 * FAMSZ) * S;
     const double* R1 = rec + (RF_COMMON + 1 * FAMSZ) * S;
-    bz_T<KIND>(BzSrc{R0 + FB1 * S, R0 + FB2 * S, R1 + FB1 * S, S, nullptr, 0}, z.c0, z.ic0, z.kb, s, u, T);
+    bz_T<KIND>(BzSrc{R0 + FB1 * S, R0 + FB2 * S, R1 + FB1 * S, S, sm, ns}, z.c0, z.ic0, z.kb, s, u, T);
   }
   if (!zz2) {
     const double* B = rec + (long long)(rec2_base<KIND>() + R2_FAM) * S;
@@ -1220,6 +1221,24 @@ __global__ void __launch_bounds__(128) k_near_m(BlockArgs B, MomArgs M, int chun
   Z.load(rec, S);
   RegB2 Z2;
   Z2.load<KIND>(rec, S);
+  // D_h: the first cluster's regime-B Taylor coefficients staged in shared memory as in k_bulk_m
+  // (about half of its near-cell nodes are in regime B, three chains each walked through L2: C5
+  // 1.70 -> 1.58 ms); V_h and K_h measured faster without (the 24 KB cost them occupancy)
+  constexpr bool STAGE = KIND == STB_D;
+  constexpr int NCH = bulk_nch<KIND>();
+  __shared__ double s_bzn[STAGE ? NCH * BZ_KBS * BZS_STRIDE : 1];
+  double* sbz = s_bzn + (STAGE ? threadIdx.x : 0);
+  int nsb = 0;
+  if (STAGE && Z.c0 > 0.0) {
+    const double* R0 = rec + (RF_COMMON + 0 * FAMSZ) * S;
+    const double* R1 = rec + (RF_COMMON + 1 * FAMSZ) * S;
+    nsb = min(Z.kb + 1, BZ_KBS);
+    for (int i = 0; i < nsb; ++i) {
+      sbz[i * BZS_STRIDE] = R0[(FB1 + i) * S];
+      if (Fams<KIND>::f0 != FAM_F) sbz[(BZ_KBS + i) * BZS_STRIDE] = R0[(FB2 + i) * S];
+      if (NCH == 3) sbz[(2 * BZ_KBS + i) * BZS_STRIDE] = R1[(FB1 + i) * S];
+    }
+  }
   unsigned long long nA = 0, nB = 0, nZ = 0, nC = 0, nK = 0;
   // node value for every lane (warp-uniform call: regime C is computed cooperatively)
   auto node = [&](int x, int y) -> double {
@@ -1232,7 +1251,8 @@ __global__ void __launch_bounds__(128) k_near_m(BlockArgs B, MomArgs M, int chun
       ++nA;
     } else {
       int reg = 0;
-      v = Z2.kb > 0 ? phi_b2<KIND>(rec, S, Z, Z2, nd.x, nd.z, &reg) : phi_bz<KIND, true>(rec, S, Z, nd.x, nd.z, &reg);
+      v = Z2.kb > 0 ? phi_b2<KIND>(rec, S, Z, Z2, nd.x, nd.z, &reg, STAGE ? sbz : nullptr, STAGE ? nsb : 0)
+                    : phi_bz<KIND, true>(rec, S, Z, nd.x, nd.z, &reg, STAGE ? sbz : nullptr, STAGE ? nsb : 0);
       nB += reg == 1;
         nK += reg == 1 ? Z.kb + Z2.kb : 0;
       nZ += reg == 2;
