@@ -337,7 +337,13 @@ static void launch_records(const MomArgs& MB, const MomArgs& MN, const MomArgs* 
   if (KIND == STB_D) {
     cudaMemsetAsync(MN.list, 0, sizeof(int), st);
     k_records<KIND, true, true><<<nblk, 128, 0, st>>>(MN);
-    k_records_warp<KIND, true><<<148 * 2, 128, 0, st>>>(MN);   // persistent: the resident warps walk the list
+    static int nsm = 0;
+    if (!nsm) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || nsm <= 0) nsm = 148;
+    }
+    k_records_warp<KIND, true><<<nsm * 2, 128, 0, st>>>(MN);   // persistent: the resident warps walk the list
     count_launch();
   } else {
     k_records<KIND, true><<<nblk, 128, 0, st>>>(MN);
