@@ -31,6 +31,16 @@ PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 # MEASURED_PEAKS sm_max_mhz); tools/fp64_peak.cu measured 34.1 TFLOP/s on this pool (profiles/).
 FP64_PEAK_DERIVED = 148 * 64 * 2 * 1.965e9 / 1e12
 FP64_TC_PEAK = 37.1   # measured DMMA m8n8k4 throughput, profiles/r01_dmma_peak.txt
+# the paper's own distributed-memory CPU timings, context only (other hardware, other workload:
+# alpha = 10, the paper's Table-1 meshes): D_h assembly wall time, Table 2
+PAPER_CONTEXT = {
+    "source": "arXiv:1811.05224 Table 2 (PAPER.md P:212-240): D_h assembly wall time",
+    "hardware": "Salomon cluster: 2x Intel Xeon E5-2680v3 (12-core Haswell) per node, 2 MPI x 12 OpenMP per node",
+    "D_h_assembly_s": {"65536 elements, 1 node": 184.1, "65536 elements, 64 nodes": 3.0,
+                       "262144 elements, 8 nodes": 373.6, "262144 elements, 128 nodes": 24.0,
+                       "1048576 elements, 64 nodes": 747.0, "1048576 elements, 256 nodes": 193.5},
+    "note": "context only, not a target (BASELINE.md section 1); this repo's L = 7 / 8 D_h on one B200: "
+            "DESIGN.md section 6.1b"}
 
 
 def parse():
@@ -470,8 +480,16 @@ def native(args):
             "gmres_solve_s": ph["solve"], "gmres_iterations": rep["iterations"],
             "gmres_true_rel_residual": rep["true_rel_residual"], "time_to_solution_s": ph["total"],
             "kernel_ms": {k: {"bulk": stats[k]["ms_bulk"], "near": stats[k]["ms_near"], "sing": stats[k]["ms_sing"]} for k in "VKD"},
+            # time to solution against its roofline: the bulk kernels' algorithmic flops at the FP64
+            # peak plus the solve's products' bytes at the HBM peak (near cells, records and the
+            # Krylov vector kernels counted as zero)
+            "time_to_solution_roofline": None if args.variant == "toeplitz" else {
+                "ideal_s": all_bulk_flops / (FP64_PEAK_DERIVED * 1e12) + n_mv * bytes_per_gemv / (hbm_peak * 1e9),
+                "frac": (all_bulk_flops / (FP64_PEAK_DERIVED * 1e12) + n_mv * bytes_per_gemv / (hbm_peak * 1e9)) / ph["total"],
+                "note": "ideal = bulk-assembly flops / FP64 peak + products x bytes / MEASURED_PEAKS hbm_gbs"},
         },
         "roofline": roofline,
+        "paper_context": PAPER_CONTEXT,
         "roofline_gemv": roof_gemv,
         "roofline_assembly": roof_asm,
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n},
