@@ -348,7 +348,7 @@ def native(args):
         t_dev, t_e2e = tt.tolist()
     entries_total = info["entries_total"]
     # units: the distinct element-pair integrals computed and stored per step (V_h and D_h keep the
-    # upper 32 x 32 tile triangle of their symmetric spatial blocks, K_h all entries); the matrix
+    # N_Gamma (N_Gamma + 1) / 2 distinct entries of their symmetric spatial blocks, K_h all); the matrix
     # entries they represent (3 x entries_total) are reported beside
     units_per_step = sum(stats[k]["entries"] for k in "VKD")   # this rank's owned blocks
     if world > 1:   # whole-job units: every rank computes the integrals of its own blocks
@@ -468,8 +468,8 @@ def native(args):
             "assembly_pairs_per_s": units_per_step / asm_s,
             "integrals_per_step": {k: stats[k]["entries"] for k in "VKD"},
             "matrix_entries_represented_per_s": represented_per_step / (1e-3 * ms),
-            "storage": "V_h, D_h: symmetric packed spatial blocks (upper 32x32 tile triangle); K_h computed "
-                       "and applied to g on the fly (bem_rhs_fused), never stored",
+            "storage": "V_h, D_h: symmetric packed spatial blocks (upper triangle: 32x32 tiles, triangular "
+                       "diagonal tiles); K_h computed and applied to g on the fly (bem_rhs_fused), never stored",
             "assembly_s": {"all_in_step": ph["assembly"],
                            "isolated": iso["seconds"] if iso else None,
                            "isolated_pairs_per_s": iso["pairs_per_s"] if iso else None,

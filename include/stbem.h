@@ -89,8 +89,9 @@ typedef struct {
 /* touching pairs by per-lag singular rules (k_sing) instead of moment records; without it the
  * records are used whenever alpha (h_X + h_Y)^2 / (4 min h_t) < 4 */
 #define BEM_QUAD_LEGACY_SING 1
-/* V_h and D_h store their symmetric spatial blocks packed (upper 32 x 32 tile triangle, about
- * half the bytes and half the assembly work); this flag stores them full */
+/* V_h and D_h store their symmetric spatial blocks packed (upper triangle: off-diagonal 32 x 32 tiles
+ * and triangular diagonal tiles, about half the bytes and half the assembly work, DESIGN.md section
+ * 4.1); this flag stores them full */
 #define BEM_QUAD_FULL_STORAGE 2
 
 typedef enum {
