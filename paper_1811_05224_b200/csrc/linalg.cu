@@ -992,9 +992,18 @@ __global__ void k_dots_sum(const double* __restrict__ part, int nch, int k, doub
   for (int c = 0; c < nch; ++c) s += part[(long long)j * nch + c];
   out[j] = s;
 }
-// per host thread and device (concurrent solves on several threads each own theirs)
-static thread_local double* g_dot_part[64] = {nullptr};
-static thread_local size_t g_dot_part_n[64] = {0};
+// per host thread and device (concurrent solves on several threads each own theirs), freed when
+// the thread exits
+struct DotScratch {
+  double* p[64] = {nullptr};
+  size_t n[64] = {0};
+  ~DotScratch() {
+    for (int d = 0; d < 64; ++d)
+      if (p[d]) cudaFree(p[d]);
+    cudaGetLastError();
+  }
+};
+static thread_local DotScratch g_dot;
 void vec_dots(const double* Q, long long ldq, int k, const double* w, long long n, double* out,
               cudaStream_t st) {
   const int nch = (int)std::max<long long>(1, std::min<long long>(DOT_MAXCH, (n + DOT_CHUNK - 1) / DOT_CHUNK));
@@ -1003,15 +1012,15 @@ void vec_dots(const double* Q, long long ldq, int k, const double* w, long long 
   cudaGetDevice(&dev);
   dev &= 63;
   const size_t need = (size_t)k * nch;
-  if (need > g_dot_part_n[dev]) {
+  if (need > g_dot.n[dev]) {
     // per-device scratch, grows rarely (largest k seen); stream-ordered free / allocation
-    if (g_dot_part[dev]) cudaFreeAsync(g_dot_part[dev], st);
-    g_dot_part_n[dev] = std::max<size_t>(need, 64 * 1024);
-    cudaMallocAsync((void**)&g_dot_part[dev], sizeof(double) * g_dot_part_n[dev], st);
+    if (g_dot.p[dev]) cudaFreeAsync(g_dot.p[dev], st);
+    g_dot.n[dev] = std::max<size_t>(need, 64 * 1024);
+    cudaMallocAsync((void**)&g_dot.p[dev], sizeof(double) * g_dot.n[dev], st);
   }
   dim3 grid(k, nch);
-  k_dots<<<grid, 256, 0, st>>>(Q, ldq, w, n, chunk, g_dot_part[dev]);
-  k_dots_sum<<<(k + 127) / 128, 128, 0, st>>>(g_dot_part[dev], nch, k, out);
+  k_dots<<<grid, 256, 0, st>>>(Q, ldq, w, n, chunk, g_dot.p[dev]);
+  k_dots_sum<<<(k + 127) / 128, 128, 0, st>>>(g_dot.p[dev], nch, k, out);
   count_launch(2);
 }
 
