@@ -12,7 +12,8 @@
 //   F~ = E1(x) + gamma + ln c              = Ein(x) + ln s
 //   Q~ = e^{-x}/x - E1(x) - s/c - gamma - ln c = PSI(x) - ln s
 // (GH, Ein, PSI entire).  Three regimes per (entry, node), chosen per lane:
-//   A  x_max = c_max/s < 4: the polynomials of moment_coeffs.h in x, so the sum over points is
+//   A  x_max = c_max/s < 8 in the bulk cells (< 4 in the near cells and touching records): the
+//      polynomials of moment_coeffs.h in x (degree 20 on [0, 8]), so the sum over points is
 //      sum_k f_k s^{-k} M_k with time-independent moments M_k = sum_p W_p c_p^k: one Horner
 //      chain in u = 1/s per kernel family, independent of the number of quadrature points.
 //   B  the points are clustered, rho = (c_max - c0)/c0 <= 0.5: Taylor expansion in c around c0
@@ -32,7 +33,7 @@
 
 namespace stb {
 
-constexpr int MKA = 17;          // regime-A polynomial degree (MGH, MEIN; MPSI padded)
+constexpr int MKA = 20;          // regime-A polynomial degree (MGH, MEIN, MPSI on [0, 8])
 constexpr int MKB = 56;          // regime-B maximum Taylor order
 constexpr double MRHO = 0.5;     // regime-B cluster bound (c_max - c0 <= MRHO c0)
 constexpr double MXZ = 50.0;     // regime Z threshold on x_min
@@ -351,7 +352,7 @@ __device__ __forceinline__ void records_body(const MomArgs& M, long long pair, i
   // near records: a cluster too wide for one Taylor centre (c_max > 3 c_min) but within 9 c_min is
   // split at c_s = sqrt(c_min c_max) into two clusters of ratio <= 3 each (regime B2)
   // (only when a near-cell node can fall between regime A and regime Z for this pair)
-  const bool two = NEAR && !okB && cmin > 0.0 && cmax <= 8.99 * cmin && cmax * M.u_near[1] >= STB_MXA &&
+  const bool two = NEAR && !okB && cmin > 0.0 && cmax <= 8.99 * cmin && cmax * M.u_near[1] >= STB_MXB &&
                    cmin * M.u_near[0] < MXZ;
   const double cs = two ? sqrt(cmin * cmax) : 0.0;
   if (two) {
@@ -1067,7 +1068,7 @@ __global__ void __launch_bounds__(128, KIND == STB_D ? 2 : 3) k_bulk_m(BlockArgs
         phi[r] = 0.0;
         nA += r_lo + r <= r_hi && r_lo + r > y;
       }
-    } else if (full && __all_sync(0xffffffffu, A.cmax * ndd[2] < STB_MXA)) {
+    } else if (full && __all_sync(0xffffffffu, A.cmax * ndd[2] < STB_MXB)) {
 #pragma unroll
       for (int r = 0; r <= R; ++r) phi[r] = A.chain(ndd[4 * r + 2]);
 #pragma unroll
@@ -1081,7 +1082,7 @@ __global__ void __launch_bounds__(128, KIND == STB_D ? 2 : 3) k_bulk_m(BlockArgs
         const int x = r_lo + r;
         const double v = A.finish(phi[r], ndd[4 * r], ndd[4 * r + 1]);
         const bool ok = x <= r_hi && x > y;
-        const bool inA = A.cmax * ndd[4 * r + 2] < STB_MXA;
+        const bool inA = A.cmax * ndd[4 * r + 2] < STB_MXB;
         phi[r] = ok ? v : 0.0;
         nA += ok && inA;
         if (ok && !inA) bmask |= 1u << r;
@@ -1245,7 +1246,7 @@ __global__ void __launch_bounds__(128) k_near_m(BlockArgs B, MomArgs M, int chun
     const double4 nd = B.lag[x * B.ldlag + y];
     double v = 0.0;
     bool needC = false, inA = false;
-    if (A.cmax * nd.z < STB_MXA) {
+    if (A.cmax * nd.z < STB_MXB) {
       v = A.eval(nd.x, nd.y, nd.z);
       inA = true;
       ++nA;

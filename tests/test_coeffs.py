@@ -68,10 +68,13 @@ def test_gb_large_x():
 
 @pytest.mark.parametrize("name", ["MEIN", "MGH", "MPSI"])
 def test_moment_polynomials(name):
-    """the regime-A polynomials in x on [0, 4] (MKA = their degree bound)"""
+    """the regime-A polynomials in x on [0, STB_MXB] (= 8, the bulk cells' regime-A interval; the
+    near cells and touching records use them on [0, STB_MXA] = [0, 4]); MKA = their degree bound"""
     c = _coeffs("moment_coeffs.h", name)
     assert len(c) - 1 <= _constexpr("MKA")
-    x = np.linspace(1e-6, 4.0, 4001)
+    xb = _define("moment_coeffs.h", "MXB")
+    assert xb >= _define("moment_coeffs.h", "MXA")
+    x = np.linspace(1e-6, xb, 8001)
     ein = exp1(x) + EULER + np.log(x)
     ref = {"MEIN": ein, "MGH": (1 + x) * ein - np.exp(-x), "MPSI": np.expm1(-x) / x - ein}[name]
     scale = _horner(np.abs(c), x)          # sum |c_k| x^k: the rounding scale of the Horner sum
