@@ -300,13 +300,14 @@ static void launch_kind(int which, const BlockArgs& BA, const MomArgs& M, int ng
                         int nz, cudaStream_t st) {
   dim3 grid((ng + 31) / 32, (ng + 3) / 4, nz);
   if (which == 0) {
-    constexpr size_t smem = bulk_smem_bytes<KIND, 8>();
+    constexpr int R = bulk_r<KIND>();
+    constexpr size_t smem = bulk_smem_bytes<KIND, R>();
     static bool attr = false;   // per template instance
     if (!attr) {
-      cudaFuncSetAttribute(k_bulk_m<KIND, 8, PROD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(k_bulk_m<KIND, R, PROD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       attr = true;
     }
-    k_bulk_m<KIND, 8, PROD><<<grid, 128, smem, st>>>(BA, M);
+    k_bulk_m<KIND, R, PROD><<<grid, 128, smem, st>>>(BA, M);
   }
   else k_near_m<KIND, PROD><<<grid, 128, 0, st>>>(BA, M, nband_or_chunk);
   count_launch();
@@ -522,7 +523,7 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, const Qua
     BA.pslots = pslots;
     BA.ntile = ntile;
     BA.ell = MB.ell;
-    const int R = 8;                  // test steps per band of k_bulk_m
+    const int R = (kind == STB_D && !prod) ? bulk_r<STB_D>() : bulk_r<STB_V>();   // band of k_bulk_m
     const int nband = (blk.a1 - blk.a0 + R - 1) / R;
     if (blk.a1 - 1 - blk.b0 >= 2) {
       if (prod) launch_kind<STB_K, true>(0, BA, MB, ng, nband, nband, st);

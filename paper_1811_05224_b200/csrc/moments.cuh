@@ -949,6 +949,10 @@ __device__ __forceinline__ void count_regimes(unsigned long long* ctr, unsigned 
 // index and summed over the thread's columns; one warp sum per (test row, trial tile) is written
 // to the block's partial buffer (fixed slots: deterministic)
 constexpr int LAG_CH = 16;
+// test steps per band: 7 for V_h and K_h g (their 3-CTA register budget: 8 spilled in the B path,
+// C5 V 10.1 -> 9.7 ms, K g 16.5 -> 16.0 ms at 7), 8 for D_h (2 CTAs, 11.6 vs 12.1 ms at 7)
+template <int KIND>
+__host__ __device__ constexpr int bulk_r() { return KIND == STB_D ? 8 : 7; }
 template <int KIND>
 __host__ __device__ constexpr int bulk_nch() { return Fams<KIND>::n == 2 ? 3 : 2; }
 // dynamic shared memory of k_bulk_m: staged regime-B coefficients + two lag chunks
