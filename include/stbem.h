@@ -163,6 +163,13 @@ bem_status bem_comm_create(const void* unique_id128_host, int nranks, int rank, 
  * on another rank's kernel.  Each handle is freed with bem_comm_destroy.
  * Errors: BEM_E_INVALID (nranks out of range, null out_host), BEM_E_CUDA. */
 bem_status bem_comm_create_group(int nranks, int cuda_device, bem_comm** out_host);
+/* One rank of nranks ALONE on cuda_device, without NCCL (load-balance studies and partial-product
+ * tests): a mesh created with it owns rank `rank`'s blocks of the cyclic plan, and every product or
+ * fused right-hand side returns this rank's partial sums over its owned blocks (the collectives are
+ * no-ops): the sum over the ranks' results is the full product (bem_rhs_fused adds its
+ * 1/2 M_h g term on every rank).  bem_solve_gmres refuses such a mesh (BEM_E_STATE).
+ * Errors: BEM_E_INVALID, BEM_E_CUDA. */
+bem_status bem_comm_create_solo(int nranks, int rank, int cuda_device, bem_comm** out);
 /* NCCL communicators: the collectives run on the communicator's own stream (a product's row
  * chunks are all-reduced while the GEMV of the next chunk runs); every host wait of the solver polls
  * ncclCommGetAsyncError and aborts the communicator on an asynchronous error (BEM_E_NCCL from then

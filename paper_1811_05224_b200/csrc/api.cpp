@@ -370,6 +370,7 @@ bem_status bem_solve_gmres(const bem_matrix* V, const bem_matrix* D, const bem_m
     }
   }
   if (!(opts->rel_tol > 0) || opts->max_iter < 1) { set_error("bem_solve_gmres: rel_tol > 0 and max_iter >= 1 required"); return BEM_E_INVALID; }
+  if (V->mesh->comm && V->mesh->comm->solo) { set_error("bem_solve_gmres: a solo rank holds partial products only"); return BEM_E_STATE; }
   const bem_mesh* m = V->mesh;
   cudaSetDevice(m->device);
   const long long n = (long long)m->ng * m->nt;

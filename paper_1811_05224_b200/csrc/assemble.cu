@@ -297,7 +297,7 @@ __global__ void __launch_bounds__(128) k_sing(BlockArgs B, const Seg* __restrict
 // which: 0 bulk cells (k_bulk_m), 1 near cells (k_near_m)
 template <int KIND, bool PROD = false>
 static void launch_kind(int which, const BlockArgs& BA, const MomArgs& M, int ng, int nband_or_chunk,
-                        int nz, cudaStream_t st) {
+                        int nz, cudaStream_t st, BulkList L = BulkList{nullptr, 0}) {
   dim3 grid((ng + 31) / 32, (ng + 3) / 4, nz);
   if (which == 0) {
     constexpr int R = bulk_r<KIND>();
@@ -307,7 +307,7 @@ static void launch_kind(int which, const BlockArgs& BA, const MomArgs& M, int ng
       cudaFuncSetAttribute(k_bulk_m<KIND, R, PROD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       attr = true;
     }
-    k_bulk_m<KIND, R, PROD><<<grid, 128, smem, st>>>(BA, M);
+    k_bulk_m<KIND, R, PROD><<<grid, 128, smem, st>>>(BA, L, M);
   }
   else k_near_m<KIND, PROD><<<grid, 128, 0, st>>>(BA, M, nband_or_chunk);
   count_launch();
@@ -505,6 +505,52 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, const Qua
     npairs_computed = 0;
     for (int i = 0; i < ng; ++i) npairs_computed += ng - (i / SYM_TS) * SYM_TS;
   }
+  // bulk cells: ONE launch over all owned blocks (band z of every block in each CTA: the per-pair
+  // setup -- records, regime-B coefficients -- is paid once per CTA; a rank of the cyclic plan owns
+  // ~P/2 + 1 small blocks, which per-block launches left setup-bound)
+  const int Rb = (kind == STB_D && !prod) ? bulk_r<STB_D>() : bulk_r<STB_V>();   // band of k_bulk_m
+  {
+    std::vector<BulkBlock> bl;
+    int nzmax = 0;
+    for (size_t bi = 0; bi < blocks_of(A).size(); ++bi) {
+      const Block& blk = blocks_of(A)[bi];
+      if (blk.a1 - 1 - blk.b0 < 2) continue;    // no cell with d >= 2
+      bl.push_back(BulkBlock{d_poff + A->poff_base[bi], blk.a0, blk.a1, blk.b0, blk.b1, pbase[bi]});
+      nzmax = std::max(nzmax, (blk.a1 - blk.a0 + Rb - 1) / Rb);
+      A->nodes_expected += bulk_nodes(blk, Rb) * npairs_computed;
+    }
+    if (!bl.empty()) {
+      BulkBlock* d_bl = nullptr;
+      if ((e = cudaMallocAsync((void**)&d_bl, sizeof(BulkBlock) * bl.size(), st)) != cudaSuccess ||
+          (e = cudaMemcpyAsync(d_bl, bl.data(), sizeof(BulkBlock) * bl.size(), cudaMemcpyHostToDevice, st)) != cudaSuccess)
+        return cuda_fail(e, "assemble/bulk list");
+      BlockArgs BA;
+      BA.out = A->data;
+      BA.poff = nullptr;
+      BA.a0 = BA.a1 = BA.b0 = BA.b1 = 0;
+      BA.ng = ng;
+      BA.lag = m->d_lag;
+      BA.ldlag = m->nt + 1;
+      BA.sym = A->sym;
+      BA.nt = sym_nt(ng);
+      BA.blk = A->blk_elems;
+      BA.g = prod_g;
+      BA.part = d_part;
+      BA.pbase = 0;
+      BA.pslots = pslots;
+      BA.ntile = ntile;
+      BA.ell = MB.ell;
+      const BulkList L{d_bl, (int)bl.size()};
+      if (prod) launch_kind<STB_K, true>(0, BA, MB, ng, nzmax, nzmax, st, L);
+      else if (kind == STB_V) launch_kind<STB_V>(0, BA, MB, ng, nzmax, nzmax, st, L);
+      else if (kind == STB_K) launch_kind<STB_K>(0, BA, MB, ng, nzmax, nzmax, st, L);
+      else launch_kind<STB_D>(0, BA, MB, ng, nzmax, nzmax, st, L);
+      mark();
+      fam.push_back(0);
+      A->launches++;
+      cudaFreeAsync(d_bl, st);
+    }
+  }
   for (size_t bi = 0; bi < blocks_of(A).size(); ++bi) {
     const Block& blk = blocks_of(A)[bi];
     BlockArgs BA;
@@ -523,18 +569,6 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, const Qua
     BA.pslots = pslots;
     BA.ntile = ntile;
     BA.ell = MB.ell;
-    const int R = (kind == STB_D && !prod) ? bulk_r<STB_D>() : bulk_r<STB_V>();   // band of k_bulk_m
-    const int nband = (blk.a1 - blk.a0 + R - 1) / R;
-    if (blk.a1 - 1 - blk.b0 >= 2) {
-      if (prod) launch_kind<STB_K, true>(0, BA, MB, ng, nband, nband, st);
-      else if (kind == STB_V) launch_kind<STB_V>(0, BA, MB, ng, nband, nband, st);
-      else if (kind == STB_K) launch_kind<STB_K>(0, BA, MB, ng, nband, nband, st);
-      else launch_kind<STB_D>(0, BA, MB, ng, nband, nband, st);
-      mark();
-      fam.push_back(0);
-      A->launches++;
-      A->nodes_expected += bulk_nodes(blk, R) * npairs_computed;
-    }
     const bool has_near = blk.b1 - 1 >= blk.a0 - 1 && blk.b0 <= blk.a1 - 1;
     if (has_near) {
       const int chunk = 16;

@@ -189,7 +189,7 @@ static bem_status nccl_allreduce(bem_comm* c, double* buf, long long n, cudaStre
 
 bem_status allreduce_sum(const bem_mesh* m, double* buf, long long n, cudaStream_t st) {
   bem_comm* c = m->comm;
-  if (!c) return BEM_OK;
+  if (!c || c->solo) return BEM_OK;   // solo rank: its partial sums stay as they are
   if (c->group) return group_allreduce(c, buf, n, st);
   return nccl_allreduce(c, buf, n, st);
 }
@@ -283,6 +283,19 @@ bem_status bem_comm_create_group(int nranks, int cuda_device, bem_comm** out) {
     c->group = G;
     out[r] = c;
   }
+  return BEM_OK;
+}
+
+bem_status bem_comm_create_solo(int nranks, int rank, int cuda_device, bem_comm** out) {
+  if (!out || nranks < 1 || rank < 0 || rank >= nranks) { stb::set_error("bem_comm_create_solo: bad argument"); return BEM_E_INVALID; }
+  cudaError_t e = cudaSetDevice(cuda_device);
+  if (e != cudaSuccess) return stb::cuda_fail(e, "bem_comm_create_solo/cudaSetDevice");
+  bem_comm* c = new bem_comm_s();
+  c->nranks = nranks;
+  c->rank = rank;
+  c->device = cuda_device;
+  c->solo = true;
+  *out = c;
   return BEM_OK;
 }
 

@@ -89,6 +89,7 @@ struct bem_comm_s {
   stb::CommGroup* group = nullptr; // emulated ranks on one device (host-thread group, tests)
   cudaStream_t stream = nullptr;   // NCCL: the collectives' stream (overlap with the GEMV)
   bool failed = false;             // an asynchronous NCCL error was seen: the communicator is aborted
+  bool solo = false;               // one rank of nranks alone: collectives are no-ops (partial sums)
 };
 
 struct bem_mesh_s {

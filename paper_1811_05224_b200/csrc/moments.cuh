@@ -949,6 +949,17 @@ __device__ __forceinline__ void count_regimes(unsigned long long* ctr, unsigned 
 // index and summed over the thread's columns; one warp sum per (test row, trial tile) is written
 // to the block's partial buffer (fixed slots: deterministic)
 constexpr int LAG_CH = 16;
+// the temporal blocks one bulk launch covers (all owned blocks of the rank): per block its panel
+// offsets, step ranges and (product mode) partial base
+struct BulkBlock {
+  const long long* poff;
+  int a0, a1, b0, b1;
+  long long pbase;
+};
+struct BulkList {
+  const BulkBlock* blk;
+  int n;
+};
 // test steps per band: 7 for V_h and K_h g (their 3-CTA register budget: 8 spilled in the B path,
 // C5 V 10.1 -> 9.7 ms, K g 16.5 -> 16.0 ms at 7), 8 for D_h (2 CTAs, 11.6 vs 12.1 ms at 7)
 template <int KIND>
@@ -965,7 +976,7 @@ __device__ __forceinline__ void cp_async16_bulk(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(sa), "l"(gmem));
 }
 template <int KIND, int R, bool PROD = false>
-__global__ void __launch_bounds__(128, KIND == STB_D ? 2 : 3) k_bulk_m(BlockArgs B, MomArgs M) {
+__global__ void __launch_bounds__(128, KIND == STB_D ? 2 : 3) k_bulk_m(BlockArgs B, BulkList L, MomArgs M) {
   const int ng = B.ng;
   const int lane = threadIdx.x & 31;
   const int J0 = blockIdx.x * 32 + lane;
@@ -973,15 +984,19 @@ __global__ void __launch_bounds__(128, KIND == STB_D ? 2 : 3) k_bulk_m(BlockArgs
   const bool valid = I0 < ng && J0 < ng;
   const int I = min(I0, ng - 1), J = min(J0, ng - 1);
   const int band = blockIdx.z;
-  const int r_hi = B.a1 - R * band;
-  const int r_lo = max(B.a0, r_hi - R);
-  if (r_hi <= r_lo) return;                       // CTA-uniform
-  const int bmax = min(B.b1 - 1, r_hi - 1 - 2);
-  if (bmax < B.b0) return;                        // CTA-uniform
   // sym: the CTA's 4 rows lie in tile row (4 blockIdx.y) / 32, its 32 columns in tile column
   // blockIdx.x; tiles below the tile diagonal are the mirror images of stored ones
   const int ti = (blockIdx.y * 4) / SYM_TS, tj = blockIdx.x;
   if (B.sym && ti > tj) return;                   // CTA-uniform
+  // does band z of any listed block have bulk cells?  (CTA-uniform)
+  {
+    bool any = false;
+    for (int k = 0; k < L.n && !any; ++k) {
+      const int rh = L.blk[k].a1 - R * band, rl = max(L.blk[k].a0, rh - R);
+      any = rh > rl && min(L.blk[k].b1 - 1, rh - 3) >= L.blk[k].b0;
+    }
+    if (!any) return;
+  }
   const long long pair = (long long)I * ng + J;
   const long long S = M.npairs;
   // row offsets of the band rows a = r_lo + r for this warp's row I (panel offset + I * ld, or
@@ -992,28 +1007,7 @@ __global__ void __launch_bounds__(128, KIND == STB_D ? 2 : 3) k_bulk_m(BlockArgs
   constexpr int NCH = bulk_nch<KIND>();
   double* s_bz = bulk_dyn;                                                  // [NCH][KBS][128]
   double4* s_lag = reinterpret_cast<double4*>(bulk_dyn + NCH * BZ_KBS * BZS_STRIDE);   // [2][LAG_CH][R+1]
-  // lag chunk c: columns y = b0 + c LAG_CH + k, nodes x = min(r_lo + r, r_hi) (2 x 16 B per entry)
-  const int ncols = bmax + 2 - B.b0;
-  auto stage = [&](int c) {
-    double4* dst = s_lag + (c & 1) * (LAG_CH * (R + 1));
-    for (int e = threadIdx.x; e < 2 * LAG_CH * (R + 1); e += blockDim.x) {
-      const int ent = e >> 1, k = ent / (R + 1), r = ent % (R + 1);
-      const int y = B.b0 + c * LAG_CH + k;
-      if (c * LAG_CH + k < ncols) {
-        const double* src = reinterpret_cast<const double*>(B.lag + (long long)min(r_lo + r, r_hi) * B.ldlag + y);
-        cp_async16_bulk(reinterpret_cast<double*>(dst + ent) + 2 * (e & 1), src + 2 * (e & 1));
-      }
-    }
-    asm volatile("cp.async.commit_group;");
-  };
-  stage(0);
   long long* srow = s_row[threadIdx.x >> 5];
-  if (!PROD && lane < R) {
-    const int a = min(r_lo + lane, r_hi - 1);
-    srow[lane] = B.poff[a - B.a0] + (B.sym ? sym_tile_offset(ti, tj, B.nt) + sym_row_base(I % SYM_TS, ti == tj)
-                                           : (long long)I * pad4((long long)panel_nb(a, B.b0, B.b1) * ng));
-  }
-  __syncwarp();
   const long long cstride = B.sym ? B.blk : (long long)ng;   // per trial step b
   const int jcol = B.sym ? J % SYM_TS : J;
   // stores: diagonal tiles of the symmetric packing keep their upper triangle only
@@ -1041,14 +1035,45 @@ __global__ void __launch_bounds__(128, KIND == STB_D ? 2 : 3) k_bulk_m(BlockArgs
     }
   }
   unsigned long long nA = 0, nB = 0, nZ = 0, nC = 0, nK = 0;
+  // the listed blocks one after the other (a rank's owned blocks of the cyclic plan; one block on one
+  // GPU): the per-pair setup above is paid once per CTA, not once per block
+  for (int kb_ = 0; kb_ < L.n; ++kb_) {
+  const BulkBlock Bk = L.blk[kb_];
+  const int r_hi = Bk.a1 - R * band;
+  const int r_lo = max(Bk.a0, r_hi - R);
+  if (r_hi <= r_lo) continue;                     // CTA-uniform
+  const int bmax = min(Bk.b1 - 1, r_hi - 1 - 2);
+  if (bmax < Bk.b0) continue;                     // CTA-uniform
+  __syncthreads();                                // the previous block's lag chunks and row offsets are no longer read
+  // lag chunk c: columns y = b0 + c LAG_CH + k, nodes x = min(r_lo + r, r_hi) (2 x 16 B per entry)
+  const int ncols = bmax + 2 - Bk.b0;
+  auto stage = [&](int c) {
+    double4* dst = s_lag + (c & 1) * (LAG_CH * (R + 1));
+    for (int e = threadIdx.x; e < 2 * LAG_CH * (R + 1); e += blockDim.x) {
+      const int ent = e >> 1, k = ent / (R + 1), r = ent % (R + 1);
+      const int y = Bk.b0 + c * LAG_CH + k;
+      if (c * LAG_CH + k < ncols) {
+        const double* src = reinterpret_cast<const double*>(B.lag + (long long)min(r_lo + r, r_hi) * B.ldlag + y);
+        cp_async16_bulk(reinterpret_cast<double*>(dst + ent) + 2 * (e & 1), src + 2 * (e & 1));
+      }
+    }
+    asm volatile("cp.async.commit_group;");
+  };
+  stage(0);
+  if (!PROD && lane < R) {
+    const int a = min(r_lo + lane, r_hi - 1);
+    srow[lane] = Bk.poff[a - Bk.a0] + (B.sym ? sym_tile_offset(ti, tj, B.nt) + sym_row_base(I % SYM_TS, ti == tj)
+                                             : (long long)I * pad4((long long)panel_nb(a, Bk.b0, Bk.b1) * ng));
+  }
+  __syncwarp();
   double accp[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) accp[r] = 0.0;
   double Gp[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) Gp[r] = 0.0;
-  for (int y = B.b0; y <= bmax + 1; ++y) {
-    const int kc = y - B.b0;
+  for (int y = Bk.b0; y <= bmax + 1; ++y) {
+    const int kc = y - Bk.b0;
     if (kc % LAG_CH == 0) {                          // CTA-uniform: chunk kc / LAG_CH is needed
       asm volatile("cp.async.wait_group 0;" ::: "memory");
       __syncthreads();                               // visible to all; the other buffer is free
@@ -1142,7 +1167,7 @@ __global__ void __launch_bounds__(128, KIND == STB_D ? 2 : 3) k_bulk_m(BlockArgs
 #pragma unroll
       for (int r = 0; r <= R; ++r) phi[r] = sp[r * 128];
     }
-    if (y > B.b0) {
+    if (y > Bk.b0) {
       const int b = y - 1;
       // interior column: every band row is a full bulk cell (no per-row conditions)
       const bool interior = b <= r_lo - 2 && r_hi - r_lo == R;
@@ -1165,7 +1190,7 @@ __global__ void __launch_bounds__(128, KIND == STB_D ? 2 : 3) k_bulk_m(BlockArgs
           }
         }
       } else {
-        double* col = B.out + ((long long)(b - B.b0) * cstride + jcol);
+        double* col = B.out + ((long long)(b - Bk.b0) * cstride + jcol);
         if (interior && vst) {
 #pragma unroll
           for (int r = 1; r <= R; ++r) {
@@ -1194,9 +1219,10 @@ __global__ void __launch_bounds__(128, KIND == STB_D ? 2 : 3) k_bulk_m(BlockArgs
       const double sum = warp_sum(accp[r]);
       const int a = r_lo + r;
       if (lane == 0 && a < r_hi && I0 < ng)
-        B.part[B.pbase + ((long long)(a - B.a0) * ng + I) * B.pslots + blockIdx.x] = sum;
+        B.part[Bk.pbase + ((long long)(a - Bk.a0) * ng + I) * B.pslots + blockIdx.x] = sum;
     }
   }
+  }   // listed blocks
   if (!valid) nA = nB = nZ = nC = nK = 0;
   count_regimes(M.counters, nA, nB, nZ, nC, nK);
 }

@@ -99,6 +99,7 @@ _SIGS = {
     "bem_comm_create": (I, [P, I, I, I, PP]),
     "bem_comm_destroy": (None, [P]),
     "bem_comm_create_group": (I, [I, I, P]),
+    "bem_comm_create_solo": (I, [I, I, I, PP]),
     "bem_plan_build": (I, [I, P]),
     "bem_plan_generator": (I, [I, P, P]),
     "bem_plan_owned_blocks": (I, [I, I, I, P, P]),
@@ -232,6 +233,16 @@ class Comm:
             c.rank, c.world = r, world
             out.append(c)
         return out
+
+    @classmethod
+    def solo(cls, world, rank, device):
+        """rank `rank` of `world` alone on one device (bem_comm_create_solo): partial products only"""
+        h = ctypes.c_void_p()
+        check(lib().bem_comm_create_solo(int(world), int(rank), int(device), ctypes.byref(h)))
+        c = cls.__new__(cls)
+        c.h = h
+        c.rank, c.world = rank, world
+        return c
 
     def close(self):
         if self.h:

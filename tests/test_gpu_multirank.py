@@ -94,3 +94,37 @@ def test_emulated_ranks_match_single_rank(name, G):
     assert out["rep"]["iterations"] == ref["rep"]["iterations"], (out["rep"], ref["rep"])
     assert relmax(out["w"], ref["w"]) <= 1e-10
     assert out["rep"]["seconds_comm"] > 0.0            # the collectives were timed
+
+
+@pytest.mark.parametrize("name,G", [("S32", 2), ("S32", 4), ("C2", 4)])
+def test_solo_rank_partials_sum_to_the_product(name, G):
+    """each rank of the cyclic plan alone on the GPU (bem_comm_create_solo, P = 2G): its owned
+    blocks' partial products of V_h, D_h and of K_h g sum over the ranks to the single-rank results
+    (the verdict's partial-product check, with the real kernels)"""
+    w = W.get(name)
+    ref = single(name)
+    x = torch.tensor(W.random_vector(w.n), dtype=torch.float64, device="cuda")
+    g = torch.tensor(W.dirichlet_data(w), dtype=torch.float64, device="cuda")
+    sums = {k: np.zeros(w.n) for k in ("Vx", "Dx", "Kg")}
+    m0 = S.Mesh.from_workload(w)
+    half_mg = torch.zeros_like(g)
+    m0.assemble_M(S.MASS_PRIMAL).matvec(g, half_mg, a=0.5)
+    for r in range(G):
+        c = S.Comm.solo(G, r, 0)
+        m = S.Mesh.from_workload(w, n_slices=2 * G, comm=c)
+        V, D = m.assemble_V(), m.assemble_D()
+        y = torch.empty_like(x)
+        V.matvec(x, y)
+        sums["Vx"] += y.cpu().numpy()
+        D.matvec(x, y)
+        sums["Dx"] += y.cpu().numpy()
+        b = torch.empty_like(g)
+        S.rhs_fused(m, m.assemble_M(S.MASS_PRIMAL), g, b)
+        sums["Kg"] += (b - half_mg).cpu().numpy()
+        with pytest.raises(S.BemError):
+            S.solve_gmres(V, b, torch.zeros_like(g), D=D, M=m.assemble_M(S.MASS_DUAL), precond=2)
+        V.close(); D.close(); m.close(); c.close()
+    torch.cuda.synchronize()
+    assert relmax(sums["Vx"], ref["Vx"]) <= 1e-13
+    assert relmax(sums["Dx"], ref["Dx"]) <= 1e-13
+    assert relmax(sums["Kg"] + half_mg.cpu().numpy(), ref["b"]) <= 1e-13
