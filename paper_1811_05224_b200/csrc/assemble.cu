@@ -331,7 +331,7 @@ __global__ void k_prod_reduce(const double* __restrict__ part, const int* __rest
 template <int KIND>
 static void launch_records(const MomArgs& MB, const MomArgs& MN, const MomArgs* MS, int q_sing,
                            cudaStream_t st) {
-  const unsigned nblk = (unsigned)((MB.npairs + 127) / 128);
+  const unsigned nblk = (unsigned)((MB.p_hi - MB.p_lo + 127) / 128);   // this rank's pairs
   // D_h near records: the pairs with touching or close half-segment sub-pairs (distance-dependent
   // orders, skipped sub-pairs) warp per pair, the others thread per pair (k_records near_special)
   k_records<KIND, false><<<nblk, 128, 0, st>>>(MB);
@@ -448,7 +448,12 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, const Qua
     cudaFreeAsync(d_poff, st);
     return cuda_fail(e, "assemble/list");
   }
-  const size_t rec_bytes = sizeof(double) * ((size_t)nf * (npairs + nsrec) + (size_t)nfn * npairs);
+  // pair records in G = record_ranks chunks of cs pairs, chunk c = [bulk fields | near fields];
+  // rank r computes chunk r, an all-gather completes the others (one chunk without a communicator)
+  const int G = record_ranks(m);
+  const long long cs = G == 1 ? npairs : (npairs + G - 1) / G;
+  const long long rec_main = (long long)(nf + nfn) * cs * G;
+  const size_t rec_bytes = sizeof(double) * ((size_t)rec_main + (size_t)nf * nsrec);
   if ((e = storage_acquire(m->device, rec_bytes, st, (void**)&d_rec)) != cudaSuccess ||
       (e = cudaMallocAsync((void**)&d_ctr, sizeof(unsigned long long) * 15, st)) != cudaSuccess ||
       (e = cudaMemsetAsync(d_ctr, 0, sizeof(unsigned long long) * 15, st)) != cudaSuccess) {
@@ -473,9 +478,13 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, const Qua
   const int qfar = qc.q_near;
   MomArgs MB{d_rec, npairs, m->d_seg, m->d_half, m->d_dual, m->alpha, ng, q_bulk, qfar, d_ctr};
   MB.near_gap = qc.near_gap;
+  MB.cs = cs;
+  MB.nfc = nf + nfn;
+  MB.p_lo = G == 1 ? 0 : std::min(npairs, (long long)m->comm->rank * cs);
+  MB.p_hi = std::min(npairs, MB.p_lo + cs);
   MB.ell = m->htmin > 0.0 ? std::sqrt(4.0 * m->htmin / m->alpha) : 0.0;
   MomArgs MN = MB;
-  MN.rec = d_rec + (long long)nf * npairs;
+  MN.rec = d_rec + (long long)nf * cs;
   MN.list = d_list;
   // the near cells' nodes: s = t_{a+1} - t_a and t_{a+1} - t_{a-1} (and t_a - t_{a-1})
   {
@@ -489,13 +498,24 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, const Qua
   }
   MN.counters = d_ctr + 5;
   MomArgs MS = MB;
-  MS.rec = d_rec + (long long)nf * npairs + (long long)nfn * npairs;
-  MS.npairs = nsrec;
+  MS.rec = d_rec + rec_main;
+  MS.npairs = MS.cs = MS.p_hi = nsrec;
+  MS.p_lo = 0;
   MS.counters = d_ctr + 10;
   mark();
   if (kind == STB_V) launch_records<STB_V>(MB, MN, fused_sing ? &MS : nullptr, q_sing, st);
   else if (kind == STB_K) launch_records<STB_K>(MB, MN, fused_sing ? &MS : nullptr, q_sing, st);
   else launch_records<STB_D>(MB, MN, fused_sing ? &MS : nullptr, q_sing, st);
+  if (G > 1) {
+    bem_status gs = allgather_chunks(m, d_rec, (long long)(nf + nfn) * cs, st);
+    if (gs != BEM_OK) {
+      storage_release(m->device, d_rec, rec_bytes, st);
+      if (d_part) storage_release(m->device, d_part, part_bytes, st);
+      if (d_list) cudaFreeAsync(d_list, st);
+      cudaFreeAsync(d_poff, st);
+      return gs;
+    }
+  }
   mark();
   fam.push_back(3);
   A->launches += 2;

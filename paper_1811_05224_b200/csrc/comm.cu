@@ -34,6 +34,7 @@ struct NcclApi {
   ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
   ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
   bool ok = false;
 };
@@ -52,8 +53,9 @@ void load_nccl() {
   g_nccl.CommAbort = (decltype(g_nccl.CommAbort))dlsym(g_nccl.h, "ncclCommAbort");
   g_nccl.CommGetAsyncError = (decltype(g_nccl.CommGetAsyncError))dlsym(g_nccl.h, "ncclCommGetAsyncError");
   g_nccl.AllReduce = (decltype(g_nccl.AllReduce))dlsym(g_nccl.h, "ncclAllReduce");
+  g_nccl.AllGather = (decltype(g_nccl.AllGather))dlsym(g_nccl.h, "ncclAllGather");
   g_nccl.GetErrorString = (decltype(g_nccl.GetErrorString))dlsym(g_nccl.h, "ncclGetErrorString");
-  g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.CommDestroy && g_nccl.AllReduce;
+  g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.CommDestroy && g_nccl.AllReduce && g_nccl.AllGather;
 }
 bool nccl() {
   std::call_once(g_nccl_once, load_nccl);
@@ -135,6 +137,30 @@ static bem_status group_allreduce(bem_comm* c, double* buf, long long n, cudaStr
   return e == cudaSuccess ? BEM_OK : cuda_fail(e, "group all-reduce");
 }
 
+// in-place all-gather over the emulated ranks: each rank copies the other ranks' chunks into its
+// own buffer between two barriers (every chunk complete before; nobody reads after)
+static bem_status group_allgather(bem_comm* c, double* buf, long long chunk, cudaStream_t st) {
+  CommGroup* G = c->group;
+  const double t0 = now_s();
+  cudaError_t e = cudaStreamSynchronize(st);                      // this rank's chunk is complete
+  if (e != cudaSuccess) return cuda_fail(e, "group all-gather");
+  G->bufs[c->rank] = buf;
+  if (!G->barrier()) {
+    set_error("emulated-rank all-gather: the other ranks did not arrive (300 s)");
+    return BEM_E_STATE;
+  }
+  for (int r = 0; r < G->n && e == cudaSuccess; ++r)
+    if (r != c->rank && chunk > 0)
+      e = cudaMemcpyAsync(buf + r * chunk, G->bufs[r] + r * chunk, sizeof(double) * chunk, cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (!G->barrier()) {
+    set_error("emulated-rank all-gather: the other ranks did not arrive (300 s)");
+    return BEM_E_STATE;
+  }
+  if (t_timer) t_timer->host_s += now_s() - t0;
+  return e == cudaSuccess ? BEM_OK : cuda_fail(e, "group all-gather");
+}
+
 // ------------------------------------------------------------------ NCCL
 static bem_status nccl_check(bem_comm* c) {
   if (!c || !c->nccl) return BEM_OK;
@@ -192,6 +218,28 @@ bem_status allreduce_sum(const bem_mesh* m, double* buf, long long n, cudaStream
   if (!c || c->solo) return BEM_OK;   // solo rank: its partial sums stay as they are
   if (c->group) return group_allreduce(c, buf, n, st);
   return nccl_allreduce(c, buf, n, st);
+}
+
+int record_ranks(const bem_mesh* m) {
+  const bem_comm* c = m->comm;
+  return (!c || c->solo) ? 1 : c->nranks;
+}
+
+bem_status allgather_chunks(const bem_mesh* m, double* buf, long long chunk, cudaStream_t st) {
+  bem_comm* c = m->comm;
+  if (!c || c->solo || c->nranks == 1) return BEM_OK;
+  if (c->group) return group_allgather(c, buf, chunk, st);
+  if (!nccl()) return BEM_E_NCCL;
+  bem_status s = nccl_check(c);
+  if (s != BEM_OK) return s;
+  timer_mark(st);
+  // in place: the send buffer is the rank's own slot of the receive buffer
+  ncclResult_t r = g_nccl.AllGather(buf + (long long)c->rank * chunk, buf, (size_t)chunk, ncclDouble,
+                                    (ncclComm_t)c->nccl, st);
+  timer_mark(st);
+  if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather");
+  count_launch();
+  return BEM_OK;
 }
 
 bool comm_overlaps(const bem_mesh* m) { return m->comm && m->comm->nccl && m->comm->stream; }

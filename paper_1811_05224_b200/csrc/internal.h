@@ -269,6 +269,12 @@ void vec_combine(double* out, const double* Q, long long ldq, int k, const doubl
 void vec_mul(double* y, const double* d, const double* x, long long n, cudaStream_t st);
 // collectives (comm.cpp)
 bem_status allreduce_sum(const bem_mesh* m, double* buf, long long n, cudaStream_t st);
+// ranks that share the pair-record computation (nranks of a NCCL or emulated-rank communicator;
+// 1 without one and for a solo rank, which computes every record itself)
+int record_ranks(const bem_mesh* m);
+// in-place all-gather of G = record_ranks(m) chunks of `chunk` doubles: rank r's chunk is
+// buf[r * chunk, (r + 1) * chunk); afterwards every rank holds all G chunks (stream-ordered on st)
+bem_status allgather_chunks(const bem_mesh* m, double* buf, long long chunk, cudaStream_t st);
 // stream on which allreduce_sum_async runs the NCCL collective after waiting on `ready` (recorded
 // on the compute stream); the caller joins it back with comm_join.  Group / no communicator:
 // the plain allreduce_sum on st.

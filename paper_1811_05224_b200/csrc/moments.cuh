@@ -92,7 +92,16 @@ struct MomArgs {
                           // cells of at most ell (no subdivision while kappa <= 1)
   double near_gap;        // near records: distance ratio below which the measured orders apply
   int* list;              // D_h near records: [0] count, [1..] the near_special pairs (k_records appends)
+  // record layout: the pairs in chunks of cs, chunk c holding nfc fields of stride cs (one chunk,
+  // cs = npairs, on one rank).  Distributed (G ranks): rank r computes the pairs [p_lo, p_hi) of
+  // chunk r and the chunks are all-gathered
+  long long cs = 0;
+  int nfc = 0;
+  long long p_lo = 0, p_hi = 0;
 };
+__device__ __forceinline__ long long rec_base(const MomArgs& M, long long pair) {
+  return M.cs == M.npairs ? pair : (pair / M.cs) * M.nfc * M.cs + pair % M.cs;
+}
 
 // composite subdivision of a sub-pair: cells per direction.  R24: pairs
 // closer than 8 ell with elements longer than ell; R25 (NEAR: the near cells keep the ln c and 1/c
@@ -286,8 +295,8 @@ __device__ __forceinline__ void rec_points(const MomArgs& M, int I, int J, int l
 template <int KIND, bool NEAR, bool WARP>
 __device__ __forceinline__ void records_body(const MomArgs& M, long long pair, int lane) {
   const int I = (int)(pair / M.ng), J = (int)(pair % M.ng);
-  double* rec = M.rec + pair;
-  const long long S = M.npairs;
+  double* rec = M.rec + rec_base(M, pair);
+  const long long S = M.cs;
   const bool wr = !WARP || lane == 0;   // the lane that writes the record
   // one pass: c range, regime-A moments M_k = sum W c^k and the affine constants of both
   // families (the constants need c > 0 at every point: dropped at the end if one c is 0)
@@ -497,8 +506,8 @@ __device__ __forceinline__ bool near_special(const MomArgs& M, int I, int J) {
 // and the persistent warp kernel takes them from the list
 template <int KIND, bool NEAR, bool SPLIT = false>
 __global__ void __launch_bounds__(128) k_records(MomArgs M) {
-  const long long pair = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (pair >= M.npairs) return;
+  const long long pair = M.p_lo + (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (pair >= M.p_hi) return;
   if (SPLIT && near_special<KIND>(M, (int)(pair / M.ng), (int)(pair % M.ng))) {
     M.list[1 + atomicAdd(M.list, 1)] = (int)pair;
     return;
@@ -998,7 +1007,8 @@ __global__ void __launch_bounds__(128, KIND == STB_D ? 2 : 3) k_bulk_m(BlockArgs
     if (!any) return;
   }
   const long long pair = (long long)I * ng + J;
-  const long long S = M.npairs;
+  const long long S = M.cs;
+  const double* recp = M.rec + rec_base(M, pair);   // the pair's record (field stride S)
   // row offsets of the band rows a = r_lo + r for this warp's row I (panel offset + I * ld, or
   // the tile's offset + (I mod 32) * 32), shared by the warp: a store is one LDS + one address add
   __shared__ long long s_row[4][R];
@@ -1013,20 +1023,20 @@ __global__ void __launch_bounds__(128, KIND == STB_D ? 2 : 3) k_bulk_m(BlockArgs
   // stores: diagonal tiles of the symmetric packing keep their upper triangle only
   const bool vst = valid && (!B.sym || ti != tj || jcol >= I % SYM_TS);
   RegA<KIND> A;
-  A.load(M.rec + pair, S);
+  A.load(recp, S);
   // pairs without quadrature points (K_h on collinear elements: the kernel vanishes) hold
   // only zero entries: a warp of them writes zeros (or, in product mode, nothing) and skips the
   // node evaluations, counted as regime A (warp-uniform; the warp still joins the lag staging)
   const bool zero_warp = __all_sync(0xffffffffu, A.cmax == 0.0 && A.P[0] == 0.0 && A.l0 == 0.0);
   RegBZ<KIND> Z;
-  Z.load(M.rec + pair, S);
+  Z.load(recp, S);
   // the pair's regime-B Taylor coefficients, orders < BZ_KBS (and K's top entry), staged once in
   // shared memory: this thread's column of s_bz (only this thread reads it, no barrier needed)
   double* sbz = s_bz + threadIdx.x;
   int nsb = 0;
   if (!zero_warp && Z.c0 > 0.0) {
-    const double* R0 = M.rec + pair + (RF_COMMON + 0 * FAMSZ) * S;
-    const double* R1 = M.rec + pair + (RF_COMMON + 1 * FAMSZ) * S;
+    const double* R0 = recp + (RF_COMMON + 0 * FAMSZ) * S;
+    const double* R1 = recp + (RF_COMMON + 1 * FAMSZ) * S;
     nsb = min(Z.kb + 1, BZ_KBS);
     for (int i = 0; i < nsb; ++i) {
       sbz[i * BZS_STRIDE] = R0[(FB1 + i) * S];
@@ -1134,7 +1144,7 @@ __global__ void __launch_bounds__(128, KIND == STB_D ? 2 : 3) k_bulk_m(BlockArgs
         const double4 q = ndc[r], q2 = ndc[r2];
         int reg = 0, reg2 = 0;
         double v = 0.0, v2 = 0.0;
-        phi_bz2<KIND>(M.rec + pair, S, Z, q.x, q.z, q2.x, q2.z, v, v2, &reg, &reg2, sbz, nsb);
+        phi_bz2<KIND>(recp, S, Z, q.x, q.z, q2.x, q2.z, v, v2, &reg, &reg2, sbz, nsb);
         if (r2 == r) reg2 = 0;
         nB += (reg == 1) + (reg2 == 1);
         nK += (reg == 1 ? Z.kb : 0) + (reg2 == 1 ? Z.kb : 0);
@@ -1244,8 +1254,8 @@ __global__ void __launch_bounds__(128) k_near_m(BlockArgs B, MomArgs M, int chun
   const int a_end = min(B.a1, a_beg + chunk);
   if (B.sym && (int)(blockIdx.y * 4) / SYM_TS > (int)blockIdx.x) return;   // CTA-uniform (mirror tiles)
   const long long pair = (long long)I * ng + J;
-  const long long S = M.npairs;
-  const double* rec = M.rec + pair;
+  const long long S = M.cs;
+  const double* rec = M.rec + rec_base(M, pair);
   RegA<KIND> A;
   A.load(rec, S);
   RegBZ<KIND> Z;

@@ -128,3 +128,53 @@ def test_solo_rank_partials_sum_to_the_product(name, G):
     assert relmax(sums["Vx"], ref["Vx"]) <= 1e-13
     assert relmax(sums["Dx"], ref["Dx"]) <= 1e-13
     assert relmax(sums["Kg"] + half_mg.cpu().numpy(), ref["b"]) <= 1e-13
+
+
+@pytest.mark.parametrize("name,G", [("S32", 3), ("C2", 4), ("C2", 8)])
+def test_distributed_records_entries_bitwise(name, G):
+    """emulated ranks compute 1/G of the pair records each and all-gather them (assemble.cu,
+    DESIGN.md section 4.5): every owned entry equals the single-rank entry bit for bit and every
+    entry is owned by exactly one rank (the others read 0), so the sum over ranks is exact"""
+    w = W.get(name)
+    rng = np.random.default_rng(7)
+    rows = rng.integers(0, w.n, 40000)
+    cols = rng.integers(0, w.n, 40000)
+    cols = np.where(cols // w.n_gamma > rows // w.n_gamma, rows, cols)   # causal entries (b <= a)
+    m0 = S.Mesh.from_workload(w)
+    ref = {}
+    for k, f in (("V", m0.assemble_V), ("D", m0.assemble_D)):
+        A = f()
+        ref[k] = A.entries(rows, cols)
+        A.close()
+    m0.close()
+    comms = S.Comm.group(G, 0)
+    got, errs = [None] * G, []
+
+    def run(r):
+        try:
+            torch.cuda.set_device(0)
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                m = S.Mesh.from_workload(w, n_slices=2 * G, comm=comms[r])
+                out = {}
+                for k, f in (("V", m.assemble_V), ("D", m.assemble_D)):
+                    A = f(stream=st)
+                    out[k] = A.entries(rows, cols)
+                    A.close()
+                m.close()
+            got[r] = out
+        except Exception as e:   # noqa: BLE001
+            errs.append(repr(e))
+    th = [threading.Thread(target=run, args=(r,)) for r in range(G)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(600)
+    for c in comms:
+        c.close()
+    assert not errs, errs
+    for k in ("V", "D"):
+        nz = np.stack([got[r][k] != 0.0 for r in range(G)])
+        assert np.all(nz.sum(axis=0) <= 1), k                 # one owner per entry
+        tot = sum(got[r][k] for r in range(G))
+        assert np.array_equal(tot, ref[k]), (k, relmax(tot, ref[k]))

@@ -7,7 +7,11 @@ step of G GPUs is
     max_r (assembly_r + n_V gemv_V,r + n_D gemv_D,r)  +  n_coll x t_allreduce  +  replicated vector work
 with the products per solve of the measured single-GPU solve (n_V = it + 1, n_D = it + 2), one
 all-reduce of N doubles per product (t_allreduce ASSUMED, see --allreduce-us: NVLink all-reduce of
-0.5-0.8 MB, latency-bound) and the replicated Krylov work taken from the single-GPU solve.  It shows
+0.5-0.8 MB, latency-bound) and the replicated Krylov work taken from the single-GPU solve.  A solo
+rank computes every pair record itself; with a real communicator the records of V_h and D_h are
+split into G chunks and all-gathered (assemble.cu), which the projection models as
+    records_r -> records_r / G + (G - 1) / G x record_bytes / --allgather-gbs
+(record bytes from the field counts; the K_h g records are left replicated: conservative).  It shows
 the load balance of the ownership plan with the real kernels; it is not a scaling measurement.
 
 python tools/scaling_projection.py C5 [--allreduce-us 30]
@@ -23,6 +27,11 @@ import torch  # noqa: E402
 
 import workloads as W  # noqa: E402
 from paper_1811_05224_b200 import stbem as S  # noqa: E402
+
+
+# doubles per pair record, bulk + near fields (moments.cuh rec_fields + rec_fields_near)
+# (RF_COMMON + n_fam FAMSZ) + (R2_FAM + n_fam R2_FAMSZ) with FAMSZ = 139, R2_FAMSZ = 114
+REC_FIELDS = {"V": 144 + 118, "D": 283 + 232}
 
 
 def timed(fn):
@@ -65,6 +74,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("config", nargs="?", default="C5")
     ap.add_argument("--allreduce-us", type=float, default=30.0)
+    ap.add_argument("--allgather-gbs", type=float, default=400.0)   # ASSUMED NVLink all-gather bus bandwidth
     ap.add_argument("--pfac", type=int, default=2)   # P = pfac x G temporal slices
     args = ap.parse_args()
     w = W.get(args.config)
@@ -89,7 +99,13 @@ def main():
     for G in (1, 2, 4, 8):
         rank_work(w, G, 0, args.pfac)   # warm-up: the storage of this size is mapped once (first touch)
         ranks = [rank_work(w, G, r, args.pfac) for r in range(G)]
-        per = [rk["assembly_s"] + (it + 1) * rk["gemv_V_s"] + (it + 2) * rk["gemv_D_s"] for rk in ranks]
+        # distributed records: 1/G of the V_h, D_h records per rank plus their all-gather
+        rec_bytes = 8.0 * w.n_gamma ** 2 * (REC_FIELDS["V"] + REC_FIELDS["D"])
+        gather = (G - 1) / G * rec_bytes / (args.allgather_gbs * 1e9) if G > 1 else 0.0
+        for rk in ranks:
+            rk["records_distributed_s"] = rk["records_VD_s"] / G + gather
+        per = [rk["assembly_s"] - rk["records_VD_s"] + rk["records_distributed_s"]
+               + (it + 1) * rk["gemv_V_s"] + (it + 2) * rk["gemv_D_s"] for rk in ranks]
         n_coll = (2 * it + 4) if G > 1 else 0   # one per product + the fused right-hand side
         step = max(per) + replicated + n_coll * args.allreduce_us * 1e-6
         base = base or step
