@@ -317,6 +317,12 @@ bem_status bem_release_storage(void);
  * x_dev, out_dev: device arrays of length count. */
 bem_status bem_eval_special(int which, long long count, const double* x_dev, double* out_dev,
                             bem_stream stream);
+/* live FP64 DFMA rate of the current device (TFLOP/s, an FMA = 2 flops): a DFMA loop run back to
+ * back for `seconds` (0 < seconds <= 60) on a private stream, the rate of the second half written
+ * to *tflops_host.  The denominator of the assembly roofline in the power state of the moment (the
+ * FP64-bound kernels run under the board power cap: clocks below the maximum).  Synchronous.
+ * Errors: BEM_E_INVALID, BEM_E_CUDA. */
+bem_status bem_diag_fp64_rate(double seconds, double* tflops_host);
 
 #ifdef __cplusplus
 }

@@ -354,6 +354,11 @@ bem_status bem_eval_special(int which, long long count, const double* x, double*
   return eval_special(which, count, x, out, S(s));
 }
 
+bem_status bem_diag_fp64_rate(double seconds, double* tflops_host) {
+  if (!tflops_host || !(seconds > 0.0) || seconds > 60.0) { set_error("bem_diag_fp64_rate: 0 < seconds <= 60, non-null output"); return BEM_E_INVALID; }
+  return diag_fp64_rate(seconds, tflops_host);
+}
+
 // ------------------------------------------------------------------ GMRES
 bem_status bem_solve_gmres(const bem_matrix* V, const bem_matrix* D, const bem_matrix* M,
                            const double* b, double* w, const bem_gmres_opts* opts,

@@ -249,6 +249,7 @@ bem_status mass_apply(const bem_matrix* M, double a, const double* x, double b, 
 bem_status mass_solve(const bem_matrix* M, int transpose, const double* x, double* y,
                       cudaStream_t st);
 bem_status eval_special(int which, long long n, const double* x, double* out, cudaStream_t st);
+bem_status diag_fp64_rate(double seconds, double* tflops);
 bem_status eval_potential_initial(const bem_mesh* m, int nnode, const double* nodes, int ntri, const int* tris,
                                   const double* u0, long long npts, const double* pts, double* out,
                                   cudaStream_t st);

@@ -1112,6 +1112,62 @@ bem_status eval_special(int which, long long n, const double* x, double* out, cu
 }  // namespace stb
 
 namespace stb {
+// live FP64 rate (bem_diag_fp64_rate): 8 independent DFMA chains per thread, 256 threads, 8 CTAs
+// per SM -- the denominator of the assembly roofline measured in the thermal / power state of the
+// moment (the bulk kernels run under the board power cap)
+__global__ void __launch_bounds__(256) k_dfma_rate(double* out, int iters, double a, double b) {
+  double x[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) x[k] = threadIdx.x * 1e-9 + k * 1e-3;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) x[k] = fma(x[k], a, b);
+    }
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += x[k];
+  if (s == 12345.678) out[0] = s;   // keeps the chains alive
+}
+bem_status diag_fp64_rate(double seconds, double* tflops) {
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  double* d = nullptr;
+  cudaError_t e = cudaMalloc((void**)&d, sizeof(double));
+  if (e != cudaSuccess) return cuda_fail(e, "bem_diag_fp64_rate");
+  cudaStream_t st;
+  cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  const int grid = nsm * 8, tpb = 256, iters = 2000;
+  const double flops = 2.0 * grid * tpb * (double)iters * 16 * 8;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  // back to back for `seconds`; the rate of the second half (the sustained clock)
+  double total = 0.0, t_half = 0.0, fl_half = 0.0;
+  while (total < seconds) {
+    cudaEventRecord(e0, st);
+    for (int r = 0; r < 4; ++r) k_dfma_rate<<<grid, tpb, 0, st>>>(d, iters, 0.999999, 1e-7);
+    cudaEventRecord(e1, st);
+    if ((e = cudaEventSynchronize(e1)) != cudaSuccess) break;
+    float ms = 0.0f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (ms <= 0.0f) break;
+    total += 1e-3 * ms;
+    if (total >= 0.5 * seconds) { t_half += 1e-3 * ms; fl_half += 4.0 * flops; }
+  }
+  count_launch();
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaStreamDestroy(st);
+  cudaFree(d);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "bem_diag_fp64_rate");
+  *tflops = t_half > 0.0 ? fl_half / t_half / 1e12 : 0.0;
+  return BEM_OK;
+}
 __global__ void k_gather(const double* __restrict__ data, const long long* __restrict__ offs, long long n,
                          double* __restrict__ out) {
   const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;

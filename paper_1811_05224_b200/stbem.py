@@ -127,6 +127,7 @@ _SIGS = {
     "bem_matrix_destroy": (None, [P]),
     "bem_release_storage": (I, []),
     "bem_eval_special": (I, [I, LL, P, P, P]),
+    "bem_diag_fp64_rate": (I, [ctypes.c_double, P]),
 }
 
 
@@ -425,6 +426,13 @@ def solve_gmres(V, b, w, D=None, M=None, rel_tol=1e-10, max_iter=500, precond=0,
     if history:
         r["history"] = hist[: rep.iterations + 1].tolist()
     return r
+
+
+def diag_fp64_rate(seconds=1.0):
+    """live FP64 DFMA rate (TFLOP/s) of the current device over `seconds` (bem_diag_fp64_rate)"""
+    out = ctypes.c_double(0.0)
+    check(lib().bem_diag_fp64_rate(float(seconds), ctypes.addressof(out)))
+    return out.value
 
 
 def eval_special(which, x, out, stream=None):

@@ -30,8 +30,8 @@ from paper_1811_05224_b200 import stbem as S  # noqa: E402
 
 
 # doubles per pair record, bulk + near fields (moments.cuh rec_fields + rec_fields_near)
-# (RF_COMMON + n_fam FAMSZ) + (R2_FAM + n_fam R2_FAMSZ) with FAMSZ = 139, R2_FAMSZ = 114
-REC_FIELDS = {"V": 144 + 118, "D": 283 + 232}
+# nf + nfn: rec_fields = RF_COMMON + n_fam FAMSZ, rec_fields_near = rec_fields + R2_FAM + n_fam R2_FAMSZ
+REC_FIELDS = {"V": 144 + 262, "D": 283 + 515}
 
 
 def timed(fn):
