@@ -428,14 +428,14 @@ def native(args):
                  "bytes_note": "algorithmic: 8 B per stored double of the product's matrix (block lower "
                                "triangle; V_h / D_h symmetric packed spatial blocks) + 16 N"}
     if args.variant == "toeplitz":
-        # the product is the FP64 tensor-core GEMM k_toeplitz_mm: algorithmic flops per product
+        # the product is the FP64 tensor-core GEMM k_toeplitz_tma (TMA-staged DMMA): algorithmic flops per product
         # 2 ng^2 sum_a (a + 1) (the block lower triangle of lags) against the measured DMMA peak
         ng_, nt_t = w.n_gamma, w.n_steps
         fl = 2.0 * ng_ * ng_ * nt_t * (nt_t + 1) / 2
         tf = fl / gemv_s / 1e12 if gemv_s > 0 else None
-        roof_gemv = {"bound": "tensor", "kernel": "k_toeplitz_mm", "achieved": tf, "peak": FP64_TC_PEAK,
+        roof_gemv = {"bound": "tensor", "kernel": "k_toeplitz_tma<256,32,3>", "achieved": tf, "peak": FP64_TC_PEAK,
                      "unit": "TFLOP/s", "frac": (tf / FP64_TC_PEAK) if tf else None,
-                     "traffic": traffic.get("k_toeplitz_mm"),
+                     "traffic": traffic.get("k_toeplitz_tma"),
                      "flops_per_launch": fl,
                      "peak_note": "FP64 tensor cores (DMMA m8n8k4) measured 37.1 TFLOP/s on this pool's B200 "
                                   "(profiles/r01_dmma_peak.txt; DFMA 34.1)",

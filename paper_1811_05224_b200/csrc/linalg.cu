@@ -561,9 +561,14 @@ __global__ void __launch_bounds__(256, 2) k_toeplitz_mm(const double* __restrict
 // b < 0 are zero-filled by the TMA unit), 128-byte swizzled in shared memory so that the DMMA
 // fragment loads (8 rows x 16 B per quarter warp) stay conflict-free without row padding.  Same
 // tiles, work units, warp layout and k order as k_toeplitz_mm.
-constexpr int TZ_TSTAGE = (TZ_TI + TZ_TA) * TZ_TK;                 // doubles per stage
-constexpr int TZ_TSTAGES = 4;                                       // TMA pipeline depth
-constexpr size_t TZ_TMA_SMEM = sizeof(double) * TZ_TSTAGES * TZ_TSTAGE + 1024 + 128;
+// Tile shapes (TI x TA, pipeline depth NS): 128 x 64 (4 stages) or 256 x 32 (3 stages; halves the
+// zero triangle of each a-tile's last lag chunk, TA^2 / 2 per tile, at twice the T-tile traffic
+// from L2).  8 warps of 32 x 32: TI / 32 in i, TA / 32 in a.
+template <int TI, int TA, int NS>
+struct TzShape {
+  static constexpr int stage = (TI + TA) * TZ_TK;                   // doubles per stage
+  static constexpr size_t smem = sizeof(double) * NS * stage + 1024 + 128;
+};
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
   asm volatile(
@@ -576,25 +581,50 @@ __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
 __device__ __forceinline__ const double2* swz(const double* base, int r, int k) {
   return reinterpret_cast<const double2*>(base + r * TZ_TK + ((((k >> 1) ^ (r & 7))) << 1));
 }
+// one K step (16 deep) of a warp's 32 x 32 tile, the 8-column tiles v >= V0 (V0 = 0: all; skipping
+// the causal triangle's zero tiles with V0 > 0 per lag measured slower)
+template <int V0>
+__device__ __forceinline__ void tz_mma(double (&acc)[TZ_UI][TZ_VA][2], const double* Ts, const double* Xs, int wi,
+                                       int wa, int fr, int fc) {
+#pragma unroll
+  for (int h = 0; h < TZ_TK / 8; ++h) {
+    double2 af[TZ_UI], bf[TZ_VA];
+#pragma unroll
+    for (int u = 0; u < TZ_UI; ++u) af[u] = *swz(Ts, wi + 8 * u + fc, 4 * fr + 2 * h);
+#pragma unroll
+    for (int v = V0; v < TZ_VA; ++v) bf[v] = *swz(Xs, wa + 8 * v + fc, 4 * fr + 2 * h);
+#pragma unroll
+    for (int u = 0; u < TZ_UI; ++u)
+#pragma unroll
+      for (int v = V0; v < TZ_VA; ++v) dmma_8x8x4(acc[u][v], af[u].x, bf[v].x);
+#pragma unroll
+    for (int u = 0; u < TZ_UI; ++u)
+#pragma unroll
+      for (int v = V0; v < TZ_VA; ++v) dmma_8x8x4(acc[u][v], af[u].y, bf[v].y);
+  }
+}
+template <int TI, int TA, int NS>
 __global__ void __launch_bounds__(256, 2) k_toeplitz_tma(const __grid_constant__ CUtensorMap tmT,
                                                      const __grid_constant__ CUtensorMap tmX, int ng, int nt,
                                                      int dpz, double* __restrict__ part) {
+  constexpr int TZ_TSTAGES = NS, TZ_TSTAGE = TzShape<TI, TA, NS>::stage, NWI = TI / 32;
+  static_assert(NWI * (TA / 32) == 8, "8 warps of 32 x 32");
   extern __shared__ __align__(16) unsigned char tz_raw[];
   // 1024-byte aligned stages (the swizzle pattern repeats every 8 rows of 128 B)
   double* tz = reinterpret_cast<double*>((reinterpret_cast<size_t>(tz_raw) + 1023) & ~size_t(1023));
   unsigned long long* bar = reinterpret_cast<unsigned long long*>(tz + TZ_TSTAGES * TZ_TSTAGE);   // full
   unsigned long long* ebar = bar + TZ_TSTAGES;                                                  // empty
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wi = (warp & 3) * (8 * TZ_UI), wa = (warp >> 2) * (8 * TZ_VA), fr = lane & 3, fc = lane >> 2;
-  const int nti = (ng + TZ_TI - 1) / TZ_TI;
+  const int wi = (warp % NWI) * (8 * TZ_UI), wa = (warp / NWI) * (8 * TZ_VA), fr = lane & 3, fc = lane >> 2;
+  const int nti = (ng + TI - 1) / TI;
   int r = blockIdx.x, at = 0;
   for (;; ++at) {
-    const int cnt = nti * ((min(nt, (at + 1) * TZ_TA) + dpz - 1) / dpz);
+    const int cnt = nti * ((min(nt, (at + 1) * TA) + dpz - 1) / dpz);
     if (r < cnt) break;
     r -= cnt;
   }
-  const int chunk = r / nti, i0 = (r % nti) * TZ_TI, a0 = at * TZ_TA;
-  const int d0 = chunk * dpz, d1 = min(min(nt, d0 + dpz), a0 + TZ_TA);
+  const int chunk = r / nti, i0 = (r % nti) * TI, a0 = at * TA;
+  const int d0 = chunk * dpz, d1 = min(min(nt, d0 + dpz), a0 + TA);
   const int nj = (ng + TZ_TK - 1) / TZ_TK;
   const int nsteps = max(0, d1 - d0) * nj;
   if (tid == 0) {
@@ -608,7 +638,7 @@ __global__ void __launch_bounds__(256, 2) k_toeplitz_tma(const __grid_constant__
   auto issue = [&](int step) {   // thread 0
     const int s = step % TZ_TSTAGES;
     double* Ts = tz + s * TZ_TSTAGE;
-    double* Xs = Ts + TZ_TI * TZ_TK;
+    double* Xs = Ts + TI * TZ_TK;
     const int d = d0 + step / nj, j0 = (step % nj) * TZ_TK;
     const unsigned b = smem_u32(bar + s);
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(b), "r"((unsigned)(sizeof(double) * TZ_TSTAGE)) : "memory");
@@ -633,24 +663,8 @@ __global__ void __launch_bounds__(256, 2) k_toeplitz_tma(const __grid_constant__
     const int st_ = step % TZ_TSTAGES;
     const unsigned ph = (unsigned)((step / TZ_TSTAGES) & 1);
     mbar_wait(smem_u32(bar + st_), ph);
-    const double* Ts = tz + (step % TZ_TSTAGES) * TZ_TSTAGE;
-    const double* Xs = Ts + TZ_TI * TZ_TK;
-#pragma unroll
-    for (int h = 0; h < TZ_TK / 8; ++h) {
-      double2 af[TZ_UI], bf[TZ_VA];
-#pragma unroll
-      for (int u = 0; u < TZ_UI; ++u) af[u] = *swz(Ts, wi + 8 * u + fc, 4 * fr + 2 * h);
-#pragma unroll
-      for (int v = 0; v < TZ_VA; ++v) bf[v] = *swz(Xs, wa + 8 * v + fc, 4 * fr + 2 * h);
-#pragma unroll
-      for (int u = 0; u < TZ_UI; ++u)
-#pragma unroll
-        for (int v = 0; v < TZ_VA; ++v) dmma_8x8x4(acc[u][v], af[u].x, bf[v].x);
-#pragma unroll
-      for (int u = 0; u < TZ_UI; ++u)
-#pragma unroll
-        for (int v = 0; v < TZ_VA; ++v) dmma_8x8x4(acc[u][v], af[u].y, bf[v].y);
-    }
+    const double* Ts = tz + st_ * TZ_TSTAGE;
+    tz_mma<0>(acc, Ts, Ts + TI * TZ_TK, wi, wa, fr, fc);
     __syncwarp();
     if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(ebar + st_)) : "memory");
     if (tid == 0 && step + TZ_TSTAGES < nsteps) {
@@ -699,6 +713,24 @@ __global__ void k_toeplitz_reduce(const double* __restrict__ part, int nsplit, l
   y[r] = (beta == 0.0) ? alpha * s : fma(alpha, s, beta * y[r]);
 }
 
+// one TMA tile shape's launch: tensor maps, occupancy, lag chunk, units (false: not applicable)
+struct TzLaunch {
+  int ti, ta, ns, ctas;
+  size_t smem;
+  void (*kern)(CUtensorMap, CUtensorMap, int, int, int, double*);
+};
+template <int TI, int TA, int NS>
+static TzLaunch tz_launch() {
+  static int ctas = 0;
+  const size_t smem = TzShape<TI, TA, NS>::smem;
+  if (!ctas) {
+    cudaFuncSetAttribute(k_toeplitz_tma<TI, TA, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas, k_toeplitz_tma<TI, TA, NS>, 256, smem) != cudaSuccess || ctas < 1) ctas = 1;
+  }
+  return TzLaunch{TI, TA, NS, ctas, smem,
+                  reinterpret_cast<void (*)(CUtensorMap, CUtensorMap, int, int, int, double*)>(k_toeplitz_tma<TI, TA, NS>)};
+}
+
 bem_status toeplitz_gemv(const bem_matrix* A, double a, const double* x, double b, double* y,
                          cudaStream_t st) {
   const bem_mesh* m = A->mesh;
@@ -711,12 +743,35 @@ bem_status toeplitz_gemv(const bem_matrix* A, double a, const double* x, double 
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tz_ctas, k_toeplitz_mm, 256, TZ_SMEM) != cudaSuccess || tz_ctas < 1) tz_ctas = 1;
     attr = true;
   }
+  const long long ldT_d = A->poff.size() > 1 ? A->poff[1] - A->poff[0] : 0;
+  // TMA path: tensor maps of T (j, i, d) and of this product's x (j, b); the strides must be
+  // multiples of 16 bytes (N_Gamma even) and x 16-byte aligned -- otherwise the cp.async kernel
+  static const bool no_tma = getenv("BEM_TOEPLITZ_NO_TMA") != nullptr;
+  static const int shape = getenv("BEM_TZ_SHAPE") ? atoi(getenv("BEM_TZ_SHAPE")) : 1;
+  EncodeTiledFn enc = no_tma ? nullptr : encode_tiled();
+  bool tma = enc && ng % 2 == 0 && ((size_t)x & 15) == 0 && ldT_d > 0 && nt > 1;
+  TzLaunch L{TZ_TI, TZ_TA, TZ_STAGES, tz_ctas, TZ_SMEM, nullptr};
+  if (tma) L = shape == 0 ? tz_launch<128, 64, 4>() : (shape == 2 ? tz_launch<256, 32, 4>() : tz_launch<256, 32, 3>());
+  CUtensorMap tmT, tmX;
+  if (tma) {
+    const cuuint64_t gT[3] = {(cuuint64_t)ng, (cuuint64_t)ng, (cuuint64_t)nt};
+    const cuuint64_t sT[2] = {(cuuint64_t)pad4(ng) * 8, (cuuint64_t)ldT_d * 8};
+    const cuuint32_t bT[3] = {TZ_TK, (cuuint32_t)L.ti, 1}, one3[3] = {1, 1, 1};
+    const cuuint64_t gX[2] = {(cuuint64_t)ng, (cuuint64_t)nt};
+    const cuuint64_t sX[1] = {(cuuint64_t)ng * 8};
+    const cuuint32_t bX[2] = {TZ_TK, (cuuint32_t)L.ta}, one2[2] = {1, 1};
+    tma = enc(&tmT, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)A->data, gT, sT, bT, one3, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS &&
+          enc(&tmX, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)x, gX, sX, bX, one2, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
+  if (!tma) L = TzLaunch{TZ_TI, TZ_TA, TZ_STAGES, tz_ctas, TZ_SMEM, nullptr};   // the cp.async kernel
   // lag chunk dpz: minimise the busiest SM's time, (units per SM) x (dpz + 4), where two co-resident
   // units share the SM's FP64 tensor pipe at ~1.15x the throughput of one (C4 measured)
-  const int nti = (ng + TZ_TI - 1) / TZ_TI, nta = (nt + TZ_TA - 1) / TZ_TA, sms = num_sms();
+  const int nti = (ng + L.ti - 1) / L.ti, nta = (nt + L.ta - 1) / L.ta, sms = num_sms();
   auto units = [&](int dz) {
     long long u = 0;
-    for (int at = 0; at < nta; ++at) u += (long long)nti * ((std::min(nt, (at + 1) * TZ_TA) + dz - 1) / dz);
+    for (int at = 0; at < nta; ++at) u += (long long)nti * ((std::min(nt, (at + 1) * L.ta) + dz - 1) / dz);
     return u;
   };
   int dpz = nt;
@@ -724,7 +779,7 @@ bem_status toeplitz_gemv(const bem_matrix* A, double a, const double* x, double 
   for (int dz = std::min(nt, 8); dz <= nt; ++dz) {
     const long long u = units(dz);
     const long long per_sm = (u + sms - 1) / sms;
-    const double cost = (double)per_sm * (dz + 4) / (per_sm >= 2 && tz_ctas >= 2 ? 1.15 : 1.0);   // + 4: fill / epilogue
+    const double cost = (double)per_sm * (dz + 4) / (per_sm >= 2 && L.ctas >= 2 ? 1.15 : 1.0);   // + 4: fill / epilogue
     if (cost < best) best = cost, dpz = dz;
   }
   const long long nunits = units(dpz);
@@ -734,32 +789,8 @@ bem_status toeplitz_gemv(const bem_matrix* A, double a, const double* x, double 
   cudaError_t e = storage_acquire(m->device, bytes, st, (void**)&part);
   if (e != cudaSuccess) return cuda_fail(e, "toeplitz product");
   e = cudaMemsetAsync(part, 0, bytes, st);   // lag ranges beyond a tile's columns leave their slots zero
-  const long long ldT_d = A->poff.size() > 1 ? A->poff[1] - A->poff[0] : 0;
-  // TMA path: tensor maps of T (j, i, d) and of this product's x (j, b); the strides must be
-  // multiples of 16 bytes (N_Gamma even) and x 16-byte aligned -- otherwise the cp.async kernel
-  static bool tma_attr = false;
-  static const bool no_tma = getenv("BEM_TOEPLITZ_NO_TMA") != nullptr;
-  EncodeTiledFn enc = no_tma ? nullptr : encode_tiled();
-  bool tma = enc && ng % 2 == 0 && ((size_t)x & 15) == 0 && ldT_d > 0 && nt > 1;
-  CUtensorMap tmT, tmX;
   if (tma) {
-    const cuuint64_t gT[3] = {(cuuint64_t)ng, (cuuint64_t)ng, (cuuint64_t)nt};
-    const cuuint64_t sT[2] = {(cuuint64_t)pad4(ng) * 8, (cuuint64_t)ldT_d * 8};
-    const cuuint32_t bT[3] = {TZ_TK, TZ_TI, 1}, one3[3] = {1, 1, 1};
-    const cuuint64_t gX[2] = {(cuuint64_t)ng, (cuuint64_t)nt};
-    const cuuint64_t sX[1] = {(cuuint64_t)ng * 8};
-    const cuuint32_t bX[2] = {TZ_TK, TZ_TA}, one2[2] = {1, 1};
-    tma = enc(&tmT, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)A->data, gT, sT, bT, one3, CU_TENSOR_MAP_INTERLEAVE_NONE,
-              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS &&
-          enc(&tmX, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)x, gX, sX, bX, one2, CU_TENSOR_MAP_INTERLEAVE_NONE,
-              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-  }
-  if (tma) {
-    if (!tma_attr) {
-      cudaFuncSetAttribute(k_toeplitz_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TZ_TMA_SMEM);
-      tma_attr = true;
-    }
-    k_toeplitz_tma<<<(unsigned)nunits, 256, TZ_TMA_SMEM, st>>>(tmT, tmX, ng, nt, dpz, part);
+    L.kern<<<(unsigned)nunits, 256, L.smem, st>>>(tmT, tmX, ng, nt, dpz, part);
   } else {
     k_toeplitz_mm<<<(unsigned)nunits, 256, TZ_SMEM, st>>>(A->data, ldT_d, (int)pad4(ng), x, ng, nt, dpz, part);
   }

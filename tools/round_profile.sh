@@ -31,6 +31,8 @@ for K in D Kg V; do
 done
 ncu --set full --clock-control none --import-source on -k regex:k_records -s 1 -c 2 -o $O/rec_D_near_C5 \
     python tools/prof_probe.py C5 D > $O/ncu_rec.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_toeplitz_tma -s 4 -c 1 -o $O/toeplitz_C4 \
+    python bench.py --variant toeplitz --config C4 --steps 1 --warmup 3 --no-cpu-baseline --no-isolated > $O/ncu_tz.log 2>&1
 # text summaries on the box (gpurun copies back at most 64 MiB): keep the GEMV and K g reports
 for f in $O/*.ncu-rep; do
   b=$(basename $f .ncu-rep)
