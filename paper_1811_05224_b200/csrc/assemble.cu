@@ -295,19 +295,24 @@ __global__ void __launch_bounds__(128) k_sing(BlockArgs B, const Seg* __restrict
 
 // ================================================================= launch
 // which: 0 bulk cells (k_bulk_m), 1 near cells (k_near_m)
+template <int KIND, int R, bool PROD>
+static void launch_bulk(const BlockArgs& BA, const MomArgs& M, dim3 grid, cudaStream_t st, BulkList L) {
+  constexpr size_t smem = bulk_smem_bytes<KIND, R>();
+  static bool attr = false;   // per template instance
+  if (!attr) {
+    cudaFuncSetAttribute(k_bulk_m<KIND, R, PROD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  k_bulk_m<KIND, R, PROD><<<grid, 128, smem, st>>>(BA, L, M);
+}
 template <int KIND, bool PROD = false>
 static void launch_kind(int which, const BlockArgs& BA, const MomArgs& M, int ng, int nband_or_chunk,
-                        int nz, cudaStream_t st, BulkList L = BulkList{nullptr, 0}) {
+                        int nz, cudaStream_t st, BulkList L = BulkList{nullptr, 0}, int R_ = 0) {
   dim3 grid((ng + 31) / 32, (ng + 3) / 4, nz);
-  if (which == 0) {
-    constexpr int R = bulk_r<KIND>();
-    constexpr size_t smem = bulk_smem_bytes<KIND, R>();
-    static bool attr = false;   // per template instance
-    if (!attr) {
-      cudaFuncSetAttribute(k_bulk_m<KIND, R, PROD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr = true;
-    }
-    k_bulk_m<KIND, R, PROD><<<grid, 128, smem, st>>>(BA, L, M);
+  if (which == 0 && KIND != STB_D && R_ == 8) {
+    launch_bulk<KIND, 8, PROD>(BA, M, grid, st, L);
+  } else if (which == 0) {
+    launch_bulk<KIND, bulk_r<KIND>(), PROD>(BA, M, grid, st, L);
   }
   else k_near_m<KIND, PROD><<<grid, 128, 0, st>>>(BA, M, nband_or_chunk);
   count_launch();
@@ -528,7 +533,26 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, const Qua
   // bulk cells: ONE launch over all owned blocks (band z of every block in each CTA: the per-pair
   // setup -- records, regime-B coefficients -- is paid once per CTA; a rank of the cyclic plan owns
   // ~P/2 + 1 small blocks, which per-block launches left setup-bound)
-  const int Rb = (kind == STB_D && !prod) ? bulk_r<STB_D>() : bulk_r<STB_V>();   // band of k_bulk_m
+  // band height of k_bulk_m: every band evaluates R + 1 node rows per trial column whatever its
+  // height, so the blocks' row counts decide: V_h and K_h g take 8 (one spill-penalised kernel, +4%
+  // per node on C5) when that needs fewer node rows than 7 -- a rank's small blocks of 2^k steps
+  // (16 steps: bands 7 + 7 + 2 cost 24 rows per column against 2 x 9 = 18); D_h always 8
+  auto node_rows = [&](int R) {
+    double c = 0.0;
+    for (size_t bi = 0; bi < blocks_of(A).size(); ++bi) {
+      const Block& b = blocks_of(A)[bi];
+      const int nband = (b.a1 - b.a0 + R - 1) / R;
+      for (int band = 0; band < nband; ++band) {
+        const int r_hi = b.a1 - R * band;
+        const int bmax = std::min(b.b1 - 1, r_hi - 1 - 2);
+        if (bmax >= b.b0) c += (double)(R + 1) * (bmax + 2 - b.b0);
+      }
+    }
+    return c;
+  };
+  const int Rb = (kind == STB_D && !prod) ? bulk_r<STB_D>()
+                 : (node_rows(8) * 1.04 < node_rows(7) ? 8 : bulk_r<STB_V>());
+  A->bulk_r = Rb;
   {
     std::vector<BulkBlock> bl;
     int nzmax = 0;
@@ -561,10 +585,10 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, const Qua
       BA.ntile = ntile;
       BA.ell = MB.ell;
       const BulkList L{d_bl, (int)bl.size()};
-      if (prod) launch_kind<STB_K, true>(0, BA, MB, ng, nzmax, nzmax, st, L);
-      else if (kind == STB_V) launch_kind<STB_V>(0, BA, MB, ng, nzmax, nzmax, st, L);
-      else if (kind == STB_K) launch_kind<STB_K>(0, BA, MB, ng, nzmax, nzmax, st, L);
-      else launch_kind<STB_D>(0, BA, MB, ng, nzmax, nzmax, st, L);
+      if (prod) launch_kind<STB_K, true>(0, BA, MB, ng, nzmax, nzmax, st, L, Rb);
+      else if (kind == STB_V) launch_kind<STB_V>(0, BA, MB, ng, nzmax, nzmax, st, L, Rb);
+      else if (kind == STB_K) launch_kind<STB_K>(0, BA, MB, ng, nzmax, nzmax, st, L, Rb);
+      else launch_kind<STB_D>(0, BA, MB, ng, nzmax, nzmax, st, L, Rb);
       mark();
       fam.push_back(0);
       A->launches++;

@@ -123,6 +123,7 @@ struct bem_mesh_s {
 enum { STB_V = 0, STB_K = 1, STB_D = 2, STB_MASS = 3 };
 
 struct bem_matrix_s {
+  int bulk_r = 0;                  // band height (test steps) of the bulk kernel of the last assembly
   int kind = 0;
   const bem_mesh* mesh = nullptr;
   // every device buffer of the matrix is allocated and freed stream-ordered on this stream (the
