@@ -984,8 +984,11 @@ __device__ __forceinline__ void cp_async16_bulk(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(sa), "l"(gmem));
 }
+#ifndef STB_BULK_MINB_K
+#define STB_BULK_MINB_K 3   // CTAs per SM the K_h bulk kernels are register-budgeted for
+#endif
 template <int KIND, int R, bool PROD = false>
-__global__ void __launch_bounds__(128, KIND == STB_D ? 2 : 3) k_bulk_m(BlockArgs B, BulkList L, MomArgs M) {
+__global__ void __launch_bounds__(128, KIND == STB_D ? 2 : (KIND == STB_K ? STB_BULK_MINB_K : 3)) k_bulk_m(BlockArgs B, BulkList L, MomArgs M) {
   const int ng = B.ng;
   const int lane = threadIdx.x & 31;
   const int J0 = blockIdx.x * 32 + lane;
@@ -1079,9 +1082,10 @@ __global__ void __launch_bounds__(128, KIND == STB_D ? 2 : 3) k_bulk_m(BlockArgs
   double accp[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) accp[r] = 0.0;
-  double Gp[R];
+  double Gp[PROD ? 1 : R];   // stored mode: the previous column's node differences
 #pragma unroll
-  for (int r = 0; r < R; ++r) Gp[r] = 0.0;
+  for (int r = 0; r < (PROD ? 1 : R); ++r) Gp[r] = 0.0;
+  double gprev = 0.0;        // product mode: g of the previous trial step (0 before b0)
   for (int y = Bk.b0; y <= bmax + 1; ++y) {
     const int kc = y - Bk.b0;
     if (kc % LAG_CH == 0) {                          // CTA-uniform: chunk kc / LAG_CH is needed
@@ -1177,45 +1181,44 @@ __global__ void __launch_bounds__(128, KIND == STB_D ? 2 : 3) k_bulk_m(BlockArgs
 #pragma unroll
       for (int r = 0; r <= R; ++r) phi[r] = sp[r * 128];
     }
-    if (y > Bk.b0) {
+    if (PROD) {
+      // K_h g by summation by parts over the trial steps: with G_y = phi_y[r] - phi_y[r-1] the
+      // row's entries are E_b = G_b - G_{b+1}, and sum_b E_b g_b = sum_y G_y (g~_y - g~_{y-1}),
+      // g~_y = g_y on the row's bulk columns b0 <= y <= min(bmax, a - 2), 0 elsewhere (the same
+      // sum, re-associated: no previous-column G per row is kept)
+      const double gv = (valid && y <= bmax) ? B.g[(long long)y * ng + J] : 0.0;
+      if (y <= r_lo - 2 && r_hi - r_lo == R) {      // interior column: g~ = g for every row
+        const double dg = gv - gprev;
+#pragma unroll
+        for (int r = 1; r <= R; ++r) accp[r - 1] = fma(phi[r] - phi[r - 1], dg, accp[r - 1]);
+      } else {
+#pragma unroll
+        for (int r = 1; r <= R; ++r) {
+          const int a = r_lo + r - 1;
+          const double dg = (y <= a - 2 ? gv : 0.0) - (y - 1 <= a - 2 ? gprev : 0.0);
+          if (a < r_hi) accp[r - 1] = fma(phi[r] - phi[r - 1], dg, accp[r - 1]);
+        }
+      }
+      gprev = gv;
+    } else if (y > Bk.b0) {
       const int b = y - 1;
       // interior column: every band row is a full bulk cell (no per-row conditions)
       const bool interior = b <= r_lo - 2 && r_hi - r_lo == R;
-      if (PROD) {
-        const double gv = valid ? B.g[(long long)b * ng + J] : 0.0;
-        if (interior) {
+      double* col = B.out + ((long long)(b - Bk.b0) * cstride + jcol);
+      if (interior && vst) {
 #pragma unroll
-          for (int r = 1; r <= R; ++r) {
-            const double G = phi[r] - phi[r - 1];
-            accp[r - 1] = fma(Gp[r - 1] - G, gv, accp[r - 1]);
-            Gp[r - 1] = G;
-          }
-        } else {
-#pragma unroll
-          for (int r = 1; r <= R; ++r) {
-            const int a = r_lo + r - 1;
-            const double G = phi[r] - phi[r - 1];
-            if (a < r_hi && a - b >= 2) accp[r - 1] = fma(Gp[r - 1] - G, gv, accp[r - 1]);
-            Gp[r - 1] = G;
-          }
+        for (int r = 1; r <= R; ++r) {
+          const double G = phi[r] - phi[r - 1];
+          col[srow[r - 1]] = Gp[r - 1] - G;
+          Gp[r - 1] = G;
         }
       } else {
-        double* col = B.out + ((long long)(b - Bk.b0) * cstride + jcol);
-        if (interior && vst) {
 #pragma unroll
-          for (int r = 1; r <= R; ++r) {
-            const double G = phi[r] - phi[r - 1];
-            col[srow[r - 1]] = Gp[r - 1] - G;
-            Gp[r - 1] = G;
-          }
-        } else {
-#pragma unroll
-          for (int r = 1; r <= R; ++r) {
-            const int a = r_lo + r - 1;
-            const double G = phi[r] - phi[r - 1];
-            if (vst && a < r_hi && a - b >= 2) col[srow[r - 1]] = Gp[r - 1] - G;
-            Gp[r - 1] = G;
-          }
+        for (int r = 1; r <= R; ++r) {
+          const int a = r_lo + r - 1;
+          const double G = phi[r] - phi[r - 1];
+          if (vst && a < r_hi && a - b >= 2) col[srow[r - 1]] = Gp[r - 1] - G;
+          Gp[r - 1] = G;
         }
       }
     } else {
