@@ -399,7 +399,8 @@ def native(args):
             if tj.get("config") == args.config:
                 traffic[tj["kernel"]] = tj["traffic_bytes_per_launch"]
     try:
-        fp64_live = S.diag_fp64_rate(2.0) if args.variant != "toeplitz" else None
+        # context for the isolated pass (skipped with it: a launch-list run measures the step only)
+        fp64_live = S.diag_fp64_rate(2.0) if (args.variant != "toeplitz" and iso) else None
     except Exception:
         fp64_live = None
     roof_asm = {"bound": "alu", "kernel": f"k_bulk_m<{kdom}>", "achieved": achieved, "peak": FP64_PEAK_DERIVED,

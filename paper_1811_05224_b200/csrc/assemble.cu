@@ -295,15 +295,23 @@ __global__ void __launch_bounds__(128) k_sing(BlockArgs B, const Seg* __restrict
 
 // ================================================================= launch
 // which: 0 bulk cells (k_bulk_m), 1 near cells (k_near_m)
-template <int KIND, int R, bool PROD>
-static void launch_bulk(const BlockArgs& BA, const MomArgs& M, dim3 grid, cudaStream_t st, BulkList L) {
+template <int KIND, int R, bool PROD, bool MULTI>
+static void launch_bulk_t(const BlockArgs& BA, const MomArgs& M, dim3 grid, cudaStream_t st, BulkList L) {
   constexpr size_t smem = bulk_smem_bytes<KIND, R>();
   static bool attr = false;   // per template instance
   if (!attr) {
-    cudaFuncSetAttribute(k_bulk_m<KIND, R, PROD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_bulk_m<KIND, R, PROD, MULTI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  k_bulk_m<KIND, R, PROD><<<grid, 128, smem, st>>>(BA, L, M);
+  k_bulk_m<KIND, R, PROD, MULTI><<<grid, 128, smem, st>>>(BA, L, M);
+}
+// one block: its geometry in BA (the single-block kernel); several: the list L
+template <int KIND, int R, bool PROD>
+static void launch_bulk(const BlockArgs& BA, const MomArgs& M, dim3 grid, cudaStream_t st, BulkList L) {
+  // the list kernel also for one block of the K_h g product: its register allocation spills less
+  // there (stack 32 vs 72 B; C5 bulk 15.2 vs 15.7 ms), the stored kinds keep the one-block kernel
+  if (L.n > 1 || (KIND == STB_K && PROD)) launch_bulk_t<KIND, R, PROD, true>(BA, M, grid, st, L);
+  else launch_bulk_t<KIND, R, PROD, false>(BA, M, grid, st, L);
 }
 template <int KIND, bool PROD = false>
 static void launch_kind(int which, const BlockArgs& BA, const MomArgs& M, int ng, int nband_or_chunk,
@@ -332,6 +340,14 @@ __global__ void k_prod_reduce(const double* __restrict__ part, const int* __rest
     for (int q = 0; q < pslots; ++q) s += p[q];
   }
   y[r] = s;
+}
+// distributed records: staging chunk c = [nfc fields x cs pairs] -> field-major rec[f npairs + p]
+__global__ void k_rec_reorder(const double* __restrict__ stage, double* __restrict__ rec, int nfc, long long npairs,
+                              long long cs) {
+  const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= (long long)nfc * npairs) return;
+  const long long f = k / npairs, p = k - f * npairs, c = p / cs;
+  rec[k] = stage[c * nfc * cs + f * cs + (p - c * cs)];
 }
 template <int KIND>
 static void launch_records(const MomArgs& MB, const MomArgs& MN, const MomArgs* MS, int q_sing,
@@ -453,12 +469,23 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, const Qua
     cudaFreeAsync(d_poff, st);
     return cuda_fail(e, "assemble/list");
   }
-  // pair records in G = record_ranks chunks of cs pairs, chunk c = [bulk fields | near fields];
-  // rank r computes chunk r, an all-gather completes the others (one chunk without a communicator)
+  // pair records, field-major with stride npairs: [bulk fields | near fields | touching records].
+  // With G = record_ranks > 1 ranks, rank r computes the pairs of test segments [r rpc, (r+1) rpc)
+  // into chunk r of a staging buffer (chunk c = [bulk | near fields], stride cs = rpc N_Gamma), an
+  // in-place all-gather completes the other chunks and one kernel reorders them into the layout
+  // above (the bulk and near kernels address a record as rec + pair: a chunked address costs them
+  // registers)
   const int G = record_ranks(m);
-  const long long cs = G == 1 ? npairs : (npairs + G - 1) / G;
-  const long long rec_main = (long long)(nf + nfn) * cs * G;
+  const int rpc = (ng + G - 1) / G;                    // test segments per chunk
+  const long long cs = (long long)rpc * ng;
+  const long long rec_main = (long long)(nf + nfn) * npairs;
   const size_t rec_bytes = sizeof(double) * ((size_t)rec_main + (size_t)nf * nsrec);
+  const size_t stage_bytes = G > 1 ? sizeof(double) * (size_t)(nf + nfn) * cs * G : 0;
+  double* d_stage = nullptr;
+  if (G > 1 && (e = storage_acquire(m->device, stage_bytes, st, (void**)&d_stage)) != cudaSuccess) {
+    cudaFreeAsync(d_poff, st);
+    return cuda_fail(e, "assemble/record staging");
+  }
   if ((e = storage_acquire(m->device, rec_bytes, st, (void**)&d_rec)) != cudaSuccess ||
       (e = cudaMallocAsync((void**)&d_ctr, sizeof(unsigned long long) * 15, st)) != cudaSuccess ||
       (e = cudaMemsetAsync(d_ctr, 0, sizeof(unsigned long long) * 15, st)) != cudaSuccess) {
@@ -483,13 +510,14 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, const Qua
   const int qfar = qc.q_near;
   MomArgs MB{d_rec, npairs, m->d_seg, m->d_half, m->d_dual, m->alpha, ng, q_bulk, qfar, d_ctr};
   MB.near_gap = qc.near_gap;
-  MB.cs = cs;
+  MB.cs = npairs;
+  MB.rpc = ng;
   MB.nfc = nf + nfn;
-  MB.p_lo = G == 1 ? 0 : std::min(npairs, (long long)m->comm->rank * cs);
-  MB.p_hi = std::min(npairs, MB.p_lo + cs);
+  MB.p_lo = 0;
+  MB.p_hi = npairs;
   MB.ell = m->htmin > 0.0 ? std::sqrt(4.0 * m->htmin / m->alpha) : 0.0;
   MomArgs MN = MB;
-  MN.rec = d_rec + (long long)nf * cs;
+  MN.rec = d_rec + (long long)nf * npairs;
   MN.list = d_list;
   // the near cells' nodes: s = t_{a+1} - t_a and t_{a+1} - t_{a-1} (and t_a - t_{a-1})
   {
@@ -507,12 +535,28 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, const Qua
   MS.npairs = MS.cs = MS.p_hi = nsrec;
   MS.p_lo = 0;
   MS.counters = d_ctr + 10;
-  mark();
-  if (kind == STB_V) launch_records<STB_V>(MB, MN, fused_sing ? &MS : nullptr, q_sing, st);
-  else if (kind == STB_K) launch_records<STB_K>(MB, MN, fused_sing ? &MS : nullptr, q_sing, st);
-  else launch_records<STB_D>(MB, MN, fused_sing ? &MS : nullptr, q_sing, st);
+  // the records kernels' arguments: this rank's chunk of the staging buffer when distributed
+  MomArgs MBr = MB, MNr = MN;
   if (G > 1) {
-    bem_status gs = allgather_chunks(m, d_rec, (long long)(nf + nfn) * cs, st);
+    MBr.rec = d_stage;
+    MNr.rec = d_stage + (long long)nf * cs;
+    MBr.cs = MNr.cs = cs;
+    MBr.rpc = MNr.rpc = rpc;
+    MBr.p_lo = MNr.p_lo = std::min(npairs, (long long)m->comm->rank * cs);
+    MBr.p_hi = MNr.p_hi = std::min(npairs, MBr.p_lo + cs);
+  }
+  mark();
+  if (kind == STB_V) launch_records<STB_V>(MBr, MNr, fused_sing ? &MS : nullptr, q_sing, st);
+  else if (kind == STB_K) launch_records<STB_K>(MBr, MNr, fused_sing ? &MS : nullptr, q_sing, st);
+  else launch_records<STB_D>(MBr, MNr, fused_sing ? &MS : nullptr, q_sing, st);
+  if (G > 1) {
+    bem_status gs = allgather_chunks(m, d_stage, (long long)(nf + nfn) * cs, st);
+    if (gs == BEM_OK) {
+      const long long tot = (long long)(nf + nfn) * npairs;
+      k_rec_reorder<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(d_stage, d_rec, nf + nfn, npairs, cs);
+      count_launch();
+    }
+    storage_release(m->device, d_stage, stage_bytes, st);
     if (gs != BEM_OK) {
       storage_release(m->device, d_rec, rec_bytes, st);
       if (d_part) storage_release(m->device, d_part, part_bytes, st);
@@ -584,6 +628,11 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, const Qua
       BA.pslots = pslots;
       BA.ntile = ntile;
       BA.ell = MB.ell;
+      if (bl.size() == 1) {   // the single-block kernel takes the block from its parameters
+        BA.poff = bl[0].poff;
+        BA.a0 = bl[0].a0; BA.a1 = bl[0].a1; BA.b0 = bl[0].b0; BA.b1 = bl[0].b1;
+        BA.pbase = bl[0].pbase;
+      }
       const BulkList L{d_bl, (int)bl.size()};
       if (prod) launch_kind<STB_K, true>(0, BA, MB, ng, nzmax, nzmax, st, L, Rb);
       else if (kind == STB_V) launch_kind<STB_V>(0, BA, MB, ng, nzmax, nzmax, st, L, Rb);

@@ -92,15 +92,18 @@ struct MomArgs {
                           // cells of at most ell (no subdivision while kappa <= 1)
   double near_gap;        // near records: distance ratio below which the measured orders apply
   int* list;              // D_h near records: [0] count, [1..] the near_special pairs (k_records appends)
-  // record layout: the pairs in chunks of cs, chunk c holding nfc fields of stride cs (one chunk,
-  // cs = npairs, on one rank).  Distributed (G ranks): rank r computes the pairs [p_lo, p_hi) of
-  // chunk r and the chunks are all-gathered
+  // records kernels: the pairs (I, J) in chunks of rpc test segments I (cs = rpc N_Gamma pairs),
+  // chunk c holding nfc fields of stride cs; one chunk (rpc = N_Gamma, cs = npairs: the layout the
+  // bulk and near kernels read) on one rank.  Distributed (G ranks): rank r computes the pairs
+  // [p_lo, p_hi) of chunk r into a staging buffer
   long long cs = 0;
-  int nfc = 0;
+  int nfc = 0, rpc = 0;
   long long p_lo = 0, p_hi = 0;
 };
-__device__ __forceinline__ long long rec_base(const MomArgs& M, long long pair) {
-  return M.cs == M.npairs ? pair : (pair / M.cs) * M.nfc * M.cs + pair % M.cs;
+// offset of pair (I, J)'s record in the records kernels' layout (32-bit division)
+__device__ __forceinline__ long long rec_base(const MomArgs& M, int I, int J) {
+  const int c = I / M.rpc, r = I - c * M.rpc;
+  return (long long)c * M.nfc * M.cs + (long long)r * M.ng + J;
 }
 
 // composite subdivision of a sub-pair: cells per direction.  R24: pairs
@@ -295,7 +298,7 @@ __device__ __forceinline__ void rec_points(const MomArgs& M, int I, int J, int l
 template <int KIND, bool NEAR, bool WARP>
 __device__ __forceinline__ void records_body(const MomArgs& M, long long pair, int lane) {
   const int I = (int)(pair / M.ng), J = (int)(pair % M.ng);
-  double* rec = M.rec + rec_base(M, pair);
+  double* rec = M.rec + rec_base(M, I, J);
   const long long S = M.cs;
   const bool wr = !WARP || lane == 0;   // the lane that writes the record
   // one pass: c range, regime-A moments M_k = sum W c^k and the affine constants of both
@@ -987,7 +990,10 @@ __device__ __forceinline__ void cp_async16_bulk(void* smem, const void* gmem) {
 #ifndef STB_BULK_MINB_K
 #define STB_BULK_MINB_K 3   // CTAs per SM the K_h bulk kernels are register-budgeted for
 #endif
-template <int KIND, int R, bool PROD = false>
+// MULTI: the blocks of the list L (a rank's owned blocks); otherwise the one block of B (kernel
+// parameters: the loop and the list reads compile away -- the list form costs one GPU's single
+// block ~7% in spills, C5 V 9.7 vs 10.4 ms)
+template <int KIND, int R, bool PROD = false, bool MULTI = false>
 __global__ void __launch_bounds__(128, KIND == STB_D ? 2 : (KIND == STB_K ? STB_BULK_MINB_K : 3)) k_bulk_m(BlockArgs B, BulkList L, MomArgs M) {
   const int ng = B.ng;
   const int lane = threadIdx.x & 31;
@@ -1001,17 +1007,22 @@ __global__ void __launch_bounds__(128, KIND == STB_D ? 2 : (KIND == STB_K ? STB_
   const int ti = (blockIdx.y * 4) / SYM_TS, tj = blockIdx.x;
   if (B.sym && ti > tj) return;                   // CTA-uniform
   // does band z of any listed block have bulk cells?  (CTA-uniform)
+  const int nlist = MULTI ? L.n : 1;
+  auto block_k = [&](int k) -> BulkBlock {
+    return MULTI ? L.blk[k] : BulkBlock{B.poff, B.a0, B.a1, B.b0, B.b1, B.pbase};
+  };
   {
     bool any = false;
-    for (int k = 0; k < L.n && !any; ++k) {
-      const int rh = L.blk[k].a1 - R * band, rl = max(L.blk[k].a0, rh - R);
-      any = rh > rl && min(L.blk[k].b1 - 1, rh - 3) >= L.blk[k].b0;
+    for (int k = 0; k < nlist && !any; ++k) {
+      const BulkBlock Q = block_k(k);
+      const int rh = Q.a1 - R * band, rl = max(Q.a0, rh - R);
+      any = rh > rl && min(Q.b1 - 1, rh - 3) >= Q.b0;
     }
     if (!any) return;
   }
   const long long pair = (long long)I * ng + J;
-  const long long S = M.cs;
-  const double* recp = M.rec + rec_base(M, pair);   // the pair's record (field stride S)
+  const long long S = M.npairs;
+  const double* recp = M.rec + pair;               // the pair's record (field stride S)
   // row offsets of the band rows a = r_lo + r for this warp's row I (panel offset + I * ld, or
   // the tile's offset + (I mod 32) * 32), shared by the warp: a store is one LDS + one address add
   __shared__ long long s_row[4][R];
@@ -1050,14 +1061,14 @@ __global__ void __launch_bounds__(128, KIND == STB_D ? 2 : (KIND == STB_K ? STB_
   unsigned long long nA = 0, nB = 0, nZ = 0, nC = 0, nK = 0;
   // the listed blocks one after the other (a rank's owned blocks of the cyclic plan; one block on one
   // GPU): the per-pair setup above is paid once per CTA, not once per block
-  for (int kb_ = 0; kb_ < L.n; ++kb_) {
-  const BulkBlock Bk = L.blk[kb_];
+  for (int kb_ = 0; kb_ < nlist; ++kb_) {
+  const BulkBlock Bk = block_k(kb_);
   const int r_hi = Bk.a1 - R * band;
   const int r_lo = max(Bk.a0, r_hi - R);
   if (r_hi <= r_lo) continue;                     // CTA-uniform
   const int bmax = min(Bk.b1 - 1, r_hi - 1 - 2);
   if (bmax < Bk.b0) continue;                     // CTA-uniform
-  __syncthreads();                                // the previous block's lag chunks and row offsets are no longer read
+  if (MULTI) __syncthreads();                     // the previous block's lag chunks and row offsets are no longer read
   // lag chunk c: columns y = b0 + c LAG_CH + k, nodes x = min(r_lo + r, r_hi) (2 x 16 B per entry)
   const int ncols = bmax + 2 - Bk.b0;
   auto stage = [&](int c) {
@@ -1257,8 +1268,8 @@ __global__ void __launch_bounds__(128) k_near_m(BlockArgs B, MomArgs M, int chun
   const int a_end = min(B.a1, a_beg + chunk);
   if (B.sym && (int)(blockIdx.y * 4) / SYM_TS > (int)blockIdx.x) return;   // CTA-uniform (mirror tiles)
   const long long pair = (long long)I * ng + J;
-  const long long S = M.cs;
-  const double* rec = M.rec + rec_base(M, pair);
+  const long long S = M.npairs;
+  const double* rec = M.rec + pair;
   RegA<KIND> A;
   A.load(rec, S);
   RegBZ<KIND> Z;

@@ -56,6 +56,13 @@ def oracle_dense(name, kind):
 
 
 # ------------------------------------------------------------- special functions
+def test_diag_fp64_rate_is_a_plausible_dfma_rate():
+    """the live DFMA rate bench.py reports beside the assembly roofline: positive and below the
+    max-clock FP64 peak (148 SMs x 64 DFMA/clk x 2 flops x 1.965 GHz = 37.2 TFLOP/s, + 2%)"""
+    r = S.diag_fp64_rate(0.3)
+    assert 5.0 < r < 37.2 * 1.02, r
+
+
 @pytest.mark.parametrize("which", [0, 1, 2, 3])
 def test_special_functions_against_mpmath(which):
     xs = np.concatenate([np.logspace(-13, np.log10(3.999), 300), np.linspace(3.99, 4.01, 21),

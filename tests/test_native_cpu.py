@@ -108,3 +108,11 @@ def test_no_cpu_fallback_without_gpu():
     with pytest.raises(S.BemError) as e:
         S.Mesh(SQ, [2, 2, 2, 2], np.linspace(0, 1, 5), 1.0)
     assert e.value.status == S.BEM_E_CUDA
+
+
+def test_diag_fp64_rate_rejects_bad_arguments():
+    """bem_diag_fp64_rate validates before touching the device (0 < seconds <= 60)"""
+    for sec in (0.0, -1.0, 61.0):
+        with pytest.raises(S.BemError) as e:
+            S.diag_fp64_rate(sec)
+        assert e.value.status == S.BEM_E_INVALID

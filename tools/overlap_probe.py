@@ -16,13 +16,13 @@ def ev():
     return torch.cuda.Event(enable_timing=True)
 
 
-def main(name="C5", nprod=6):
+def main(name="C5", nprod=6, prio=0):
     w = W.get(name)
     m = S.Mesh.from_workload(w)
     V = m.assemble_V()
     x = torch.tensor(W.random_vector(w.n), dtype=torch.float64, device="cuda")
     y = torch.empty_like(x)
-    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream(priority=prio)   # prio -1: products first
     res = {}
     for rep in range(3):
         # products alone
@@ -55,10 +55,10 @@ def main(name="C5", nprod=6):
         torch.cuda.synchronize()
         t_asm_c, t_prod_c = a.elapsed_time(b1), a.elapsed_time(b2)
         D.close()
-        res = {"prod_alone_ms": t_prod, "asm_alone_ms": t_asm, "sum_ms": t_prod + t_asm,
+        res = {"prio": prio, "prod_alone_ms": t_prod, "asm_alone_ms": t_asm, "sum_ms": t_prod + t_asm,
                "together_ms": max(t_asm_c, t_prod_c), "asm_done_ms": t_asm_c, "prod_done_ms": t_prod_c}
         print(json.dumps({k: round(v, 2) for k, v in res.items()}), flush=True)
 
 
 if __name__ == "__main__":
-    main(*(sys.argv[1:2] or ["C5"]))
+    main(sys.argv[1] if len(sys.argv) > 1 else "C5", 6, int(sys.argv[2]) if len(sys.argv) > 2 else 0)
