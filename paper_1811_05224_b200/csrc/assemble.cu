@@ -466,6 +466,7 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, const Qua
   unsigned long long* d_ctr = nullptr;
   int* d_list = nullptr;   // D_h near records: the near_special pairs
   if (kind == STB_D && (e = cudaMallocAsync((void**)&d_list, sizeof(int) * (npairs + 1), st)) != cudaSuccess) {
+    if (d_part) storage_release(m->device, d_part, part_bytes, st);
     cudaFreeAsync(d_poff, st);
     return cuda_fail(e, "assemble/list");
   }
@@ -483,12 +484,18 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, const Qua
   const size_t stage_bytes = G > 1 ? sizeof(double) * (size_t)(nf + nfn) * cs * G : 0;
   double* d_stage = nullptr;
   if (G > 1 && (e = storage_acquire(m->device, stage_bytes, st, (void**)&d_stage)) != cudaSuccess) {
+    if (d_part) storage_release(m->device, d_part, part_bytes, st);
+    if (d_list) cudaFreeAsync(d_list, st);
     cudaFreeAsync(d_poff, st);
     return cuda_fail(e, "assemble/record staging");
   }
   if ((e = storage_acquire(m->device, rec_bytes, st, (void**)&d_rec)) != cudaSuccess ||
       (e = cudaMallocAsync((void**)&d_ctr, sizeof(unsigned long long) * 15, st)) != cudaSuccess ||
       (e = cudaMemsetAsync(d_ctr, 0, sizeof(unsigned long long) * 15, st)) != cudaSuccess) {
+    if (d_rec) storage_release(m->device, d_rec, rec_bytes, st);
+    if (d_stage) storage_release(m->device, d_stage, stage_bytes, st);
+    if (d_part) storage_release(m->device, d_part, part_bytes, st);
+    if (d_list) cudaFreeAsync(d_list, st);
     cudaFreeAsync(d_poff, st);
     return cuda_fail(e, "assemble/records");
   }
