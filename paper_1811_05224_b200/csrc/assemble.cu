@@ -753,11 +753,13 @@ bem_status finalize_assembly_stats(bem_matrix* A) {
   for (auto x : A->ev) cudaEventDestroy(x);
   A->ev.clear();
   // algorithmic FP64 flops of the bulk kernel, static counts of the shipped
-  // forms (DFMA = 2): regime A per node V 46, K 42, D 88 (20-step Horner per family + log terms);
-  // regime B per node 61 (E1 / GB3 and the closing terms, exp not counted) + per Taylor order
-  // one FMA per Horner chain: V (S1, S2), K (S1, S3) 4, D (S1, S2 of H, S1 of F) 6
+  // forms (DFMA = 2): regime A per node = the Horner chain in u plus the closing s / ln s terms
+  // (RegA::chain + RegA::finish): V 19 + 3, K 20 + 1, D 20 + 3 FMAs (D's two families are one
+  // merged chain) = 44 / 42 / 46 flops; regime B per node 61 (E1 / GB3 and the closing terms, exp
+  // not counted) + per Taylor order one FMA per Horner chain: V (S1, S2), K (S1, S3) 4,
+  // D (S1, S2 of H, S1 of F) 6
   const int kind = A->kind;
-  const double fA = kind == STB_V ? 46.0 : (kind == STB_K ? 42.0 : 88.0);
+  const double fA = kind == STB_V ? 44.0 : (kind == STB_K ? 42.0 : 46.0);
   const double fK = kind == STB_D ? 6.0 : 4.0;
   A->flops_bulk = fA * (double)A->nodes_bulk[0] + 61.0 * (double)A->nodes_bulk[1] + fK * (double)ctr[4];
   A->ev_bulk = A->nodes_bulk[0] + A->nodes_bulk[1] + A->nodes_bulk[2] + A->nodes_bulk[3];

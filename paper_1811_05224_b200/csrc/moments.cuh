@@ -974,8 +974,14 @@ struct BulkList {
 };
 // test steps per band: 7 for V_h and K_h g (their 3-CTA register budget: 8 spilled in the B path,
 // C5 V 10.1 -> 9.7 ms, K g 16.5 -> 16.0 ms at 7), 8 for D_h (2 CTAs, 11.6 vs 12.1 ms at 7)
+#ifndef STB_BULK_R_D
+#define STB_BULK_R_D 8      // band height of the D_h bulk kernel
+#endif
+#ifndef STB_BULK_MINB_D
+#define STB_BULK_MINB_D 2   // CTAs per SM the D_h bulk kernel is register-budgeted for
+#endif
 template <int KIND>
-__host__ __device__ constexpr int bulk_r() { return KIND == STB_D ? 8 : 7; }
+__host__ __device__ constexpr int bulk_r() { return KIND == STB_D ? STB_BULK_R_D : 7; }
 template <int KIND>
 __host__ __device__ constexpr int bulk_nch() { return Fams<KIND>::n == 2 ? 3 : 2; }
 // dynamic shared memory of k_bulk_m: staged regime-B coefficients + two lag chunks
@@ -994,7 +1000,7 @@ __device__ __forceinline__ void cp_async16_bulk(void* smem, const void* gmem) {
 // parameters: the loop and the list reads compile away -- the list form costs one GPU's single
 // block ~7% in spills, C5 V 9.7 vs 10.4 ms)
 template <int KIND, int R, bool PROD = false, bool MULTI = false>
-__global__ void __launch_bounds__(128, KIND == STB_D ? 2 : (KIND == STB_K ? STB_BULK_MINB_K : 3)) k_bulk_m(BlockArgs B, BulkList L, MomArgs M) {
+__global__ void __launch_bounds__(128, KIND == STB_D ? STB_BULK_MINB_D : (KIND == STB_K ? STB_BULK_MINB_K : 3)) k_bulk_m(BlockArgs B, BulkList L, MomArgs M) {
   const int ng = B.ng;
   const int lane = threadIdx.x & 31;
   const int J0 = blockIdx.x * 32 + lane;
