@@ -582,6 +582,15 @@ struct RegA {
   }
   __device__ __forceinline__ double eval(double s, double lns, double u) const { return finish(chain(u), s, lns); }
 };
+// RegA::chain with the coefficients in shared memory (this thread's column, entry k at sp[k * 128])
+template <int KIND>
+__device__ __forceinline__ double chain_s(const double* sp, double u) {
+  constexpr int NC = RegA<KIND>::NC;
+  double acc = sp[(NC - 1) * 128];
+#pragma unroll
+  for (int k = NC - 2; k >= 0; --k) acc = fma(acc, u, sp[k * 128]);
+  return acc;
+}
 
 // point-by-point regularised contributions (regime C), same function as regimes A / B / Z
 __device__ __forceinline__ double pt_h(double c, double s, double lns, double u) {
@@ -669,7 +678,10 @@ __device__ __forceinline__ double gb3_cb(double t) { return horner<STB_GB3_DEG>(
 // pair in shared memory once per thread (sm: [chain][i] with stride BZS_STRIDE between entries), so
 // that a node's chains read L2 only for orders >= ns: a chain walked through L2 costs one L2 round
 // trip per unrolled step, which made a regime-B node ~25x the cost of a regime-A node.
-constexpr int BZ_KBS = 12;          // staged orders per chain (kb <= 11 for ~90% of the C3 / C5 nodes)
+#ifndef STB_BZ_KBS
+#define STB_BZ_KBS 12
+#endif
+constexpr int BZ_KBS = STB_BZ_KBS;  // staged orders per chain (kb <= 11 for ~90% of the C3 / C5 nodes)
 constexpr int BZS_STRIDE = 128;     // threads per bulk CTA: entry i of chain f at sm[(f KBS + i) 128]
 struct BzSrc {
   const double* p1;
@@ -984,10 +996,20 @@ template <int KIND>
 __host__ __device__ constexpr int bulk_r() { return KIND == STB_D ? STB_BULK_R_D : 7; }
 template <int KIND>
 __host__ __device__ constexpr int bulk_nch() { return Fams<KIND>::n == 2 ? 3 : 2; }
-// dynamic shared memory of k_bulk_m: staged regime-B coefficients + two lag chunks
+#ifndef STB_BULK_SMP
+#define STB_BULK_SMP 1
+#endif
+// regime-A chain coefficients of the V_h bulk kernel in shared memory (one column per thread, read
+// once per Horner step for all R + 1 chains) instead of registers: no spills at 152 registers, C5
+// 9.53 -> 9.25 ms; K_h g measured the same (15.19 / 15.24 ms), and at four CTAs per SM (128
+// registers, 8 staged regime-B orders) both were slower (V 9.41, K g 16.06 ms)
+template <int KIND>
+__host__ __device__ constexpr bool bulk_smp() { return STB_BULK_SMP && KIND == STB_V; }
+// dynamic shared memory of k_bulk_m: staged regime-B coefficients + two lag chunks (+ SMP chains)
 template <int KIND, int R>
 __host__ __device__ constexpr size_t bulk_smem_bytes() {
-  return sizeof(double) * bulk_nch<KIND>() * BZ_KBS * BZS_STRIDE + sizeof(double4) * 2 * LAG_CH * (R + 1);
+  return sizeof(double) * bulk_nch<KIND>() * BZ_KBS * BZS_STRIDE + sizeof(double4) * 2 * LAG_CH * (R + 1) +
+         (bulk_smp<KIND>() ? sizeof(double) * RegA<KIND>::NC * 128 : 0);
 }
 __device__ __forceinline__ void cp_async16_bulk(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
@@ -999,8 +1021,11 @@ __device__ __forceinline__ void cp_async16_bulk(void* smem, const void* gmem) {
 // MULTI: the blocks of the list L (a rank's owned blocks); otherwise the one block of B (kernel
 // parameters: the loop and the list reads compile away -- the list form costs one GPU's single
 // block ~7% in spills, C5 V 9.7 vs 10.4 ms)
+#ifndef STB_BULK_MINB_V
+#define STB_BULK_MINB_V 3   // CTAs per SM the V_h bulk kernel is register-budgeted for
+#endif
 template <int KIND, int R, bool PROD = false, bool MULTI = false>
-__global__ void __launch_bounds__(128, KIND == STB_D ? STB_BULK_MINB_D : (KIND == STB_K ? STB_BULK_MINB_K : 3)) k_bulk_m(BlockArgs B, BulkList L, MomArgs M) {
+__global__ void __launch_bounds__(128, KIND == STB_D ? STB_BULK_MINB_D : (KIND == STB_K ? STB_BULK_MINB_K : STB_BULK_MINB_V)) k_bulk_m(BlockArgs B, BulkList L, MomArgs M) {
   const int ng = B.ng;
   const int lane = threadIdx.x & 31;
   const int J0 = blockIdx.x * 32 + lane;
@@ -1037,6 +1062,9 @@ __global__ void __launch_bounds__(128, KIND == STB_D ? STB_BULK_MINB_D : (KIND =
   constexpr int NCH = bulk_nch<KIND>();
   double* s_bz = bulk_dyn;                                                  // [NCH][KBS][128]
   double4* s_lag = reinterpret_cast<double4*>(bulk_dyn + NCH * BZ_KBS * BZS_STRIDE);   // [2][LAG_CH][R+1]
+  constexpr bool SMP = bulk_smp<KIND>();
+  // SMP: this thread's chain coefficients, entry k at sPt[k * 128]
+  double* sPt = reinterpret_cast<double*>(s_lag + 2 * LAG_CH * (R + 1)) + threadIdx.x;
   long long* srow = s_row[threadIdx.x >> 5];
   const long long cstride = B.sym ? B.blk : (long long)ng;   // per trial step b
   const int jcol = B.sym ? J % SYM_TS : J;
@@ -1044,6 +1072,10 @@ __global__ void __launch_bounds__(128, KIND == STB_D ? STB_BULK_MINB_D : (KIND =
   const bool vst = valid && (!B.sym || ti != tj || jcol >= I % SYM_TS);
   RegA<KIND> A;
   A.load(recp, S);
+  if (SMP) {
+#pragma unroll
+    for (int k = 0; k < RegA<KIND>::NC; ++k) sPt[k * 128] = A.P[k];   // read back by this thread only
+  }
   // pairs without quadrature points (K_h on collinear elements: the kernel vanishes) hold
   // only zero entries: a warp of them writes zeros (or, in product mode, nothing) and skips the
   // node evaluations, counted as regime A (warp-uniform; the warp still joins the lag staging)
@@ -1130,13 +1162,13 @@ __global__ void __launch_bounds__(128, KIND == STB_D ? STB_BULK_MINB_D : (KIND =
       }
     } else if (full && __all_sync(0xffffffffu, A.cmax * ndd[2] < STB_MXB)) {
 #pragma unroll
-      for (int r = 0; r <= R; ++r) phi[r] = A.chain(ndd[4 * r + 2]);
+      for (int r = 0; r <= R; ++r) phi[r] = SMP ? chain_s<KIND>(sPt, ndd[4 * r + 2]) : A.chain(ndd[4 * r + 2]);
 #pragma unroll
       for (int r = 0; r <= R; ++r) phi[r] = A.finish(phi[r], ndd[4 * r], ndd[4 * r + 1]);
       nA += R + 1;
     } else {
 #pragma unroll
-      for (int r = 0; r <= R; ++r) phi[r] = A.chain(ndd[4 * r + 2]);
+      for (int r = 0; r <= R; ++r) phi[r] = SMP ? chain_s<KIND>(sPt, ndd[4 * r + 2]) : A.chain(ndd[4 * r + 2]);
 #pragma unroll
       for (int r = 0; r <= R; ++r) {
         const int x = r_lo + r;
