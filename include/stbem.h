@@ -93,6 +93,10 @@ typedef struct {
  * and triangular diagonal tiles, about half the bytes and half the assembly work, DESIGN.md section
  * 4.1); this flag stores them full */
 #define BEM_QUAD_FULL_STORAGE 2
+/* bem_rhs_fused: evaluate every regime-A node of K_h pair by pair instead of summing the regime-A
+ * fields of the trial pairs first (trial-moment table; same quadrature and
+ * regime forms, re-associated over the trial index) -- the reference path for tests */
+#define BEM_QUAD_KG_ENTRYWISE 4
 
 typedef enum {
   BEM_MASS_PRIMAL = 0,      /* M_h of eq. (4): <phi^10_(a,n), phi^0_(a,i)> */
@@ -136,6 +140,8 @@ typedef struct {
   long long nodes_bulk[4];   /* bulk node evaluations per regime A, B, Z, C */
   long long nodes_near[4];   /* near-cell node evaluations per regime */
   int fused_sing;            /* 1: touching pairs through moment records, 0: per-lag k_sing */
+  long long nodes_bulk_tab;  /* bem_rhs_fused: bulk regime-A nodes summed over the trial index by the
+                                trial-moment table (included in nodes_bulk[0]; 0 otherwise) */
 } bem_assembly_stats;
 
 /* ---------------------------------------------------------------- general */

@@ -683,6 +683,7 @@ bem_status bem_matrix_stats(const bem_matrix* A, bem_assembly_stats* o) {
   o->flops_bulk = A->flops_bulk;
   o->ms_records = A->ms_records;
   o->fused_sing = A->fused_sing;
+  o->nodes_bulk_tab = A->nodes_tab;
   for (int k = 0; k < 4; ++k) {
     o->nodes_bulk[k] = A->nodes_bulk[k];
     o->nodes_near[k] = A->nodes_near[k];

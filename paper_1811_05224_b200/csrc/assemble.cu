@@ -62,8 +62,9 @@ struct BlockArgs {
   const double* g;
   double* part;           // partials of this block: [(a - a0) * ng + i] * pslots + slot
   long long pbase;
-  int pslots;             // 2 * ntile + 5: bulk trial tiles, near trial tiles, touching records
+  int pslots;             // 2 * ntile + 6: bulk trial tiles, near trial tiles, touching records, k_kg_tab
   int ntile;              // ceil(ng / 32)
+  int kgtab = 0;          // product mode: regime-A nodes with y <= x - 3 summed by k_kg_tab
   double ell;             // sqrt(4 min h_t / alpha): composite singular rules when h > ell
 };
 
@@ -294,6 +295,15 @@ __global__ void __launch_bounds__(128) k_sing(BlockArgs B, const Seg* __restrict
 }
 
 // ================================================================= launch
+static int max_smem_optin() {
+  static int v = 0;
+  if (!v) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess || v <= 0) v = 48 * 1024;
+  }
+  return v;
+}
 // which: 0 bulk cells (k_bulk_m), 1 near cells (k_near_m)
 template <int KIND, int R, bool PROD, bool MULTI>
 static void launch_bulk_t(const BlockArgs& BA, const MomArgs& M, dim3 grid, cudaStream_t st, BulkList L) {
@@ -414,7 +424,7 @@ bem_status resolve_quad(int kind, const bem_mesh* m, const bem_quad_opts* o, con
   if (q.q_far < 3 || q.q_far > 8 || q.q_far == 7) { set_error(std::string(where) + ": q_far must be one of 3,4,5,6,8"); return BEM_E_INVALID; }
   if (q.q_near < 3 || q.q_near > QMAX) { set_error(std::string(where) + ": q_near must be in [3,16]"); return BEM_E_INVALID; }
   if (q.q_sing < 4 || q.q_sing > QSING_MAX) { set_error(std::string(where) + ": q_sing must be in [4,16]"); return BEM_E_INVALID; }
-  if (q.flags & ~(BEM_QUAD_LEGACY_SING | BEM_QUAD_FULL_STORAGE)) { set_error(std::string(where) + ": unknown flags"); return BEM_E_INVALID; }
+  if (q.flags & ~(BEM_QUAD_LEGACY_SING | BEM_QUAD_FULL_STORAGE | BEM_QUAD_KG_ENTRYWISE)) { set_error(std::string(where) + ": unknown flags"); return BEM_E_INVALID; }
   *out = q;
   return BEM_OK;
 }
@@ -445,7 +455,7 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, const Qua
   A->fused_sing = fused_sing ? 1 : 0;
   if (prod && !fused_sing) { set_error("assemble: product mode needs the touching-pair records"); return BEM_E_STATE; }
   // product mode: partial sums per block, row (a, i) and slot (bulk / near trial tiles, records)
-  const int ntile = (ng + 31) / 32, pslots = 2 * ntile + 5;
+  const int ntile = (ng + 31) / 32, pslots = 2 * ntile + 6;
   double* d_part = nullptr;
   size_t part_bytes = 0;
   std::vector<long long> pbase(blocks_of(A).size(), 0);
@@ -490,8 +500,8 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, const Qua
     return cuda_fail(e, "assemble/record staging");
   }
   if ((e = storage_acquire(m->device, rec_bytes, st, (void**)&d_rec)) != cudaSuccess ||
-      (e = cudaMallocAsync((void**)&d_ctr, sizeof(unsigned long long) * 15, st)) != cudaSuccess ||
-      (e = cudaMemsetAsync(d_ctr, 0, sizeof(unsigned long long) * 15, st)) != cudaSuccess) {
+      (e = cudaMallocAsync((void**)&d_ctr, sizeof(unsigned long long) * CTR_N, st)) != cudaSuccess ||
+      (e = cudaMemsetAsync(d_ctr, 0, sizeof(unsigned long long) * CTR_N, st)) != cudaSuccess) {
     if (d_rec) storage_release(m->device, d_rec, rec_bytes, st);
     if (d_stage) storage_release(m->device, d_stage, stage_bytes, st);
     if (d_part) storage_release(m->device, d_part, part_bytes, st);
@@ -635,14 +645,45 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, const Qua
       BA.pslots = pslots;
       BA.ntile = ntile;
       BA.ell = MB.ell;
+      // K_h g: the regime-A nodes of the interior columns as trial-moment sums (k_kg_tab) when its
+      // shared-memory tables fit (N_Gamma up to ~590) and not disabled by BEM_QUAD_KG_ENTRYWISE
+      int nxmax = 0;
+      for (const BulkBlock& q : bl) nxmax = std::max(nxmax, q.a1 - q.a0 + 1);
+      const size_t tab_smem = kg_tab_smem(ng, nxmax);
+      BA.kgtab = prod && !(flags & BEM_QUAD_KG_ENTRYWISE) && tab_smem + 2048 <= (size_t)max_smem_optin() &&
+                 nxmax <= KGT_XPT * KGT_THREADS && (ng + KGT_CH - 1) / KGT_CH <= 40 ? 1 : 0;
+      A->kg_tab = BA.kgtab;
       if (bl.size() == 1) {   // the single-block kernel takes the block from its parameters
         BA.poff = bl[0].poff;
         BA.a0 = bl[0].a0; BA.a1 = bl[0].a1; BA.b0 = bl[0].b0; BA.b1 = bl[0].b1;
         BA.pbase = bl[0].pbase;
       }
       const BulkList L{d_bl, (int)bl.size()};
-      if (prod) launch_kind<STB_K, true>(0, BA, MB, ng, nzmax, nzmax, st, L, Rb);
-      else if (kind == STB_V) launch_kind<STB_V>(0, BA, MB, ng, nzmax, nzmax, st, L, Rb);
+      if (prod) {
+        launch_kind<STB_K, true>(0, BA, MB, ng, nzmax, nzmax, st, L, Rb);
+        if (BA.kgtab) {
+          static bool attr = false;
+          if (!attr) {
+            cudaFuncSetAttribute(k_kg_tab<24>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem_optin() - 2048);
+            cudaFuncSetAttribute(k_kg_tab<40>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem_optin() - 2048);
+            attr = true;
+          }
+          const dim3 tg((unsigned)ng, (unsigned)bl.size());
+          if (kg_chm(ng) == 24) k_kg_tab<24><<<tg, KGT_THREADS, tab_smem, st>>>(BA, L, MB, nxmax);
+          else k_kg_tab<40><<<tg, KGT_THREADS, tab_smem, st>>>(BA, L, MB, nxmax);
+          count_launch();
+          A->launches++;
+          // algorithmic flops of the table: per (i, trial step y) the 22 prefix scans (one FMA per pair
+          // and field), per covered node (x, y, i) the 21-term chain and the ln s term
+          for (const BulkBlock& q : bl) {
+            const int ymax = std::min(q.b1, q.a1 - 3);
+            for (int y = q.b0; y <= ymax; ++y) {
+              const int nxn = q.a1 - std::max(q.a0, y + 3) + 1;
+              A->flops_tab += (double)ng * (2.0 * KGT_NF * ng + 44.0 * std::max(0, nxn));
+            }
+          }
+        }
+      } else if (kind == STB_V) launch_kind<STB_V>(0, BA, MB, ng, nzmax, nzmax, st, L, Rb);
       else if (kind == STB_K) launch_kind<STB_K>(0, BA, MB, ng, nzmax, nzmax, st, L, Rb);
       else launch_kind<STB_D>(0, BA, MB, ng, nzmax, nzmax, st, L, Rb);
       mark();
@@ -736,7 +777,7 @@ bem_status finalize_assembly_stats(bem_matrix* A) {
   if (A->stats_ready) return BEM_OK;
   A->stats_ready = true;
   if (!A->ev.empty()) cudaEventSynchronize(A->ev.back());
-  unsigned long long ctr[15] = {0};
+  unsigned long long ctr[CTR_N] = {0};
   cudaError_t e = cudaMemcpy(ctr, A->d_ctr, sizeof(ctr), cudaMemcpyDeviceToHost);
   if (e != cudaSuccess) return cuda_fail(e, "assembly stats");
   for (int k = 0; k < 4; ++k) {
@@ -761,7 +802,11 @@ bem_status finalize_assembly_stats(bem_matrix* A) {
   const int kind = A->kind;
   const double fA = kind == STB_V ? 44.0 : (kind == STB_K ? 42.0 : 46.0);
   const double fK = kind == STB_D ? 6.0 : 4.0;
-  A->flops_bulk = fA * (double)A->nodes_bulk[0] + 61.0 * (double)A->nodes_bulk[1] + fK * (double)ctr[4];
+  // K_h g with the trial-moment table: its nodes are not evaluated pair by pair (ctr[CTR_TAB]); the
+  // table kernel's own flops (prefix scans, one chain per covered node and test segment) instead
+  A->nodes_tab = (long long)ctr[CTR_TAB];
+  A->flops_bulk = fA * (double)(A->nodes_bulk[0] - A->nodes_tab) + 61.0 * (double)A->nodes_bulk[1] +
+                  fK * (double)ctr[4] + A->flops_tab;
   A->ev_bulk = A->nodes_bulk[0] + A->nodes_bulk[1] + A->nodes_bulk[2] + A->nodes_bulk[3];
   A->ev_near = A->nodes_near[0] + A->nodes_near[1] + A->nodes_near[2] + A->nodes_near[3];
   // self-checks of the kernels' coverage

@@ -189,6 +189,9 @@ struct bem_matrix_s {
   long long ev_bulk = 0, ev_near = 0, nodes_expected = 0;
   long long nodes_bulk[4] = {0, 0, 0, 0}, nodes_near[4] = {0, 0, 0, 0};  // regimes A, B, Z, C
   double flops_bulk = 0;
+  long long nodes_tab = 0;   // K_h g: bulk regime-A nodes summed by the trial-moment table
+  double flops_tab = 0;      // its algorithmic flops (host count at launch)
+  int kg_tab = 0;
   int q_bulk = 0, q_sing = 0, launches = 0, fused_sing = 0;
 };
 

@@ -937,6 +937,9 @@ __device__ __forceinline__ double affine_part(const double* __restrict__ rec, lo
   return out;
 }
 
+// counter slots (assemble.cu): bulk [0..4], near [5..9], touching records [10..14], and the bulk
+// regime-A nodes summed by the K_h g trial-moment table (k_kg_tab; also counted in slot 0)
+constexpr int CTR_TAB = 15, CTR_N = 16;
 // warp-aggregated regime counters: [A, B, Z, C, sum of the regime-B Taylor orders]
 __device__ __forceinline__ void count_regimes(unsigned long long* ctr, unsigned long long nA,
                                               unsigned long long nB, unsigned long long nZ,
@@ -1096,7 +1099,7 @@ __global__ void __launch_bounds__(128, KIND == STB_D ? STB_BULK_MINB_D : (KIND =
       if (NCH == 3) sbz[(2 * BZ_KBS + i) * BZS_STRIDE] = R1[(FB1 + i) * S];
     }
   }
-  unsigned long long nA = 0, nB = 0, nZ = 0, nC = 0, nK = 0;
+  unsigned long long nA = 0, nB = 0, nZ = 0, nC = 0, nK = 0, nT = 0;
   // the listed blocks one after the other (a rank's owned blocks of the cyclic plan; one block on one
   // GPU): the per-pair setup above is paid once per CTA, not once per block
   for (int kb_ = 0; kb_ < nlist; ++kb_) {
@@ -1154,7 +1157,21 @@ __global__ void __launch_bounds__(128, KIND == STB_D ? STB_BULK_MINB_D : (KIND =
     // full columns (every band node above the trial node) whose smallest-lag node is in regime A
     // for every lane: all nodes are (s grows with x), no masks or regime tests per node
     const bool full = r_lo > y && r_hi - r_lo == R;       // CTA-uniform
-    if (zero_warp) {
+    // K_h g with the trial-moment sums (k_kg_tab): the regime-A nodes (x, y) with y <= x - 3 are
+    // summed over the trial index there; a column whose nodes all satisfy y <= x - 3 leaves only
+    // this lane's nodes outside regime A (B / Z / C) to evaluate here -- no Horner chains
+    const bool tabcol = PROD && B.kgtab && y <= r_lo - 3;  // CTA-uniform
+    if (tabcol) {
+#pragma unroll
+      for (int r = 0; r <= R; ++r) {
+        const bool ok = r_lo + r <= r_hi;
+        const bool inA = A.cmax * ndd[4 * r + 2] < STB_MXB;
+        phi[r] = 0.0;
+        nA += ok && inA;
+        nT += ok && inA;
+        if (ok && !inA && !zero_warp) bmask |= 1u << r;
+      }
+    } else if (zero_warp) {
 #pragma unroll
       for (int r = 0; r <= R; ++r) {
         phi[r] = 0.0;
@@ -1166,6 +1183,14 @@ __global__ void __launch_bounds__(128, KIND == STB_D ? STB_BULK_MINB_D : (KIND =
 #pragma unroll
       for (int r = 0; r <= R; ++r) phi[r] = A.finish(phi[r], ndd[4 * r], ndd[4 * r + 1]);
       nA += R + 1;
+      if (PROD && B.kgtab) {   // nodes y <= x - 3 are the table's (regime A here)
+#pragma unroll
+        for (int r = 0; r <= R; ++r)
+          if (y <= r_lo + r - 3) {
+            phi[r] = 0.0;
+            ++nT;
+          }
+      }
     } else {
 #pragma unroll
       for (int r = 0; r <= R; ++r) phi[r] = SMP ? chain_s<KIND>(sPt, ndd[4 * r + 2]) : A.chain(ndd[4 * r + 2]);
@@ -1175,8 +1200,10 @@ __global__ void __launch_bounds__(128, KIND == STB_D ? STB_BULK_MINB_D : (KIND =
         const double v = A.finish(phi[r], ndd[4 * r], ndd[4 * r + 1]);
         const bool ok = x <= r_hi && x > y;
         const bool inA = A.cmax * ndd[4 * r + 2] < STB_MXB;
-        phi[r] = ok ? v : 0.0;
+        const bool tab = PROD && B.kgtab && inA && y <= x - 3;   // the table's node
+        phi[r] = ok && !tab ? v : 0.0;
         nA += ok && inA;
+        nT += ok && tab;
         if (ok && !inA) bmask |= 1u << r;
       }
     }
@@ -1285,8 +1312,170 @@ __global__ void __launch_bounds__(128, KIND == STB_D ? STB_BULK_MINB_D : (KIND =
     }
   }
   }   // listed blocks
-  if (!valid) nA = nB = nZ = nC = nK = 0;
+  if (!valid) nA = nB = nZ = nC = nK = nT = 0;
   count_regimes(M.counters, nA, nB, nZ, nC, nK);
+  if (PROD && M.counters) {   // regime-A nodes left to the trial-moment table (counted in A above)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nT += __shfl_xor_sync(0xffffffffu, nT, o);
+    if (lane == 0 && nT) atomicAdd(M.counters + CTR_TAB, nT);
+  }
+}
+
+// ------------------------------------------------------------- K_h g: regime-A trial-moment sums
+// In the regime-A form a node value of pair (i, n) is linear in the pair's fields,
+//   Phi~_n(x, y) = sum_k P_k(i, n) u^k - ln s P_21(i, n)     (RegA<K>: P_k = poly_k M_k, P_21 = M_0),
+// so over the pairs n of test segment i that are in regime A at the node (c_max(i, n) u < 8: a
+// prefix of the pairs sorted by c_max) the trial sum is one Horner chain on prefix sums:
+//   sum_{n in A} Phi~_n(x, y) dg_y(n) = sum_k u^k T_k[m] - ln s T_21[m],
+//   T_f[m] = sum_{m' < m} P_f(i, ord[m']) dg_y(ord[m']),   m = #{n : c_max(i, n) u < 8}.
+// The same quadrature and regime forms as pair by pair, re-associated over n.
+// Covered: the nodes (x, y) with y <= x - 3, b0 <= y <= b1, a0 <= x <= a1 of a listed block, whose
+// weight in every row that uses them is dg_y = g~_y - g~_{y-1} (g~ = g on the block's trial steps);
+// the per-pair kernel (kgtab) skips exactly these (same predicate on the same lag-table u).  Row a
+// receives S(a+1) - S(a), S(x) = sum_y of the node sums, in its own partial slot (2 ntile + 5).
+// CTA = (test segment i, listed block), thread = (field f, chunk c of the sorted pairs) for the
+// scans, with the chunk's 22 x CHM fields in registers: per trial step y one chunk-local scan in
+// registers, the chunk offsets through shared memory, the prefix table written once; then thread t
+// takes the test nodes x = a0 + t (+ KGT_THREADS): its node sums S(x) and its cutoff m stay in
+// registers (m only falls as y grows at fixed x: a walk down the sorted c_max instead of a search).
+constexpr int KGT_NF = MKA + 2;
+constexpr int KGT_CH = 16;
+constexpr int KGT_THREADS = KGT_NF * KGT_CH;   // 352
+constexpr int KGT_XPT = 2;                     // test nodes per thread: N_I + 1 <= 704
+// odd row stride of the [field][m] prefix table: the 22 lanes of a chunk write 22 different banks
+__host__ __device__ inline int kg_ld_t(int ng) { return (ng + 1) | 1; }
+__host__ __device__ inline size_t kg_tab_smem(int ng, int nxmax) {
+  return sizeof(double) * ((size_t)KGT_NF * kg_ld_t(ng) + 3 * (size_t)ng + nxmax + 2 * KGT_NF * KGT_CH) +
+         sizeof(int) * (size_t)ng;
+}
+// pairs per chunk the register arrays hold (template instances 24: N_Gamma <= 384, 40: <= 640)
+__host__ __device__ inline int kg_chm(int ng) { return (ng + KGT_CH - 1) / KGT_CH <= 24 ? 24 : 40; }
+#ifndef STB_KGT_MINB
+#define STB_KGT_MINB 1   // CTAs per SM of k_kg_tab<24> (2: 80 registers with spills, C5 3.2 vs 2.4 ms)
+#endif
+template <int CHM>
+__global__ void __launch_bounds__(KGT_THREADS, CHM <= 24 ? STB_KGT_MINB : 1) k_kg_tab(BlockArgs B, BulkList L, MomArgs M, int nxmax) {
+  extern __shared__ __align__(16) double kgt[];
+  const int ng = B.ng, i = blockIdx.x, t = threadIdx.x;
+  const BulkBlock Bk = L.blk[blockIdx.y];
+  const int ymax = min(Bk.b1, Bk.a1 - 3);
+  if (ymax < Bk.b0) return;                                   // CTA-uniform: no covered node
+  const long long S = M.npairs;
+  const int ldt = kg_ld_t(ng);
+  double* T = kgt;                                            // [KGT_NF][ldt] prefix sums (m = 0..ng)
+  double* cmx = T + (size_t)KGT_NF * ldt;                     // [ng] sorted c_max
+  double* w = cmx + ng;                                       // [2][ng] dg_y in sorted order
+  double* Sx = w + 2 * ng;                                    // [nx] node sums S(x) (end)
+  double* tot = Sx + nxmax;                                   // [2][KGT_CH][KGT_NF] chunk totals
+  int* ord = reinterpret_cast<int*>(tot + 2 * KGT_NF * KGT_CH);   // [ng]
+  const double* rec = M.rec + (long long)i * ng;
+  // sort the row's pairs by c_max (rank = #smaller, ties by index): the scratch is T's space
+  for (int n = t; n < ng; n += KGT_THREADS) T[n] = rec[RF_CMAX * S + n];
+  __syncthreads();
+  for (int n = t; n < ng; n += KGT_THREADS) {
+    const double c = T[n];
+    int rk = 0;
+    for (int n2 = 0; n2 < ng; ++n2) {
+      const double c2 = T[n2];
+      rk += c2 < c || (c2 == c && n2 < n);
+    }
+    ord[rk] = n;
+    cmx[rk] = c;
+  }
+  __syncthreads();
+  // this thread's fields in sorted order (registers)
+  const int ch = (ng + KGT_CH - 1) / KGT_CH;
+  const int f = t % KGT_NF, c = t / KGT_NF;
+  const int m0 = min(ng, c * ch), nm = min(ng, m0 + ch) - m0;
+  const double* Rf = rec + (long long)(RF_COMMON + (f < MKA + 1 ? FA + f : FM0)) * S;
+  double cs[CHM];
+#pragma unroll
+  for (int j = 0; j < CHM; ++j) cs[j] = j < nm ? Rf[ord[m0 + j]] : 0.0;
+  double* Tf = T + (size_t)f * ldt;
+  if (c == 0) Tf[0] = 0.0;
+  auto gt = [&](int yy, int n) -> double {   // g~ on the block's trial steps
+    return (yy >= Bk.b0 && yy < Bk.b1) ? B.g[(long long)yy * ng + n] : 0.0;
+  };
+  // the test nodes of this thread, their sums and cutoffs
+  double sx[KGT_XPT];
+  int mx[KGT_XPT];
+#pragma unroll
+  for (int k = 0; k < KGT_XPT; ++k) {
+    sx[k] = 0.0;
+    mx[k] = ng;
+  }
+  // software pipeline over the trial steps y: the weights dg_(y+1) (double-buffered w) and the
+  // chunk totals (double-buffered tot) of the next step, so that two barriers per step suffice:
+  //   [scan 1: tot(y) from w(y); loads of g(y+1), lag(x, y)] B1 [scan 2: T(y); w(y+1) stored] B2 [nodes(y)]
+  // (T(y) is rewritten only after B1 of y+1, which every thread reaches after its nodes of y)
+  constexpr int GPT = 2;   // pairs per thread of the w loads: N_Gamma <= 704
+  for (int m = t; m < ng; m += KGT_THREADS) w[m] = gt(Bk.b0, ord[m]) - gt(Bk.b0 - 1, ord[m]);
+  __syncthreads();
+  for (int y = Bk.b0; y <= ymax; ++y) {
+    const double* wy = w + (size_t)((y - Bk.b0) & 1) * ng;
+    double* wn = w + (size_t)((y + 1 - Bk.b0) & 1) * ng;
+    double* toty = tot + ((y - Bk.b0) & 1) * (KGT_NF * KGT_CH);
+    // loads for later in this step: g of the next step, the lag entries of this step's nodes
+    double gn[GPT], gc[GPT];
+#pragma unroll
+    for (int k = 0; k < GPT; ++k) {
+      const int m = t + k * KGT_THREADS;
+      const int n = m < ng ? ord[m] : 0;
+      gn[k] = (m < ng && y < ymax) ? gt(y + 1, n) : 0.0;
+      gc[k] = (m < ng && y < ymax) ? gt(y, n) : 0.0;
+    }
+    double4 q[KGT_XPT];
+#pragma unroll
+    for (int k = 0; k < KGT_XPT; ++k) {
+      const int x = Bk.a0 + t + k * KGT_THREADS;
+      q[k] = (x <= Bk.a1 && x >= y + 3) ? B.lag[(long long)x * B.ldlag + y] : make_double4(0.0, 0.0, 0.0, 0.0);
+    }
+    // prefix sums of the 22 fields weighted by dg_y: the chunk total first, then (after the other
+    // chunks' totals are in) the chunk's scan again from its offset, one store per prefix entry --
+    // twice the FMAs, but only the fields are held in registers
+    double run = 0.0;
+#pragma unroll
+    for (int j = 0; j < CHM; ++j) run = fma(cs[j], wy[m0 + min(j, max(nm - 1, 0))], run);   // (cs = 0 past the chunk)
+    toty[t] = run;
+    __syncthreads();
+    run = 0.0;
+    for (int c2 = 0; c2 < c; ++c2) run += toty[c2 * KGT_NF + f];
+#pragma unroll
+    for (int j = 0; j < CHM; ++j) {
+      run = fma(cs[j], wy[m0 + min(j, max(nm - 1, 0))], run);
+      if (j < nm) Tf[m0 + j + 1] = run;
+    }
+#pragma unroll
+    for (int k = 0; k < GPT; ++k) {
+      const int m = t + k * KGT_THREADS;
+      if (m < ng) wn[m] = gn[k] - gc[k];
+    }
+    __syncthreads();
+    // the covered nodes of trial step y (lag table: s, ln s, u)
+#pragma unroll
+    for (int k = 0; k < KGT_XPT; ++k) {
+      const int x = Bk.a0 + t + k * KGT_THREADS;
+      if (x <= Bk.a1 && x >= y + 3) {
+        const double u = q[k].z;
+        int m = mx[k];                                        // m = #{c_max u < 8}, falling with y
+        while (m > 0 && !(cmx[m - 1] * u < STB_MXB)) --m;
+        mx[k] = m;
+        double acc = T[(size_t)MKA * ldt + m];
+#pragma unroll
+        for (int kk = MKA - 1; kk >= 0; --kk) acc = fma(acc, u, T[(size_t)kk * ldt + m]);
+        sx[k] += fma(-q[k].y, T[(size_t)(MKA + 1) * ldt + m], acc);
+      }
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < KGT_XPT; ++k) {
+    const int x = Bk.a0 + t + k * KGT_THREADS;
+    if (x <= Bk.a1) Sx[x - Bk.a0] = sx[k];
+  }
+  __syncthreads();
+  for (int a = Bk.a0 + t; a < Bk.a1; a += KGT_THREADS)
+    B.part[Bk.pbase + ((long long)(a - Bk.a0) * ng + i) * B.pslots + 2 * B.ntile + 5] = Sx[a + 1 - Bk.a0] - Sx[a - Bk.a0];
 }
 
 // ------------------------------------------------------------- near cells (d <= 1)

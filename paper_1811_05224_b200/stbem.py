@@ -66,6 +66,7 @@ class SolveReport(ctypes.Structure):
 
 QUAD_LEGACY_SING = 1   # bem_quad_opts.flags: touching pairs by the per-lag singular kernel
 QUAD_FULL_STORAGE = 2  # bem_quad_opts.flags: V_h / D_h stored full instead of symmetric packed
+QUAD_KG_ENTRYWISE = 4  # bem_quad_opts.flags: fused K_h g pair by pair (no trial-moment table)
 
 
 class AssemblyStats(ctypes.Structure):
@@ -74,13 +75,14 @@ class AssemblyStats(ctypes.Structure):
                 ("q_bulk", ctypes.c_int), ("q_sing", ctypes.c_int), ("launches", ctypes.c_int),
                 ("entries", ctypes.c_longlong), ("flops_bulk", ctypes.c_double),
                 ("ms_records", ctypes.c_double), ("nodes_bulk", ctypes.c_longlong * 4),
-                ("nodes_near", ctypes.c_longlong * 4), ("fused_sing", ctypes.c_int)]
+                ("nodes_near", ctypes.c_longlong * 4), ("fused_sing", ctypes.c_int),
+                ("nodes_bulk_tab", ctypes.c_longlong)]
 
     def as_dict(self):
         out = {}
         for k, _ in self._fields_:
             v = getattr(self, k)
-            out[k] = list(v) if k.startswith("nodes_") else v
+            out[k] = list(v) if isinstance(v, ctypes.Array) else v
         return out
 
 
@@ -370,10 +372,11 @@ def rhs(K, Mp, g, b, stream=None):
     return b
 
 
-def rhs_fused(mesh, Mp, g, b, q_bulk=0, q_sing=0, legacy_sing=False, stats=False, stream=None):
+def rhs_fused(mesh, Mp, g, b, q_bulk=0, q_sing=0, legacy_sing=False, stats=False, stream=None, entrywise=False):
     """b = 1/2 M g + K g with K_h computed on the fly and never stored (bem_rhs_fused); returns
-    the K_h kernel statistics when stats=True (synchronises), else b"""
-    o = quad_opts(q_bulk, q_sing, QUAD_LEGACY_SING if legacy_sing else 0)
+    the K_h kernel statistics when stats=True (synchronises), else b.  entrywise: every regime-A
+    node pair by pair (BEM_QUAD_KG_ENTRYWISE) instead of the trial-moment table"""
+    o = quad_opts(q_bulk, q_sing, (QUAD_LEGACY_SING if legacy_sing else 0) | (QUAD_KG_ENTRYWISE if entrywise else 0))
     st = AssemblyStats() if stats else None
     check(lib().bem_rhs_fused(mesh.h, ctypes.byref(o), Mp.h, _ptr(g), _ptr(b),
                               ctypes.byref(st) if stats else None, _stream(stream)))

@@ -318,6 +318,32 @@ def test_rhs_fused(name, n_slices):
     assert st["fused_sing"] == 1 and st["evals_bulk"] > 0
 
 
+@pytest.mark.parametrize("name,n_slices", [("C1", 1), ("C1", 3), ("C2", 1), ("C2", 5), ("C5", 1), ("ragged33", 1),
+                                          ("grade2", 2), ("pentagon", 1), ("alpha_small", 1), ("acute", 1)])
+def test_rhs_fused_trial_moment_table(name, n_slices):
+    """K_h g: the regime-A nodes of the interior bulk columns summed over the trial index first
+    (k_kg_tab, the default) against every node evaluated pair by pair (BEM_QUAD_KG_ENTRYWISE):
+    the same quadrature and regime forms re-associated, so equal to rounding; n_slices > 1 runs the
+    per-block tables of the multi-block list (trial ranges b0..b1 inside the block triangle)"""
+    from workloads.edge import edge_workloads
+    w = edge_workloads()[name] if name in edge_workloads() else W.get(name)
+    m = S.Mesh.from_workload(w, n_slices=n_slices)
+    g = cuda(W.dirichlet_data(w))
+    Mp = m.assemble_M(S.MASS_PRIMAL)
+    b_tab, b_ent = torch.empty_like(g), torch.empty_like(g)
+    st_t = S.rhs_fused(m, Mp, g, b_tab, stats=True)
+    st_e = S.rhs_fused(m, Mp, g, b_ent, stats=True, entrywise=True)
+    err = relmax(b_tab.cpu().numpy(), b_ent.cpu().numpy())
+    assert err <= 1e-12, err   # re-association over up to N_Gamma trial pairs (C5: 1.1e-13)
+    # the same nodes by regime; the table took a share of the regime-A ones (none without bulk nodes
+    # three steps apart)
+    assert st_t["nodes_bulk"] == st_e["nodes_bulk"]
+    assert st_e["nodes_bulk_tab"] == 0
+    assert st_t["nodes_bulk_tab"] <= st_t["nodes_bulk"][0]
+    if name in ("C1", "C2", "C5"):
+        assert st_t["nodes_bulk_tab"] > 0.5 * st_t["nodes_bulk"][0]
+
+
 @pytest.mark.parametrize("name", ["C1", "S32", "ragged33"])
 def test_block_toeplitz_variant(name):
     """row f3: on equal time steps the first block column T_d = A(d, 0) reproduces every entry
