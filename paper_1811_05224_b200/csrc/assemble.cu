@@ -651,7 +651,7 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, const Qua
       for (const BulkBlock& q : bl) nxmax = std::max(nxmax, q.a1 - q.a0 + 1);
       const size_t tab_smem = kg_tab_smem(ng, nxmax);
       BA.kgtab = prod && !(flags & BEM_QUAD_KG_ENTRYWISE) && tab_smem + 2048 <= (size_t)max_smem_optin() &&
-                 nxmax <= KGT_XPT * KGT_THREADS && (ng + KGT_CH - 1) / KGT_CH <= 40 ? 1 : 0;
+                 nxmax <= KGT_XPT * KGT_THREADS && kg_ch(ng) <= 40 ? 1 : 0;
       A->kg_tab = BA.kgtab;
       if (bl.size() == 1) {   // the single-block kernel takes the block from its parameters
         BA.poff = bl[0].poff;

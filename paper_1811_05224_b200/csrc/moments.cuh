@@ -1333,44 +1333,51 @@ __global__ void __launch_bounds__(128, KIND == STB_D ? STB_BULK_MINB_D : (KIND =
 // weight in every row that uses them is dg_y = g~_y - g~_{y-1} (g~ = g on the block's trial steps);
 // the per-pair kernel (kgtab) skips exactly these (same predicate on the same lag-table u).  Row a
 // receives S(a+1) - S(a), S(x) = sum_y of the node sums, in its own partial slot (2 ntile + 5).
-// CTA = (test segment i, listed block), thread = (field f, chunk c of the sorted pairs) for the
-// scans, with the chunk's 22 x CHM fields in registers: per trial step y one chunk-local scan in
-// registers, the chunk offsets through shared memory, the prefix table written once; then thread t
-// takes the test nodes x = a0 + t (+ KGT_THREADS): its node sums S(x) and its cutoff m stay in
-// registers (m only falls as y grows at fixed x: a walk down the sorted c_max instead of a search).
+// CTA = (test segment i, listed block), thread = (field f, chunk c of the sorted pairs): lanes
+// 0-15 / 16-31 of a warp are the 16 chunks of two fields, the chunk's fields in registers.  Per
+// trial step y: the chunk total, its exclusive prefix over the chunks by a 16-lane shuffle scan,
+// the chunk's scan again from that offset into the prefix table; then thread t takes the test
+// nodes x = a0 + t (+ KGT_THREADS), whose sums S(x) and cutoffs m stay in registers (m only falls
+// as y grows at fixed x: a walk down the sorted c_max instead of a search).  The prefix table and
+// the weights are double-buffered, so one barrier per trial step separates the scans of y from
+// the node reads of y (and, one step later, from the scans of y + 2 into the same buffer).
+// Storage of the pairs in chunks of ch with one padding slot per chunk (stride ch + 1, odd for
+// the even chunk lengths): the 16 lanes of a field read and write 16 different banks.
 constexpr int KGT_NF = MKA + 2;
 constexpr int KGT_CH = 16;
 constexpr int KGT_THREADS = KGT_NF * KGT_CH;   // 352
 constexpr int KGT_XPT = 2;                     // test nodes per thread: N_I + 1 <= 704
-// odd row stride of the [field][m] prefix table: the 22 lanes of a chunk write 22 different banks
-__host__ __device__ inline int kg_ld_t(int ng) { return (ng + 1) | 1; }
+__host__ __device__ inline int kg_ch(int ng) { return (ng + KGT_CH - 1) / KGT_CH; }
+__host__ __device__ inline int kg_pch(int ng) { return kg_ch(ng) + 1 - (kg_ch(ng) & 1); }   // odd, > ch - 1
+__host__ __device__ inline int kg_ld_t(int ng) { return (KGT_CH * kg_pch(ng) + 1) | 1; }
 __host__ __device__ inline size_t kg_tab_smem(int ng, int nxmax) {
-  return sizeof(double) * ((size_t)KGT_NF * kg_ld_t(ng) + 3 * (size_t)ng + nxmax + 2 * KGT_NF * KGT_CH) +
-         sizeof(int) * (size_t)ng;
+  return sizeof(double) * (2 * (size_t)KGT_NF * kg_ld_t(ng) + 2 * ((size_t)KGT_CH * kg_pch(ng) + 40) + (size_t)ng + nxmax) +
+         sizeof(int) * (2 * (size_t)ng + 1);
 }
 // pairs per chunk the register arrays hold (template instances 24: N_Gamma <= 384, 40: <= 640)
-__host__ __device__ inline int kg_chm(int ng) { return (ng + KGT_CH - 1) / KGT_CH <= 24 ? 24 : 40; }
-#ifndef STB_KGT_MINB
-#define STB_KGT_MINB 1   // CTAs per SM of k_kg_tab<24> (2: 80 registers with spills, C5 3.2 vs 2.4 ms)
-#endif
+__host__ __device__ inline int kg_chm(int ng) { return kg_ch(ng) <= 24 ? 24 : 40; }
 template <int CHM>
-__global__ void __launch_bounds__(KGT_THREADS, CHM <= 24 ? STB_KGT_MINB : 1) k_kg_tab(BlockArgs B, BulkList L, MomArgs M, int nxmax) {
+__global__ void __launch_bounds__(KGT_THREADS, 1) k_kg_tab(BlockArgs B, BulkList L, MomArgs M, int nxmax) {
   extern __shared__ __align__(16) double kgt[];
   const int ng = B.ng, i = blockIdx.x, t = threadIdx.x;
   const BulkBlock Bk = L.blk[blockIdx.y];
   const int ymax = min(Bk.b1, Bk.a1 - 3);
   if (ymax < Bk.b0) return;                                   // CTA-uniform: no covered node
   const long long S = M.npairs;
-  const int ldt = kg_ld_t(ng);
-  double* T = kgt;                                            // [KGT_NF][ldt] prefix sums (m = 0..ng)
-  double* cmx = T + (size_t)KGT_NF * ldt;                     // [ng] sorted c_max
-  double* w = cmx + ng;                                       // [2][ng] dg_y in sorted order
-  double* Sx = w + 2 * ng;                                    // [nx] node sums S(x) (end)
-  double* tot = Sx + nxmax;                                   // [2][KGT_CH][KGT_NF] chunk totals
-  int* ord = reinterpret_cast<int*>(tot + 2 * KGT_NF * KGT_CH);   // [ng]
+  // ldw: one weight buffer, its last chunk followed by CHM zeros (the scans read CHM entries per chunk)
+  const int ch = kg_ch(ng), pch = kg_pch(ng), ldt = kg_ld_t(ng), ldw = KGT_CH * pch + CHM;
+  double* T = kgt;                                            // [2][KGT_NF][ldt] prefix sums
+  double* w = T + 2 * (size_t)KGT_NF * ldt;                   // [2][ldw] dg_y, padded sorted order
+  double* cmx = w + 2 * (size_t)ldw;                          // [ng] sorted c_max
+  double* Sx = cmx + ng;                                      // [nx] node sums S(x) (end)
+  int* ord = reinterpret_cast<int*>(Sx + nxmax);              // [ng] pair of sorted index m
+  int* pos = ord + ng;                                        // [ng + 1] table slot of prefix m
   const double* rec = M.rec + (long long)i * ng;
+  auto padm = [&](int m) { return (m / ch) * pch + m % ch; };
   // sort the row's pairs by c_max (rank = #smaller, ties by index): the scratch is T's space
   for (int n = t; n < ng; n += KGT_THREADS) T[n] = rec[RF_CMAX * S + n];
+  for (int e = t; e < 2 * ldw; e += KGT_THREADS) w[e] = 0.0;   // padding slots stay 0
+  for (int m = t; m <= ng; m += KGT_THREADS) pos[m] = m == 0 ? 0 : 1 + padm(m - 1);
   __syncthreads();
   for (int n = t; n < ng; n += KGT_THREADS) {
     const double c = T[n];
@@ -1384,15 +1391,13 @@ __global__ void __launch_bounds__(KGT_THREADS, CHM <= 24 ? STB_KGT_MINB : 1) k_k
   }
   __syncthreads();
   // this thread's fields in sorted order (registers)
-  const int ch = (ng + KGT_CH - 1) / KGT_CH;
-  const int f = t % KGT_NF, c = t / KGT_NF;
+  const int f = t / KGT_CH, c = t % KGT_CH;
   const int m0 = min(ng, c * ch), nm = min(ng, m0 + ch) - m0;
   const double* Rf = rec + (long long)(RF_COMMON + (f < MKA + 1 ? FA + f : FM0)) * S;
   double cs[CHM];
 #pragma unroll
   for (int j = 0; j < CHM; ++j) cs[j] = j < nm ? Rf[ord[m0 + j]] : 0.0;
-  double* Tf = T + (size_t)f * ldt;
-  if (c == 0) Tf[0] = 0.0;
+  if (c == 0) T[(size_t)f * ldt] = T[((size_t)KGT_NF + f) * ldt] = 0.0;   // prefix m = 0
   auto gt = [&](int yy, int n) -> double {   // g~ on the block's trial steps
     return (yy >= Bk.b0 && yy < Bk.b1) ? B.g[(long long)yy * ng + n] : 0.0;
   };
@@ -1404,17 +1409,17 @@ __global__ void __launch_bounds__(KGT_THREADS, CHM <= 24 ? STB_KGT_MINB : 1) k_k
     sx[k] = 0.0;
     mx[k] = ng;
   }
-  // software pipeline over the trial steps y: the weights dg_(y+1) (double-buffered w) and the
-  // chunk totals (double-buffered tot) of the next step, so that two barriers per step suffice:
-  //   [scan 1: tot(y) from w(y); loads of g(y+1), lag(x, y)] B1 [scan 2: T(y); w(y+1) stored] B2 [nodes(y)]
-  // (T(y) is rewritten only after B1 of y+1, which every thread reaches after its nodes of y)
-  constexpr int GPT = 2;   // pairs per thread of the w loads: N_Gamma <= 704
-  for (int m = t; m < ng; m += KGT_THREADS) w[m] = gt(Bk.b0, ord[m]) - gt(Bk.b0 - 1, ord[m]);
+  constexpr int GPT = 2;   // pairs per thread of the weight loads: N_Gamma <= 704
+  int wslot[GPT];          // their slots in a weight buffer (the division once)
+#pragma unroll
+  for (int k = 0; k < GPT; ++k) wslot[k] = padm(min(ng - 1, t + k * KGT_THREADS));
+  for (int m = t; m < ng; m += KGT_THREADS) w[padm(m)] = gt(Bk.b0, ord[m]) - gt(Bk.b0 - 1, ord[m]);
   __syncthreads();
   for (int y = Bk.b0; y <= ymax; ++y) {
-    const double* wy = w + (size_t)((y - Bk.b0) & 1) * ng;
-    double* wn = w + (size_t)((y + 1 - Bk.b0) & 1) * ng;
-    double* toty = tot + ((y - Bk.b0) & 1) * (KGT_NF * KGT_CH);
+    const int par = (y - Bk.b0) & 1;
+    const double* wy = w + (size_t)par * ldw + c * pch;
+    double* wn = w + (size_t)(par ^ 1) * ldw;
+    double* Ty = T + (size_t)par * KGT_NF * ldt;
     // loads for later in this step: g of the next step, the lag entries of this step's nodes
     double gn[GPT], gc[GPT];
 #pragma unroll
@@ -1430,25 +1435,38 @@ __global__ void __launch_bounds__(KGT_THREADS, CHM <= 24 ? STB_KGT_MINB : 1) k_k
       const int x = Bk.a0 + t + k * KGT_THREADS;
       q[k] = (x <= Bk.a1 && x >= y + 3) ? B.lag[(long long)x * B.ldlag + y] : make_double4(0.0, 0.0, 0.0, 0.0);
     }
-    // prefix sums of the 22 fields weighted by dg_y: the chunk total first, then (after the other
-    // chunks' totals are in) the chunk's scan again from its offset, one store per prefix entry --
-    // twice the FMAs, but only the fields are held in registers
-    double run = 0.0;
+    // prefix sums of the 22 fields weighted by dg_y: the chunk total, its exclusive prefix over the
+    // field's 16 chunks (lanes of one half warp), the chunk's scan again from there
+    double tot = 0.0;
 #pragma unroll
-    for (int j = 0; j < CHM; ++j) run = fma(cs[j], wy[m0 + min(j, max(nm - 1, 0))], run);   // (cs = 0 past the chunk)
-    toty[t] = run;
-    __syncthreads();
-    run = 0.0;
-    for (int c2 = 0; c2 < c; ++c2) run += toty[c2 * KGT_NF + f];
+    for (int j = 0; j < CHM; ++j) tot = fma(cs[j], wy[j], tot);   // (past the chunk: cs = 0, wy finite)
+    // (exclusive scan of the totals shifted by one lane: inc - tot would cancel the small prefix
+    // against the large totals of the last chunks, whose c_max^k moments dominate the high fields)
+    double run = __shfl_up_sync(0xffffffffu, tot, 1, KGT_CH);
+    if (c == 0) run = 0.0;
 #pragma unroll
-    for (int j = 0; j < CHM; ++j) {
-      run = fma(cs[j], wy[m0 + min(j, max(nm - 1, 0))], run);
-      if (j < nm) Tf[m0 + j + 1] = run;
+    for (int d = 1; d < KGT_CH; d <<= 1) {
+      const double v = __shfl_up_sync(0xffffffffu, run, d, KGT_CH);
+      if (c >= d) run += v;
+    }
+    double* Tc = Ty + (size_t)f * ldt + 1 + c * pch;
+    if (nm == CHM) {   // full chunks (every chunk when CHM = ch and 16 | N_Gamma): no store predicates
+#pragma unroll
+      for (int j = 0; j < CHM; ++j) {
+        run = fma(cs[j], wy[j], run);
+        Tc[j] = run;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < CHM; ++j) {
+        run = fma(cs[j], wy[j], run);
+        if (j < nm) Tc[j] = run;
+      }
     }
 #pragma unroll
     for (int k = 0; k < GPT; ++k) {
       const int m = t + k * KGT_THREADS;
-      if (m < ng) wn[m] = gn[k] - gc[k];
+      if (m < ng) wn[wslot[k]] = gn[k] - gc[k];
     }
     __syncthreads();
     // the covered nodes of trial step y (lag table: s, ln s, u)
@@ -1460,14 +1478,14 @@ __global__ void __launch_bounds__(KGT_THREADS, CHM <= 24 ? STB_KGT_MINB : 1) k_k
         int m = mx[k];                                        // m = #{c_max u < 8}, falling with y
         while (m > 0 && !(cmx[m - 1] * u < STB_MXB)) --m;
         mx[k] = m;
-        double acc = T[(size_t)MKA * ldt + m];
+        const double* Tm = Ty + pos[m];
+        double acc = Tm[(size_t)MKA * ldt];
 #pragma unroll
-        for (int kk = MKA - 1; kk >= 0; --kk) acc = fma(acc, u, T[(size_t)kk * ldt + m]);
-        sx[k] += fma(-q[k].y, T[(size_t)(MKA + 1) * ldt + m], acc);
+        for (int kk = MKA - 1; kk >= 0; --kk) acc = fma(acc, u, Tm[(size_t)kk * ldt]);
+        sx[k] += fma(-q[k].y, Tm[(size_t)(MKA + 1) * ldt], acc);
       }
     }
   }
-  __syncthreads();
 #pragma unroll
   for (int k = 0; k < KGT_XPT; ++k) {
     const int x = Bk.a0 + t + k * KGT_THREADS;
