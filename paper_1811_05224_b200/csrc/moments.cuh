@@ -1124,7 +1124,35 @@ __global__ void __launch_bounds__(128, KIND == STB_D ? STB_BULK_MINB_D : (KIND =
     }
     asm volatile("cp.async.commit_group;");
   };
-  stage(0);
+  // K_h g with the table: the leading columns whose nodes are all regime A for every lane of the
+  // CTA are the table's entirely (A at the band's first node x = r_lo implies A at every node: u
+  // falls with x, and rises with y) -- the loop starts at the first chunk holding a column where a
+  // lane leaves regime A (binary search along the lag row of x = r_lo, CTA minimum)
+  int ystart = Bk.b0;
+  if (PROD && B.kgtab) {
+    __shared__ int s_ys[4];
+    const int yhi = min(bmax + 1, r_lo - 2);          // the table columns are y <= r_lo - 3
+    int lo = Bk.b0, hi = max(Bk.b0, yhi);
+    if (valid && !zero_warp) {
+      const double4* lrow = B.lag + (long long)r_lo * B.ldlag;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (A.cmax * lrow[mid].z < STB_MXB) lo = mid + 1;
+        else hi = mid;
+      }
+    } else {
+      lo = max(Bk.b0, yhi);
+    }
+    lo = __reduce_min_sync(0xffffffffu, lo);
+    if (lane == 0) s_ys[threadIdx.x >> 5] = lo;
+    __syncthreads();
+    ystart = min(min(s_ys[0], s_ys[1]), min(s_ys[2], s_ys[3]));
+    ystart = Bk.b0 + ((ystart - Bk.b0) / LAG_CH) * LAG_CH;   // a chunk boundary
+    const unsigned long long skipped = (unsigned long long)(ystart - Bk.b0) * (r_hi - r_lo + 1);
+    nA += skipped;
+    nT += skipped;
+  }
+  stage((ystart - Bk.b0) / LAG_CH);
   if (!PROD && lane < R) {
     const int a = min(r_lo + lane, r_hi - 1);
     srow[lane] = Bk.poff[a - Bk.a0] + (B.sym ? sym_tile_offset(ti, tj, B.nt) + sym_row_base(I % SYM_TS, ti == tj)
@@ -1138,7 +1166,8 @@ __global__ void __launch_bounds__(128, KIND == STB_D ? STB_BULK_MINB_D : (KIND =
 #pragma unroll
   for (int r = 0; r < (PROD ? 1 : R); ++r) Gp[r] = 0.0;
   double gprev = 0.0;        // product mode: g of the previous trial step (0 before b0)
-  for (int y = Bk.b0; y <= bmax + 1; ++y) {
+  bool gp_ok = ystart == Bk.b0;   // gprev holds it (else loaded when the next column is used)
+  for (int y = ystart; y <= bmax + 1; ++y) {
     const int kc = y - Bk.b0;
     if (kc % LAG_CH == 0) {                          // CTA-uniform: chunk kc / LAG_CH is needed
       asm volatile("cp.async.wait_group 0;" ::: "memory");
@@ -1170,6 +1199,10 @@ __global__ void __launch_bounds__(128, KIND == STB_D ? STB_BULK_MINB_D : (KIND =
         nA += ok && inA;
         nT += ok && inA;
         if (ok && !inA && !zero_warp) bmask |= 1u << r;
+      }
+      if (!__any_sync(0xffffffffu, bmask != 0)) {   // the table's column entirely
+        gp_ok = false;
+        continue;
       }
     } else if (zero_warp) {
 #pragma unroll
@@ -1263,6 +1296,7 @@ __global__ void __launch_bounds__(128, KIND == STB_D ? STB_BULK_MINB_D : (KIND =
       // g~_y = g_y on the row's bulk columns b0 <= y <= min(bmax, a - 2), 0 elsewhere (the same
       // sum, re-associated: no previous-column G per row is kept)
       const double gv = (valid && y <= bmax) ? B.g[(long long)y * ng + J] : 0.0;
+      if (!gp_ok) gprev = (valid && y - 1 >= Bk.b0 && y - 1 <= bmax) ? B.g[(long long)(y - 1) * ng + J] : 0.0;
       if (y <= r_lo - 2 && r_hi - r_lo == R) {      // interior column: g~ = g for every row
         const double dg = gv - gprev;
 #pragma unroll
@@ -1276,6 +1310,7 @@ __global__ void __launch_bounds__(128, KIND == STB_D ? STB_BULK_MINB_D : (KIND =
         }
       }
       gprev = gv;
+      gp_ok = true;
     } else if (y > Bk.b0) {
       const int b = y - 1;
       // interior column: every band row is a full bulk cell (no per-row conditions)
