@@ -651,7 +651,7 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, const Qua
       for (const BulkBlock& q : bl) nxmax = std::max(nxmax, q.a1 - q.a0 + 1);
       const size_t tab_smem = kg_tab_smem(ng, nxmax);
       BA.kgtab = prod && !(flags & BEM_QUAD_KG_ENTRYWISE) && tab_smem + 2048 <= (size_t)max_smem_optin() &&
-                 nxmax <= KGT_XPT * KGT_THREADS && kg_ch(ng) <= 40 ? 1 : 0;
+                 nxmax <= KGT_NODE && ng <= KGT_THREADS && kg_ch(ng) <= 20 ? 1 : 0;
       A->kg_tab = BA.kgtab;
       if (bl.size() == 1) {   // the single-block kernel takes the block from its parameters
         BA.poff = bl[0].poff;
@@ -664,13 +664,13 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, const Qua
         if (BA.kgtab) {
           static bool attr = false;
           if (!attr) {
-            cudaFuncSetAttribute(k_kg_tab<24>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem_optin() - 2048);
-            cudaFuncSetAttribute(k_kg_tab<40>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem_optin() - 2048);
+            cudaFuncSetAttribute(k_kg_tab<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem_optin() - 2048);
+            cudaFuncSetAttribute(k_kg_tab<20>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem_optin() - 2048);
             attr = true;
           }
           const dim3 tg((unsigned)ng, (unsigned)bl.size());
-          if (kg_chm(ng) == 24) k_kg_tab<24><<<tg, KGT_THREADS, tab_smem, st>>>(BA, L, MB, nxmax);
-          else k_kg_tab<40><<<tg, KGT_THREADS, tab_smem, st>>>(BA, L, MB, nxmax);
+          if (kg_chm(ng) == 12) k_kg_tab<12><<<tg, KGT_THREADS, tab_smem, st>>>(BA, L, MB, nxmax);
+          else k_kg_tab<20><<<tg, KGT_THREADS, tab_smem, st>>>(BA, L, MB, nxmax);
           count_launch();
           A->launches++;
           // algorithmic flops of the table: per (i, trial step y) the 22 prefix scans (one FMA per pair

@@ -1368,29 +1368,29 @@ __global__ void __launch_bounds__(128, KIND == STB_D ? STB_BULK_MINB_D : (KIND =
 // weight in every row that uses them is dg_y = g~_y - g~_{y-1} (g~ = g on the block's trial steps);
 // the per-pair kernel (kgtab) skips exactly these (same predicate on the same lag-table u).  Row a
 // receives S(a+1) - S(a), S(x) = sum_y of the node sums, in its own partial slot (2 ntile + 5).
-// CTA = (test segment i, listed block), thread = (field f, chunk c of the sorted pairs): lanes
-// 0-15 / 16-31 of a warp are the 16 chunks of two fields, the chunk's fields in registers.  Per
-// trial step y: the chunk total, its exclusive prefix over the chunks by a 16-lane shuffle scan,
+// CTA = (test segment i, listed block), thread = (field f, chunk c of the sorted pairs): warp f,
+// lane c -- the 32 chunks of one field per warp, the chunk's fields in registers.  Per trial step
+// y: the chunk total, its exclusive prefix over the chunks by a warp shuffle scan,
 // the chunk's scan again from that offset into the prefix table; then thread t takes the test
 // nodes x = a0 + t (+ KGT_THREADS), whose sums S(x) and cutoffs m stay in registers (m only falls
 // as y grows at fixed x: a walk down the sorted c_max instead of a search).  The prefix table and
 // the weights are double-buffered, so one barrier per trial step separates the scans of y from
 // the node reads of y (and, one step later, from the scans of y + 2 into the same buffer).
 // Storage of the pairs in chunks of ch with one padding slot per chunk (stride ch + 1, odd for
-// the even chunk lengths): the 16 lanes of a field read and write 16 different banks.
+// the even chunk lengths): the 32 lanes of a field read and write 32 different banks.
 constexpr int KGT_NF = MKA + 2;
-constexpr int KGT_CH = 16;
-constexpr int KGT_THREADS = KGT_NF * KGT_CH;   // 352
-constexpr int KGT_XPT = 2;                     // test nodes per thread: N_I + 1 <= 704
+constexpr int KGT_CH = 32;
+constexpr int KGT_THREADS = KGT_NF * KGT_CH;   // 704
 __host__ __device__ inline int kg_ch(int ng) { return (ng + KGT_CH - 1) / KGT_CH; }
 __host__ __device__ inline int kg_pch(int ng) { return kg_ch(ng) + 1 - (kg_ch(ng) & 1); }   // odd, > ch - 1
 __host__ __device__ inline int kg_ld_t(int ng) { return (KGT_CH * kg_pch(ng) + 1) | 1; }
 __host__ __device__ inline size_t kg_tab_smem(int ng, int nxmax) {
   return sizeof(double) * (2 * (size_t)KGT_NF * kg_ld_t(ng) + 2 * ((size_t)KGT_CH * kg_pch(ng) + 40) + (size_t)ng + nxmax) +
-         sizeof(int) * (2 * (size_t)ng + 1);
+         sizeof(int) * (2 * (size_t)ng + 1 + 3 * (size_t)nxmax);
 }
-// pairs per chunk the register arrays hold (template instances 24: N_Gamma <= 384, 40: <= 640)
-__host__ __device__ inline int kg_chm(int ng) { return kg_ch(ng) <= 24 ? 24 : 40; }
+constexpr int KGT_NODE = KGT_THREADS / 2;   // threads [0, 352) evaluate the nodes, [352, 704) find their cutoffs
+// pairs per chunk the register arrays hold (template instances 12: N_Gamma <= 384, 20: <= 640)
+__host__ __device__ inline int kg_chm(int ng) { return kg_ch(ng) <= 12 ? 12 : 20; }
 template <int CHM>
 __global__ void __launch_bounds__(KGT_THREADS, 1) k_kg_tab(BlockArgs B, BulkList L, MomArgs M, int nxmax) {
   extern __shared__ __align__(16) double kgt[];
@@ -1407,6 +1407,7 @@ __global__ void __launch_bounds__(KGT_THREADS, 1) k_kg_tab(BlockArgs B, BulkList
   double* Sx = cmx + ng;                                      // [nx] node sums S(x) (end)
   int* ord = reinterpret_cast<int*>(Sx + nxmax);              // [ng] pair of sorted index m
   int* pos = ord + ng;                                        // [ng + 1] table slot of prefix m
+  int* mcut = pos + ng + 1;                                   // [3][nxmax] cutoffs m(x, y), y mod 3
   const double* rec = M.rec + (long long)i * ng;
   auto padm = [&](int m) { return (m / ch) * pch + m % ch; };
   // sort the row's pairs by c_max (rank = #smaller, ties by index): the scratch is T's space
@@ -1436,56 +1437,73 @@ __global__ void __launch_bounds__(KGT_THREADS, 1) k_kg_tab(BlockArgs B, BulkList
   auto gt = [&](int yy, int n) -> double {   // g~ on the block's trial steps
     return (yy >= Bk.b0 && yy < Bk.b1) ? B.g[(long long)yy * ng + n] : 0.0;
   };
-  // the test nodes of this thread, their sums and cutoffs
-  double sx[KGT_XPT];
-  int mx[KGT_XPT];
-#pragma unroll
-  for (int k = 0; k < KGT_XPT; ++k) {
-    sx[k] = 0.0;
-    mx[k] = ng;
-  }
-  constexpr int GPT = 2;   // pairs per thread of the weight loads: N_Gamma <= 704
-  int wslot[GPT];          // their slots in a weight buffer (the division once)
-#pragma unroll
-  for (int k = 0; k < GPT; ++k) wslot[k] = padm(min(ng - 1, t + k * KGT_THREADS));
+  // node x = a0 + t (threads t < KGT_NODE: its sum S(x)); cutoff thread t' = t - KGT_NODE finds
+  // m(x', y + 1) for node x' = a0 + t' during step y (galloping down from m(x', y): the cutoff only
+  // falls as y grows), triple-buffered by y mod 3 so that one barrier per step orders it
+  const bool nodet = t < KGT_NODE;
+  const int xk = Bk.a0 + (nodet ? t : t - KGT_NODE);
+  const int nxk = Bk.a1 - Bk.a0 + 1;
+  double sx = 0.0;
+  int mprev = ng;
+  auto cutoff = [&](double u, int H) {          // #{m : c_max[m] u < 8} given it is <= H
+    int L = -1, step = 1;
+    while (true) {
+      const int k = H - step;
+      if (k < 0) break;
+      if (cmx[k] * u < STB_MXB) { L = k; break; }
+      H = k;
+      step <<= 1;
+    }
+    while (H - L > 1) {
+      const int mid = (L + H) >> 1;
+      if (cmx[mid] * u < STB_MXB) L = mid;
+      else H = mid;
+    }
+    return H;
+  };
+  const int wslot = padm(min(ng - 1, t));
+  const int nt_ = t < ng ? ord[t] : 0;
   for (int m = t; m < ng; m += KGT_THREADS) w[padm(m)] = gt(Bk.b0, ord[m]) - gt(Bk.b0 - 1, ord[m]);
+  // global loads one trial step ahead (L2 latency off the step's critical path): the lag entry
+  // (u, ln s) of this thread's node (node threads: step y + 1; cutoff threads: step y + 2) and g
+  // of the weights stored during the step
+  auto ldq = [&](int yy) -> double2 {
+    if (yy > ymax || xk > Bk.a1 || xk < yy + 3) return make_double2(0.0, 0.0);
+    const double4 q = B.lag[(long long)xk * B.ldlag + yy];
+    return make_double2(q.z, q.y);
+  };
+  if (!nodet && xk <= Bk.a1 && xk >= Bk.b0 + 3) {          // cutoff of step b0
+    mprev = cutoff(ldq(Bk.b0).x, ng);
+    mcut[xk - Bk.a0] = mprev;
+  }
+  double2 qc = ldq(nodet ? Bk.b0 : Bk.b0 + 1);
+  double ga = (t < ng && Bk.b0 < ymax) ? gt(Bk.b0 + 1, nt_) : 0.0;   // weights of step b0 + 1
+  double gb = (t < ng && Bk.b0 < ymax) ? gt(Bk.b0, nt_) : 0.0;
   __syncthreads();
   for (int y = Bk.b0; y <= ymax; ++y) {
     const int par = (y - Bk.b0) & 1;
     const double* wy = w + (size_t)par * ldw + c * pch;
     double* wn = w + (size_t)(par ^ 1) * ldw;
     double* Ty = T + (size_t)par * KGT_NF * ldt;
-    // loads for later in this step: g of the next step, the lag entries of this step's nodes
-    double gn[GPT], gc[GPT];
-#pragma unroll
-    for (int k = 0; k < GPT; ++k) {
-      const int m = t + k * KGT_THREADS;
-      const int n = m < ng ? ord[m] : 0;
-      gn[k] = (m < ng && y < ymax) ? gt(y + 1, n) : 0.0;
-      gc[k] = (m < ng && y < ymax) ? gt(y, n) : 0.0;
-    }
-    double4 q[KGT_XPT];
-#pragma unroll
-    for (int k = 0; k < KGT_XPT; ++k) {
-      const int x = Bk.a0 + t + k * KGT_THREADS;
-      q[k] = (x <= Bk.a1 && x >= y + 3) ? B.lag[(long long)x * B.ldlag + y] : make_double4(0.0, 0.0, 0.0, 0.0);
-    }
+    const double2 qn = ldq(nodet ? y + 1 : y + 2);
+    const double gan = (t < ng && y + 1 < ymax) ? gt(y + 2, nt_) : 0.0;
+    const double gbn = (t < ng && y + 1 < ymax) ? gt(y + 1, nt_) : 0.0;
     // prefix sums of the 22 fields weighted by dg_y: the chunk total, its exclusive prefix over the
-    // field's 16 chunks (lanes of one half warp), the chunk's scan again from there
+    // field's 32 chunks (the lanes of its warp), the chunk's scan again from there
     double tot = 0.0;
 #pragma unroll
     for (int j = 0; j < CHM; ++j) tot = fma(cs[j], wy[j], tot);   // (past the chunk: cs = 0, wy finite)
     // (exclusive scan of the totals shifted by one lane: inc - tot would cancel the small prefix
     // against the large totals of the last chunks, whose c_max^k moments dominate the high fields)
-    double run = __shfl_up_sync(0xffffffffu, tot, 1, KGT_CH);
+    double run = __shfl_up_sync(0xffffffffu, tot, 1);
     if (c == 0) run = 0.0;
 #pragma unroll
     for (int d = 1; d < KGT_CH; d <<= 1) {
-      const double v = __shfl_up_sync(0xffffffffu, run, d, KGT_CH);
+      const double v = __shfl_up_sync(0xffffffffu, run, d);
       if (c >= d) run += v;
     }
     double* Tc = Ty + (size_t)f * ldt + 1 + c * pch;
-    if (nm == CHM) {   // full chunks (every chunk when CHM = ch and 16 | N_Gamma): no store predicates
+    if (nm == CHM) {   // full chunks (every chunk when CHM = ch and 32 | N_Gamma): no store predicates
 #pragma unroll
       for (int j = 0; j < CHM; ++j) {
         run = fma(cs[j], wy[j], run);
@@ -1498,34 +1516,27 @@ __global__ void __launch_bounds__(KGT_THREADS, 1) k_kg_tab(BlockArgs B, BulkList
         if (j < nm) Tc[j] = run;
       }
     }
-#pragma unroll
-    for (int k = 0; k < GPT; ++k) {
-      const int m = t + k * KGT_THREADS;
-      if (m < ng) wn[wslot[k]] = gn[k] - gc[k];
+    if (t < ng && y < ymax) wn[wslot] = ga - gb;
+    // cutoff threads: m(x', y + 1) into buffer (y + 1) mod 3
+    if (!nodet && xk <= Bk.a1 && xk >= y + 4 && y < ymax) {
+      mprev = cutoff(qc.x, mprev);
+      mcut[((y + 1 - Bk.b0) % 3) * nxk + xk - Bk.a0] = mprev;
     }
     __syncthreads();
-    // the covered nodes of trial step y (lag table: s, ln s, u)
+    // the covered node of trial step y (lag table: s, ln s, u)
+    if (nodet && xk <= Bk.a1 && xk >= y + 3) {
+      const double u = qc.x;
+      const double* Tm = Ty + pos[mcut[((y - Bk.b0) % 3) * nxk + xk - Bk.a0]];
+      double acc = Tm[(size_t)MKA * ldt];
 #pragma unroll
-    for (int k = 0; k < KGT_XPT; ++k) {
-      const int x = Bk.a0 + t + k * KGT_THREADS;
-      if (x <= Bk.a1 && x >= y + 3) {
-        const double u = q[k].z;
-        int m = mx[k];                                        // m = #{c_max u < 8}, falling with y
-        while (m > 0 && !(cmx[m - 1] * u < STB_MXB)) --m;
-        mx[k] = m;
-        const double* Tm = Ty + pos[m];
-        double acc = Tm[(size_t)MKA * ldt];
-#pragma unroll
-        for (int kk = MKA - 1; kk >= 0; --kk) acc = fma(acc, u, Tm[(size_t)kk * ldt]);
-        sx[k] += fma(-q[k].y, Tm[(size_t)(MKA + 1) * ldt], acc);
-      }
+      for (int kk = MKA - 1; kk >= 0; --kk) acc = fma(acc, u, Tm[(size_t)kk * ldt]);
+      sx += fma(-qc.y, Tm[(size_t)(MKA + 1) * ldt], acc);
     }
+    qc = qn;
+    ga = gan;
+    gb = gbn;
   }
-#pragma unroll
-  for (int k = 0; k < KGT_XPT; ++k) {
-    const int x = Bk.a0 + t + k * KGT_THREADS;
-    if (x <= Bk.a1) Sx[x - Bk.a0] = sx[k];
-  }
+  if (nodet && xk <= Bk.a1) Sx[xk - Bk.a0] = sx;
   __syncthreads();
   for (int a = Bk.a0 + t; a < Bk.a1; a += KGT_THREADS)
     B.part[Bk.pbase + ((long long)(a - Bk.a0) * ng + i) * B.pslots + 2 * B.ntile + 5] = Sx[a + 1 - Bk.a0] - Sx[a - Bk.a0];
