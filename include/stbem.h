@@ -108,19 +108,25 @@ typedef struct {
   double rel_tol;  /* stop when ||C(b - V w_k)|| <= rel_tol ||C b|| (Givens estimate) */
   int max_iter;    /* full GMRES, no restart */
   int precond;     /* 0 none, 1 lumped dual mass, 2 exact dual mass (cyclic tridiagonal) */
+  int flags;       /* BEM_GMRES_* below (0: defaults) */
 } bem_gmres_opts;
+/* the true residual at exit from two fresh products C V w (one V_h and one D_h product more)
+ * instead of from the products of the Arnoldi steps: C(b - V w) = C b - sum_i y_i (C V q_i) by
+ * linearity, with the vectors C V q_i kept as they leave the products (before orthogonalisation),
+ * so that the default check costs no product; both are independent of the Givens recurrence */
+#define BEM_GMRES_FRESH_RESIDUAL 1
 
 typedef struct {
   int iterations;
   int converged;
   double rel_residual;       /* Givens estimate at exit */
-  double true_rel_residual;  /* ||C(b - V w)|| / ||C b|| recomputed at exit */
+  double true_rel_residual;  /* ||C(b - V w)|| / ||C b|| recomputed at exit (BEM_GMRES_FRESH_RESIDUAL) */
   double seconds_total;
   double seconds_matvec;     /* V and D products (device time) */
   double seconds_comm;       /* collectives: device time of the NCCL calls (CUDA events on their
                                 stream, overlapped with the GEMV where chunked), host time of the
                                 emulated ranks' all-reduces; 0 without a communicator */
-  int n_matvec_V;            /* V_h products performed (incl. the true-residual check) */
+  int n_matvec_V;            /* V_h products performed (incl. a fresh true-residual check) */
   int n_matvec_D;            /* D_h products performed */
 } bem_solve_report;
 

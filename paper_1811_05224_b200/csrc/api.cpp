@@ -375,6 +375,8 @@ bem_status bem_solve_gmres(const bem_matrix* V, const bem_matrix* D, const bem_m
     }
   }
   if (!(opts->rel_tol > 0) || opts->max_iter < 1) { set_error("bem_solve_gmres: rel_tol > 0 and max_iter >= 1 required"); return BEM_E_INVALID; }
+  if (opts->flags & ~BEM_GMRES_FRESH_RESIDUAL) { set_error("bem_solve_gmres: unknown flags"); return BEM_E_INVALID; }
+  const bool fresh_res = (opts->flags & BEM_GMRES_FRESH_RESIDUAL) != 0;
   if (V->mesh->comm && V->mesh->comm->solo) { set_error("bem_solve_gmres: a solo rank holds partial products only"); return BEM_E_STATE; }
   const bem_mesh* m = V->mesh;
   cudaSetDevice(m->device);
@@ -382,6 +384,7 @@ bem_status bem_solve_gmres(const bem_matrix* V, const bem_matrix* D, const bem_m
   const int kmax = opts->max_iter;
   cudaStream_t st = S(stream);
   double *Q = nullptr, *tmp = nullptr, *u = nullptr, *v = nullptr, *dh = nullptr, *wk = nullptr;
+  double* CQ = nullptr;    // C V q_k as the products leave them (true residual without products)
   double* hpin = nullptr;  // pinned host copy of the Hessenberg column (persistent, grow-only)
   cudaError_t e;
   // per host thread (concurrent solves on several threads, e.g. emulated ranks, each own theirs)
@@ -408,12 +411,14 @@ bem_status bem_solve_gmres(const bem_matrix* V, const bem_matrix* D, const bem_m
   // stream-ordered allocations: no device-wide synchronisation
   const size_t q_bytes = sizeof(double) * n * (kmax + 1);
   if ((e = storage_acquire(m->device, q_bytes, st, (void**)&Q)) != cudaSuccess ||
+      (!fresh_res && (e = storage_acquire(m->device, q_bytes, st, (void**)&CQ)) != cudaSuccess) ||
       (e = cudaMallocAsync(&tmp, sizeof(double) * n, st)) != cudaSuccess ||
       (e = cudaMallocAsync(&u, sizeof(double) * n, st)) != cudaSuccess ||
       (e = cudaMallocAsync(&v, sizeof(double) * n, st)) != cudaSuccess ||
       (e = cudaMallocAsync(&wk, sizeof(double) * n, st)) != cudaSuccess ||
       (e = cudaMallocAsync(&dh, sizeof(double) * 2 * (kmax + 2), st)) != cudaSuccess) {
     storage_release(m->device, Q, q_bytes, st); cudaFreeAsync(tmp, st); cudaFreeAsync(u, st); cudaFreeAsync(v, st);
+    if (CQ) storage_release(m->device, CQ, q_bytes, st);
     cudaFreeAsync(wk, st); cudaFreeAsync(dh, st);
     cudaGetLastError();
     set_error("bem_solve_gmres: allocation failed");
@@ -477,8 +482,10 @@ bem_status bem_solve_gmres(const bem_matrix* V, const bem_matrix* D, const bem_m
   auto enqueue_step = [&](int k) -> bem_status {
     double* qk = Q + (long long)k * n;
     bem_status s1 = apply_V(qk, tmp);
-    if (s1 == BEM_OK) s1 = apply_C(tmp, wk);
+    double* cq = CQ ? CQ + (long long)k * n : wk;
+    if (s1 == BEM_OK) s1 = apply_C(tmp, cq);
     if (s1 != BEM_OK) return s1;
+    if (CQ && cudaMemcpyAsync(wk, cq, sizeof(double) * n, cudaMemcpyDeviceToDevice, st) != cudaSuccess) return BEM_E_CUDA;
     vec_dots(Q, n, k + 1, wk, n, dh, st);
     vec_update(wk, Q, n, k + 1, dh, n, st);
     vec_dots(Q, n, k + 1, wk, n, dh + (k + 1), st);
@@ -564,8 +571,19 @@ bem_status bem_solve_gmres(const bem_matrix* V, const bem_matrix* D, const bem_m
     }
   }
   double true_res = resid;
-  if (status == BEM_OK && beta > 0.0) {
-    // true preconditioned residual ||C(b - V w)|| / ||C b||
+  if (status == BEM_OK && beta > 0.0 && !fresh_res) {
+    // true preconditioned residual ||C(b - V w)|| / ||C b|| from the kept products:
+    // C b - C V w = beta q_0 - sum_i y_i (C V q_i)  (y still in dh; no Hessenberg data involved)
+    if (iters > 0) {
+      vec_combine(wk, CQ, n, iters, dh, n, st);
+      vec_axpby(wk, beta, Q, -1.0, n, st);
+    } else {
+      vec_axpby(wk, beta, Q, 0.0, n, st);
+    }
+    const double nr = norm(wk);
+    if (status == BEM_OK) true_res = nr / beta;
+  } else if (status == BEM_OK && beta > 0.0) {
+    // true preconditioned residual ||C(b - V w)|| / ||C b|| from fresh products
     status = apply_V(w, tmp);
     if (status == BEM_OK) {
       vec_axpby(tmp, 1.0, b, -1.0, n, st);
@@ -588,6 +606,7 @@ bem_status bem_solve_gmres(const bem_matrix* V, const bem_matrix* D, const bem_m
   for (auto x : mvev) cudaEventDestroy(x);
   e = cudaGetLastError();
   storage_release(m->device, Q, q_bytes, st); cudaFreeAsync(tmp, st); cudaFreeAsync(u, st); cudaFreeAsync(v, st);
+  if (CQ) storage_release(m->device, CQ, q_bytes, st);
   cudaFreeAsync(wk, st); cudaFreeAsync(dh, st);
   cudaStreamSynchronize(st);
   comm_timer_set(nullptr);

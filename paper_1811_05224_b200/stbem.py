@@ -50,7 +50,8 @@ def quad_opts(q_bulk=0, q_sing=0, flags=0, q_near=0, near_gap=0):
 
 
 class GmresOpts(ctypes.Structure):
-    _fields_ = [("rel_tol", ctypes.c_double), ("max_iter", ctypes.c_int), ("precond", ctypes.c_int)]
+    _fields_ = [("rel_tol", ctypes.c_double), ("max_iter", ctypes.c_int), ("precond", ctypes.c_int),
+                ("flags", ctypes.c_int)]
 
 
 class SolveReport(ctypes.Structure):
@@ -415,8 +416,12 @@ def eval_potential_initial(mesh, nodes, tris, u0, pts, out, stream=None):
     return out
 
 
-def solve_gmres(V, b, w, D=None, M=None, rel_tol=1e-10, max_iter=500, precond=0, history=True, stream=None):
-    o = GmresOpts(float(rel_tol), int(max_iter), int(precond))
+GMRES_FRESH_RESIDUAL = 1  # bem_gmres_opts.flags: true residual from fresh products
+
+
+def solve_gmres(V, b, w, D=None, M=None, rel_tol=1e-10, max_iter=500, precond=0, history=True, stream=None,
+                fresh_residual=False):
+    o = GmresOpts(float(rel_tol), int(max_iter), int(precond), GMRES_FRESH_RESIDUAL if fresh_residual else 0)
     rep = SolveReport()
     hist = np.zeros(max_iter + 1) if history else None
     st = lib().bem_solve_gmres(V.h, D.h if D else None, M.h if M else None, _ptr(b), _ptr(w),

@@ -219,6 +219,31 @@ def solve(name, precond, tol):
     return wv.cpu().numpy(), rep
 
 
+@pytest.mark.parametrize("name,precond", [("C1", 0), ("C1", 2), ("C2", 1), ("C2", 2)])
+def test_true_residual_from_kept_products(name, precond):
+    """the default true residual ||C(b - V w)|| / ||C b|| = ||beta q_0 - sum_i y_i C V q_i|| / beta
+    from the products of the Arnoldi steps (by linearity) against fresh products C V w
+    (BEM_GMRES_FRESH_RESIDUAL): the same solution, the same residual up to the rounding of the
+    products, and one V_h and one D_h product fewer"""
+    w, m, A = gpu_mats(name)
+    g = cuda(W.dirichlet_data(w))
+    b = torch.empty_like(g)
+    S.rhs(A["K"], m.assemble_M(S.MASS_PRIMAL), g, b)
+    M = m.assemble_M(S.MASS_DUAL_LUMPED if precond == 1 else S.MASS_DUAL) if precond else None
+    out = []
+    for fresh in (False, True):
+        wv = torch.zeros_like(g)
+        rep = S.solve_gmres(A["V"], b, wv, D=A["D"] if precond else None, M=M, rel_tol=1e-10, max_iter=300,
+                            precond=precond, fresh_residual=fresh)
+        out.append((wv.cpu().numpy(), rep))
+    (w0, r0), (w1, r1) = out
+    assert np.array_equal(w0, w1) and r0["iterations"] == r1["iterations"]
+    assert abs(r0["true_rel_residual"] - r1["true_rel_residual"]) <= 1e-13 + 1e-3 * r1["true_rel_residual"], (r0, r1)
+    assert r0["true_rel_residual"] <= 2e-10
+    assert r1["n_matvec_V"] == r0["n_matvec_V"] + 1
+    assert r1["n_matvec_D"] == r0["n_matvec_D"] + (1 if precond else 0)
+
+
 @pytest.mark.parametrize("precond,band", [(0, (20, 35)), (1, (14, 26)), (2, (10, 22))])
 def test_gmres_c1(precond, band):
     w = W.get("C1")

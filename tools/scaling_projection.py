@@ -5,7 +5,7 @@ through a solo communicator (bem_comm_create_solo: the owned blocks only, partia
 V_h, D_h and K_h g assembly and its V_h, D_h products are timed with CUDA events.  The projected
 step of G GPUs is
     max_r (assembly_r + n_V gemv_V,r + n_D gemv_D,r)  +  n_coll x t_allreduce  +  replicated vector work
-with the products per solve of the measured single-GPU solve (n_V = it + 1, n_D = it + 2), one
+with the products per solve of the measured single-GPU solve (n_matvec_V, n_matvec_D of its report), one
 all-reduce of N doubles per product (t_allreduce ASSUMED, see --allreduce-us: NVLink all-reduce of
 0.5-0.8 MB, latency-bound) and the replicated Krylov work taken from the single-GPU solve.  A solo
 rank computes every pair record itself; with a real communicator the records of V_h and D_h are
@@ -89,6 +89,7 @@ def main():
     S.solve_gmres(V, b, wv, D=D, M=Md, precond=2, rel_tol=w.tol, history=False)   # warm
     rep = S.solve_gmres(V, b, wv, D=D, M=Md, precond=2, rel_tol=w.tol, history=False)
     it = rep["iterations"]
+    n_v, n_d = rep["n_matvec_V"], rep["n_matvec_D"]
     replicated = rep["seconds_total"] - rep["seconds_matvec"]
     for A in (V, D, Mp, Md):
         A.close()
@@ -105,8 +106,8 @@ def main():
         for rk in ranks:
             rk["records_distributed_s"] = rk["records_VD_s"] / G + gather
         per = [rk["assembly_s"] - rk["records_VD_s"] + rk["records_distributed_s"]
-               + (it + 1) * rk["gemv_V_s"] + (it + 2) * rk["gemv_D_s"] for rk in ranks]
-        n_coll = (2 * it + 4) if G > 1 else 0   # one per product + the fused right-hand side
+               + n_v * rk["gemv_V_s"] + n_d * rk["gemv_D_s"] for rk in ranks]
+        n_coll = (n_v + n_d + 1) if G > 1 else 0   # one per product + the fused right-hand side
         step = max(per) + replicated + n_coll * args.allreduce_us * 1e-6
         base = base or step
         res["projection"][G] = {"step_s": step, "speedup": base / step, "max_rank_s": max(per),
