@@ -1006,8 +1006,11 @@ __host__ __device__ constexpr int bulk_nch() { return Fams<KIND>::n == 2 ? 3 : 2
 // once per Horner step for all R + 1 chains) instead of registers: no spills at 152 registers, C5
 // 9.53 -> 9.25 ms; K_h g measured the same (15.19 / 15.24 ms), and at four CTAs per SM (128
 // registers, 8 staged regime-B orders) both were slower (V 9.41, K g 16.06 ms)
+#ifndef STB_BULK_SMP_D
+#define STB_BULK_SMP_D 0
+#endif
 template <int KIND>
-__host__ __device__ constexpr bool bulk_smp() { return STB_BULK_SMP && KIND == STB_V; }
+__host__ __device__ constexpr bool bulk_smp() { return (STB_BULK_SMP && KIND == STB_V) || (STB_BULK_SMP_D && KIND == STB_D); }
 // dynamic shared memory of k_bulk_m: staged regime-B coefficients + two lag chunks (+ SMP chains)
 template <int KIND, int R>
 __host__ __device__ constexpr size_t bulk_smem_bytes() {
