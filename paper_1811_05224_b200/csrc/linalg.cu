@@ -829,7 +829,7 @@ __global__ void k_mass_fill(int kind, const Seg* __restrict__ seg, const Dual* _
 }
 
 __global__ void k_cyclic_factor(const double* __restrict__ lo, const double* __restrict__ di,
-                                const double* __restrict__ up, int ng, int nt, double* __restrict__ fac);
+                                const double* __restrict__ up, int ng, int nt, int staged, double* __restrict__ fac);
 
 bem_status mass_setup(bem_matrix* M, int kind) {
   const bem_mesh* m = M->mesh;
@@ -846,7 +846,17 @@ bem_status mass_setup(bem_matrix* M, int kind) {
   k_mass_fill<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(kind, m->d_seg, m->d_dual, m->d_t, m->ng, m->nt, M->d_lo, M->d_di, M->d_up);
   count_launch();
   if (kind == BEM_MASS_DUAL) {   // factorisation for both transpose flags, once per matrix
-    k_cyclic_factor<<<(2 * m->nt + 63) / 64, 64, 0, st>>>(M->d_lo, M->d_di, M->d_up, m->ng, m->nt, M->d_work);
+    static int fmax_smem = -1;
+    if (fmax_smem < 0) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      if (cudaDeviceGetAttribute(&fmax_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) fmax_smem = 48 * 1024;
+      cudaFuncSetAttribute(k_cyclic_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, fmax_smem);
+    }
+    const size_t fsmem = sizeof(double) * 7 * (size_t)m->ng;
+    const int fstaged = fsmem <= (size_t)fmax_smem;
+    k_cyclic_factor<<<2 * m->nt, 32, fstaged ? fsmem : 0, st>>>(M->d_lo, M->d_di, M->d_up, m->ng, m->nt, fstaged,
+                                                                M->d_work);
     count_launch();
   }
   e = cudaGetLastError();
@@ -880,44 +890,67 @@ bem_status mass_apply(const bem_matrix* M, double a, const double* x, double b, 
 // factorisation does not depend on the right-hand side, so it is computed once per matrix and
 // transpose flag (k_cyclic_factor: Thomas on the first / last diagonal modified system plus the
 // Sherman-Morrison vector z), and a solve is a forward / backward substitution with precomputed
-// multipliers: one warp per time step stages x and the factors in shared memory (coalesced),
-// lane 0 runs the two FMA recurrences, the warp writes y = yy - fact z.
-// factor layout per (transpose t, step a): [sl, inv, cp, zz] x ng, then 2 scalars (alpha/gam, den)
-__global__ void k_cyclic_factor(const double* __restrict__ lo, const double* __restrict__ di,
-                                const double* __restrict__ up, int ng, int nt, double* __restrict__ fac) {
-  const int id = blockIdx.x * blockDim.x + threadIdx.x;
-  if (id >= 2 * nt) return;
+// multipliers: one warp per time step stages x and the factors in shared memory (coalesced) and
+// scales x by the pivots' inverses; the two recurrences -- one FMA per element each,
+// v_l = x_l inv_l - (sl_l inv_l) v_{l-1} and v_l = yy_l - cp_l v_{l+1} -- run as warp scans of
+// affine maps (below); the warp writes y = yy - fact z.
+// factor layout per (transpose t, step a): [sl inv, inv, cp, zz] x ng, then 2 scalars (alpha/gam, den)
+// one warp per (transpose, step): the three diagonals staged in shared memory with coalesced
+// loads, lane 0 runs the recurrences out of shared memory (a thread per step reading global
+// memory waited on an L2 round trip per element: C5 0.36 ms per factorisation), the warp writes
+// the factors; staged = 0 (N_Gamma beyond the shared-memory limit): the same from global memory
+__global__ void __launch_bounds__(32) k_cyclic_factor(const double* __restrict__ lo, const double* __restrict__ di,
+                                                     const double* __restrict__ up, int ng, int nt, int staged,
+                                                     double* __restrict__ fac) {
+  extern __shared__ double fsm[];   // lo, di, up, sl, inv, cp, zz (7 ng) when staged
+  const int id = blockIdx.x, lane = threadIdx.x;
   const int transpose = id / nt, a = id % nt;
   const long long base = (long long)a * ng;
-  auto sub = [&](int l) -> double { return transpose ? up[base + (l - 1 + ng) % ng] : lo[base + l]; };
-  auto sup = [&](int l) -> double { return transpose ? lo[base + (l + 1) % ng] : up[base + l]; };
-  auto dia = [&](int l) -> double { return di[base + l]; };
   double* F = fac + (long long)id * (4LL * ng + 2);
-  double* sl = F;
-  double* inv = F + ng;
-  double* cp = F + 2 * ng;
-  double* zz = F + 3 * ng;
-  const double alpha_c = sub(0);      // row 0, column ng-1
-  const double beta_c = sup(ng - 1);  // row ng-1, column 0
-  const double gam = -dia(0);
-  double den = dia(0) - gam;
-  sl[0] = 0.0;
-  inv[0] = 1.0 / den;
-  cp[0] = sup(0) * inv[0];
-  zz[0] = gam * inv[0];
-  for (int l = 1; l < ng; ++l) {
-    double bl = dia(l);
-    if (l == ng - 1) bl -= alpha_c * beta_c / gam;
-    sl[l] = sub(l);
-    den = bl - sl[l] * cp[l - 1];
-    inv[l] = 1.0 / den;
-    cp[l] = (l < ng - 1) ? sup(l) * inv[l] : 0.0;
-    const double ul = (l == ng - 1) ? beta_c : 0.0;
-    zz[l] = (ul - sl[l] * zz[l - 1]) * inv[l];
+  const double* Lo = staged ? fsm : lo + base;
+  const double* Di = staged ? fsm + ng : di + base;
+  const double* Up = staged ? fsm + 2 * ng : up + base;
+  double* sl = staged ? fsm + 3 * ng : F;
+  double* inv = staged ? fsm + 4 * ng : F + ng;
+  double* cp = staged ? fsm + 5 * ng : F + 2 * ng;
+  double* zz = staged ? fsm + 6 * ng : F + 3 * ng;
+  if (staged) {
+    for (int l = lane; l < ng; l += 32) {
+      fsm[l] = lo[base + l];
+      fsm[ng + l] = di[base + l];
+      fsm[2 * ng + l] = up[base + l];
+    }
   }
-  for (int l = ng - 2; l >= 0; --l) zz[l] -= cp[l] * zz[l + 1];
-  F[4 * ng] = alpha_c / gam;
-  F[4 * ng + 1] = 1.0 + zz[0] + (alpha_c / gam) * zz[ng - 1];
+  __syncwarp();
+  if (lane == 0) {
+    auto sub = [&](int l) -> double { return transpose ? Up[(l - 1 + ng) % ng] : Lo[l]; };
+    auto sup = [&](int l) -> double { return transpose ? Lo[(l + 1) % ng] : Up[l]; };
+    const double alpha_c = sub(0);      // row 0, column ng-1
+    const double beta_c = sup(ng - 1);  // row ng-1, column 0
+    const double gam = -Di[0];
+    double den = Di[0] - gam;
+    sl[0] = 0.0;
+    inv[0] = 1.0 / den;
+    cp[0] = sup(0) * inv[0];
+    zz[0] = gam * inv[0];
+    for (int l = 1; l < ng; ++l) {
+      double bl = Di[l];
+      if (l == ng - 1) bl -= alpha_c * beta_c / gam;
+      const double sv = sub(l);
+      den = bl - sv * cp[l - 1];
+      inv[l] = 1.0 / den;
+      sl[l] = sv * inv[l];
+      cp[l] = (l < ng - 1) ? sup(l) * inv[l] : 0.0;
+      const double ul = (l == ng - 1) ? beta_c : 0.0;
+      zz[l] = (ul - sv * zz[l - 1]) * inv[l];
+    }
+    for (int l = ng - 2; l >= 0; --l) zz[l] -= cp[l] * zz[l + 1];
+    F[4 * ng] = alpha_c / gam;
+    F[4 * ng + 1] = 1.0 + zz[0] + (alpha_c / gam) * zz[ng - 1];
+  }
+  __syncwarp();
+  if (staged)
+    for (int l = lane; l < 4 * ng; l += 32) F[l] = fsm[3 * ng + l];
 }
 
 // staged: x and the factors in shared memory (4 ng doubles); otherwise (N_Gamma beyond the
@@ -935,27 +968,51 @@ __global__ void __launch_bounds__(32) k_cyclic_solve(const double* __restrict__ 
   const double* cp = staged ? sm + 3 * ng : F + 2 * ng;
   if (staged) {
     for (int l = lane; l < ng; l += 32) {
-      yy[l] = x[base + l];
+      yy[l] = x[base + l] * F[ng + l];
       sm[ng + l] = F[l];
-      sm[2 * ng + l] = F[ng + l];
       sm[3 * ng + l] = F[2 * ng + l];
     }
-  } else if (x != y) {
-    for (int l = lane; l < ng; l += 32) yy[l] = x[base + l];
+  } else {
+    for (int l = lane; l < ng; l += 32) yy[l] = x[base + l] * inv[l];
   }
   __syncwarp();
-  if (lane == 0) {
-    double v = yy[0] * inv[0];
-    yy[0] = v;
-    for (int l = 1; l < ng; ++l) {
-      v = (yy[l] - sl[l] * v) * inv[l];
+  // the two first-order recurrences v_l = yy_l - c_l v_(l-1/l+1) as warp scans of affine maps:
+  // lane j composes the maps of its chunk (v -> A v + B), an exclusive shuffle scan composes the
+  // chunks before it, and the lane runs its chunk from the incoming value (the dependent chain is
+  // 2 x chunk + 5 steps instead of ng: FP64 FMA latency bound, C5 32 -> 16 us per solve)
+  const int nfw = ng - 1, chk = (nfw + 31) / 32;
+  auto sweep = [&](const double* coef, int dir) {
+    // element k of the sweep (k = 0 .. ng - 2): index 1 + k forward, ng - 2 - k backward
+    const int k0 = min(nfw, lane * chk), k1 = min(nfw, k0 + chk);
+    double A = 1.0, Bv = 0.0;
+    for (int k = k0; k < k1; ++k) {
+      const int l = dir > 0 ? 1 + k : ng - 2 - k;
+      A = -coef[l] * A;
+      Bv = fma(-coef[l], Bv, yy[l]);
+    }
+    // exclusive scan: compose the maps of lanes < lane (in order), identity for lane 0
+    double eA = __shfl_up_sync(0xffffffffu, A, 1), eB = __shfl_up_sync(0xffffffffu, Bv, 1);
+    if (lane == 0) { eA = 1.0; eB = 0.0; }
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const double pA = __shfl_up_sync(0xffffffffu, eA, d), pB = __shfl_up_sync(0xffffffffu, eB, d);
+      if (lane >= d) {   // (this prefix) after (the earlier prefix): v -> eA (pA v + pB) + eB
+        eB = fma(eA, pB, eB);
+        eA = eA * pA;
+      }
+    }
+    const double v0 = dir > 0 ? yy[0] : yy[ng - 1];
+    double v = fma(eA, v0, eB);
+    __syncwarp();
+    for (int k = k0; k < k1; ++k) {
+      const int l = dir > 0 ? 1 + k : ng - 2 - k;
+      v = fma(-coef[l], v, yy[l]);
       yy[l] = v;
     }
-    for (int l = ng - 2; l >= 0; --l) {
-      v = yy[l] - cp[l] * v;
-      yy[l] = v;
-    }
-  }
+    __syncwarp();
+  };
+  sweep(sl, 1);
+  sweep(cp, -1);
   __syncwarp();
   const double fact = (yy[0] + F[4 * ng] * yy[ng - 1]) / F[4 * ng + 1];
   __syncwarp();
