@@ -1027,6 +1027,9 @@ __device__ __forceinline__ void cp_async16_bulk(void* smem, const void* gmem) {
 // MULTI: the blocks of the list L (a rank's owned blocks); otherwise the one block of B (kernel
 // parameters: the loop and the list reads compile away -- the list form costs one GPU's single
 // block ~7% in spills, C5 V 9.7 vs 10.4 ms)
+#ifndef STB_BULK_LEAD
+#define STB_BULK_LEAD 1     // per-chunk regime-A prefix instead of a per-column vote
+#endif
 #ifndef STB_BULK_MINB_V
 #define STB_BULK_MINB_V 3   // CTAs per SM the V_h bulk kernel is register-budgeted for
 #endif
@@ -1170,12 +1173,23 @@ __global__ void __launch_bounds__(128, KIND == STB_D ? STB_BULK_MINB_D : (KIND =
   for (int r = 0; r < (PROD ? 1 : R); ++r) Gp[r] = 0.0;
   double gprev = 0.0;        // product mode: g of the previous trial step (0 before b0)
   bool gp_ok = ystart == Bk.b0;   // gprev holds it (else loaded when the next column is used)
+  int ylead = ystart;        // columns y < ylead: regime A at the smallest-lag node for the whole warp
   for (int y = ystart; y <= bmax + 1; ++y) {
     const int kc = y - Bk.b0;
     if (kc % LAG_CH == 0) {                          // CTA-uniform: chunk kc / LAG_CH is needed
       asm volatile("cp.async.wait_group 0;" ::: "memory");
       __syncthreads();                               // visible to all; the other buffer is free
       if (kc + LAG_CH < ncols) stage(kc / LAG_CH + 1);
+      if (STB_BULK_LEAD) {
+        // the chunk's leading columns whose smallest-lag node (x = r_lo) is in regime A for every
+        // lane of the warp (u grows with y, so a prefix): one batch of independent shared loads per
+        // chunk instead of a load -> compare -> vote chain per column
+        const double4* c0p = s_lag + ((kc / LAG_CH) & 1) * (LAG_CH * (R + 1));
+        unsigned m = 0;
+#pragma unroll
+        for (int k = 0; k < LAG_CH; ++k) m |= (unsigned)(A.cmax * c0p[k * (R + 1)].z < STB_MXB) << k;
+        ylead = y + __reduce_min_sync(0xffffffffu, (unsigned)(__ffs(~m) - 1));
+      }
     }
     const double4* ndc = s_lag + ((kc / LAG_CH) & 1) * (LAG_CH * (R + 1)) + (kc % LAG_CH) * (R + 1);
     // every node of the column by the regime-A form, branch-free (clamped into the lag table,
@@ -1213,7 +1227,7 @@ __global__ void __launch_bounds__(128, KIND == STB_D ? STB_BULK_MINB_D : (KIND =
         phi[r] = 0.0;
         nA += r_lo + r <= r_hi && r_lo + r > y;
       }
-    } else if (full && __all_sync(0xffffffffu, A.cmax * ndd[2] < STB_MXB)) {
+    } else if (full && (STB_BULK_LEAD ? y < ylead : __all_sync(0xffffffffu, A.cmax * ndd[2] < STB_MXB))) {
 #pragma unroll
       for (int r = 0; r <= R; ++r) phi[r] = SMP ? chain_s<KIND>(sPt, ndd[4 * r + 2]) : A.chain(ndd[4 * r + 2]);
 #pragma unroll
