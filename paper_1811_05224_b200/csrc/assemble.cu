@@ -295,6 +295,9 @@ __global__ void __launch_bounds__(128) k_sing(BlockArgs B, const Seg* __restrict
 }
 
 // ================================================================= launch
+#ifndef STB_NEAR_CHUNK
+#define STB_NEAR_CHUNK 32   // test steps per k_near_m CTA (the per-pair setup is paid once per chunk)
+#endif
 static int max_smem_optin() {
   static int v = 0;
   if (!v) {
@@ -712,7 +715,7 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, const Qua
     BA.ell = MB.ell;
     const bool has_near = blk.b1 - 1 >= blk.a0 - 1 && blk.b0 <= blk.a1 - 1;
     if (has_near) {
-      const int chunk = 16;
+      const int chunk = STB_NEAR_CHUNK;
       const int nz = (blk.a1 - blk.a0 + chunk - 1) / chunk;
       if (prod) launch_kind<STB_K, true>(1, BA, MN, ng, chunk, nz, st);
       else if (kind == STB_V) launch_kind<STB_V>(1, BA, MN, ng, chunk, nz, st);

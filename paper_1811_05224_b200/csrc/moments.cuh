@@ -845,13 +845,13 @@ __device__ __forceinline__ double phi_b2(const double* __restrict__ rec, long lo
 // two nodes of the same pair at once (the bulk columns usually hold several regime-B nodes per
 // lane): the two Taylor recurrences interleave (ILP 2 on a latency-bound chain) and share the
 // moment loads.  reg1 / reg2 as in phi_bz.
-template <int KIND>
+template <int KIND, bool TRUEV = false>
 __device__ __forceinline__ void phi_bz2(const double* __restrict__ rec, long long S, const RegBZ<KIND>& z,
                                         double s1, double u1, double s2, double u2, double& v1,
                                         double& v2, int* reg1, int* reg2, const double* sm = nullptr, int ns = 0) {
   if (!(z.c0 > 0.0)) {   // no cluster: Z or C per node
-    v1 = phi_bz<KIND>(rec, S, z, s1, u1, reg1);
-    v2 = phi_bz<KIND>(rec, S, z, s2, u2, reg2);
+    v1 = phi_bz<KIND, TRUEV>(rec, S, z, s1, u1, reg1);
+    v2 = phi_bz<KIND, TRUEV>(rec, S, z, s2, u2, reg2);
     return;
   }
   const bool zz1 = z.cmin > 0.0 && z.cmin * u1 >= MXZ, zz2 = z.cmin > 0.0 && z.cmin * u2 >= MXZ;
@@ -886,7 +886,10 @@ __device__ __forceinline__ void phi_bz2(const double* __restrict__ rec, long lon
   for (int f = 0; f < Fams<KIND>::n; ++f) {
     const int fam = f == 0 ? Fams<KIND>::f0 : Fams<KIND>::f1;
     const double t1 = zz1 ? 0.0 : T1[f], t2 = zz2 ? 0.0 : T2[f];
-    if (fam == FAM_H) {
+    if (TRUEV) {   // the true node value (near cells): no affine terms
+      v1 += fam == FAM_H ? s1 * t1 : t1;
+      v2 += fam == FAM_H ? s2 * t2 : t2;
+    } else if (fam == FAM_H) {
       v1 += fma(s1, t1 + z.C0[f], z.C1[f]);
       v2 += fma(s2, t2 + z.C0[f], z.C1[f]);
     } else if (fam == FAM_F) {
@@ -1029,6 +1032,9 @@ __device__ __forceinline__ void cp_async16_bulk(void* smem, const void* gmem) {
 // block ~7% in spills, C5 V 9.7 vs 10.4 ms)
 #ifndef STB_BULK_LEAD
 #define STB_BULK_LEAD 1     // per-chunk regime-A prefix instead of a per-column vote
+#endif
+#ifndef STB_NEAR_TWO
+#define STB_NEAR_TWO 1      // k_near_m: the two nodes of a test step evaluated together
 #endif
 #ifndef STB_BULK_MINB_V
 #define STB_BULK_MINB_V 3   // CTAs per SM the V_h bulk kernel is register-budgeted for
@@ -1603,27 +1609,29 @@ __global__ void __launch_bounds__(128) k_near_m(BlockArgs B, MomArgs M, int chun
     }
   }
   unsigned long long nA = 0, nB = 0, nZ = 0, nC = 0, nK = 0;
-  // node value for every lane (warp-uniform call: regime C is computed cooperatively)
-  auto node = [&](int x, int y) -> double {
-    const double4 nd = B.lag[x * B.ldlag + y];
-    double v = 0.0;
-    bool needC = false, inA = false;
-    if (A.cmax * nd.z < STB_MXB) {
-      v = A.eval(nd.x, nd.y, nd.z);
-      inA = true;
+  // node value without regime C (per lane): inA -> the regularised regime-A value, else the true
+  // value of regimes B / B2 / Z; needC -> regime C, left to the warp-cooperative pass
+  auto node_nc = [&](const double4& nd, bool& inA, bool& needC) -> double {
+    needC = false;
+    inA = A.cmax * nd.z < STB_MXB;
+    if (inA) {
       ++nA;
-    } else {
-      int reg = 0;
-      v = Z2.kb > 0 ? phi_b2<KIND>(rec, S, Z, Z2, nd.x, nd.z, &reg, STAGE ? sbz : nullptr, STAGE ? nsb : 0)
-                    : phi_bz<KIND, true>(rec, S, Z, nd.x, nd.z, &reg, STAGE ? sbz : nullptr, STAGE ? nsb : 0);
-      nB += reg == 1;
-        nK += reg == 1 ? Z.kb + Z2.kb : 0;
-      nZ += reg == 2;
-      if (reg == 3) {
-        needC = true;
-        ++nC;
-      }
+      return A.eval(nd.x, nd.y, nd.z);
     }
+    int reg = 0;
+    const double v = Z2.kb > 0 ? phi_b2<KIND>(rec, S, Z, Z2, nd.x, nd.z, &reg, STAGE ? sbz : nullptr, STAGE ? nsb : 0)
+                               : phi_bz<KIND, true>(rec, S, Z, nd.x, nd.z, &reg, STAGE ? sbz : nullptr, STAGE ? nsb : 0);
+    nB += reg == 1;
+    nK += reg == 1 ? Z.kb + Z2.kb : 0;
+    nZ += reg == 2;
+    if (reg == 3) {
+      needC = true;
+      ++nC;
+    }
+    return v;
+  };
+  // regime C of the lanes that need it at node nd (warp-uniform call)
+  auto pass_c = [&](const double4& nd, bool needC, double& v) {
     unsigned lanes = __ballot_sync(0xffffffffu, needC);
     while (lanes) {
       const int src = __ffs(lanes) - 1;
@@ -1632,21 +1640,64 @@ __global__ void __launch_bounds__(128) k_near_m(BlockArgs B, MomArgs M, int chun
       const double c = phi_c_warp<KIND, true>(M, Is, Js, nd.x, nd.y, nd.z);
       if (lane == src) v = c;
     }
+  };
+  // node value for every lane (warp-uniform call: regime C is computed cooperatively)
+  auto node = [&](int x, int y) -> double {
+    const double4 nd = B.lag[x * B.ldlag + y];
+    bool inA, needC;
+    double v = node_nc(nd, inA, needC);
+    pass_c(nd, needC, v);
     // regime A gives the regularised value; B, Z and C return the true value directly
     return inA ? v - affine_part<KIND>(rec, S, nd.x) : v;
+  };
+  // two nodes of the same pair at once (Phi(a+1, a) and Phi(a+1, a-1)), warp-uniform call: both
+  // regime-A chains in one block, or both single-cluster regime-B Taylor sums interleaved by
+  // phi_bz2 (ILP 2, shared coefficient loads); per lane, the C pass after it for the whole warp
+  auto node2 = [&](int x1, int y1, int x2, int y2, double& o1, double& o2) {
+    if (!STB_NEAR_TWO) {
+      o1 = node(x1, y1);
+      o2 = node(x2, y2);
+      return;
+    }
+    const double4 n1 = B.lag[x1 * B.ldlag + y1], n2 = B.lag[x2 * B.ldlag + y2];
+    const bool a1 = A.cmax * n1.z < STB_MXB, a2 = A.cmax * n2.z < STB_MXB;
+    double v1 = 0.0, v2 = 0.0;
+    bool i1 = a1, i2 = a2, c1 = false, c2 = false;
+    if (a1 && a2) {
+      v1 = A.eval(n1.x, n1.y, n1.z);
+      v2 = A.eval(n2.x, n2.y, n2.z);
+      nA += 2;
+    } else if (!a1 && !a2 && Z2.kb == 0) {
+      int r1 = 0, r2 = 0;
+      phi_bz2<KIND, true>(rec, S, Z, n1.x, n1.z, n2.x, n2.z, v1, v2, &r1, &r2, STAGE ? sbz : nullptr,
+                          STAGE ? nsb : 0);
+      nB += (r1 == 1) + (r2 == 1);
+      nK += (r1 == 1 ? Z.kb : 0) + (r2 == 1 ? Z.kb : 0);
+      nZ += (r1 == 2) + (r2 == 2);
+      c1 = r1 == 3;
+      c2 = r2 == 3;
+      nC += c1 + c2;
+    } else {
+      v1 = node_nc(n1, i1, c1);
+      v2 = node_nc(n2, i2, c2);
+    }
+    pass_c(n1, c1, v1);
+    pass_c(n2, c2, v2);
+    o1 = i1 ? v1 - affine_part<KIND>(rec, S, n1.x) : v1;
+    o2 = i2 ? v2 - affine_part<KIND>(rec, S, n2.x) : v2;
   };
   double prev = 0.0;  // Phi(a, a-1)
   if (a_beg < a_end && a_beg >= 1 && a_beg - 1 >= B.b0 && a_beg - 1 < B.b1) prev = node(a_beg, a_beg - 1);
 #pragma unroll 1
   for (int a = a_beg; a < a_end; ++a) {
     const bool d0 = a >= B.b0 && a < B.b1, d1 = a - 1 >= B.b0 && a - 1 < B.b1;
-    double p10 = 0.0;
-    if (d0 || d1) p10 = node(a + 1, a);
+    double p10 = 0.0, p20 = 0.0;
+    if (d1) node2(a + 1, a, a + 1, a - 1, p10, p20);   // CTA-uniform conditions
+    else if (d0) p10 = node(a + 1, a);
     if (PROD) {
       double c = 0.0;
       if (d0 && valid) c = p10 * B.g[(long long)a * ng + J];
       if (d1) {
-        const double p20 = node(a + 1, a - 1);
         if (valid) c = fma(p20 - prev - p10, B.g[(long long)(a - 1) * ng + J], c);
       }
       c = warp_sum(c);
@@ -1655,10 +1706,7 @@ __global__ void __launch_bounds__(128) k_near_m(BlockArgs B, MomArgs M, int chun
     } else {
       const bool vst = valid && (!B.sym || sym_stored(I, J));
       if (d0 && vst) *entry_ptr(B, a, I, a, J) = p10;
-      if (d1) {
-        const double p20 = node(a + 1, a - 1);
-        if (vst) *entry_ptr(B, a, I, a - 1, J) = p20 - prev - p10;
-      }
+      if (d1 && vst) *entry_ptr(B, a, I, a - 1, J) = p20 - prev - p10;
     }
     prev = p10;
   }
