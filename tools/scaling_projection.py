@@ -11,8 +11,9 @@ all-reduce of N doubles per product (t_allreduce ASSUMED, see --allreduce-us: NV
 rank computes every pair record itself; with a real communicator the records of V_h and D_h are
 split into G chunks and all-gathered (assemble.cu), which the projection models as
     records_r -> records_r / G + (G - 1) / G x record_bytes / --allgather-gbs
-(record bytes from the field counts; the K_h g records are left replicated: conservative).  The
-all-gathers run on the V_h / D_h assembly streams while the other assemblies compute (bench.py's
+(record bytes from the field counts; V_h, D_h and K_h g alike, as `launch_assembly` splits every
+kind's records over a real communicator).  The all-gathers run on each matrix's own assembly stream
+while the other assemblies compute (bench.py's
 step puts V_h, D_h and K_h g on three streams), so the default model takes a rank's assembly as
     max(sum of its kernel times,  the longest stream: records / G + all-gather + that matrix's kernels)
 and `step_serial_s` keeps the pessimistic sum with the all-gathers serialised.  It shows the load
@@ -35,7 +36,7 @@ from paper_1811_05224_b200 import stbem as S  # noqa: E402
 
 # doubles per pair record, bulk + near fields (moments.cuh rec_fields + rec_fields_near)
 # nf + nfn: rec_fields = RF_COMMON + n_fam FAMSZ, rec_fields_near = rec_fields + R2_FAM + n_fam R2_FAMSZ
-REC_FIELDS = {"V": 144 + 262, "D": 283 + 515}
+REC_FIELDS = {"V": 144 + 262, "D": 283 + 515, "K": 144 + 262}
 
 
 def timed(fn):
@@ -56,7 +57,7 @@ def rank_work(w, G, r, pfac=2):
     b = torch.empty_like(g)
     tV, V = timed(lambda: m.assemble_V())
     tD, D = timed(lambda: m.assemble_D())
-    tK, _ = timed(lambda: S.rhs_fused(m, Mp, g, b))
+    tK, stK = timed(lambda: S.rhs_fused(m, Mp, g, b, stats=True))
     x = torch.tensor(W.random_vector(w.n), dtype=torch.float64, device="cuda")
     y = torch.empty_like(x)
     gv, gd = [], []
@@ -64,9 +65,10 @@ def rank_work(w, G, r, pfac=2):
         gv.append(timed(lambda: V.matvec(x, y))[0])
         gd.append(timed(lambda: D.matvec(x, y))[0])
     stV, stD = V.stats(), D.stats()
-    rec = 1e-3 * (stV["ms_records"] + stD["ms_records"])
-    fam = {k: {f: round(st[f], 3) for f in ("ms_records", "ms_bulk", "ms_near", "ms_sing")} for k, st in (("V", stV), ("D", stD))}
-    out = {"assembly_s": tV + tD + tK, "asm": [tV, tD, tK], "records_VD_s": rec, "kernels_ms": fam, "gemv_V_s": float(np.median(gv[1:])),
+    rec = 1e-3 * (stV["ms_records"] + stD["ms_records"] + stK["ms_records"])
+    fam = {k: {f: round(st[f], 3) for f in ("ms_records", "ms_bulk", "ms_near", "ms_sing")}
+           for k, st in (("V", stV), ("D", stD), ("K", stK))}
+    out = {"assembly_s": tV + tD + tK, "asm": [tV, tD, tK], "records_s": rec, "kernels_ms": fam, "gemv_V_s": float(np.median(gv[1:])),
            "gemv_D_s": float(np.median(gd[1:])), "entries": m.info.entries_owned, "blocks": m.info.n_owned_blocks}
     V.close(); D.close(); Mp.close(); m.close()
     if c:
@@ -105,19 +107,19 @@ def main():
         rank_work(w, G, 0, args.pfac)   # warm-up: the storage of this size is mapped once (first touch)
         ranks = [rank_work(w, G, r, args.pfac) for r in range(G)]
         # distributed records: 1/G of the V_h, D_h records per rank plus their all-gather
-        rec_bytes = 8.0 * w.n_gamma ** 2 * (REC_FIELDS["V"] + REC_FIELDS["D"])
+        rec_bytes = 8.0 * w.n_gamma ** 2 * sum(REC_FIELDS.values())
         gather = (G - 1) / G * rec_bytes / (args.allgather_gbs * 1e9) if G > 1 else 0.0
-        gshare = {k: REC_FIELDS[k] / (REC_FIELDS["V"] + REC_FIELDS["D"]) for k in "VD"}
+        gshare = {k: REC_FIELDS[k] / sum(REC_FIELDS.values()) for k in "VDK"}
         per, per_serial = [], []
         for rk in ranks:
-            rk["records_distributed_s"] = rk["records_VD_s"] / G + gather
-            compute = rk["assembly_s"] - rk["records_VD_s"] + rk["records_VD_s"] / G
+            rk["records_distributed_s"] = rk["records_s"] / G + gather
+            compute = rk["assembly_s"] - rk["records_s"] + rk["records_s"] / G
             chains = [rk["asm"][i] - 1e-3 * rk["kernels_ms"][k]["ms_records"] * (1.0 - 1.0 / G) + gather * gshare[k]
-                      for i, k in ((0, "V"), (1, "D"))] + [rk["asm"][2]]
+                      for i, k in ((0, "V"), (1, "D"), (2, "K"))]
             rk["assembly_overlapped_s"] = max(compute, max(chains))
             prod = n_v * rk["gemv_V_s"] + n_d * rk["gemv_D_s"]
             per.append(rk["assembly_overlapped_s"] + prod)
-            per_serial.append(rk["assembly_s"] - rk["records_VD_s"] + rk["records_distributed_s"] + prod)
+            per_serial.append(rk["assembly_s"] - rk["records_s"] + rk["records_distributed_s"] + prod)
         n_coll = (n_v + n_d + 1) if G > 1 else 0   # one per product + the fused right-hand side
         step = max(per) + replicated + n_coll * args.allreduce_us * 1e-6
         step_serial = max(per_serial) + replicated + n_coll * args.allreduce_us * 1e-6
