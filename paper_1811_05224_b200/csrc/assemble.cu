@@ -627,6 +627,15 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, const Qua
       nzmax = std::max(nzmax, (blk.a1 - blk.a0 + Rb - 1) / Rb);
       A->nodes_expected += bulk_nodes(blk, Rb) * npairs_computed;
     }
+    // the blocks of one trial range contiguous (k_kg_tab shares a trial slice's tables between them);
+    // every kernel takes the list in any order (per-block partial slots)
+    std::stable_sort(bl.begin(), bl.end(), [](const BulkBlock& x, const BulkBlock& y) {
+      return x.b0 != y.b0 ? x.b0 < y.b0 : (x.b1 != y.b1 ? x.b1 < y.b1 : x.a0 < y.a0);
+    });
+    std::vector<int> gsv;   // group starts in bl (+ end)
+    for (size_t k = 0; k < bl.size(); ++k)
+      if (k == 0 || bl[k].b0 != bl[k - 1].b0 || bl[k].b1 != bl[k - 1].b1) gsv.push_back((int)k);
+    gsv.push_back((int)bl.size());
     if (!bl.empty()) {
       BulkBlock* d_bl = nullptr;
       if ((e = cudaMallocAsync((void**)&d_bl, sizeof(BulkBlock) * bl.size(), st)) != cudaSuccess ||
@@ -650,8 +659,12 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, const Qua
       BA.ell = MB.ell;
       // K_h g: the regime-A nodes of the interior columns as trial-moment sums (k_kg_tab) when its
       // shared-memory tables fit (N_Gamma up to ~590) and not disabled by BEM_QUAD_KG_ENTRYWISE
-      int nxmax = 0;
-      for (const BulkBlock& q : bl) nxmax = std::max(nxmax, q.a1 - q.a0 + 1);
+      int nxmax = 0;   // test nodes of the largest trial-range group
+      for (size_t gi = 0; gi + 1 < gsv.size(); ++gi) {
+        int nx = 0;
+        for (int k = gsv[gi]; k < gsv[gi + 1]; ++k) nx += bl[k].a1 - bl[k].a0 + 1;
+        nxmax = std::max(nxmax, nx);
+      }
       const size_t tab_smem = kg_tab_smem(ng, nxmax);
       BA.kgtab = prod && !(flags & BEM_QUAD_KG_ENTRYWISE) && tab_smem + 2048 <= (size_t)max_smem_optin() &&
                  nxmax <= KGT_NODE && ng <= KGT_THREADS && kg_ch(ng) <= 20 ? 1 : 0;
@@ -671,18 +684,30 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, const Qua
             cudaFuncSetAttribute(k_kg_tab<20>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem_optin() - 2048);
             attr = true;
           }
-          const dim3 tg((unsigned)ng, (unsigned)bl.size());
-          if (kg_chm(ng) == 12) k_kg_tab<12><<<tg, KGT_THREADS, tab_smem, st>>>(BA, L, MB, nxmax);
-          else k_kg_tab<20><<<tg, KGT_THREADS, tab_smem, st>>>(BA, L, MB, nxmax);
+          int* d_gs = nullptr;
+          if ((e = cudaMallocAsync((void**)&d_gs, sizeof(int) * gsv.size(), st)) != cudaSuccess ||
+              (e = cudaMemcpyAsync(d_gs, gsv.data(), sizeof(int) * gsv.size(), cudaMemcpyHostToDevice, st)) != cudaSuccess)
+          {
+            cudaFreeAsync(d_bl, st);
+            return cuda_fail(e, "assemble/table groups");
+          }
+          const dim3 tg((unsigned)ng, (unsigned)(gsv.size() - 1));
+          if (kg_chm(ng) == 12) k_kg_tab<12><<<tg, KGT_THREADS, tab_smem, st>>>(BA, L, MB, nxmax, d_gs);
+          else k_kg_tab<20><<<tg, KGT_THREADS, tab_smem, st>>>(BA, L, MB, nxmax, d_gs);
+          cudaFreeAsync(d_gs, st);
           count_launch();
           A->launches++;
-          // algorithmic flops of the table: per (i, trial step y) the 22 prefix scans (one FMA per pair
-          // and field), per covered node (x, y, i) the 21-term chain and the ln s term
-          for (const BulkBlock& q : bl) {
-            const int ymax = std::min(q.b1, q.a1 - 3);
-            for (int y = q.b0; y <= ymax; ++y) {
-              const int nxn = q.a1 - std::max(q.a0, y + 3) + 1;
-              A->flops_tab += (double)ng * (2.0 * KGT_NF * ng + 44.0 * std::max(0, nxn));
+          // algorithmic flops of the table: per (i, trial step y) of a trial-range group the 22 prefix
+          // scans (one FMA per pair and field), per covered node (x, y, i) the 21-term chain and ln s term
+          for (size_t gi = 0; gi + 1 < gsv.size(); ++gi) {
+            const BulkBlock& g0 = bl[gsv[gi]];
+            int a1max = g0.a1;
+            for (int k = gsv[gi]; k < gsv[gi + 1]; ++k) a1max = std::max(a1max, bl[k].a1);
+            for (int y = g0.b0; y <= std::min(g0.b1, a1max - 3); ++y) {
+              double nodes = 0.0;
+              for (int k = gsv[gi]; k < gsv[gi + 1]; ++k)
+                if (y <= std::min(bl[k].b1, bl[k].a1 - 3)) nodes += std::max(0, bl[k].a1 - std::max(bl[k].a0, y + 3) + 1);
+              A->flops_tab += (double)ng * (2.0 * KGT_NF * ng + 44.0 * nodes);
             }
           }
         }

@@ -1415,11 +1415,21 @@ constexpr int KGT_NODE = KGT_THREADS / 2;   // threads [0, 352) evaluate the nod
 // pairs per chunk the register arrays hold (template instances 12: N_Gamma <= 384, 20: <= 640)
 __host__ __device__ inline int kg_chm(int ng) { return kg_ch(ng) <= 12 ? 12 : 20; }
 template <int CHM>
-__global__ void __launch_bounds__(KGT_THREADS, 1) k_kg_tab(BlockArgs B, BulkList L, MomArgs M, int nxmax) {
+__global__ void __launch_bounds__(KGT_THREADS, 1) k_kg_tab(BlockArgs B, BulkList L, MomArgs M, int nxmax,
+                                                            const int* __restrict__ gs) {
   extern __shared__ __align__(16) double kgt[];
   const int ng = B.ng, i = blockIdx.x, t = threadIdx.x;
-  const BulkBlock Bk = L.blk[blockIdx.y];
-  const int ymax = min(Bk.b1, Bk.a1 - 3);
+  // CTA = (test segment i, group of listed blocks with one trial range [b0, b1]): the sort, the field
+  // loads and the prefix scans of a trial step depend on the trial range only, so the blocks of one
+  // trial slice (a rank's owned blocks (I, J) of one J) share them; their test nodes are concatenated
+  const int k0 = gs[blockIdx.y], k1 = gs[blockIdx.y + 1];
+  const BulkBlock Bk = L.blk[k0];                             // b0, b1 of the group
+  int a1max = Bk.a1, nxt = 0;
+  for (int k = k0; k < k1; ++k) {
+    a1max = max(a1max, L.blk[k].a1);
+    nxt += L.blk[k].a1 - L.blk[k].a0 + 1;
+  }
+  const int ymax = min(Bk.b1, a1max - 3);
   if (ymax < Bk.b0) return;                                   // CTA-uniform: no covered node
   const long long S = M.npairs;
   // ldw: one weight buffer, its last chunk followed by CHM zeros (the scans read CHM entries per chunk)
@@ -1464,8 +1474,20 @@ __global__ void __launch_bounds__(KGT_THREADS, 1) k_kg_tab(BlockArgs B, BulkList
   // m(x', y + 1) for node x' = a0 + t' during step y (galloping down from m(x', y): the cutoff only
   // falls as y grows), triple-buffered by y mod 3 so that one barrier per step orders it
   const bool nodet = t < KGT_NODE;
-  const int xk = Bk.a0 + (nodet ? t : t - KGT_NODE);
-  const int nxk = Bk.a1 - Bk.a0 + 1;
+  const int jn = nodet ? t : t - KGT_NODE;                    // this thread's node in the group
+  int xk = 0, xa1 = -1;                                       // its test node x and its block's a1
+  {
+    int cum = 0;
+    for (int k = k0; k < k1; ++k) {
+      const int nx = L.blk[k].a1 - L.blk[k].a0 + 1;
+      if (jn >= cum && jn < cum + nx) {
+        xk = L.blk[k].a0 + jn - cum;
+        xa1 = L.blk[k].a1;
+      }
+      cum += nx;
+    }
+  }
+  const int nxk = nxt;
   double sx = 0.0;
   int mprev = ng;
   auto cutoff = [&](double u, int H) {          // #{m : c_max[m] u < 8} given it is <= H
@@ -1491,13 +1513,13 @@ __global__ void __launch_bounds__(KGT_THREADS, 1) k_kg_tab(BlockArgs B, BulkList
   // (u, ln s) of this thread's node (node threads: step y + 1; cutoff threads: step y + 2) and g
   // of the weights stored during the step
   auto ldq = [&](int yy) -> double2 {
-    if (yy > ymax || xk > Bk.a1 || xk < yy + 3) return make_double2(0.0, 0.0);
+    if (yy > ymax || xk > xa1 || xk < yy + 3) return make_double2(0.0, 0.0);
     const double4 q = B.lag[(long long)xk * B.ldlag + yy];
     return make_double2(q.z, q.y);
   };
-  if (!nodet && xk <= Bk.a1 && xk >= Bk.b0 + 3) {          // cutoff of step b0
+  if (!nodet && xk <= xa1 && xk >= Bk.b0 + 3) {            // cutoff of step b0
     mprev = cutoff(ldq(Bk.b0).x, ng);
-    mcut[xk - Bk.a0] = mprev;
+    mcut[jn] = mprev;
   }
   double2 qc = ldq(nodet ? Bk.b0 : Bk.b0 + 1);
   double ga = (t < ng && Bk.b0 < ymax) ? gt(Bk.b0 + 1, nt_) : 0.0;   // weights of step b0 + 1
@@ -1541,15 +1563,15 @@ __global__ void __launch_bounds__(KGT_THREADS, 1) k_kg_tab(BlockArgs B, BulkList
     }
     if (t < ng && y < ymax) wn[wslot] = ga - gb;
     // cutoff threads: m(x', y + 1) into buffer (y + 1) mod 3
-    if (!nodet && xk <= Bk.a1 && xk >= y + 4 && y < ymax) {
+    if (!nodet && xk <= xa1 && xk >= y + 4 && y < ymax) {
       mprev = cutoff(qc.x, mprev);
-      mcut[((y + 1 - Bk.b0) % 3) * nxk + xk - Bk.a0] = mprev;
+      mcut[((y + 1 - Bk.b0) % 3) * nxk + jn] = mprev;
     }
     __syncthreads();
     // the covered node of trial step y (lag table: s, ln s, u)
-    if (nodet && xk <= Bk.a1 && xk >= y + 3) {
+    if (nodet && xk <= xa1 && xk >= y + 3) {
       const double u = qc.x;
-      const double* Tm = Ty + pos[mcut[((y - Bk.b0) % 3) * nxk + xk - Bk.a0]];
+      const double* Tm = Ty + pos[mcut[((y - Bk.b0) % 3) * nxk + jn]];
       double acc = Tm[(size_t)MKA * ldt];
 #pragma unroll
       for (int kk = MKA - 1; kk >= 0; --kk) acc = fma(acc, u, Tm[(size_t)kk * ldt]);
@@ -1559,10 +1581,14 @@ __global__ void __launch_bounds__(KGT_THREADS, 1) k_kg_tab(BlockArgs B, BulkList
     ga = gan;
     gb = gbn;
   }
-  if (nodet && xk <= Bk.a1) Sx[xk - Bk.a0] = sx;
+  if (nodet && xk <= xa1) Sx[jn] = sx;
   __syncthreads();
-  for (int a = Bk.a0 + t; a < Bk.a1; a += KGT_THREADS)
-    B.part[Bk.pbase + ((long long)(a - Bk.a0) * ng + i) * B.pslots + 2 * B.ntile + 5] = Sx[a + 1 - Bk.a0] - Sx[a - Bk.a0];
+  for (int k = k0, cum = 0; k < k1; ++k) {
+    const BulkBlock Q = L.blk[k];
+    for (int a = Q.a0 + t; a < Q.a1; a += KGT_THREADS)
+      B.part[Q.pbase + ((long long)(a - Q.a0) * ng + i) * B.pslots + 2 * B.ntile + 5] = Sx[cum + a + 1 - Q.a0] - Sx[cum + a - Q.a0];
+    cum += Q.a1 - Q.a0 + 1;
+  }
 }
 
 // ------------------------------------------------------------- near cells (d <= 1)
