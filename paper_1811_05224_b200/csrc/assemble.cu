@@ -328,14 +328,15 @@ static void launch_bulk(const BlockArgs& BA, const MomArgs& M, dim3 grid, cudaSt
 }
 template <int KIND, bool PROD = false>
 static void launch_kind(int which, const BlockArgs& BA, const MomArgs& M, int ng, int nband_or_chunk,
-                        int nz, cudaStream_t st, BulkList L = BulkList{nullptr, 0}, int R_ = 0) {
+                        int nz, cudaStream_t st, BulkList L = BulkList{nullptr, 0}, int R_ = 0,
+                        const NearItem* items = nullptr) {
   dim3 grid((ng + 31) / 32, (ng + 3) / 4, nz);
   if (which == 0 && KIND != STB_D && R_ == 8) {
     launch_bulk<KIND, 8, PROD>(BA, M, grid, st, L);
   } else if (which == 0) {
     launch_bulk<KIND, bulk_r<KIND>(), PROD>(BA, M, grid, st, L);
   }
-  else k_near_m<KIND, PROD><<<grid, 128, 0, st>>>(BA, M, nband_or_chunk);
+  else k_near_m<KIND, PROD><<<grid, 128, 0, st>>>(BA, M, nband_or_chunk, items);
   count_launch();
 }
 
@@ -720,6 +721,50 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, const Qua
       cudaFreeAsync(d_bl, st);
     }
   }
+  // near cells of every owned block in ONE launch (grid z = (block, chunk of its test steps)): a rank
+  // of the cyclic plan owns several small blocks, whose per-block launches were each setup-bound
+  NearItem* d_items = nullptr;
+  {
+    std::vector<NearItem> items;
+    const int chunk = STB_NEAR_CHUNK;
+    for (size_t bi = 0; bi < blocks_of(A).size(); ++bi) {
+      const Block& blk = blocks_of(A)[bi];
+      if (!(blk.b1 - 1 >= blk.a0 - 1 && blk.b0 <= blk.a1 - 1)) continue;
+      for (int a = blk.a0; a < blk.a1; a += chunk)
+        items.push_back(NearItem{BulkBlock{d_poff + A->poff_base[bi], blk.a0, blk.a1, blk.b0, blk.b1, pbase[bi]},
+                                 a, std::min(blk.a1, a + chunk)});
+    }
+    if (items.size() > 1) {
+      if ((e = cudaMallocAsync((void**)&d_items, sizeof(NearItem) * items.size(), st)) != cudaSuccess ||
+          (e = cudaMemcpyAsync(d_items, items.data(), sizeof(NearItem) * items.size(), cudaMemcpyHostToDevice, st)) != cudaSuccess)
+        return cuda_fail(e, "assemble/near items");
+      BlockArgs BA;
+      BA.out = A->data;
+      BA.poff = nullptr;
+      BA.a0 = BA.a1 = BA.b0 = BA.b1 = 0;
+      BA.ng = ng;
+      BA.lag = m->d_lag;
+      BA.ldlag = m->nt + 1;
+      BA.sym = A->sym;
+      BA.nt = sym_nt(ng);
+      BA.blk = A->blk_elems;
+      BA.g = prod_g;
+      BA.part = d_part;
+      BA.pbase = 0;
+      BA.pslots = pslots;
+      BA.ntile = ntile;
+      BA.ell = MB.ell;
+      const int nz = (int)items.size();
+      if (prod) launch_kind<STB_K, true>(1, BA, MN, ng, chunk, nz, st, BulkList{nullptr, 0}, 0, d_items);
+      else if (kind == STB_V) launch_kind<STB_V>(1, BA, MN, ng, chunk, nz, st, BulkList{nullptr, 0}, 0, d_items);
+      else if (kind == STB_K) launch_kind<STB_K>(1, BA, MN, ng, chunk, nz, st, BulkList{nullptr, 0}, 0, d_items);
+      else launch_kind<STB_D>(1, BA, MN, ng, chunk, nz, st, BulkList{nullptr, 0}, 0, d_items);
+      mark();
+      fam.push_back(1);
+      A->launches++;
+      cudaFreeAsync(d_items, st);
+    }
+  }
   for (size_t bi = 0; bi < blocks_of(A).size(); ++bi) {
     const Block& blk = blocks_of(A)[bi];
     BlockArgs BA;
@@ -740,14 +785,17 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, const Qua
     BA.ell = MB.ell;
     const bool has_near = blk.b1 - 1 >= blk.a0 - 1 && blk.b0 <= blk.a1 - 1;
     if (has_near) {
-      const int chunk = STB_NEAR_CHUNK;
-      const int nz = (blk.a1 - blk.a0 + chunk - 1) / chunk;
-      if (prod) launch_kind<STB_K, true>(1, BA, MN, ng, chunk, nz, st);
-      else if (kind == STB_V) launch_kind<STB_V>(1, BA, MN, ng, chunk, nz, st);
-      else if (kind == STB_K) launch_kind<STB_K>(1, BA, MN, ng, chunk, nz, st);
-      else launch_kind<STB_D>(1, BA, MN, ng, chunk, nz, st);
-      mark();
-      fam.push_back(1);
+      if (!d_items) {   // a single slab: the one-block form
+        const int chunk = STB_NEAR_CHUNK;
+        const int nz = (blk.a1 - blk.a0 + chunk - 1) / chunk;
+        if (prod) launch_kind<STB_K, true>(1, BA, MN, ng, chunk, nz, st);
+        else if (kind == STB_V) launch_kind<STB_V>(1, BA, MN, ng, chunk, nz, st);
+        else if (kind == STB_K) launch_kind<STB_K>(1, BA, MN, ng, chunk, nz, st);
+        else launch_kind<STB_D>(1, BA, MN, ng, chunk, nz, st);
+        mark();
+        fam.push_back(1);
+        A->launches++;
+      }
       if (fused_sing) {
         if (prod) launch_sing_m<STB_K, true>(BA, MS, blk.a1 - blk.a0, st);
         else if (kind == STB_V) launch_sing_m<STB_V>(BA, MS, blk.a1 - blk.a0, st);
@@ -765,7 +813,7 @@ bem_status launch_assembly(int kind, const bem_mesh* m, bem_matrix* A, const Qua
       }
       mark();
       fam.push_back(2);
-      A->launches += 2;
+      A->launches++;
     }
   }
   if (prod) {

@@ -986,6 +986,11 @@ struct BulkBlock {
   int a0, a1, b0, b1;
   long long pbase;
 };
+// one CTA slab of the near cells: test steps [a_beg, a_end) of an owned block (all blocks in one launch)
+struct NearItem {
+  BulkBlock blk;
+  int a_beg, a_end;
+};
 struct BulkList {
   const BulkBlock* blk;
   int n;
@@ -1597,15 +1602,31 @@ __global__ void __launch_bounds__(KGT_THREADS, 1) k_kg_tab(BlockArgs B, BulkList
 // with the true node values Phi = Phi~ - affine part (the affine terms do not cancel here).
 // Touching sub-pairs are excluded from the near records; k_sing adds them afterwards.
 template <int KIND, bool PROD = false>
-__global__ void __launch_bounds__(128) k_near_m(BlockArgs B, MomArgs M, int chunk) {
+__global__ void __launch_bounds__(128) k_near_m(BlockArgs B0, MomArgs M, int chunk, const NearItem* __restrict__ items) {
+  // items: grid z enumerates (owned block, chunk of its test steps) of every block with near cells
+  // (one launch for a rank's blocks); nullptr: the one block of B0, chunk z
+  BlockArgs B = B0;
+  int a_beg, a_end;
+  if (items) {
+    const NearItem it = items[blockIdx.z];
+    B.poff = it.blk.poff;
+    B.a0 = it.blk.a0;
+    B.a1 = it.blk.a1;
+    B.b0 = it.blk.b0;
+    B.b1 = it.blk.b1;
+    B.pbase = it.blk.pbase;
+    a_beg = it.a_beg;
+    a_end = it.a_end;
+  } else {
+    a_beg = B.a0 + blockIdx.z * chunk;
+    a_end = min(B.a1, a_beg + chunk);
+  }
   const int ng = B.ng;
   const int lane = threadIdx.x & 31;
   const int J0 = blockIdx.x * 32 + lane;
   const int I0 = blockIdx.y * 4 + (threadIdx.x >> 5);
   const bool valid = I0 < ng && J0 < ng;
   const int I = min(I0, ng - 1), J = min(J0, ng - 1);
-  const int a_beg = B.a0 + blockIdx.z * chunk;
-  const int a_end = min(B.a1, a_beg + chunk);
   if (B.sym && (int)(blockIdx.y * 4) / SYM_TS > (int)blockIdx.x) return;   // CTA-uniform (mirror tiles)
   const long long pair = (long long)I * ng + J;
   const long long S = M.npairs;
