@@ -65,6 +65,7 @@ struct BlockArgs {
   int pslots;             // 2 * ntile + 6: bulk trial tiles, near trial tiles, touching records, k_kg_tab
   int ntile;              // ceil(ng / 32)
   int kgtab = 0;          // product mode: regime-A nodes with y <= x - 3 summed by k_kg_tab
+  int nsub = 1;           // k_bulk_m (list form): CTAs per band sharing the listed blocks
   double ell;             // sqrt(4 min h_t / alpha): composite singular rules when h > ell
 };
 
@@ -331,10 +332,19 @@ static void launch_kind(int which, const BlockArgs& BA, const MomArgs& M, int ng
                         int nz, cudaStream_t st, BulkList L = BulkList{nullptr, 0}, int R_ = 0,
                         const NearItem* items = nullptr) {
   dim3 grid((ng + 31) / 32, (ng + 3) / 4, nz);
+  BlockArgs B2 = BA;
+  if (which == 0 && L.n > 1) {
+    // the listed blocks split over nsub CTAs per band until the grid holds ~16 waves of 2 CTAs / SM
+    const long long per_z = (long long)grid.x * grid.y * nz;
+    int nsub = 1;
+    while (nsub < L.n && per_z * nsub < 16LL * 2 * 148) nsub *= 2;
+    B2.nsub = std::min(nsub, L.n);
+    grid.z = nz * B2.nsub;
+  }
   if (which == 0 && KIND != STB_D && R_ == 8) {
-    launch_bulk<KIND, 8, PROD>(BA, M, grid, st, L);
+    launch_bulk<KIND, 8, PROD>(B2, M, grid, st, L);
   } else if (which == 0) {
-    launch_bulk<KIND, bulk_r<KIND>(), PROD>(BA, M, grid, st, L);
+    launch_bulk<KIND, bulk_r<KIND>(), PROD>(B2, M, grid, st, L);
   }
   else k_near_m<KIND, PROD><<<grid, 128, 0, st>>>(BA, M, nband_or_chunk, items);
   count_launch();

@@ -1052,7 +1052,10 @@ __global__ void __launch_bounds__(128, KIND == STB_D ? STB_BULK_MINB_D : (KIND =
   const int I0 = blockIdx.y * 4 + (threadIdx.x >> 5);
   const bool valid = I0 < ng && J0 < ng;
   const int I = min(I0, ng - 1), J = min(J0, ng - 1);
-  const int band = blockIdx.z;
+  // MULTI: grid z = band x nsub, CTA (band, sub) takes the listed blocks sub, sub + nsub, ... (a
+  // rank's many small blocks spread over more CTAs: whole waves instead of a few long CTAs)
+  const int nsub = MULTI ? B.nsub : 1;
+  const int band = blockIdx.z / nsub, ksub = blockIdx.z % nsub;
   // sym: the CTA's 4 rows lie in tile row (4 blockIdx.y) / 32, its 32 columns in tile column
   // blockIdx.x; tiles below the tile diagonal are the mirror images of stored ones
   const int ti = (blockIdx.y * 4) / SYM_TS, tj = blockIdx.x;
@@ -1064,7 +1067,7 @@ __global__ void __launch_bounds__(128, KIND == STB_D ? STB_BULK_MINB_D : (KIND =
   };
   {
     bool any = false;
-    for (int k = 0; k < nlist && !any; ++k) {
+    for (int k = ksub; k < nlist && !any; k += nsub) {
       const BulkBlock Q = block_k(k);
       const int rh = Q.a1 - R * band, rl = max(Q.a0, rh - R);
       any = rh > rl && min(Q.b1 - 1, rh - 3) >= Q.b0;
@@ -1119,7 +1122,7 @@ __global__ void __launch_bounds__(128, KIND == STB_D ? STB_BULK_MINB_D : (KIND =
   unsigned long long nA = 0, nB = 0, nZ = 0, nC = 0, nK = 0, nT = 0;
   // the listed blocks one after the other (a rank's owned blocks of the cyclic plan; one block on one
   // GPU): the per-pair setup above is paid once per CTA, not once per block
-  for (int kb_ = 0; kb_ < nlist; ++kb_) {
+  for (int kb_ = ksub; kb_ < nlist; kb_ += nsub) {
   const BulkBlock Bk = block_k(kb_);
   const int r_hi = Bk.a1 - R * band;
   const int r_lo = max(Bk.a0, r_hi - R);
